@@ -1,0 +1,325 @@
+/*
+ * oracle.c -- CPU oracle for the LiRank sparse-embedding hot path.
+ * TEST INFRASTRUCTURE ONLY (see oracle.h).  Each function follows SURVEY.md §8(c)
+ * step by step; the paper passages are cited at each definition in oracle.h.
+ *
+ * Build: gcc -O2 -std=c99 -ffp-contract=off -fno-fast-math -fPIC -shared oracle.c -lm
+ */
+#include "oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ------------------------------------------------------------------------- */
+/* Row addressing                                    */
+/* ------------------------------------------------------------------------- */
+
+/* base[t] = sum of the rows of tables < t (caller frees). */
+static int64_t* table_bases(const ora_cfg* c) {
+  int64_t* base = (int64_t*)malloc(sizeof(int64_t) * (size_t)(c->num_tables + 1));
+  base[0] = 0;
+  for (int32_t t = 0; t < c->num_tables; ++t) base[t + 1] = base[t] + c->table_rows[t];
+  return base;
+}
+
+/* Global key of id `id` read by feature f, or -1 if the id is out of range. */
+static int64_t row_key(const ora_cfg* c, const int64_t* base, int32_t f, int32_t id) {
+  int32_t t = c->feature_table[f];
+  if (id < 0 || (int64_t)id >= c->table_rows[t]) return -1;
+  return base[t] + id;
+}
+
+/* ------------------------------------------------------------------------- */
+/* a2 forward pooled lookup                                                   */
+/* ------------------------------------------------------------------------- */
+
+int64_t ora_forward(const ora_cfg* c, const float* W, const int32_t* ids,
+                    const int32_t* offsets, int32_t B, float* out) {
+  const int32_t D = c->dim, F = c->num_features;
+  int64_t invalid = 0;
+  int64_t* base = table_bases(c);
+  float* acc = (float*)malloc(sizeof(float) * (size_t)D);
+  for (int32_t f = 0; f < F; ++f) {
+    for (int32_t b = 0; b < B; ++b) {
+      int64_t bag = (int64_t)f * B + b;
+      int32_t lo = offsets[bag], hi = offsets[bag + 1];
+      for (int32_t d = 0; d < D; ++d) acc[d] = 0.0f;
+      for (int32_t j = lo; j < hi; ++j) {
+        int64_t key = row_key(c, base, f, ids[j]);
+        if (key < 0) { ++invalid; continue; }
+        const float* row = W + key * D;
+        for (int32_t d = 0; d < D; ++d) acc[d] = acc[d] + row[d];
+      }
+      if (c->pooling == 1) {
+        int32_t L = hi - lo;
+        for (int32_t d = 0; d < D; ++d) acc[d] = (L > 0) ? acc[d] / (float)L : 0.0f;
+      }
+      float* o = out + ((int64_t)b * F + f) * D;
+      for (int32_t d = 0; d < D; ++d) o[d] = acc[d];
+    }
+  }
+  free(acc);
+  free(base);
+  return invalid;
+}
+
+/* ------------------------------------------------------------------------- */
+/* a5 dedup: stable sort by key (ties by occurrence index), then run-length   */
+/* ------------------------------------------------------------------------- */
+
+typedef struct { int64_t key, occ, bag; } occ_t;
+
+static int cmp_occ(const void* a, const void* b) {
+  const occ_t* x = (const occ_t*)a;
+  const occ_t* y = (const occ_t*)b;
+  if (x->key != y->key) return x->key < y->key ? -1 : 1;
+  if (x->occ != y->occ) return x->occ < y->occ ? -1 : 1; /* stability, explicitly */
+  return 0;
+}
+
+int64_t ora_dedup(const ora_cfg* c, const int32_t* ids, const int32_t* offsets, int32_t B,
+                  int64_t* unique_keys, int64_t* seg_offsets, int64_t* sorted_bags,
+                  int64_t* n_valid) {
+  const int32_t F = c->num_features;
+  int64_t nnz = offsets[(int64_t)F * B];
+  int64_t* base = table_bases(c);
+  occ_t* v = (occ_t*)malloc(sizeof(occ_t) * (size_t)(nnz > 0 ? nnz : 1));
+  int64_t n = 0;
+  for (int32_t f = 0; f < F; ++f)
+    for (int32_t b = 0; b < B; ++b) {
+      int64_t bag = (int64_t)f * B + b;
+      for (int32_t j = offsets[bag]; j < offsets[bag + 1]; ++j) {
+        int64_t key = row_key(c, base, f, ids[j]);
+        if (key < 0) continue;
+        v[n].key = key; v[n].occ = j; v[n].bag = bag; ++n;
+      }
+    }
+  qsort(v, (size_t)n, sizeof(occ_t), cmp_occ);
+  int64_t U = 0;
+  for (int64_t k = 0; k < n; ++k) {
+    if (k == 0 || v[k].key != v[k - 1].key) {
+      unique_keys[U] = v[k].key;
+      seg_offsets[U] = k;
+      ++U;
+    }
+    sorted_bags[k] = v[k].bag;
+  }
+  seg_offsets[U] = n;
+  *n_valid = n;
+  free(v);
+  free(base);
+  return U;
+}
+
+/* ------------------------------------------------------------------------- */
+/* a6 segment-reduce                                                          */
+/* ------------------------------------------------------------------------- */
+
+void ora_segment_reduce(const ora_cfg* c, const int32_t* offsets, int32_t B, int64_t U,
+                        const int64_t* seg_offsets, const int64_t* sorted_bags,
+                        const float* grad, float* G) {
+  const int32_t D = c->dim, F = c->num_features;
+  double* acc = (double*)malloc(sizeof(double) * (size_t)D);
+  for (int64_t u = 0; u < U; ++u) {
+    for (int32_t d = 0; d < D; ++d) acc[d] = 0.0;
+    for (int64_t k = seg_offsets[u]; k < seg_offsets[u + 1]; ++k) {
+      int64_t bag = sorted_bags[k];
+      int64_t f = bag / B, b = bag % B;
+      const float* g = grad + (b * F + f) * D;
+      if (c->pooling == 1) {
+        int32_t L = offsets[bag + 1] - offsets[bag];
+        double inv = 1.0 / (double)L;
+        for (int32_t d = 0; d < D; ++d) acc[d] = acc[d] + (double)g[d] * inv;
+      } else {
+        for (int32_t d = 0; d < D; ++d) acc[d] = acc[d] + (double)g[d];
+      }
+    }
+    for (int32_t d = 0; d < D; ++d) G[u * D + d] = (float)acc[d];
+  }
+  free(acc);
+}
+
+/* ------------------------------------------------------------------------- */
+/* a7 global norm and clip factor                                             */
+/* ------------------------------------------------------------------------- */
+
+double ora_sq_norm(const float* G, int64_t U, int32_t dim, double extra) {
+  double S = 0.0;
+  for (int64_t u = 0; u < U; ++u)
+    for (int32_t d = 0; d < dim; ++d) {
+      double x = (double)G[u * dim + d];
+      S = S + x * x;
+    }
+  return S + extra;
+}
+
+float ora_clip_factor(double S, float max_norm, int* nonfinite) {
+  *nonfinite = 0;
+  if (!isfinite(S)) { *nonfinite = 1; return 0.0f; }
+  double n = sqrt(S);
+  return (n > (double)max_norm) ? (float)((double)max_norm / n) : 1.0f;
+}
+
+void ora_clip(const float* G, int64_t n, float c, float* g) {
+  for (int64_t i = 0; i < n; ++i) g[i] = G[i] * c;
+}
+
+/* ------------------------------------------------------------------------- */
+/* a8 sparse AdaGrad on touched rows                                          */
+/* ------------------------------------------------------------------------- */
+
+void ora_adagrad_rowwise(float* W, float* A, const int64_t* keys, int64_t U,
+                         const float* g, int32_t dim, float lr, float eps) {
+  for (int64_t u = 0; u < U; ++u) {
+    int64_t r = keys[u];
+    const float* gu = g + u * dim;
+    double ss = 0.0;
+    for (int32_t d = 0; d < dim; ++d) ss = ss + (double)gu[d] * (double)gu[d];
+    float s = (float)(ss / (double)dim);
+    float a = A[r] + s;
+    A[r] = a;
+    float den = sqrtf(a) + eps;
+    float mult = lr / den;
+    float* w = W + r * dim;
+    for (int32_t d = 0; d < dim; ++d) w[d] = w[d] - mult * gu[d];
+  }
+}
+
+void ora_adagrad_elementwise(float* W, float* A, const int64_t* keys, int64_t U,
+                             const float* g, int32_t dim, float lr, float eps) {
+  for (int64_t u = 0; u < U; ++u) {
+    int64_t r = keys[u];
+    const float* gu = g + u * dim;
+    float* w = W + r * dim;
+    float* a = A + r * dim;
+    for (int32_t d = 0; d < dim; ++d) {
+      float sq = gu[d] * gu[d];
+      float an = a[d] + sq;
+      a[d] = an;
+      float den = sqrtf(an) + eps;
+      float step = (-lr * gu[d]) / den;
+      w[d] = w[d] + step;
+    }
+  }
+}
+
+/* ------------------------------------------------------------------------- */
+/* a9 middle-max quantization                                                 */
+/* ------------------------------------------------------------------------- */
+
+int32_t ora_quantize_row(const float* x, int32_t dim, int8_t* codes, float* middle, float* scale) {
+  for (int32_t d = 0; d < dim; ++d)
+    if (!isfinite(x[d])) {
+      for (int32_t e = 0; e < dim; ++e) codes[e] = 0;
+      *middle = 0.0f; *scale = 0.0f;
+      return 1;
+    }
+  float mn = x[0], mx = x[0];
+  for (int32_t d = 1; d < dim; ++d) {
+    if (x[d] < mn) mn = x[d];
+    if (x[d] > mx) mx = x[d];
+  }
+  if (mx == mn) {
+    *middle = mx; *scale = 0.0f;
+    for (int32_t d = 0; d < dim; ++d) codes[d] = 0;
+    return 0;
+  }
+  /* X^middle = (X^max * 2^(b-1) + X^min * (2^(b-1) - 1)) / (2^b - 1), b = 8 */
+  float hi = mx * 128.0f;
+  float lo = mn * 127.0f;
+  float mid = (hi + lo) / 255.0f;
+  /* X^scale = (X^max - X^min) / (2^b - 1) */
+  float sc = (mx - mn) / 255.0f;
+  *middle = mid; *scale = sc;
+  for (int32_t d = 0; d < dim; ++d) {
+    if (sc == 0.0f) { codes[d] = 0; continue; }
+    /* X^int = round((X - X^middle) / X^scale), half away from zero, saturated */
+    float q = (x[d] - mid) / sc;
+    float r = roundf(q);
+    if (r < -128.0f) r = -128.0f;
+    if (r > 127.0f) r = 127.0f;
+    codes[d] = (int8_t)r;
+  }
+  return 0;
+}
+
+int64_t ora_quantize_mm8(const float* X, int64_t rows, int32_t dim, int8_t* codes,
+                         float* middle, float* scale) {
+  int64_t bad = 0;
+  for (int64_t r = 0; r < rows; ++r)
+    bad += ora_quantize_row(X + r * dim, dim, codes + r * dim, middle + r, scale + r);
+  return bad;
+}
+
+/* ------------------------------------------------------------------------- */
+/* a10 quantized-table pooled lookup                                          */
+/* ------------------------------------------------------------------------- */
+
+int64_t ora_forward_q8(const ora_cfg* c, const int8_t* codes, const float* middle,
+                       const float* scale, const int32_t* ids, const int32_t* offsets,
+                       int32_t B, float* out) {
+  const int32_t D = c->dim, F = c->num_features;
+  int64_t invalid = 0;
+  int64_t* base = table_bases(c);
+  float* acc = (float*)malloc(sizeof(float) * (size_t)D);
+  for (int32_t f = 0; f < F; ++f)
+    for (int32_t b = 0; b < B; ++b) {
+      int64_t bag = (int64_t)f * B + b;
+      int32_t lo = offsets[bag], hi = offsets[bag + 1];
+      for (int32_t d = 0; d < D; ++d) acc[d] = 0.0f;
+      for (int32_t j = lo; j < hi; ++j) {
+        int64_t key = row_key(c, base, f, ids[j]);
+        if (key < 0) { ++invalid; continue; }
+        const int8_t* q = codes + key * D;
+        for (int32_t d = 0; d < D; ++d) {
+          float v = fmaf((float)q[d], scale[key], middle[key]); /* middle + int * scale */
+          acc[d] = acc[d] + v;
+        }
+      }
+      if (c->pooling == 1) {
+        int32_t L = hi - lo;
+        for (int32_t d = 0; d < D; ++d) acc[d] = (L > 0) ? acc[d] / (float)L : 0.0f;
+      }
+      float* o = out + ((int64_t)b * F + f) * D;
+      for (int32_t d = 0; d < D; ++d) o[d] = acc[d];
+    }
+  free(acc);
+  free(base);
+  return invalid;
+}
+
+/* ------------------------------------------------------------------------- */
+/* one whole training step                                                    */
+/* ------------------------------------------------------------------------- */
+
+int32_t ora_train_step(const ora_cfg* c, float* W, float* A, int32_t adagrad_mode,
+                       const int32_t* ids, const int32_t* offsets, int32_t B,
+                       const float* grad, float lr, float eps, float max_norm,
+                       double extra_sq_norm, float* out, double* S_out, float* c_out,
+                       int64_t* U_out) {
+  const int32_t D = c->dim;
+  int64_t nnz = offsets[(int64_t)c->num_features * B];
+  size_t n1 = (size_t)(nnz > 0 ? nnz : 1);
+  if (out) ora_forward(c, W, ids, offsets, B, out);
+  int64_t* keys = (int64_t*)malloc(sizeof(int64_t) * n1);
+  int64_t* segs = (int64_t*)malloc(sizeof(int64_t) * (n1 + 1));
+  int64_t* bags = (int64_t*)malloc(sizeof(int64_t) * n1);
+  int64_t n_valid = 0;
+  int64_t U = ora_dedup(c, ids, offsets, B, keys, segs, bags, &n_valid);
+  float* G = (float*)malloc(sizeof(float) * (size_t)(U > 0 ? U : 1) * D);
+  ora_segment_reduce(c, offsets, B, U, segs, bags, grad, G);
+  double S = ora_sq_norm(G, U, D, extra_sq_norm);
+  int nonfinite = 0;
+  float cf = ora_clip_factor(S, max_norm, &nonfinite);
+  if (S_out) *S_out = S;
+  if (c_out) *c_out = cf;
+  if (U_out) *U_out = U;
+  if (!nonfinite) {
+    ora_clip(G, U * D, cf, G);
+    if (adagrad_mode == 0) ora_adagrad_rowwise(W, A, keys, U, G, D, lr, eps);
+    else ora_adagrad_elementwise(W, A, keys, U, G, D, lr, eps);
+  }
+  free(keys); free(segs); free(bags); free(G);
+  return nonfinite ? 1 : 0;
+}

@@ -1,0 +1,114 @@
+/*
+ * oracle.h -- CPU oracle for the LiRank (arXiv 2402.06859) sparse-embedding hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load liboracle.so.  The product library
+ * (paper_2402_06859_b200/) never includes, links or calls anything in this directory,
+ * and this directory never includes anything from the product.
+ *
+ * Plain, sequential, obviously-correct C99.  Built with -O2 -ffp-contract=off and no
+ * fast-math, so every float operation below is one IEEE-754 binary32 round-to-nearest
+ * operation in the written order ("fl(.)" in SURVEY.md §8(c)).  Sums that the contract
+ * accumulates in fp64 are plain sequential double sums.
+ *
+ * Tables are dense row-major fp32 [total_rows][dim], the tables of cfg concatenated in
+ * table order (table t starts at row base[t] = sum of rows of tables < t).  The "global
+ * row key" of id i of feature f is base[feature_table[f]] + i; it is valid iff
+ * 0 <= i < table_rows[feature_table[f]].
+ *
+ * Parity status of each function is stated in DESIGN.md §"Oracle pins".
+ */
+#ifndef LIRANK_ORACLE_H
+#define LIRANK_ORACLE_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct {
+  int32_t num_tables;
+  const int64_t* table_rows;     /* [num_tables] */
+  int32_t dim;
+  int32_t num_features;
+  const int32_t* feature_table;  /* [num_features] */
+  int32_t pooling;               /* 0 = SUM, 1 = MEAN */
+} ora_cfg;
+
+/* a2, PAPER.md:194 ("transformed into dense embeddings through lookup in embedding
+ * tables"), PAPER.md:538 ("concatenated with all other dense features").
+ * out[b][f][d] = sum over j in bag(f,b), in bag order, of W[key_j][d]; MEAN divides by
+ * the bag length L (L = 0 -> zeros).  Invalid ids contribute nothing.
+ * Returns the number of invalid ids. */
+int64_t ora_forward(const ora_cfg* c, const float* W, const int32_t* ids,
+                    const int32_t* offsets, int32_t B, float* out);
+
+/* a5 dedup.  Stable sort of the valid occurrences k (feature-major order) by global
+ * key; unique_keys[U] ascending, seg_offsets[U+1] CSR starts into the sorted
+ * occurrence list, sorted_bags[n_valid] = bag index (f*B+b) of each sorted occurrence.
+ * Returns U. */
+int64_t ora_dedup(const ora_cfg* c, const int32_t* ids, const int32_t* offsets, int32_t B,
+                  int64_t* unique_keys, int64_t* seg_offsets, int64_t* sorted_bags,
+                  int64_t* n_valid);
+
+/* a6 segment-reduce, PAPER.md:17 ("the global gradient").  G[u][d] = (float) of the
+ * fp64 sequential sum over the occurrences of segment u (ascending occurrence order) of
+ * grad[b][f][d] (MEAN: times (double)1/L). */
+void ora_segment_reduce(const ora_cfg* c, const int32_t* offsets, int32_t B, int64_t U,
+                        const int64_t* seg_offsets, const int64_t* sorted_bags,
+                        const float* grad, float* G);
+
+/* a7: S = sum_u sum_d (double)G[u][d]^2 in (u,d) order, + extra. */
+double ora_sq_norm(const float* G, int64_t U, int32_t dim, double extra);
+
+/* a7, PAPER.md:17 ("clip the global gradient to have unit norm").
+ * n = sqrt(S); c = (n > max_norm) ? (float)(max_norm / n) : 1.0f.
+ * Non-finite S -> *nonfinite = 1 and returns 0 (the step must not update). */
+float ora_clip_factor(double S, float max_norm, int* nonfinite);
+
+/* a8 clip: g[i] = fl(G[i] * c). */
+void ora_clip(const float* G, int64_t n, float c, float* g);
+
+/* a8 row-wise AdaGrad on touched rows (BASELINE.json north_star "row-wise AdaGrad";
+ * Duchi et al. as cited at PAPER.md:12).  For each u, row r = keys[u]:
+ *   s = (float)((sum_d (double)g[d]^2) / dim); A' = fl(A[r] + s);
+ *   den = fl(sqrtf(A') + eps); mult = fl(lr / den); w'[d] = fl(w[d] - fl(mult * g[d])). */
+void ora_adagrad_rowwise(float* W, float* A, const int64_t* keys, int64_t U,
+                         const float* g, int32_t dim, float lr, float eps);
+
+/* a8 element-wise AdaGrad (TF/Keras default form):
+ *   A'[d] = fl(A[d] + fl(g*g)); den = fl(sqrtf(A'[d]) + eps); w'[d] = fl(w + fl(fl(-lr*g)/den)). */
+void ora_adagrad_elementwise(float* W, float* A, const int64_t* keys, int64_t U,
+                             const float* g, int32_t dim, float lr, float eps);
+
+/* a9, PAPER.md:340-342 middle-max row-wise 8-bit quantization of one row x[0..dim).
+ *   mn = min x, mx = max x;
+ *   mx == mn:  middle = mx, scale = 0, codes 0;
+ *   else middle = fl(fl(fl(mx*128) + fl(mn*127)) / 255), scale = fl(fl(mx - mn) / 255);
+ *        scale == 0 -> codes 0; else code = clamp(roundf(fl(fl(x - middle) / scale)), -128, 127)
+ *   (roundf = half away from zero).  Non-finite x -> codes 0, middle 0, scale 0, returns 1. */
+int32_t ora_quantize_row(const float* x, int32_t dim, int8_t* codes, float* middle, float* scale);
+
+/* a9 over rows [0, rows).  Returns the number of non-finite rows. */
+int64_t ora_quantize_mm8(const float* X, int64_t rows, int32_t dim, int8_t* codes,
+                         float* middle, float* scale);
+
+/* a10, PAPER.md:341 (X^dequant = X^middle + X^int * X^scale): out[b][f][d] = sum in bag
+ * order of fmaf((float)code, scale, middle).  MEAN divides by L.  Returns #invalid ids. */
+int64_t ora_forward_q8(const ora_cfg* c, const int8_t* codes, const float* middle,
+                       const float* scale, const int32_t* ids, const int32_t* offsets,
+                       int32_t B, float* out);
+
+/* Convenience: one whole training step on dense W / A (a2, a5-a8), as the steps above.
+ * adagrad_mode 0 = row-wise, 1 = element-wise.  Returns 0 ok, 1 non-finite (no update).
+ * out may be NULL (forward skipped). S_out / c_out / U_out optional. */
+int32_t ora_train_step(const ora_cfg* c, float* W, float* A, int32_t adagrad_mode,
+                       const int32_t* ids, const int32_t* offsets, int32_t B,
+                       const float* grad, float lr, float eps, float max_norm,
+                       double extra_sq_norm, float* out, double* S_out, float* c_out,
+                       int64_t* U_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif
