@@ -1,0 +1,224 @@
+/*
+ * lirank_emb.h -- C ABI of the B200-native LiRank sparse-embedding hot path.
+ *
+ * The library (paper_2402_06859_b200/liblirank_emb.so, sm_100a) implements the
+ * sparse-feature embedding path of LiRank (arXiv 2402.06859):
+ *
+ *   a2  pooled multi-hot lookup          PAPER.md:194 ("Sparse ID embedding features are
+ *                                        transformed into dense embeddings through lookup in
+ *                                        embedding tables"), PAPER.md:536-538 (features,
+ *                                        "concatenated with all other dense features")
+ *   a5  id dedup (radix sort)            BASELINE.json north_star; SURVEY.md §8(a)
+ *   a6  segment-reduce of the gradient   PAPER.md:17 ("the global gradient")
+ *   a7  global-norm clip to unit norm    PAPER.md:17 ("clip the global gradient to have
+ *                                        unit norm for all experiments")
+ *   a8  sparse AdaGrad on touched rows   PAPER.md:17, 516 ("we had to leverage AdaGrad for
+ *                                        models where the number of sparse features was high")
+ *   a9  middle-max row-wise 8-bit quant  PAPER.md:338-345 (X^middle, X^scale, X^int)
+ *   a10 quantized-table pooled lookup    PAPER.md:341 (X^dequant = X^middle + X^int * X^scale)
+ *   a1/a3/a4 all-to-all exchange (W>1)   PAPER.md:576 ("each GPU's input batch is
+ *                                        all-to-all'ed ... lookups are all-to-all'ed to
+ *                                        return the output")
+ *
+ * The exact arithmetic of every step (operation order, fp64 accumulations, rounding)
+ * is SURVEY.md §8(c) with the readings listed in DESIGN.md §3.
+ *
+ * Conventions
+ * -----------
+ * - Memory ownership: the CALLER owns all device memory.  emb_plan() reports the byte
+ *   sizes of the buffers a configuration needs; the caller allocates them (e.g. torch
+ *   tensors) and passes them to emb_create().  The library owns only the handle and its
+ *   host-side metadata (and, for world_size > 1, its NCCL communicator).  All device
+ *   buffers must be 256-byte aligned and stay valid until emb_destroy().
+ * - Streams: every call is enqueued on cfg.stream (a cudaStream_t; NULL = legacy default
+ *   stream) and returns without waiting, unless it is documented to return host values.
+ * - Pointers "host or device": ids, offsets, grad and out arguments may be device
+ *   pointers or host pointers (detected with cudaPointerGetAttributes).  Host inputs are
+ *   copied into library workspace on the stream before the kernels; a host `out` is
+ *   filled by a device-to-host copy enqueued after the kernels.  Host buffers must stay
+ *   valid (and host outputs are only complete) after emb_sync() returns.  Pinned host
+ *   memory gives asynchronous copies; pageable memory works but copies synchronously.
+ * - Errors: argument errors are returned synchronously and nothing is enqueued.  Data-
+ *   dependent errors (out-of-range ids, non-finite gradient norm, non-finite table row
+ *   at quantize) are recorded in a sticky device status word and reported (and cleared)
+ *   by emb_sync().  CUDA launch/copy failures return EMB_ECUDA.
+ * - Threading: one handle per (process, device); calls on a handle are not thread-safe.
+ * - Multi-GPU (world_size > 1): every call is collective -- all ranks must issue the same
+ *   sequence of calls.
+ */
+#ifndef LIRANK_EMB_H
+#define LIRANK_EMB_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EMB_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define EMB_API __attribute__((visibility("default")))
+#else
+#define EMB_API
+#endif
+
+typedef enum {
+  EMB_OK = 0,
+  EMB_EINVAL = 1,      /* bad argument (null pointer, size out of range, misalignment)   */
+  EMB_ENOMEM = 2,      /* a supplied buffer is smaller than emb_plan() asked for         */
+  EMB_ECUDA = 3,       /* a CUDA runtime call failed                                     */
+  EMB_ENCCL = 4,       /* an NCCL call failed                                            */
+  EMB_EIDRANGE = 5,    /* sticky: an id was < 0 or >= rows of its table (it was skipped) */
+  EMB_ENONFINITE = 6,  /* sticky: non-finite global norm (update skipped) or non-finite
+                          row at quantize (row stored as codes 0, middle 0, scale 0)      */
+  EMB_ESTATE = 7       /* call out of order (backward before forward, q8 before quantize) */
+} emb_status;
+
+enum { EMB_POOL_SUM = 0, EMB_POOL_MEAN = 1 };
+enum { EMB_ADAGRAD_ROWWISE = 0, EMB_ADAGRAD_ELEMENTWISE = 1 };
+enum { EMB_SHARD_NONE = 0, EMB_SHARD_TABLE = 1, EMB_SHARD_ROW = 2 };
+
+/* cfg.flags */
+#define EMB_F_Q8 1u       /* allocate the int8 store (codes + per-row meta) for a9/a10       */
+#define EMB_F_REQUANT 2u  /* (needs EMB_F_Q8) every AdaGrad update also re-quantizes the rows
+                             it touched, so the q8 store tracks the fp32 tables between
+                             full emb_quantize_mm8() passes                                   */
+
+typedef struct {
+  uint32_t abi_version;          /* must be EMB_ABI_VERSION                                    */
+  int32_t num_tables;            /* T >= 1                                                    */
+  const int64_t* table_rows;     /* host [T]: rows of each (global, unsharded) table, < 2^31  */
+  int32_t dim;                   /* D in [1, 1024]: embedding width, shared by all tables     */
+  int32_t num_features;          /* F >= 1                                                    */
+  const int32_t* feature_table;  /* host [F]: the table feature f reads.  Several features may
+                                    share a table ("40 categorical features ...
+                                    through 5 shared embedding matrices"); they then share its
+                                    rows, and dedup merges their occurrences (reading 19).    */
+  int32_t pooling;               /* EMB_POOL_SUM (default) or EMB_POOL_MEAN                   */
+  int32_t adagrad_mode;          /* EMB_ADAGRAD_ROWWISE (default) or EMB_ADAGRAD_ELEMENTWISE  */
+  float init_accumulator;        /* AdaGrad A0 (Keras default 0.1)                            */
+  float eps;                     /* AdaGrad epsilon, outside the sqrt (Keras default 1e-7)    */
+  float max_norm;                /* global-norm clip threshold (paper: 1.0)      */
+  int64_t max_nnz;               /* capacity: ids per call on this rank, < 2^30               */
+  int32_t max_batch;             /* capacity: local batch B per call                          */
+  int32_t sharding;              /* EMB_SHARD_NONE (world_size 1), _TABLE or _ROW              */
+  const int32_t* table_owner;    /* host [T] or NULL: explicit table-wise plan (owner rank)   */
+  int32_t rank, world_size;      /* this process's rank and the number of ranks               */
+  const void* nccl_unique_id;    /* 128-byte ncclUniqueId from rank 0 (NULL if world_size 1)  */
+  void* stream;                  /* cudaStream_t every call is enqueued on                    */
+  uint32_t flags;                /* EMB_F_*                                                   */
+} emb_config;
+
+typedef struct {
+  int64_t weights_bytes;    /* fp32 [local_rows][row_pitch]                                    */
+  int64_t accum_bytes;      /* fp32 [local_rows] (row-wise) or [local_rows][row_pitch]         */
+  int64_t q8_codes_bytes;   /* int8 [local_rows][q8_pitch]           (0 without EMB_F_Q8)      */
+  int64_t q8_meta_bytes;    /* fp32 {middle, scale} [local_rows][2]  (0 without EMB_F_Q8)      */
+  int64_t workspace_bytes;  /* library scratch (staging, sort, segment partials, scalars)      */
+  int64_t local_rows;       /* rows stored on this rank (sum over its local tables)            */
+  int32_t row_pitch;        /* floats per stored fp32 row: round_up(D, 4) (16-B aligned rows)  */
+  int32_t q8_pitch;         /* bytes per stored code row: round_up(D, 16)                      */
+} emb_sizes;
+
+typedef struct {
+  void* weights;    /* device; caller initialises it (layout: emb_local_layout) or uses
+                       emb_write_rows                                                      */
+  void* accum;      /* device; emb_create fills it with init_accumulator                   */
+  void* q8_codes;   /* device or NULL without EMB_F_Q8                                     */
+  void* q8_meta;    /* device or NULL without EMB_F_Q8                                     */
+  void* workspace;  /* device                                                              */
+} emb_buffers;
+
+typedef struct emb_handle* emb_t;
+
+EMB_API int32_t emb_abi_version(void);
+EMB_API const char* emb_status_string(emb_status s);
+
+/* Validate cfg and report buffer sizes (host-only; no CUDA calls).  For sharded
+ * configurations it also fixes the plan: table-wise = cfg.table_owner if given, else a
+ * greedy longest-processing-time assignment of tables by rows (ties to the lower rank);
+ * row-wise = rank r owns rows [r*ceil(R/W), (r+1)*ceil(R/W)) of every table. */
+EMB_API emb_status emb_plan(const emb_config* cfg, emb_sizes* out);
+
+/* Per-table layout of this rank's weights buffer (host-only).  For each table t:
+ * local_base[t] = first stored row of table t in `weights` (or -1 if t has no rows
+ * here), row_lo[t] / row_hi[t] = the global rows [row_lo, row_hi) of t stored here.
+ * Stored row (local_base[t] + (r - row_lo[t])) holds global row r of table t. */
+EMB_API emb_status emb_local_layout(const emb_config* cfg, int64_t* local_base, int64_t* row_lo,
+                            int64_t* row_hi);
+
+/* Bind buffers, fill the accumulators with init_accumulator, clear the status word, and
+ * (world_size > 1) create the NCCL communicator.  Enqueued on cfg.stream. */
+EMB_API emb_status emb_create(const emb_config* cfg, const emb_buffers* buf, emb_t* out);
+
+/* a2 (+ a1/a3 when sharded).  ids: int32 [nnz] feature-major, offsets: int32 [F*B+1]
+ * with offsets[0] = 0 and offsets[F*B] = nnz; bag (f, b) is ids[offsets[f*B+b] ..
+ * offsets[f*B+b+1]).  out: fp32 [B][F][D] (sample-major, feature order = feature index,
+ * reading 20), 16-B aligned when D % 4 == 0.  Bag sums are taken in bag order; MEAN
+ * divides by the bag length; an empty bag gives zeros.  An id outside [0, rows) of its
+ * table is skipped (contributes 0, gets no gradient) and sets sticky EMB_EIDRANGE.
+ * Also records this batch's (row, bag) occurrences for the next emb_backward_adagrad. */
+EMB_API emb_status emb_forward(emb_t h, const int32_t* ids, const int32_t* offsets, int32_t batch,
+                       int64_t nnz, float* out);
+
+/* a5-a8 (+ a4 when sharded) for the batch of the most recent emb_forward (EMB_ESTATE if
+ * none).  grad_out: fp32 [B][F][D] = dL/d(out) of that forward.  Dedups the occurrences by
+ * (table, row), reduces G_u in fp64, forms the global squared norm
+ * S = sum_u ||G_u||^2 + extra_sq_norm (summed over ranks in rank order), the clip factor
+ * c = min(1, max_norm / sqrt(S)), and applies AdaGrad (cfg.adagrad_mode) with step lr to
+ * the touched rows only.  extra_sq_norm lets the caller fold the dense-tower gradient into
+ * the global norm (pass 0 otherwise).  Non-finite S: no row is updated, sticky
+ * EMB_ENONFINITE.  If sq_norm_out (host) is non-NULL the call waits for the step and
+ * returns S there. */
+EMB_API emb_status emb_backward_adagrad(emb_t h, const float* grad_out, float lr, double extra_sq_norm,
+                                double* sq_norm_out);
+
+/* a9: quantize every local row (middle-max, 8 bits) into the q8 store.
+ * The fp32 tables are kept.  EMB_ESTATE without EMB_F_Q8. */
+EMB_API emb_status emb_quantize_mm8(emb_t h);
+
+/* a10: like emb_forward, but reading the q8 store: out = sum in bag order of
+ * fmaf(code, scale, middle).  EMB_ESTATE before the first emb_quantize_mm8 (unless
+ * EMB_F_REQUANT has kept it current).  Does not record occurrences for backward. */
+EMB_API emb_status emb_forward_q8(emb_t h, const int32_t* ids, const int32_t* offsets, int32_t batch,
+                          int64_t nnz, float* out);
+
+/* Wait for the stream; return and clear the sticky status (EMB_OK if none). */
+EMB_API emb_status emb_sync(emb_t h);
+
+/* Synchronous introspection (waits for the stream).  Rows are GLOBAL row indices of
+ * `table`; every requested row must be stored on this rank (EMB_EINVAL otherwise).
+ * w: host fp32 [n][D]; acc: host fp32 [n] (row-wise) or [n][D] (element-wise), may be
+ * NULL. */
+EMB_API emb_status emb_read_rows(emb_t h, int32_t table, const int64_t* rows, int64_t n, float* w,
+                         float* acc);
+EMB_API emb_status emb_write_rows(emb_t h, int32_t table, const int64_t* rows, int64_t n,
+                          const float* w, const float* acc);
+/* codes: host int8 [n][D]; middle, scale: host fp32 [n] (either may be NULL). */
+EMB_API emb_status emb_read_q8(emb_t h, int32_t table, const int64_t* rows, int64_t n, int8_t* codes,
+                       float* middle, float* scale);
+
+/* Synchronous: the dedup of the last backward (a5).  unique: host int32 [cap] local row
+ * keys (stored-row indices, ascending); seg_offsets: host int32 [cap+1] CSR starts into
+ * the sorted occurrence list; sorted_bags: host int32 [cap_occ] bag index (f*B+b) of each
+ * sorted occurrence (may be NULL).  n_unique / n_valid receive U and the number of valid
+ * occurrences.  EMB_ENOMEM if cap < U or cap_occ < n_valid. */
+EMB_API emb_status emb_last_dedup(emb_t h, int32_t* unique, int32_t* seg_offsets, int64_t cap,
+                          int32_t* sorted_bags, int64_t cap_occ, int64_t* n_unique,
+                          int64_t* n_valid);
+
+/* Synchronous: scalars of the last backward: global squared norm S (incl. extra and
+ * other ranks), clip factor c, U on this rank. */
+EMB_API emb_status emb_last_stats(emb_t h, double* sq_norm, float* clip, int64_t* n_unique);
+
+/* Number of kernels this handle has launched so far (for launch accounting). */
+EMB_API int64_t emb_kernel_launches(emb_t h);
+
+/* Release the handle (and its NCCL communicator).  Does not free caller buffers. */
+EMB_API emb_status emb_destroy(emb_t h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LIRANK_EMB_H */

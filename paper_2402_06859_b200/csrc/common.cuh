@@ -1,0 +1,92 @@
+// common.cuh -- shared device helpers for the LiRank embedding kernels (sm_100a).
+//
+// Numerics discipline (SURVEY.md §7 "bit-exactness discipline"): the library is built
+// with -fmad=false and without fast-math, and every parity-critical float operation is
+// written with an explicit round-to-nearest intrinsic (__fadd_rn, __fmul_rn, __fdiv_rn,
+// __fsqrt_rn) so the operation order of SURVEY.md §8(c) is the one executed.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace lirank {
+
+constexpr int kWarp = 32;
+
+// Sticky status bits (device word; emb_sync maps them to emb_status).
+constexpr uint32_t kStIdRange = 1u;
+constexpr uint32_t kStNonFinite = 2u;
+
+// ---------------------------------------------------------------------------
+// Row-group geometry.  One "group" of LPB lanes (a power of two <= 32) owns one
+// embedding row of nvec = pitch/4 float4 vectors; lane l holds vectors l, l+LPB, ...
+// (VPL = ceil(nvec / LPB) per lane).  D=64: LPB=16, VPL=1 -> half-warp per row,
+// one 128-bit load per lane, 256 B per row request.
+// ---------------------------------------------------------------------------
+struct Geom {
+  int lpb;  // lanes per group
+  int vpl;  // float4 vectors per lane
+};
+
+inline Geom geom_for(int pitch) {
+  int nvec = pitch / 4;
+  int lpb = 1;
+  while (lpb < nvec && lpb < 32) lpb <<= 1;
+  int vpl = (nvec + lpb - 1) / lpb;
+  return Geom{lpb, vpl};
+}
+
+// Group-level shuffle helpers (width = LPB).
+template <int LPB>
+__device__ __forceinline__ unsigned group_mask() {
+  if constexpr (LPB == 32) {
+    return 0xffffffffu;
+  } else {
+    unsigned lane = threadIdx.x & 31;
+    unsigned base = lane & ~(unsigned)(LPB - 1);
+    return ((1u << LPB) - 1u) << base;
+  }
+}
+
+// 128-bit streaming loads/stores.
+__device__ __forceinline__ float4 ld_nc_f4(const float* p) {
+  float4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ float4 ld_f4(const float* p) {
+  return *reinterpret_cast<const float4*>(p);
+}
+__device__ __forceinline__ void st_f4(float* p, float4 v) {
+  *reinterpret_cast<float4*>(p) = v;
+}
+__device__ __forceinline__ int ld_nc_i32(const int* p) {
+  int r;
+  asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(r) : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ float4 f4_add_rn(float4 a, float4 b) {
+  return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z),
+                     __fadd_rn(a.w, b.w));
+}
+
+__device__ __forceinline__ void set_status(uint32_t* st, uint32_t bit) {
+  // Rare path; one atomic per offending warp is plenty.
+  atomicOr(st, bit);
+}
+
+// Per-feature metadata resolved on the host (row addressing).
+// An id i of feature f is valid iff 0 <= i < rows; it is stored on this rank iff
+// lo <= i < hi, at stored row base + (i - lo).
+struct FeatMeta {
+  int64_t base;  // stored row of global row `lo` of the feature's table (-1: not local)
+  int32_t rows;  // global rows of the table
+  int32_t lo;    // first global row stored here
+  int32_t hi;    // one past the last global row stored here
+  int32_t pad;
+};
+
+}  // namespace lirank

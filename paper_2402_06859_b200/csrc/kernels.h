@@ -1,0 +1,125 @@
+// kernels.h -- internal launcher interface between api.cu and the kernel files.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace lirank {
+
+struct FwdArgs {
+  const float* W;
+  int pitch;
+  const int* ids;
+  const int* offsets;
+  int B, F, D;
+  const FeatMeta* meta;
+  float* out;
+  uint32_t* keys_out;  // NULL: do not record occurrences
+  uint32_t* vals_out;
+  uint32_t sentinel;
+  uint32_t* status;
+  bool mean;
+};
+cudaError_t launch_pool_fwd_f32(const FwdArgs& a, cudaStream_t s);
+
+struct FwdQ8Args {
+  const uint8_t* codes;
+  int qpitch;
+  const float2* qmeta;
+  const int* ids;
+  const int* offsets;
+  int B, F, D;
+  const FeatMeta* meta;
+  float* out;
+  uint32_t* status;
+  bool mean;
+};
+cudaError_t launch_pool_fwd_q8(const FwdQ8Args& a, cudaStream_t s);
+
+// ---- a5 dedup: LSD radix sort (onesweep) + run-length encode -------------------------
+constexpr int kRadixBits = 8;
+constexpr int kRadixBins = 1 << kRadixBits;
+constexpr int kSortThreads = 256;
+constexpr int kSortItems = 16;  // per thread
+constexpr int kSortTile = kSortThreads * kSortItems;
+constexpr int kMaxPasses = 4;   // keys < 2^32
+
+struct SortWs {
+  uint32_t* hist;         // [kMaxPasses][kRadixBins] (zeroed by the sort)
+  uint32_t* counters;     // [kMaxPasses + 2] dynamic tile counters (zeroed by the sort)
+  unsigned long long* status;  // [max_tiles][kRadixBins] look-back words (epoch tagged)
+  int64_t max_tiles;
+};
+
+// Sorts (keys, vals) of length n by the low `bits` bits of key, stably.  Ping-pongs
+// between (k0,v0) and (k1,v1); returns in *result_in_1 whether the result is in (k1,v1).
+cudaError_t radix_sort_pairs(uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1, int64_t n,
+                             int bits, const SortWs& ws, uint32_t epoch, int* passes_out,
+                             bool* result_in_1, int64_t* launches, cudaStream_t s);
+
+// Run-length encode sorted keys (sentinel = invalid, sorts last): unique[U], seg[U+1],
+// *U_out (device int32).  Requires seg/U prepared by the caller only for n == 0.
+cudaError_t launch_rle(const uint32_t* keys, int64_t n, uint32_t sentinel, uint32_t* unique,
+                       uint32_t* seg, uint32_t* U_out, uint32_t* counter,
+                       unsigned long long* status, uint32_t epoch, cudaStream_t s);
+
+// ---- a6-a8 ----------------------------------------------------------------------------
+constexpr int kChunk = 256;  // occurrences per group in the segment-reduce
+
+struct BwdArgs {
+  // dedup results
+  const uint32_t* unique;   // [U]
+  const uint32_t* seg;      // [U+1]
+  const uint32_t* U;        // device scalar
+  const uint32_t* vals;     // sorted bag index per occurrence
+  int64_t nnz;              // upper bound of valid occurrences
+  // gradient input
+  const float* grad;        // [B][F][D]
+  const int* offsets;       // [F*B+1] (MEAN only)
+  int B, F, D, pitch;
+  bool mean;
+  // workspace
+  float* G;                 // [max_unique][pitch]
+  double* part_first;       // [chunks][pitch]
+  double* part_last;        // [chunks][pitch]
+  double* norm_main;        // [chunks]
+  double* norm_fix;         // [chunks]
+  uint32_t* owner_list;     // [chunks]
+  uint32_t* owner_count;    // device scalar (zeroed by launch_segreduce)
+  int64_t chunks;
+  // norm / clip
+  double* S_local;          // device scalar: this rank's sum of squares
+  double* S_global;         // device scalar
+  float* clip;              // device scalar
+  uint32_t* status;
+  double extra_sq_norm;
+  float max_norm;
+  // update
+  float* Wt;                // tables
+  float* A;                 // accumulators
+  bool rowwise;
+  float lr, eps;
+  uint8_t* q8_codes;        // requantize touched rows (NULL: no)
+  float2* q8_meta;
+  int qpitch;
+};
+cudaError_t launch_segreduce(const BwdArgs& a, int64_t* launches, cudaStream_t s);
+// reduces norm partials -> S_local (deterministic fixed order)
+cudaError_t launch_norm_partial(const BwdArgs& a, cudaStream_t s);
+// S_global = sum of `nparts` rank partials (rank order) + extra -> clip factor, status
+cudaError_t launch_norm_finalize(const double* parts, int nparts, const BwdArgs& a,
+                                 cudaStream_t s);
+cudaError_t launch_adagrad(const BwdArgs& a, cudaStream_t s);
+
+// ---- a9 ----------------------------------------------------------------------------
+cudaError_t launch_quantize(const float* W, int pitch, int64_t rows, int D, uint8_t* codes,
+                            int qpitch, float2* qmeta, uint32_t* status, cudaStream_t s);
+
+// ---- misc --------------------------------------------------------------------------
+cudaError_t launch_fill(float* p, int64_t n, float v, cudaStream_t s);
+cudaError_t launch_gather_rows(const float* src, int pitch, const int64_t* rows, int64_t n,
+                               int D, float* dst, cudaStream_t s);
+
+}  // namespace lirank

@@ -1,0 +1,223 @@
+"""Thin Python front end of the C ABI: torch tensors supply device memory and streams.
+
+Every step of the hot path runs in liblirank_emb.so; this module only allocates the
+buffers emb_plan() asks for, passes pointers, and converts statuses to exceptions.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib as L
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _arr(a, ctype):
+    a = np.ascontiguousarray(a)
+    return a, a.ctypes.data_as(C.POINTER(ctype))
+
+
+class ShardedEmbedding:
+    """Embedding tables of the LiRank sparse path on one GPU (one shard when world_size > 1).
+
+    Tables: ``table_rows[t]`` rows of width ``dim``; feature f reads table
+    ``feature_table[f]``.  Inputs per call: feature-major ids [nnz] and offsets [F*B+1]
+    (int32, CUDA or CPU-pinned tensors); output [B, F, dim] fp32.
+    """
+
+    def __init__(self, table_rows: Sequence[int], dim: int, feature_table: Sequence[int], *,
+                 max_nnz: int, max_batch: int, pooling: str = "sum",
+                 adagrad: str = "rowwise", init_accumulator: float = 0.1, eps: float = 1e-7,
+                 max_norm: float = 1.0, q8: bool = False, requant: bool = False,
+                 device: Optional[torch.device] = None, stream: Optional[torch.cuda.Stream] = None,
+                 rank: int = 0, world_size: int = 1, sharding: str = "none",
+                 table_owner: Optional[Sequence[int]] = None, nccl_unique_id: Optional[bytes] = None):
+        self.lib = L.load()
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        self.dim = int(dim)
+        self.num_features = len(feature_table)
+        self.table_rows = [int(r) for r in table_rows]
+        self._rows, rows_p = _arr(np.asarray(table_rows, dtype=np.int64), C.c_int64)
+        self._ft, ft_p = _arr(np.asarray(feature_table, dtype=np.int32), C.c_int32)
+        owner_p = None
+        if table_owner is not None:
+            self._owner, owner_p = _arr(np.asarray(table_owner, dtype=np.int32), C.c_int32)
+        self._uid = None
+        if nccl_unique_id is not None:
+            self._uid = C.create_string_buffer(bytes(nccl_unique_id), len(nccl_unique_id))
+        self.cfg = L.EmbConfig(
+            abi_version=L.EMB_ABI_VERSION, num_tables=len(self.table_rows), table_rows=rows_p,
+            dim=self.dim, num_features=self.num_features, feature_table=ft_p,
+            pooling={"sum": L.EMB_POOL_SUM, "mean": L.EMB_POOL_MEAN}[pooling],
+            adagrad_mode={"rowwise": L.EMB_ADAGRAD_ROWWISE, "elementwise": L.EMB_ADAGRAD_ELEMENTWISE}[adagrad],
+            init_accumulator=init_accumulator, eps=eps, max_norm=max_norm,
+            max_nnz=int(max_nnz), max_batch=int(max_batch),
+            sharding={"none": L.EMB_SHARD_NONE, "table": L.EMB_SHARD_TABLE, "row": L.EMB_SHARD_ROW}[sharding],
+            table_owner=owner_p, rank=rank, world_size=world_size,
+            nccl_unique_id=C.cast(self._uid, C.c_void_p) if self._uid is not None else None,
+            stream=C.c_void_p(self.stream.cuda_stream),
+            flags=(L.EMB_F_Q8 if (q8 or requant) else 0) | (L.EMB_F_REQUANT if requant else 0))
+        self.sizes = L.EmbSizes()
+        L.check(self.lib.emb_plan(C.byref(self.cfg), C.byref(self.sizes)), "emb_plan")
+        s = self.sizes
+        nT = len(self.table_rows)
+        self.local_base = np.zeros(nT, dtype=np.int64)
+        self.row_lo = np.zeros(nT, dtype=np.int64)
+        self.row_hi = np.zeros(nT, dtype=np.int64)
+        L.check(self.lib.emb_local_layout(C.byref(self.cfg), self.local_base.ctypes.data_as(C.c_void_p),
+                                          self.row_lo.ctypes.data_as(C.c_void_p),
+                                          self.row_hi.ctypes.data_as(C.c_void_p)), "emb_local_layout")
+        dev = self.device
+
+        def alloc(nbytes, dtype=torch.uint8):
+            n = max(int(nbytes), 16)
+            return torch.empty(n, dtype=torch.uint8, device=dev)
+
+        self.weights_buf = alloc(s.weights_bytes)
+        self.accum_buf = alloc(s.accum_bytes)
+        self.workspace = alloc(s.workspace_bytes)
+        self.codes_buf = alloc(s.q8_codes_bytes) if s.q8_codes_bytes else None
+        self.meta_buf = alloc(s.q8_meta_bytes) if s.q8_meta_bytes else None
+        self.local_rows = int(s.local_rows)
+        self.pitch = int(s.row_pitch)
+        self.q8_pitch = int(s.q8_pitch)
+        bufs = L.EmbBuffers(_ptr(self.weights_buf), _ptr(self.accum_buf), _ptr(self.codes_buf),
+                            _ptr(self.meta_buf), _ptr(self.workspace))
+        self.h = C.c_void_p()
+        L.check(self.lib.emb_create(C.byref(self.cfg), C.byref(bufs), C.byref(self.h)), "emb_create")
+
+    # ---- views -------------------------------------------------------------------------
+    @property
+    def weights(self) -> torch.Tensor:
+        """fp32 [local_rows, row_pitch] view of the stored tables (device)."""
+        n = self.local_rows * self.pitch
+        return self.weights_buf[: 4 * n].view(torch.float32).view(self.local_rows, self.pitch)
+
+    def table_view(self, t: int) -> torch.Tensor:
+        b = int(self.local_base[t])
+        if b < 0:
+            return self.weights[:0]
+        return self.weights[b: b + int(self.row_hi[t] - self.row_lo[t])]
+
+    # ---- hot path ----------------------------------------------------------------------
+    def forward(self, ids: torch.Tensor, offsets: torch.Tensor, batch: int,
+                out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        if out is None:
+            out = torch.empty((batch, self.num_features, self.dim), dtype=torch.float32,
+                              device=ids.device if ids.is_cuda else "cpu", pin_memory=not ids.is_cuda)
+        _check_io(ids, offsets, out)
+        L.check(self.lib.emb_forward(self.h, _ptr(ids), _ptr(offsets), int(batch), int(ids.numel()),
+                                     _ptr(out)), "emb_forward")
+        return out
+
+    def backward_adagrad(self, grad: torch.Tensor, lr: float, extra_sq_norm: float = 0.0,
+                         want_norm: bool = False):
+        assert grad.dtype == torch.float32 and grad.is_contiguous()
+        if want_norm:
+            S = C.c_double(0)
+            L.check(self.lib.emb_backward_adagrad(self.h, _ptr(grad), float(lr), float(extra_sq_norm),
+                                                  C.byref(S)), "emb_backward_adagrad")
+            return S.value
+        L.check(self.lib.emb_backward_adagrad(self.h, _ptr(grad), float(lr), float(extra_sq_norm), None),
+                "emb_backward_adagrad")
+        return None
+
+    def quantize(self):
+        L.check(self.lib.emb_quantize_mm8(self.h), "emb_quantize_mm8")
+
+    def forward_q8(self, ids: torch.Tensor, offsets: torch.Tensor, batch: int,
+                   out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        if out is None:
+            out = torch.empty((batch, self.num_features, self.dim), dtype=torch.float32,
+                              device=ids.device if ids.is_cuda else "cpu", pin_memory=not ids.is_cuda)
+        _check_io(ids, offsets, out)
+        L.check(self.lib.emb_forward_q8(self.h, _ptr(ids), _ptr(offsets), int(batch), int(ids.numel()),
+                                        _ptr(out)), "emb_forward_q8")
+        return out
+
+    def sync(self, raise_on_error: bool = False) -> int:
+        code = self.lib.emb_sync(self.h)
+        if raise_on_error:
+            L.check(code, "emb_sync")
+        return code
+
+    # ---- introspection -----------------------------------------------------------------
+    def read_rows(self, table: int, rows, with_acc: bool = True):
+        rows = np.ascontiguousarray(rows, dtype=np.int64)
+        w = np.zeros((len(rows), self.dim), dtype=np.float32)
+        acc = None
+        if with_acc:
+            acc = np.zeros((len(rows),) if self.cfg.adagrad_mode == L.EMB_ADAGRAD_ROWWISE
+                           else (len(rows), self.dim), dtype=np.float32)
+        L.check(self.lib.emb_read_rows(self.h, int(table), rows.ctypes.data_as(C.c_void_p), len(rows),
+                                       w.ctypes.data_as(C.c_void_p),
+                                       acc.ctypes.data_as(C.c_void_p) if acc is not None else None),
+                "emb_read_rows")
+        return (w, acc) if with_acc else w
+
+    def write_rows(self, table: int, rows, w=None, acc=None):
+        rows = np.ascontiguousarray(rows, dtype=np.int64)
+        wp = None if w is None else np.ascontiguousarray(w, dtype=np.float32)
+        ap = None if acc is None else np.ascontiguousarray(acc, dtype=np.float32)
+        L.check(self.lib.emb_write_rows(self.h, int(table), rows.ctypes.data_as(C.c_void_p), len(rows),
+                                        None if wp is None else wp.ctypes.data_as(C.c_void_p),
+                                        None if ap is None else ap.ctypes.data_as(C.c_void_p)),
+                "emb_write_rows")
+
+    def read_q8(self, table: int, rows):
+        rows = np.ascontiguousarray(rows, dtype=np.int64)
+        codes = np.zeros((len(rows), self.dim), dtype=np.int8)
+        mid = np.zeros(len(rows), dtype=np.float32)
+        sc = np.zeros(len(rows), dtype=np.float32)
+        L.check(self.lib.emb_read_q8(self.h, int(table), rows.ctypes.data_as(C.c_void_p), len(rows),
+                                     codes.ctypes.data_as(C.c_void_p), mid.ctypes.data_as(C.c_void_p),
+                                     sc.ctypes.data_as(C.c_void_p)), "emb_read_q8")
+        return codes, mid, sc
+
+    def last_dedup(self, with_bags: bool = True):
+        U = C.c_int64(0)
+        nv = C.c_int64(0)
+        L.check(self.lib.emb_last_dedup(self.h, None, None, 0, None, 0, C.byref(U), C.byref(nv)),
+                "emb_last_dedup")
+        uniq = np.zeros(max(U.value, 1), dtype=np.int32)
+        seg = np.zeros(U.value + 1, dtype=np.int32)
+        bags = np.zeros(max(nv.value, 1), dtype=np.int32) if with_bags else None
+        L.check(self.lib.emb_last_dedup(self.h, uniq.ctypes.data_as(C.c_void_p), seg.ctypes.data_as(C.c_void_p),
+                                        len(uniq), None if bags is None else bags.ctypes.data_as(C.c_void_p),
+                                        0 if bags is None else len(bags), C.byref(U), C.byref(nv)),
+                "emb_last_dedup")
+        return uniq[:U.value], seg, (bags[:nv.value] if bags is not None else None)
+
+    def last_stats(self):
+        S = C.c_double(0)
+        c = C.c_float(0)
+        U = C.c_int64(0)
+        L.check(self.lib.emb_last_stats(self.h, C.byref(S), C.byref(c), C.byref(U)), "emb_last_stats")
+        return S.value, np.float32(c.value), U.value
+
+    @property
+    def launches(self) -> int:
+        return int(self.lib.emb_kernel_launches(self.h))
+
+    def close(self):
+        if getattr(self, "h", None) and self.h.value:
+            self.lib.emb_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _check_io(ids, offsets, out):
+    assert ids.dtype == torch.int32 and offsets.dtype == torch.int32 and out.dtype == torch.float32
+    assert ids.is_contiguous() and offsets.is_contiguous() and out.is_contiguous()

@@ -1,0 +1,432 @@
+"""GPU parity: the sm_100a path through the C ABI vs the CPU oracle on the same seeded inputs.
+
+Gates (BASELINE.json north_star, SURVEY.md §8(c) comparison classes):
+* dedup (unique rows, segment offsets, sorted bag list), int8 codes and q8 metadata:
+  bit-exact;
+* pooled fp32 outputs: |gpu - ora| <= 1e-5 * sum_j |term_j| (condition-aware 1e-5 rel.);
+* updated accumulators: <= 1e-6 relative; updated rows: <= 1e-6 * max(|w'|, |w|, |step|).
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from helpers import (Compact, cond_close, dense_tables, init_tables_gpu, init_tables_host, make_emb,
+                     problem, sample_bags, w_close)
+from workload import configs, gen
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def dev(a, dtype=None):
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    if dtype is not None:
+        t = t.to(dtype)
+    return t.cuda()
+
+
+def small_cfg(dim=32, rows=(10_000, 3000, 777, 10_000), F=None, B=256, maxlen=10, seed=1):
+    ft = F if F is not None else list(range(len(rows)))
+    return configs.Config(f"small{dim}", list(rows), dim, [(t, ("range", 0, maxlen)) for t in ft], B, seed=seed)
+
+
+# ---------------------------------------------------------------------------
+# generator pin (the GPU copy of workload/gen.py)
+# ---------------------------------------------------------------------------
+
+def test_gpu_generator_matches_numpy(gpu):
+    from workload import gpu as G
+    buf = torch.zeros(1000 * 68, device=gpu)
+    G.fill_table(buf, 1000, 66, 68, 12345, 3, row0=999_000_000)
+    torch.cuda.synchronize()
+    got = buf.view(1000, 68).cpu().numpy()
+    ref = gen.table_rows(12345, 3, np.arange(999_000_000, 999_001_000), 66)
+    assert (got[:, :66] == ref).all() and (got[:, 66:] == 0).all()
+    g = torch.zeros(7 * 3 * 16, device=gpu)
+    G.fill_grad(g, 7, 3, 16, 99, 5, 30, sample0=11)
+    torch.cuda.synchronize()
+    assert (g.view(7, 3, 16).cpu().numpy() == gen.grad_values(99, 5, 7, 3, 16, 30, sample0=11)).all()
+
+
+# ---------------------------------------------------------------------------
+# a2 forward
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("dim", [32, 64, 128, 30, 8, 4, 1, 256, 1000])
+@pytest.mark.parametrize("pooling", ["sum", "mean"])
+def test_forward_small(gpu, dim, pooling):
+    cfg = small_cfg(dim=dim, rows=(5000, 300, 7), F=[0, 1, 0, 2, 1])
+    B = 200
+    ids, off = gen.make_batch(cfg.table_rows, cfg.features, B, cfg.seed, 0, alpha=1.05)
+    emb = make_emb(cfg, max_nnz=len(ids) + 10, max_batch=B, pooling=pooling)
+    init_tables_host(emb, cfg)
+    out = emb.forward(dev(ids), dev(off), B)
+    assert emb.sync() == 0
+    pb = problem(cfg, 1 if pooling == "mean" else 0)
+    W = dense_tables(cfg)
+    ref, bad = O.forward(pb, W, ids, off, B)
+    mag, _ = O.forward(pb, np.abs(W), ids, off, B)
+    got = out.cpu().numpy()
+    assert bad == 0
+    assert cond_close(got, ref, mag).all()
+    assert (got == ref).all()  # same add order -> bit-exact expected
+
+
+def test_forward_invalid_ids_and_empty_bags(gpu):
+    cfg = small_cfg(dim=64, rows=(100, 50))
+    B = 64
+    ids, off = gen.make_batch(cfg.table_rows, cfg.features, B, 3, 0)
+    ids = ids.copy()
+    ids[::7] = -3
+    ids[1::11] = 10**6
+    emb = make_emb(cfg, max_nnz=len(ids), max_batch=B)
+    init_tables_host(emb, cfg)
+    out = emb.forward(dev(ids), dev(off), B)
+    from paper_2402_06859_b200._lib import EMB_EIDRANGE
+    assert emb.sync() == EMB_EIDRANGE
+    assert emb.sync() == 0  # cleared
+    ref, bad = O.forward(problem(cfg), dense_tables(cfg), ids, off, B)
+    assert bad > 0
+    assert (out.cpu().numpy() == ref).all()
+    assert (np.diff(off) == 0).any()
+
+
+def test_forward_long_bag_and_duplicates(gpu):
+    cfg = small_cfg(dim=64, rows=(1000,), F=[0])
+    B = 3
+    lens = [100_000, 0, 5]
+    rng = np.random.default_rng(0)
+    ids = rng.integers(0, 1000, sum(lens)).astype(np.int32)
+    ids[-5:] = 7  # duplicates inside a bag count with multiplicity
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    emb = make_emb(cfg, max_nnz=len(ids), max_batch=B)
+    init_tables_host(emb, cfg)
+    out = emb.forward(dev(ids), dev(off), B).cpu().numpy()
+    ref, _ = O.forward(problem(cfg), dense_tables(cfg), ids, off, B)
+    assert (out == ref).all()
+
+
+def test_forward_host_pointers_equal_device(gpu):
+    cfg = configs.tiny()
+    ids, off = gen.make_batch(cfg.table_rows, cfg.features, cfg.batch, cfg.seed, 1)
+    emb = make_emb(cfg, max_nnz=len(ids), max_batch=cfg.batch)
+    init_tables_host(emb, cfg)
+    a = emb.forward(dev(ids), dev(off), cfg.batch).cpu().numpy()
+    hi = torch.from_numpy(ids).pin_memory()
+    ho = torch.from_numpy(off).pin_memory()
+    out_h = torch.empty((cfg.batch, cfg.num_features, cfg.dim), dtype=torch.float32).pin_memory()
+    emb.forward(hi, ho, cfg.batch, out=out_h)
+    assert emb.sync() == 0
+    assert (out_h.numpy() == a).all()
+
+
+# ---------------------------------------------------------------------------
+# a5-a8 backward
+# ---------------------------------------------------------------------------
+
+def run_train_step(cfg, mode, pooling="sum", lr=0.05, gshift=None, ids=None, off=None, B=None,
+                   init="host", extra=0.0, max_norm=1.0):
+    B = cfg.batch if B is None else B
+    if ids is None:
+        ids, off = gen.make_batch(cfg.table_rows, cfg.features, B, cfg.seed, 0, alpha=cfg.alpha)
+    nnz = len(ids)
+    gshift = gen.grad_shift_for(nnz, cfg.dim) if gshift is None else gshift
+    grad = gen.grad_values(cfg.seed, 0, B, cfg.num_features, cfg.dim, gshift)
+    emb = make_emb(cfg, max_nnz=max(nnz, 1), max_batch=B, adagrad=mode, pooling=pooling, max_norm=max_norm)
+    (init_tables_host if init == "host" else init_tables_gpu)(emb, cfg)
+    out = emb.forward(dev(ids), dev(off), B)
+    S = emb.backward_adagrad(dev(grad), lr, extra_sq_norm=extra, want_norm=True)
+    st = emb.sync()
+    return emb, ids, off, B, grad, out, S, st
+
+
+@pytest.mark.parametrize("mode", ["rowwise", "elementwise"])
+@pytest.mark.parametrize("pooling", ["sum", "mean"])
+@pytest.mark.parametrize("dim", [32, 64, 30])
+def test_train_step_small_dense_oracle(gpu, mode, pooling, dim):
+    cfg = small_cfg(dim=dim, rows=(2000, 500, 60), F=[0, 1, 0, 2], B=256)
+    emb, ids, off, B, grad, out, S, st = run_train_step(cfg, mode, pooling)
+    assert st == 0
+    pb = problem(cfg, 1 if pooling == "mean" else 0)
+    W0 = dense_tables(cfg)
+    W = W0.copy()
+    A = np.full((cfg.total_rows,) if mode == "rowwise" else (cfg.total_rows, dim), 0.1, dtype=np.float32)
+    r = O.train_step(pb, W, A, ids, off, B, grad, 0.05, 1e-7, 1.0, mode=mode)
+    # forward bit-exact
+    assert (out.cpu().numpy() == r["out"]).all()
+    # dedup bit-exact
+    keys, segs, bags = O.dedup(pb, ids, off, B)
+    u, s, bg = emb.last_dedup()
+    assert (u == keys).all() and (s == segs).all() and (bg == bags).all()
+    # norm / clip
+    S_gpu, c_gpu, U = emb.last_stats()
+    assert U == len(keys)
+    assert abs(S_gpu - r["S"]) <= 1e-12 * r["S"]
+    assert abs(float(c_gpu) - float(r["c"])) <= 2e-7 * float(r["c"])
+    if pooling == "sum":
+        assert r["c"] < 1.0  # clip active at the generated grad scale
+    # updated rows (touched) and untouched rows
+    base = np.concatenate([[0], np.cumsum(cfg.table_rows)])
+    Wg, Ag = [], []
+    for t in range(cfg.num_tables):
+        w, a = emb.read_rows(t, np.arange(cfg.table_rows[t]))
+        Wg.append(w)
+        Ag.append(a)
+    Wg, Ag = np.concatenate(Wg), np.concatenate(Ag)
+    G = O.segment_reduce(pb, off, B, segs, bags, grad)
+    g = O.clip(G, r["c"])
+    if mode == "rowwise":
+        den = np.sqrt(A[keys]) + np.float32(1e-7)
+        step = np.abs(0.05 / den[:, None] * g)
+        assert (np.abs(Ag - A) <= 1e-6 * np.abs(A)).all()
+    else:
+        den = np.sqrt(A[keys]) + np.float32(1e-7)
+        step = np.abs(0.05 * g / den)
+        assert (np.abs(Ag - A) <= 1e-6 * np.abs(A)).all()
+    assert w_close(Wg[keys], W[keys], W0[keys], step).all()
+    untouched = np.setdiff1d(np.arange(cfg.total_rows), keys)
+    assert (Wg[untouched] == W0[untouched]).all()
+    frac = (Wg[keys] == W[keys]).mean()
+    assert frac > 0.99, frac  # bit-exact except rare 1-ulp fp64-order flips
+
+
+def test_train_step_clip_inactive_and_extra_norm(gpu):
+    cfg = small_cfg(dim=32)
+    ids, off = gen.make_batch(cfg.table_rows, cfg.features, 256, 5, 0)
+    gshift = gen.grad_shift_for(len(ids), 32, target_norm=0.5)
+    emb, ids, off, B, grad, out, S, st = run_train_step(cfg, "rowwise", ids=ids, off=off, B=256, gshift=gshift)
+    S0, c, U = emb.last_stats()
+    assert c == 1.0 and S0 < 1.0
+    # extra_sq_norm folds a dense-tower norm into the clip ("global gradient")
+    emb, *_ = run_train_step(cfg, "rowwise", ids=ids, off=off, B=256, gshift=gshift, extra=3.0)
+    S1, c1, _ = emb.last_stats()
+    assert abs(S1 - (S0 + 3.0)) < 1e-12 and abs(float(c1) - 1 / np.sqrt(S1)) < 1e-7
+
+
+def test_nonfinite_grad_skips_update(gpu):
+    cfg = small_cfg(dim=32)
+    B = 64
+    ids, off = gen.make_batch(cfg.table_rows, cfg.features, B, 7, 0)
+    grad = gen.grad_values(7, 0, B, cfg.num_features, 32, 30)
+    grad[3, 1, 5] = np.inf
+    emb = make_emb(cfg, max_nnz=len(ids), max_batch=B)
+    init_tables_host(emb, cfg)
+    w0 = emb.weights.clone()
+    emb.forward(dev(ids), dev(off), B)
+    emb.backward_adagrad(dev(grad), 0.05)
+    from paper_2402_06859_b200._lib import EMB_ENONFINITE
+    assert emb.sync() == EMB_ENONFINITE
+    assert torch.equal(emb.weights, w0)
+
+
+def test_empty_batch_and_all_invalid(gpu):
+    cfg = small_cfg(dim=32)
+    emb = make_emb(cfg, max_nnz=100, max_batch=16)
+    init_tables_host(emb, cfg)
+    w0 = emb.weights.clone()
+    ids = np.zeros(0, dtype=np.int32)
+    off = np.zeros(4 * 16 + 1, dtype=np.int32)
+    out = emb.forward(torch.zeros(0, dtype=torch.int32, device=gpu), dev(off), 16)
+    emb.backward_adagrad(torch.ones(16, 4, 32, device=gpu), 0.1)
+    assert emb.sync() == 0
+    assert (out.cpu().numpy() == 0).all() and torch.equal(emb.weights, w0)
+    S, c, U = emb.last_stats()
+    assert U == 0 and S == 0 and c == 1.0
+    ids = np.full(40, -1, dtype=np.int32)
+    off = np.zeros(4 * 16 + 1, dtype=np.int32)
+    off[1:] = 40
+    emb.forward(dev(ids), dev(off), 16)
+    emb.backward_adagrad(torch.ones(16, 4, 32, device=gpu), 0.1)
+    emb.sync()
+    assert torch.equal(emb.weights, w0)
+    assert emb.last_stats()[2] == 0
+
+
+def test_hot_row_spans_many_chunks(gpu):
+    # one row with 300k occurrences: exercises the chunk partials and the long fix-up
+    cfg = small_cfg(dim=64, rows=(5000,), F=[0, 0])
+    B = 4096
+    rng = np.random.default_rng(2)
+    lens = rng.integers(1, 100, 2 * B)
+    ids = rng.integers(0, 5000, lens.sum()).astype(np.int32)
+    ids[rng.random(len(ids)) < 0.7] = 1234
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    emb, ids, off, B, grad, out, S, st = run_train_step(cfg, "rowwise", ids=ids, off=off, B=B)
+    pb = problem(cfg)
+    W0 = dense_tables(cfg)
+    W = W0.copy()
+    A = np.full(5000, 0.1, dtype=np.float32)
+    r = O.train_step(pb, W, A, ids, off, B, grad, 0.05, 1e-7, 1.0)
+    keys, segs, bags = O.dedup(pb, ids, off, B)
+    u, s, bg = emb.last_dedup()
+    assert (u == keys).all() and (s == segs).all() and (bg == bags).all()
+    Sg, c, U = emb.last_stats()
+    assert abs(Sg - r["S"]) <= 1e-9 * r["S"]
+    w, a = emb.read_rows(0, keys)
+    assert (np.abs(a - A[keys]) <= 1e-6 * A[keys]).all()
+    G = O.segment_reduce(pb, off, B, segs, bags, grad)
+    g = O.clip(G, r["c"])
+    step = np.abs(0.05 / (np.sqrt(A[keys]) + 1e-7)[:, None] * g)
+    assert w_close(w, W[keys], W0[keys], step).all()
+
+
+def test_multi_step_and_determinism(gpu):
+    cfg = small_cfg(dim=64, rows=(3000, 800), F=[0, 1, 1], B=512)
+    pb = problem(cfg)
+    W = dense_tables(cfg)
+    A = np.full(cfg.total_rows, 0.1, dtype=np.float32)
+    embs = [make_emb(cfg, max_nnz=20000, max_batch=512) for _ in range(2)]
+    for e in embs:
+        init_tables_host(e, cfg)
+    for step in range(4):
+        ids, off = gen.make_batch(cfg.table_rows, cfg.features, 512, 11, step)
+        grad = gen.grad_values(11, step, 512, 3, 64, gen.grad_shift_for(len(ids), 64))
+        outs = []
+        for e in embs:
+            outs.append(e.forward(dev(ids), dev(off), 512).cpu().numpy())
+            e.backward_adagrad(dev(grad), 0.05)
+            assert e.sync() == 0
+        r = O.train_step(pb, W, A, ids, off, 512, grad, 0.05, 1e-7, 1.0)
+        assert (outs[0] == outs[1]).all()
+        assert cond_close(outs[0], r["out"], O.forward(pb, np.abs(W), ids, off, 512)[0] + 1e-3).all()
+    assert torch.equal(embs[0].weights, embs[1].weights)  # run-to-run deterministic
+    assert torch.equal(embs[0].accum_buf, embs[1].accum_buf)
+    w = np.concatenate([embs[0].read_rows(t, np.arange(r), with_acc=False) for t, r in enumerate(cfg.table_rows)])
+    rel = np.abs(w - W) / np.maximum(np.abs(W), 1e-3)
+    assert rel.max() < 1e-5
+
+
+# ---------------------------------------------------------------------------
+# a9 / a10
+# ---------------------------------------------------------------------------
+
+def special_rows(dim):
+    rows = [np.full(dim, 0.25), np.linspace(-1, 1, dim), np.full(dim, 1e6) + np.arange(dim) % 3 * 0.0625]
+    tie = np.zeros(dim)
+    tie[:5] = [0, 255, 0.5, 1.5, 2.5]
+    tie[5:] = 128
+    rows.append(tie)
+    r = np.zeros(dim)
+    r[0] = 1.0
+    rows.append(r)
+    return np.array(rows, dtype=np.float32)
+
+
+@pytest.mark.parametrize("dim", [64, 32, 30, 128, 5])
+def test_quantize_bit_exact(gpu, dim):
+    cfg = small_cfg(dim=dim, rows=(3000, 41), F=[0, 1])
+    emb = make_emb(cfg, max_nnz=100, max_batch=8, q8=True)
+    init_tables_host(emb, cfg)
+    sp = special_rows(dim)
+    emb.write_rows(0, np.arange(len(sp)), sp)
+    bad = np.full((1, dim), 1.0, dtype=np.float32)
+    bad[0, dim // 2] = np.nan
+    emb.write_rows(1, [40], bad)
+    emb.quantize()
+    from paper_2402_06859_b200._lib import EMB_ENONFINITE
+    assert emb.sync() == EMB_ENONFINITE
+    W = dense_tables(cfg)
+    W[:len(sp)] = sp
+    W[3000 + 40] = bad
+    codes, mid, sc, nbad = O.quantize(W)
+    assert nbad == 1
+    c0, m0, s0 = emb.read_q8(0, np.arange(3000))
+    c1, m1, s1 = emb.read_q8(1, np.arange(41))
+    assert (np.concatenate([c0, c1]) == codes).all()
+    assert (np.concatenate([m0, m1]).view(np.uint32) == mid.view(np.uint32)).all()
+    assert (np.concatenate([s0, s1]).view(np.uint32) == sc.view(np.uint32)).all()
+
+
+@pytest.mark.parametrize("dim", [64, 32, 30])
+def test_forward_q8(gpu, dim):
+    cfg = small_cfg(dim=dim, rows=(4000, 900), F=[0, 1, 0])
+    B = 300
+    ids, off = gen.make_batch(cfg.table_rows, cfg.features, B, 9, 0)
+    ids = ids.copy()
+    ids[5] = -1
+    emb = make_emb(cfg, max_nnz=len(ids), max_batch=B, q8=True)
+    init_tables_host(emb, cfg)
+    emb.quantize()
+    out = emb.forward_q8(dev(ids), dev(off), B).cpu().numpy()
+    from paper_2402_06859_b200._lib import EMB_EIDRANGE
+    assert emb.sync() == EMB_EIDRANGE
+    W = dense_tables(cfg)
+    codes, mid, sc, _ = O.quantize(W)
+    pb = problem(cfg)
+    ref, bad = O.forward_q8(pb, codes, mid, sc, ids, off, B)
+    assert bad == 1
+    assert (out == ref).all()
+
+
+def test_requant_tracks_updates(gpu):
+    cfg = small_cfg(dim=64, rows=(3000,), F=[0, 0])
+    B = 256
+    ids, off = gen.make_batch(cfg.table_rows, cfg.features, B, 4, 0)
+    grad = gen.grad_values(4, 0, B, 2, 64, gen.grad_shift_for(len(ids), 64))
+    emb = make_emb(cfg, max_nnz=len(ids), max_batch=B, q8=True, requant=True)
+    init_tables_host(emb, cfg)
+    emb.quantize()
+    emb.forward(dev(ids), dev(off), B)
+    emb.backward_adagrad(dev(grad), 0.05)
+    assert emb.sync() == 0
+    w = emb.read_rows(0, np.arange(3000), with_acc=False)
+    codes, mid, sc, _ = O.quantize(w)   # oracle quantize of the GPU's updated table
+    c, m, s = emb.read_q8(0, np.arange(3000))
+    assert (c == codes).all() and (m == mid).all() and (s == sc).all()
+
+
+# ---------------------------------------------------------------------------
+# full-size configs (the bench's launch configuration)
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("name", ["jobs", "feed1"])
+def test_full_config_train_step(gpu, name):
+    cfg = configs.get(name)
+    B = cfg.batch
+    ids, off = gen.make_batch(cfg.table_rows, cfg.features, B, cfg.seed, 0, alpha=cfg.alpha)
+    nnz = len(ids)
+    emb = make_emb(cfg, max_nnz=nnz, max_batch=B, q8=True)
+    init_tables_gpu(emb, cfg)
+    gshift = gen.grad_shift_for(nnz, cfg.dim)
+    grad = torch.empty((B, cfg.num_features, cfg.dim), device=gpu)
+    from workload import gpu as G
+    G.fill_grad(grad, B, cfg.num_features, cfg.dim, cfg.seed, 0, gshift)
+    out = emb.forward(dev(ids), dev(off), B)
+    S = emb.backward_adagrad(grad, 0.05, want_norm=True)
+    assert emb.sync() == 0
+    comp = Compact(cfg, ids, off, B)
+    # forward: sampled samples (all features) vs the oracle
+    rng = np.random.default_rng(0)
+    samples = np.sort(rng.choice(B, 64, replace=False))
+    sids, soff = sample_bags(cfg, comp.cids, off, B, samples)
+    ref, _ = O.forward(comp.pb, comp.W, sids, soff, len(samples))
+    got = out.cpu().numpy()[samples]
+    assert (got == ref).all()
+    # whole backward on the compact problem
+    W = comp.W.copy()
+    A = np.full(len(comp.keys), 0.1, dtype=np.float32)
+    g_host = grad.cpu().numpy()
+    assert (g_host[:3] == gen.grad_values(cfg.seed, 0, 3, cfg.num_features, cfg.dim, gshift)).all()
+    r = O.train_step(comp.pb, W, A, comp.cids, off, B, g_host, 0.05, 1e-7, 1.0, want_out=False)
+    u, s, bg = emb.last_dedup()
+    keys, segs, bags = O.dedup(comp.pb, comp.cids, off, B)
+    assert len(u) == len(comp.keys) == r["U"]
+    assert (u.astype(np.int64) == comp.keys).all()  # W=1: local key = global key
+    assert (s == segs).all() and (bg == bags).all()
+    assert abs(S - r["S"]) <= 1e-10 * r["S"]
+    # updated rows: a sample of touched rows, incl. the hottest
+    counts = np.diff(segs)
+    pick = np.unique(np.concatenate([np.argsort(counts)[-50:], rng.choice(len(keys), 2000, replace=False)]))
+    for t in np.unique(comp.table_of_key[pick]):
+        m = pick[comp.table_of_key[pick] == t]
+        w, a = emb.read_rows(int(t), comp.row_of_key[m])
+        assert (np.abs(a - A[m]) <= 1e-6 * A[m]).all()
+        assert w_close(w, W[m], comp.W[m], np.abs(W[m] - comp.W[m])).all()
+    # q8 of the updated table on a sample of rows
+    emb.quantize()
+    rows = rng.choice(cfg.table_rows[0], 5000, replace=False)
+    c, mm, ss = emb.read_q8(0, rows)
+    w = emb.read_rows(0, rows, with_acc=False)
+    codes, mid, sc, _ = O.quantize(w)
+    assert (c == codes).all() and (mm == mid).all() and (ss == sc).all()

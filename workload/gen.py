@@ -80,8 +80,14 @@ def table_rows(seed: int, table: int, rows: np.ndarray, dim: int,
     Element counter e = row * dim + d, stream = table.
     """
     rows = np.asarray(rows, dtype=np.uint64).reshape(-1, 1)
-    e = rows * np.uint64(dim) + np.arange(dim, dtype=np.uint64).reshape(1, -1)
-    return ih4_values(stream_key(seed, table), e, shift)
+    key = stream_key(seed, table)
+    out = np.empty((rows.shape[0], dim), dtype=np.float32)
+    step = max(1, (1 << 22) // max(dim, 1))  # bound temporaries to ~4M elements
+    cols = np.arange(dim, dtype=np.uint64).reshape(1, -1)
+    for i in range(0, rows.shape[0], step):
+        e = rows[i:i + step] * np.uint64(dim) + cols
+        out[i:i + step] = ih4_values(key, e, shift)
+    return out
 
 
 def grad_values(seed: int, step: int, batch: int, num_features: int, dim: int,
