@@ -1,0 +1,458 @@
+#!/usr/bin/env python
+"""Benchmark of the LiRank sparse-embedding hot path on B200 (BASELINE.json metric:
+"pooled lookups/s and train samples/s at 1/2/4/8 B200; % HBM roofline").
+
+One step = the whole hot path over one batch: a2 fp32 pooled lookup
+-> a5 dedup -> a6 segment-reduce -> a7 global norm/clip -> a8 clip+row-wise AdaGrad with
+a9 re-quantization of every updated row fused in -> a10 q8 pooled lookup of the same
+batch from the refreshed int8 store.  The full-table a9 pass is timed separately
+(`quantize_full`).  Workload at N=1: Feed-1 (the north_star's
+"1-GPU Feed-shaped config"), synthetic Zipf(1.05) ids, seeded tables.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config feed1] [--impl reference]
+
+Under torchrun (N>1) every rank runs; timing is the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+from workload import configs, gen  # noqa: E402
+
+METRIC = "pooled lookups/s and train samples/s at 1/2/4/8 B200; % HBM roofline"
+LR = 0.05
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="feed1")
+    ap.add_argument("--alpha", type=float, default=None)
+    ap.add_argument("--batches", type=int, default=3, help="distinct resident batches, rotated")
+    ap.add_argument("--adagrad", default="rowwise", choices=["rowwise", "elementwise"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-samples", type=int, default=8192)
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# algorithmic bytes per unit
+# ---------------------------------------------------------------------------
+
+def alg_bytes(phase, cfg, nnz, U, B, pitch, mode="rowwise"):
+    D = cfg.dim
+    F = cfg.num_features
+    row = 4 * pitch
+    if phase == "fwd":       # per id: 4 B id + one fp32 row; per bag: 4 B offset + 4D B output
+        return nnz * (4 + row) + B * F * (4 + 4 * D)
+    if phase == "fwd_q8":    # per id: 4 B id + D B codes + 8 B (middle, scale); per bag as fwd
+        return nnz * (4 + D + 8) + B * F * (4 + 4 * D)
+    if phase == "segreduce":  # per id: 4 B key + 4 B bag + one grad row; per unique: G row write
+        return nnz * (8 + 4 * D) + U * row
+    if phase == "update":    # per unique: G read + w read/write + A (+ key); + requant 72 B out
+        acc = 8 if mode == "rowwise" else 2 * row
+        return U * (row + 2 * row + acc + 4 + (D + 8))
+    if phase == "sort":      # implementation overhead: 16 B/id/pass (reported separately)
+        return None
+    return None
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (pynvml)
+# ---------------------------------------------------------------------------
+
+REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+           0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x1: "gpu_idle",
+           0x2: "applications_clocks_setting", 0x10: "sync_boost"}
+
+
+class ClockSampler(threading.Thread):
+    def __init__(self, index):
+        super().__init__(daemon=True)
+        self.index = index
+        self.samples = []
+        self.reasons = 0
+        self.stop_ev = threading.Event()
+        self.max_mhz = None
+        self.ok = False
+
+    def run(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+            while not self.stop_ev.is_set():
+                self.samples.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                try:
+                    self.reasons |= pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                except Exception:
+                    self.reasons |= pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                time.sleep(0.05)
+        except Exception as e:  # no NVML: report that
+            self.err = repr(e)
+
+    def result(self):
+        self.stop_ev.set()
+        self.join(timeout=2)
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"]}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(n for b, n in REASONS.items() if self.reasons & b and b != 0x1),
+                "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle on a bounded sample (cpu_baseline and --impl reference)
+# ---------------------------------------------------------------------------
+
+class OracleSample:
+    """The oracle's whole step (a2, a5-a8, a9 on the touched rows, a10) on the first
+    `samples` samples of batch 0, over the compact table of the rows they touch."""
+
+    def __init__(self, cfg, ids, off, B, samples, mode):
+        import oracle as O
+        self.O = O
+        F = cfg.num_features
+        Bs = min(samples, B)
+        off64 = off.astype(np.int64)
+        sub_ids, lens = [], []
+        for f in range(F):
+            a, b = off64[f * B], off64[f * B + Bs]
+            sub_ids.append(ids[a:b])
+            lens.append(np.diff(off64[f * B:f * B + Bs + 1]))
+        sids = np.concatenate(sub_ids)
+        soff = np.zeros(F * Bs + 1, dtype=np.int64)
+        soff[1:] = np.cumsum(np.concatenate(lens))
+        base = np.concatenate([[0], np.cumsum(cfg.table_rows)]).astype(np.int64)
+        bag_of = np.repeat(np.arange(F * Bs), np.diff(soff))
+        t = np.asarray(cfg.feature_table, dtype=np.int64)[bag_of // Bs]
+        gkey = base[t] + sids.astype(np.int64)
+        keys = np.unique(gkey)
+        self.cids = np.searchsorted(keys, gkey).astype(np.int32)
+        tk = np.searchsorted(base, keys, side="right") - 1
+        W = np.zeros((len(keys), cfg.dim), dtype=np.float32)
+        for tt in np.unique(tk):
+            m = tk == tt
+            W[m] = gen.table_rows(cfg.seed, int(tt), keys[m] - base[tt], cfg.dim)
+        self.W0 = W
+        self.soff = soff.astype(np.int32)
+        self.Bs = Bs
+        self.nnz = len(sids)
+        self.pb = O.Problem([len(keys)], cfg.dim, [0] * F)
+        self.grad = gen.grad_values(cfg.seed, 0, Bs, F, cfg.dim, gen.grad_shift_for(len(ids), cfg.dim))
+        self.mode = mode
+        self.reset()
+
+    def reset(self):
+        self.W = self.W0.copy()
+        shape = (len(self.W),) if self.mode == "rowwise" else self.W.shape
+        self.A = np.full(shape, 0.1, dtype=np.float32)
+
+    def step(self):
+        O = self.O
+        r = O.train_step(self.pb, self.W, self.A, self.cids, self.soff, self.Bs, self.grad, LR, 1e-7, 1.0,
+                         mode=self.mode)
+        codes, mid, sc, _ = O.quantize(self.W)  # a9 of the touched rows (every row here is touched)
+        O.forward_q8(self.pb, codes, mid, sc, self.cids, self.soff, self.Bs)
+        return r
+
+    def time(self, steps, warmup=0):
+        for _ in range(warmup):
+            self.step()
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            self.step()
+        return (time.perf_counter() - t0) / max(steps, 1)
+
+
+def cpu_baseline(cfg, ids, off, B, samples, mode, budget_s=15.0):
+    smp = OracleSample(cfg, ids, off, B, samples, mode)
+    t1 = smp.time(1)
+    reps = max(1, int(budget_s / max(t1, 1e-3)))
+    t = smp.time(reps)
+    return {"value": smp.Bs / t, "unit": "samples/s", "cores": 1, "kind": "oracle",
+            "sample": f"{smp.Bs} of {B} samples of batch 0 ({smp.nnz} ids), whole step "
+                      f"(a2,a5-a8,a9 on touched rows,a10) over the {len(smp.W)} touched rows, "
+                      f"single-threaded C oracle, {reps + 1} reps"}
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the oracle, as it stands, on the host cores
+# ---------------------------------------------------------------------------
+
+def run_reference(args, cfg, rank, world):
+    if rank != 0:
+        return
+    B = cfg.batch
+    ids, off = gen.make_batch(cfg.table_rows, cfg.features, B, cfg.seed, 0, alpha=cfg.alpha)
+    smp = OracleSample(cfg, ids, off, B, args.cpu_samples, args.adagrad)
+    t = smp.time(args.steps, args.warmup)
+    value = smp.Bs / t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": cfg.name, "sample_batch": smp.Bs, "global_batch": B, "alpha": cfg.alpha,
+                   "parallelism": "cpu-oracle"},
+        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": 1, "kind": "oracle",
+                         "sample": f"{smp.Bs} of {B} samples per step ({smp.nnz} ids), whole step over the "
+                                   f"touched rows, single-threaded C oracle"},
+        "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+def run_ours(args, cfg, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2402_06859_b200 import ShardedEmbedding
+    from workload import gpu as G
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.Stream(dev)
+    B = cfg.batch  # per rank (replicas: weak scaling)
+    D, F = cfg.dim, cfg.num_features
+
+    # inputs: nb distinct batches, resident in HBM (and pinned on the host for e2e)
+    batches = []
+    for k in range(args.batches):
+        ids, off = gen.make_batch(cfg.table_rows, cfg.features, B, cfg.seed + 7919 * rank, k, alpha=cfg.alpha)
+        batches.append((ids, off))
+    max_nnz = max(len(i) for i, _ in batches)
+    emb = ShardedEmbedding(cfg.table_rows, D, cfg.feature_table, max_nnz=max_nnz, max_batch=B,
+                           adagrad=args.adagrad, q8=True, requant=True, device=dev, stream=stream)
+    with torch.cuda.stream(stream):
+        for t in range(cfg.num_tables):
+            v = emb.table_view(t)
+            G.fill_table(v, v.shape[0], D, emb.pitch, cfg.seed, t, row0=int(emb.row_lo[t]), stream=stream)
+        emb.quantize()
+        gshift = gen.grad_shift_for(max_nnz, D)
+        dev_in = []
+        for k, (ids, off) in enumerate(batches):
+            gd = torch.empty((B, F, D), device=dev)
+            G.fill_grad(gd, B, F, D, cfg.seed, k, gshift, sample0=rank * B, stream=stream)
+            dev_in.append((torch.from_numpy(ids).to(dev), torch.from_numpy(off).to(dev), gd))
+        out = torch.empty((B, F, D), device=dev)
+        out_q8 = torch.empty((B, F, D), device=dev)
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    stream.synchronize()
+    assert emb.sync() == 0
+
+    def step(k):
+        ids_d, off_d, gd = dev_in[k % len(dev_in)]
+        emb.forward(ids_d, off_d, B, out=out)
+        emb.backward_adagrad(gd, LR)
+        emb.forward_q8(ids_d, off_d, B, out=out_q8)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for k in range(args.warmup):
+        step(k)
+    stream.synchronize()
+    st = emb.sync()
+    assert st == 0, f"status {st} after warm-up"
+
+    # ---- timed region: device-resident inputs --------------------------------------
+    K = args.steps
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    barrier()
+    torch.cuda.synchronize(dev)
+    launches0 = emb.launches
+    emb.profile(True)
+    emb.profile_read(reset=True)
+    for k in range(K):
+        G.flush_l2(flush, stream=stream)
+        with torch.cuda.stream(stream):
+            evs[k][0].record(stream)
+        emb.profile(True)
+        step(args.warmup + k)
+        emb.profile(False)
+        with torch.cuda.stream(stream):
+            evs[k][1].record(stream)
+    torch.cuda.synchronize(dev)
+    barrier()
+    clk = clocks.result()
+    launches = emb.launches - launches0
+    phases = emb.profile_read()
+    st = emb.sync()
+    assert st == 0, f"status {st} in timed region"
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    ms = float(np.mean(step_ms))
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    S, c, U = emb.last_stats()
+
+    # ---- e2e: through the C ABI with pinned HOST buffers (copies inside the region) ----
+    e2e = None
+    if not args.no_e2e:
+        host_in = []
+        for k, (ids, off) in enumerate(batches):
+            host_in.append((torch.from_numpy(ids).pin_memory(), torch.from_numpy(off).pin_memory(),
+                            dev_in[k][2].cpu().pin_memory()))
+        out_h = torch.empty((B, F, D), dtype=torch.float32).pin_memory()
+        outq_h = torch.empty((B, F, D), dtype=torch.float32).pin_memory()
+        eev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+        barrier()
+        torch.cuda.synchronize(dev)
+        for k in range(K):
+            ids_h, off_h, g_h = host_in[k % len(host_in)]
+            G.flush_l2(flush, stream=stream)
+            with torch.cuda.stream(stream):
+                eev[k][0].record(stream)
+            emb.forward(ids_h, off_h, B, out=out_h)
+            emb.backward_adagrad(g_h, LR)
+            emb.forward_q8(ids_h, off_h, B, out=outq_h)
+            with torch.cuda.stream(stream):
+                eev[k][1].record(stream)
+        torch.cuda.synchronize(dev)
+        barrier()
+        assert emb.sync() == 0
+        e_ms = float(np.mean([a.elapsed_time(b) for a, b in eev]))
+        if world > 1:
+            t = torch.tensor([e_ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        nnz_avg = float(np.mean([len(i) for i, _ in batches]))
+        h2d = int(nnz_avg * 4 + (F * B + 1) * 4 + B * F * D * 4)
+        d2h = int(2 * B * F * D * 4)
+        e2e = {"value": world * B / (e_ms / 1e3), "unit": "samples/s", "ms_per_step": e_ms,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "path": "emb_forward/emb_backward_adagrad/emb_forward_q8 with pinned host pointers"}
+
+    # ---- full-table quantize (a9), timed alone ----------------------------------------
+    emb.profile(True)
+    emb.profile_read(reset=True)
+    for _ in range(3):
+        G.flush_l2(flush, stream=stream)
+        emb.quantize()
+    q = emb.profile_read()["quantize"]
+    emb.profile(False)
+    q_ms = q[0] / max(q[1], 1)
+    q_bytes = emb.local_rows * (4 * emb.pitch + D + 8)
+
+    # ---- roofline ----------------------------------------------------------------------
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if "hbm_gbs" in peaks else "fallback 6650 GB/s (B200_PROFILING.md)"
+    nnz_avg = float(np.mean([len(i) for i, _ in batches]))
+    per_phase = {}
+    for p, (tot, n) in phases.items():
+        if n == 0:
+            continue
+        per = tot / n
+        ab = alg_bytes(p, cfg, nnz_avg, U, B, emb.pitch, args.adagrad)
+        ent = {"ms": per, "instances": n}
+        if ab:
+            ent["alg_bytes"] = ab
+            ent["gbs"] = ab / (per / 1e3) / 1e9
+            ent["frac_of_hbm"] = ent["gbs"] / hbm_peak
+        per_phase[p] = ent
+    single = [p for p in ("fwd", "fwd_q8", "update", "segreduce") if p in per_phase]
+    dom = max(single, key=lambda p: per_phase[p]["ms"])
+    traffic = None
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        traffic = tr.get(dom, {}).get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    roof = {"bound": "hbm", "kernel": dom, "achieved": per_phase[dom]["gbs"], "peak": hbm_peak, "unit": "GB/s",
+            "frac": per_phase[dom]["gbs"] / hbm_peak, "traffic": traffic,
+            "alg_bytes_per_launch": per_phase[dom]["alg_bytes"], "peak_source": peak_src,
+            "timing": "CUDA events on the library stream around the kernel phase, mean over timed steps"}
+
+    value = world * B / (ms / 1e3)
+    fwd_ms = per_phase["fwd"]["ms"]
+    bwd_ms = sum(per_phase[p]["ms"] for p in ("sort", "rle", "segreduce", "norm", "update") if p in per_phase)
+    line = {
+        "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": K,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded Zipf ids, Irwin-Hall tables/grads)",
+        "config": {"workload": cfg.name, "tables": cfg.table_rows, "dim": D, "features": F,
+                   "global_batch": world * B, "batch_per_gpu": B, "nnz_per_step": nnz_avg, "alpha": cfg.alpha,
+                   "unique_rows": U, "adagrad": args.adagrad,
+                   "parallelism": "single" if world == 1 else f"replicas{world}",
+                   "step": "a2 fwd + a5-a8 bwd (a9 requant of touched rows fused) + a10 q8 fwd",
+                   "l2": "flushed between timed steps (256 MiB write, untimed)",
+                   "batches_rotated": len(batches)},
+        "lookups_per_s": world * nnz_avg / (fwd_ms / 1e3),
+        "q8_lookups_per_s": world * nnz_avg / (per_phase["fwd_q8"]["ms"] / 1e3) if "fwd_q8" in per_phase else None,
+        "train_samples_per_s": world * B / ((fwd_ms + bwd_ms) / 1e3),
+        "phases": per_phase,
+        "quantize_full": {"ms": q_ms, "rows": emb.local_rows, "alg_bytes": q_bytes,
+                          "gbs": q_bytes / (q_ms / 1e3) / 1e9, "frac_of_hbm": q_bytes / (q_ms / 1e3) / 1e9 / hbm_peak},
+        "roofline": roof,
+        "clocks": clk,
+        "gpu_launches": launches,
+        "e2e": e2e,
+        "clip": {"sq_norm": S, "c": float(c)},
+    }
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            line["cpu_baseline"] = cpu_baseline(cfg, batches[0][0], batches[0][1], B, args.cpu_samples,
+                                                args.adagrad)
+            line["cpu_baseline"]["cores_available"] = os.cpu_count()
+        except Exception as e:  # report, never hide
+            line["cpu_baseline"] = {"error": repr(e)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    cfg = configs.get(args.config)
+    if args.alpha is not None:
+        cfg = cfg.with_(alpha=args.alpha)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, cfg, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

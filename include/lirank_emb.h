@@ -215,6 +215,28 @@ EMB_API emb_status emb_last_stats(emb_t h, double* sq_norm, float* clip, int64_t
 /* Number of kernels this handle has launched so far (for launch accounting). */
 EMB_API int64_t emb_kernel_launches(emb_t h);
 
+/* Phase profiling with CUDA events recorded on cfg.stream around each phase of every
+ * call (the kernels of one phase run back to back, so a phase's event pair times them).
+ * emb_profile(h, 1) starts recording, (h, 0) stops.  emb_profile_read waits for the
+ * stream, adds the elapsed times of all recorded phases into ms[EMB_PH_COUNT] (and the
+ * number of recorded phase instances into count[EMB_PH_COUNT]; either may be NULL), and
+ * with reset != 0 clears the accumulators first. */
+enum {
+  EMB_PH_FWD = 0,        /* a2 fp32 pooled lookup kernel                         */
+  EMB_PH_SORT = 1,       /* a5 radix histogram + digit passes                    */
+  EMB_PH_RLE = 2,        /* a5 run-length encode                                 */
+  EMB_PH_SEGREDUCE = 3,  /* a6 chunk segment-reduce + fix-ups                    */
+  EMB_PH_NORM = 4,       /* a7 norm partial (+ rank exchange) + clip factor      */
+  EMB_PH_UPDATE = 5,     /* a8 clip + AdaGrad (+ fused re-quantize)              */
+  EMB_PH_FWD_Q8 = 6,     /* a10 q8 pooled lookup kernel                          */
+  EMB_PH_QUANTIZE = 7,   /* a9 full-table quantize                               */
+  EMB_PH_COPY = 8,       /* host<->device staging copies                         */
+  EMB_PH_EXCHANGE = 9,   /* a1/a3/a4 multi-GPU exchange                          */
+  EMB_PH_COUNT = 10
+};
+EMB_API emb_status emb_profile(emb_t h, int32_t enable);
+EMB_API emb_status emb_profile_read(emb_t h, double* ms, int64_t* count, int32_t reset);
+
 /* Release the handle (and its NCCL communicator).  Does not free caller buffers. */
 EMB_API emb_status emb_destroy(emb_t h);
 

@@ -167,8 +167,47 @@ emb_status make_plan(const emb_config* c, Plan* p) {
 
 }  // namespace
 
+// CUDA-event phase profiler (emb_profile / emb_profile_read).
+struct Prof {
+  bool on = false;
+  struct Rec { int ph; cudaEvent_t a, b; };
+  std::vector<Rec> pending;
+  std::vector<cudaEvent_t> pool;
+  double ms[EMB_PH_COUNT] = {};
+  int64_t n[EMB_PH_COUNT] = {};
+  cudaEvent_t get() {
+    if (!pool.empty()) { cudaEvent_t e = pool.back(); pool.pop_back(); return e; }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+  }
+  ~Prof() {
+    for (auto& r : pending) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+    for (auto e : pool) cudaEventDestroy(e);
+  }
+};
+
+// RAII phase marker: records a start event now and an end event at scope exit.
+struct Phase {
+  Prof* pr;
+  cudaStream_t s;
+  int ph;
+  cudaEvent_t a = nullptr;
+  Phase(Prof& p, cudaStream_t st, int phase) : pr(p.on ? &p : nullptr), s(st), ph(phase) {
+    if (pr) { a = pr->get(); cudaEventRecord(a, s); }
+  }
+  ~Phase() {
+    if (pr) {
+      cudaEvent_t b = pr->get();
+      cudaEventRecord(b, s);
+      pr->pending.push_back({ph, a, b});
+    }
+  }
+};
+
 struct emb_handle {
   Plan p;
+  Prof prof;
   cudaStream_t stream = nullptr;
   float* W = nullptr;
   float* A = nullptr;
@@ -406,6 +445,36 @@ emb_status emb_destroy(emb_t h) {
 
 int64_t emb_kernel_launches(emb_t h) { return h ? h->launches : -1; }
 
+emb_status emb_profile(emb_t h, int32_t enable) {
+  if (!h) return EMB_EINVAL;
+  h->prof.on = enable != 0;
+  return EMB_OK;
+}
+
+emb_status emb_profile_read(emb_t h, double* ms, int64_t* count, int32_t reset) {
+  if (!h) return EMB_EINVAL;
+  Prof& pr = h->prof;
+  if (reset) {
+    for (int i = 0; i < EMB_PH_COUNT; ++i) { pr.ms[i] = 0; pr.n[i] = 0; }
+  }
+  CK(cudaStreamSynchronize(h->stream));
+  for (auto& r : pr.pending) {
+    float t = 0.f;
+    if (cudaEventElapsedTime(&t, r.a, r.b) == cudaSuccess) {
+      pr.ms[r.ph] += t;
+      pr.n[r.ph] += 1;
+    }
+    pr.pool.push_back(r.a);
+    pr.pool.push_back(r.b);
+  }
+  pr.pending.clear();
+  for (int i = 0; i < EMB_PH_COUNT; ++i) {
+    if (ms) ms[i] = pr.ms[i];
+    if (count) count[i] = pr.n[i];
+  }
+  return EMB_OK;
+}
+
 emb_status emb_sync(emb_t h) {
   if (!h) return EMB_EINVAL;
   CK(cudaStreamSynchronize(h->stream));
@@ -470,7 +539,10 @@ emb_status emb_forward(emb_t h, const int32_t* ids, const int32_t* offsets, int3
   const Plan& p = h->p;
   if (p.world > 1) return exchange_forward(h, ids, offsets, batch, nnz, out, /*q8=*/false);
   Staged st;
-  s = stage_inputs(h, ids, offsets, batch, nnz, out, &st);
+  {
+    Phase ph(h->prof, h->stream, EMB_PH_COPY);
+    s = stage_inputs(h, ids, offsets, batch, nnz, out, &st);
+  }
   if (s != EMB_OK) return s;
   FwdArgs a;
   a.W = h->W;
@@ -487,14 +559,20 @@ emb_status emb_forward(emb_t h, const int32_t* ids, const int32_t* offsets, int3
   a.sentinel = (uint32_t)p.local_rows;
   a.status = h->d_status;
   a.mean = p.pooling == EMB_POOL_MEAN;
-  CK(launch_pool_fwd_f32(a, h->stream));
+  {
+    Phase ph(h->prof, h->stream, EMB_PH_FWD);
+    CK(launch_pool_fwd_f32(a, h->stream));
+  }
   h->launches += (int64_t)p.F * batch > 0;
-  if (a.mean)
-    CK(cudaMemcpyAsync(h->off_copy, st.offsets, sizeof(int) * ((int64_t)p.F * batch + 1),
-                       cudaMemcpyDeviceToDevice, h->stream));
-  if (st.host_out)
-    CK(cudaMemcpyAsync(out, st.out, sizeof(float) * (int64_t)batch * p.F * p.D,
-                       cudaMemcpyDeviceToHost, h->stream));
+  if (a.mean || st.host_out) {
+    Phase ph(h->prof, h->stream, EMB_PH_COPY);
+    if (a.mean)
+      CK(cudaMemcpyAsync(h->off_copy, st.offsets, sizeof(int) * ((int64_t)p.F * batch + 1),
+                         cudaMemcpyDeviceToDevice, h->stream));
+    if (st.host_out)
+      CK(cudaMemcpyAsync(out, st.out, sizeof(float) * (int64_t)batch * p.F * p.D,
+                         cudaMemcpyDeviceToHost, h->stream));
+  }
   h->have_fwd = true;
   h->fwd_nnz = nnz;
   h->fwd_B = batch;
@@ -510,7 +588,10 @@ emb_status emb_forward_q8(emb_t h, const int32_t* ids, const int32_t* offsets, i
   if (!(p.flags & EMB_F_Q8) || !h->have_q8) return EMB_ESTATE;
   if (p.world > 1) return exchange_forward(h, ids, offsets, batch, nnz, out, /*q8=*/true);
   Staged st;
-  s = stage_inputs(h, ids, offsets, batch, nnz, out, &st);
+  {
+    Phase ph(h->prof, h->stream, EMB_PH_COPY);
+    s = stage_inputs(h, ids, offsets, batch, nnz, out, &st);
+  }
   if (s != EMB_OK) return s;
   FwdQ8Args a;
   a.codes = h->codes;
@@ -525,11 +606,16 @@ emb_status emb_forward_q8(emb_t h, const int32_t* ids, const int32_t* offsets, i
   a.out = st.out;
   a.status = h->d_status;
   a.mean = p.pooling == EMB_POOL_MEAN;
-  CK(launch_pool_fwd_q8(a, h->stream));
+  {
+    Phase ph(h->prof, h->stream, EMB_PH_FWD_Q8);
+    CK(launch_pool_fwd_q8(a, h->stream));
+  }
   h->launches += (int64_t)p.F * batch > 0;
-  if (st.host_out)
+  if (st.host_out) {
+    Phase ph(h->prof, h->stream, EMB_PH_COPY);
     CK(cudaMemcpyAsync(out, st.out, sizeof(float) * (int64_t)batch * p.F * p.D,
                        cudaMemcpyDeviceToHost, h->stream));
+  }
   return EMB_OK;
 }
 
@@ -549,10 +635,14 @@ emb_status backward_local(emb_t h, const float* grad_dev, float lr, double extra
   if (n > 0) {
     int passes = 0;
     bool in1 = false;
-    CK(radix_sort_pairs(h->kA, h->vA, h->kB, h->vB, n, p.key_bits, h->sort, h->epoch, &passes,
-                        &in1, &h->launches, h->stream));
+    {
+      Phase ph(h->prof, h->stream, EMB_PH_SORT);
+      CK(radix_sort_pairs(h->kA, h->vA, h->kB, h->vB, n, p.key_bits, h->sort, h->epoch, &passes,
+                          &in1, &h->launches, h->stream));
+    }
     h->epoch += (uint32_t)passes;
     if (in1) { kres = h->kB; vres = h->vB; }
+    Phase ph(h->prof, h->stream, EMB_PH_RLE);
     CK(launch_rle(kres, n, (uint32_t)p.local_rows, h->unique, h->seg, h->d_U,
                   h->sort.counters + kMaxPasses, h->sort.status, h->epoch, h->stream));
     h->epoch += 1;
@@ -601,7 +691,11 @@ emb_status backward_local(emb_t h, const float* grad_dev, float lr, double extra
   a.q8_meta = (p.flags & EMB_F_REQUANT) ? h->qmeta : nullptr;
   a.qpitch = p.qpitch;
 
-  CK(launch_segreduce(a, &h->launches, h->stream));
+  {
+    Phase ph(h->prof, h->stream, EMB_PH_SEGREDUCE);
+    CK(launch_segreduce(a, &h->launches, h->stream));
+  }
+  Phase ph_norm(h->prof, h->stream, EMB_PH_NORM);
   CK(launch_norm_partial(a, h->stream));
   h->launches += 1;
   const double* parts = h->S_local;
@@ -616,6 +710,8 @@ emb_status backward_local(emb_t h, const float* grad_dev, float lr, double extra
   }
   CK(launch_norm_finalize(parts, np, a, h->stream));
   h->launches += 1;
+  ph_norm.~Phase();
+  new (&ph_norm) Phase(h->prof, h->stream, EMB_PH_UPDATE);
   CK(launch_adagrad(a, h->stream));
   h->launches += n > 0;
   if ((p.flags & EMB_F_REQUANT) && n > 0) h->have_q8 = true;
@@ -634,6 +730,7 @@ emb_status emb_backward_adagrad(emb_t h, const float* grad_out, float lr, double
   } else {
     const float* g = grad_out;
     if (!is_device_ptr(grad_out)) {
+      Phase ph(h->prof, h->stream, EMB_PH_COPY);
       CK(cudaMemcpyAsync(h->stage_dense, grad_out, sizeof(float) * (int64_t)h->fwd_B * p.F * p.D,
                          cudaMemcpyHostToDevice, h->stream));
       g = h->stage_dense;
@@ -658,8 +755,11 @@ emb_status emb_quantize_mm8(emb_t h) {
   if (!h) return EMB_EINVAL;
   const Plan& p = h->p;
   if (!(p.flags & EMB_F_Q8)) return EMB_ESTATE;
-  CK(launch_quantize(h->W, p.pitch, p.local_rows, p.D, h->codes, p.qpitch, h->qmeta, h->d_status,
-                     h->stream));
+  {
+    Phase ph(h->prof, h->stream, EMB_PH_QUANTIZE);
+    CK(launch_quantize(h->W, p.pitch, p.local_rows, p.D, h->codes, p.qpitch, h->qmeta, h->d_status,
+                       h->stream));
+  }
   h->launches += p.local_rows > 0;
   h->have_q8 = true;
   return EMB_OK;

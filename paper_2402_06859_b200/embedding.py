@@ -206,6 +206,17 @@ class ShardedEmbedding:
     def launches(self) -> int:
         return int(self.lib.emb_kernel_launches(self.h))
 
+    def profile(self, enable: bool = True):
+        L.check(self.lib.emb_profile(self.h, 1 if enable else 0), "emb_profile")
+
+    def profile_read(self, reset: bool = False):
+        """{phase: (total ms, instances)} accumulated from the library's CUDA events."""
+        ms = np.zeros(len(L.PHASES), dtype=np.float64)
+        n = np.zeros(len(L.PHASES), dtype=np.int64)
+        L.check(self.lib.emb_profile_read(self.h, ms.ctypes.data_as(C.c_void_p), n.ctypes.data_as(C.c_void_p),
+                                          1 if reset else 0), "emb_profile_read")
+        return {p: (float(ms[i]), int(n[i])) for i, p in enumerate(L.PHASES)}
+
     def close(self):
         if getattr(self, "h", None) and self.h.value:
             self.lib.emb_destroy(self.h)
