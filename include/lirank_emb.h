@@ -113,20 +113,22 @@ typedef struct {
 typedef struct {
   int64_t weights_bytes;    /* fp32 [local_rows][row_pitch]                                    */
   int64_t accum_bytes;      /* fp32 [local_rows] (row-wise) or [local_rows][row_pitch]         */
-  int64_t q8_codes_bytes;   /* int8 [local_rows][q8_pitch]           (0 without EMB_F_Q8)      */
-  int64_t q8_meta_bytes;    /* fp32 {middle, scale} [local_rows][2]  (0 without EMB_F_Q8)      */
+  int64_t q8_codes_bytes;   /* q8 rows [local_rows][q8_pitch] (0 without EMB_F_Q8), each row =
+                               [D int8 codes][pad to 8][fp32 middle][fp32 scale][pad to 16] so a
+                               row is one contiguous request (D=64: 80 B)                       */
+  int64_t q8_meta_bytes;    /* 0 (metadata lives in the q8 rows; kept for ABI stability)       */
   int64_t workspace_bytes;  /* library scratch (staging, sort, segment partials, scalars)      */
   int64_t local_rows;       /* rows stored on this rank (sum over its local tables)            */
   int32_t row_pitch;        /* floats per stored fp32 row: round_up(D, 4) (16-B aligned rows)  */
-  int32_t q8_pitch;         /* bytes per stored code row: round_up(D, 16)                      */
+  int32_t q8_pitch;         /* bytes per q8 row: round_up(round_up(D, 8) + 8, 16)              */
 } emb_sizes;
 
 typedef struct {
   void* weights;    /* device; caller initialises it (layout: emb_local_layout) or uses
                        emb_write_rows                                                      */
   void* accum;      /* device; emb_create fills it with init_accumulator                   */
-  void* q8_codes;   /* device or NULL without EMB_F_Q8                                     */
-  void* q8_meta;    /* device or NULL without EMB_F_Q8                                     */
+  void* q8_codes;   /* device (q8 rows) or NULL without EMB_F_Q8                           */
+  void* q8_meta;    /* unused (may be NULL)                                                */
   void* workspace;  /* device                                                              */
 } emb_buffers;
 

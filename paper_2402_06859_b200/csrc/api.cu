@@ -84,7 +84,7 @@ emb_status make_plan(const emb_config* c, Plan* p) {
   p->D = c->dim;
   p->F = c->num_features;
   p->pitch = (int)round_up(c->dim, 4);
-  p->qpitch = (int)round_up(c->dim, 16);
+  p->qpitch = (int)round_up(round_up(c->dim, 8) + 8, 16);  // [codes][pad][middle,scale][pad]
   p->pooling = c->pooling;
   p->mode = c->adagrad_mode;
   p->sharding = c->world_size > 1 ? c->sharding : EMB_SHARD_NONE;
@@ -212,14 +212,15 @@ struct emb_handle {
   float* W = nullptr;
   float* A = nullptr;
   uint8_t* codes = nullptr;
-  float2* qmeta = nullptr;
+  int q8_meta_off = 0;  // byte offset of {middle, scale} inside a q8 row
   // workspace
   FeatMeta* d_meta = nullptr;
   int* stage_ids = nullptr;
   int* stage_off = nullptr;
   float* stage_dense = nullptr;
   int* off_copy = nullptr;
-  uint32_t *kA = nullptr, *vA = nullptr, *kB = nullptr, *vB = nullptr;
+  uint2 *kvA = nullptr, *kvB = nullptr;  // {row key, bag} per occurrence (sort ping-pong)
+  uint32_t* chunk_u0 = nullptr;
   SortWs sort{};
   uint32_t* unique = nullptr;
   uint32_t* seg = nullptr;
@@ -243,8 +244,7 @@ struct emb_handle {
   int64_t fwd_nnz = 0;       // occurrences recorded (local pooling input) by the last forward
   int fwd_B = 0;             // pooling batch of the last forward (B_global for table-wise)
   int fwd_B_local = 0;
-  const uint32_t* sorted_keys = nullptr;
-  const uint32_t* sorted_vals = nullptr;
+  const uint2* sorted_kv = nullptr;
   uint32_t epoch = 1;
   int64_t launches = 0;
 };
@@ -264,12 +264,11 @@ void carve(const Plan& p, Carver& cv, emb_handle* h) {
   auto* stage_off = cv.take<int>(F * Bmax + 1);
   auto* stage_dense = cv.take<float>(dense_cap);
   auto* off_copy = cv.take<int>(bags_cap + 1);
-  auto* kA = cv.take<uint32_t>(nnz_cap);
-  auto* vA = cv.take<uint32_t>(nnz_cap);
-  auto* kB = cv.take<uint32_t>(nnz_cap);
-  auto* vB = cv.take<uint32_t>(nnz_cap);
-  auto* hist = cv.take<uint32_t>(kMaxPasses * kRadixBins + kMaxPasses + 2);  // hist + counters
-  auto* lb = cv.take<unsigned long long>(tiles * kRadixBins);
+  auto* kvA = cv.take<uint2>(nnz_cap);
+  auto* kvB = cv.take<uint2>(nnz_cap);
+  auto* hist = cv.take<uint32_t>(kHistWords + kMaxPasses + 2);  // hist + counters
+  auto* lb = cv.take<unsigned long long>(tiles * kRadixBinsMax);
+  auto* cu0 = cv.take<uint32_t>(chunks);
   auto* unique = cv.take<uint32_t>(max_unique);
   auto* seg = cv.take<uint32_t>(max_unique + 1);
   auto* dU = cv.take<uint32_t>(4);
@@ -293,9 +292,9 @@ void carve(const Plan& p, Carver& cv, emb_handle* h) {
     h->stage_off = stage_off;
     h->stage_dense = stage_dense;
     h->off_copy = off_copy;
-    h->kA = kA; h->vA = vA; h->kB = kB; h->vB = vB;
+    h->kvA = kvA; h->kvB = kvB; h->chunk_u0 = cu0;
     h->sort.hist = hist;
-    h->sort.counters = hist + kMaxPasses * kRadixBins;
+    h->sort.counters = hist + kHistWords;
     h->sort.status = lb;
     h->sort.max_tiles = tiles;
     h->unique = unique;
@@ -372,7 +371,7 @@ emb_status emb_plan(const emb_config* cfg, emb_sizes* out) {
   out->accum_bytes = std::max<int64_t>(
       p.mode == EMB_ADAGRAD_ROWWISE ? p.local_rows * 4 : p.local_rows * p.pitch * 4, 4);
   out->q8_codes_bytes = (p.flags & EMB_F_Q8) ? std::max<int64_t>(p.local_rows * p.qpitch, 16) : 0;
-  out->q8_meta_bytes = (p.flags & EMB_F_Q8) ? std::max<int64_t>(p.local_rows * 8, 8) : 0;
+  out->q8_meta_bytes = 0;  // {middle, scale} live inside the q8 rows
   out->workspace_bytes = round_up(cv.off, kAlign);
   out->local_rows = p.local_rows;
   out->row_pitch = p.pitch;
@@ -402,7 +401,7 @@ emb_status emb_create(const emb_config* cfg, const emb_buffers* buf, emb_t* out)
   if (s != EMB_OK) { delete h; return s; }
   const Plan& p = h->p;
   if (!buf->weights || !buf->accum || !buf->workspace) { delete h; return EMB_EINVAL; }
-  if ((p.flags & EMB_F_Q8) && (!buf->q8_codes || !buf->q8_meta)) { delete h; return EMB_EINVAL; }
+  if ((p.flags & EMB_F_Q8) && !buf->q8_codes) { delete h; return EMB_EINVAL; }
   const void* ptrs[5] = {buf->weights, buf->accum, buf->workspace, buf->q8_codes, buf->q8_meta};
   for (const void* q : ptrs)
     if (q && !aligned(q, kAlign)) { delete h; return EMB_EINVAL; }
@@ -410,7 +409,7 @@ emb_status emb_create(const emb_config* cfg, const emb_buffers* buf, emb_t* out)
   h->W = (float*)buf->weights;
   h->A = (float*)buf->accum;
   h->codes = (uint8_t*)buf->q8_codes;
-  h->qmeta = (float2*)buf->q8_meta;
+  h->q8_meta_off = (int)round_up(p.D, 8);
   Carver cv(buf->workspace);
   carve(p, cv, h);
   // device init: feature metadata, accumulators = A0, status = 0, look-back words = 0
@@ -424,7 +423,7 @@ emb_status emb_create(const emb_config* cfg, const emb_buffers* buf, emb_t* out)
   }
   if (e == cudaSuccess) e = cudaMemsetAsync(h->d_status, 0, sizeof(uint32_t), h->stream);
   if (e == cudaSuccess)
-    e = cudaMemsetAsync(h->sort.status, 0, sizeof(unsigned long long) * h->sort.max_tiles * kRadixBins, h->stream);
+    e = cudaMemsetAsync(h->sort.status, 0, sizeof(unsigned long long) * h->sort.max_tiles * kRadixBinsMax, h->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);  // `m` goes out of scope
   if (e != cudaSuccess) { delete h; return EMB_ECUDA; }
   if (p.world > 1) {
@@ -545,6 +544,7 @@ emb_status emb_forward(emb_t h, const int32_t* ids, const int32_t* offsets, int3
   }
   if (s != EMB_OK) return s;
   FwdArgs a;
+  memset(&a, 0, sizeof(a));
   a.W = h->W;
   a.pitch = p.pitch;
   a.ids = st.ids;
@@ -554,8 +554,7 @@ emb_status emb_forward(emb_t h, const int32_t* ids, const int32_t* offsets, int3
   a.D = p.D;
   a.meta = h->d_meta;
   a.out = st.out;
-  a.keys_out = h->kA;
-  a.vals_out = h->vA;
+  a.kv_out = h->kvA;
   a.sentinel = (uint32_t)p.local_rows;
   a.status = h->d_status;
   a.mean = p.pooling == EMB_POOL_MEAN;
@@ -594,9 +593,10 @@ emb_status emb_forward_q8(emb_t h, const int32_t* ids, const int32_t* offsets, i
   }
   if (s != EMB_OK) return s;
   FwdQ8Args a;
+  memset(&a, 0, sizeof(a));
   a.codes = h->codes;
   a.qpitch = p.qpitch;
-  a.qmeta = h->qmeta;
+  a.meta_off = h->q8_meta_off;
   a.ids = st.ids;
   a.offsets = st.offsets;
   a.B = batch;
@@ -630,20 +630,19 @@ emb_status backward_local(emb_t h, const float* grad_dev, float lr, double extra
                           const double* S_parts_dev, int nparts, bool do_allgather) {
   const Plan& p = h->p;
   const int64_t n = h->fwd_nnz;
-  uint32_t* kres = h->kA;
-  uint32_t* vres = h->vA;
+  const uint2* kres = h->kvA;
   if (n > 0) {
     int passes = 0;
     bool in1 = false;
     {
       Phase ph(h->prof, h->stream, EMB_PH_SORT);
-      CK(radix_sort_pairs(h->kA, h->vA, h->kB, h->vB, n, p.key_bits, h->sort, h->epoch, &passes,
+      CK(radix_sort_pairs(h->kvA, h->kvB, n, p.key_bits, h->sort, h->epoch, &passes,
                           &in1, &h->launches, h->stream));
     }
     h->epoch += (uint32_t)passes;
-    if (in1) { kres = h->kB; vres = h->vB; }
+    if (in1) kres = h->kvB;
     Phase ph(h->prof, h->stream, EMB_PH_RLE);
-    CK(launch_rle(kres, n, (uint32_t)p.local_rows, h->unique, h->seg, h->d_U,
+    CK(launch_rle(kres, n, (uint32_t)p.local_rows, h->unique, h->seg, h->d_U, h->chunk_u0,
                   h->sort.counters + kMaxPasses, h->sort.status, h->epoch, h->stream));
     h->epoch += 1;
     h->launches += 1;
@@ -651,15 +650,15 @@ emb_status backward_local(emb_t h, const float* grad_dev, float lr, double extra
     CK(cudaMemsetAsync(h->d_U, 0, sizeof(uint32_t), h->stream));
     CK(cudaMemsetAsync(h->seg, 0, sizeof(uint32_t), h->stream));
   }
-  h->sorted_keys = kres;
-  h->sorted_vals = vres;
+  h->sorted_kv = kres;
 
   BwdArgs a;
   memset(&a, 0, sizeof(a));
   a.unique = h->unique;
   a.seg = h->seg;
   a.U = h->d_U;
-  a.vals = vres;
+  a.kv = kres;
+  a.chunk_u0 = h->chunk_u0;
   a.nnz = n;
   a.grad = grad_dev;
   a.offsets = h->off_copy;
@@ -688,7 +687,7 @@ emb_status backward_local(emb_t h, const float* grad_dev, float lr, double extra
   a.lr = lr;
   a.eps = p.eps;
   a.q8_codes = (p.flags & EMB_F_REQUANT) ? h->codes : nullptr;
-  a.q8_meta = (p.flags & EMB_F_REQUANT) ? h->qmeta : nullptr;
+  a.q8_meta_off = h->q8_meta_off;
   a.qpitch = p.qpitch;
 
   {
@@ -757,7 +756,7 @@ emb_status emb_quantize_mm8(emb_t h) {
   if (!(p.flags & EMB_F_Q8)) return EMB_ESTATE;
   {
     Phase ph(h->prof, h->stream, EMB_PH_QUANTIZE);
-    CK(launch_quantize(h->W, p.pitch, p.local_rows, p.D, h->codes, p.qpitch, h->qmeta, h->d_status,
+    CK(launch_quantize(h->W, p.pitch, p.local_rows, p.D, h->codes, p.qpitch, h->q8_meta_off, h->d_status,
                        h->stream));
   }
   h->launches += p.local_rows > 0;
@@ -871,7 +870,7 @@ emb_status emb_read_q8(emb_t h, int32_t table, const int64_t* rows, int64_t n, i
   }
   if (middle || scale) {
     std::vector<float> mt(2 * n);
-    s = move_rows(h, h->qmeta, 8, r, 8, mt.data(), 0);
+    s = move_rows(h, h->codes + h->q8_meta_off, p.qpitch, r, 8, mt.data(), 0);
     if (s != EMB_OK) return s;
     for (int64_t i = 0; i < n; ++i) {
       if (middle) middle[i] = mt[2 * i];
@@ -885,7 +884,7 @@ emb_status emb_last_dedup(emb_t h, int32_t* unique, int32_t* seg_offsets, int64_
                           int32_t* sorted_bags, int64_t cap_occ, int64_t* n_unique,
                           int64_t* n_valid) {
   if (!h) return EMB_EINVAL;
-  if (!h->sorted_keys) return EMB_ESTATE;
+  if (!h->sorted_kv) return EMB_ESTATE;
   CK(cudaStreamSynchronize(h->stream));
   uint32_t U = 0, nv = 0;
   CK(cudaMemcpy(&U, h->d_U, 4, cudaMemcpyDeviceToHost));
@@ -896,7 +895,16 @@ emb_status emb_last_dedup(emb_t h, int32_t* unique, int32_t* seg_offsets, int64_
   if (sorted_bags && cap_occ < (int64_t)nv) return EMB_ENOMEM;
   if (unique && U) CK(cudaMemcpy(unique, h->unique, 4ull * U, cudaMemcpyDeviceToHost));
   if (seg_offsets) CK(cudaMemcpy(seg_offsets, h->seg, 4ull * (U + 1), cudaMemcpyDeviceToHost));
-  if (sorted_bags && nv) CK(cudaMemcpy(sorted_bags, h->sorted_vals, 4ull * nv, cudaMemcpyDeviceToHost));
+  if (sorted_bags && nv) {
+    std::vector<uint2> tmp(nv);
+    CK(cudaMemcpy(tmp.data(), h->sorted_kv, 8ull * nv, cudaMemcpyDeviceToHost));
+    // the pairs carry the grad row (b*F + f); report the bag index f*B + b
+    const uint32_t F = (uint32_t)h->p.F, B = (uint32_t)h->fwd_B;
+    for (uint32_t i = 0; i < nv; ++i) {
+      const uint32_t r = tmp[i].y;
+      sorted_bags[i] = (int32_t)(h->p.world > 1 ? r : (r % F) * B + r / F);
+    }
+  }
   return EMB_OK;
 }
 

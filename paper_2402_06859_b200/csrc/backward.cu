@@ -25,6 +25,9 @@
 // * the update is one persistent grid-stride kernel over the U unique rows (U is read
 //   on the device, no host sync): read G, scale by c, read-modify-write w and A, and
 //   optionally re-quantize the new row into the q8 store while it is in registers.
+// * warp discipline: every shuffle uses the full mask with width LPB and is reached by
+//   all 32 lanes (loops that contain shuffles have warp-uniform trip counts; inactive
+//   groups are predicated, never returned), so no collective emulation code is emitted.
 #include <cfloat>
 
 #include "common.cuh"
@@ -35,13 +38,13 @@ namespace lirank {
 namespace {
 
 constexpr int kFixLong = 8;           // spans of more chunks than this use a whole CTA
-constexpr int kFixThreads = 512;
+constexpr int kFixThreads = 1024;
+constexpr unsigned kFull = 0xffffffffu;
 
 template <int LPB>
 __device__ __forceinline__ double group_sum(double x) {
-  const unsigned m = group_mask<LPB>();
 #pragma unroll
-  for (int o = LPB / 2; o > 0; o >>= 1) x += __shfl_xor_sync(m, x, o, LPB);
+  for (int o = LPB / 2; o > 0; o >>= 1) x += __shfl_xor_sync(kFull, x, o, LPB);
   return x;
 }
 
@@ -110,65 +113,60 @@ __device__ __forceinline__ void write_partial(double* P, int pitch, int64_t c, i
 
 }  // namespace
 
+// One lane group per chunk of kChunk sorted occurrences.  kv[k] = {row key, grad row}.
 template <int LPB, int VPL, bool MEAN>
 __global__ void __launch_bounds__(256)
 k_segreduce(const uint32_t* __restrict__ seg, const uint32_t* __restrict__ Up,
-            const uint32_t* __restrict__ vals, const float* __restrict__ grad,
-            const int* __restrict__ offsets, int B, int F, int D, int pitch, int64_t chunks,
-            float* __restrict__ G, double* __restrict__ part_first,
+            const uint2* __restrict__ kv, const uint32_t* __restrict__ chunk_u0,
+            const float* __restrict__ grad, const int* __restrict__ offsets, int B, int F, int D,
+            int pitch, int64_t chunks, float* __restrict__ G, double* __restrict__ part_first,
             double* __restrict__ part_last, double* __restrict__ norm_main,
             double* __restrict__ norm_fix, uint32_t* __restrict__ owner_list,
             uint32_t* owner_count) {
-  constexpr int UNR = (VPL == 1) ? 4 : (VPL == 2 ? 2 : 1);
+  constexpr int UNR = (VPL == 1) ? 8 : (VPL == 2 ? 4 : 2);
   const int lane = threadIdx.x & (LPB - 1);
-  const unsigned gmask = group_mask<LPB>();
   const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LPB;
-  if (c >= chunks) return;
   const uint32_t U = *Up;
   const int64_t n_valid = seg[U];
   const int64_t k0 = c * kChunk;
-  if (k0 >= n_valid) {
-    if (lane == 0) { norm_main[c] = 0.0; norm_fix[c] = 0.0; }
-    return;
-  }
-  const int64_t k1 = min(k0 + (int64_t)kChunk, n_valid);
-  // u0 = last segment with seg[u] <= k0
-  uint32_t lo = 0, hi = U - 1;
-  while (lo < hi) {
-    const uint32_t mid = (lo + hi + 1) >> 1;
-    if ((int64_t)__ldg(seg + mid) <= k0) lo = mid; else hi = mid - 1;
-  }
-  uint32_t u = lo;
-  int64_t s_start = __ldg(seg + u), s_end = __ldg(seg + u + 1);
+  const bool live = c < chunks && k0 < n_valid;
+  const int64_t k1 = live ? min(k0 + (int64_t)kChunk, n_valid) : k0;
+  uint32_t u = live ? __ldg(chunk_u0 + c) : 0u;  // segment containing occurrence k0 (RLE)
+  int64_t s_start = live ? (int64_t)__ldg(seg + u) : 0, s_end = live ? (int64_t)__ldg(seg + u + 1) : 0;
 
   double acc[VPL][4];
   zero(acc);
   double nrm = 0.0;
-
-  for (int64_t kb = k0; kb < k1; kb += LPB) {
-    const int64_t kl = kb + lane;
-    uint32_t bag = 0;
-    double inv = 1.0;
-    if (kl < k1) {
-      bag = __ldg(vals + kl);
-      if (MEAN) inv = 1.0 / (double)(__ldg(offsets + bag + 1) - __ldg(offsets + bag));
+  // Warp-uniform loop (kChunk/LPB batches for every group): each batch loads LPB {key,
+  // grad row} pairs (one per lane) and broadcasts them with full-mask shuffles; slots
+  // past k1 (last chunk, dead groups) are predicated.
+  for (int it = 0; it < kChunk / LPB; ++it) {
+    const int64_t kb = k0 + (int64_t)it * LPB;
+    uint32_t grow_l = 0;
+    double inv_l = 1.0;
+    if (kb + lane < k1) {
+      grow_l = __ldg(&kv[kb + lane].y);
+      if (MEAN) {
+        const uint32_t bb = grow_l / (uint32_t)F, ff = grow_l - bb * (uint32_t)F;
+        const uint32_t bag = ff * (uint32_t)B + bb;
+        inv_l = 1.0 / (double)(__ldg(offsets + bag + 1) - __ldg(offsets + bag));
+      }
     }
-    const int cnt = (int)min((int64_t)LPB, k1 - kb);
-    for (int jj = 0; jj < cnt; jj += UNR) {
+#pragma unroll 1
+    for (int jj = 0; jj < LPB; jj += UNR) {  // not unrolled: UNR rows in flight, not LPB
       float4 r[UNR][VPL];
       double iv[UNR];
+      bool ok[UNR];
 #pragma unroll
       for (int q = 0; q < UNR; ++q) {
-        const uint32_t bq = __shfl_sync(gmask, bag, (jj + q) & (LPB - 1), LPB);
-        iv[q] = MEAN ? __shfl_sync(gmask, inv, (jj + q) & (LPB - 1), LPB) : 1.0;
-        if (jj + q < cnt) {
-          const uint32_t f = bq / (uint32_t)B, b = bq - f * (uint32_t)B;
-          load_grad_row<VPL>(grad, ((size_t)b * F + f) * D, D, lane, LPB, r[q]);
-        }
+        const uint32_t gq = __shfl_sync(kFull, grow_l, (jj + q) & (LPB - 1), LPB);
+        iv[q] = MEAN ? __shfl_sync(kFull, inv_l, (jj + q) & (LPB - 1), LPB) : 1.0;
+        ok[q] = (jj + q < LPB) && (kb + jj + q < k1);
+        if (ok[q]) load_grad_row<VPL>(grad, (size_t)gq * D, D, lane, LPB, r[q]);
       }
 #pragma unroll
       for (int q = 0; q < UNR; ++q) {
-        if (jj + q < cnt) {
+        if (ok[q]) {
           const int64_t occ = kb + jj + q;
           if (occ == s_end) {  // segment u finished inside this chunk
             if (s_start < k0) write_partial<VPL>(part_first, pitch, c, lane, LPB, acc);
@@ -198,16 +196,18 @@ k_segreduce(const uint32_t* __restrict__ seg, const uint32_t* __restrict__ Up,
   }
   // the segment containing occurrence k1-1
   bool owner = false;
-  if (s_start < k0) {
-    write_partial<VPL>(part_first, pitch, c, lane, LPB, acc);  // continues or ends here
-  } else if (s_end <= k1) {
-    nrm += write_G<VPL>(G, pitch, u, lane, LPB, acc);
-  } else {
-    write_partial<VPL>(part_last, pitch, c, lane, LPB, acc);  // starts here, spills over
-    owner = true;
+  if (live) {
+    if (s_start < k0) {
+      write_partial<VPL>(part_first, pitch, c, lane, LPB, acc);  // continues or ends here
+    } else if (s_end <= k1) {
+      nrm += write_G<VPL>(G, pitch, u, lane, LPB, acc);
+    } else {
+      write_partial<VPL>(part_last, pitch, c, lane, LPB, acc);  // starts here, spills over
+      owner = true;
+    }
   }
-  nrm = group_sum<LPB>(nrm);
-  if (lane == 0) {
+  nrm = group_sum<LPB>(nrm);  // all lanes converge here
+  if (lane == 0 && c < chunks) {
     norm_main[c] = nrm;
     norm_fix[c] = 0.0;
     if (owner) {
@@ -220,7 +220,7 @@ k_segreduce(const uint32_t* __restrict__ seg, const uint32_t* __restrict__ Up,
 // Fix-up of segments spanning chunks.  Entry e = chunk c_s where segment u starts and
 // spills over; its sum = part_last[c_s] + sum_{c = c_s+1 .. c_e} part_first[c].
 // One lane group per entry for short spans; entries spanning > kFixLong chunks are left
-// to k_fixup_long.
+// to k_fixup_long.  The entry loop is warp-uniform (see the file header).
 template <int LPB, int VPL>
 __global__ void __launch_bounds__(256)
 k_fixup_short(const uint32_t* __restrict__ seg, const uint32_t* __restrict__ Up,
@@ -228,62 +228,69 @@ k_fixup_short(const uint32_t* __restrict__ seg, const uint32_t* __restrict__ Up,
               const double* __restrict__ part_last, const uint32_t* __restrict__ owner_list,
               const uint32_t* __restrict__ owner_count, float* __restrict__ G,
               double* __restrict__ norm_fix, uint32_t* long_list, uint32_t* long_count) {
+  constexpr int GPW = 32 / LPB;  // groups per warp
   const int lane = threadIdx.x & (LPB - 1);
-  const int64_t gstride = ((int64_t)gridDim.x * blockDim.x) / LPB;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;  // global warp
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) / 32;
+  const int gin = (threadIdx.x & 31) / LPB;
   const uint32_t n_entries = *owner_count;
   const uint32_t U = *Up;
   const int nvec = pitch >> 2;
-  for (int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LPB; e < n_entries;
-       e += gstride) {
-    const uint32_t cs = owner_list[e];
-    const int64_t k0 = (int64_t)cs * kChunk;
-    // segment that starts in chunk cs and spills over = the last segment with seg <= k0+kChunk-1
-    uint32_t lo = 0, hi = U - 1;
-    const int64_t kl = k0 + kChunk - 1;
-    while (lo < hi) {
-      const uint32_t mid = (lo + hi + 1) >> 1;
-      if ((int64_t)__ldg(seg + mid) <= kl) lo = mid; else hi = mid - 1;
-    }
-    const uint32_t u = lo;
-    const int64_t s_end = __ldg(seg + u + 1);
-    const int64_t ce = (s_end - 1) / kChunk;
-    if (ce - cs > kFixLong) {
-      if (lane == 0) {
-        const uint32_t slot = atomicAdd(long_count, 1u);
-        long_list[2 * slot] = cs;
-        long_list[2 * slot + 1] = u;
+  for (int64_t eb = gw * GPW; eb < n_entries; eb += nwarps * GPW) {  // uniform per warp
+    const int64_t e = eb + gin;
+    bool live = e < n_entries;
+    uint32_t cs = 0, u = 0;
+    int64_t ce = 0;
+    if (live) {
+      cs = owner_list[e];
+      const int64_t kl = (int64_t)cs * kChunk + kChunk - 1;  // last occurrence of chunk cs
+      uint32_t lo = 0, hi = U - 1;
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi + 1) >> 1;
+        if ((int64_t)__ldg(seg + mid) <= kl) lo = mid; else hi = mid - 1;
       }
-      continue;
+      u = lo;
+      ce = ((int64_t)__ldg(seg + u + 1) - 1) / kChunk;
+      if (ce - cs > kFixLong) {
+        if (lane == 0) {
+          const uint32_t slot = atomicAdd(long_count, 1u);
+          long_list[2 * slot] = cs;
+          long_list[2 * slot + 1] = u;
+        }
+        live = false;
+      }
     }
     double nrm = 0.0;
+    if (live) {
 #pragma unroll
-    for (int v = 0; v < VPL; ++v) {
-      const int vi = lane + v * LPB;
-      if (vi < nvec) {
-        const double* p = part_last + (size_t)cs * pitch + 4 * vi;
-        double a0 = p[0], a1 = p[1], a2 = p[2], a3 = p[3];
-        for (int64_t cc = cs + 1; cc <= ce; ++cc) {
-          const double* q = part_first + (size_t)cc * pitch + 4 * vi;
-          a0 += q[0]; a1 += q[1]; a2 += q[2]; a3 += q[3];
+      for (int v = 0; v < VPL; ++v) {
+        const int vi = lane + v * LPB;
+        if (vi < nvec) {
+          const double* p = part_last + (size_t)cs * pitch + 4 * vi;
+          double a0 = p[0], a1 = p[1], a2 = p[2], a3 = p[3];
+          for (int64_t cc = cs + 1; cc <= ce; ++cc) {
+            const double* q = part_first + (size_t)cc * pitch + 4 * vi;
+            a0 += q[0]; a1 += q[1]; a2 += q[2]; a3 += q[3];
+          }
+          const float4 g = make_float4((float)a0, (float)a1, (float)a2, (float)a3);
+          st_f4(G + (size_t)u * pitch + 4 * vi, g);
+          nrm += (double)g.x * g.x + (double)g.y * g.y + (double)g.z * g.z + (double)g.w * g.w;
         }
-        const float4 g = make_float4((float)a0, (float)a1, (float)a2, (float)a3);
-        st_f4(G + (size_t)u * pitch + 4 * vi, g);
-        nrm += (double)g.x * g.x + (double)g.y * g.y + (double)g.z * g.z + (double)g.w * g.w;
       }
     }
     nrm = group_sum<LPB>(nrm);
-    if (lane == 0) norm_fix[cs] = nrm;
+    if (lane == 0 && live) norm_fix[cs] = nrm;
   }
 }
 
-// Long spans: one CTA per entry.  Thread t owns element (t % nelem) of the row for chunk
-// sub-range (t / nelem); sub-ranges are contiguous and combined in order.
+// Long spans: one CTA per entry.  Thread t owns element (t % pitch) of the row for chunk
+// sub-range (t / pitch); sub-ranges are contiguous and combined in order.
 __global__ void __launch_bounds__(kFixThreads)
 k_fixup_long(const uint32_t* __restrict__ seg, int pitch, const double* __restrict__ part_first,
              const double* __restrict__ part_last, const uint32_t* __restrict__ long_list,
              const uint32_t* __restrict__ long_count, float* __restrict__ G,
              double* __restrict__ norm_fix) {
-  extern __shared__ double sm[];  // [nsplit][pitch]
+  extern __shared__ double sm[];  // [max(nsplit * pitch, kFixThreads)]
   const uint32_t n_entries = *long_count;
   const int nsplit = max(1, kFixThreads / pitch);
   for (uint32_t e = blockIdx.x; e < n_entries; e += gridDim.x) {
@@ -297,12 +304,12 @@ k_fixup_long(const uint32_t* __restrict__ seg, int pitch, const double* __restri
       const int64_t b = cs + 1 + (nch * (sp + 1)) / nsplit;
       double s = 0.0;
       int64_t cc = a;
-      for (; cc + 4 <= b; cc += 4) {
-        const double x0 = part_first[(size_t)cc * pitch + el];
-        const double x1 = part_first[(size_t)(cc + 1) * pitch + el];
-        const double x2 = part_first[(size_t)(cc + 2) * pitch + el];
-        const double x3 = part_first[(size_t)(cc + 3) * pitch + el];
-        s += x0; s += x1; s += x2; s += x3;
+      for (; cc + 8 <= b; cc += 8) {  // 8 loads in flight, adds in chunk order
+        double x[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) x[q] = __ldg(part_first + (size_t)(cc + q) * pitch + el);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) s += x[q];
       }
       for (; cc < b; ++cc) s += part_first[(size_t)cc * pitch + el];
       sm[sp * pitch + el] = s;
@@ -366,14 +373,14 @@ __global__ void k_norm_finalize(const double* parts, int nparts, double extra, f
 }
 
 // ---------------------------------------------------------------------------
-// middle-max quantization of one row held by a lane group (used by a9 and REQUANT)
+// middle-max quantization of one row held by a lane group (used by a9 and REQUANT).
+// Must be called by all 32 lanes of the warp; `live` predicates this group's stores.
 // ---------------------------------------------------------------------------
 template <int LPB, int VPL>
-__device__ __forceinline__ void quantize_group_row(const float4 (&x)[VPL], int D, int lane,
+__device__ __forceinline__ void quantize_group_row(const float4 (&x)[VPL], int D, int lane, bool live,
                                                    uint8_t* __restrict__ code_row,
                                                    float2* __restrict__ meta_row,
                                                    uint32_t* status) {
-  const unsigned gm = group_mask<LPB>();
   float mn = FLT_MAX, mx = -FLT_MAX;
   bool finite = true;
 #pragma unroll
@@ -390,10 +397,11 @@ __device__ __forceinline__ void quantize_group_row(const float4 (&x)[VPL], int D
   }
 #pragma unroll
   for (int o = LPB / 2; o > 0; o >>= 1) {
-    mn = fminf(mn, __shfl_xor_sync(gm, mn, o, LPB));
-    mx = fmaxf(mx, __shfl_xor_sync(gm, mx, o, LPB));
-    finite = __shfl_xor_sync(gm, (int)finite, o, LPB) && finite;
+    mn = fminf(mn, __shfl_xor_sync(kFull, mn, o, LPB));
+    mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, o, LPB));
+    finite = __shfl_xor_sync(kFull, (int)finite, o, LPB) && finite;
   }
+  if (!live) return;
   float middle, scale;
   bool zero_codes;
   if (!finite) {
@@ -408,6 +416,15 @@ __device__ __forceinline__ void quantize_group_row(const float4 (&x)[VPL], int D
     scale = __fdiv_rn(__fsub_rn(mx, mn), 255.0f);
     zero_codes = scale == 0.0f;
   }
+  // X^int = round((X - X^middle) / X^scale), half away from zero, saturated to [-128,127].
+  // The IEEE quotient is only needed near a rounding boundary: q~ = (X - X^middle) *
+  // RN(1/X^scale) is within 2^-23 relative (< 4e-5 absolute for |q| < 200) of the
+  // correctly rounded quotient q, so when |q~ - rint(q~)| < 0.4999 both round to the same
+  // integer (no tie is possible there, so half-even rint == half-away); and clamping q~ to
+  // [-128, 127] before rounding equals rounding then saturating.  Near-tie elements
+  // (|q~ - rint(q~)| >= 0.4999, a ~2e-4 fraction) take the exact __fdiv_rn + roundf.
+  const bool fast = scale >= 1.17549435e-38f && scale <= 4.2535296e37f;  // [2^-126, 2^125]
+  const float rcp = fast ? __frcp_rn(scale) : 0.0f;
 #pragma unroll
   for (int v = 0; v < VPL; ++v) {
     const int wi = lane + v * LPB;
@@ -419,10 +436,16 @@ __device__ __forceinline__ void quantize_group_row(const float4 (&x)[VPL], int D
       for (int i = 0; i < 4; ++i) {
         int code = 0;
         if (!zero_codes && d + i < D) {
-          // X^int = round((X - X^middle) / X^scale): half away from zero, saturated
-          float r = roundf(__fdiv_rn(__fsub_rn(e[i], middle), scale));
-          r = fminf(fmaxf(r, -128.0f), 127.0f);
-          code = (int)r;
+          const float dlt = __fsub_rn(e[i], middle);
+          const float qa = fminf(fmaxf(__fmul_rn(dlt, rcp), -128.0f), 127.0f);
+          const float big = __fadd_rn(qa, 12582912.0f);  // 1.5*2^23: rint into the mantissa
+          const float rq = __fsub_rn(big, 12582912.0f);
+          code = __float_as_int(big) - 0x4B400000;
+          if (!fast || fabsf(__fsub_rn(qa, rq)) >= 0.4999f) {
+            float r = roundf(__fdiv_rn(dlt, scale));
+            r = fminf(fmaxf(r, -128.0f), 127.0f);
+            code = (int)r;
+          }
         }
         word |= ((uint32_t)(code & 0xff)) << (8 * i);
       }
@@ -432,106 +455,149 @@ __device__ __forceinline__ void quantize_group_row(const float4 (&x)[VPL], int D
   if (lane == 0) *meta_row = make_float2(middle, scale);
 }
 
+// a9 over all rows.  Geometry: LPB lanes per row with VPL float4 each (D=64: 4 lanes x 4):
+// few lanes per row keep the per-row reductions cheap; R rows per group per iteration.
 template <int LPB, int VPL>
 __global__ void __launch_bounds__(256)
 k_quantize(const float* __restrict__ W, int pitch, int64_t rows, int D,
-           uint8_t* __restrict__ codes, int qpitch, float2* __restrict__ qmeta,
-           uint32_t* status) {
+           uint8_t* __restrict__ codes, int qpitch, int meta_off, uint32_t* status) {
+  constexpr int R = VPL >= 4 ? 2 : 4;  // rows in flight per group
   const int lane = threadIdx.x & (LPB - 1);
   const int64_t gstride = ((int64_t)gridDim.x * blockDim.x) / LPB;
+  const int64_t g0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LPB;
+  const int64_t gbase = g0 - (threadIdx.x & 31) / LPB;  // first group of my warp
   const int nvec = pitch >> 2;
-  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LPB; r < rows;
-       r += gstride) {
-    float4 x[VPL];
+  for (int64_t rb = gbase; rb < rows; rb += R * gstride) {  // uniform per warp
+    const int64_t r0 = g0 + (rb - gbase);
+    float4 x[R][VPL];
 #pragma unroll
-    for (int v = 0; v < VPL; ++v) {
-      const int vi = lane + v * LPB;
-      x[v] = vi < nvec ? ld_nc_f4(W + (size_t)r * pitch + 4 * vi) : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int q = 0; q < R; ++q) {
+      const int64_t r = r0 + q * gstride;
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) {
+        const int vi = lane + v * LPB;
+        x[q][v] = (r < rows && vi < nvec) ? ld_nc_f4(W + (size_t)r * pitch + 4 * vi)
+                                          : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
     }
-    quantize_group_row<LPB, VPL>(x, D, lane, codes + (size_t)r * qpitch, qmeta + r, status);
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const int64_t r = r0 + q * gstride;
+      const bool live = r < rows;
+      uint8_t* row = codes + (size_t)(live ? r : 0) * qpitch;
+      quantize_group_row<LPB, VPL>(x[q], D, lane, live, row,
+                                   reinterpret_cast<float2*>(row + meta_off), status);
+    }
   }
 }
 
-// Fused clip + sparse AdaGrad on the U unique rows (+ optional re-quantize).
+// Fused clip + sparse AdaGrad on the U unique rows (+ optional re-quantize).  Each lane
+// group handles R rows per iteration, all their loads issued before any update.
 template <int LPB, int VPL, bool ROWWISE, bool REQUANT>
 __global__ void __launch_bounds__(256)
 k_adagrad(const uint32_t* __restrict__ unique, const uint32_t* __restrict__ Up,
           const float* __restrict__ G, const float* __restrict__ clip, float* __restrict__ Wt,
           float* __restrict__ A, int pitch, int D, float lr, float eps,
-          uint8_t* __restrict__ codes, int qpitch, float2* __restrict__ qmeta,
-          uint32_t* status) {
+          uint8_t* __restrict__ codes, int qpitch, int meta_off, uint32_t* status) {
+  constexpr int R = 2;
   const float c = *clip;
-  if (c < 0.0f) return;  // non-finite global norm: skip the step
+  if (c < 0.0f) return;  // non-finite global norm: skip the step (uniform over the grid)
   const uint32_t U = *Up;
   const int lane = threadIdx.x & (LPB - 1);
   const int64_t gstride = ((int64_t)gridDim.x * blockDim.x) / LPB;
+  const int64_t g0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LPB;
+  const int64_t gbase = g0 - (threadIdx.x & 31) / LPB;
   const int nvec = pitch >> 2;
-  const double invD = (double)D;
-  for (int64_t u = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LPB; u < U; u += gstride) {
-    const uint32_t key = __ldg(unique + u);
-    float4 g[VPL], w[VPL];
+  const double dimD = (double)D;
+  for (int64_t ub = gbase; ub < U; ub += R * gstride) {  // uniform per warp
+    const int64_t u0 = g0 + (ub - gbase);
+    uint32_t key[R];
+    bool has[R];
+    float4 g[R][VPL], w[R][VPL], av[ROWWISE ? 1 : R][VPL];
+    float arow[R];
 #pragma unroll
-    for (int v = 0; v < VPL; ++v) {
-      const int vi = lane + v * LPB;
-      if (vi < nvec) {
-        const float4 Gv = ld_nc_f4(G + (size_t)u * pitch + 4 * vi);
-        g[v] = make_float4(__fmul_rn(Gv.x, c), __fmul_rn(Gv.y, c), __fmul_rn(Gv.z, c),
-                           __fmul_rn(Gv.w, c));
-        w[v] = ld_f4(Wt + (size_t)key * pitch + 4 * vi);
-      } else {
-        g[v] = make_float4(0.f, 0.f, 0.f, 0.f);
-        w[v] = g[v];
-      }
+    for (int q = 0; q < R; ++q) {
+      const int64_t u = u0 + q * gstride;
+      has[q] = u < U;
+      key[q] = has[q] ? __ldg(unique + u) : 0u;
     }
-    if (ROWWISE) {
-      double ss = 0.0;
 #pragma unroll
-      for (int v = 0; v < VPL; ++v) {
-        ss += (double)g[v].x * (double)g[v].x;
-        ss += (double)g[v].y * (double)g[v].y;
-        ss += (double)g[v].z * (double)g[v].z;
-        ss += (double)g[v].w * (double)g[v].w;
-      }
-      ss = group_sum<LPB>(ss);
-      const float s = (float)(ss / invD);
-      const float a = __fadd_rn(__ldg(A + key), s);
-      const float den = __fadd_rn(__fsqrt_rn(a), eps);
-      const float mult = __fdiv_rn(lr, den);
-#pragma unroll
-      for (int v = 0; v < VPL; ++v) {
-        w[v].x = __fsub_rn(w[v].x, __fmul_rn(mult, g[v].x));
-        w[v].y = __fsub_rn(w[v].y, __fmul_rn(mult, g[v].y));
-        w[v].z = __fsub_rn(w[v].z, __fmul_rn(mult, g[v].z));
-        w[v].w = __fsub_rn(w[v].w, __fmul_rn(mult, g[v].w));
-      }
-      if (lane == 0) A[key] = a;
-    } else {
-      const float nlr = -lr;
+    for (int q = 0; q < R; ++q) {
+      const int64_t u = u0 + q * gstride;
+      if (ROWWISE) arow[q] = has[q] ? __ldg(A + key[q]) : 0.f;
 #pragma unroll
       for (int v = 0; v < VPL; ++v) {
         const int vi = lane + v * LPB;
-        if (vi < nvec) {
-          float* ap = A + (size_t)key * pitch + 4 * vi;
-          float4 a = ld_f4(ap);
-          a.x = __fadd_rn(a.x, __fmul_rn(g[v].x, g[v].x));
-          a.y = __fadd_rn(a.y, __fmul_rn(g[v].y, g[v].y));
-          a.z = __fadd_rn(a.z, __fmul_rn(g[v].z, g[v].z));
-          a.w = __fadd_rn(a.w, __fmul_rn(g[v].w, g[v].w));
-          w[v].x = __fadd_rn(w[v].x, __fdiv_rn(__fmul_rn(nlr, g[v].x), __fadd_rn(__fsqrt_rn(a.x), eps)));
-          w[v].y = __fadd_rn(w[v].y, __fdiv_rn(__fmul_rn(nlr, g[v].y), __fadd_rn(__fsqrt_rn(a.y), eps)));
-          w[v].z = __fadd_rn(w[v].z, __fdiv_rn(__fmul_rn(nlr, g[v].z), __fadd_rn(__fsqrt_rn(a.z), eps)));
-          w[v].w = __fadd_rn(w[v].w, __fdiv_rn(__fmul_rn(nlr, g[v].w), __fadd_rn(__fsqrt_rn(a.w), eps)));
-          st_f4(ap, a);
+        if (has[q] && vi < nvec) {
+          const float4 Gv = ld_nc_f4(G + (size_t)u * pitch + 4 * vi);
+          g[q][v] = make_float4(__fmul_rn(Gv.x, c), __fmul_rn(Gv.y, c), __fmul_rn(Gv.z, c),
+                                __fmul_rn(Gv.w, c));
+          w[q][v] = ld_f4(Wt + (size_t)key[q] * pitch + 4 * vi);
+          if (!ROWWISE) av[ROWWISE ? 0 : q][v] = ld_f4(A + (size_t)key[q] * pitch + 4 * vi);
+        } else {
+          g[q][v] = make_float4(0.f, 0.f, 0.f, 0.f);
+          w[q][v] = g[q][v];
+          if (!ROWWISE) av[ROWWISE ? 0 : q][v] = g[q][v];
         }
       }
     }
 #pragma unroll
-    for (int v = 0; v < VPL; ++v) {
-      const int vi = lane + v * LPB;
-      if (vi < nvec) st_f4(Wt + (size_t)key * pitch + 4 * vi, w[v]);
+    for (int q = 0; q < R; ++q) {
+      if (ROWWISE) {
+        double ss = 0.0;
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) {
+          ss += (double)g[q][v].x * (double)g[q][v].x;
+          ss += (double)g[q][v].y * (double)g[q][v].y;
+          ss += (double)g[q][v].z * (double)g[q][v].z;
+          ss += (double)g[q][v].w * (double)g[q][v].w;
+        }
+        ss = group_sum<LPB>(ss);  // all lanes (has[] only predicates)
+        const float s = (float)(ss / dimD);
+        const float a = __fadd_rn(arow[q], s);
+        const float den = __fadd_rn(__fsqrt_rn(a), eps);
+        const float mult = __fdiv_rn(lr, den);
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) {
+          w[q][v].x = __fsub_rn(w[q][v].x, __fmul_rn(mult, g[q][v].x));
+          w[q][v].y = __fsub_rn(w[q][v].y, __fmul_rn(mult, g[q][v].y));
+          w[q][v].z = __fsub_rn(w[q][v].z, __fmul_rn(mult, g[q][v].z));
+          w[q][v].w = __fsub_rn(w[q][v].w, __fmul_rn(mult, g[q][v].w));
+        }
+        if (has[q] && lane == 0) A[key[q]] = a;
+      } else if (has[q]) {
+        const float nlr = -lr;
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) {
+          const int vi = lane + v * LPB;
+          if (vi < nvec) {
+            float4 a = av[ROWWISE ? 0 : q][v];
+            const float4 gg = g[q][v];
+            a.x = __fadd_rn(a.x, __fmul_rn(gg.x, gg.x));
+            a.y = __fadd_rn(a.y, __fmul_rn(gg.y, gg.y));
+            a.z = __fadd_rn(a.z, __fmul_rn(gg.z, gg.z));
+            a.w = __fadd_rn(a.w, __fmul_rn(gg.w, gg.w));
+            w[q][v].x = __fadd_rn(w[q][v].x, __fdiv_rn(__fmul_rn(nlr, gg.x), __fadd_rn(__fsqrt_rn(a.x), eps)));
+            w[q][v].y = __fadd_rn(w[q][v].y, __fdiv_rn(__fmul_rn(nlr, gg.y), __fadd_rn(__fsqrt_rn(a.y), eps)));
+            w[q][v].z = __fadd_rn(w[q][v].z, __fdiv_rn(__fmul_rn(nlr, gg.z), __fadd_rn(__fsqrt_rn(a.z), eps)));
+            w[q][v].w = __fadd_rn(w[q][v].w, __fdiv_rn(__fmul_rn(nlr, gg.w), __fadd_rn(__fsqrt_rn(a.w), eps)));
+            st_f4(A + (size_t)key[q] * pitch + 4 * vi, a);
+          }
+        }
+      }
+      if (has[q]) {
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) {
+          const int vi = lane + v * LPB;
+          if (vi < nvec) st_f4(Wt + (size_t)key[q] * pitch + 4 * vi, w[q][v]);
+        }
+      }
+      if (REQUANT) {
+        uint8_t* row = codes + (size_t)key[q] * qpitch;
+        quantize_group_row<LPB, VPL>(w[q], D, lane, has[q], row,
+                                     reinterpret_cast<float2*>(row + meta_off), status);
+      }
     }
-    if (REQUANT)
-      quantize_group_row<LPB, VPL>(w, D, lane, codes + (size_t)key * qpitch, qmeta + key, status);
   }
 }
 
@@ -566,8 +632,8 @@ cudaError_t launch_segreduce(const BwdArgs& a, int64_t* launches, cudaStream_t s
   const unsigned grid = (unsigned)((a.chunks * g.lpb + 255) / 256);
 #define LAUNCH_SR(MEAN)                                                                     \
   LIRANK_GEOM_DISPATCH(g, (k_segreduce<L_, V_, MEAN><<<grid, 256, 0, s>>>(                 \
-                              a.seg, a.U, a.vals, a.grad, a.offsets, a.B, a.F, a.D, a.pitch, \
-                              a.chunks, a.G, a.part_first, a.part_last, a.norm_main,        \
+                              a.seg, a.U, a.kv, a.chunk_u0, a.grad, a.offsets, a.B, a.F, a.D, \
+                              a.pitch, a.chunks, a.G, a.part_first, a.part_last, a.norm_main, \
                               a.norm_fix, a.owner_list, a.owner_count)))
   if (a.mean) LAUNCH_SR(true); else LAUNCH_SR(false);
 #undef LAUNCH_SR
@@ -606,7 +672,7 @@ cudaError_t launch_adagrad(const BwdArgs& a, cudaStream_t s) {
 #define LAUNCH_AG(RW, RQ)                                                                   \
   LIRANK_GEOM_DISPATCH(g, (k_adagrad<L_, V_, RW, RQ><<<grid, 256, 0, s>>>(                 \
                               a.unique, a.U, a.G, a.clip, a.Wt, a.A, a.pitch, a.D, a.lr,    \
-                              a.eps, a.q8_codes, a.qpitch, a.q8_meta, a.status)))
+                              a.eps, a.q8_codes, a.qpitch, a.q8_meta_off, a.status)))
   const bool rq = a.q8_codes != nullptr;
   if (a.rowwise) {
     if (rq) LAUNCH_AG(true, true); else LAUNCH_AG(true, false);
@@ -617,13 +683,28 @@ cudaError_t launch_adagrad(const BwdArgs& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// Quantize geometry: aim for 4 float4 vectors per lane (D=64: 4 lanes per row).
+static Geom quant_geom(int pitch) {
+  const int nvec = pitch / 4;
+  int lpb = 1;
+  while (lpb * 4 < nvec && lpb < 32) lpb <<= 1;
+  return Geom{lpb, (nvec + lpb - 1) / lpb};
+}
+
 cudaError_t launch_quantize(const float* W, int pitch, int64_t rows, int D, uint8_t* codes,
-                            int qpitch, float2* qmeta, uint32_t* status, cudaStream_t s) {
+                            int qpitch, int meta_off, uint32_t* status, cudaStream_t s) {
   if (rows == 0) return cudaSuccess;
-  const Geom g = geom_for(pitch);
+  const Geom g = quant_geom(pitch);
   const unsigned grid = persistent_grid(rows, g.lpb);
-  LIRANK_GEOM_DISPATCH(g, (k_quantize<L_, V_><<<grid, 256, 0, s>>>(W, pitch, rows, D, codes,
-                                                                    qpitch, qmeta, status)));
+#define LAUNCH_Q(L, V) k_quantize<L, V><<<grid, 256, 0, s>>>(W, pitch, rows, D, codes, qpitch, meta_off, status)
+  if (g.lpb == 1) {
+    if (g.vpl == 1) LAUNCH_Q(1, 1); else if (g.vpl == 2) LAUNCH_Q(1, 2); else if (g.vpl == 3) LAUNCH_Q(1, 3); else LAUNCH_Q(1, 4);
+  } else if (g.lpb == 2) { if (g.vpl <= 3) LAUNCH_Q(2, 3); else LAUNCH_Q(2, 4); }
+  else if (g.lpb == 4) { if (g.vpl <= 3) LAUNCH_Q(4, 3); else LAUNCH_Q(4, 4); }
+  else if (g.lpb == 8) { if (g.vpl <= 3) LAUNCH_Q(8, 3); else LAUNCH_Q(8, 4); }
+  else if (g.lpb == 16) { if (g.vpl <= 3) LAUNCH_Q(16, 3); else LAUNCH_Q(16, 4); }
+  else { if (g.vpl <= 4) LAUNCH_Q(32, 4); else LAUNCH_Q(32, 8); }
+#undef LAUNCH_Q
   return cudaGetLastError();
 }
 

@@ -4,62 +4,104 @@
 // W[key_j][:]; MEAN divides by the bag length; empty bag -> 0; invalid ids skipped.
 // a10: the same over the q8 store, each term fmaf(code, scale, middle).
 //
-// Design (B200): one group of LPB lanes per bag (D=64 -> half-warp), 128-bit row loads
-// (ld.global.nc.L1::no_allocate: rows are streamed, L2 keeps Zipf-hot rows), ids of a
-// bag loaded LPB at a time and broadcast by shuffle, row loads of UNR ids issued before
-// the in-order adds.  Grid: one group per bag, 256-thread CTAs.  The fp32 kernel also
-// emits the (row key, bag) pair of every occurrence for the backward's dedup, so the
-// backward never re-reads ids/offsets (8 extra bytes written per id).
+// Design (B200).  One group of LPB lanes per bag (D=64 fp32: 16 lanes x one 128-bit load
+// = one 256-B row).  The group loads LPB ids at once (one per lane) and broadcasts them by
+// full-mask shuffles (the id loop runs to the longest bag of the warp, so every lane
+// reaches every shuffle); it then issues the row loads of UNR ids back to back
+// (ld.global.nc.L1::no_allocate: rows are streamed, L2 keeps the Zipf-hot rows) before
+// adding them in bag order.  (Per-slot id loads by every lane made the id->row dependence
+// chain 4x longer and were measurably slower.)  Measured
+// (profiles/): a random 256-B row gather on this part is DRAM-activation bound at
+// ~24 G rows/s (~6.3 TB/s) for uniform ids; this kernel runs the Feed-1 batch at that
+// rate incl. its offsets/ids/outputs.  A CTA-staged variant (offsets + ids through shared
+// memory, 4 bags per group) was slower (fewer independent groups in flight) and was
+// dropped.  The fp32 kernel also emits, per occurrence, the packed {row key, grad row}
+// pair the backward's dedup sorts (8 B per id), so the backward never re-reads ids or
+// offsets.
 #include "common.cuh"
 #include "kernels.h"
 
 namespace lirank {
 
+namespace {
+
+__device__ __forceinline__ uint32_t row_key(int id, const FeatMeta& m, uint32_t none, bool& bad) {
+  const bool valid = id >= 0 && id < m.rows;
+  bad |= !valid;
+  return (valid && id >= m.lo && id < m.hi) ? (uint32_t)(m.base + (id - m.lo)) : none;
+}
+
+template <int N>
+__device__ __forceinline__ void mean_div(float4 (&acc)[N], int L) {
+  if (L <= 0) return;
+  const float fl = (float)L;
+#pragma unroll
+  for (int v = 0; v < N; ++v)
+    acc[v] = make_float4(__fdiv_rn(acc[v].x, fl), __fdiv_rn(acc[v].y, fl),
+                         __fdiv_rn(acc[v].z, fl), __fdiv_rn(acc[v].w, fl));
+}
+
+__device__ __forceinline__ void store4(float* o, int d, int D, float4 a) {
+  if ((D & 3) == 0) {
+    if (d < D) st_f4(o + d, a);
+  } else {
+    if (d + 0 < D) o[d + 0] = a.x;
+    if (d + 1 < D) o[d + 1] = a.y;
+    if (d + 2 < D) o[d + 2] = a.z;
+    if (d + 3 < D) o[d + 3] = a.w;
+  }
+}
+
+// Output row of bag (f, b) where the F features form source blocks of Fb features each:
+// out row = (blk * B + b) * Fb + (f % Fb).  Unsharded: Fb = F, row = b * F + f.
+__device__ __forceinline__ size_t out_row(int f, int b, int B, int Fb) {
+  const int blk = f / Fb;
+  return ((size_t)blk * B + b) * Fb + (f - blk * Fb);
+}
+
+}  // namespace
+
 template <int LPB, int VPL, bool MEAN, bool EMIT>
 __global__ void __launch_bounds__(256)
 k_pool_fwd_f32(const float* __restrict__ W, int pitch, const int* __restrict__ ids,
-               const int* __restrict__ offsets, int B, int F, int D,
+               const int* __restrict__ offsets, int B, int F, int Fb, int D,
                const FeatMeta* __restrict__ meta, float* __restrict__ out,
-               uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
-               uint32_t sentinel, uint32_t* status) {
+               uint2* __restrict__ kv_out, uint32_t sentinel, uint32_t* status) {
   constexpr int UNR = (VPL == 1) ? 4 : (VPL == 2 ? 2 : 1);
+  constexpr unsigned kFull = 0xffffffffu;
   const int lane = threadIdx.x & (LPB - 1);
   const long long bag = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / LPB;
-  if (bag >= (long long)F * B) return;
-  const unsigned gmask = group_mask<LPB>();
-  const int f = (int)(bag / B);
-  const int b = (int)(bag - (long long)f * B);
+  const bool live = bag < (long long)F * B;  // predicate, never return: shuffles below
+  const int f = live ? (int)(bag / B) : 0;
+  const int b = live ? (int)(bag - (long long)f * B) : 0;
   const FeatMeta m = meta[f];
-  const int lo = __ldg(offsets + bag);
-  const int hi = __ldg(offsets + bag + 1);
+  const int lo = live ? __ldg(offsets + bag) : 0;
+  const int hi = live ? __ldg(offsets + bag + 1) : 0;
+  const int len = hi - lo;
   const int nvec = pitch >> 2;
-
+  const uint32_t grow = (uint32_t)out_row(f, b, B, Fb);
   float4 acc[VPL];
 #pragma unroll
   for (int v = 0; v < VPL; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
-
   bool bad = false;
-  for (int j0 = lo; j0 < hi; j0 += LPB) {
+  // Warp-uniform trip count (the longest bag among the warp's groups): every lane reaches
+  // every shuffle, so shuffles use the full mask; shorter bags are predicated.
+  const int maxlen = __reduce_max_sync(kFull, len);
+  for (int j0 = 0; j0 < maxlen; j0 += LPB) {
     const int j = j0 + lane;
     uint32_t key = sentinel;
-    if (j < hi) {
-      const int id = ld_nc_i32(ids + j);
-      const bool valid = id >= 0 && id < m.rows;
-      bad |= !valid;
-      if (valid && id >= m.lo && id < m.hi) key = (uint32_t)(m.base + (id - m.lo));
-      if (EMIT) {
-        keys_out[j] = key;
-        vals_out[j] = (uint32_t)bag;
-      }
+    if (j < len) {  // one id per lane, LPB ids per group at once
+      key = row_key(__ldg(ids + lo + j), m, sentinel, bad);
+      if (EMIT) kv_out[lo + j] = make_uint2(key, grow);
     }
-    const int cnt = min(LPB, hi - j0);
-    for (int jj = 0; jj < cnt; jj += UNR) {
+#pragma unroll
+    for (int jj = 0; jj < LPB; jj += UNR) {
       uint32_t k[UNR];
       float4 r[UNR][VPL];
 #pragma unroll
       for (int u = 0; u < UNR; ++u) {
-        k[u] = __shfl_sync(gmask, key, (jj + u) & (LPB - 1), LPB);
-        if (jj + u >= cnt) k[u] = sentinel;
+        k[u] = __shfl_sync(kFull, key, (jj + u) & (LPB - 1), LPB);
+        if (jj + u >= LPB || j0 + jj + u >= len) k[u] = sentinel;
       }
 #pragma unroll
       for (int u = 0; u < UNR; ++u) {
@@ -68,8 +110,7 @@ k_pool_fwd_f32(const float* __restrict__ W, int pitch, const int* __restrict__ i
 #pragma unroll
           for (int v = 0; v < VPL; ++v) {
             const int vi = lane + v * LPB;
-            r[u][v] = (VPL * LPB == 1 || vi < nvec) ? ld_nc_f4(row + 4 * vi)
-                                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+            r[u][v] = vi < nvec ? ld_nc_f4(row + 4 * vi) : make_float4(0.f, 0.f, 0.f, 0.f);
           }
         }
       }
@@ -81,141 +122,101 @@ k_pool_fwd_f32(const float* __restrict__ W, int pitch, const int* __restrict__ i
         }
     }
   }
-  if (bad) set_status(status, kStIdRange);
-
-  if (MEAN) {
-    const int L = hi - lo;
-    if (L > 0) {
-      const float fl = (float)L;
+  if (!live) return;
+  if (bad && lane == 0) set_status(status, kStIdRange);
+  if (MEAN) mean_div(acc, len);
+  float* o = out + (size_t)grow * D;
 #pragma unroll
-      for (int v = 0; v < VPL; ++v)
-        acc[v] = make_float4(__fdiv_rn(acc[v].x, fl), __fdiv_rn(acc[v].y, fl),
-                             __fdiv_rn(acc[v].z, fl), __fdiv_rn(acc[v].w, fl));
-    }
-  }
-  float* o = out + ((size_t)b * F + f) * D;
-  if ((D & 3) == 0) {
-#pragma unroll
-    for (int v = 0; v < VPL; ++v) {
-      const int vi = lane + v * LPB;
-      if (4 * vi < D) st_f4(o + 4 * vi, acc[v]);
-    }
-  } else {
-#pragma unroll
-    for (int v = 0; v < VPL; ++v) {
-      const int d = 4 * (lane + v * LPB);
-      if (d + 0 < D) o[d + 0] = acc[v].x;
-      if (d + 1 < D) o[d + 1] = acc[v].y;
-      if (d + 2 < D) o[d + 2] = acc[v].z;
-      if (d + 3 < D) o[d + 3] = acc[v].w;
-    }
-  }
+  for (int v = 0; v < VPL; ++v) store4(o, 4 * (lane + v * LPB), D, acc[v]);
 }
 
-__device__ __forceinline__ float4 deq4(uint32_t w, float scale, float middle) {
-  // X^dequant = X^middle + X^int * X^scale, one fmaf per element (reading 7)
-  const float c0 = (float)(int)(int8_t)(w & 0xffu);
-  const float c1 = (float)(int)(int8_t)((w >> 8) & 0xffu);
-  const float c2 = (float)(int)(int8_t)((w >> 16) & 0xffu);
-  const float c3 = (float)(int)(int8_t)(w >> 24);
-  return make_float4(__fmaf_rn(c0, scale, middle), __fmaf_rn(c1, scale, middle),
-                     __fmaf_rn(c2, scale, middle), __fmaf_rn(c3, scale, middle));
+// X^dequant = X^middle + X^int * X^scale: one fmaf per element (reading 7).
+// The int8 code becomes an exact float without a conversion instruction: with
+// u = byte ^ 0x80 = code + 128, the float with bits 0x4B0000uu is 2^23 + u, so
+// (2^23 + u) - (2^23 + 128) = code exactly.
+__device__ __forceinline__ float code_f(uint32_t x, uint32_t sel) {
+  return __fsub_rn(__int_as_float((int)__byte_perm(x, 0x4B000000u, sel)), 8388736.0f);
+}
+__device__ __forceinline__ void deq8(uint2 w, float scale, float middle, float4& lo, float4& hi) {
+  const uint32_t x = w.x ^ 0x80808080u, y = w.y ^ 0x80808080u;
+  lo = make_float4(__fmaf_rn(code_f(x, 0x7540), scale, middle), __fmaf_rn(code_f(x, 0x7541), scale, middle),
+                   __fmaf_rn(code_f(x, 0x7542), scale, middle), __fmaf_rn(code_f(x, 0x7543), scale, middle));
+  hi = make_float4(__fmaf_rn(code_f(y, 0x7540), scale, middle), __fmaf_rn(code_f(y, 0x7541), scale, middle),
+                   __fmaf_rn(code_f(y, 0x7542), scale, middle), __fmaf_rn(code_f(y, 0x7543), scale, middle));
+}
+__device__ __forceinline__ uint2 ld_nc_u2(const void* p) {
+  uint2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+  return r;
 }
 
-// a10.  Lane l of a group reads code words l, l+LPB, ... (4 codes each) of the row and the
-// row's {middle, scale} (one broadcast 8-B load per group).
+// a10.  q8 row layout: [codes: D int8][pad to 8][middle f32][scale f32][pad to 16]
+// (D=64: 80 B, one contiguous run per row).  Lane l of a group of LPB lanes reads code
+// vectors l, l+LPB, ... (8 codes, one 8-B load each) and the row's {middle, scale} (8 B,
+// same address for the whole group).  D=64: 8 lanes per bag, 4 bags per warp.
 template <int LPB, int VPL, bool MEAN>
 __global__ void __launch_bounds__(256)
-k_pool_fwd_q8(const uint8_t* __restrict__ codes, int qpitch, const float2* __restrict__ qmeta,
-              const int* __restrict__ ids, const int* __restrict__ offsets, int B, int F,
+k_pool_fwd_q8(const uint8_t* __restrict__ codes, int qpitch, int meta_off,
+              const int* __restrict__ ids, const int* __restrict__ offsets, int B, int F, int Fb,
               int D, const FeatMeta* __restrict__ meta, float* __restrict__ out,
               uint32_t* status) {
-  constexpr int UNR = (VPL == 1) ? 4 : (VPL == 2 ? 2 : 1);
+  constexpr int UNR = (VPL == 1) ? 8 : (VPL == 2 ? 4 : 2);
+  constexpr uint32_t kNone = 0xffffffffu;
   const int lane = threadIdx.x & (LPB - 1);
   const long long bag = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / LPB;
   if (bag >= (long long)F * B) return;
-  const unsigned gmask = group_mask<LPB>();
   const int f = (int)(bag / B);
   const int b = (int)(bag - (long long)f * B);
   const FeatMeta m = meta[f];
   const int lo = __ldg(offsets + bag);
   const int hi = __ldg(offsets + bag + 1);
-  const int nw = (D + 3) >> 2;  // code words that carry dims < D
-  constexpr uint32_t kNone = 0xffffffffu;
-
-  float4 acc[VPL];
+  const int nv8 = (D + 7) >> 3;  // 8-code vectors carrying dims < D
+  float4 acc[2 * VPL];
 #pragma unroll
-  for (int v = 0; v < VPL; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
-
+  for (int v = 0; v < 2 * VPL; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
   bool bad = false;
-  for (int j0 = lo; j0 < hi; j0 += LPB) {
-    const int j = j0 + lane;
-    uint32_t key = kNone;
-    if (j < hi) {
-      const int id = ld_nc_i32(ids + j);
-      const bool valid = id >= 0 && id < m.rows;
-      bad |= !valid;
-      if (valid && id >= m.lo && id < m.hi) key = (uint32_t)(m.base + (id - m.lo));
+  for (int j0 = lo; j0 < hi; j0 += UNR) {
+    uint32_t k[UNR];
+    uint2 w[UNR][VPL];
+    float2 mt[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int j = j0 + u;
+      k[u] = j < hi ? row_key(__ldg(ids + j), m, kNone, bad) : kNone;
     }
-    const int cnt = min(LPB, hi - j0);
-    for (int jj = 0; jj < cnt; jj += UNR) {
-      uint32_t k[UNR];
-      uint32_t w[UNR][VPL];
-      float2 mt[UNR];
 #pragma unroll
-      for (int u = 0; u < UNR; ++u) {
-        k[u] = __shfl_sync(gmask, key, (jj + u) & (LPB - 1), LPB);
-        if (jj + u >= cnt) k[u] = kNone;
-      }
+    for (int u = 0; u < UNR; ++u) {
+      if (k[u] != kNone) {
+        const uint8_t* row = codes + (size_t)k[u] * qpitch;
+        mt[u] = *reinterpret_cast<const float2*>(row + meta_off);
 #pragma unroll
-      for (int u = 0; u < UNR; ++u) {
-        if (k[u] != kNone) {
-          mt[u] = __ldg(qmeta + k[u]);
-          const uint32_t* row = reinterpret_cast<const uint32_t*>(codes + (size_t)k[u] * qpitch);
-#pragma unroll
-          for (int v = 0; v < VPL; ++v) {
-            const int wi = lane + v * LPB;
-            w[u][v] = (wi < nw) ? (uint32_t)ld_nc_i32(reinterpret_cast<const int*>(row + wi)) : 0u;
-          }
+        for (int v = 0; v < VPL; ++v) {
+          const int vi = lane + v * LPB;
+          w[u][v] = vi < nv8 ? ld_nc_u2(row + 8 * vi) : make_uint2(0x80808080u, 0x80808080u);
         }
       }
+    }
 #pragma unroll
-      for (int u = 0; u < UNR; ++u)
-        if (k[u] != kNone) {
+    for (int u = 0; u < UNR; ++u)
+      if (k[u] != kNone) {
 #pragma unroll
-          for (int v = 0; v < VPL; ++v)
-            acc[v] = f4_add_rn(acc[v], deq4(w[u][v], mt[u].y, mt[u].x));
+        for (int v = 0; v < VPL; ++v) {
+          float4 dl, dh;
+          deq8(w[u][v], mt[u].y, mt[u].x, dl, dh);
+          acc[2 * v] = f4_add_rn(acc[2 * v], dl);
+          acc[2 * v + 1] = f4_add_rn(acc[2 * v + 1], dh);
         }
-    }
+      }
   }
-  if (bad) set_status(status, kStIdRange);
-
-  if (MEAN) {
-    const int L = hi - lo;
-    if (L > 0) {
-      const float fl = (float)L;
+  if (bad && lane == 0) set_status(status, kStIdRange);
+  if (MEAN) mean_div(acc, hi - lo);
+  // lane l holds dims 8*(l + v*LPB) .. +8
+  float* o = out + out_row(f, b, B, Fb) * D;
 #pragma unroll
-      for (int v = 0; v < VPL; ++v)
-        acc[v] = make_float4(__fdiv_rn(acc[v].x, fl), __fdiv_rn(acc[v].y, fl),
-                             __fdiv_rn(acc[v].z, fl), __fdiv_rn(acc[v].w, fl));
-    }
-  }
-  float* o = out + ((size_t)b * F + f) * D;
-  if ((D & 3) == 0) {
-#pragma unroll
-    for (int v = 0; v < VPL; ++v) {
-      const int vi = lane + v * LPB;
-      if (4 * vi < D) st_f4(o + 4 * vi, acc[v]);
-    }
-  } else {
-#pragma unroll
-    for (int v = 0; v < VPL; ++v) {
-      const int d = 4 * (lane + v * LPB);
-      if (d + 0 < D) o[d + 0] = acc[v].x;
-      if (d + 1 < D) o[d + 1] = acc[v].y;
-      if (d + 2 < D) o[d + 2] = acc[v].z;
-      if (d + 3 < D) o[d + 3] = acc[v].w;
-    }
+  for (int v = 0; v < VPL; ++v) {
+    const int d = 8 * (lane + v * LPB);
+    store4(o, d, D, acc[2 * v]);
+    store4(o, d + 4, D, acc[2 * v + 1]);
   }
 }
 
@@ -240,32 +241,32 @@ cudaError_t launch_pool_fwd_f32(const FwdArgs& a, cudaStream_t s) {
   const Geom g = geom_for(a.pitch);
   const long long bags = (long long)a.F * a.B;
   if (bags == 0) return cudaSuccess;
-  const long long threads = bags * g.lpb;
-  const unsigned grid = (unsigned)((threads + 255) / 256);
+  const unsigned grid = (unsigned)((bags * g.lpb + 255) / 256);
+  const int Fb = a.Fb > 0 ? a.Fb : a.F;
 #define LAUNCH_F32(MEAN, EMIT)                                                             \
   LIRANK_GEOM_DISPATCH(g, (k_pool_fwd_f32<L_, V_, MEAN, EMIT><<<grid, 256, 0, s>>>(        \
-                              a.W, a.pitch, a.ids, a.offsets, a.B, a.F, a.D, a.meta, a.out, \
-                              a.keys_out, a.vals_out, a.sentinel, a.status)))
+                              a.W, a.pitch, a.ids, a.offsets, a.B, a.F, Fb, a.D, a.meta,    \
+                              a.out, a.kv_out, a.sentinel, a.status)))
   if (a.mean) {
-    if (a.keys_out) LAUNCH_F32(true, true); else LAUNCH_F32(true, false);
+    if (a.kv_out) LAUNCH_F32(true, true); else LAUNCH_F32(true, false);
   } else {
-    if (a.keys_out) LAUNCH_F32(false, true); else LAUNCH_F32(false, false);
+    if (a.kv_out) LAUNCH_F32(false, true); else LAUNCH_F32(false, false);
   }
 #undef LAUNCH_F32
   return cudaGetLastError();
 }
 
 cudaError_t launch_pool_fwd_q8(const FwdQ8Args& a, cudaStream_t s) {
-  // geometry over 32-bit code words (4 dims each)
-  const Geom g = geom_for(4 * ((a.D + 3) / 4));
+  // geometry over 8-code vectors (one 8-B load each)
+  const Geom g = geom_for(4 * ((a.D + 7) / 8));
   const long long bags = (long long)a.F * a.B;
   if (bags == 0) return cudaSuccess;
-  const long long threads = bags * g.lpb;
-  const unsigned grid = (unsigned)((threads + 255) / 256);
+  const unsigned grid = (unsigned)((bags * g.lpb + 255) / 256);
+  const int Fb = a.Fb > 0 ? a.Fb : a.F;
 #define LAUNCH_Q8(MEAN)                                                                    \
   LIRANK_GEOM_DISPATCH(g, (k_pool_fwd_q8<L_, V_, MEAN><<<grid, 256, 0, s>>>(               \
-                              a.codes, a.qpitch, a.qmeta, a.ids, a.offsets, a.B, a.F, a.D, \
-                              a.meta, a.out, a.status)))
+                              a.codes, a.qpitch, a.meta_off, a.ids, a.offsets, a.B, a.F, Fb, \
+                              a.D, a.meta, a.out, a.status)))
   if (a.mean) LAUNCH_Q8(true); else LAUNCH_Q8(false);
 #undef LAUNCH_Q8
   return cudaGetLastError();

@@ -14,10 +14,10 @@ struct FwdArgs {
   const int* ids;
   const int* offsets;
   int B, F, D;
+  int Fb;              // features per source block (0: F, unsharded)
   const FeatMeta* meta;
   float* out;
-  uint32_t* keys_out;  // NULL: do not record occurrences
-  uint32_t* vals_out;
+  uint2* kv_out;       // NULL: do not record occurrences ({row key, bag} per id)
   uint32_t sentinel;
   uint32_t* status;
   bool mean;
@@ -25,12 +25,13 @@ struct FwdArgs {
 cudaError_t launch_pool_fwd_f32(const FwdArgs& a, cudaStream_t s);
 
 struct FwdQ8Args {
-  const uint8_t* codes;
+  const uint8_t* codes;   // q8 rows: [codes][pad][middle, scale][pad], qpitch bytes
   int qpitch;
-  const float2* qmeta;
+  int meta_off;           // byte offset of {middle, scale} in a q8 row
   const int* ids;
   const int* offsets;
   int B, F, D;
+  int Fb;
   const FeatMeta* meta;
   float* out;
   uint32_t* status;
@@ -39,30 +40,32 @@ struct FwdQ8Args {
 cudaError_t launch_pool_fwd_q8(const FwdQ8Args& a, cudaStream_t s);
 
 // ---- a5 dedup: LSD radix sort (onesweep) + run-length encode -------------------------
-constexpr int kRadixBits = 8;
-constexpr int kRadixBins = 1 << kRadixBits;
+// Occurrences are packed {key = stored row (sentinel if invalid), bag index} pairs.
+constexpr int kRadixBinsMax = 512;      // 8- or 9-bit digits
 constexpr int kSortThreads = 256;
-constexpr int kSortItems = 16;  // per thread
+constexpr int kSortItems = 16;          // per thread
 constexpr int kSortTile = kSortThreads * kSortItems;
-constexpr int kMaxPasses = 4;   // keys < 2^32
+constexpr int kMaxPasses = 4;           // keys < 2^32
+constexpr int kHistWords = kMaxPasses * kRadixBinsMax;
 
 struct SortWs {
-  uint32_t* hist;         // [kMaxPasses][kRadixBins] (zeroed by the sort)
-  uint32_t* counters;     // [kMaxPasses + 2] dynamic tile counters (zeroed by the sort)
-  unsigned long long* status;  // [max_tiles][kRadixBins] look-back words (epoch tagged)
+  uint32_t* hist;         // [kHistWords] digit histograms, then [kMaxPasses + 2] tile
+  uint32_t* counters;     // counters (both zeroed by the sort)
+  unsigned long long* status;  // [max_tiles][kRadixBinsMax] look-back words (epoch tagged)
   int64_t max_tiles;
 };
 
-// Sorts (keys, vals) of length n by the low `bits` bits of key, stably.  Ping-pongs
-// between (k0,v0) and (k1,v1); returns in *result_in_1 whether the result is in (k1,v1).
-cudaError_t radix_sort_pairs(uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1, int64_t n,
-                             int bits, const SortWs& ws, uint32_t epoch, int* passes_out,
-                             bool* result_in_1, int64_t* launches, cudaStream_t s);
+// Sorts n pairs by the low `bits` bits of .x, stably.  Ping-pongs between kv0 and kv1;
+// *result_in_1 tells whether the result is in kv1.  Uses epochs [epoch, epoch+passes).
+cudaError_t radix_sort_pairs(uint2* kv0, uint2* kv1, int64_t n, int bits, const SortWs& ws,
+                             uint32_t epoch, int* passes_out, bool* result_in_1, int64_t* launches,
+                             cudaStream_t s);
 
-// Run-length encode sorted keys (sentinel = invalid, sorts last): unique[U], seg[U+1],
-// *U_out (device int32).  Requires seg/U prepared by the caller only for n == 0.
-cudaError_t launch_rle(const uint32_t* keys, int64_t n, uint32_t sentinel, uint32_t* unique,
-                       uint32_t* seg, uint32_t* U_out, uint32_t* counter,
+// Run-length encode sorted pairs (sentinel = invalid, sorts last): unique[U], seg[U+1],
+// *U_out, and chunk_u0[c] = segment containing occurrence c*kChunk.  For n == 0 the caller
+// writes U = 0, seg[0] = 0.
+cudaError_t launch_rle(const uint2* kv, int64_t n, uint32_t sentinel, uint32_t* unique,
+                       uint32_t* seg, uint32_t* U_out, uint32_t* chunk_u0, uint32_t* counter,
                        unsigned long long* status, uint32_t epoch, cudaStream_t s);
 
 // ---- a6-a8 ----------------------------------------------------------------------------
@@ -73,7 +76,8 @@ struct BwdArgs {
   const uint32_t* unique;   // [U]
   const uint32_t* seg;      // [U+1]
   const uint32_t* U;        // device scalar
-  const uint32_t* vals;     // sorted bag index per occurrence
+  const uint2* kv;          // sorted {key, bag} per occurrence
+  const uint32_t* chunk_u0; // [chunks] segment containing the chunk's first occurrence
   int64_t nnz;              // upper bound of valid occurrences
   // gradient input
   const float* grad;        // [B][F][D]
@@ -102,7 +106,7 @@ struct BwdArgs {
   bool rowwise;
   float lr, eps;
   uint8_t* q8_codes;        // requantize touched rows (NULL: no)
-  float2* q8_meta;
+  int q8_meta_off;
   int qpitch;
 };
 cudaError_t launch_segreduce(const BwdArgs& a, int64_t* launches, cudaStream_t s);
@@ -115,7 +119,7 @@ cudaError_t launch_adagrad(const BwdArgs& a, cudaStream_t s);
 
 // ---- a9 ----------------------------------------------------------------------------
 cudaError_t launch_quantize(const float* W, int pitch, int64_t rows, int D, uint8_t* codes,
-                            int qpitch, float2* qmeta, uint32_t* status, cudaStream_t s);
+                            int qpitch, int meta_off, uint32_t* status, cudaStream_t s);
 
 // ---- misc --------------------------------------------------------------------------
 cudaError_t launch_fill(float* p, int64_t n, float v, cudaStream_t s);

@@ -1,17 +1,22 @@
 // sort.cu -- a5 dedup: stable LSD radix sort of (row key, bag) pairs + run-length encode.
 //
 // The dedup gives, for every touched row, the CSR list of its occurrences in ascending
-// occurrence order (the ordering is reading 16).  Keys are the
-// stored-row index (< 2^31), invalid occurrences carry a sentinel key (= local rows) that
+// occurrence order (the tie order is reading 16).  Keys are the
+// stored-row index (< 2^31); invalid occurrences carry a sentinel key (= local rows) that
 // sorts after every valid key and is cut off by the run-length encode.
 //
-// Design (B200): "onesweep" LSD radix sort -- one upfront histogram kernel for all digit
-// passes, then ONE kernel per 8-bit digit pass that ranks a 4096-key tile in registers
-// (warp match_any ranking, stable in index order), finds the tile's global digit offsets
-// with a decoupled look-back over earlier tiles (64-bit epoch-tagged status words, so
-// no per-step memset), and scatters.  Each pass moves 16 B per key (read key+value,
-// write key+value).  Tiles are claimed in launch order through an atomic counter, so a
-// look-back only ever waits on tiles that are already resident.
+// Design (B200): "onesweep" LSD radix sort over packed 8-byte {key, bag} pairs.
+// * One upfront histogram kernel computes the digit histograms of every pass in a single
+//   read of the keys (ballot-matched digits counted into per-warp private shared-memory
+//   histograms: no atomics in the loop; shared atomics are slow on this part).
+// * ONE kernel per digit pass (8- or 9-bit digits: 27-bit Feed-1 keys take 3 passes):
+//   a 4096-pair tile is loaded with coalesced 8-B loads and ranked in registers (warp
+//   multisplit by ballots, stable in index order), the tile's digit counts are published
+//   and the global offsets found by a decoupled look-back over earlier tiles (64-bit
+//   epoch-tagged status words, so no per-step memset), overlapped with staging the tile
+//   in shared memory in sorted order; the tile is then written out in digit runs
+//   (coalesced).  Each pass moves 16 B per pair.  Tiles are claimed in launch order
+//   through an atomic counter, so a look-back only waits on tiles already resident.
 #include "common.cuh"
 #include "kernels.h"
 
@@ -22,12 +27,12 @@ namespace {
 constexpr unsigned long long kFlagAgg = 1ull << 30;
 constexpr unsigned long long kFlagPrefix = 2ull << 30;
 constexpr unsigned long long kCountMask = (1ull << 30) - 1;
+constexpr int NW = kSortThreads / 32;
 
 __device__ __forceinline__ unsigned long long pack(uint32_t epoch, unsigned long long flag,
                                                    uint32_t count) {
   return ((unsigned long long)epoch << 32) | flag | (unsigned long long)count;
 }
-
 __device__ __forceinline__ void st_volatile(unsigned long long* p, unsigned long long v) {
   *reinterpret_cast<volatile unsigned long long*>(p) = v;
 }
@@ -35,28 +40,38 @@ __device__ __forceinline__ unsigned long long ld_volatile(const unsigned long lo
   return *reinterpret_cast<const volatile unsigned long long*>(p);
 }
 
-// Exclusive prefix of everything before `tile` for the value published at
-// status[tile * stride + slot]; publishes this tile's aggregate and then its inclusive
-// prefix.  Called by one thread per slot.
-__device__ __forceinline__ uint32_t lookback(unsigned long long* status, int64_t tile,
-                                             int stride, int slot, uint32_t epoch,
-                                             uint32_t aggregate) {
-  unsigned long long* mine = status + tile * stride + slot;
-  if (tile == 0) {
-    st_volatile(mine, pack(epoch, kFlagPrefix, aggregate));
-    return 0;
-  }
-  st_volatile(mine, pack(epoch, kFlagAgg, aggregate));
+// Decoupled look-back, split in two so the caller can overlap work between publishing
+// its aggregate and waiting for its prefix.
+__device__ __forceinline__ void lb_publish(unsigned long long* status, int64_t tile, int stride,
+                                           int slot, uint32_t epoch, uint32_t aggregate) {
+  st_volatile(status + tile * stride + slot,
+              pack(epoch, tile == 0 ? kFlagPrefix : kFlagAgg, aggregate));
+}
+__device__ __forceinline__ uint32_t lb_wait(unsigned long long* status, int64_t tile, int stride,
+                                            int slot, uint32_t epoch, uint32_t aggregate) {
+  // Look back kLB predecessors per round (independent loads, one L2 round trip), walking
+  // from the nearest: add aggregates until an inclusive prefix is found; a predecessor
+  // that has not published yet is re-polled from where the walk stopped.
+  constexpr int kLB = 8;
+  if (tile == 0) return 0;
   uint32_t excl = 0;
   int64_t p = tile - 1;
   while (true) {
-    const unsigned long long w = ld_volatile(status + p * stride + slot);
-    if ((uint32_t)(w >> 32) != epoch || (w & (3ull << 30)) == 0) continue;  // not yet
-    excl += (uint32_t)(w & kCountMask);
-    if (w & kFlagPrefix) break;
-    --p;
+    unsigned long long w[kLB];
+#pragma unroll
+    for (int i = 0; i < kLB; ++i)
+      w[i] = p - i >= 0 ? ld_volatile(status + (p - i) * stride + slot) : 0ull;
+    bool done = false;
+    int i = 0;
+    for (; i < kLB && p - i >= 0; ++i) {
+      if ((uint32_t)(w[i] >> 32) != epoch || (w[i] & (3ull << 30)) == 0) break;  // not yet
+      excl += (uint32_t)(w[i] & kCountMask);
+      if (w[i] & kFlagPrefix) { done = true; break; }
+    }
+    if (done) break;
+    p -= i;
   }
-  st_volatile(mine, pack(epoch, kFlagPrefix, excl + aggregate));
+  st_volatile(status + tile * stride + slot, pack(epoch, kFlagPrefix, excl + aggregate));
   return excl;
 }
 
@@ -66,149 +81,268 @@ __device__ __forceinline__ unsigned lanemask_lt() {
   return m;
 }
 
+// Lanes of the warp whose digit equals mine (warp multisplit by ballots), among `valid`.
+template <int BITS>
+__device__ __forceinline__ unsigned peers_of(uint32_t d, unsigned valid) {
+  unsigned m = valid;
+#pragma unroll
+  for (int b = 0; b < BITS; ++b) {
+    const unsigned bb = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+    m &= ((d >> b) & 1u) ? bb : ~bb;
+  }
+  return m;
+}
+
+// Exclusive block scan of one value per thread (256 threads); returns the exclusive
+// prefix, *total gets the block sum.
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp, uint32_t* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_warp[warp] = x;
+  __syncthreads();
+  uint32_t wpre = 0, tot = 0;
+#pragma unroll
+  for (int w = 0; w < NW; ++w) {
+    const uint32_t s = s_warp[w];
+    if (w < warp) wpre += s;
+    tot += s;
+  }
+  __syncthreads();
+  *total = tot;
+  return wpre + x - v;
+}
+
 }  // namespace
 
-// Histogram of every digit pass in one read of the keys.
-__global__ void __launch_bounds__(256)
-k_radix_hist(const uint32_t* __restrict__ keys, int64_t n, int passes, uint32_t* hist) {
-  __shared__ uint32_t sh[kMaxPasses * kRadixBins];
-  for (int i = threadIdx.x; i < kMaxPasses * kRadixBins; i += blockDim.x) sh[i] = 0;
+// ---------------------------------------------------------------------------
+// Upfront histogram of every digit pass.  128-thread CTAs, per-warp private histograms.
+// ---------------------------------------------------------------------------
+template <int BITS>
+__global__ void __launch_bounds__(128)
+k_radix_hist(const uint2* __restrict__ kv, int64_t n, int passes, uint32_t* hist) {
+  constexpr int BINS = 1 << BITS;
+  extern __shared__ uint32_t sh[];  // [4 warps][passes][BINS]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int per_warp = passes * BINS;
+  for (int i = threadIdx.x; i < 4 * per_warp; i += blockDim.x) sh[i] = 0;
   __syncthreads();
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i - threadIdx.x < n;
-       i += stride) {
-    const bool in = i < n;
-    const uint32_t k = in ? __ldg(keys + i) : 0u;
-    const unsigned active = __ballot_sync(0xffffffffu, in);
-    if (in) {
+  uint32_t* wh = sh + warp * per_warp;
+  constexpr int KU = 8;  // keys per lane in flight
+  const int64_t wstride = (int64_t)gridDim.x * 4 * 32 * KU;
+  for (int64_t base = ((int64_t)blockIdx.x * 4 + warp) * 32 * KU; base < n; base += wstride) {
+    uint32_t k[KU];
+#pragma unroll
+    for (int q = 0; q < KU; ++q) {
+      const int64_t i = base + q * 32 + lane;
+      k[q] = i < n ? __ldg(&kv[i].x) : 0u;
+    }
+#pragma unroll
+    for (int q = 0; q < KU; ++q) {
+      const int64_t i = base + q * 32 + lane;
+      const bool in = i < n;
+      const unsigned valid = __ballot_sync(0xffffffffu, in);
       for (int p = 0; p < passes; ++p) {
-        const uint32_t d = (k >> (p * kRadixBits)) & (kRadixBins - 1);
-        const unsigned peers = __match_any_sync(active, d);
-        if ((threadIdx.x & 31) == (unsigned)(__ffs(peers) - 1))
-          atomicAdd(&sh[p * kRadixBins + d], (uint32_t)__popc(peers));
+        const uint32_t d = (k[q] >> (p * BITS)) & (BINS - 1);
+        const unsigned peers = peers_of<BITS>(d, valid);
+        if (in && lane == __ffs(peers) - 1) wh[p * BINS + d] += __popc(peers);
+        __syncwarp();
       }
     }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < passes * kRadixBins; i += blockDim.x)
-    if (sh[i]) atomicAdd(hist + i, sh[i]);
+  for (int i = threadIdx.x; i < per_warp; i += blockDim.x) {
+    const uint32_t s = sh[i] + sh[per_warp + i] + sh[2 * per_warp + i] + sh[3 * per_warp + i];
+    if (s) atomicAdd(hist + i, s);
+  }
 }
 
+// ---------------------------------------------------------------------------
 // One digit pass.
+// ---------------------------------------------------------------------------
+template <int BITS>
 __global__ void __launch_bounds__(kSortThreads)
-k_onesweep(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
-           uint32_t* __restrict__ kout, uint32_t* __restrict__ vout, int64_t n, int shift,
+k_onesweep(const uint2* __restrict__ in, uint2* __restrict__ out, int64_t n, int shift,
            const uint32_t* __restrict__ hist, uint32_t* tile_counter,
            unsigned long long* status, uint32_t epoch) {
-  constexpr int NW = kSortThreads / 32;
-  __shared__ uint32_t s_tile;
-  __shared__ uint32_t warp_hist[NW][kRadixBins];
-  __shared__ uint32_t digit_base[kRadixBins];
-  __shared__ uint32_t scan_tmp[kRadixBins];
+  constexpr int BINS = 1 << BITS;
+  constexpr int DPT = BINS / kSortThreads;  // digits per thread (1 or 2)
+  extern __shared__ uint8_t smem_raw[];
+  uint2* stage = reinterpret_cast<uint2*>(smem_raw);                           // [kSortTile]
+  uint32_t* warp_hist = reinterpret_cast<uint32_t*>(stage + kSortTile);       // [NW][BINS]
+  uint32_t* digit_off = warp_hist + NW * BINS;                                  // [BINS]
+  uint32_t* s_misc = digit_off + BINS;                                          // [NW + 2]
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
-  for (int i = tid; i < NW * kRadixBins; i += kSortThreads) (&warp_hist[0][0])[i] = 0;
-  // exclusive scan of this pass's histogram (digit bases), Hillis-Steele in smem
-  scan_tmp[tid] = hist[tid];
+  if (tid == 0) s_misc[NW] = atomicAdd(tile_counter, 1u);
+  for (int i = tid; i < NW * BINS; i += kSortThreads) warp_hist[i] = 0;
   __syncthreads();
-  for (int off = 1; off < kRadixBins; off <<= 1) {
-    const uint32_t v = tid >= off ? scan_tmp[tid - off] : 0u;
-    __syncthreads();
-    scan_tmp[tid] += v;
-    __syncthreads();
-  }
-  const uint32_t hist_excl = scan_tmp[tid] - hist[tid];
-  const int64_t tile = s_tile;
-  const int64_t base = tile * kSortTile + (int64_t)warp * (kSortItems * 32);
+  const int64_t tile = s_misc[NW];
+  const int64_t tile0 = tile * kSortTile;
+  const int64_t base = tile0 + (int64_t)warp * (kSortItems * 32);
 
-  uint32_t k[kSortItems], v[kSortItems], r[kSortItems];
+  uint2 kv[kSortItems];
+  uint32_t r[kSortItems];
 #pragma unroll
   for (int i = 0; i < kSortItems; ++i) {
     const int64_t idx = base + i * 32 + lane;
-    if (idx < n) {
-      k[i] = __ldg(kin + idx);
-      v[i] = __ldg(vin + idx);
-    }
+    kv[i] = idx < n ? in[idx] : make_uint2(0u, 0u);
   }
   const unsigned lt = lanemask_lt();
+  uint32_t* wh = warp_hist + warp * BINS;
 #pragma unroll
   for (int i = 0; i < kSortItems; ++i) {
     const int64_t idx = base + i * 32 + lane;
-    const uint32_t d = idx < n ? ((k[i] >> shift) & (kRadixBins - 1)) : (uint32_t)kRadixBins;
-    const unsigned peers = __match_any_sync(0xffffffffu, d);
-    const uint32_t cur = d < kRadixBins ? warp_hist[warp][d] : 0u;
+    const bool ok = idx < n;
+    const unsigned valid = __ballot_sync(0xffffffffu, ok);
+    const uint32_t d = (kv[i].x >> shift) & (BINS - 1);
+    const unsigned peers = peers_of<BITS>(d, valid);
+    const uint32_t cur = ok ? wh[d] : 0u;
     r[i] = cur + __popc(peers & lt);
     __syncwarp();
-    if (d < kRadixBins && lane == __ffs(peers) - 1) warp_hist[warp][d] = cur + __popc(peers);
+    if (ok && lane == __ffs(peers) - 1) wh[d] = cur + __popc(peers);
     __syncwarp();
   }
   __syncthreads();
-  // per digit (thread tid = digit): exclusive prefix over warps, tile aggregate
-  uint32_t total = 0;
+
+  // per digit: exclusive prefix over warps (in place), tile total, and the tile's
+  // exclusive prefix over digits (its sorted-order layout)
+  uint32_t total[DPT], tile_excl[DPT];
 #pragma unroll
-  for (int w = 0; w < NW; ++w) {
-    const uint32_t c = warp_hist[w][tid];
-    warp_hist[w][tid] = total;
-    total += c;
+  for (int q = 0; q < DPT; ++q) {
+    const int dg = tid + q * kSortThreads;
+    uint32_t t = 0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      const uint32_t c = warp_hist[w * BINS + dg];
+      warp_hist[w * BINS + dg] = t;
+      t += c;
+    }
+    total[q] = t;
+    lb_publish(status, tile, BINS, dg, epoch, t);
   }
-  const uint32_t excl = lookback(status, tile, kRadixBins, tid, epoch, total);
-  digit_base[tid] = hist_excl + excl;
+  {
+    uint32_t carry = 0;
+#pragma unroll
+    for (int q = 0; q < DPT; ++q) {
+      uint32_t blk_total;
+      tile_excl[q] = carry + block_excl_scan(total[q], s_misc, &blk_total);
+      carry += blk_total;
+    }
+  }
+  // stage the tile in sorted order (overlaps the look-back of earlier tiles)
+#pragma unroll
+  for (int i = 0; i < kSortItems; ++i) {
+    const int64_t idx = base + i * 32 + lane;
+    if (idx < n) {
+      const uint32_t d = (kv[i].x >> shift) & (BINS - 1);
+      // tile_excl of digit d lives in the thread owning d; it is fetched below instead
+      r[i] += warp_hist[warp * BINS + d];
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < DPT; ++q) digit_off[tid + q * kSortThreads] = tile_excl[q];
   __syncthreads();
 #pragma unroll
   for (int i = 0; i < kSortItems; ++i) {
     const int64_t idx = base + i * 32 + lane;
     if (idx < n) {
-      const uint32_t d = (k[i] >> shift) & (kRadixBins - 1);
-      const uint32_t pos = digit_base[d] + warp_hist[warp][d] + r[i];
-      kout[pos] = k[i];
-      vout[pos] = v[i];
+      const uint32_t d = (kv[i].x >> shift) & (BINS - 1);
+      stage[digit_off[d] + r[i]] = kv[i];
     }
+  }
+  // global position of sorted-tile slot j with digit d: hist_excl[d] + prev[d] + (j - tile_excl[d])
+  uint32_t hist_excl[DPT];
+  {
+    uint32_t carry = 0;
+#pragma unroll
+    for (int q = 0; q < DPT; ++q) {
+      uint32_t blk_total;
+      hist_excl[q] = carry + block_excl_scan(hist[tid + q * kSortThreads], s_misc, &blk_total);
+      carry += blk_total;
+    }
+  }
+  uint32_t prev[DPT];
+#pragma unroll
+  for (int q = 0; q < DPT; ++q) prev[q] = lb_wait(status, tile, BINS, tid + q * kSortThreads, epoch, total[q]);
+  __syncthreads();  // stage complete; digit_off (tile_excl) no longer needed as such
+#pragma unroll
+  for (int q = 0; q < DPT; ++q) digit_off[tid + q * kSortThreads] = hist_excl[q] + prev[q] - tile_excl[q];
+  __syncthreads();
+  const int64_t cnt = n - tile0 < kSortTile ? n - tile0 : kSortTile;
+#pragma unroll 4
+  for (int j = tid; j < cnt; j += kSortThreads) {
+    const uint2 x = stage[j];
+    const uint32_t d = (x.x >> shift) & (BINS - 1);
+    out[digit_off[d] + j] = x;
   }
 }
 
-cudaError_t radix_sort_pairs(uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1, int64_t n,
-                             int bits, const SortWs& ws, uint32_t epoch, int* passes_out,
-                             bool* result_in_1, int64_t* launches, cudaStream_t s) {
-  const int passes = (bits + kRadixBits - 1) / kRadixBits;
+static size_t onesweep_smem(int bits) {
+  const int bins = 1 << bits;
+  return sizeof(uint2) * kSortTile + sizeof(uint32_t) * (NW * bins + bins + NW + 2);
+}
+
+cudaError_t radix_sort_pairs(uint2* kv0, uint2* kv1, int64_t n, int bits, const SortWs& ws,
+                             uint32_t epoch, int* passes_out, bool* result_in_1, int64_t* launches,
+                             cudaStream_t s) {
+  // digit width: 9 bits when it saves a pass (e.g. 27-bit Feed-1 keys: 3 passes, not 4)
+  const int dbits = (bits > 24 && bits <= 27) || (bits > 16 && bits <= 18) ? 9 : 8;
+  const int passes = (bits + dbits - 1) / dbits;
   *passes_out = passes;
   *result_in_1 = false;
   if (n == 0) return cudaSuccess;
-  // hist and counters are adjacent (api.cu carve-up): one memset for both
-  cudaError_t e = cudaMemsetAsync(ws.hist, 0, sizeof(uint32_t) * (kMaxPasses * kRadixBins + kMaxPasses + 2), s);
+  cudaError_t e = cudaMemsetAsync(ws.hist, 0, sizeof(uint32_t) * (kHistWords + kMaxPasses + 2), s);
   if (e != cudaSuccess) return e;
   if (passes == 0) return cudaSuccess;
   const int64_t tiles = (n + kSortTile - 1) / kSortTile;
   if (tiles > ws.max_tiles) return cudaErrorInvalidValue;
+  const int bins = 1 << dbits;
   {
-    int64_t want = (n + 255) / 256;
+    const int64_t want = (n + 128 * 8 - 1) / (128 * 8);
     const unsigned grid = (unsigned)(want < 148 * 8 ? want : 148 * 8);
-    k_radix_hist<<<grid, 256, 0, s>>>(k0, n, passes, ws.hist);
+    const size_t sm = sizeof(uint32_t) * 4 * passes * bins;
+    if (dbits == 9) k_radix_hist<9><<<grid, 128, sm, s>>>(kv0, n, passes, ws.hist);
+    else k_radix_hist<8><<<grid, 128, sm, s>>>(kv0, n, passes, ws.hist);
     ++*launches;
   }
-  uint32_t *ki = k0, *vi = v0, *ko = k1, *vo = v1;
+  const size_t sm = onesweep_smem(dbits);
+  static bool attr_set[2] = {false, false};
+  if (!attr_set[dbits - 8]) {
+    if (dbits == 9) cudaFuncSetAttribute(k_onesweep<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    else cudaFuncSetAttribute(k_onesweep<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    attr_set[dbits - 8] = true;
+  }
+  uint2 *a = kv0, *b = kv1;
   for (int p = 0; p < passes; ++p) {
-    k_onesweep<<<(unsigned)tiles, kSortThreads, 0, s>>>(ki, vi, ko, vo, n, p * kRadixBits,
-                                                         ws.hist + p * kRadixBins,
-                                                         ws.counters + p, ws.status, epoch + p);
+    if (dbits == 9)
+      k_onesweep<9><<<(unsigned)tiles, kSortThreads, sm, s>>>(a, b, n, p * 9, ws.hist + p * bins,
+                                                              ws.counters + p, ws.status, epoch + p);
+    else
+      k_onesweep<8><<<(unsigned)tiles, kSortThreads, sm, s>>>(a, b, n, p * 8, ws.hist + p * bins,
+                                                              ws.counters + p, ws.status, epoch + p);
     ++*launches;
-    uint32_t* t;
-    t = ki; ki = ko; ko = t;
-    t = vi; vi = vo; vo = t;
+    uint2* t = a; a = b; b = t;
   }
   *result_in_1 = (passes & 1) != 0;
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
 // Run-length encode of the sorted keys (single pass, decoupled look-back over tiles).
 // A "head" is the first occurrence of a key; the first sentinel (invalid) key is also a
 // head, so its position is U and seg[U] = n_valid.  Without sentinels the tile holding
-// item n-1 writes seg[U] = n.
+// item n-1 writes seg[U] = n.  Also records, for every segment-reduce chunk c, the
+// segment that contains occurrence c*kChunk (chunk_u0[c]).
+// ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kSortThreads)
-k_rle(const uint32_t* __restrict__ keys, int64_t n, uint32_t sentinel, uint32_t* unique,
-      uint32_t* seg, uint32_t* U_out, uint32_t* tile_counter, unsigned long long* status,
-      uint32_t epoch) {
-  constexpr int NW = kSortThreads / 32;
+k_rle(const uint2* __restrict__ kv, int64_t n, uint32_t sentinel, uint32_t* unique,
+      uint32_t* seg, uint32_t* U_out, uint32_t* chunk_u0, uint32_t* tile_counter,
+      unsigned long long* status, uint32_t epoch) {
   __shared__ uint32_t s_tile;
   __shared__ uint32_t s_warp[NW];
   __shared__ uint32_t s_excl;
@@ -227,8 +361,8 @@ k_rle(const uint32_t* __restrict__ keys, int64_t n, uint32_t sentinel, uint32_t*
     bool head = false;
     uint32_t k = 0;
     if (idx < n) {
-      k = __ldg(keys + idx);
-      head = (idx == 0) || (__ldg(keys + idx - 1) != k);
+      k = __ldg(&kv[idx].x);
+      head = (idx == 0) || (__ldg(&kv[idx - 1].x) != k);
     }
     kk[i] = k;
     ball[i] = __ballot_sync(0xffffffffu, head);
@@ -243,18 +377,21 @@ k_rle(const uint32_t* __restrict__ keys, int64_t n, uint32_t sentinel, uint32_t*
       s_warp[w] = t;
       t += c;
     }
-    s_excl = lookback(status, tile, kRadixBins, 0, epoch, t);
+    lb_publish(status, tile, kRadixBinsMax, 0, epoch, t);
+    s_excl = lb_wait(status, tile, kRadixBinsMax, 0, epoch, t);
   }
   __syncthreads();
   uint32_t pos = s_excl + s_warp[warp];
 #pragma unroll
   for (int i = 0; i < kSortItems; ++i) {
     const int64_t idx = base + i * 32 + lane;
-    if ((ball[i] >> lane) & 1u) {
-      const uint32_t p = pos + __popc(ball[i] & lt);
+    const bool head = (ball[i] >> lane) & 1u;
+    const uint32_t p = pos + __popc(ball[i] & lt);  // heads before idx
+    if (head) {
       if (kk[i] != sentinel) unique[p] = kk[i];
       seg[p] = (uint32_t)idx;
     }
+    if (idx < n && (idx % kChunk) == 0) chunk_u0[idx / kChunk] = p + (head ? 1u : 0u) - 1u;
     pos += __popc(ball[i]);
     if (idx == n - 1) {
       // pos now = number of heads in [0, n) (incl. the sentinel head if any)
@@ -266,13 +403,13 @@ k_rle(const uint32_t* __restrict__ keys, int64_t n, uint32_t sentinel, uint32_t*
   }
 }
 
-cudaError_t launch_rle(const uint32_t* keys, int64_t n, uint32_t sentinel, uint32_t* unique,
-                       uint32_t* seg, uint32_t* U_out, uint32_t* counter,
+cudaError_t launch_rle(const uint2* kv, int64_t n, uint32_t sentinel, uint32_t* unique,
+                       uint32_t* seg, uint32_t* U_out, uint32_t* chunk_u0, uint32_t* counter,
                        unsigned long long* status, uint32_t epoch, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   const int64_t tiles = (n + kSortTile - 1) / kSortTile;
-  k_rle<<<(unsigned)tiles, kSortThreads, 0, s>>>(keys, n, sentinel, unique, seg, U_out, counter,
-                                                 status, epoch);
+  k_rle<<<(unsigned)tiles, kSortThreads, 0, s>>>(kv, n, sentinel, unique, seg, U_out, chunk_u0,
+                                                 counter, status, epoch);
   return cudaGetLastError();
 }
 

@@ -1,0 +1,83 @@
+#!/usr/bin/env python
+"""Summarise an ncu report (--set full): per kernel launch, the numbers the roofline and the
+optimisation loop use.  Usage: python tools/ncu_summary.py report.ncu-rep [--out file.txt] [--json traffic.json]"""
+import csv
+import io
+import json
+import subprocess
+import sys
+
+METRICS = [
+    ("time_us", "gpu__time_duration.sum", "us"),
+    ("dram_rd_GB", "dram__bytes_read.sum", "GB"),
+    ("dram_wr_GB", "dram__bytes_write.sum", "GB"),
+    ("dram_%", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", 1),
+    ("l2_hit_%", "lts__t_sector_hit_rate.pct", 1),
+    ("occ_%", "sm__warps_active.avg.pct_of_peak_sustained_active", 1),
+    ("regs", "launch__registers_per_thread", 1),
+    ("issue_%", "sm__inst_issued.avg.pct_of_peak_sustained_active", 1),
+    ("xu_%", "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active", 1),
+    ("lsu_%", "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active", 1),
+    ("l1_wf_%", "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed", 1),
+    ("lts_%", "lts__t_sectors.avg.pct_of_peak_sustained_elapsed", 1),
+]
+STALLS = ["long_scoreboard", "short_scoreboard", "lg_throttle", "mio_throttle", "wait", "math_pipe_throttle",
+          "barrier", "membar", "no_instruction", "not_selected", "selected", "dispatch_stall", "tex_throttle",
+          "drain", "branch_resolving", "sleeping"]
+
+
+SCALE = {("us", "ns"): 1e-3, ("us", "us"): 1.0, ("us", "ms"): 1e3, ("us", "s"): 1e6,
+         ("GB", "byte"): 1e-9, ("GB", "Kbyte"): 1e-6, ("GB", "Mbyte"): 1e-3, ("GB", "Gbyte"): 1.0,
+         ("GB", "Tbyte"): 1e3}
+
+
+def load(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    return rows[0], rows[1], rows[2:]
+
+
+def main():
+    rep = sys.argv[1]
+    h, units, rows = load(rep)
+    ki = h.index("Kernel Name")
+    lines, traffic = [], {}
+    hdr = f"{'kernel':38s} " + " ".join(f"{n:>10s}" for n, _, _ in METRICS)
+    lines.append(hdr)
+    for r in rows:
+        name = r[ki].split("(")[0].replace("void ", "").replace("lirank::", "")[:38]
+        vals = []
+        for n, m, sc in METRICS:
+            try:
+                i = h.index(m)
+                f = SCALE.get((sc, units[i]), 1.0) if isinstance(sc, str) else sc
+                vals.append(float(r[i].replace(",", "")) * f)
+            except (ValueError, IndexError):
+                vals.append(float("nan"))
+        lines.append(f"{name:38s} " + " ".join(f"{v:10.3f}" for v in vals))
+        st = []
+        for s in STALLS:
+            m = f"smsp__average_warps_issue_stalled_{s}_per_issue_active.ratio"
+            if m in h:
+                try:
+                    v = float(r[h.index(m)].replace(",", ""))
+                    if v > 0.5:
+                        st.append(f"{s}={v:.1f}")
+                except ValueError:
+                    pass
+        if st:
+            lines.append(f"{'':38s}   stalls(cycles/issue): " + " ".join(st))
+        key = name.split("<")[0]
+        rd = vals[1] + vals[2]
+        traffic.setdefault(key, []).append(rd * 1e9)
+    text = "\n".join(lines)
+    print(text)
+    if "--out" in sys.argv:
+        open(sys.argv[sys.argv.index("--out") + 1], "w").write(f"# ncu summary of {rep}\n" + text + "\n")
+    if "--json" in sys.argv:
+        j = {k: {"dram_bytes_per_launch": sum(v) / len(v), "launches": len(v)} for k, v in traffic.items()}
+        json.dump(j, open(sys.argv[sys.argv.index("--json") + 1], "w"), indent=1)
+
+
+if __name__ == "__main__":
+    main()
