@@ -114,13 +114,13 @@ typedef struct {
   int64_t weights_bytes;    /* fp32 [local_rows][row_pitch]                                    */
   int64_t accum_bytes;      /* fp32 [local_rows] (row-wise) or [local_rows][row_pitch]         */
   int64_t q8_codes_bytes;   /* q8 rows [local_rows][q8_pitch] (0 without EMB_F_Q8), each row =
-                               [D int8 codes][pad to 8][fp32 middle][fp32 scale][pad to 16] so a
-                               row is one contiguous request (D=64: 80 B)                       */
+                               [D int8 codes][pad to 8][fp32 middle][fp32 scale][pad to 32]: one
+                               contiguous run of whole 32-B sectors (D=64: 96 B)                       */
   int64_t q8_meta_bytes;    /* 0 (metadata lives in the q8 rows; kept for ABI stability)       */
   int64_t workspace_bytes;  /* library scratch (staging, sort, segment partials, scalars)      */
   int64_t local_rows;       /* rows stored on this rank (sum over its local tables)            */
   int32_t row_pitch;        /* floats per stored fp32 row: round_up(D, 4) (16-B aligned rows)  */
-  int32_t q8_pitch;         /* bytes per q8 row: round_up(round_up(D, 8) + 8, 16)              */
+  int32_t q8_pitch;         /* bytes per q8 row: round_up(round_up(D, 8) + 8, 32)              */
 } emb_sizes;
 
 typedef struct {

@@ -84,7 +84,9 @@ emb_status make_plan(const emb_config* c, Plan* p) {
   p->D = c->dim;
   p->F = c->num_features;
   p->pitch = (int)round_up(c->dim, 4);
-  p->qpitch = (int)round_up(round_up(c->dim, 8) + 8, 16);  // [codes][pad][middle,scale][pad]
+  // q8 row: [codes][pad to 8][middle, scale][pad to 32]: whole 32-B sectors, so the
+  // fused re-quantize never partially writes a sector (no L2 fill reads)
+  p->qpitch = (int)round_up(round_up(c->dim, 8) + 8, 32);
   p->pooling = c->pooling;
   p->mode = c->adagrad_mode;
   p->sharding = c->world_size > 1 ? c->sharding : EMB_SHARD_NONE;

@@ -499,7 +499,7 @@ k_adagrad(const uint32_t* __restrict__ unique, const uint32_t* __restrict__ Up,
           const float* __restrict__ G, const float* __restrict__ clip, float* __restrict__ Wt,
           float* __restrict__ A, int pitch, int D, float lr, float eps,
           uint8_t* __restrict__ codes, int qpitch, int meta_off, uint32_t* status) {
-  constexpr int R = 2;
+  constexpr int R = VPL >= 4 ? 1 : 2;
   const float c = *clip;
   if (c < 0.0f) return;  // non-finite global norm: skip the step (uniform over the grid)
   const uint32_t U = *Up;
@@ -617,6 +617,36 @@ k_adagrad(const uint32_t* __restrict__ unique, const uint32_t* __restrict__ Up,
     else { constexpr int L_ = 32, V_ = 8; KERNEL_LAUNCH; }                  \
   } while (0)
 
+static Geom geom_target(int pitch, int target);
+
+#define LIRANK_GEOM4_DISPATCH(G, KERNEL_LAUNCH)                             \
+  do {                                                                      \
+    if ((G).lpb == 1) {                                                     \
+      if ((G).vpl == 1) { constexpr int L_ = 1, V_ = 1; KERNEL_LAUNCH; }    \
+      else if ((G).vpl == 2) { constexpr int L_ = 1, V_ = 2; KERNEL_LAUNCH; } \
+      else { constexpr int L_ = 1, V_ = 4; KERNEL_LAUNCH; }                 \
+    } else if ((G).lpb == 2) { constexpr int L_ = 2, V_ = 4; KERNEL_LAUNCH; } \
+    else if ((G).lpb == 4) { constexpr int L_ = 4, V_ = 4; KERNEL_LAUNCH; } \
+    else if ((G).lpb == 8) { constexpr int L_ = 8, V_ = 4; KERNEL_LAUNCH; } \
+    else if ((G).lpb == 16) { constexpr int L_ = 16, V_ = 4; KERNEL_LAUNCH; } \
+    else if ((G).vpl <= 4) { constexpr int L_ = 32, V_ = 4; KERNEL_LAUNCH; } \
+    else { constexpr int L_ = 32, V_ = 8; KERNEL_LAUNCH; }                  \
+  } while (0)
+
+#define LIRANK_GEOM2_DISPATCH(G, KERNEL_LAUNCH)                             \
+  do {                                                                      \
+    if ((G).lpb == 1) {                                                     \
+      if ((G).vpl == 1) { constexpr int L_ = 1, V_ = 1; KERNEL_LAUNCH; }    \
+      else { constexpr int L_ = 1, V_ = 2; KERNEL_LAUNCH; }                 \
+    } else if ((G).lpb == 2) { constexpr int L_ = 2, V_ = 2; KERNEL_LAUNCH; } \
+    else if ((G).lpb == 4) { constexpr int L_ = 4, V_ = 2; KERNEL_LAUNCH; } \
+    else if ((G).lpb == 8) { constexpr int L_ = 8, V_ = 2; KERNEL_LAUNCH; } \
+    else if ((G).lpb == 16) { constexpr int L_ = 16, V_ = 2; KERNEL_LAUNCH; } \
+    else if ((G).vpl <= 2) { constexpr int L_ = 32, V_ = 2; KERNEL_LAUNCH; } \
+    else if ((G).vpl <= 4) { constexpr int L_ = 32, V_ = 4; KERNEL_LAUNCH; } \
+    else { constexpr int L_ = 32, V_ = 8; KERNEL_LAUNCH; }                  \
+  } while (0)
+
 static unsigned persistent_grid(int64_t groups, int lpb) {
   // 148 SMs x 8 resident 256-thread CTAs
   const int64_t want = (groups * lpb + 255) / 256;
@@ -626,12 +656,12 @@ static unsigned persistent_grid(int64_t groups, int lpb) {
 
 cudaError_t launch_segreduce(const BwdArgs& a, int64_t* launches, cudaStream_t s) {
   if (a.nnz == 0) return cudaSuccess;
-  const Geom g = geom_for(a.pitch);
+  const Geom g = geom_target(a.pitch, 2);  // D=64: 8 lanes x 2 float4 per occurrence
   cudaError_t e = cudaMemsetAsync(a.owner_count, 0, 2 * sizeof(uint32_t), s);
   if (e != cudaSuccess) return e;
   const unsigned grid = (unsigned)((a.chunks * g.lpb + 255) / 256);
 #define LAUNCH_SR(MEAN)                                                                     \
-  LIRANK_GEOM_DISPATCH(g, (k_segreduce<L_, V_, MEAN><<<grid, 256, 0, s>>>(                 \
+  LIRANK_GEOM2_DISPATCH(g, (k_segreduce<L_, V_, MEAN><<<grid, 256, 0, s>>>(                \
                               a.seg, a.U, a.kv, a.chunk_u0, a.grad, a.offsets, a.B, a.F, a.D, \
                               a.pitch, a.chunks, a.G, a.part_first, a.part_last, a.norm_main, \
                               a.norm_fix, a.owner_list, a.owner_count)))
@@ -641,7 +671,7 @@ cudaError_t launch_segreduce(const BwdArgs& a, int64_t* launches, cudaStream_t s
   uint32_t* long_count = a.owner_count + 1;
   uint32_t* long_list = a.owner_list + a.chunks;  // [2 * chunks] after the owner list
   const unsigned fgrid = persistent_grid(a.chunks, g.lpb);
-  LIRANK_GEOM_DISPATCH(g, (k_fixup_short<L_, V_><<<fgrid, 256, 0, s>>>(
+  LIRANK_GEOM2_DISPATCH(g, (k_fixup_short<L_, V_><<<fgrid, 256, 0, s>>>(
                               a.seg, a.U, a.pitch, a.part_first, a.part_last, a.owner_list,
                               a.owner_count, a.G, a.norm_fix, long_list, long_count)));
   ++*launches;
@@ -667,7 +697,7 @@ cudaError_t launch_norm_finalize(const double* parts, int nparts, const BwdArgs&
 
 cudaError_t launch_adagrad(const BwdArgs& a, cudaStream_t s) {
   if (a.nnz == 0) return cudaSuccess;
-  const Geom g = geom_for(a.pitch);
+  const Geom g = geom_for(a.pitch);  // D=64: 16 lanes x 1 float4 per row (measured best)
   const unsigned grid = persistent_grid(a.nnz, g.lpb);
 #define LAUNCH_AG(RW, RQ)                                                                   \
   LIRANK_GEOM_DISPATCH(g, (k_adagrad<L_, V_, RW, RQ><<<grid, 256, 0, s>>>(                 \
@@ -683,13 +713,15 @@ cudaError_t launch_adagrad(const BwdArgs& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-// Quantize geometry: aim for 4 float4 vectors per lane (D=64: 4 lanes per row).
-static Geom quant_geom(int pitch) {
+// Geometry with about `target` float4 vectors per lane (fewer lanes per row: cheaper
+// per-row reductions and more rows in flight per warp).
+static Geom geom_target(int pitch, int target) {
   const int nvec = pitch / 4;
   int lpb = 1;
-  while (lpb * 4 < nvec && lpb < 32) lpb <<= 1;
+  while (lpb * target < nvec && lpb < 32) lpb <<= 1;
   return Geom{lpb, (nvec + lpb - 1) / lpb};
 }
+static Geom quant_geom(int pitch) { return geom_target(pitch, 4); }
 
 cudaError_t launch_quantize(const float* W, int pitch, int64_t rows, int D, uint8_t* codes,
                             int qpitch, int meta_off, uint32_t* status, cudaStream_t s) {

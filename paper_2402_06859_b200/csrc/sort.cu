@@ -7,8 +7,7 @@
 //
 // Design (B200): "onesweep" LSD radix sort over packed 8-byte {key, bag} pairs.
 // * One upfront histogram kernel computes the digit histograms of every pass in a single
-//   read of the keys (ballot-matched digits counted into per-warp private shared-memory
-//   histograms: no atomics in the loop; shared atomics are slow on this part).
+//   read of the keys (per-warp private shared-memory histograms).
 // * ONE kernel per digit pass (8- or 9-bit digits: 27-bit Feed-1 keys take 3 passes):
 //   a 4096-pair tile is loaded with coalesced 8-B loads and ranked in registers (warp
 //   multisplit by ballots, stable in index order), the tile's digit counts are published
@@ -120,7 +119,9 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp
 }  // namespace
 
 // ---------------------------------------------------------------------------
-// Upfront histogram of every digit pass.  128-thread CTAs, per-warp private histograms.
+// Upfront histogram of every digit pass.  128-thread CTAs, per-warp private shared
+// histograms (shared atomics; a private copy per warp keeps Zipf-hot digits from
+// serialising a whole CTA), 8 keys per lane in flight.
 // ---------------------------------------------------------------------------
 template <int BITS>
 __global__ void __launch_bounds__(128)
@@ -143,15 +144,9 @@ k_radix_hist(const uint2* __restrict__ kv, int64_t n, int passes, uint32_t* hist
     }
 #pragma unroll
     for (int q = 0; q < KU; ++q) {
-      const int64_t i = base + q * 32 + lane;
-      const bool in = i < n;
-      const unsigned valid = __ballot_sync(0xffffffffu, in);
-      for (int p = 0; p < passes; ++p) {
-        const uint32_t d = (k[q] >> (p * BITS)) & (BINS - 1);
-        const unsigned peers = peers_of<BITS>(d, valid);
-        if (in && lane == __ffs(peers) - 1) wh[p * BINS + d] += __popc(peers);
-        __syncwarp();
-      }
+      if (base + q * 32 + lane < n)
+        for (int p = 0; p < passes; ++p)
+          atomicAdd(&wh[p * BINS + ((k[q] >> (p * BITS)) & (BINS - 1))], 1u);
     }
   }
   __syncthreads();

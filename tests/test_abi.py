@@ -67,9 +67,9 @@ def test_plan_sizes():
     cfg, keep = make_cfg([100, 50], 30, [0, 1, 0], flags=L.EMB_F_Q8)
     code, s = plan(cfg)
     assert code == 0
-    assert s.row_pitch == 32 and s.q8_pitch == 48 and s.local_rows == 150  # 30 codes+2 pad+8 meta+8 pad
+    assert s.row_pitch == 32 and s.q8_pitch == 64 and s.local_rows == 150  # 30 codes+2 pad+8 meta, to 32 B
     assert s.weights_bytes == 150 * 32 * 4 and s.accum_bytes == 150 * 4
-    assert s.q8_codes_bytes == 150 * 48 and s.q8_meta_bytes == 0
+    assert s.q8_codes_bytes == 150 * 64 and s.q8_meta_bytes == 0
     assert s.workspace_bytes > 0 and s.workspace_bytes % 256 == 0
     cfg.adagrad_mode = 1
     assert plan(cfg)[1].accum_bytes == 150 * 32 * 4
