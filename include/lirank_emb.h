@@ -84,6 +84,11 @@ enum { EMB_SHARD_NONE = 0, EMB_SHARD_TABLE = 1, EMB_SHARD_ROW = 2 };
 #define EMB_F_REQUANT 2u  /* (needs EMB_F_Q8) every AdaGrad update also re-quantizes the rows
                              it touched, so the q8 store tracks the fp32 tables between
                              full emb_quantize_mm8() passes                                   */
+#define EMB_F_LOOPBACK 4u /* (world_size > 1) TEST TRANSPORT: the ranks are threads of one
+                             process sharing one device; cfg.nccl_unique_id is the hub from
+                             emb_loopback_hub_create().  Every collective becomes a host
+                             rendezvous + stream-ordered device copies (no kernel waits on
+                             another rank).  Same exchange code path as NCCL otherwise.       */
 
 typedef struct {
   uint32_t abi_version;          /* must be EMB_ABI_VERSION                                    */
@@ -150,8 +155,21 @@ EMB_API emb_status emb_plan(const emb_config* cfg, emb_sizes* out);
 EMB_API emb_status emb_local_layout(const emb_config* cfg, int64_t* local_base, int64_t* row_lo,
                             int64_t* row_hi);
 
+/* Multi-GPU bootstrap (host-only).  Rank 0 calls emb_nccl_unique_id and distributes the
+ * 128 bytes (e.g. a torch.distributed broadcast); every rank passes them as
+ * cfg.nccl_unique_id.  NCCL is loaded at run time (libnccl.so.2, the copy PyTorch ships);
+ * EMB_ENCCL if it is unavailable.  The loopback hub (EMB_F_LOOPBACK) is for tests. */
+EMB_API emb_status emb_nccl_unique_id(void* out128);
+EMB_API emb_status emb_loopback_hub_create(int32_t world, void** hub);
+EMB_API emb_status emb_loopback_hub_destroy(void* hub);
+
 /* Bind buffers, fill the accumulators with init_accumulator, clear the status word, and
- * (world_size > 1) create the NCCL communicator.  Enqueued on cfg.stream. */
+ * (world_size > 1) create the communicator.  Enqueued on cfg.stream.
+ * Sharded configurations (world_size > 1): every rank passes its own local batch B (the
+ * same B on all ranks) to emb_forward; rows are exchanged with their owners (a1), pooled
+ * there and returned (a3: table-wise all-to-all, row-wise reduce-scatter of partial sums),
+ * and gradients flow back (a4) to the owners' a5-a8.  MEAN pooling is not supported when
+ * sharded (EMB_EINVAL). */
 EMB_API emb_status emb_create(const emb_config* cfg, const emb_buffers* buf, emb_t* out);
 
 /* a2 (+ a1/a3 when sharded).  ids: int32 [nnz] feature-major, offsets: int32 [F*B+1]

@@ -5,6 +5,6 @@ this package is its thin binding.  It never imports ``oracle/`` and has no CPU
 fallback: without the library or a CUDA device, compute calls raise.
 """
 from ._lib import EmbError, load  # noqa: F401
-from .embedding import ShardedEmbedding  # noqa: F401
+from .embedding import LoopbackHub, ShardedEmbedding, nccl_unique_id  # noqa: F401
 
-__all__ = ["ShardedEmbedding", "EmbError", "load"]
+__all__ = ["ShardedEmbedding", "LoopbackHub", "nccl_unique_id", "EmbError", "load"]

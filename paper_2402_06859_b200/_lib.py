@@ -15,7 +15,7 @@ EMB_ABI_VERSION = 1
 EMB_POOL_SUM, EMB_POOL_MEAN = 0, 1
 EMB_ADAGRAD_ROWWISE, EMB_ADAGRAD_ELEMENTWISE = 0, 1
 EMB_SHARD_NONE, EMB_SHARD_TABLE, EMB_SHARD_ROW = 0, 1, 2
-EMB_F_Q8, EMB_F_REQUANT = 1, 2
+EMB_F_Q8, EMB_F_REQUANT, EMB_F_LOOPBACK = 1, 2, 4
 PHASES = ["fwd", "sort", "rle", "segreduce", "norm", "update", "fwd_q8", "quantize", "copy", "exchange"]
 
 STATUS = {0: "EMB_OK", 1: "EMB_EINVAL", 2: "EMB_ENOMEM", 3: "EMB_ECUDA", 4: "EMB_ENCCL",
@@ -91,6 +91,9 @@ SIGNATURES = {
     "emb_last_dedup": (C.c_int, [P, P, P, C.c_int64, P, C.c_int64, P, P]),
     "emb_last_stats": (C.c_int, [P, P, P, P]),
     "emb_kernel_launches": (C.c_int64, [P]),
+    "emb_nccl_unique_id": (C.c_int, [P]),
+    "emb_loopback_hub_create": (C.c_int, [C.c_int32, P]),
+    "emb_loopback_hub_destroy": (C.c_int, [P]),
     "emb_profile": (C.c_int, [P, C.c_int32]),
     "emb_profile_read": (C.c_int, [P, P, P, C.c_int32]),
     "emb_destroy": (C.c_int, [P]),

@@ -23,8 +23,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",
          "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr",
          "-I", os.path.join(ROOT, "include")]
-SOURCES = ["forward.cu", "sort.cu", "backward.cu", "api.cu", "comm.cu"]
-HEADERS = ["common.cuh", "kernels.h", "comm.h"]
+SOURCES = ["forward.cu", "sort.cu", "backward.cu", "exchange.cu", "api.cu", "comm.cu"]
+HEADERS = ["common.cuh", "kernels.h", "comm.h", "handle.h", "lookback.cuh"]
 
 
 def _newest(paths):
@@ -53,7 +53,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
                 raise RuntimeError(f"nvcc failed for {cmd[-3]}")
     if force or jobs or not os.path.exists(LIB) or os.path.getmtime(LIB) < _newest(objs):
         cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs,
-               "-Xlinker", "--exclude-libs,ALL"]
+               "-Xlinker", "--exclude-libs,ALL", "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)

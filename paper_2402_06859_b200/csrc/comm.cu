@@ -1,26 +1,231 @@
-// comm.cu -- multi-GPU exchange.  Round-1 state: the sharded path is not built yet;
-// world_size > 1 handles are refused at emb_create (EMB_ENCCL) and the exchange entry
-// points return EMB_EINVAL.
+// comm.cu -- NCCL and loopback transports for the sharded exchange (see comm.h).
 #include "comm.h"
+
+#include <dlfcn.h>
+#include <string.h>
+
+#include <condition_variable>
+#include <mutex>
+#include <vector>
 
 namespace lirank {
 
-struct Comm {
-  int rank = 0, world = 1;
+// ---------------------------------------------------------------------------
+// NCCL (dlopen'ed: the library has no link-time NCCL dependency; inside a PyTorch process
+// this binds to the already-loaded torch NCCL, 2.28.x).  Types/values of nccl.h (2.x ABI).
+// ---------------------------------------------------------------------------
+namespace nccl {
+typedef struct { char internal[128]; } UniqueId;
+typedef void* Comm;
+typedef int Result;                  // ncclSuccess = 0
+enum { kUint8 = 1, kFloat32 = 7 };   // ncclUint8, ncclFloat32
+enum { kSum = 0 };                   // ncclSum
+struct Api {
+  Result (*GetUniqueId)(UniqueId*) = nullptr;
+  Result (*CommInitRank)(Comm*, int, UniqueId, int) = nullptr;
+  Result (*CommDestroy)(Comm) = nullptr;
+  Result (*GroupStart)() = nullptr;
+  Result (*GroupEnd)() = nullptr;
+  Result (*Send)(const void*, size_t, int, int, Comm, cudaStream_t) = nullptr;
+  Result (*Recv)(void*, size_t, int, int, Comm, cudaStream_t) = nullptr;
+  Result (*AllGather)(const void*, void*, size_t, int, Comm, cudaStream_t) = nullptr;
+  Result (*ReduceScatter)(const void*, void*, size_t, int, int, Comm, cudaStream_t) = nullptr;
+  bool ok = false;
+};
+static Api& api() {
+  static Api a = [] {
+    Api x;
+    void* lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!lib) return x;
+    x.GetUniqueId = (Result(*)(UniqueId*))dlsym(lib, "ncclGetUniqueId");
+    x.CommInitRank = (Result(*)(Comm*, int, UniqueId, int))dlsym(lib, "ncclCommInitRank");
+    x.CommDestroy = (Result(*)(Comm))dlsym(lib, "ncclCommDestroy");
+    x.GroupStart = (Result(*)())dlsym(lib, "ncclGroupStart");
+    x.GroupEnd = (Result(*)())dlsym(lib, "ncclGroupEnd");
+    x.Send = (Result(*)(const void*, size_t, int, int, Comm, cudaStream_t))dlsym(lib, "ncclSend");
+    x.Recv = (Result(*)(void*, size_t, int, int, Comm, cudaStream_t))dlsym(lib, "ncclRecv");
+    x.AllGather = (Result(*)(const void*, void*, size_t, int, Comm, cudaStream_t))dlsym(lib, "ncclAllGather");
+    x.ReduceScatter =
+        (Result(*)(const void*, void*, size_t, int, int, Comm, cudaStream_t))dlsym(lib, "ncclReduceScatter");
+    x.ok = x.GetUniqueId && x.CommInitRank && x.CommDestroy && x.GroupStart && x.GroupEnd &&
+           x.Send && x.Recv && x.AllGather && x.ReduceScatter;
+    return x;
+  }();
+  return a;
+}
+}  // namespace nccl
+
+struct NcclTransport : Transport {
+  nccl::Comm comm = nullptr;
+  int world = 1;
+  ~NcclTransport() override {
+    if (comm) nccl::api().CommDestroy(comm);
+  }
+  bool allgather(const void* send, void* recv, size_t bytes, cudaStream_t s) override {
+    return nccl::api().AllGather(send, recv, bytes, nccl::kUint8, comm, s) == 0;
+  }
+  bool reduce_scatter_f32(const float* send, float* recv, size_t count, cudaStream_t s) override {
+    return nccl::api().ReduceScatter(send, recv, count, nccl::kFloat32, nccl::kSum, comm, s) == 0;
+  }
+  bool alltoallv(const void* send, const size_t* soff, const size_t* sbytes, void* recv,
+                 const size_t* roff, const size_t* rbytes, cudaStream_t s) override {
+    auto& a = nccl::api();
+    if (a.GroupStart() != 0) return false;
+    bool ok = true;
+    for (int r = 0; r < world; ++r) {
+      if (sbytes[r]) ok &= a.Send((const uint8_t*)send + soff[r], sbytes[r], nccl::kUint8, r, comm, s) == 0;
+      if (rbytes[r]) ok &= a.Recv((uint8_t*)recv + roff[r], rbytes[r], nccl::kUint8, r, comm, s) == 0;
+    }
+    ok &= a.GroupEnd() == 0;
+    return ok;
+  }
 };
 
-Comm* comm_create(const void*, int, int) { return nullptr; }
-void comm_destroy(Comm* c) { delete c; }
-bool comm_allgather_f64(Comm*, const double*, double*, cudaStream_t) { return false; }
-void carve_exchange(int, int, int, int64_t, int64_t, int64_t, int, uint8_t*, int64_t*,
-                    ExchangeWs* x) {
-  x->bytes = 0;
+bool nccl_get_unique_id(void* out128) {
+  auto& a = nccl::api();
+  if (!a.ok) return false;
+  nccl::UniqueId id;
+  if (a.GetUniqueId(&id) != 0) return false;
+  memcpy(out128, &id, sizeof(id));
+  return true;
+}
+
+Transport* make_nccl_transport(const void* unique_id, int rank, int world) {
+  auto& a = nccl::api();
+  if (!a.ok || !unique_id) return nullptr;
+  nccl::UniqueId id;
+  memcpy(&id, unique_id, sizeof(id));
+  auto* t = new NcclTransport();
+  t->world = world;
+  if (a.CommInitRank(&t->comm, world, id, rank) != 0) {
+    t->comm = nullptr;
+    delete t;
+    return nullptr;
+  }
+  return t;
+}
+
+// ---------------------------------------------------------------------------
+// Loopback: W ranks = W threads of one process on one device.
+// ---------------------------------------------------------------------------
+namespace {
+
+struct Slot {
+  const void* send = nullptr;
+  const size_t* soff = nullptr;
+  const size_t* sbytes = nullptr;
+  cudaEvent_t ready = nullptr;
+  cudaEvent_t done = nullptr;
+};
+
+struct Hub {
+  int world;
+  std::mutex m;
+  std::condition_variable cv;
+  int arrived = 0;
+  int64_t gen = 0;
+  std::vector<Slot> slots;
+  explicit Hub(int w) : world(w), slots(w) {}
+  void barrier() {
+    std::unique_lock<std::mutex> lk(m);
+    const int64_t g = gen;
+    if (++arrived == world) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != g; });
+    }
+  }
+};
+
+__global__ void k_add_f32(float* __restrict__ dst, const float* __restrict__ src, size_t n) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    dst[i] = __fadd_rn(dst[i], src[i]);
+}
+
+struct LoopbackTransport : Transport {
+  Hub* hub;
+  int rank;
+  cudaEvent_t ready = nullptr, done = nullptr;
+  LoopbackTransport(Hub* h, int r) : hub(h), rank(r) {
+    cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&done, cudaEventDisableTiming);
+  }
+  ~LoopbackTransport() override {
+    cudaEventDestroy(ready);
+    cudaEventDestroy(done);
+  }
+  // phase 1: publish + barrier; caller issues its reads; phase 2: done + barriers.
+  void publish(const void* send, const size_t* soff, const size_t* sbytes, cudaStream_t s) {
+    Slot& me = hub->slots[rank];
+    me.send = send;
+    me.soff = soff;
+    me.sbytes = sbytes;
+    cudaEventRecord(ready, s);
+    me.ready = ready;
+    me.done = done;
+    hub->barrier();
+  }
+  void finish(cudaStream_t s) {
+    cudaEventRecord(done, s);
+    hub->barrier();
+    for (int r = 0; r < hub->world; ++r)
+      if (r != rank) cudaStreamWaitEvent(s, hub->slots[r].done, 0);
+    hub->barrier();
+  }
+  bool allgather(const void* send, void* recv, size_t bytes, cudaStream_t s) override {
+    publish(send, nullptr, nullptr, s);
+    bool ok = true;
+    for (int r = 0; r < hub->world; ++r) {
+      ok &= cudaStreamWaitEvent(s, hub->slots[r].ready, 0) == cudaSuccess;
+      ok &= cudaMemcpyAsync((uint8_t*)recv + r * bytes, hub->slots[r].send, bytes,
+                            cudaMemcpyDeviceToDevice, s) == cudaSuccess;
+    }
+    finish(s);
+    return ok;
+  }
+  bool reduce_scatter_f32(const float* send, float* recv, size_t count, cudaStream_t s) override {
+    publish(send, nullptr, nullptr, s);
+    bool ok = true;
+    for (int r = 0; r < hub->world; ++r) {  // rank order: deterministic sum
+      ok &= cudaStreamWaitEvent(s, hub->slots[r].ready, 0) == cudaSuccess;
+      const float* src = (const float*)hub->slots[r].send + (size_t)rank * count;
+      if (r == 0) {
+        ok &= cudaMemcpyAsync(recv, src, count * sizeof(float), cudaMemcpyDeviceToDevice, s) == cudaSuccess;
+      } else if (count) {
+        k_add_f32<<<148 * 4, 256, 0, s>>>(recv, src, count);
+        ok &= cudaGetLastError() == cudaSuccess;
+      }
+    }
+    finish(s);
+    return ok;
+  }
+  bool alltoallv(const void* send, const size_t* soff, const size_t* sbytes, void* recv,
+                 const size_t* roff, const size_t* rbytes, cudaStream_t s) override {
+    publish(send, soff, sbytes, s);
+    bool ok = true;
+    for (int r = 0; r < hub->world; ++r) {
+      const Slot& src = hub->slots[r];
+      const size_t n = src.sbytes[rank];
+      ok &= n == rbytes[r];
+      ok &= cudaStreamWaitEvent(s, src.ready, 0) == cudaSuccess;
+      if (n)
+        ok &= cudaMemcpyAsync((uint8_t*)recv + roff[r], (const uint8_t*)src.send + src.soff[rank], n,
+                              cudaMemcpyDeviceToDevice, s) == cudaSuccess;
+    }
+    finish(s);
+    return ok;
+  }
+};
+
+}  // namespace
+
+void* loopback_hub_create(int world) { return world >= 1 ? new Hub(world) : nullptr; }
+void loopback_hub_destroy(void* hub) { delete (Hub*)hub; }
+Transport* make_loopback_transport(void* hub, int rank) {
+  if (!hub) return nullptr;
+  return new LoopbackTransport((Hub*)hub, rank);
 }
 
 }  // namespace lirank
-
-emb_status exchange_forward(emb_t, const int32_t*, const int32_t*, int32_t, int64_t, float*,
-                            bool) {
-  return EMB_EINVAL;
-}
-emb_status exchange_backward(emb_t, const float*, float, double) { return EMB_EINVAL; }

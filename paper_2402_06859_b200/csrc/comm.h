@@ -1,30 +1,39 @@
-// comm.h -- multi-GPU exchange (a1/a3/a4) for world_size > 1.
+// comm.h -- transports of the sharded exchange (a1/a3/a4 and the norm exchange).
+//
+// Two implementations behind one interface:
+// * NcclTransport: NCCL (torch's libnccl.so.2, dlopen'ed) over NVLink/NVSwitch, one rank
+//   per GPU, communicator created from a 128-B ncclUniqueId the caller distributes.
+// * LoopbackTransport: W ranks as W host threads of ONE process (test transport): every
+//   collective is a host rendezvous plus cudaMemcpyAsync between the ranks' buffers,
+//   ordered with CUDA events (no kernel ever waits on another rank's kernel).
+// All calls enqueue on the caller's stream and are collective (same order on all ranks).
 #pragma once
 
 #include <cuda_runtime.h>
+#include <stddef.h>
 #include <stdint.h>
-
-#include "../../include/lirank_emb.h"
 
 namespace lirank {
 
-struct Comm;
-
-// Device buffers of the sharded exchange, carved from the workspace.
-struct ExchangeWs {
-  int64_t bytes = 0;
+struct Transport {
+  virtual ~Transport() {}
+  // recv[r * bytes .. (r+1) * bytes) = send of rank r.
+  virtual bool allgather(const void* send, void* recv, size_t bytes, cudaStream_t s) = 0;
+  // recv[0..count) = sum over ranks r of send_r[rank * count ..], fp32.
+  virtual bool reduce_scatter_f32(const float* send, float* recv, size_t count, cudaStream_t s) = 0;
+  // to every rank r: sbytes[r] bytes from send + soff[r]; from every rank r: rbytes[r]
+  // bytes into recv + roff[r] (sizes must match pairwise; host arrays of length world).
+  virtual bool alltoallv(const void* send, const size_t* soff, const size_t* sbytes, void* recv,
+                         const size_t* roff, const size_t* rbytes, cudaStream_t s) = 0;
 };
 
-Comm* comm_create(const void* nccl_unique_id, int rank, int world);
-void comm_destroy(Comm* c);
-// dst[r] = src of rank r (one double per rank), enqueued on s.
-bool comm_allgather_f64(Comm* c, const double* src, double* dst, cudaStream_t s);
+// NCCL: returns nullptr (and a reason) if libnccl.so.2 cannot be loaded or init fails.
+Transport* make_nccl_transport(const void* unique_id, int rank, int world);
+bool nccl_get_unique_id(void* out128);
 
-void carve_exchange(int world, int F, int max_batch, int64_t max_nnz, int64_t nnz_cap,
-                    int64_t bags_cap, int D, uint8_t* base, int64_t* off, ExchangeWs* x);
+// Loopback hub shared by the W in-process ranks.
+void* loopback_hub_create(int world);
+void loopback_hub_destroy(void* hub);
+Transport* make_loopback_transport(void* hub, int rank);
 
 }  // namespace lirank
-
-emb_status exchange_forward(emb_t h, const int32_t* ids, const int32_t* offsets, int32_t batch,
-                            int64_t nnz, float* out, bool q8);
-emb_status exchange_backward(emb_t h, const float* grad_out, float lr, double extra_sq_norm);

@@ -1,0 +1,393 @@
+// exchange.cu -- the sharded path: a1 bucketize + ids exchange, a3 pooled exchange, a4 grad
+// exchange ("Each embedding table is placed on a GPU, and each GPU's input
+// batch is all-to-all'ed so that every GPU receives the input columns belonging to its
+// embedding table.  Each GPU does its local embedding lookup, and the lookups are
+// all-to-all'ed to return the output to the GPU that the input column came from.").
+//
+// Rank r holds a local batch of B samples (feature-major ids/offsets, like W=1).
+//   a1: every occurrence goes to the owner of its row (table-wise: owner[t];
+//       row-wise: id / ceil(rows/W)), already translated to the owner's stored-row key.
+//       Per destination the message is [features of that owner][B] bag lengths + the keys
+//       in (feature, sample, bag) order -- built by count -> exclusive scan -> stable
+//       scatter, then one count exchange (the only host sync of the step) and two
+//       all-to-alls (keys: variable sizes; lengths: sizes fixed by the plan).
+//   owner: pools every source's bags with the a2 kernel into [src][B][Fr][D] and records
+//       the {key, grad row} pairs for its backward.
+//   a3: table-wise: all-to-all of the pooled blocks back + a column permute into
+//       [B][F][D]; row-wise (every owner holds a slice of every table): reduce-scatter of
+//       the per-owner partial sums lands [B][F][D] directly.
+//   a4: the transpose (table-wise all-to-all of grad blocks; row-wise all-gather), then
+//       the owner's local a5-a8; the global norm sums one fp64 per rank in rank order.
+#include "handle.h"
+#include "lookback.cuh"
+
+namespace lirank {
+
+namespace {
+
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 16;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+// Exclusive scan of n uint32 (one pass, decoupled look-back); out[n] = total.
+__global__ void __launch_bounds__(kScanThreads)
+k_scan_excl(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, int64_t n,
+            uint32_t* tile_counter, unsigned long long* status, uint32_t epoch) {
+  __shared__ uint32_t s_tile, s_warp[kScanThreads / 32], s_excl;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
+  __syncthreads();
+  const int64_t tile = s_tile;
+  const int64_t base = tile * kScanTile + (int64_t)tid * kScanItems;  // blocked per thread
+  uint32_t v[kScanItems], sum = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    v[i] = base + i < n ? __ldg(in + base + i) : 0u;
+    sum += v[i];
+  }
+  uint32_t x = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_warp[warp] = x;
+  __syncthreads();
+  if (tid == 0) {
+    uint32_t t = 0;
+    for (int w = 0; w < kScanThreads / 32; ++w) {
+      const uint32_t c = s_warp[w];
+      s_warp[w] = t;
+      t += c;
+    }
+    lb_publish(status, tile, kRadixBinsMax, 0, epoch, t);
+    s_excl = lb_wait(status, tile, kRadixBinsMax, 0, epoch, t);
+  }
+  __syncthreads();
+  uint32_t run = s_excl + s_warp[warp] + x - sum;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    if (base + i < n) out[base + i] = run;
+    if (base + i == n - 1) out[n] = run + v[i];
+    run += v[i];
+  }
+}
+
+// a1 count: ids of bag (f, b) per destination rank -> lens[dest_base[o]*B + j*B + b].
+__global__ void k_bucket_count(const int* __restrict__ ids, const int* __restrict__ offsets, int B,
+                               int F, int W, const FeatMeta* __restrict__ meta,
+                               const int32_t* __restrict__ owner0, const int32_t* __restrict__ blk,
+                               const int32_t* __restrict__ jmap, const int32_t* __restrict__ dest_base,
+                               uint32_t* __restrict__ lens, uint32_t* status) {
+  const int64_t bag = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (bag >= (int64_t)F * B) return;
+  const int f = (int)(bag / B), b = (int)(bag - (int64_t)f * B);
+  const int rows = meta[f].rows, o0 = owner0[f], bk = blk[f];
+  uint32_t cnt[kMaxWorld];
+#pragma unroll
+  for (int o = 0; o < kMaxWorld; ++o) cnt[o] = 0;
+  bool bad = false;
+  for (int j = __ldg(offsets + bag), e = __ldg(offsets + bag + 1); j < e; ++j) {
+    const int id = __ldg(ids + j);
+    if (id < 0 || id >= rows) { bad = true; continue; }
+    const int o = o0 + id / bk;
+#pragma unroll
+    for (int q = 0; q < kMaxWorld; ++q) cnt[q] += (q == o);
+  }
+  if (bad) atomicOr(status, kStIdRange);
+#pragma unroll
+  for (int o = 0; o < kMaxWorld; ++o) {
+    if (o >= W) break;
+    const int jj = jmap[o * F + f];
+    if (jj >= 0) lens[((int64_t)dest_base[o] + jj) * B + b] = cnt[o];
+  }
+}
+
+// a1 scatter: keys (owner-local stored rows) into the send buffer, stable per bag.
+__global__ void k_bucket_scatter(const int* __restrict__ ids, const int* __restrict__ offsets, int B,
+                                 int F, int W, const FeatMeta* __restrict__ meta,
+                                 const int32_t* __restrict__ owner0, const int32_t* __restrict__ blk,
+                                 const int32_t* __restrict__ jmap, const int32_t* __restrict__ dest_base,
+                                 const int64_t* __restrict__ key_base, const uint32_t* __restrict__ pos,
+                                 uint32_t* __restrict__ send_keys) {
+  const int64_t bag = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (bag >= (int64_t)F * B) return;
+  const int f = (int)(bag / B), b = (int)(bag - (int64_t)f * B);
+  const int rows = meta[f].rows, o0 = owner0[f], bk = blk[f];
+  uint32_t p[kMaxWorld];
+#pragma unroll
+  for (int o = 0; o < kMaxWorld; ++o) {
+    const int jj = o < W ? jmap[o * F + f] : -1;
+    p[o] = jj >= 0 ? pos[((int64_t)dest_base[o] + jj) * B + b] : 0u;
+  }
+  for (int j = __ldg(offsets + bag), e = __ldg(offsets + bag + 1); j < e; ++j) {
+    const int id = __ldg(ids + j);
+    if (id < 0 || id >= rows) continue;
+    const int o = o0 + id / bk;
+    const uint32_t key = (uint32_t)(key_base[(int64_t)o * F + f] + (id - (int64_t)(o - o0) * bk));
+    uint32_t at = 0;
+#pragma unroll
+    for (int q = 0; q < kMaxWorld; ++q)
+      if (q == o) { at = p[q]; p[q] = at + 1; }
+    send_keys[at] = key;
+  }
+}
+
+// per-destination send counts from the scanned lengths
+__global__ void k_send_counts(const uint32_t* __restrict__ pos, const int32_t* __restrict__ dest_base,
+                              int W, int B, uint32_t* __restrict__ cnt) {
+  const int o = threadIdx.x;
+  if (o < W) cnt[o] = pos[(int64_t)dest_base[o + 1] * B] - pos[(int64_t)dest_base[o] * B];
+}
+
+// table-wise a3: out[b][f] = recv block of owner(f) at [b][j(f)]  (and the a4 transpose)
+template <bool TO_OUT>
+__global__ void k_permute(float* __restrict__ dense, float* __restrict__ blocks, int B, int F, int D,
+                          const int32_t* __restrict__ fmap) {
+  const int64_t total = (int64_t)B * F * D;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / D;
+    const int d = (int)(i - row * D);
+    const int b = (int)(row / F), f = (int)(row - (int64_t)b * F);
+    const int64_t src = ((int64_t)fmap[3 * f] + (int64_t)b * fmap[3 * f + 1] + fmap[3 * f + 2]) * D + d;
+    if (TO_OUT) dense[i] = blocks[src];
+    else blocks[src] = dense[i];
+  }
+}
+
+emb_status scan(emb_t h, const uint32_t* in, uint32_t* out, int64_t n, int which) {
+  CK(cudaMemsetAsync(h->x.scan_counter + which, 0, sizeof(uint32_t), h->stream));
+  if (n == 0) return cudaMemsetAsync(out, 0, sizeof(uint32_t), h->stream) == cudaSuccess ? EMB_OK : EMB_ECUDA;
+  const int64_t tiles = (n + kScanTile - 1) / kScanTile;
+  k_scan_excl<<<(unsigned)tiles, kScanThreads, 0, h->stream>>>(in, out, n, h->x.scan_counter + which,
+                                                               h->sort.status, h->epoch);
+  h->epoch += 1;
+  h->launches += 1;
+  return cudaGetLastError() == cudaSuccess ? EMB_OK : EMB_ECUDA;
+}
+
+}  // namespace
+
+void carve_exchange(const Plan& p, Carver& cv, ExchangeWs* x) {
+  const int64_t W = p.world, B = p.max_batch, F = p.F, Fr = p.Fr, D = p.D;
+  const int64_t Ltot = B * p.dest_base[W];
+  x->lens = cv.take<uint32_t>(Ltot);
+  x->pos = cv.take<uint32_t>(Ltot + 1);
+  x->send_keys = cv.take<uint32_t>(p.max_nnz);
+  x->cnt = cv.take<uint32_t>(W + W * W);
+  x->recv_lens = cv.take<uint32_t>(W * Fr * B);
+  x->recv_off = cv.take<uint32_t>(W * Fr * B + 1);
+  x->recv_keys = cv.take<uint32_t>(p.recv_nnz_cap);
+  x->pooled = cv.take<float>(W * B * Fr * D);
+  x->xdense = cv.take<float>(B * F * D);
+  x->ident = cv.take<FeatMeta>(W * Fr);
+  x->d_jmap = cv.take<int32_t>(W * F);
+  x->d_fmap = cv.take<int32_t>(3 * F);
+  x->d_feats_by_dest = cv.take<int32_t>(F);
+  x->d_dest_base = cv.take<int32_t>(W + 1);
+  x->d_key_base = cv.take<int64_t>(W * F);
+  x->d_owner0 = cv.take<int32_t>(F);
+  x->d_blk = cv.take<int32_t>(F);
+  x->scan_counter = cv.take<uint32_t>(4);
+}
+
+emb_status exchange_init(emb_t h) {
+  const Plan& p = h->p;
+  const int W = p.world, F = p.F;
+  std::vector<FeatMeta> ident((size_t)W * p.Fr);
+  for (auto& m : ident) { m.base = 0; m.rows = 0x7fffffff; m.lo = 0; m.hi = 0x7fffffff; m.pad = 0; }
+  std::vector<int32_t> fmap(3 * F, 0);
+  if (p.sharding == EMB_SHARD_TABLE)
+    for (int f = 0; f < F; ++f) {
+      const int o = p.owner[p.feature_table[f]];
+      fmap[3 * f] = 0;  // filled with B at use (dest_base * B), see exchange_forward
+      fmap[3 * f + 1] = p.Fo[o];
+      fmap[3 * f + 2] = p.jmap[(size_t)o * F + f];
+    }
+  const ExchangeWs& x = h->x;
+  CK(cudaMemcpyAsync(x.ident, ident.data(), sizeof(FeatMeta) * ident.size(), cudaMemcpyHostToDevice, h->stream));
+  CK(cudaMemcpyAsync(x.d_jmap, p.jmap.data(), 4 * p.jmap.size(), cudaMemcpyHostToDevice, h->stream));
+  CK(cudaMemcpyAsync(x.d_dest_base, p.dest_base.data(), 4 * p.dest_base.size(), cudaMemcpyHostToDevice, h->stream));
+  CK(cudaMemcpyAsync(x.d_key_base, p.key_base.data(), 8 * p.key_base.size(), cudaMemcpyHostToDevice, h->stream));
+  CK(cudaMemcpyAsync(x.d_owner0, p.owner0.data(), 4 * p.owner0.size(), cudaMemcpyHostToDevice, h->stream));
+  CK(cudaMemcpyAsync(x.d_blk, p.blk.data(), 4 * p.blk.size(), cudaMemcpyHostToDevice, h->stream));
+  CK(cudaMemcpyAsync(x.d_fmap, fmap.data(), 4 * fmap.size(), cudaMemcpyHostToDevice, h->stream));
+  CK(cudaStreamSynchronize(h->stream));  // host vectors go out of scope
+  return EMB_OK;
+}
+
+// fmap[3f] must hold dest_base(owner(f)) * B for the current B (B may change per call).
+static emb_status upload_fmap(emb_t h, int B) {
+  if (h->fmap_B == B) return EMB_OK;
+  h->fmap_B = B;
+  const Plan& p = h->p;
+  const int F = p.F;
+  std::vector<int32_t> fmap(3 * F);
+  for (int f = 0; f < F; ++f) {
+    const int o = p.owner[p.feature_table[f]];
+    fmap[3 * f] = p.dest_base[o] * B;
+    fmap[3 * f + 1] = p.Fo[o];
+    fmap[3 * f + 2] = p.jmap[(size_t)o * F + f];
+  }
+  CK(cudaMemcpyAsync(h->x.d_fmap, fmap.data(), 4 * fmap.size(), cudaMemcpyHostToDevice, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  return EMB_OK;
+}
+
+emb_status exchange_forward(emb_t h, const Staged& st, int32_t batch, int64_t nnz, bool q8) {
+  const Plan& p = h->p;
+  const ExchangeWs& x = h->x;
+  const int W = p.world, F = p.F, Fr = p.Fr, D = p.D, B = batch, r = p.rank;
+  const int64_t Ltot = (int64_t)B * p.dest_base[W];
+  const unsigned bag_grid = (unsigned)(((int64_t)F * B + 255) / 256);
+  emb_status s;
+  int64_t n_recv = 0;
+  {
+    Phase ph(h->prof, h->stream, EMB_PH_EXCHANGE);
+    // ---- a1: bucketize -----------------------------------------------------------------
+    if (F * (int64_t)B > 0) {
+      k_bucket_count<<<bag_grid, 256, 0, h->stream>>>(st.ids, st.offsets, B, F, W, h->d_meta, x.d_owner0,
+                                                      x.d_blk, x.d_jmap, x.d_dest_base, x.lens, h->d_status);
+      h->launches += 1;
+      CK(cudaGetLastError());
+    }
+    if ((s = scan(h, x.lens, x.pos, Ltot, 0)) != EMB_OK) return s;
+    if (F * (int64_t)B > 0) {
+      k_bucket_scatter<<<bag_grid, 256, 0, h->stream>>>(st.ids, st.offsets, B, F, W, h->d_meta, x.d_owner0,
+                                                        x.d_blk, x.d_jmap, x.d_dest_base, x.d_key_base,
+                                                        x.pos, x.send_keys);
+      h->launches += 1;
+    }
+    k_send_counts<<<1, 32, 0, h->stream>>>(x.pos, x.d_dest_base, W, B, x.cnt);
+    h->launches += 1;
+    CK(cudaGetLastError());
+    // one count exchange + host read: the only host sync of the step
+    if (!h->comm->allgather(x.cnt, x.cnt + W, sizeof(uint32_t) * W, h->stream)) return EMB_ENCCL;
+    h->h_cnt.resize((size_t)W * W);
+    CK(cudaMemcpyAsync(h->h_cnt.data(), x.cnt + W, 4ull * W * W, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    std::vector<size_t> soff(W), sb(W), roff(W), rb(W);
+    size_t so = 0, ro = 0;
+    for (int o = 0; o < W; ++o) {
+      sb[o] = 4ull * h->h_cnt[(size_t)r * W + o];
+      soff[o] = so;
+      so += sb[o];
+      rb[o] = 4ull * h->h_cnt[(size_t)o * W + r];
+      roff[o] = ro;
+      ro += rb[o];
+    }
+    n_recv = (int64_t)(ro / 4);
+    if (n_recv > p.recv_nnz_cap) return EMB_ENOMEM;
+    if (!h->comm->alltoallv(x.send_keys, soff.data(), sb.data(), x.recv_keys, roff.data(), rb.data(), h->stream))
+      return EMB_ENCCL;
+    // bag lengths: [Fo x B] to each owner; [Fr x B] from each source
+    for (int o = 0; o < W; ++o) {
+      soff[o] = 4ull * p.dest_base[o] * B;
+      sb[o] = 4ull * p.Fo[o] * B;
+      roff[o] = 4ull * o * Fr * B;
+      rb[o] = 4ull * Fr * B;
+    }
+    if (!h->comm->alltoallv(x.lens, soff.data(), sb.data(), x.recv_lens, roff.data(), rb.data(), h->stream))
+      return EMB_ENCCL;
+    if ((s = scan(h, x.recv_lens, x.recv_off, (int64_t)W * Fr * B, 1)) != EMB_OK) return s;
+  }
+  // ---- owner: pool every source's bags into [src][B][Fr][D] -------------------------------
+  if (!q8) {
+    FwdArgs a;
+    memset(&a, 0, sizeof(a));
+    a.W = h->W;
+    a.pitch = p.pitch;
+    a.ids = (const int*)x.recv_keys;
+    a.offsets = (const int*)x.recv_off;
+    a.B = B;
+    a.F = W * Fr;
+    a.Fb = Fr;
+    a.D = D;
+    a.meta = x.ident;
+    a.out = x.pooled;
+    a.kv_out = h->kvA;
+    a.sentinel = (uint32_t)p.local_rows;
+    a.status = h->d_status;
+    Phase ph(h->prof, h->stream, EMB_PH_FWD);
+    CK(launch_pool_fwd_f32(a, h->stream));
+  } else {
+    FwdQ8Args a;
+    memset(&a, 0, sizeof(a));
+    a.codes = h->codes;
+    a.qpitch = p.qpitch;
+    a.meta_off = h->q8_meta_off;
+    a.ids = (const int*)x.recv_keys;
+    a.offsets = (const int*)x.recv_off;
+    a.B = B;
+    a.F = W * Fr;
+    a.Fb = Fr;
+    a.D = D;
+    a.meta = x.ident;
+    a.out = x.pooled;
+    a.status = h->d_status;
+    Phase ph(h->prof, h->stream, EMB_PH_FWD_Q8);
+    CK(launch_pool_fwd_q8(a, h->stream));
+  }
+  h->launches += (int64_t)W * Fr * B > 0;
+  // ---- a3: pooled exchange back ----------------------------------------------------------
+  {
+    Phase ph(h->prof, h->stream, EMB_PH_EXCHANGE);
+    if (p.sharding == EMB_SHARD_ROW) {
+      if (!h->comm->reduce_scatter_f32(x.pooled, st.out, (size_t)B * F * D, h->stream)) return EMB_ENCCL;
+    } else {
+      std::vector<size_t> soff(W), sb(W), roff(W), rb(W);
+      for (int o = 0; o < W; ++o) {
+        soff[o] = 4ull * o * B * Fr * D;
+        sb[o] = 4ull * B * Fr * D;
+        roff[o] = 4ull * p.dest_base[o] * B * D;
+        rb[o] = 4ull * p.Fo[o] * B * D;
+      }
+      if (!h->comm->alltoallv(x.pooled, soff.data(), sb.data(), x.xdense, roff.data(), rb.data(), h->stream))
+        return EMB_ENCCL;
+      if ((s = upload_fmap(h, B)) != EMB_OK) return s;
+      if ((int64_t)B * F * D > 0) {
+        k_permute<true><<<148 * 8, 256, 0, h->stream>>>(st.out, x.xdense, B, F, D, x.d_fmap);
+        h->launches += 1;
+        CK(cudaGetLastError());
+      }
+    }
+  }
+  if (!q8) {
+    h->have_fwd = true;
+    h->fwd_nnz = n_recv;
+    h->fwd_B = B;
+  }
+  return EMB_OK;
+}
+
+emb_status exchange_backward(emb_t h, const float* grad_dev) {
+  const Plan& p = h->p;
+  const ExchangeWs& x = h->x;
+  const int W = p.world, F = p.F, Fr = p.Fr, D = p.D, B = h->fwd_B;
+  {
+    Phase ph(h->prof, h->stream, EMB_PH_EXCHANGE);
+    if (p.sharding == EMB_SHARD_ROW) {
+      if (!h->comm->allgather(grad_dev, x.pooled, 4ull * B * F * D, h->stream)) return EMB_ENCCL;
+    } else {
+      if ((int64_t)B * F * D > 0) {
+        k_permute<false><<<148 * 8, 256, 0, h->stream>>>(const_cast<float*>(grad_dev), x.xdense, B, F, D,
+                                                         x.d_fmap);
+        h->launches += 1;
+        CK(cudaGetLastError());
+      }
+      std::vector<size_t> soff(W), sb(W), roff(W), rb(W);
+      for (int o = 0; o < W; ++o) {
+        soff[o] = 4ull * p.dest_base[o] * B * D;
+        sb[o] = 4ull * p.Fo[o] * B * D;
+        roff[o] = 4ull * o * B * Fr * D;
+        rb[o] = 4ull * B * Fr * D;
+      }
+      if (!h->comm->alltoallv(x.xdense, soff.data(), sb.data(), x.pooled, roff.data(), rb.data(), h->stream))
+        return EMB_ENCCL;
+    }
+  }
+  return EMB_OK;
+}
+
+}  // namespace lirank

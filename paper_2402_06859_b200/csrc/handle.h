@@ -1,0 +1,204 @@
+// handle.h -- internal: the plan, the handle, and helpers shared by api.cu and exchange.cu.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "../../include/lirank_emb.h"
+#include "comm.h"
+#include "common.cuh"
+#include "kernels.h"
+
+namespace lirank {
+
+constexpr int64_t kAlign = 256;
+constexpr int kMaxWorld = 16;
+
+inline int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+// Bump allocator over the caller's workspace; with base == nullptr it only sizes.
+struct Carver {
+  uint8_t* base;
+  int64_t off = 0;
+  explicit Carver(void* b) : base((uint8_t*)b) {}
+  template <class T>
+  T* take(int64_t count) {
+    off = round_up(off, kAlign);
+    T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+    off += (int64_t)sizeof(T) * std::max<int64_t>(count, 1);
+    return p;
+  }
+};
+
+// Where the rows of every table live on one rank.
+struct Layout {
+  std::vector<int64_t> local_base, row_lo, row_hi;  // per table (-1 base: not stored here)
+  int64_t local_rows = 0;
+};
+
+struct Plan {
+  int T = 0, D = 0, F = 0, pitch = 0, qpitch = 0;
+  int pooling = 0, mode = 0, sharding = 0, rank = 0, world = 1;
+  uint32_t flags = 0;
+  float A0 = 0.f, eps = 0.f, max_norm = 0.f;
+  int64_t max_nnz = 0;
+  int max_batch = 0;
+  std::vector<int64_t> table_rows, local_base, row_lo, row_hi;  // this rank's layout
+  std::vector<int32_t> feature_table, owner;                    // owner: table-wise plan
+  int64_t local_rows = 0;
+  int key_bits = 0;
+  // ---- sharded exchange (world > 1), identical on every rank --------------------------
+  std::vector<Layout> layouts;              // [world]
+  std::vector<std::vector<int>> feats_of;   // [world]: features whose table has rows there
+  std::vector<int> Fo;                      // [world] = feats_of[o].size()
+  std::vector<int> dest_base;               // [world+1]: prefix of Fo (units of B bags)
+  std::vector<int32_t> jmap;                // [world][F]: index of f in feats_of[o] or -1
+  std::vector<int64_t> key_base;            // [world][F]: local base of t(f) on o or -1
+  std::vector<int32_t> owner0, blk;         // [F]: owner(id) = owner0 + id / blk
+  int Fr = 0;                               // = Fo[rank]
+  int64_t recv_nnz_cap = 0;                 // occurrences this rank may pool per step
+  int64_t owner_bags_cap = 0;               // bags this rank may pool per step
+};
+
+emb_status make_plan(const emb_config* c, Plan* p);
+
+// CUDA-event phase profiler (emb_profile / emb_profile_read).
+struct Prof {
+  bool on = false;
+  struct Rec { int ph; cudaEvent_t a, b; };
+  std::vector<Rec> pending;
+  std::vector<cudaEvent_t> pool;
+  double ms[EMB_PH_COUNT] = {};
+  int64_t n[EMB_PH_COUNT] = {};
+  cudaEvent_t get() {
+    if (!pool.empty()) { cudaEvent_t e = pool.back(); pool.pop_back(); return e; }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+  }
+  ~Prof() {
+    for (auto& r : pending) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+    for (auto e : pool) cudaEventDestroy(e);
+  }
+};
+
+// RAII phase marker: records a start event now and an end event at scope exit.
+struct Phase {
+  Prof* pr;
+  cudaStream_t s;
+  int ph;
+  cudaEvent_t a = nullptr;
+  Phase(Prof& p, cudaStream_t st, int phase) : pr(p.on ? &p : nullptr), s(st), ph(phase) {
+    if (pr) { a = pr->get(); cudaEventRecord(a, s); }
+  }
+  ~Phase() {
+    if (pr) {
+      cudaEvent_t b = pr->get();
+      cudaEventRecord(b, s);
+      pr->pending.push_back({ph, a, b});
+    }
+  }
+};
+
+// Device buffers of the sharded exchange (carved from the workspace when world > 1).
+struct ExchangeWs {
+  uint32_t* lens = nullptr;       // [sum_o Fo * B] ids per (dest, feature, sample)
+  uint32_t* pos = nullptr;        // [.. + 1] exclusive scan of lens = send positions
+  uint32_t* send_keys = nullptr;  // [max_nnz] owner-local row keys, grouped by dest
+  uint32_t* cnt = nullptr;        // [world] send counts, then [world][world] all counts
+  uint32_t* recv_lens = nullptr;  // [world * Fr * B]
+  uint32_t* recv_off = nullptr;   // [world * Fr * B + 1]
+  uint32_t* recv_keys = nullptr;  // [recv_nnz_cap]
+  float* pooled = nullptr;        // [world][B][Fr][D]: owner partials / owner grads
+  float* xdense = nullptr;        // [B][F][D]: table-wise return / grad send blocks
+  FeatMeta* ident = nullptr;      // [world * Fr] identity metas for the owner's pooling
+  int32_t* d_jmap = nullptr;      // [world][F]
+  int32_t* d_fmap = nullptr;      // [F][3]: {dest_base(owner) * B, Fo(owner), j} (table-wise)
+  int32_t* d_feats_by_dest = nullptr;  // [F]: feats_of concatenated by dest (table-wise)
+  int32_t* d_dest_base = nullptr;      // [world+1]
+  int64_t* d_key_base = nullptr;       // [world][F]
+  int32_t* d_owner0 = nullptr;         // [F]
+  int32_t* d_blk = nullptr;            // [F]
+  uint32_t* scan_counter = nullptr;    // [4] tile counters of the exchange scans
+};
+
+}  // namespace lirank
+
+struct emb_handle {
+  lirank::Plan p;
+  lirank::Prof prof;
+  cudaStream_t stream = nullptr;
+  float* W = nullptr;
+  float* A = nullptr;
+  uint8_t* codes = nullptr;
+  int q8_meta_off = 0;  // byte offset of {middle, scale} inside a q8 row
+  // workspace
+  lirank::FeatMeta* d_meta = nullptr;
+  int* stage_ids = nullptr;
+  int* stage_off = nullptr;
+  float* stage_dense = nullptr;
+  int* off_copy = nullptr;
+  uint2 *kvA = nullptr, *kvB = nullptr;  // {row key, grad row} per occurrence (sort ping-pong)
+  uint32_t* chunk_u0 = nullptr;
+  lirank::SortWs sort{};
+  uint32_t* unique = nullptr;
+  uint32_t* seg = nullptr;
+  uint32_t* d_U = nullptr;
+  float* G = nullptr;
+  double *part_first = nullptr, *part_last = nullptr, *norm_main = nullptr, *norm_fix = nullptr;
+  uint32_t* owner_list = nullptr;
+  uint32_t* owner_count = nullptr;
+  int64_t chunks_cap = 0;
+  double* S_parts = nullptr;  // [world]
+  double* S_local = nullptr;
+  double* S_global = nullptr;
+  float* d_clip = nullptr;
+  uint32_t* d_status = nullptr;
+  // sharded exchange
+  lirank::ExchangeWs x{};
+  lirank::Transport* comm = nullptr;
+  std::vector<uint32_t> h_cnt;  // [world][world] counts of the last forward
+  int fmap_B = -1;              // batch the table-wise permute map was uploaded for
+  // state
+  bool have_fwd = false;
+  bool have_q8 = false;
+  int64_t fwd_nnz = 0;  // occurrences recorded (pooled on this rank) by the last forward
+  int fwd_B = 0;        // local batch of the last forward
+  const uint2* sorted_kv = nullptr;
+  uint32_t epoch = 1;
+  int64_t launches = 0;
+};
+
+namespace lirank {
+
+bool is_device_ptr(const void* ptr);
+inline bool aligned(const void* ptr, uintptr_t a) { return ((uintptr_t)ptr % a) == 0; }
+
+#define CK(x)                                  \
+  do {                                         \
+    cudaError_t e_ = (x);                      \
+    if (e_ != cudaSuccess) return EMB_ECUDA;   \
+  } while (0)
+
+struct Staged {
+  const int* ids;
+  const int* offsets;
+  float* out;
+  bool host_out;
+};
+emb_status stage_inputs(emb_t h, const int32_t* ids, const int32_t* offsets, int32_t batch,
+                        int64_t nnz, float* out, Staged* s);
+
+// a5-a8 on this rank's recorded occurrences (see api.cu).
+emb_status backward_local(emb_t h, const float* grad_dev, float lr, double extra);
+
+// sharded forward / backward (exchange.cu)
+emb_status exchange_forward(emb_t h, const Staged& st, int32_t batch, int64_t nnz, bool q8);
+emb_status exchange_backward(emb_t h, const float* grad_dev);
+void carve_exchange(const Plan& p, Carver& cv, ExchangeWs* x);
+emb_status exchange_init(emb_t h);  // upload the exchange maps (emb_create)
+
+}  // namespace lirank

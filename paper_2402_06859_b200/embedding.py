@@ -18,6 +18,35 @@ def _ptr(t: Optional[torch.Tensor]):
     return None if t is None else C.c_void_p(t.data_ptr())
 
 
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id (rank 0 creates it; every rank passes it to the constructor)."""
+    lib = L.load()
+    buf = C.create_string_buffer(128)
+    L.check(lib.emb_nccl_unique_id(buf), "emb_nccl_unique_id")
+    return buf.raw
+
+
+class LoopbackHub:
+    """Test transport: W ranks as W threads of one process on one device (EMB_F_LOOPBACK)."""
+
+    def __init__(self, world: int):
+        self.lib = L.load()
+        self.ptr = C.c_void_p()
+        L.check(self.lib.emb_loopback_hub_create(int(world), C.byref(self.ptr)), "emb_loopback_hub_create")
+        self.world = world
+
+    def close(self):
+        if self.ptr.value:
+            self.lib.emb_loopback_hub_destroy(self.ptr)
+            self.ptr = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def _arr(a, ctype):
     a = np.ascontiguousarray(a)
     return a, a.ctypes.data_as(C.POINTER(ctype))
@@ -37,7 +66,8 @@ class ShardedEmbedding:
                  max_norm: float = 1.0, q8: bool = False, requant: bool = False,
                  device: Optional[torch.device] = None, stream: Optional[torch.cuda.Stream] = None,
                  rank: int = 0, world_size: int = 1, sharding: str = "none",
-                 table_owner: Optional[Sequence[int]] = None, nccl_unique_id: Optional[bytes] = None):
+                 table_owner: Optional[Sequence[int]] = None, nccl_unique_id: Optional[bytes] = None,
+                 loopback_hub: Optional["LoopbackHub"] = None):
         self.lib = L.load()
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
@@ -50,8 +80,13 @@ class ShardedEmbedding:
         if table_owner is not None:
             self._owner, owner_p = _arr(np.asarray(table_owner, dtype=np.int32), C.c_int32)
         self._uid = None
+        uid_ptr = None
         if nccl_unique_id is not None:
             self._uid = C.create_string_buffer(bytes(nccl_unique_id), len(nccl_unique_id))
+            uid_ptr = C.cast(self._uid, C.c_void_p)
+        self._hub = loopback_hub
+        if loopback_hub is not None:
+            uid_ptr = loopback_hub.ptr
         self.cfg = L.EmbConfig(
             abi_version=L.EMB_ABI_VERSION, num_tables=len(self.table_rows), table_rows=rows_p,
             dim=self.dim, num_features=self.num_features, feature_table=ft_p,
@@ -61,9 +96,10 @@ class ShardedEmbedding:
             max_nnz=int(max_nnz), max_batch=int(max_batch),
             sharding={"none": L.EMB_SHARD_NONE, "table": L.EMB_SHARD_TABLE, "row": L.EMB_SHARD_ROW}[sharding],
             table_owner=owner_p, rank=rank, world_size=world_size,
-            nccl_unique_id=C.cast(self._uid, C.c_void_p) if self._uid is not None else None,
+            nccl_unique_id=uid_ptr,
             stream=C.c_void_p(self.stream.cuda_stream),
-            flags=(L.EMB_F_Q8 if (q8 or requant) else 0) | (L.EMB_F_REQUANT if requant else 0))
+            flags=(L.EMB_F_Q8 if (q8 or requant) else 0) | (L.EMB_F_REQUANT if requant else 0)
+            | (L.EMB_F_LOOPBACK if loopback_hub is not None else 0))
         self.sizes = L.EmbSizes()
         L.check(self.lib.emb_plan(C.byref(self.cfg), C.byref(self.sizes)), "emb_plan")
         s = self.sizes

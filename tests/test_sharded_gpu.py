@@ -1,0 +1,164 @@
+"""Sharded path (a1/a3/a4) on one GPU through the loopback transport: W ranks
+as W threads of this process, each with its own handle and stream, exchanging through the
+same exchange code as NCCL (only the transport differs).  Results must equal the unsharded
+oracle on the global batch: forward per rank (table-wise bit-exact: each bag is pooled by
+one owner in bag order; row-wise within the pooled gate: partial sums from several owners),
+dedup/update per owner within the update gates."""
+import threading
+
+import numpy as np
+import pytest
+
+import oracle as O
+from helpers import cond_close, dense_tables, init_tables_host, w_close
+from workload import configs, gen
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+def run_ranks(W, fn):
+    out, err = [None] * W, []
+
+    def body(r):
+        try:
+            out[r] = fn(r)
+        except Exception as e:  # surface in the main thread
+            err.append((r, e))
+
+    ts = [threading.Thread(target=body, args=(r,)) for r in range(W)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=600)
+    if err:
+        raise err[0][1]
+    return out
+
+
+def global_batch(per_rank, F, B):
+    """Concatenate per-rank feature-major batches into one global batch (sample r*B + b)."""
+    ids_g, lens = [], []
+    for f in range(F):
+        for (ids, off) in per_rank:
+            o = off.astype(np.int64)
+            ids_g.append(ids[o[f * B]:o[(f + 1) * B]])
+            lens.append(np.diff(o[f * B:(f + 1) * B + 1]))
+    off_g = np.zeros(F * B * len(per_rank) + 1, dtype=np.int64)
+    off_g[1:] = np.cumsum(np.concatenate(lens))
+    return np.concatenate(ids_g).astype(np.int32), off_g.astype(np.int32)
+
+
+@pytest.mark.parametrize("W", [2, 4, 3])
+@pytest.mark.parametrize("sharding", ["table", "row"])
+def test_sharded_train_step_matches_unsharded_oracle(gpu, W, sharding):
+    from paper_2402_06859_b200 import LoopbackHub, ShardedEmbedding
+    rows = [3000, 1200, 500, 77, 2000]
+    ft = [0, 1, 2, 3, 4, 0, 1]  # features 5, 6 share tables 0, 1
+    cfg = configs.Config("shard", rows, 32, [(t, ("range", 0, 12)) for t in ft], 64, seed=3)
+    B, F, D = cfg.batch, cfg.num_features, cfg.dim
+    per_rank = [gen.make_batch(rows, cfg.features, B, cfg.seed + r, 0) for r in range(W)]
+    ids_g, off_g = global_batch(per_rank, F, B)
+    gshift = gen.grad_shift_for(len(ids_g), D)
+    grad_g = gen.grad_values(cfg.seed, 0, W * B, F, D, gshift)
+    hub = LoopbackHub(W)
+    embs = []
+    for r in range(W):
+        s = torch.cuda.Stream()
+        e = ShardedEmbedding(rows, D, ft, max_nnz=max(len(i) for i, _ in per_rank), max_batch=B,
+                             device=torch.device("cuda:0"), stream=s, rank=r, world_size=W,
+                             sharding=sharding, loopback_hub=hub)
+        init_tables_host(e, cfg)
+        embs.append(e)
+    torch.cuda.synchronize()
+
+    def step(r):
+        e = embs[r]
+        ids, off = per_rank[r]
+        with torch.cuda.stream(e.stream):
+            out = e.forward(torch.from_numpy(ids).cuda(), torch.from_numpy(off).cuda(), B)
+            g = torch.from_numpy(grad_g[r * B:(r + 1) * B].copy()).cuda()
+            e.backward_adagrad(g, 0.05)
+        st = e.sync()
+        return out.cpu().numpy(), st
+
+    res = run_ranks(W, step)
+    assert all(st == 0 for _, st in res)
+    pb = O.Problem(rows, D, ft)
+    W0 = dense_tables(cfg)
+    Wo = W0.copy()
+    A = np.full(cfg.total_rows, 0.1, dtype=np.float32)
+    r_or = O.train_step(pb, Wo, A, ids_g, off_g, W * B, grad_g, 0.05, 1e-7, 1.0)
+    mag, _ = O.forward(pb, np.abs(W0), ids_g, off_g, W * B)
+    for r in range(W):
+        got = res[r][0]
+        ref = r_or["out"][r * B:(r + 1) * B]
+        assert cond_close(got, ref, mag[r * B:(r + 1) * B]).all()
+        if sharding == "table":
+            assert (got == ref).all()
+    # global norm identical on every rank (rank partials summed in rank order)
+    Ss = [e.last_stats()[0] for e in embs]
+    assert all(S == Ss[0] for S in Ss)
+    assert abs(Ss[0] - r_or["S"]) <= 1e-12 * r_or["S"]
+    assert sum(e.last_stats()[2] for e in embs) == r_or["U"]
+    # every row from its owner
+    base = np.concatenate([[0], np.cumsum(rows)])
+    keys, segs, bags = O.dedup(pb, ids_g, off_g, W * B)
+    G = O.segment_reduce(pb, off_g, W * B, segs, bags, grad_g)
+    g = O.clip(G, r_or["c"])
+    step = np.zeros_like(W0)
+    step[keys] = np.abs(0.05 / (np.sqrt(np.full(len(keys), 0.1, np.float32) + 0.0) + 1e-7))[:, None] * np.abs(g)
+    for t, R in enumerate(rows):
+        for e in embs:
+            lo, hi = int(e.row_lo[t]), int(e.row_hi[t])
+            if e.local_base[t] < 0 or hi <= lo:
+                continue
+            w, a = e.read_rows(t, np.arange(lo, hi))
+            sl = slice(base[t] + lo, base[t] + hi)
+            assert (np.abs(a - A[sl]) <= 1e-6 * A[sl]).all()
+            assert w_close(w, Wo[sl], W0[sl], np.maximum(step[sl], np.abs(Wo[sl] - W0[sl]))).all()
+    for e in embs:
+        e.close()
+    hub.close()
+
+
+@pytest.mark.parametrize("sharding", ["table", "row"])
+def test_sharded_q8_forward(gpu, sharding):
+    from paper_2402_06859_b200 import LoopbackHub, ShardedEmbedding
+    W = 2
+    rows = [2000, 900, 300]
+    ft = [0, 1, 2, 1]
+    cfg = configs.Config("shq8", rows, 64, [(t, ("range", 1, 9)) for t in ft], 48, seed=8)
+    B, F, D = cfg.batch, cfg.num_features, cfg.dim
+    per_rank = [gen.make_batch(rows, cfg.features, B, cfg.seed + r, 0) for r in range(W)]
+    hub = LoopbackHub(W)
+    embs = []
+    for r in range(W):
+        e = ShardedEmbedding(rows, D, ft, max_nnz=max(len(i) for i, _ in per_rank), max_batch=B,
+                             device=torch.device("cuda:0"), stream=torch.cuda.Stream(), rank=r,
+                             world_size=W, sharding=sharding, q8=True, loopback_hub=hub)
+        init_tables_host(e, cfg)
+        e.quantize()
+        embs.append(e)
+    torch.cuda.synchronize()
+
+    def fwd(r):
+        e = embs[r]
+        ids, off = per_rank[r]
+        with torch.cuda.stream(e.stream):
+            out = e.forward_q8(torch.from_numpy(ids).cuda(), torch.from_numpy(off).cuda(), B)
+        assert e.sync() == 0
+        return out.cpu().numpy()
+
+    outs = run_ranks(W, fwd)
+    W0 = dense_tables(cfg)
+    codes, mid, sc, _ = O.quantize(W0)
+    pb = O.Problem(rows, D, ft)
+    deq = np.abs(mid.astype(np.float64))[:, None] + np.abs(codes.astype(np.float64) * sc[:, None])
+    for r in range(W):
+        ref, _ = O.forward_q8(pb, codes, mid, sc, per_rank[r][0], per_rank[r][1], B)
+        mag, _ = O.forward(pb, deq.astype(np.float32), per_rank[r][0], per_rank[r][1], B)
+        assert cond_close(outs[r], ref, mag).all()
+        if sharding == "table":
+            assert (outs[r] == ref).all()
+    hub.close()
