@@ -233,7 +233,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     stream = torch.cuda.Stream(dev)
-    B = cfg.batch  # per rank (replicas: weak scaling)
+    B = cfg.batch  # per rank: weak scaling (tables grow with the ranks, see main())
     D, F = cfg.dim, cfg.num_features
 
     # inputs: nb distinct batches, resident in HBM (and pinned on the host for e2e)
@@ -242,8 +242,18 @@ def run_ours(args, cfg, rank, world, local_rank):
         ids, off = gen.make_batch(cfg.table_rows, cfg.features, B, cfg.seed + 7919 * rank, k, alpha=cfg.alpha)
         batches.append((ids, off))
     max_nnz = max(len(i) for i, _ in batches)
+    shard_kw = {}
+    if world > 1:
+        # row-wise sharding over NCCL; rank 0 makes the unique id, a broadcast distributes it
+        from paper_2402_06859_b200 import nccl_unique_id
+        uid = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(uid, 0)
+        shard_kw = dict(rank=rank, world_size=world, sharding="row", nccl_unique_id=uid.cpu().numpy().tobytes(),
+                        max_recv_nnz=3 * max_nnz)
     emb = ShardedEmbedding(cfg.table_rows, D, cfg.feature_table, max_nnz=max_nnz, max_batch=B,
-                           adagrad=args.adagrad, q8=True, requant=True, device=dev, stream=stream)
+                           adagrad=args.adagrad, q8=True, requant=True, device=dev, stream=stream, **shard_kw)
     with torch.cuda.stream(stream):
         for t in range(cfg.num_tables):
             v = emb.table_view(t)
@@ -403,7 +413,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         "config": {"workload": cfg.name, "tables": cfg.table_rows, "dim": D, "features": F,
                    "global_batch": world * B, "batch_per_gpu": B, "nnz_per_step": nnz_avg, "alpha": cfg.alpha,
                    "unique_rows": U, "adagrad": args.adagrad,
-                   "parallelism": "single" if world == 1 else f"replicas{world}",
+                   "parallelism": "single" if world == 1 else f"row-sharded x{world} (NCCL all-to-all ids, reduce-scatter pooled, all-gather grads)",
                    "step": "a2 fwd + a5-a8 bwd (a9 requant of touched rows fused) + a10 q8 fwd",
                    "l2": "flushed between timed steps (256 MiB write, untimed)",
                    "batches_rotated": len(batches)},
@@ -438,6 +448,10 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and args.impl == "ours":
+        # weak scaling: every GPU keeps the 1-GPU shard size and batch; the tables are the
+        # W-fold Feed tables (W=8: the 1B-row Feed config of BASELINE.json), row-wise sharded
+        cfg = cfg.with_(name=f"{cfg.name}-x{world}", table_rows=[r * world for r in cfg.table_rows])
     if args.impl == "reference":
         run_reference(args, cfg, rank, world)
         return

@@ -84,6 +84,8 @@ enum { EMB_SHARD_NONE = 0, EMB_SHARD_TABLE = 1, EMB_SHARD_ROW = 2 };
 #define EMB_F_REQUANT 2u  /* (needs EMB_F_Q8) every AdaGrad update also re-quantizes the rows
                              it touched, so the q8 store tracks the fp32 tables between
                              full emb_quantize_mm8() passes                                   */
+#define EMB_F_EXCHANGE 8u /* run the sharded exchange path even at world_size 1 (a 1-rank
+                             communicator; exercises the transport on a single GPU)          */
 #define EMB_F_LOOPBACK 4u /* (world_size > 1) TEST TRANSPORT: the ranks are threads of one
                              process sharing one device; cfg.nccl_unique_id is the hub from
                              emb_loopback_hub_create().  Every collective becomes a host
@@ -113,6 +115,9 @@ typedef struct {
   const void* nccl_unique_id;    /* 128-byte ncclUniqueId from rank 0 (NULL if world_size 1)  */
   void* stream;                  /* cudaStream_t every call is enqueued on                    */
   uint32_t flags;                /* EMB_F_*                                                   */
+  int64_t max_recv_nnz;          /* sharded: capacity of occurrences this rank pools per call
+                                    (its rows' share of every rank's ids); 0 = min(2, W) *
+                                    max_nnz.  A call that exceeds it returns EMB_ENOMEM.      */
 } emb_config;
 
 typedef struct {

@@ -83,7 +83,10 @@ emb_status make_plan(const emb_config* c, Plan* p) {
   p->qpitch = (int)round_up(round_up(c->dim, 8) + 8, 32);
   p->pooling = c->pooling;
   p->mode = c->adagrad_mode;
-  p->sharding = c->world_size > 1 ? c->sharding : EMB_SHARD_NONE;
+  p->exch = c->world_size > 1 || (c->flags & EMB_F_EXCHANGE);
+  if (p->exch && c->sharding == EMB_SHARD_NONE) return EMB_EINVAL;
+  if (p->exch && c->pooling == EMB_POOL_MEAN) return EMB_EINVAL;
+  p->sharding = p->exch ? c->sharding : EMB_SHARD_NONE;
   p->rank = c->rank;
   p->world = c->world_size;
   p->flags = c->flags;
@@ -169,8 +172,11 @@ emb_status make_plan(const emb_config* c, Plan* p) {
   p->Fr = p->Fo[p->rank];
   // Capacities: a rank can receive every id of every rank, and pools every bag of every rank
   // that reads its tables.  (Capacity, not expectation.)
-  p->recv_nnz_cap = W > 1 ? std::min<int64_t>(p->max_nnz * W, (int64_t(1) << 30) - 1) : p->max_nnz;
-  p->owner_bags_cap = (int64_t)p->max_batch * (W > 1 ? (int64_t)p->Fr * W : F);
+  if (c->max_recv_nnz < 0 || c->max_recv_nnz >= (int64_t(1) << 30)) return EMB_EINVAL;
+  p->recv_nnz_cap = !p->exch ? p->max_nnz
+                  : c->max_recv_nnz > 0 ? c->max_recv_nnz
+                                        : std::min<int64_t>(p->max_nnz * std::min(W, 2), (int64_t(1) << 30) - 1);
+  p->owner_bags_cap = (int64_t)p->max_batch * (p->exch ? (int64_t)p->Fr * W : F);
   return EMB_OK;
 }
 
@@ -211,7 +217,7 @@ void carve(const Plan& p, Carver& cv, emb_handle* h) {
   auto* cl = cv.take<float>(1);
   auto* st = cv.take<uint32_t>(1);
   ExchangeWs x{};
-  if (p.world > 1) carve_exchange(p, cv, &x);
+  if (p.exch) carve_exchange(p, cv, &x);
   if (h) {
     h->d_meta = meta;
     h->stage_ids = stage_ids;
@@ -361,7 +367,7 @@ emb_status backward_local(emb_t h, const float* grad_dev, float lr, double extra
     h->launches += 1;
     const double* parts = h->S_local;
     int np = 1;
-    if (p.world > 1) {
+    if (p.exch) {
       if (!h->comm->allgather(h->S_local, h->S_parts, sizeof(double), h->stream)) return EMB_ENCCL;
       parts = h->S_parts;
       np = p.world;
@@ -528,7 +534,7 @@ emb_status emb_create(const emb_config* cfg, const emb_buffers* buf, emb_t* out)
   const void* ptrs[5] = {buf->weights, buf->accum, buf->workspace, buf->q8_codes, buf->q8_meta};
   for (const void* q : ptrs)
     if (q && !aligned(q, kAlign)) { delete h; return EMB_EINVAL; }
-  if (p.world > 1 && !cfg->nccl_unique_id) { delete h; return EMB_EINVAL; }
+  if (p.exch && !cfg->nccl_unique_id) { delete h; return EMB_EINVAL; }
   h->stream = (cudaStream_t)cfg->stream;
   h->W = (float*)buf->weights;
   h->A = (float*)buf->accum;
@@ -550,7 +556,7 @@ emb_status emb_create(const emb_config* cfg, const emb_buffers* buf, emb_t* out)
     e = cudaMemsetAsync(h->sort.status, 0, sizeof(unsigned long long) * h->sort.max_tiles * kRadixBinsMax, h->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);  // `m` goes out of scope
   if (e != cudaSuccess) { delete h; return EMB_ECUDA; }
-  if (p.world > 1) {
+  if (p.exch) {
     h->comm = (p.flags & EMB_F_LOOPBACK) ? make_loopback_transport((void*)cfg->nccl_unique_id, p.rank)
                                          : make_nccl_transport(cfg->nccl_unique_id, p.rank, p.world);
     if (!h->comm) { delete h; return EMB_ENCCL; }
@@ -626,7 +632,7 @@ emb_status emb_forward(emb_t h, const int32_t* ids, const int32_t* offsets, int3
     s = stage_inputs(h, ids, offsets, batch, nnz, out, &st);
   }
   if (s != EMB_OK) return s;
-  if (p.world > 1) {
+  if (p.exch) {
     s = exchange_forward(h, st, batch, nnz, /*q8=*/false);
     if (s != EMB_OK) return s;
   } else {
@@ -679,7 +685,7 @@ emb_status emb_forward_q8(emb_t h, const int32_t* ids, const int32_t* offsets, i
     s = stage_inputs(h, ids, offsets, batch, nnz, out, &st);
   }
   if (s != EMB_OK) return s;
-  if (p.world > 1) {
+  if (p.exch) {
     s = exchange_forward(h, st, batch, nnz, /*q8=*/true);
     if (s != EMB_OK) return s;
   } else {
@@ -731,7 +737,7 @@ emb_status emb_backward_adagrad(emb_t h, const float* grad_out, float lr, double
     return EMB_EINVAL;
   }
   emb_status s;
-  if (p.world > 1) {
+  if (p.exch) {
     if ((s = exchange_backward(h, g)) != EMB_OK) return s;
     s = backward_local(h, h->x.pooled, lr, extra_sq_norm);
   } else {
@@ -847,7 +853,7 @@ emb_status emb_last_dedup(emb_t h, int32_t* unique, int32_t* seg_offsets, int64_
     const uint32_t F = (uint32_t)h->p.F, B = (uint32_t)h->fwd_B;
     for (uint32_t i = 0; i < nv; ++i) {
       const uint32_t r = tmp[i].y;
-      sorted_bags[i] = (int32_t)(h->p.world > 1 ? r : (r % F) * B + r / F);
+      sorted_bags[i] = (int32_t)(h->p.exch ? r : (r % F) * B + r / F);
     }
   }
   return EMB_OK;

@@ -59,6 +59,7 @@ struct Plan {
   std::vector<int64_t> key_base;            // [world][F]: local base of t(f) on o or -1
   std::vector<int32_t> owner0, blk;         // [F]: owner(id) = owner0 + id / blk
   int Fr = 0;                               // = Fo[rank]
+  bool exch = false;                        // run the exchange path (world > 1, or forced)
   int64_t recv_nnz_cap = 0;                 // occurrences this rank may pool per step
   int64_t owner_bags_cap = 0;               // bags this rank may pool per step
 };

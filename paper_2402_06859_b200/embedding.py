@@ -67,7 +67,8 @@ class ShardedEmbedding:
                  device: Optional[torch.device] = None, stream: Optional[torch.cuda.Stream] = None,
                  rank: int = 0, world_size: int = 1, sharding: str = "none",
                  table_owner: Optional[Sequence[int]] = None, nccl_unique_id: Optional[bytes] = None,
-                 loopback_hub: Optional["LoopbackHub"] = None):
+                 loopback_hub: Optional["LoopbackHub"] = None, force_exchange: bool = False,
+                 max_recv_nnz: int = 0):
         self.lib = L.load()
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
@@ -99,7 +100,9 @@ class ShardedEmbedding:
             nccl_unique_id=uid_ptr,
             stream=C.c_void_p(self.stream.cuda_stream),
             flags=(L.EMB_F_Q8 if (q8 or requant) else 0) | (L.EMB_F_REQUANT if requant else 0)
-            | (L.EMB_F_LOOPBACK if loopback_hub is not None else 0))
+            | (L.EMB_F_LOOPBACK if loopback_hub is not None else 0)
+            | (L.EMB_F_EXCHANGE if force_exchange else 0),
+            max_recv_nnz=int(max_recv_nnz))
         self.sizes = L.EmbSizes()
         L.check(self.lib.emb_plan(C.byref(self.cfg), C.byref(self.sizes)), "emb_plan")
         s = self.sizes

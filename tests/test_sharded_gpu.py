@@ -66,6 +66,7 @@ def test_sharded_train_step_matches_unsharded_oracle(gpu, W, sharding):
     for r in range(W):
         s = torch.cuda.Stream()
         e = ShardedEmbedding(rows, D, ft, max_nnz=max(len(i) for i, _ in per_rank), max_batch=B,
+                             max_recv_nnz=W * max(len(i) for i, _ in per_rank),
                              device=torch.device("cuda:0"), stream=s, rank=r, world_size=W,
                              sharding=sharding, loopback_hub=hub)
         init_tables_host(e, cfg)
@@ -135,6 +136,7 @@ def test_sharded_q8_forward(gpu, sharding):
     embs = []
     for r in range(W):
         e = ShardedEmbedding(rows, D, ft, max_nnz=max(len(i) for i, _ in per_rank), max_batch=B,
+                             max_recv_nnz=W * max(len(i) for i, _ in per_rank),
                              device=torch.device("cuda:0"), stream=torch.cuda.Stream(), rank=r,
                              world_size=W, sharding=sharding, q8=True, loopback_hub=hub)
         init_tables_host(e, cfg)
@@ -162,3 +164,38 @@ def test_sharded_q8_forward(gpu, sharding):
         if sharding == "table":
             assert (outs[r] == ref).all()
     hub.close()
+
+
+@pytest.mark.parametrize("sharding", ["table", "row"])
+def test_nccl_transport_single_rank(gpu, sharding):
+    """The NCCL transport (torch's libnccl, dlopen'ed) on a 1-rank communicator: the whole
+    exchange path runs (send/recv to self, all-gather, reduce-scatter) and must reproduce
+    the unsharded handle bit for bit (with one rank the owner sees occurrences in the
+    unsharded order)."""
+    from paper_2402_06859_b200 import ShardedEmbedding, nccl_unique_id
+    rows = [3000, 700, 90]
+    ft = [0, 1, 2, 0]
+    cfg = configs.Config("nccl1", rows, 64, [(t, ("range", 0, 12)) for t in ft], 128, seed=5)
+    B, F, D = cfg.batch, cfg.num_features, cfg.dim
+    ids, off = gen.make_batch(rows, cfg.features, B, cfg.seed, 0)
+    grad = torch.from_numpy(gen.grad_values(cfg.seed, 0, B, F, D, gen.grad_shift_for(len(ids), D))).cuda()
+    uid = nccl_unique_id()
+    assert len(uid) == 128
+    ex = ShardedEmbedding(rows, D, ft, max_nnz=len(ids), max_batch=B, device=torch.device("cuda:0"),
+                          rank=0, world_size=1, sharding=sharding, nccl_unique_id=uid, force_exchange=True,
+                          q8=True)
+    ref = ShardedEmbedding(rows, D, ft, max_nnz=len(ids), max_batch=B, device=torch.device("cuda:0"), q8=True)
+    for e in (ex, ref):
+        init_tables_host(e, cfg)
+    outs = []
+    for e in (ex, ref):
+        o = e.forward(torch.from_numpy(ids).cuda(), torch.from_numpy(off).cuda(), B)
+        e.backward_adagrad(grad, 0.05)
+        e.quantize()
+        q = e.forward_q8(torch.from_numpy(ids).cuda(), torch.from_numpy(off).cuda(), B)
+        assert e.sync() == 0
+        outs.append((o.cpu().numpy(), q.cpu().numpy()))
+    assert (outs[0][0] == outs[1][0]).all() and (outs[0][1] == outs[1][1]).all()
+    assert torch.equal(ex.weights, ref.weights) and torch.equal(ex.accum_buf[:4 * sum(rows)], ref.accum_buf[:4 * sum(rows)])
+    assert ex.last_stats()[0] == ref.last_stats()[0]
+    ex.close()
