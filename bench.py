@@ -104,7 +104,7 @@ class ClockSampler(threading.Thread):
                     self.reasons |= pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
                 except Exception:
                     self.reasons |= pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)
-                time.sleep(0.05)
+                time.sleep(0.005)
         except Exception as e:  # no NVML: report that
             self.err = repr(e)
 

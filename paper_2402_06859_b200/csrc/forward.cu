@@ -123,7 +123,7 @@ k_pool_fwd_f32(const float* __restrict__ W, int pitch, const int* __restrict__ i
     }
   }
   if (!live) return;
-  if (bad && lane == 0) set_status(status, kStIdRange);
+  if (bad) set_status(status, kStIdRange);  // any lane: each lane validated its own ids
   if (MEAN) mean_div(acc, len);
   float* o = out + (size_t)grow * D;
 #pragma unroll
@@ -137,86 +137,101 @@ k_pool_fwd_f32(const float* __restrict__ W, int pitch, const int* __restrict__ i
 __device__ __forceinline__ float code_f(uint32_t x, uint32_t sel) {
   return __fsub_rn(__int_as_float((int)__byte_perm(x, 0x4B000000u, sel)), 8388736.0f);
 }
-__device__ __forceinline__ void deq8(uint2 w, float scale, float middle, float4& lo, float4& hi) {
-  const uint32_t x = w.x ^ 0x80808080u, y = w.y ^ 0x80808080u;
-  lo = make_float4(__fmaf_rn(code_f(x, 0x7540), scale, middle), __fmaf_rn(code_f(x, 0x7541), scale, middle),
-                   __fmaf_rn(code_f(x, 0x7542), scale, middle), __fmaf_rn(code_f(x, 0x7543), scale, middle));
-  hi = make_float4(__fmaf_rn(code_f(y, 0x7540), scale, middle), __fmaf_rn(code_f(y, 0x7541), scale, middle),
-                   __fmaf_rn(code_f(y, 0x7542), scale, middle), __fmaf_rn(code_f(y, 0x7543), scale, middle));
+// 4 codes (one 32-bit word) -> acc += middle + code * scale, element by element.
+__device__ __forceinline__ float4 deq4_add(float4 acc, uint32_t w, float scale, float middle) {
+  const uint32_t x = w ^ 0x80808080u;
+  acc.x = __fadd_rn(acc.x, __fmaf_rn(code_f(x, 0x7540), scale, middle));
+  acc.y = __fadd_rn(acc.y, __fmaf_rn(code_f(x, 0x7541), scale, middle));
+  acc.z = __fadd_rn(acc.z, __fmaf_rn(code_f(x, 0x7542), scale, middle));
+  acc.w = __fadd_rn(acc.w, __fmaf_rn(code_f(x, 0x7543), scale, middle));
+  return acc;
 }
-__device__ __forceinline__ uint2 ld_nc_u2(const void* p) {
-  uint2 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+__device__ __forceinline__ uint4 ld_nc_u4(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
   return r;
 }
 
-// a10.  q8 row layout: [codes: D int8][pad to 8][middle f32][scale f32][pad to 16]
-// (D=64: 80 B, one contiguous run per row).  Lane l of a group of LPB lanes reads code
-// vectors l, l+LPB, ... (8 codes, one 8-B load each) and the row's {middle, scale} (8 B,
-// same address for the whole group).  D=64: 8 lanes per bag, 4 bags per warp.
+// a10.  q8 row layout: [codes: D int8][pad to 8][middle f32][scale f32][pad to 32]
+// (D=64: 96 B = 3 whole sectors).  Lane l of a group of LPB lanes reads 16-code vectors
+// l, l+LPB, ... (one 16-B load each) and the row's {middle, scale} (8 B, same address for
+// the group).  D=64: 4 lanes per bag, 8 bags per warp, 16 dims per lane.  As in the fp32
+// kernel, ids are loaded LPB at a time and broadcast by full-mask shuffles over a
+// warp-uniform trip count, so a lane spends its instructions on the dequant, not on
+// per-slot key arithmetic.
 template <int LPB, int VPL, bool MEAN>
 __global__ void __launch_bounds__(256)
 k_pool_fwd_q8(const uint8_t* __restrict__ codes, int qpitch, int meta_off,
               const int* __restrict__ ids, const int* __restrict__ offsets, int B, int F, int Fb,
               int D, const FeatMeta* __restrict__ meta, float* __restrict__ out,
               uint32_t* status) {
-  constexpr int UNR = (VPL == 1) ? 8 : (VPL == 2 ? 4 : 2);
+  constexpr int UNR = (VPL == 1) ? 4 : 2;
   constexpr uint32_t kNone = 0xffffffffu;
+  constexpr unsigned kFull = 0xffffffffu;
   const int lane = threadIdx.x & (LPB - 1);
   const long long bag = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / LPB;
-  if (bag >= (long long)F * B) return;
-  const int f = (int)(bag / B);
-  const int b = (int)(bag - (long long)f * B);
+  const bool live = bag < (long long)F * B;  // predicate, never return: shuffles below
+  const int f = live ? (int)(bag / B) : 0;
+  const int b = live ? (int)(bag - (long long)f * B) : 0;
   const FeatMeta m = meta[f];
-  const int lo = __ldg(offsets + bag);
-  const int hi = __ldg(offsets + bag + 1);
-  const int nv8 = (D + 7) >> 3;  // 8-code vectors carrying dims < D
-  float4 acc[2 * VPL];
+  const int lo = live ? __ldg(offsets + bag) : 0;
+  const int hi = live ? __ldg(offsets + bag + 1) : 0;
+  const int len = hi - lo;
+  const int nv16 = (D + 15) >> 4;  // 16-code vectors carrying dims < D
+  float4 acc[4 * VPL];
 #pragma unroll
-  for (int v = 0; v < 2 * VPL; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int v = 0; v < 4 * VPL; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
   bool bad = false;
-  for (int j0 = lo; j0 < hi; j0 += UNR) {
-    uint32_t k[UNR];
-    uint2 w[UNR][VPL];
-    float2 mt[UNR];
+  const int maxlen = __reduce_max_sync(kFull, len);
+  for (int j0 = 0; j0 < maxlen; j0 += LPB) {
+    const int j = j0 + lane;
+    const uint32_t key = j < len ? row_key(__ldg(ids + lo + j), m, kNone, bad) : kNone;
+#pragma unroll 1
+    for (int jj = 0; jj < LPB; jj += UNR) {
+      uint32_t k[UNR];
+      uint4 w[UNR][VPL];
+      float2 mt[UNR];
 #pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-      const int j = j0 + u;
-      k[u] = j < hi ? row_key(__ldg(ids + j), m, kNone, bad) : kNone;
-    }
+      for (int u = 0; u < UNR; ++u) {
+        k[u] = __shfl_sync(kFull, key, (jj + u) & (LPB - 1), LPB);
+        if (jj + u >= LPB || j0 + jj + u >= len) k[u] = kNone;
+      }
 #pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-      if (k[u] != kNone) {
-        const uint8_t* row = codes + (size_t)k[u] * qpitch;
-        mt[u] = *reinterpret_cast<const float2*>(row + meta_off);
+      for (int u = 0; u < UNR; ++u) {
+        if (k[u] != kNone) {
+          const uint8_t* row = codes + (size_t)k[u] * qpitch;
+          mt[u] = *reinterpret_cast<const float2*>(row + meta_off);
 #pragma unroll
-        for (int v = 0; v < VPL; ++v) {
-          const int vi = lane + v * LPB;
-          w[u][v] = vi < nv8 ? ld_nc_u2(row + 8 * vi) : make_uint2(0x80808080u, 0x80808080u);
+          for (int v = 0; v < VPL; ++v) {
+            const int vi = lane + v * LPB;
+            w[u][v] = vi < nv16 ? ld_nc_u4(row + 16 * vi) : make_uint4(0u, 0u, 0u, 0u);
+          }
         }
       }
-    }
 #pragma unroll
-    for (int u = 0; u < UNR; ++u)
-      if (k[u] != kNone) {
+      for (int u = 0; u < UNR; ++u)
+        if (k[u] != kNone) {
 #pragma unroll
-        for (int v = 0; v < VPL; ++v) {
-          float4 dl, dh;
-          deq8(w[u][v], mt[u].y, mt[u].x, dl, dh);
-          acc[2 * v] = f4_add_rn(acc[2 * v], dl);
-          acc[2 * v + 1] = f4_add_rn(acc[2 * v + 1], dh);
+          for (int v = 0; v < VPL; ++v) {
+            acc[4 * v + 0] = deq4_add(acc[4 * v + 0], w[u][v].x, mt[u].y, mt[u].x);
+            acc[4 * v + 1] = deq4_add(acc[4 * v + 1], w[u][v].y, mt[u].y, mt[u].x);
+            acc[4 * v + 2] = deq4_add(acc[4 * v + 2], w[u][v].z, mt[u].y, mt[u].x);
+            acc[4 * v + 3] = deq4_add(acc[4 * v + 3], w[u][v].w, mt[u].y, mt[u].x);
+          }
         }
-      }
+    }
   }
-  if (bad && lane == 0) set_status(status, kStIdRange);
-  if (MEAN) mean_div(acc, hi - lo);
-  // lane l holds dims 8*(l + v*LPB) .. +8
+  if (!live) return;
+  if (bad) set_status(status, kStIdRange);  // any lane: each lane validated its own ids
+  if (MEAN) mean_div(acc, len);
+  // lane l holds dims 16*(l + v*LPB) .. +16
   float* o = out + out_row(f, b, B, Fb) * D;
 #pragma unroll
   for (int v = 0; v < VPL; ++v) {
-    const int d = 8 * (lane + v * LPB);
-    store4(o, d, D, acc[2 * v]);
-    store4(o, d + 4, D, acc[2 * v + 1]);
+    const int d = 16 * (lane + v * LPB);
+#pragma unroll
+    for (int h = 0; h < 4; ++h) store4(o, d + 4 * h, D, acc[4 * v + h]);
   }
 }
 
@@ -257,8 +272,8 @@ cudaError_t launch_pool_fwd_f32(const FwdArgs& a, cudaStream_t s) {
 }
 
 cudaError_t launch_pool_fwd_q8(const FwdQ8Args& a, cudaStream_t s) {
-  // geometry over 8-code vectors (one 8-B load each)
-  const Geom g = geom_for(4 * ((a.D + 7) / 8));
+  // geometry over 16-code vectors (one 16-B load each)
+  const Geom g = geom_for(4 * ((a.D + 15) / 16));
   const long long bags = (long long)a.F * a.B;
   if (bags == 0) return cudaSuccess;
   const unsigned grid = (unsigned)((bags * g.lpb + 255) / 256);
