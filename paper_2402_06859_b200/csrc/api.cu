@@ -187,8 +187,8 @@ void carve(const Plan& p, Carver& cv, emb_handle* h) {
   const int64_t nnz_cap = p.recv_nnz_cap;  // occurrences pooled here per step
   const int64_t bags_cap = p.owner_bags_cap;
   const int64_t dense_cap = std::max<int64_t>(Bmax * F * p.D, 1);
-  const int64_t tiles = (std::max<int64_t>(nnz_cap, bags_cap + Bmax * p.dest_base[p.world]) + kSortTile - 1) /
-                            kSortTile + 1;
+  const int64_t tiles = (std::max<int64_t>(nnz_cap, bags_cap + Bmax * p.dest_base[p.world]) + kSortTileMin - 1) /
+                            kSortTileMin + 1;
   const int64_t chunks = (nnz_cap + kChunk - 1) / kChunk + 1;
   const int64_t max_unique = std::min<int64_t>(nnz_cap, p.local_rows) + 1;
   auto* meta = cv.take<FeatMeta>(F);
@@ -294,30 +294,50 @@ emb_status stage_inputs(emb_t h, const int32_t* ids, const int32_t* offsets, int
 // a5-a8 on this rank's recorded occurrences; grad is the pooled-gradient input in the
 // layout of the recorded bags (unsharded: [B][F][D]; owner: [src][B][Fr][D]).  With W > 1
 // the rank partials of the global squared norm are all-gathered and summed in rank order.
-emb_status backward_local(emb_t h, const float* grad_dev, float lr, double extra) {
+emb_status launch_dedup(emb_t h) {
   const Plan& p = h->p;
   const int64_t n = h->fwd_nnz;
   const uint2* kres = h->kvA;
+  CK(cudaEventRecord(h->ev_kv, h->stream));
+  CK(cudaStreamWaitEvent(h->side, h->ev_kv, 0));
   if (n > 0) {
     int passes = 0;
     bool in1 = false;
     {
-      Phase ph(h->prof, h->stream, EMB_PH_SORT);
+      Phase ph(h->prof, h->side, EMB_PH_SORT);
       CK(radix_sort_pairs(h->kvA, h->kvB, n, p.key_bits, h->sort, h->epoch, &passes, &in1,
-                          &h->launches, h->stream));
+                          &h->launches, h->side));
     }
     h->epoch += (uint32_t)passes;
     if (in1) kres = h->kvB;
-    Phase ph(h->prof, h->stream, EMB_PH_RLE);
+    Phase ph(h->prof, h->side, EMB_PH_RLE);
     CK(launch_rle(kres, n, (uint32_t)p.local_rows, h->unique, h->seg, h->d_U, h->chunk_u0,
-                  h->sort.counters + kMaxPasses, h->sort.status, h->epoch, h->stream));
+                  h->sort.counters + kMaxPasses, h->sort.status, h->epoch, h->side));
     h->epoch += 1;
     h->launches += 1;
   } else {
-    CK(cudaMemsetAsync(h->d_U, 0, sizeof(uint32_t), h->stream));
-    CK(cudaMemsetAsync(h->seg, 0, sizeof(uint32_t), h->stream));
+    CK(cudaMemsetAsync(h->d_U, 0, sizeof(uint32_t), h->side));
+    CK(cudaMemsetAsync(h->seg, 0, sizeof(uint32_t), h->side));
   }
+  CK(cudaEventRecord(h->ev_dedup, h->side));
+  h->dedup_pending = true;
   h->sorted_kv = kres;
+  return EMB_OK;
+}
+
+emb_status join_dedup(emb_t h) {
+  if (!h->dedup_pending) return EMB_OK;
+  CK(cudaStreamWaitEvent(h->stream, h->ev_dedup, 0));
+  h->dedup_pending = false;
+  return EMB_OK;
+}
+
+emb_status backward_local(emb_t h, const float* grad_dev, float lr, double extra) {
+  const Plan& p = h->p;
+  const int64_t n = h->fwd_nnz;
+  emb_status js = join_dedup(h);  // a5 ran on the side stream since the forward
+  if (js != EMB_OK) return js;
+  const uint2* kres = h->sorted_kv;
 
   BwdArgs a;
   memset(&a, 0, sizeof(a));
@@ -555,6 +575,9 @@ emb_status emb_create(const emb_config* cfg, const emb_buffers* buf, emb_t* out)
   if (e == cudaSuccess)
     e = cudaMemsetAsync(h->sort.status, 0, sizeof(unsigned long long) * h->sort.max_tiles * kRadixBinsMax, h->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);  // `m` goes out of scope
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_kv, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_dedup, cudaEventDisableTiming);
   if (e != cudaSuccess) { delete h; return EMB_ECUDA; }
   if (p.exch) {
     h->comm = (p.flags & EMB_F_LOOPBACK) ? make_loopback_transport((void*)cfg->nccl_unique_id, p.rank)
@@ -568,6 +591,12 @@ emb_status emb_create(const emb_config* cfg, const emb_buffers* buf, emb_t* out)
 
 emb_status emb_destroy(emb_t h) {
   if (!h) return EMB_EINVAL;
+  if (h->side) {
+    cudaStreamSynchronize(h->side);
+    cudaStreamDestroy(h->side);
+  }
+  if (h->ev_kv) cudaEventDestroy(h->ev_kv);
+  if (h->ev_dedup) cudaEventDestroy(h->ev_dedup);
   delete h->comm;
   delete h;
   return EMB_OK;
@@ -588,6 +617,7 @@ emb_status emb_profile_read(emb_t h, double* ms, int64_t* count, int32_t reset) 
     for (int i = 0; i < EMB_PH_COUNT; ++i) { pr.ms[i] = 0; pr.n[i] = 0; }
   }
   CK(cudaStreamSynchronize(h->stream));
+  CK(cudaStreamSynchronize(h->side));
   for (auto& r : pr.pending) {
     float t = 0.f;
     if (cudaEventElapsedTime(&t, r.a, r.b) == cudaSuccess) {
@@ -607,6 +637,7 @@ emb_status emb_profile_read(emb_t h, double* ms, int64_t* count, int32_t reset) 
 
 emb_status emb_sync(emb_t h) {
   if (!h) return EMB_EINVAL;
+  CK(cudaStreamSynchronize(h->side));
   CK(cudaStreamSynchronize(h->stream));
   uint32_t st = 0;
   CK(cudaMemcpy(&st, h->d_status, sizeof(st), cudaMemcpyDeviceToHost));
@@ -626,6 +657,7 @@ emb_status emb_forward(emb_t h, const int32_t* ids, const int32_t* offsets, int3
   emb_status s = check_batch_args(h, ids, offsets, batch, nnz, out);
   if (s != EMB_OK) return s;
   const Plan& p = h->p;
+  if ((s = join_dedup(h)) != EMB_OK) return s;  // the previous dedup may still read kvA/kvB
   Staged st;
   {
     Phase ph(h->prof, h->stream, EMB_PH_COPY);
@@ -635,6 +667,7 @@ emb_status emb_forward(emb_t h, const int32_t* ids, const int32_t* offsets, int3
   if (p.exch) {
     s = exchange_forward(h, st, batch, nnz, /*q8=*/false);
     if (s != EMB_OK) return s;
+    if ((s = launch_dedup(h)) != EMB_OK) return s;
   } else {
     FwdArgs a;
     memset(&a, 0, sizeof(a));
@@ -664,6 +697,7 @@ emb_status emb_forward(emb_t h, const int32_t* ids, const int32_t* offsets, int3
     h->have_fwd = true;
     h->fwd_nnz = nnz;
     h->fwd_B = batch;
+    if ((s = launch_dedup(h)) != EMB_OK) return s;  // a5 starts now, on the side stream
   }
   if (st.host_out) {
     Phase ph(h->prof, h->stream, EMB_PH_COPY);
@@ -836,6 +870,7 @@ emb_status emb_last_dedup(emb_t h, int32_t* unique, int32_t* seg_offsets, int64_
                           int64_t* n_valid) {
   if (!h) return EMB_EINVAL;
   if (!h->sorted_kv) return EMB_ESTATE;
+  CK(cudaStreamSynchronize(h->side));
   CK(cudaStreamSynchronize(h->stream));
   uint32_t U = 0, nv = 0;
   CK(cudaMemcpy(&U, h->d_U, 4, cudaMemcpyDeviceToHost));
@@ -861,6 +896,7 @@ emb_status emb_last_dedup(emb_t h, int32_t* unique, int32_t* seg_offsets, int64_
 
 emb_status emb_last_stats(emb_t h, double* sq_norm, float* clip, int64_t* n_unique) {
   if (!h) return EMB_EINVAL;
+  CK(cudaStreamSynchronize(h->side));
   CK(cudaStreamSynchronize(h->stream));
   if (sq_norm) CK(cudaMemcpy(sq_norm, h->S_global, 8, cudaMemcpyDeviceToHost));
   if (clip) CK(cudaMemcpy(clip, h->d_clip, 4, cudaMemcpyDeviceToHost));

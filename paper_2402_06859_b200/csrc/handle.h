@@ -132,6 +132,12 @@ struct emb_handle {
   lirank::Plan p;
   lirank::Prof prof;
   cudaStream_t stream = nullptr;
+  // a5 dedup runs on a side stream as soon as the forward has recorded the occurrences,
+  // overlapping whatever the caller does before emb_backward_adagrad (the dense tower).
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_kv = nullptr;     // forward wrote kvA (main stream)
+  cudaEvent_t ev_dedup = nullptr;  // dedup finished (side stream)
+  bool dedup_pending = false;      // dedup of the last forward was launched on `side`
   float* W = nullptr;
   float* A = nullptr;
   uint8_t* codes = nullptr;
@@ -195,6 +201,10 @@ emb_status stage_inputs(emb_t h, const int32_t* ids, const int32_t* offsets, int
 
 // a5-a8 on this rank's recorded occurrences (see api.cu).
 emb_status backward_local(emb_t h, const float* grad_dev, float lr, double extra);
+// a5 (sort + run-length encode) of the recorded occurrences on the side stream.
+emb_status launch_dedup(emb_t h);
+// make the main stream wait for a pending dedup (before reusing kvA or reading its output)
+emb_status join_dedup(emb_t h);
 
 // sharded forward / backward (exchange.cu)
 emb_status exchange_forward(emb_t h, const Staged& st, int32_t batch, int64_t nnz, bool q8);

@@ -16,6 +16,8 @@
 //   in shared memory in sorted order; the tile is then written out in digit runs
 //   (coalesced).  Each pass moves 16 B per pair.  Tiles are claimed in launch order
 //   through an atomic counter, so a look-back only waits on tiles already resident.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "lookback.cuh"
@@ -103,18 +105,20 @@ k_radix_hist(const uint2* __restrict__ kv, int64_t n, int passes, uint32_t* hist
 }
 
 // ---------------------------------------------------------------------------
-// One digit pass.
+// One digit pass.  ITEMS pairs per thread (tile = 256 * ITEMS); MATCH selects the warp
+// ranking primitive (match.any vs a BITS-ballot multisplit).
 // ---------------------------------------------------------------------------
-template <int BITS>
+template <int BITS, int ITEMS, bool MATCH>
 __global__ void __launch_bounds__(kSortThreads)
 k_onesweep(const uint2* __restrict__ in, uint2* __restrict__ out, int64_t n, int shift,
            const uint32_t* __restrict__ hist, uint32_t* tile_counter,
            unsigned long long* status, uint32_t epoch) {
   constexpr int BINS = 1 << BITS;
   constexpr int DPT = BINS / kSortThreads;  // digits per thread (1 or 2)
+  constexpr int TILE = kSortThreads * ITEMS;
   extern __shared__ uint8_t smem_raw[];
-  uint2* stage = reinterpret_cast<uint2*>(smem_raw);                           // [kSortTile]
-  uint32_t* warp_hist = reinterpret_cast<uint32_t*>(stage + kSortTile);       // [NW][BINS]
+  uint2* stage = reinterpret_cast<uint2*>(smem_raw);                           // [TILE]
+  uint32_t* warp_hist = reinterpret_cast<uint32_t*>(stage + TILE);            // [NW][BINS]
   uint32_t* digit_off = warp_hist + NW * BINS;                                  // [BINS]
   uint32_t* s_misc = digit_off + BINS;                                          // [NW + 2]
 
@@ -123,25 +127,29 @@ k_onesweep(const uint2* __restrict__ in, uint2* __restrict__ out, int64_t n, int
   for (int i = tid; i < NW * BINS; i += kSortThreads) warp_hist[i] = 0;
   __syncthreads();
   const int64_t tile = s_misc[NW];
-  const int64_t tile0 = tile * kSortTile;
-  const int64_t base = tile0 + (int64_t)warp * (kSortItems * 32);
+  const int64_t tile0 = tile * TILE;
+  const int64_t base = tile0 + (int64_t)warp * (ITEMS * 32);
 
-  uint2 kv[kSortItems];
-  uint32_t r[kSortItems];
+  uint2 kv[ITEMS];
+  uint32_t r[ITEMS];
 #pragma unroll
-  for (int i = 0; i < kSortItems; ++i) {
+  for (int i = 0; i < ITEMS; ++i) {
     const int64_t idx = base + i * 32 + lane;
     kv[i] = idx < n ? in[idx] : make_uint2(0u, 0u);
   }
   const unsigned lt = lanemask_lt();
   uint32_t* wh = warp_hist + warp * BINS;
 #pragma unroll
-  for (int i = 0; i < kSortItems; ++i) {
+  for (int i = 0; i < ITEMS; ++i) {
     const int64_t idx = base + i * 32 + lane;
     const bool ok = idx < n;
-    const unsigned valid = __ballot_sync(0xffffffffu, ok);
-    const uint32_t d = (kv[i].x >> shift) & (BINS - 1);
-    const unsigned peers = peers_of<BITS>(d, valid);
+    const uint32_t d = ok ? (kv[i].x >> shift) & (BINS - 1) : (uint32_t)BINS;
+    unsigned peers;
+    if (MATCH) {
+      peers = __match_any_sync(0xffffffffu, d);
+    } else {
+      peers = peers_of<BITS + 1>(d, 0xffffffffu);  // bit BITS separates the out-of-range lanes
+    }
     const uint32_t cur = ok ? wh[d] : 0u;
     r[i] = cur + __popc(peers & lt);
     __syncwarp();
@@ -177,19 +185,15 @@ k_onesweep(const uint2* __restrict__ in, uint2* __restrict__ out, int64_t n, int
   }
   // stage the tile in sorted order (overlaps the look-back of earlier tiles)
 #pragma unroll
-  for (int i = 0; i < kSortItems; ++i) {
+  for (int i = 0; i < ITEMS; ++i) {
     const int64_t idx = base + i * 32 + lane;
-    if (idx < n) {
-      const uint32_t d = (kv[i].x >> shift) & (BINS - 1);
-      // tile_excl of digit d lives in the thread owning d; it is fetched below instead
-      r[i] += warp_hist[warp * BINS + d];
-    }
+    if (idx < n) r[i] += warp_hist[warp * BINS + ((kv[i].x >> shift) & (BINS - 1))];
   }
 #pragma unroll
   for (int q = 0; q < DPT; ++q) digit_off[tid + q * kSortThreads] = tile_excl[q];
   __syncthreads();
 #pragma unroll
-  for (int i = 0; i < kSortItems; ++i) {
+  for (int i = 0; i < ITEMS; ++i) {
     const int64_t idx = base + i * 32 + lane;
     if (idx < n) {
       const uint32_t d = (kv[i].x >> shift) & (BINS - 1);
@@ -214,7 +218,7 @@ k_onesweep(const uint2* __restrict__ in, uint2* __restrict__ out, int64_t n, int
 #pragma unroll
   for (int q = 0; q < DPT; ++q) digit_off[tid + q * kSortThreads] = hist_excl[q] + prev[q] - tile_excl[q];
   __syncthreads();
-  const int64_t cnt = n - tile0 < kSortTile ? n - tile0 : kSortTile;
+  const int64_t cnt = n - tile0 < TILE ? n - tile0 : TILE;
 #pragma unroll 4
   for (int j = tid; j < cnt; j += kSortThreads) {
     const uint2 x = stage[j];
@@ -223,9 +227,21 @@ k_onesweep(const uint2* __restrict__ in, uint2* __restrict__ out, int64_t n, int
   }
 }
 
-static size_t onesweep_smem(int bits) {
-  const int bins = 1 << bits;
-  return sizeof(uint2) * kSortTile + sizeof(uint32_t) * (NW * bins + bins + NW + 2);
+template <int BITS, int ITEMS, bool MATCH>
+static cudaError_t onesweep_pass(const uint2* a, uint2* b, int64_t n, int shift, const uint32_t* hist,
+                                 uint32_t* counter, unsigned long long* status, uint32_t epoch,
+                                 cudaStream_t s) {
+  constexpr int TILE = kSortThreads * ITEMS;
+  const size_t sm = sizeof(uint2) * TILE + sizeof(uint32_t) * (NW * (1 << BITS) + (1 << BITS) + NW + 2);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_onesweep<BITS, ITEMS, MATCH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    attr = true;
+  }
+  const int64_t tiles = (n + TILE - 1) / TILE;
+  k_onesweep<BITS, ITEMS, MATCH><<<(unsigned)tiles, kSortThreads, sm, s>>>(a, b, n, shift, hist, counter,
+                                                                          status, epoch);
+  return cudaGetLastError();
 }
 
 cudaError_t radix_sort_pairs(uint2* kv0, uint2* kv1, int64_t n, int bits, const SortWs& ws,
@@ -240,8 +256,7 @@ cudaError_t radix_sort_pairs(uint2* kv0, uint2* kv1, int64_t n, int bits, const 
   cudaError_t e = cudaMemsetAsync(ws.hist, 0, sizeof(uint32_t) * (kHistWords + kMaxPasses + 2), s);
   if (e != cudaSuccess) return e;
   if (passes == 0) return cudaSuccess;
-  const int64_t tiles = (n + kSortTile - 1) / kSortTile;
-  if (tiles > ws.max_tiles) return cudaErrorInvalidValue;
+  if ((n + kSortTileMin - 1) / kSortTileMin > ws.max_tiles) return cudaErrorInvalidValue;
   const int bins = 1 << dbits;
   {
     const int64_t want = (n + 128 * 8 - 1) / (128 * 8);
@@ -251,21 +266,26 @@ cudaError_t radix_sort_pairs(uint2* kv0, uint2* kv1, int64_t n, int bits, const 
     else k_radix_hist<8><<<grid, 128, sm, s>>>(kv0, n, passes, ws.hist);
     ++*launches;
   }
-  const size_t sm = onesweep_smem(dbits);
-  static bool attr_set[2] = {false, false};
-  if (!attr_set[dbits - 8]) {
-    if (dbits == 9) cudaFuncSetAttribute(k_onesweep<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    else cudaFuncSetAttribute(k_onesweep<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    attr_set[dbits - 8] = true;
-  }
+  static const int variant = [] {
+    const char* v = getenv("LIRANK_SORT_VARIANT");  // tuning experiments only
+    return v ? atoi(v) : 0;
+  }();
   uint2 *a = kv0, *b = kv1;
   for (int p = 0; p < passes; ++p) {
-    if (dbits == 9)
-      k_onesweep<9><<<(unsigned)tiles, kSortThreads, sm, s>>>(a, b, n, p * 9, ws.hist + p * bins,
-                                                              ws.counters + p, ws.status, epoch + p);
-    else
-      k_onesweep<8><<<(unsigned)tiles, kSortThreads, sm, s>>>(a, b, n, p * 8, ws.hist + p * bins,
-                                                              ws.counters + p, ws.status, epoch + p);
+    const int shift = p * dbits;
+    const uint32_t* hp = ws.hist + p * bins;
+    uint32_t* ctr = ws.counters + p;
+#define OS(BITS) \
+    switch (variant) { \
+      case 1: e = onesweep_pass<BITS, 8, false>(a, b, n, shift, hp, ctr, ws.status, epoch + p, s); break; \
+      case 2: e = onesweep_pass<BITS, 16, true>(a, b, n, shift, hp, ctr, ws.status, epoch + p, s); break; \
+      case 3: e = onesweep_pass<BITS, 12, false>(a, b, n, shift, hp, ctr, ws.status, epoch + p, s); break; \
+      case 4: e = onesweep_pass<BITS, 8, true>(a, b, n, shift, hp, ctr, ws.status, epoch + p, s); break; \
+      default: e = onesweep_pass<BITS, 16, false>(a, b, n, shift, hp, ctr, ws.status, epoch + p, s); \
+    }
+    if (dbits == 9) { OS(9) } else { OS(8) }
+#undef OS
+    if (e != cudaSuccess) return e;
     ++*launches;
     uint2* t = a; a = b; b = t;
   }
