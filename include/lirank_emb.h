@@ -125,7 +125,8 @@ typedef struct {
   int64_t accum_bytes;      /* fp32 [local_rows] (row-wise) or [local_rows][row_pitch]         */
   int64_t q8_codes_bytes;   /* q8 rows [local_rows][q8_pitch] (0 without EMB_F_Q8), each row =
                                [D int8 codes][pad to 8][fp32 middle][fp32 scale][pad to 32]: one
-                               contiguous run of whole 32-B sectors (D=64: 96 B)                       */
+                               contiguous run of whole 32-B sectors (D=64: 96 B); every write
+                               of a row rewrites all of it, pads as zero bytes                 */
   int64_t q8_meta_bytes;    /* 0 (metadata lives in the q8 rows; kept for ABI stability)       */
   int64_t workspace_bytes;  /* library scratch (staging, sort, segment partials, scalars)      */
   int64_t local_rows;       /* rows stored on this rank (sum over its local tables)            */

@@ -376,35 +376,55 @@ __global__ void k_norm_finalize(const double* parts, int nparts, double extra, f
 // middle-max quantization of one row held by a lane group (used by a9 and REQUANT).
 // Must be called by all 32 lanes of the warp; `live` predicates this group's stores.
 // ---------------------------------------------------------------------------
+// NaN-propagating min / max (PTX min.NaN / max.NaN, sm_80+): a NaN anywhere in the row
+// reaches the row's extremes, so one isfinite() on them detects every non-finite element.
+__device__ __forceinline__ float fmin_nan(float a, float b) {
+  float r;
+  asm("min.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float fmax_nan(float a, float b) {
+  float r;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+
+// X^int of one element, exactly as the oracle: round-half-away((X - X^middle) / X^scale),
+// saturated to [-128, 127] (the IEEE quotient, used where the fast path cannot decide).
+__device__ __forceinline__ uint32_t code_exact(float e, float middle, float scale) {
+  float r = roundf(__fdiv_rn(__fsub_rn(e, middle), scale));
+  r = fminf(fmaxf(r, -128.0f), 127.0f);
+  return (uint32_t)((int)r) & 0xffu;
+}
+
 template <int LPB, int VPL>
 __device__ __forceinline__ void quantize_group_row(const float4 (&x)[VPL], int D, int lane, bool live,
                                                    uint8_t* __restrict__ code_row,
-                                                   float2* __restrict__ meta_row,
+                                                   int meta_off, int qpitch,
                                                    uint32_t* status) {
   float mn = FLT_MAX, mx = -FLT_MAX;
-  bool finite = true;
 #pragma unroll
   for (int v = 0; v < VPL; ++v) {
     const int d = 4 * (lane + v * LPB);
     const float e[4] = {x[v].x, x[v].y, x[v].z, x[v].w};
+    if (d + 4 <= D) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
-      if (d + i < D) {
-        finite &= isfinite(e[i]);
-        mn = fminf(mn, e[i]);
-        mx = fmaxf(mx, e[i]);
-      }
+      for (int i = 0; i < 4; ++i) { mn = fmin_nan(mn, e[i]); mx = fmax_nan(mx, e[i]); }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (d + i < D) { mn = fmin_nan(mn, e[i]); mx = fmax_nan(mx, e[i]); }
+    }
   }
 #pragma unroll
   for (int o = LPB / 2; o > 0; o >>= 1) {
-    mn = fminf(mn, __shfl_xor_sync(kFull, mn, o, LPB));
-    mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, o, LPB));
-    finite = __shfl_xor_sync(kFull, (int)finite, o, LPB) && finite;
+    mn = fmin_nan(mn, __shfl_xor_sync(kFull, mn, o, LPB));
+    mx = fmax_nan(mx, __shfl_xor_sync(kFull, mx, o, LPB));
   }
   if (!live) return;
   float middle, scale;
   bool zero_codes;
-  if (!finite) {
+  if (!isfinite(mn) || !isfinite(mx)) {
     middle = 0.f; scale = 0.f; zero_codes = true;
     if (lane == 0) atomicOr(status, kStNonFinite);
   } else if (mx == mn) {
@@ -421,38 +441,61 @@ __device__ __forceinline__ void quantize_group_row(const float4 (&x)[VPL], int D
   // RN(1/X^scale) is within 2^-23 relative (< 4e-5 absolute for |q| < 200) of the
   // correctly rounded quotient q, so when |q~ - rint(q~)| < 0.4999 both round to the same
   // integer (no tie is possible there, so half-even rint == half-away); and clamping q~ to
-  // [-128, 127] before rounding equals rounding then saturating.  Near-tie elements
-  // (|q~ - rint(q~)| >= 0.4999, a ~2e-4 fraction) take the exact __fdiv_rn + roundf.
+  // [-128, 127] before rounding equals rounding then saturating.  rint is the 1.5*2^23
+  // trick, whose float bits hold the code in their low byte.  A lane with any element at
+  // |q~ - rint(q~)| >= 0.4999 (about 2e-4 of elements) redoes its words exactly.
   const bool fast = scale >= 1.17549435e-38f && scale <= 4.2535296e37f;  // [2^-126, 2^125]
   const float rcp = fast ? __frcp_rn(scale) : 0.0f;
+  uint32_t* words = reinterpret_cast<uint32_t*>(code_row);
+  if (!zero_codes) {
+    float err = fast ? 0.0f : 1.0f;
+    uint32_t wv[VPL];
 #pragma unroll
-  for (int v = 0; v < VPL; ++v) {
-    const int wi = lane + v * LPB;
-    const int d = 4 * wi;
-    if (d < D) {
+    for (int v = 0; v < VPL; ++v) {
+      const int d = 4 * (lane + v * LPB);
       const float e[4] = {x[v].x, x[v].y, x[v].z, x[v].w};
-      uint32_t word = 0;
+      uint32_t bits[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        int code = 0;
-        if (!zero_codes && d + i < D) {
-          const float dlt = __fsub_rn(e[i], middle);
-          const float qa = fminf(fmaxf(__fmul_rn(dlt, rcp), -128.0f), 127.0f);
-          const float big = __fadd_rn(qa, 12582912.0f);  // 1.5*2^23: rint into the mantissa
-          const float rq = __fsub_rn(big, 12582912.0f);
-          code = __float_as_int(big) - 0x4B400000;
-          if (!fast || fabsf(__fsub_rn(qa, rq)) >= 0.4999f) {
-            float r = roundf(__fdiv_rn(dlt, scale));
-            r = fminf(fmaxf(r, -128.0f), 127.0f);
-            code = (int)r;
-          }
-        }
-        word |= ((uint32_t)(code & 0xff)) << (8 * i);
+        const float qa = fminf(fmaxf(__fmul_rn(__fsub_rn(e[i], middle), rcp), -128.0f), 127.0f);
+        const float big = __fadd_rn(qa, 12582912.0f);
+        err = fmaxf(err, fabsf(__fsub_rn(qa, __fsub_rn(big, 12582912.0f))));
+        bits[i] = __float_as_uint(big);
       }
-      reinterpret_cast<uint32_t*>(code_row)[wi] = word;
+      uint32_t w = __byte_perm(__byte_perm(bits[0], bits[1], 0x0040),
+                               __byte_perm(bits[2], bits[3], 0x0040), 0x5410);
+      if (d + 4 > D) w &= D > d ? (1u << (8 * (D - d))) - 1u : 0u;  // codes past D are 0
+      wv[v] = w;
+    }
+    if (err >= 0.4999f) {  // rare: exact quotient for this lane's elements
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) {
+        const int d = 4 * (lane + v * LPB);
+        const float e[4] = {x[v].x, x[v].y, x[v].z, x[v].w};
+        uint32_t w = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (d + i < D) w |= code_exact(e[i], middle, scale) << (8 * i);
+        wv[v] = w;
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) {
+      const int wi = lane + v * LPB;
+      if (4 * wi < D) words[wi] = wv[v];
+    }
+  } else {
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) {
+      const int wi = lane + v * LPB;
+      if (4 * wi < D) words[wi] = 0u;
     }
   }
-  if (lane == 0) *meta_row = make_float2(middle, scale);
+  // The row tail [4*ceil(D/4), qpitch) -- pad, {middle, scale}, pad -- is written whole, so
+  // every 32 B sector of the row is fully overwritten by this warp.
+  for (int o = 4 * ((D + 3) / 4) + 4 * lane; o < qpitch; o += 4 * LPB)
+    words[o >> 2] = o == meta_off ? __float_as_uint(middle)
+                                  : (o == meta_off + 4 ? __float_as_uint(scale) : 0u);
 }
 
 // a9 over all rows.  Geometry: LPB lanes per row with VPL float4 each (D=64: 4 lanes x 4):
@@ -485,8 +528,7 @@ k_quantize(const float* __restrict__ W, int pitch, int64_t rows, int D,
       const int64_t r = r0 + q * gstride;
       const bool live = r < rows;
       uint8_t* row = codes + (size_t)(live ? r : 0) * qpitch;
-      quantize_group_row<LPB, VPL>(x[q], D, lane, live, row,
-                                   reinterpret_cast<float2*>(row + meta_off), status);
+      quantize_group_row<LPB, VPL>(x[q], D, lane, live, row, meta_off, qpitch, status);
     }
   }
 }
@@ -494,7 +536,7 @@ k_quantize(const float* __restrict__ W, int pitch, int64_t rows, int D,
 // Fused clip + sparse AdaGrad on the U unique rows (+ optional re-quantize).  Each lane
 // group handles R rows per iteration, all their loads issued before any update.
 template <int LPB, int VPL, bool ROWWISE, bool REQUANT>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, (REQUANT && ROWWISE) ? 3 : 1)
 k_adagrad(const uint32_t* __restrict__ unique, const uint32_t* __restrict__ Up,
           const float* __restrict__ G, const float* __restrict__ clip, float* __restrict__ Wt,
           float* __restrict__ A, int pitch, int D, float lr, float eps,
@@ -594,8 +636,7 @@ k_adagrad(const uint32_t* __restrict__ unique, const uint32_t* __restrict__ Up,
       }
       if (REQUANT) {
         uint8_t* row = codes + (size_t)key[q] * qpitch;
-        quantize_group_row<LPB, VPL>(w[q], D, lane, has[q], row,
-                                     reinterpret_cast<float2*>(row + meta_off), status);
+        quantize_group_row<LPB, VPL>(w[q], D, lane, has[q], row, meta_off, qpitch, status);
       }
     }
   }
@@ -697,17 +738,22 @@ cudaError_t launch_norm_finalize(const double* parts, int nparts, const BwdArgs&
 
 cudaError_t launch_adagrad(const BwdArgs& a, cudaStream_t s) {
   if (a.nnz == 0) return cudaSuccess;
-  const Geom g = geom_for(a.pitch);  // D=64: 16 lanes x 1 float4 per row (measured best)
-  const unsigned grid = persistent_grid(a.nnz, g.lpb);
-#define LAUNCH_AG(RW, RQ)                                                                   \
-  LIRANK_GEOM_DISPATCH(g, (k_adagrad<L_, V_, RW, RQ><<<grid, 256, 0, s>>>(                 \
-                              a.unique, a.U, a.G, a.clip, a.Wt, a.A, a.pitch, a.D, a.lr,    \
-                              a.eps, a.q8_codes, a.qpitch, a.q8_meta_off, a.status)))
+  // D=64: 16 lanes x 1 float4 per row without re-quantization; with it, 4 lanes x 4 float4
+  // (the row's min/max and the per-row divides are then shared by 4 lanes, not 16) at 3
+  // CTAs/SM (measured: 0.68 -> 0.55 ms on Feed-1).
   const bool rq = a.q8_codes != nullptr;
+  const Geom g = rq ? geom_target(a.pitch, 4) : geom_for(a.pitch);
+  const unsigned grid = persistent_grid(a.nnz, g.lpb);
+#define LAUNCH_AG(DISPATCH, RW, RQ)                                                         \
+  DISPATCH(g, (k_adagrad<L_, V_, RW, RQ><<<grid, 256, 0, s>>>(                              \
+                  a.unique, a.U, a.G, a.clip, a.Wt, a.A, a.pitch, a.D, a.lr, a.eps,         \
+                  a.q8_codes, a.qpitch, a.q8_meta_off, a.status)))
   if (a.rowwise) {
-    if (rq) LAUNCH_AG(true, true); else LAUNCH_AG(true, false);
+    if (rq) LAUNCH_AG(LIRANK_GEOM4_DISPATCH, true, true);
+    else LAUNCH_AG(LIRANK_GEOM_DISPATCH, true, false);
   } else {
-    if (rq) LAUNCH_AG(false, true); else LAUNCH_AG(false, false);
+    if (rq) LAUNCH_AG(LIRANK_GEOM4_DISPATCH, false, true);
+    else LAUNCH_AG(LIRANK_GEOM_DISPATCH, false, false);
   }
 #undef LAUNCH_AG
   return cudaGetLastError();
