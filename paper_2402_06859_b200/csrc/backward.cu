@@ -536,7 +536,7 @@ k_quantize(const float* __restrict__ W, int pitch, int64_t rows, int D,
 // Fused clip + sparse AdaGrad on the U unique rows (+ optional re-quantize).  Each lane
 // group handles R rows per iteration, all their loads issued before any update.
 template <int LPB, int VPL, bool ROWWISE, bool REQUANT>
-__global__ void __launch_bounds__(256, (REQUANT && ROWWISE) ? 3 : 1)
+__global__ void __launch_bounds__(256, (REQUANT && !ROWWISE) ? 1 : 3)
 k_adagrad(const uint32_t* __restrict__ unique, const uint32_t* __restrict__ Up,
           const float* __restrict__ G, const float* __restrict__ clip, float* __restrict__ Wt,
           float* __restrict__ A, int pitch, int D, float lr, float eps,
