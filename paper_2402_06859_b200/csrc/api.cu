@@ -216,9 +216,11 @@ void carve(const Plan& p, Carver& cv, emb_handle* h) {
   auto* sg = cv.take<double>(1);
   auto* cl = cv.take<float>(1);
   auto* st = cv.take<uint32_t>(1);
+  auto* order = cv.take<uint32_t>(kOrderWsWords(std::max<int64_t>(F * Bmax, bags_cap)));
   ExchangeWs x{};
   if (p.exch) carve_exchange(p, cv, &x);
   if (h) {
+    h->order_ws = order;
     h->d_meta = meta;
     h->stage_ids = stage_ids;
     h->stage_off = stage_off;
@@ -684,11 +686,12 @@ emb_status emb_forward(emb_t h, const int32_t* ids, const int32_t* offsets, int3
     a.sentinel = (uint32_t)p.local_rows;
     a.status = h->d_status;
     a.mean = p.pooling == EMB_POOL_MEAN;
+    a.order_ws = h->order_ws;
     {
       Phase ph(h->prof, h->stream, EMB_PH_FWD);
       CK(launch_pool_fwd_f32(a, h->stream));
     }
-    h->launches += (int64_t)p.F * batch > 0;
+    h->launches += fwd_launches((int64_t)p.F * batch, true);
     if (a.mean) {
       Phase ph(h->prof, h->stream, EMB_PH_COPY);
       CK(cudaMemcpyAsync(h->off_copy, st.offsets, sizeof(int) * ((int64_t)p.F * batch + 1),
@@ -737,11 +740,12 @@ emb_status emb_forward_q8(emb_t h, const int32_t* ids, const int32_t* offsets, i
     a.out = st.out;
     a.status = h->d_status;
     a.mean = p.pooling == EMB_POOL_MEAN;
+    a.order_ws = h->order_ws;
     {
       Phase ph(h->prof, h->stream, EMB_PH_FWD_Q8);
       CK(launch_pool_fwd_q8(a, h->stream));
     }
-    h->launches += (int64_t)p.F * batch > 0;
+    h->launches += fwd_launches((int64_t)p.F * batch, true);
   }
   if (st.host_out) {
     Phase ph(h->prof, h->stream, EMB_PH_COPY);

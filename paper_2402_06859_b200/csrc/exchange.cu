@@ -309,6 +309,7 @@ emb_status exchange_forward(emb_t h, const Staged& st, int32_t batch, int64_t nn
     a.kv_out = h->kvA;
     a.sentinel = (uint32_t)p.local_rows;
     a.status = h->d_status;
+    a.order_ws = h->order_ws;
     Phase ph(h->prof, h->stream, EMB_PH_FWD);
     CK(launch_pool_fwd_f32(a, h->stream));
   } else {
@@ -326,10 +327,11 @@ emb_status exchange_forward(emb_t h, const Staged& st, int32_t batch, int64_t nn
     a.meta = x.ident;
     a.out = x.pooled;
     a.status = h->d_status;
+    a.order_ws = h->order_ws;
     Phase ph(h->prof, h->stream, EMB_PH_FWD_Q8);
     CK(launch_pool_fwd_q8(a, h->stream));
   }
-  h->launches += (int64_t)W * Fr * B > 0;
+  h->launches += fwd_launches((int64_t)W * Fr * B, true);
   // ---- a3: pooled exchange back ----------------------------------------------------------
   {
     Phase ph(h->prof, h->stream, EMB_PH_EXCHANGE);

@@ -143,6 +143,7 @@ struct emb_handle {
   uint8_t* codes = nullptr;
   int q8_meta_off = 0;  // byte offset of {middle, scale} inside a q8 row
   // workspace
+  uint32_t* order_ws = nullptr;  // bag order of the pooling kernels (kOrderWsWords)
   lirank::FeatMeta* d_meta = nullptr;
   int* stage_ids = nullptr;
   int* stage_off = nullptr;

@@ -21,8 +21,19 @@ struct FwdArgs {
   uint32_t sentinel;
   uint32_t* status;
   bool mean;
+  uint32_t* order_ws;  // NULL: bags in index order; else [kOrderWsWords(F*B)] scratch
 };
 cudaError_t launch_pool_fwd_f32(const FwdArgs& a, cudaStream_t s);
+
+// Bags visited longest first: a permutation of the F*B bags by length (256 bins), so the
+// lane groups of a warp walk bags of about the same length (the id loop runs to the warp's
+// longest bag).  Scratch: the permutation + 2 x 256 bin counters.
+constexpr int kLenBins = 256;
+inline int64_t kOrderWsWords(int64_t bags) { return bags + 2 * kLenBins; }
+// kernels one forward launch issues (the pooling kernel, plus the 2 ordering kernels)
+inline int fwd_launches(int64_t bags, bool ordered) {
+  return bags <= 0 ? 0 : (ordered && bags >= 2 ? 3 : 1);
+}
 
 struct FwdQ8Args {
   const uint8_t* codes;   // q8 rows: [codes][pad][middle, scale][pad], qpitch bytes
@@ -36,6 +47,7 @@ struct FwdQ8Args {
   float* out;
   uint32_t* status;
   bool mean;
+  uint32_t* order_ws;  // as FwdArgs::order_ws
 };
 cudaError_t launch_pool_fwd_q8(const FwdQ8Args& a, cudaStream_t s);
 
