@@ -54,6 +54,9 @@ def lib():
             "ora_quantize_mm8": (i64, [P, i64, i32, P, P, P]),
             "ora_forward_q8": (i64, [P, P, P, P, P, P, i32, P]),
             "ora_train_step": (i32, [P, P, P, i32, P, P, i32, P, f32, f32, f32, f64, P, P, P, P]),
+            "ora_murmur3_x64_128": (None, [P, i64, C.c_uint32, P]),
+            "ora_hash_ids": (None, [P, P, i64, P]),
+            "ora_qr_expand": (None, [P, P, i64, i64, i32, i64, i32, P, P]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -192,3 +195,45 @@ def train_step(pb: Problem, W, A, ids, offsets, B, grad, lr, eps, max_norm,
                               B, _p(grad), float(lr), float(eps), float(max_norm), float(extra_sq_norm),
                               _p(out), C.byref(S), C.byref(c), C.byref(U))
     return dict(out=out, S=S.value, c=np.float32(c.value), U=U.value, nonfinite=bool(nf))
+
+
+# ---- NEXT-1: unlimited-dictionary ids (oracle.h: ora_murmur3_x64_128, ora_qr_expand) ----
+
+def murmur3_x64_128(key: bytes, seed: int = 0):
+    """(h1, h2) of MurmurHash3 x64-128."""
+    buf = np.frombuffer(bytes(key), dtype=np.uint8).copy() if len(key) else np.zeros(1, np.uint8)
+    out = np.zeros(2, dtype=np.uint64)
+    lib().ora_murmur3_x64_128(_p(buf), len(key), seed, _p(out))
+    return int(out[0]), int(out[1])
+
+
+def pack_strings(strings):
+    """UTF-8 bytes of the strings concatenated + int64 offsets [n+1]."""
+    enc = [s.encode("utf-8") if isinstance(s, str) else bytes(s) for s in strings]
+    off = np.zeros(len(enc) + 1, dtype=np.int64)
+    off[1:] = np.cumsum([len(e) for e in enc])
+    data = np.frombuffer(b"".join(enc), dtype=np.uint8).copy() if off[-1] else np.zeros(1, np.uint8)
+    return data, off
+
+
+def hash_ids(strings):
+    """int64 ids (as uint64) of id strings: h1 of MurmurHash3 x64-128, seed 0."""
+    data, off = pack_strings(strings)
+    h = np.zeros(max(len(strings), 1), dtype=np.uint64)
+    lib().ora_hash_ids(_p(data), _p(off), len(strings), _p(h))
+    return h[:len(strings)]
+
+
+def qr_expand(h, offsets, R: int, Q: int, dual: bool):
+    """QR expansion of hashed ids into rows of the concatenated QR table (oracle.h)."""
+    h = np.ascontiguousarray(h, dtype=np.uint64)
+    offsets = _i32(offsets)
+    k = 4 if dual else 2
+    ids = np.zeros(max(k * len(h), 1), dtype=np.int32)
+    off = np.zeros(len(offsets), dtype=np.int32)
+    lib().ora_qr_expand(_p(h), _p(offsets), len(offsets) - 1, len(h), R, Q, 1 if dual else 0, _p(ids), _p(off))
+    return ids[:k * len(h)], off
+
+
+def qr_rows(R: int, Q: int, dual: bool) -> int:
+    return (2 if dual else 1) * (Q + R)

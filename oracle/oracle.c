@@ -323,3 +323,72 @@ int32_t ora_train_step(const ora_cfg* c, float* W, float* A, int32_t adagrad_mod
   free(keys); free(segs); free(bags); free(G);
   return nonfinite ? 1 : 0;
 }
+
+/* ------------------------------------------------------------------------------------ */
+/* NEXT-1: MurmurHash3 x64-128 (Austin Appleby's public-domain algorithm, written out from
+ * its definition: 16-byte blocks mixed into h1/h2 with constants c1, c2, a tail of 0..15
+ * bytes, then the length and the 64-bit finalizer fmix64).                              */
+static uint64_t rotl64(uint64_t x, int r) { return (x << r) | (x >> (64 - r)); }
+static uint64_t fmix64(uint64_t k) {
+  k ^= k >> 33;
+  k *= 0xff51afd7ed558ccdULL;
+  k ^= k >> 33;
+  k *= 0xc4ceb9fe1a85ec53ULL;
+  k ^= k >> 33;
+  return k;
+}
+static uint64_t load_le64(const uint8_t* p) {
+  uint64_t v = 0;
+  for (int i = 7; i >= 0; --i) v = (v << 8) | p[i];
+  return v;
+}
+
+void ora_murmur3_x64_128(const uint8_t* key, int64_t len, uint32_t seed, uint64_t out[2]) {
+  const uint64_t c1 = 0x87c37b91114253d5ULL, c2 = 0x4cf5ad432745937fULL;
+  uint64_t h1 = seed, h2 = seed;
+  const int64_t nblocks = len / 16;
+  for (int64_t i = 0; i < nblocks; ++i) {
+    uint64_t k1 = load_le64(key + 16 * i), k2 = load_le64(key + 16 * i + 8);
+    k1 *= c1; k1 = rotl64(k1, 31); k1 *= c2; h1 ^= k1;
+    h1 = rotl64(h1, 27); h1 += h2; h1 = h1 * 5 + 0x52dce729;
+    k2 *= c2; k2 = rotl64(k2, 33); k2 *= c1; h2 ^= k2;
+    h2 = rotl64(h2, 31); h2 += h1; h2 = h2 * 5 + 0x38495ab5;
+  }
+  const uint8_t* tail = key + 16 * nblocks;
+  const int rem = (int)(len & 15);
+  uint64_t k1 = 0, k2 = 0;
+  for (int i = rem - 1; i >= 8; --i) k2 = (k2 << 8) | tail[i];  /* bytes 8..14 */
+  if (rem > 8) { k2 *= c2; k2 = rotl64(k2, 33); k2 *= c1; h2 ^= k2; }
+  for (int i = (rem < 8 ? rem : 8) - 1; i >= 0; --i) k1 = (k1 << 8) | tail[i];  /* 0..7 */
+  if (rem > 0) { k1 *= c1; k1 = rotl64(k1, 31); k1 *= c2; h1 ^= k1; }
+  h1 ^= (uint64_t)len; h2 ^= (uint64_t)len;
+  h1 += h2; h2 += h1;
+  h1 = fmix64(h1); h2 = fmix64(h2);
+  h1 += h2; h2 += h1;
+  out[0] = h1;
+  out[1] = h2;
+}
+
+void ora_hash_ids(const uint8_t* bytes, const int64_t* str_off, int64_t n, uint64_t* h) {
+  for (int64_t i = 0; i < n; ++i) {
+    uint64_t d[2];
+    ora_murmur3_x64_128(bytes + str_off[i], str_off[i + 1] - str_off[i], 0u, d);
+    h[i] = d[0];
+  }
+}
+
+void ora_qr_expand(const uint64_t* h, const int32_t* offsets, int64_t nbags, int64_t nnz,
+                   int32_t R, int64_t Q, int32_t dual, int32_t* ids_out, int32_t* offsets_out) {
+  const int k = dual ? 4 : 2;
+  for (int64_t b = 0; b <= nbags; ++b) offsets_out[b] = k * offsets[b];
+  for (int64_t i = 0; i < nnz; ++i) {
+    const uint32_t nB = (uint32_t)(h[i] & 0xffffffffULL);  /* bitcast: low half  = B */
+    const uint32_t nC = (uint32_t)(h[i] >> 32);            /*          high half = C */
+    ids_out[k * i + 0] = (int32_t)((int64_t)(nB / (uint32_t)R) % Q);
+    ids_out[k * i + 1] = (int32_t)(Q + (int64_t)(nB % (uint32_t)R));
+    if (dual) {
+      ids_out[k * i + 2] = (int32_t)(Q + R + (int64_t)(nC / (uint32_t)R) % Q);
+      ids_out[k * i + 3] = (int32_t)(2 * Q + R + (int64_t)(nC % (uint32_t)R));
+    }
+  }
+}

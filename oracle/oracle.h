@@ -108,6 +108,31 @@ int32_t ora_train_step(const ora_cfg* c, float* W, float* A, int32_t adagrad_mod
                        double extra_sq_norm, float* out, double* S_out, float* c_out,
                        int64_t* U_out);
 
+/* ---- NEXT-1: unlimited-dictionary ids ----
+ *
+ * hash_id: "a collision-resistant hashing function like MurmurHash" mapping the
+ * id string "to a space of int64".  MurmurHash3, x64 128-bit variant, seed 0
+ * (SPEC.md:290), of the UTF-8 bytes; the int64 is the first 8 bytes of the digest read
+ * little-endian, i.e. the variant's h1.  out[0] = h1, out[1] = h2. */
+void ora_murmur3_x64_128(const uint8_t* key, int64_t len, uint32_t seed, uint64_t out[2]);
+
+/* hash of n strings: string i = bytes[str_off[i] .. str_off[i+1]) -> h1. */
+void ora_hash_ids(const uint8_t* bytes, const int64_t* str_off, int64_t n, uint64_t* h);
+
+/* QR expansion ("quotient and remainder", "bitcast to convert this int64 to
+ * two numbers in int32 space (ranging from 0 to 2^32-1), B and C which will look from
+ * independent sets of QR tables"; SPEC.md:300 for the indexing).  One feature's QR tables
+ * are stored as ONE table, concatenated: [quotient_B: Q rows][remainder_B: R rows] and, in
+ * dual mode, [quotient_C: Q][remainder_C: R].  For n = low 32 bits of h (B) and, in dual
+ * mode, n' = high 32 bits (C), id i expands to the rows, in this order,
+ *   (n / R) mod Q,  Q + n mod R  [,  Q + R + (n' / R) mod Q,  2Q + R + n' mod R]
+ * (unsigned 32-bit n).  Sum aggregation ("sum aggregation worked the best") of the
+ * expanded rows is then a SUM-pooled bag over them: offsets_out[b] = k * offsets[b] with
+ * k = 2 (single) or 4 (dual), ids_out[k*i + j] = row j of id i.
+ * Rows of the concatenated table: k/2 * (Q + R). */
+void ora_qr_expand(const uint64_t* h, const int32_t* offsets, int64_t nbags, int64_t nnz,
+                   int32_t R, int64_t Q, int32_t dual, int32_t* ids_out, int32_t* offsets_out);
+
 #ifdef __cplusplus
 }
 #endif
