@@ -266,6 +266,34 @@ EMB_API emb_status emb_profile_read(emb_t h, double* ms, int64_t* count, int32_t
 /* Release the handle (and its NCCL communicator).  Does not free caller buffers. */
 EMB_API emb_status emb_destroy(emb_t h);
 
+/* ---- NEXT-1: unlimited-dictionary ids (stateless; no handle) ------------------------------
+ * PAPER.md:335 ("QR hashing ... a collision-resistant hashing function like MurmurHash",
+ * "sum aggregation worked the best") and PAPER.md:602 ("mapped with ... Murmur hashing to a
+ * space of int64 ... bitcast to convert this int64 to two numbers in int32 space (ranging
+ * from 0 to 2^32-1), B and C which will look from independent sets of QR tables").
+ * All pointers are DEVICE pointers (EMB_EINVAL otherwise); the work is enqueued on `stream`
+ * (a cudaStream_t, NULL = legacy default stream) and the call returns without waiting.
+ *
+ * emb_hash_ids: hashes[i] = h1 of MurmurHash3 x64-128, seed 0, of the UTF-8 bytes
+ *   bytes[str_offsets[i] .. str_offsets[i+1]) (i < n; offsets non-decreasing, int64).
+ *
+ * emb_qr_expand: one QR feature's tables live in ONE table of emb_qr_rows(R, Q, dual) rows,
+ *   concatenated [quotient_B: Q][remainder_B: R] (+ [quotient_C: Q][remainder_C: R] when
+ *   dual).  With n = low 32 bits of hashes[i] and n' = high 32 bits (unsigned), id i becomes
+ *   the rows (in this order) (n / R) mod Q, Q + n mod R [, Q+R + (n'/R) mod Q, 2Q+R + n' mod R]
+ *   at ids_out[k*i ..], k = 2 (single) or 4 (dual), and offsets_out[b] = k * offsets[b]
+ *   (b <= nbags).  Pooling the expanded bags with SUM (emb_forward) is the paper's sum
+ *   aggregation; their gradients flow to exactly the expanded rows (emb_backward_adagrad).
+ *   Requires 1 <= R, 1 <= Q and emb_qr_rows(R, Q, dual) < 2^31 (EMB_EINVAL otherwise);
+ *   ids_out holds k*nnz int32, offsets_out nbags+1 int32. */
+EMB_API emb_status emb_hash_ids(const uint8_t* bytes, const int64_t* str_offsets, int64_t n,
+                                uint64_t* hashes, void* stream);
+EMB_API emb_status emb_qr_expand(const uint64_t* hashes, const int32_t* offsets, int64_t nbags,
+                                 int64_t nnz, int32_t R, int64_t Q, int32_t dual,
+                                 int32_t* ids_out, int32_t* offsets_out, void* stream);
+/* rows of one feature's concatenated QR table: (dual ? 2 : 1) * (Q + R) */
+EMB_API int64_t emb_qr_rows(int32_t R, int64_t Q, int32_t dual);
+
 #ifdef __cplusplus
 }
 #endif

@@ -98,6 +98,9 @@ SIGNATURES = {
     "emb_profile": (C.c_int, [P, C.c_int32]),
     "emb_profile_read": (C.c_int, [P, P, P, C.c_int32]),
     "emb_destroy": (C.c_int, [P]),
+    "emb_hash_ids": (C.c_int, [P, P, C.c_int64, P, P]),
+    "emb_qr_expand": (C.c_int, [P, P, C.c_int64, C.c_int64, C.c_int32, C.c_int64, C.c_int32, P, P, P]),
+    "emb_qr_rows": (C.c_int64, [C.c_int32, C.c_int64, C.c_int32]),
 }
 
 _lib = None

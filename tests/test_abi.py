@@ -133,3 +133,12 @@ def test_table_plan_explicit_owner_and_lpt():
     cfg, keep = make_cfg(rows, 8, [0, 1, 2, 3], sharding=L.EMB_SHARD_TABLE, rank=0, world_size=2)
     lb, lo, hi = layout(cfg, 4)
     assert (lb >= 0).tolist() == [False, True, False, False]
+
+
+def test_qr_rows_host_only():
+    """emb_qr_rows is host arithmetic (no device needed): (dual ? 2 : 1) * (Q + R)."""
+    from paper_2402_06859_b200 import _lib as L
+    lib = L.load()
+    assert lib.emb_qr_rows(1000, 4294968, 1) == 2 * (4294968 + 1000)
+    assert lib.emb_qr_rows(7, 11, 0) == 18
+    assert lib.emb_qr_rows(0, 11, 0) < 0 and lib.emb_qr_rows(7, 0, 1) < 0
