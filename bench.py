@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--adagrad", default="rowwise", choices=["rowwise", "elementwise"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-qr", action="store_true", help="skip the NEXT-1 QR/Murmur section")
     ap.add_argument("--cpu-samples", type=int, default=8192)
     return ap.parse_args()
 
@@ -232,6 +233,115 @@ def run_reference(args, cfg, rank, world):
     }
     print(json.dumps(line), flush=True)
 
+
+
+# ---------------------------------------------------------------------------
+# NEXT-1 section: unlimited-dictionary ids (hash -> QR expand -> train step on QR tables)
+# ---------------------------------------------------------------------------
+
+def id_strings(ids, prefix: bytes):
+    """UTF-8 bytes of prefix + decimal(id) for every id (vectorised) + int64 offsets."""
+    ids = np.asarray(ids, dtype=np.int64)
+    n = len(ids)
+    nd = 1 + sum((ids >= 10 ** k).astype(np.int64) for k in range(1, 10))
+    maxd = int(nd.max()) if n else 1
+    digits = np.zeros((n, maxd), dtype=np.uint8)
+    x = ids.copy()
+    for j in range(maxd - 1, -1, -1):
+        digits[:, j] = 48 + x % 10
+        x //= 10
+    pre = np.frombuffer(prefix, dtype=np.uint8)
+    mat = np.concatenate([np.broadcast_to(pre, (n, len(pre))), digits], axis=1)
+    keep = np.concatenate([np.ones((n, len(pre)), bool), np.arange(maxd)[None, :] >= (maxd - nd)[:, None]], axis=1)
+    lens = len(pre) + nd
+    off = np.zeros(n + 1, dtype=np.int64)
+    off[1:] = np.cumsum(lens)
+    return mat[keep], off
+
+
+def qr_section(cfg, ids, off, B, dev, stream, flush, hbm_peak, reps=5):
+    """Feed-1 ids as strings ("member:<id>", "hashtag:<id>") -> emb_hash_ids -> emb_qr_expand
+    (dual, R = 1000, Q = ceil(2^32 / R): P:335's 1000x example) -> a2 + a5-a8 on the QR tables.
+    CUDA events on the library stream, L2 flushed before each repetition."""
+    import torch
+
+    from paper_2402_06859_b200 import ShardedEmbedding, qr
+    from workload import gpu as G
+    R = 1000
+    Q = -(-(1 << 32) // R)
+    F, D = cfg.num_features, cfg.dim
+    prefixes = [b"member:", b"hashtag:"] + [b"t%d:" % t for t in range(2, cfg.num_tables)]
+    datas, offs, base = [], [np.zeros(1, np.int64)], 0
+    for f in range(F):
+        a, b = off[f * B], off[(f + 1) * B]
+        d, o = id_strings(ids[a:b], prefixes[cfg.feature_table[f]])
+        datas.append(d)
+        offs.append(o[1:] + base)
+        base += int(o[-1])
+    data = torch.from_numpy(np.concatenate(datas)).to(dev)
+    soff = torch.from_numpy(np.concatenate(offs)).to(dev)
+    offd = torch.from_numpy(off).to(dev)
+    nnz = len(ids)
+    h = torch.empty(nnz, dtype=torch.int64, device=dev)
+    ids_x = torch.empty(4 * nnz, dtype=torch.int32, device=dev)
+    off_x = torch.empty(F * B + 1, dtype=torch.int32, device=dev)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(2)]
+
+    def timed(fn):
+        # a ~0.5 ms device spin before the start event keeps the GPU busy while the host
+        # enqueues the calls, so host launch overhead is not inside the events
+        ts = []
+        for _ in range(reps):
+            G.flush_l2(flush, stream=stream)
+            with torch.cuda.stream(stream):
+                torch.cuda._sleep(1_000_000)
+                ev[0][0].record(stream)
+                fn()
+                ev[0][1].record(stream)
+            stream.synchronize()
+            ts.append(ev[0][0].elapsed_time(ev[0][1]))
+        return float(np.median(ts))
+
+    with torch.cuda.stream(stream):
+        hash_ms = timed(lambda: qr.hash_ids(data, soff, out=h))
+        exp_ms = timed(lambda: qr.qr_expand(h, offd, R, Q, True, ids_out=ids_x, offsets_out=off_x))
+    rows = [qr.qr_rows(R, Q, True)] * cfg.num_tables
+    emb = ShardedEmbedding(rows, D, cfg.feature_table, max_nnz=4 * nnz, max_batch=B, device=dev, stream=stream)
+    with torch.cuda.stream(stream):
+        for t in range(cfg.num_tables):
+            v = emb.table_view(t)
+            G.fill_table(v, v.shape[0], D, emb.pitch, cfg.seed, t, stream=stream)
+        gd = torch.empty((B, F, D), device=dev)
+        G.fill_grad(gd, B, F, D, cfg.seed, 0, gen.grad_shift_for(4 * nnz, D), stream=stream)
+        out = torch.empty((B, F, D), device=dev)
+    for _ in range(3):
+        emb.forward(ids_x, off_x, B, out=out)
+        emb.backward_adagrad(gd, LR)
+    stream.synchronize()
+    emb.profile(True)
+    emb.profile_read(reset=True)
+    step_ms = timed(lambda: (emb.forward(ids_x, off_x, B, out=out), emb.backward_adagrad(gd, LR)))
+    ph = emb.profile_read()
+    emb.profile(False)
+    assert emb.sync() == 0
+    fwd_ms = ph["fwd"][0] / max(ph["fwd"][1], 1)
+    _, _, U = emb.last_stats()
+    sbytes = int(soff[-1].item())
+    hash_b = sbytes + 8 * (nnz + 1) + 8 * nnz
+    exp_b = 8 * nnz + 16 * nnz + 8 * (F * B + 1)
+    res = {
+        "what": "Feed-1 batch 0 ids as strings -> emb_hash_ids (MurmurHash3 x64-128) -> emb_qr_expand "
+                "(dual, R=1000, Q=ceil(2^32/R)) -> a2 + a5-a8 on the two QR tables (4 rows per id)",
+        "strings": nnz, "string_bytes": sbytes, "qr_rows_per_table": rows[0], "unique_rows": U,
+        "hash_ms": hash_ms, "hash_strings_per_s": nnz / (hash_ms / 1e3),
+        "hash_gbs": hash_b / (hash_ms / 1e3) / 1e9, "hash_frac_of_hbm": hash_b / (hash_ms / 1e3) / 1e9 / hbm_peak,
+        "expand_ms": exp_ms, "expand_ids_per_s": nnz / (exp_ms / 1e3),
+        "expand_gbs": exp_b / (exp_ms / 1e3) / 1e9, "expand_frac_of_hbm": exp_b / (exp_ms / 1e3) / 1e9 / hbm_peak,
+        "train_step_ms": step_ms, "train_samples_per_s": B / (step_ms / 1e3), "fwd_ms": fwd_ms,
+        "qr_lookups_per_s": 4 * nnz / (fwd_ms / 1e3),
+    }
+    del emb
+    return res
 
 # ---------------------------------------------------------------------------
 # our arm
@@ -473,6 +583,11 @@ def run_ours(args, cfg, rank, world, local_rank):
         "e2e": e2e,
         "clip": {"sq_norm": S, "c": float(c)},
     }
+    if world == 1 and not args.no_qr:
+        try:
+            line["qr"] = qr_section(cfg, batches[0][0], batches[0][1], B, dev, stream, flush, hbm_peak)
+        except Exception as e:  # report, never hide
+            line["qr"] = {"error": repr(e)}
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
             line["cpu_baseline"] = cpu_baseline(cfg, batches[0][0], batches[0][1], B, args.cpu_samples,

@@ -1,8 +1,9 @@
 // qr.cu -- NEXT-1: unlimited-dictionary ids.
 //
 // emb_hash_ids: MurmurHash3 x64-128 (seed 0) of id strings -> the int64 id (h1).  One
-//   thread per string (ids are short: "member:1234"); bytes are read with __ldg, 16-byte
-//   blocks mixed as the algorithm defines, then the 0..15-byte tail and fmix64.
+//   thread per string (ids are short: "member:1234"); each warp stages its 32 strings'
+//   contiguous bytes in shared memory with 16-B loads, then every thread mixes its 16-byte
+//   blocks as the algorithm defines, the 0..15-byte tail and fmix64.
 // emb_qr_expand: the int64 is bitcast to two 32-bit numbers B (low) and C (high); each
 //   indexes its own quotient/remainder table pair, and the rows are laid out in ONE
 //   concatenated table [qB | rB | qC | rC] so the expanded bag goes through the ordinary
@@ -26,42 +27,95 @@ __device__ __forceinline__ uint64_t fmix64(uint64_t k) {
   return k;
 }
 
-__device__ __forceinline__ uint64_t le64(const uint8_t* __restrict__ p) {
+// 8 little-endian bytes at any byte address p of a shared-memory buffer: three aligned
+// 32-bit loads and two funnel shifts (no byte loop).  Reads up to 11 bytes past p + 8.
+__device__ __forceinline__ uint64_t le64_smem(const uint8_t* p) {
+  const uintptr_t a = (uintptr_t)p;
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(a & ~(uintptr_t)3);
+  const uint32_t sh = 8u * (uint32_t)(a & 3);
+  const uint32_t w0 = w[0], w1 = w[1], w2 = w[2];
+  const uint32_t lo = __funnelshift_r(w0, w1, sh), hi = __funnelshift_r(w1, w2, sh);
+  return ((uint64_t)hi << 32) | lo;
+}
+__device__ __forceinline__ uint64_t le64_global(const uint8_t* p) {
   uint64_t v = 0;
 #pragma unroll
   for (int i = 7; i >= 0; --i) v = (v << 8) | (uint64_t)__ldg(p + i);
   return v;
 }
+// the low `nb` bytes (0..8) of x
+__device__ __forceinline__ uint64_t low_bytes(uint64_t x, int nb) {
+  return nb >= 8 ? x : (x & ((1ull << (8 * nb)) - 1ull));
+}
 
-__global__ void __launch_bounds__(256)
+// h1 of MurmurHash3 x64-128, seed 0, of key[0 .. len).  SMEM: key is in shared memory with
+// at least 16 readable bytes past its end (the tail is read as two masked 8-byte words);
+// otherwise key is global and the tail is assembled byte by byte.
+template <bool SMEM>
+__device__ __forceinline__ uint64_t murmur3_h1(const uint8_t* key, int64_t len) {
+  constexpr uint64_t c1 = 0x87c37b91114253d5ULL, c2 = 0x4cf5ad432745937fULL;
+  uint64_t h1 = 0, h2 = 0;
+  const int64_t nblocks = len >> 4;
+  for (int64_t b = 0; b < nblocks; ++b) {
+    uint64_t k1 = SMEM ? le64_smem(key + 16 * b) : le64_global(key + 16 * b);
+    uint64_t k2 = SMEM ? le64_smem(key + 16 * b + 8) : le64_global(key + 16 * b + 8);
+    k1 *= c1; k1 = rotl64(k1, 31); k1 *= c2; h1 ^= k1;
+    h1 = rotl64(h1, 27); h1 += h2; h1 = h1 * 5 + 0x52dce729;
+    k2 *= c2; k2 = rotl64(k2, 33); k2 *= c1; h2 ^= k2;
+    h2 = rotl64(h2, 31); h2 += h1; h2 = h2 * 5 + 0x38495ab5;
+  }
+  const uint8_t* tail = key + 16 * nblocks;
+  const int rem = (int)(len & 15);
+  uint64_t k1 = 0, k2 = 0;
+  if (SMEM) {
+    k1 = low_bytes(le64_smem(tail), min(rem, 8));
+    k2 = low_bytes(le64_smem(tail + 8), max(rem - 8, 0));
+  } else {
+    for (int j = rem - 1; j >= 8; --j) k2 = (k2 << 8) | (uint64_t)__ldg(tail + j);
+    for (int j = min(rem, 8) - 1; j >= 0; --j) k1 = (k1 << 8) | (uint64_t)__ldg(tail + j);
+  }
+  if (rem > 8) { k2 *= c2; k2 = rotl64(k2, 33); k2 *= c1; h2 ^= k2; }
+  if (rem > 0) { k1 *= c1; k1 = rotl64(k1, 31); k1 *= c2; h1 ^= k1; }
+  h1 ^= (uint64_t)len; h2 ^= (uint64_t)len;
+  h1 += h2; h2 += h1;
+  h1 = fmix64(h1); h2 = fmix64(h2);
+  return h1 + h2;
+}
+
+// One thread per string.  A warp's 32 strings are one contiguous byte range; when it fits
+// kWarpBytes it is staged in shared memory with 16-B loads (aligned down to 16 B, so the
+// last load may touch up to 15 bytes past the range inside the same aligned 16-B block),
+// and the threads hash from shared memory instead of issuing one byte load per byte.
+constexpr int kHashWarps = 8;
+constexpr int kWarpBytes = 2048;
+
+__global__ void __launch_bounds__(32 * kHashWarps)
 k_hash_ids(const uint8_t* __restrict__ bytes, const int64_t* __restrict__ str_off, int64_t n,
            uint64_t* __restrict__ out) {
-  constexpr uint64_t c1 = 0x87c37b91114253d5ULL, c2 = 0x4cf5ad432745937fULL;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t s0 = __ldg(str_off + i), len = __ldg(str_off + i + 1) - s0;
-    const uint8_t* key = bytes + s0;
-    uint64_t h1 = 0, h2 = 0;  // seed 0
-    const int64_t nblocks = len >> 4;
-    for (int64_t b = 0; b < nblocks; ++b) {
-      uint64_t k1 = le64(key + 16 * b), k2 = le64(key + 16 * b + 8);
-      k1 *= c1; k1 = rotl64(k1, 31); k1 *= c2; h1 ^= k1;
-      h1 = rotl64(h1, 27); h1 += h2; h1 = h1 * 5 + 0x52dce729;
-      k2 *= c2; k2 = rotl64(k2, 33); k2 *= c1; h2 ^= k2;
-      h2 = rotl64(h2, 31); h2 += h1; h2 = h2 * 5 + 0x38495ab5;
+  __shared__ __align__(16) uint8_t sbuf[kHashWarps][kWarpBytes + 32];  // + slack for tail reads
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t nwarps = (int64_t)gridDim.x * kHashWarps;
+  for (int64_t base = ((int64_t)blockIdx.x * kHashWarps + w) * 32; base < n; base += nwarps * 32) {
+    const int64_t i = base + lane;
+    const int64_t last = min(base + 32, n);
+    const int64_t s0 = __ldg(str_off + base), e0 = __ldg(str_off + last);
+    const bool live = i < n;
+    // dead lanes (past n) hash an empty string at the warp's first byte: every shared-memory
+    // address below stays inside the staged range
+    const int64_t si = live ? __ldg(str_off + i) : s0, len = live ? __ldg(str_off + i + 1) - si : 0;
+    const uintptr_t a0 = (uintptr_t)(bytes + s0) & ~(uintptr_t)15;
+    const int64_t span = (int64_t)((uintptr_t)(bytes + e0) - a0);
+    uint64_t hv;
+    if (span <= kWarpBytes) {  // warp-uniform
+      for (int64_t k = lane; 16 * k < span; k += 32)
+        reinterpret_cast<uint4*>(sbuf[w])[k] = __ldg(reinterpret_cast<const uint4*>(a0) + k);
+      __syncwarp();
+      hv = murmur3_h1<true>(sbuf[w] + ((uintptr_t)(bytes + si) - a0), len);
+      __syncwarp();
+    } else {
+      hv = murmur3_h1<false>(bytes + si, len);
     }
-    const uint8_t* tail = key + 16 * nblocks;
-    const int rem = (int)(len & 15);
-    uint64_t k1 = 0, k2 = 0;
-    for (int j = rem - 1; j >= 8; --j) k2 = (k2 << 8) | (uint64_t)__ldg(tail + j);
-    if (rem > 8) { k2 *= c2; k2 = rotl64(k2, 33); k2 *= c1; h2 ^= k2; }
-    for (int j = min(rem, 8) - 1; j >= 0; --j) k1 = (k1 << 8) | (uint64_t)__ldg(tail + j);
-    if (rem > 0) { k1 *= c1; k1 = rotl64(k1, 31); k1 *= c2; h1 ^= k1; }
-    h1 ^= (uint64_t)len; h2 ^= (uint64_t)len;
-    h1 += h2; h2 += h1;
-    h1 = fmix64(h1); h2 = fmix64(h2);
-    h1 += h2;
-    out[i] = h1;
+    if (live) out[i] = hv;
   }
 }
 
@@ -126,7 +180,7 @@ emb_status emb_hash_ids(const uint8_t* bytes, const int64_t* str_offsets, int64_
     return EMB_EINVAL;
   if (bytes && !is_device_ptr(bytes)) return EMB_EINVAL;
   cudaStream_t s = (cudaStream_t)stream;
-  k_hash_ids<<<grid_for(n), 256, 0, s>>>(bytes, str_offsets, n, hashes);
+  k_hash_ids<<<grid_for(n), 32 * kHashWarps, 0, s>>>(bytes, str_offsets, n, hashes);
   return cudaGetLastError() == cudaSuccess ? EMB_OK : EMB_ECUDA;
 }
 

@@ -45,6 +45,19 @@ def test_hash_ids_bit_exact(gpu):
     assert [int(x) for x in h] == [O.murmur3_x64_128(s, 0)[0] for s in strings]
 
 
+@pytest.mark.parametrize("n", [1, 31, 33, 1000, 32 * 4737 + 17])
+def test_hash_ids_ragged_counts(gpu, n):
+    """String counts that leave the last warp partly empty (regression: dead lanes must not
+    read outside the warp's staged bytes)."""
+    from paper_2402_06859_b200 import qr
+    rng = np.random.default_rng(n)
+    strings = [f"member:{int(x)}" for x in rng.integers(0, 10**6, size=n)]
+    data, off = qr.pack_strings(strings, gpu)
+    h = qr.hash_ids(data, off).cpu().numpy().view(np.uint64)
+    k = min(n, 3000)
+    assert (h[-k:] == O.hash_ids(strings[-k:])).all()
+
+
 @pytest.mark.parametrize("dual", [False, True])
 @pytest.mark.parametrize("R,Q", [(1000, -(-(1 << 32) // 1000)), (97, 1000), (1, 7), ((1 << 31) - 5, 3)])
 def test_qr_expand_bit_exact(gpu, dual, R, Q):
