@@ -57,6 +57,9 @@ def lib():
             "ora_murmur3_x64_128": (None, [P, i64, C.c_uint32, P]),
             "ora_hash_ids": (None, [P, P, i64, P]),
             "ora_qr_expand": (None, [P, P, i64, i64, i32, i64, i32, P, P]),
+            "ora_quantize_row_minmax": (i32, [P, i32, P, P, P]),
+            "ora_quantize_minmax": (i64, [P, i64, i32, P, P, P]),
+            "ora_forward_q8_minmax": (i64, [P, P, P, P, P, P, i32, P]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -237,3 +240,24 @@ def qr_expand(h, offsets, R: int, Q: int, dual: bool):
 
 def qr_rows(R: int, Q: int, dual: bool) -> int:
     return (2 if dual else 1) * (Q + R)
+
+
+# ---- NEXT-4: min-max row-wise 8-bit quantization (oracle.h) ---------------------------
+
+def quantize_minmax(X):
+    """(codes uint8 [rows][dim], min [rows], scale [rows], #non-finite rows)."""
+    X = _f32(X)
+    rows, dim = X.shape
+    codes = np.zeros((rows, dim), dtype=np.uint8)
+    mn = np.zeros(rows, dtype=np.float32)
+    sc = np.zeros(rows, dtype=np.float32)
+    bad = lib().ora_quantize_minmax(_p(X), rows, dim, _p(codes), _p(mn), _p(sc))
+    return codes, mn, sc, int(bad)
+
+
+def forward_q8_minmax(pb: Problem, codes, mn, scale, ids, offsets, B):
+    codes = np.ascontiguousarray(codes, dtype=np.uint8)
+    mn, scale, ids, offsets = _f32(mn), _f32(scale), _i32(ids), _i32(offsets)
+    out = np.zeros((B, pb.F, pb.dim), dtype=np.float32)
+    inv = lib().ora_forward_q8_minmax(pb.ref, _p(codes), _p(mn), _p(scale), _p(ids), _p(offsets), B, _p(out))
+    return out, int(inv)

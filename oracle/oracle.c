@@ -392,3 +392,75 @@ void ora_qr_expand(const uint64_t* h, const int32_t* offsets, int64_t nbags, int
     }
   }
 }
+
+/* ------------------------------------------------------------------------------------ */
+/* NEXT-4: min-max row-wise 8-bit quantization (oracle.h)                                 */
+int32_t ora_quantize_row_minmax(const float* x, int32_t dim, uint8_t* codes, float* mn_out,
+                                float* scale) {
+  for (int32_t d = 0; d < dim; ++d)
+    if (!isfinite(x[d])) {
+      for (int32_t e = 0; e < dim; ++e) codes[e] = 0;
+      *mn_out = 0.0f; *scale = 0.0f;
+      return 1;
+    }
+  float mn = x[0], mx = x[0];
+  for (int32_t d = 1; d < dim; ++d) {
+    if (x[d] < mn) mn = x[d];
+    if (x[d] > mx) mx = x[d];
+  }
+  *mn_out = (mx == mn) ? mx : mn;
+  if (mx == mn) {
+    *scale = 0.0f;
+    for (int32_t d = 0; d < dim; ++d) codes[d] = 0;
+    return 0;
+  }
+  float sc = (mx - mn) / 255.0f; /* X^scale = (X^max - X^min) / (2^b - 1) */
+  *scale = sc;
+  for (int32_t d = 0; d < dim; ++d) {
+    if (sc == 0.0f) { codes[d] = 0; continue; }
+    float q = (x[d] - mn) / sc;   /* X^int = round((X - X^min) / X^scale) */
+    float r = roundf(q);
+    if (r < 0.0f) r = 0.0f;
+    if (r > 255.0f) r = 255.0f;
+    codes[d] = (uint8_t)r;
+  }
+  return 0;
+}
+
+int64_t ora_quantize_minmax(const float* X, int64_t rows, int32_t dim, uint8_t* codes,
+                            float* mn, float* scale) {
+  int64_t bad = 0;
+  for (int64_t r = 0; r < rows; ++r)
+    bad += ora_quantize_row_minmax(X + r * dim, dim, codes + r * dim, mn + r, scale + r);
+  return bad;
+}
+
+int64_t ora_forward_q8_minmax(const ora_cfg* c, const uint8_t* codes, const float* mn,
+                              const float* scale, const int32_t* ids, const int32_t* offsets,
+                              int32_t B, float* out) {
+  const int32_t D = c->dim, F = c->num_features;
+  int64_t invalid = 0;
+  int64_t* base = table_bases(c);
+  float* acc = (float*)malloc(sizeof(float) * (size_t)D);
+  for (int32_t f = 0; f < F; ++f)
+    for (int32_t b = 0; b < B; ++b) {
+      int64_t bag = (int64_t)f * B + b;
+      int32_t lo = offsets[bag], hi = offsets[bag + 1];
+      for (int32_t d = 0; d < D; ++d) acc[d] = 0.0f;
+      for (int32_t j = lo; j < hi; ++j) {
+        int64_t key = row_key(c, base, f, ids[j]);
+        if (key < 0) { ++invalid; continue; }
+        const uint8_t* q = codes + key * D;
+        for (int32_t d = 0; d < D; ++d) acc[d] = acc[d] + fmaf((float)q[d], scale[key], mn[key]);
+      }
+      if (c->pooling == 1) {
+        int32_t L = hi - lo;
+        for (int32_t d = 0; d < D; ++d) acc[d] = (L > 0) ? acc[d] / (float)L : 0.0f;
+      }
+      float* o = out + ((int64_t)b * F + f) * D;
+      for (int32_t d = 0; d < D; ++d) o[d] = acc[d];
+    }
+  free(acc);
+  free(base);
+  return invalid;
+}

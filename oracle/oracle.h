@@ -133,6 +133,25 @@ void ora_hash_ids(const uint8_t* bytes, const int64_t* str_off, int64_t n, uint6
 void ora_qr_expand(const uint64_t* h, const int32_t* offsets, int64_t nbags, int64_t nnz,
                    int32_t R, int64_t Q, int32_t dual, int32_t* ids_out, int32_t* offsets_out);
 
+/* ---- NEXT-4: min-max row-wise 8-bit quantization ---------------------
+ * "min-max row-wise quantization ... saves the minimum value and the quantization bin-scale
+ * value of each embedding row", with the same X^scale = (X^max - X^min)/(2^b - 1)
+ * and codes in [0, 2^b - 1] = [0, 255] ("if x in [0, 255]"):
+ *   mn = min x, mx = max x;
+ *   mx == mn:  min = mx, scale = 0, codes 0;
+ *   else scale = fl(fl(mx - mn) / 255); scale == 0 -> codes 0;
+ *        else code = clamp(roundf(fl(fl(x - mn) / scale)), 0, 255)   (half away from zero)
+ *   dequant = fmaf((float)code, scale, min).
+ * Non-finite x -> codes 0, min 0, scale 0, returns 1. */
+int32_t ora_quantize_row_minmax(const float* x, int32_t dim, uint8_t* codes, float* mn_out,
+                                float* scale);
+int64_t ora_quantize_minmax(const float* X, int64_t rows, int32_t dim, uint8_t* codes,
+                            float* mn, float* scale);
+/* a10 over a min-max store: out = sum in bag order of fmaf((float)code, scale, min). */
+int64_t ora_forward_q8_minmax(const ora_cfg* c, const uint8_t* codes, const float* mn,
+                              const float* scale, const int32_t* ids, const int32_t* offsets,
+                              int32_t B, float* out);
+
 #ifdef __cplusplus
 }
 #endif
