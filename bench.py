@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-qr", action="store_true", help="skip the NEXT-1 QR/Murmur section")
+    ap.add_argument("--q8-mode", default="middle_max", choices=["middle_max", "min_max"],
+                    help="q8 store: the paper's middle-max (default) or NEXT-4's min-max")
     ap.add_argument("--cpu-samples", type=int, default=8192)
     return ap.parse_args()
 
@@ -377,7 +379,8 @@ def run_ours(args, cfg, rank, world, local_rank):
         shard_kw = dict(rank=rank, world_size=world, sharding="row", nccl_unique_id=uid.cpu().numpy().tobytes(),
                         max_recv_nnz=3 * max_nnz)
     emb = ShardedEmbedding(cfg.table_rows, D, cfg.feature_table, max_nnz=max_nnz, max_batch=B,
-                           adagrad=args.adagrad, q8=True, requant=True, device=dev, stream=stream, **shard_kw)
+                           adagrad=args.adagrad, q8=True, requant=True, device=dev, stream=stream,
+                           q8_mode=args.q8_mode, **shard_kw)
     with torch.cuda.stream(stream):
         for t in range(cfg.num_tables):
             v = emb.table_view(t)
@@ -566,7 +569,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded Zipf ids, Irwin-Hall tables/grads)",
         "config": {"workload": cfg.name, "tables": cfg.table_rows, "dim": D, "features": F,
                    "global_batch": world * B, "batch_per_gpu": B, "nnz_per_step": nnz_avg, "alpha": cfg.alpha,
-                   "unique_rows": U, "adagrad": args.adagrad,
+                   "unique_rows": U, "adagrad": args.adagrad, "q8": args.q8_mode,
                    "parallelism": "single" if world == 1 else f"row-sharded x{world} (NCCL all-to-all ids, reduce-scatter pooled, all-gather grads)",
                    "step": "a2 fwd -> a10 q8 fwd (overlapping a5 dedup on a side stream) -> a6-a8 bwd (a9 requant of touched rows fused)",
                    "l2": "flushed between timed steps (256 MiB write, untimed)",

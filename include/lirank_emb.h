@@ -84,6 +84,11 @@ enum { EMB_SHARD_NONE = 0, EMB_SHARD_TABLE = 1, EMB_SHARD_ROW = 2 };
 #define EMB_F_REQUANT 2u  /* (needs EMB_F_Q8) every AdaGrad update also re-quantizes the rows
                              it touched, so the q8 store tracks the fp32 tables between
                              full emb_quantize_mm8() passes                                   */
+#define EMB_F_Q8_MINMAX 16u /* (needs EMB_F_Q8) NEXT-4: the q8 store holds MIN-MAX row-wise codes
+                             (the baseline the paper contrasts middle-max with):
+                             uint8 codes = clamp(round((x - min) / scale), 0, 255), meta {min,
+                             scale} in place of {middle, scale}; a10 dequantizes
+                             fmaf(code, scale, min).  Same row layout and kernels.             */
 #define EMB_F_EXCHANGE 8u /* run the sharded exchange path even at world_size 1 (a 1-rank
                              communicator; exercises the transport on a single GPU)          */
 #define EMB_F_LOOPBACK 4u /* (world_size > 1) TEST TRANSPORT: the ranks are threads of one
@@ -221,7 +226,8 @@ EMB_API emb_status emb_read_rows(emb_t h, int32_t table, const int64_t* rows, in
                          float* acc);
 EMB_API emb_status emb_write_rows(emb_t h, int32_t table, const int64_t* rows, int64_t n,
                           const float* w, const float* acc);
-/* codes: host int8 [n][D]; middle, scale: host fp32 [n] (either may be NULL). */
+/* codes: host int8 [n][D] (the raw bytes: uint8 codes under EMB_F_Q8_MINMAX); middle, scale:
+ * host fp32 [n] (the row's min instead of its middle under EMB_F_Q8_MINMAX; either may be NULL). */
 EMB_API emb_status emb_read_q8(emb_t h, int32_t table, const int64_t* rows, int64_t n, int8_t* codes,
                        float* middle, float* scale);
 

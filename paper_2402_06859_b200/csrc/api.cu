@@ -68,6 +68,7 @@ emb_status make_plan(const emb_config* c, Plan* p) {
   if ((int64_t)c->max_batch * c->num_features >= (int64_t(1) << 31) - 1) return EMB_EINVAL;
   if (!(c->eps >= 0.f) || !(c->max_norm > 0.f) || !(c->init_accumulator >= 0.f)) return EMB_EINVAL;
   if ((c->flags & EMB_F_REQUANT) && !(c->flags & EMB_F_Q8)) return EMB_EINVAL;
+  if ((c->flags & EMB_F_Q8_MINMAX) && !(c->flags & EMB_F_Q8)) return EMB_EINVAL;
   if (c->world_size < 1 || c->world_size > kMaxWorld || c->rank < 0 || c->rank >= c->world_size)
     return EMB_EINVAL;
   if (c->sharding != EMB_SHARD_NONE && c->sharding != EMB_SHARD_TABLE && c->sharding != EMB_SHARD_ROW)
@@ -377,6 +378,7 @@ emb_status backward_local(emb_t h, const float* grad_dev, float lr, double extra
   a.eps = p.eps;
   a.q8_codes = (p.flags & EMB_F_REQUANT) ? h->codes : nullptr;
   a.q8_meta_off = h->q8_meta_off;
+  a.q8_minmax = (p.flags & EMB_F_Q8_MINMAX) != 0;
   a.qpitch = p.qpitch;
 
   {
@@ -731,6 +733,7 @@ emb_status emb_forward_q8(emb_t h, const int32_t* ids, const int32_t* offsets, i
     a.codes = h->codes;
     a.qpitch = p.qpitch;
     a.meta_off = h->q8_meta_off;
+    a.minmax = (p.flags & EMB_F_Q8_MINMAX) != 0;
     a.ids = st.ids;
     a.offsets = st.offsets;
     a.B = batch;
@@ -800,6 +803,7 @@ emb_status emb_quantize_mm8(emb_t h) {
   {
     Phase ph(h->prof, h->stream, EMB_PH_QUANTIZE);
     CK(launch_quantize(h->W, p.pitch, p.local_rows, p.D, h->codes, p.qpitch, h->q8_meta_off,
+                       (p.flags & EMB_F_Q8_MINMAX) != 0,
                        h->d_status, h->stream));
   }
   h->launches += p.local_rows > 0;

@@ -389,18 +389,19 @@ __device__ __forceinline__ float fmax_nan(float a, float b) {
   return r;
 }
 
-// X^int of one element, exactly as the oracle: round-half-away((X - X^middle) / X^scale),
-// saturated to [-128, 127] (the IEEE quotient, used where the fast path cannot decide).
-__device__ __forceinline__ uint32_t code_exact(float e, float middle, float scale) {
-  float r = roundf(__fdiv_rn(__fsub_rn(e, middle), scale));
-  r = fminf(fmaxf(r, -128.0f), 127.0f);
+// X^int of one element, exactly as the oracle: round-half-away((X - base) / X^scale),
+// saturated to [lo, hi] (the IEEE quotient, used where the fast path cannot decide).
+// Middle-max: base = X^middle, [-128, 127]; min-max (NEXT-4): base = X^min, [0, 255].
+__device__ __forceinline__ uint32_t code_exact(float e, float base, float scale, float lo, float hi) {
+  float r = roundf(__fdiv_rn(__fsub_rn(e, base), scale));
+  r = fminf(fmaxf(r, lo), hi);
   return (uint32_t)((int)r) & 0xffu;
 }
 
 template <int LPB, int VPL>
 __device__ __forceinline__ void quantize_group_row(const float4 (&x)[VPL], int D, int lane, bool live,
                                                    uint8_t* __restrict__ code_row,
-                                                   int meta_off, int qpitch,
+                                                   int meta_off, int qpitch, bool minmax,
                                                    uint32_t* status) {
   float mn = FLT_MAX, mx = -FLT_MAX;
 #pragma unroll
@@ -430,12 +431,15 @@ __device__ __forceinline__ void quantize_group_row(const float4 (&x)[VPL], int D
   } else if (mx == mn) {
     middle = mx; scale = 0.f; zero_codes = true;
   } else {
-    // X^middle = (X^max * 2^(b-1) + X^min * (2^(b-1) - 1)) / (2^b - 1), b = 8
-    middle = __fdiv_rn(__fadd_rn(__fmul_rn(mx, 128.0f), __fmul_rn(mn, 127.0f)), 255.0f);
+    // middle-max: X^middle = (X^max * 2^(b-1) + X^min * (2^(b-1) - 1)) / (2^b - 1), b = 8;
+    // min-max (NEXT-4): the saved base is X^min itself ("middle" names the base below)
+    middle = minmax ? mn
+                    : __fdiv_rn(__fadd_rn(__fmul_rn(mx, 128.0f), __fmul_rn(mn, 127.0f)), 255.0f);
     // X^scale = (X^max - X^min) / (2^b - 1)
     scale = __fdiv_rn(__fsub_rn(mx, mn), 255.0f);
     zero_codes = scale == 0.0f;
   }
+  const float qlo = minmax ? 0.0f : -128.0f, qhi = minmax ? 255.0f : 127.0f;
   // X^int = round((X - X^middle) / X^scale), half away from zero, saturated to [-128,127].
   // The IEEE quotient is only needed near a rounding boundary: q~ = (X - X^middle) *
   // RN(1/X^scale) is within 2^-23 relative (< 4e-5 absolute for |q| < 200) of the
@@ -457,7 +461,7 @@ __device__ __forceinline__ void quantize_group_row(const float4 (&x)[VPL], int D
       uint32_t bits[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        const float qa = fminf(fmaxf(__fmul_rn(__fsub_rn(e[i], middle), rcp), -128.0f), 127.0f);
+        const float qa = fminf(fmaxf(__fmul_rn(__fsub_rn(e[i], middle), rcp), qlo), qhi);
         const float big = __fadd_rn(qa, 12582912.0f);
         err = fmaxf(err, fabsf(__fsub_rn(qa, __fsub_rn(big, 12582912.0f))));
         bits[i] = __float_as_uint(big);
@@ -475,7 +479,7 @@ __device__ __forceinline__ void quantize_group_row(const float4 (&x)[VPL], int D
         uint32_t w = 0;
 #pragma unroll
         for (int i = 0; i < 4; ++i)
-          if (d + i < D) w |= code_exact(e[i], middle, scale) << (8 * i);
+          if (d + i < D) w |= code_exact(e[i], middle, scale, qlo, qhi) << (8 * i);
         wv[v] = w;
       }
     }
@@ -503,7 +507,7 @@ __device__ __forceinline__ void quantize_group_row(const float4 (&x)[VPL], int D
 template <int LPB, int VPL>
 __global__ void __launch_bounds__(256)
 k_quantize(const float* __restrict__ W, int pitch, int64_t rows, int D,
-           uint8_t* __restrict__ codes, int qpitch, int meta_off, uint32_t* status) {
+           uint8_t* __restrict__ codes, int qpitch, int meta_off, bool minmax, uint32_t* status) {
   constexpr int R = VPL >= 4 ? 2 : 4;  // rows in flight per group
   const int lane = threadIdx.x & (LPB - 1);
   const int64_t gstride = ((int64_t)gridDim.x * blockDim.x) / LPB;
@@ -528,7 +532,7 @@ k_quantize(const float* __restrict__ W, int pitch, int64_t rows, int D,
       const int64_t r = r0 + q * gstride;
       const bool live = r < rows;
       uint8_t* row = codes + (size_t)(live ? r : 0) * qpitch;
-      quantize_group_row<LPB, VPL>(x[q], D, lane, live, row, meta_off, qpitch, status);
+      quantize_group_row<LPB, VPL>(x[q], D, lane, live, row, meta_off, qpitch, minmax, status);
     }
   }
 }
@@ -540,7 +544,7 @@ __global__ void __launch_bounds__(256, (REQUANT && !ROWWISE) ? 1 : 3)
 k_adagrad(const uint32_t* __restrict__ unique, const uint32_t* __restrict__ Up,
           const float* __restrict__ G, const float* __restrict__ clip, float* __restrict__ Wt,
           float* __restrict__ A, int pitch, int D, float lr, float eps,
-          uint8_t* __restrict__ codes, int qpitch, int meta_off, uint32_t* status) {
+          uint8_t* __restrict__ codes, int qpitch, int meta_off, bool minmax, uint32_t* status) {
   constexpr int R = VPL >= 4 ? 1 : 2;
   const float c = *clip;
   if (c < 0.0f) return;  // non-finite global norm: skip the step (uniform over the grid)
@@ -636,7 +640,7 @@ k_adagrad(const uint32_t* __restrict__ unique, const uint32_t* __restrict__ Up,
       }
       if (REQUANT) {
         uint8_t* row = codes + (size_t)key[q] * qpitch;
-        quantize_group_row<LPB, VPL>(w[q], D, lane, has[q], row, meta_off, qpitch, status);
+        quantize_group_row<LPB, VPL>(w[q], D, lane, has[q], row, meta_off, qpitch, minmax, status);
       }
     }
   }
@@ -760,7 +764,7 @@ cudaError_t launch_adagrad(const BwdArgs& a, cudaStream_t s) {
   DISPATCH(g, (k_adagrad<L_, V_, RW, RQ><<<persistent_grid((const void*)k_adagrad<L_, V_, RW, RQ>, \
                                                             a.nnz, L_, 2), 256, 0, s>>>(    \
                   a.unique, a.U, a.G, a.clip, a.Wt, a.A, a.pitch, a.D, a.lr, a.eps,         \
-                  a.q8_codes, a.qpitch, a.q8_meta_off, a.status)))
+                  a.q8_codes, a.qpitch, a.q8_meta_off, a.q8_minmax, a.status)))
   if (a.rowwise) {
     if (rq) LAUNCH_AG(LIRANK_GEOM4_DISPATCH, true, true);
     else LAUNCH_AG(LIRANK_GEOM_DISPATCH, true, false);
@@ -783,12 +787,12 @@ static Geom geom_target(int pitch, int target) {
 static Geom quant_geom(int pitch) { return geom_target(pitch, 4); }
 
 cudaError_t launch_quantize(const float* W, int pitch, int64_t rows, int D, uint8_t* codes,
-                            int qpitch, int meta_off, uint32_t* status, cudaStream_t s) {
+                            int qpitch, int meta_off, bool minmax, uint32_t* status, cudaStream_t s) {
   if (rows == 0) return cudaSuccess;
   const Geom g = quant_geom(pitch);
 #define LAUNCH_Q(L, V)                                                                 \
   k_quantize<L, V><<<persistent_grid((const void*)k_quantize<L, V>, rows, L), 256, 0, s>>>( \
-      W, pitch, rows, D, codes, qpitch, meta_off, status)
+      W, pitch, rows, D, codes, qpitch, meta_off, minmax, status)
   if (g.lpb == 1) {
     if (g.vpl == 1) LAUNCH_Q(1, 1); else if (g.vpl == 2) LAUNCH_Q(1, 2); else if (g.vpl == 3) LAUNCH_Q(1, 3); else LAUNCH_Q(1, 4);
   } else if (g.lpb == 2) { if (g.vpl <= 3) LAUNCH_Q(2, 3); else LAUNCH_Q(2, 4); }

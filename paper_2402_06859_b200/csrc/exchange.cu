@@ -318,6 +318,7 @@ emb_status exchange_forward(emb_t h, const Staged& st, int32_t batch, int64_t nn
     a.codes = h->codes;
     a.qpitch = p.qpitch;
     a.meta_off = h->q8_meta_off;
+    a.minmax = (p.flags & EMB_F_Q8_MINMAX) != 0;
     a.ids = (const int*)x.recv_keys;
     a.offsets = (const int*)x.recv_off;
     a.B = B;

@@ -136,16 +136,18 @@ k_pool_fwd_f32(const float* __restrict__ W, int pitch, const int* __restrict__ i
 // The int8 code becomes an exact float without a conversion instruction: with
 // u = byte ^ 0x80 = code + 128, the float with bits 0x4B0000uu is 2^23 + u, so
 // (2^23 + u) - (2^23 + 128) = code exactly.
-__device__ __forceinline__ float code_f(uint32_t x, uint32_t sel) {
-  return __fsub_rn(__int_as_float((int)__byte_perm(x, 0x4B000000u, sel)), 8388736.0f);
+// Min-max stores (NEXT-4) hold unsigned codes u directly: xmask = 0 and magic = 2^23.
+__device__ __forceinline__ float code_f(uint32_t x, uint32_t sel, float magic) {
+  return __fsub_rn(__int_as_float((int)__byte_perm(x, 0x4B000000u, sel)), magic);
 }
-// 4 codes (one 32-bit word) -> acc += middle + code * scale, element by element.
-__device__ __forceinline__ float4 deq4_add(float4 acc, uint32_t w, float scale, float middle) {
-  const uint32_t x = w ^ 0x80808080u;
-  acc.x = __fadd_rn(acc.x, __fmaf_rn(code_f(x, 0x7540), scale, middle));
-  acc.y = __fadd_rn(acc.y, __fmaf_rn(code_f(x, 0x7541), scale, middle));
-  acc.z = __fadd_rn(acc.z, __fmaf_rn(code_f(x, 0x7542), scale, middle));
-  acc.w = __fadd_rn(acc.w, __fmaf_rn(code_f(x, 0x7543), scale, middle));
+// 4 codes (one 32-bit word) -> acc += base + code * scale, element by element.
+__device__ __forceinline__ float4 deq4_add(float4 acc, uint32_t w, float scale, float middle,
+                                           uint32_t xmask, float magic) {
+  const uint32_t x = w ^ xmask;
+  acc.x = __fadd_rn(acc.x, __fmaf_rn(code_f(x, 0x7540, magic), scale, middle));
+  acc.y = __fadd_rn(acc.y, __fmaf_rn(code_f(x, 0x7541, magic), scale, middle));
+  acc.z = __fadd_rn(acc.z, __fmaf_rn(code_f(x, 0x7542, magic), scale, middle));
+  acc.w = __fadd_rn(acc.w, __fmaf_rn(code_f(x, 0x7543, magic), scale, middle));
   return acc;
 }
 __device__ __forceinline__ uint4 ld_nc_u4(const void* p) {
@@ -168,7 +170,7 @@ k_pool_fwd_q8(const uint8_t* __restrict__ codes, int qpitch, int meta_off,
               const int* __restrict__ ids, const int* __restrict__ offsets, int B, int F, int Fb,
               int D, const FeatMeta* __restrict__ meta, float* __restrict__ out,
               uint32_t* status,
-              const uint32_t* __restrict__ order) {
+              const uint32_t* __restrict__ order, uint32_t xmask, float magic) {
   constexpr int UNR = (VPL == 1) ? 4 : 2;
   constexpr uint32_t kNone = 0xffffffffu;
   constexpr unsigned kFull = 0xffffffffu;
@@ -218,10 +220,10 @@ k_pool_fwd_q8(const uint8_t* __restrict__ codes, int qpitch, int meta_off,
         if (k[u] != kNone) {
 #pragma unroll
           for (int v = 0; v < VPL; ++v) {
-            acc[4 * v + 0] = deq4_add(acc[4 * v + 0], w[u][v].x, mt[u].y, mt[u].x);
-            acc[4 * v + 1] = deq4_add(acc[4 * v + 1], w[u][v].y, mt[u].y, mt[u].x);
-            acc[4 * v + 2] = deq4_add(acc[4 * v + 2], w[u][v].z, mt[u].y, mt[u].x);
-            acc[4 * v + 3] = deq4_add(acc[4 * v + 3], w[u][v].w, mt[u].y, mt[u].x);
+            acc[4 * v + 0] = deq4_add(acc[4 * v + 0], w[u][v].x, mt[u].y, mt[u].x, xmask, magic);
+            acc[4 * v + 1] = deq4_add(acc[4 * v + 1], w[u][v].y, mt[u].y, mt[u].x, xmask, magic);
+            acc[4 * v + 2] = deq4_add(acc[4 * v + 2], w[u][v].z, mt[u].y, mt[u].x, xmask, magic);
+            acc[4 * v + 3] = deq4_add(acc[4 * v + 3], w[u][v].w, mt[u].y, mt[u].x, xmask, magic);
           }
         }
     }
@@ -352,7 +354,8 @@ cudaError_t launch_pool_fwd_q8(const FwdQ8Args& a, cudaStream_t s) {
 #define LAUNCH_Q8(MEAN)                                                                    \
   LIRANK_GEOM_DISPATCH(g, (k_pool_fwd_q8<L_, V_, MEAN><<<grid, 256, 0, s>>>(               \
                               a.codes, a.qpitch, a.meta_off, a.ids, a.offsets, a.B, a.F, Fb, \
-                              a.D, a.meta, a.out, a.status, order)))
+                              a.D, a.meta, a.out, a.status, order,                       \
+                              a.minmax ? 0u : 0x80808080u, a.minmax ? 8388608.0f : 8388736.0f)))
   if (a.mean) LAUNCH_Q8(true); else LAUNCH_Q8(false);
 #undef LAUNCH_Q8
   return cudaGetLastError();

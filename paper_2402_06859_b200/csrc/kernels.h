@@ -48,6 +48,7 @@ struct FwdQ8Args {
   uint32_t* status;
   bool mean;
   uint32_t* order_ws;  // as FwdArgs::order_ws
+  bool minmax;         // min-max store (uint8 codes, meta {min, scale})
 };
 cudaError_t launch_pool_fwd_q8(const FwdQ8Args& a, cudaStream_t s);
 
@@ -120,6 +121,7 @@ struct BwdArgs {
   float lr, eps;
   uint8_t* q8_codes;        // requantize touched rows (NULL: no)
   int q8_meta_off;
+  bool q8_minmax;           // re-quantize min-max (else middle-max)
   int qpitch;
 };
 cudaError_t launch_segreduce(const BwdArgs& a, int64_t* launches, cudaStream_t s);
@@ -132,7 +134,7 @@ cudaError_t launch_adagrad(const BwdArgs& a, cudaStream_t s);
 
 // ---- a9 ----------------------------------------------------------------------------
 cudaError_t launch_quantize(const float* W, int pitch, int64_t rows, int D, uint8_t* codes,
-                            int qpitch, int meta_off, uint32_t* status, cudaStream_t s);
+                            int qpitch, int meta_off, bool minmax, uint32_t* status, cudaStream_t s);
 
 // ---- misc --------------------------------------------------------------------------
 cudaError_t launch_fill(float* p, int64_t n, float v, cudaStream_t s);

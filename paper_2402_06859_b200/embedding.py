@@ -68,8 +68,10 @@ class ShardedEmbedding:
                  rank: int = 0, world_size: int = 1, sharding: str = "none",
                  table_owner: Optional[Sequence[int]] = None, nccl_unique_id: Optional[bytes] = None,
                  loopback_hub: Optional["LoopbackHub"] = None, force_exchange: bool = False,
-                 max_recv_nnz: int = 0):
+                 max_recv_nnz: int = 0, q8_mode: str = "middle_max"):
         self.lib = L.load()
+        assert q8_mode in ("middle_max", "min_max")
+        self.q8_mode = q8_mode
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
         self.dim = int(dim)
@@ -101,7 +103,8 @@ class ShardedEmbedding:
             stream=C.c_void_p(self.stream.cuda_stream),
             flags=(L.EMB_F_Q8 if (q8 or requant) else 0) | (L.EMB_F_REQUANT if requant else 0)
             | (L.EMB_F_LOOPBACK if loopback_hub is not None else 0)
-            | (L.EMB_F_EXCHANGE if force_exchange else 0),
+            | (L.EMB_F_EXCHANGE if force_exchange else 0)
+            | (L.EMB_F_Q8_MINMAX if q8_mode == "min_max" else 0),
             max_recv_nnz=int(max_recv_nnz))
         self.sizes = L.EmbSizes()
         L.check(self.lib.emb_plan(C.byref(self.cfg), C.byref(self.sizes)), "emb_plan")
@@ -211,8 +214,9 @@ class ShardedEmbedding:
                 "emb_write_rows")
 
     def read_q8(self, table: int, rows):
+        """(codes, base, scale): int8 codes + middle (middle-max) or uint8 codes + min (min-max)."""
         rows = np.ascontiguousarray(rows, dtype=np.int64)
-        codes = np.zeros((len(rows), self.dim), dtype=np.int8)
+        codes = np.zeros((len(rows), self.dim), dtype=np.uint8 if self.q8_mode == "min_max" else np.int8)
         mid = np.zeros(len(rows), dtype=np.float32)
         sc = np.zeros(len(rows), dtype=np.float32)
         L.check(self.lib.emb_read_q8(self.h, int(table), rows.ctypes.data_as(C.c_void_p), len(rows),
