@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-qr", action="store_true", help="skip the NEXT-1 QR/Murmur section")
+    ap.add_argument("--no-model", action="store_true", help="skip the NEXT-2 end-to-end model section")
+    ap.add_argument("--dense-features", type=int, default=256, help="NEXT-2 dense feature count")
     ap.add_argument("--q8-mode", default="middle_max", choices=["middle_max", "min_max"],
                     help="q8 store: the paper's middle-max (default) or NEXT-4's min-max")
     ap.add_argument("--cpu-samples", type=int, default=8192)
@@ -345,6 +347,48 @@ def qr_section(cfg, ids, off, B, dev, stream, flush, hbm_peak, reps=5):
     del emb
     return res
 
+
+# ---------------------------------------------------------------------------
+# NEXT-2 section: the end-to-end Feed train step (embedding + MLP tower, one global clip)
+# ---------------------------------------------------------------------------
+
+def model_section(emb, batches, dev_in, B, dense_dim, stream, flush, steps=10, warmup=3):
+    """FeedModel (paper_2402_06859_b200/feed_model.py) on the bench's Feed-1 tables: pooled
+    embeddings ++ dense features -> 4 x 100 MLP, BCE loss, AdaGrad on sparse + dense
+    under one global clip.  Steps issued back to back; CUDA events on the library
+    stream; L2 not flushed between steps (whole-model throughput)."""
+    import torch
+
+    from paper_2402_06859_b200.feed_model import FeedModel
+    torch.backends.cuda.matmul.allow_tf32 = False
+    model = FeedModel(emb, dense_dim, lr=LR, seed=1)
+    g = torch.Generator(device=emb.device).manual_seed(5)
+    with torch.cuda.stream(stream):
+        xs = [torch.randn(B, dense_dim, device=emb.device, generator=g) for _ in dev_in]
+        ys = [(torch.rand(B, device=emb.device, generator=g) > 0.5).float() for _ in dev_in]
+    for k in range(warmup):
+        ids_d, off_d, _ = dev_in[k % len(dev_in)]
+        model.train_step(ids_d, off_d, B, xs[k % len(xs)], ys[k % len(ys)])
+    stream.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        torch.cuda._sleep(1_000_000)
+        t0.record(stream)
+    for k in range(steps):
+        ids_d, off_d, _ = dev_in[k % len(dev_in)]
+        loss = model.train_step(ids_d, off_d, B, xs[k % len(xs)], ys[k % len(ys)])
+    with torch.cuda.stream(stream):
+        t1.record(stream)
+    stream.synchronize()
+    ms = t0.elapsed_time(t1) / steps
+    assert emb.sync() == 0
+    tower = sum(p.numel() for p in model.params)
+    return {"what": "Feed-1 tables + %d dense features -> MLP 4 x 100 -> BCE; AdaGrad sparse + dense, "
+                    "one global clip (emb_backward_adagrad_dev, no host sync)" % dense_dim,
+            "ms_per_step": ms, "train_samples_per_s": B / (ms / 1e3), "tower_params": tower,
+            "loss_last": float(loss), "clip_last": float(model.c), "steps": steps, "warmup": warmup,
+            "tf32": False}
+
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
@@ -586,6 +630,11 @@ def run_ours(args, cfg, rank, world, local_rank):
         "e2e": e2e,
         "clip": {"sq_norm": S, "c": float(c)},
     }
+    if world == 1 and not args.no_model:
+        try:
+            line["model"] = model_section(emb, batches, dev_in, B, args.dense_features, stream, flush)
+        except Exception as e:  # report, never hide
+            line["model"] = {"error": repr(e)}
     if world == 1 and not args.no_qr:
         try:
             line["qr"] = qr_section(cfg, batches[0][0], batches[0][1], B, dev, stream, flush, hbm_peak)

@@ -205,6 +205,18 @@ EMB_API emb_status emb_forward(emb_t h, const int32_t* ids, const int32_t* offse
 EMB_API emb_status emb_backward_adagrad(emb_t h, const float* grad_out, float lr, double extra_sq_norm,
                                 double* sq_norm_out);
 
+/* As emb_backward_adagrad, with no host synchronisation for a dense side on the device
+ * (NEXT-2, "global gradient clipped to unit norm" over sparse + dense; P:538 tower):
+ * extra_sq_norm_dev (device fp64, optional) is the caller's dense squared gradient norm,
+ * read on the stream when the global norm is formed; clip_out_dev (device fp32, optional)
+ * receives the clip factor c the caller scales its dense gradients by (c = -1 when S is not
+ * finite: the sparse update was skipped and the caller should skip its dense update);
+ * sq_norm_out_dev (device fp64, optional) receives S.  Enqueued on cfg.stream; returns
+ * without waiting. */
+EMB_API emb_status emb_backward_adagrad_dev(emb_t h, const float* grad_out, float lr,
+                                            const double* extra_sq_norm_dev, float* clip_out_dev,
+                                            double* sq_norm_out_dev);
+
 /* a9: quantize every local row (middle-max, 8 bits) into the q8 store.
  * The fp32 tables are kept.  EMB_ESTATE without EMB_F_Q8. */
 EMB_API emb_status emb_quantize_mm8(emb_t h);

@@ -335,7 +335,8 @@ emb_status join_dedup(emb_t h) {
   return EMB_OK;
 }
 
-emb_status backward_local(emb_t h, const float* grad_dev, float lr, double extra) {
+emb_status backward_local(emb_t h, const float* grad_dev, float lr, double extra,
+                          const double* extra_dev, float* clip_out) {
   const Plan& p = h->p;
   const int64_t n = h->fwd_nnz;
   emb_status js = join_dedup(h);  // a5 ran on the side stream since the forward
@@ -370,6 +371,8 @@ emb_status backward_local(emb_t h, const float* grad_dev, float lr, double extra
   a.clip = h->d_clip;
   a.status = h->d_status;
   a.extra_sq_norm = extra;
+  a.extra_dev = extra_dev;
+  a.clip_out = clip_out;
   a.max_norm = p.max_norm;
   a.Wt = h->W;
   a.A = h->A;
@@ -762,11 +765,13 @@ emb_status emb_forward_q8(emb_t h, const int32_t* ids, const int32_t* offsets, i
 // backward
 // --------------------------------------------------------------------------------------
 
-emb_status emb_backward_adagrad(emb_t h, const float* grad_out, float lr, double extra_sq_norm,
-                                double* sq_norm_out) {
+static emb_status backward_common(emb_t h, const float* grad_out, float lr, double extra_sq_norm,
+                                  const double* extra_dev, float* clip_out) {
   if (!h || !grad_out) return EMB_EINVAL;
   if (!h->have_fwd) return EMB_ESTATE;
   if (!(lr >= 0.f) || !(extra_sq_norm >= 0.0)) return EMB_EINVAL;
+  if ((extra_dev && !is_device_ptr(extra_dev)) || (clip_out && !is_device_ptr(clip_out)))
+    return EMB_EINVAL;
   const Plan& p = h->p;
   const float* g = grad_out;
   if (!is_device_ptr(grad_out)) {
@@ -777,17 +782,34 @@ emb_status emb_backward_adagrad(emb_t h, const float* grad_out, float lr, double
   } else if ((p.D & 3) == 0 && !aligned(grad_out, 16)) {
     return EMB_EINVAL;
   }
-  emb_status s;
   if (p.exch) {
-    if ((s = exchange_backward(h, g)) != EMB_OK) return s;
-    s = backward_local(h, h->x.pooled, lr, extra_sq_norm);
-  } else {
-    s = backward_local(h, g, lr, extra_sq_norm);
+    emb_status s = exchange_backward(h, g);
+    if (s != EMB_OK) return s;
+    return backward_local(h, h->x.pooled, lr, extra_sq_norm, extra_dev, clip_out);
   }
+  return backward_local(h, g, lr, extra_sq_norm, extra_dev, clip_out);
+}
+
+emb_status emb_backward_adagrad(emb_t h, const float* grad_out, float lr, double extra_sq_norm,
+                                double* sq_norm_out) {
+  emb_status s = backward_common(h, grad_out, lr, extra_sq_norm, nullptr, nullptr);
   if (s != EMB_OK) return s;
   if (sq_norm_out) {
     CK(cudaMemcpyAsync(sq_norm_out, h->S_global, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
+  }
+  return EMB_OK;
+}
+
+emb_status emb_backward_adagrad_dev(emb_t h, const float* grad_out, float lr,
+                                    const double* extra_sq_norm_dev, float* clip_out_dev,
+                                    double* sq_norm_out_dev) {
+  emb_status s = backward_common(h, grad_out, lr, 0.0, extra_sq_norm_dev, clip_out_dev);
+  if (s != EMB_OK) return s;
+  if (sq_norm_out_dev) {
+    if (!is_device_ptr(sq_norm_out_dev)) return EMB_EINVAL;
+    CK(cudaMemcpyAsync(sq_norm_out_dev, h->S_global, sizeof(double), cudaMemcpyDeviceToDevice,
+                       h->stream));
   }
   return EMB_OK;
 }

@@ -357,19 +357,24 @@ k_norm_partial(const double* __restrict__ norm_main, const double* __restrict__ 
 
 // S = sum of rank partials in rank order + extra; c = (n > max_norm) ? max_norm/n : 1.
 // Non-finite S: c = -1 (the update kernel then skips every row) + sticky status.
-__global__ void k_norm_finalize(const double* parts, int nparts, double extra, float max_norm,
-                                double* S_global, float* clip, uint32_t* status) {
+__global__ void k_norm_finalize(const double* parts, int nparts, double extra,
+                                const double* extra_dev, float max_norm, double* S_global,
+                                float* clip, float* clip_out, uint32_t* status) {
   double S = 0.0;
   for (int r = 0; r < nparts; ++r) S += parts[r];
   S += extra;
+  if (extra_dev) S += *extra_dev;
   *S_global = S;
+  float c;
   if (!isfinite(S)) {
-    *clip = -1.0f;
+    c = -1.0f;
     atomicOr(status, kStNonFinite);
-    return;
+  } else {
+    const double n = sqrt(S);
+    c = (n > (double)max_norm) ? (float)((double)max_norm / n) : 1.0f;
   }
-  const double n = sqrt(S);
-  *clip = (n > (double)max_norm) ? (float)((double)max_norm / n) : 1.0f;
+  *clip = c;
+  if (clip_out) *clip_out = c;
 }
 
 // ---------------------------------------------------------------------------
@@ -748,8 +753,8 @@ cudaError_t launch_norm_partial(const BwdArgs& a, cudaStream_t s) {
 
 cudaError_t launch_norm_finalize(const double* parts, int nparts, const BwdArgs& a,
                                  cudaStream_t s) {
-  k_norm_finalize<<<1, 1, 0, s>>>(parts, nparts, a.extra_sq_norm, a.max_norm, a.S_global,
-                                  a.clip, a.status);
+  k_norm_finalize<<<1, 1, 0, s>>>(parts, nparts, a.extra_sq_norm, a.extra_dev, a.max_norm,
+                                  a.S_global, a.clip, a.clip_out, a.status);
   return cudaGetLastError();
 }
 

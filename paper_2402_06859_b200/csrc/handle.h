@@ -201,7 +201,8 @@ emb_status stage_inputs(emb_t h, const int32_t* ids, const int32_t* offsets, int
                         int64_t nnz, float* out, Staged* s);
 
 // a5-a8 on this rank's recorded occurrences (see api.cu).
-emb_status backward_local(emb_t h, const float* grad_dev, float lr, double extra);
+emb_status backward_local(emb_t h, const float* grad_dev, float lr, double extra,
+                          const double* extra_dev, float* clip_out);
 // a5 (sort + run-length encode) of the recorded occurrences on the side stream.
 emb_status launch_dedup(emb_t h);
 // make the main stream wait for a pending dedup (before reusing kvA or reading its output)

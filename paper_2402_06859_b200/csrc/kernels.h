@@ -113,6 +113,8 @@ struct BwdArgs {
   float* clip;              // device scalar
   uint32_t* status;
   double extra_sq_norm;
+  const double* extra_dev;  // optional device fp64 added to S (the caller's dense term)
+  float* clip_out;          // optional device copy of the clip factor c
   float max_norm;
   // update
   float* Wt;                // tables

@@ -159,6 +159,18 @@ class ShardedEmbedding:
                                      _ptr(out)), "emb_forward")
         return out
 
+    def backward_adagrad_dev(self, grad: torch.Tensor, lr: float,
+                             extra_sq_norm: Optional[torch.Tensor] = None,
+                             clip_out: Optional[torch.Tensor] = None,
+                             sq_norm_out: Optional[torch.Tensor] = None) -> None:
+        """a5-a8 with the dense side's squared norm read on the device (fp64 scalar tensor) and
+        the clip factor / S written to device tensors: no host synchronisation (NEXT-2)."""
+        assert grad.dtype == torch.float32 and grad.is_contiguous()
+        for t, dt in ((extra_sq_norm, torch.float64), (clip_out, torch.float32), (sq_norm_out, torch.float64)):
+            assert t is None or (t.is_cuda and t.dtype == dt and t.numel() == 1)
+        L.check(self.lib.emb_backward_adagrad_dev(self.h, _ptr(grad), float(lr), _ptr(extra_sq_norm),
+                                                  _ptr(clip_out), _ptr(sq_norm_out)), "emb_backward_adagrad_dev")
+
     def backward_adagrad(self, grad: torch.Tensor, lr: float, extra_sq_norm: float = 0.0,
                          want_norm: bool = False):
         assert grad.dtype == torch.float32 and grad.is_contiguous()
