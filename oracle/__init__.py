@@ -60,6 +60,10 @@ def lib():
             "ora_quantize_row_minmax": (i32, [P, i32, P, P, P]),
             "ora_quantize_minmax": (i64, [P, i64, i32, P, P, P]),
             "ora_forward_q8_minmax": (i64, [P, P, P, P, P, P, i32, P]),
+            "ora_cold_weight_init": (None, [P, P, i64, f32, P]),
+            "ora_fim_penalty": (f64, [P, i64, P, P, P, P, f32, f32]),
+            "ora_fim_penalty_grad": (None, [P, P, i64, i32, P, P, P, P, f32, f32, P]),
+            "ora_train_step_fim": (i32, [P, P, P, i32, P, P, i32, P, f32, f32, f32, f64, P, P, P, P, f32, f32, P, P]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -261,3 +265,45 @@ def forward_q8_minmax(pb: Problem, codes, mn, scale, ids, offsets, B):
     out = np.zeros((B, pb.F, pb.dim), dtype=np.float32)
     inv = lib().ora_forward_q8_minmax(pb.ref, _p(codes), _p(mn), _p(scale), _p(ids), _p(offsets), B, _p(out))
     return out, int(inv)
+
+
+# ---- NEXT-3: incremental training (oracle.h) ------------------------------------------
+
+def cold_weight_init(w0, w1, alpha):
+    w0, w1 = _f32(w0), _f32(w1)
+    out = np.zeros_like(w0)
+    lib().ora_cold_weight_init(_p(w0), _p(w1), w0.size, float(alpha), _p(out))
+    return out
+
+
+def _opt(a):
+    return None if a is None else _f32(a)
+
+
+def fim_penalty(W, w0, H0, w1, H1, lam, alpha):
+    W = _f32(W)
+    return float(lib().ora_fim_penalty(_p(W), W.size, _p(_opt(w0)), _p(_opt(H0)), _p(_opt(w1)),
+                                       _p(_opt(H1)), float(lam), float(alpha)))
+
+
+def fim_penalty_grad(W, keys, G, w0, H0, w1, H1, lam, alpha):
+    """G (float32 [U][dim]) + the penalty gradient of rows `keys` (returns a new array)."""
+    W, G = _f32(W), _f32(G).copy()
+    keys = np.ascontiguousarray(keys, dtype=np.int64)
+    lib().ora_fim_penalty_grad(_p(W), _p(keys), len(keys), G.shape[1], _p(_opt(w0)), _p(_opt(H0)),
+                               _p(_opt(w1)), _p(_opt(H1)), float(lam), float(alpha), _p(G))
+    return G
+
+
+def train_step_fim(pb: Problem, W, A, ids, offsets, B, grad, lr, eps, max_norm, w0, H0, w1, H1,
+                   lam, alpha, mode="rowwise", extra_sq_norm=0.0):
+    """In place on W, A.  Returns dict(S, c, nonfinite)."""
+    assert W.dtype == np.float32 and W.flags.c_contiguous and A.dtype == np.float32
+    ids, offsets, grad = _i32(ids), _i32(offsets), _f32(grad)
+    anchors = [_opt(x) for x in (w0, H0, w1, H1)]
+    S = C.c_double(0)
+    c = C.c_float(0)
+    nf = lib().ora_train_step_fim(pb.ref, _p(W), _p(A), 0 if mode == "rowwise" else 1, _p(ids), _p(offsets), B,
+                                  _p(grad), float(lr), float(eps), float(max_norm), float(extra_sq_norm),
+                                  *[_p(a) for a in anchors], float(lam), float(alpha), C.byref(S), C.byref(c))
+    return dict(S=S.value, c=np.float32(c.value), nonfinite=bool(nf))

@@ -464,3 +464,66 @@ int64_t ora_forward_q8_minmax(const ora_cfg* c, const uint8_t* codes, const floa
   free(base);
   return invalid;
 }
+
+/* ------------------------------------------------------------------------------------ */
+/* NEXT-3: incremental training (oracle.h)                                                */
+void ora_cold_weight_init(const float* w0, const float* w1, int64_t n, float alpha, float* w) {
+  const float beta = 1.0f - alpha;
+  for (int64_t i = 0; i < n; ++i) w[i] = alpha * w0[i] + beta * w1[i];
+}
+
+double ora_fim_penalty(const float* W, int64_t n, const float* w0, const float* H0,
+                       const float* w1, const float* H1, float lambda, float alpha) {
+  double s0 = 0.0, s1 = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    if (w0 && H0) { const double d = (double)W[i] - (double)w0[i]; s0 += (double)H0[i] * d * d; }
+    if (w1 && H1) { const double d = (double)W[i] - (double)w1[i]; s1 += (double)H1[i] * d * d; }
+  }
+  return (double)lambda / 2.0 * ((double)alpha * s0 + (1.0 - (double)alpha) * s1);
+}
+
+void ora_fim_penalty_grad(const float* W, const int64_t* keys, int64_t U, int32_t dim,
+                          const float* w0, const float* H0, const float* w1, const float* H1,
+                          float lambda, float alpha, float* G) {
+  const float beta = 1.0f - alpha;
+  for (int64_t u = 0; u < U; ++u)
+    for (int32_t d = 0; d < dim; ++d) {
+      const int64_t i = keys[u] * dim + d;
+      float t0 = 0.0f, t1 = 0.0f;
+      if (w0 && H0) t0 = alpha * (H0[i] * (W[i] - w0[i]));
+      if (w1 && H1) t1 = beta * (H1[i] * (W[i] - w1[i]));
+      const float pen = lambda * (t0 + t1);
+      G[u * dim + d] = G[u * dim + d] + pen;
+    }
+}
+
+int32_t ora_train_step_fim(const ora_cfg* c, float* W, float* A, int32_t adagrad_mode,
+                           const int32_t* ids, const int32_t* offsets, int32_t B,
+                           const float* grad, float lr, float eps, float max_norm,
+                           double extra_sq_norm, const float* w0, const float* H0,
+                           const float* w1, const float* H1, float lambda, float alpha,
+                           double* S_out, float* c_out) {
+  const int32_t D = c->dim;
+  int64_t nnz = offsets[(int64_t)c->num_features * B];
+  size_t n1 = (size_t)(nnz > 0 ? nnz : 1);
+  int64_t* keys = (int64_t*)malloc(sizeof(int64_t) * n1);
+  int64_t* segs = (int64_t*)malloc(sizeof(int64_t) * (n1 + 1));
+  int64_t* bags = (int64_t*)malloc(sizeof(int64_t) * n1);
+  int64_t n_valid = 0;
+  int64_t U = ora_dedup(c, ids, offsets, B, keys, segs, bags, &n_valid);
+  float* G = (float*)malloc(sizeof(float) * (size_t)(U > 0 ? U : 1) * D);
+  ora_segment_reduce(c, offsets, B, U, segs, bags, grad, G);
+  ora_fim_penalty_grad(W, keys, U, D, w0, H0, w1, H1, lambda, alpha, G);
+  double S = ora_sq_norm(G, U, D, extra_sq_norm);
+  int nonfinite = 0;
+  float cf = ora_clip_factor(S, max_norm, &nonfinite);
+  if (S_out) *S_out = S;
+  if (c_out) *c_out = cf;
+  if (!nonfinite) {
+    ora_clip(G, U * D, cf, G);
+    if (adagrad_mode == 0) ora_adagrad_rowwise(W, A, keys, U, G, D, lr, eps);
+    else ora_adagrad_elementwise(W, A, keys, U, G, D, lr, eps);
+  }
+  free(keys); free(segs); free(bags); free(G);
+  return nonfinite ? 1 : 0;
+}

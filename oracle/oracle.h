@@ -152,6 +152,36 @@ int64_t ora_forward_q8_minmax(const ora_cfg* c, const uint8_t* codes, const floa
                               const float* scale, const int32_t* ids, const int32_t* offsets,
                               int32_t B, float* out);
 
+/* ---- NEXT-3: incremental training (Eq. 2-3) ---------
+ * Total loss = loss_D(w) + lambda_f/2 [alpha (w-w0)^T H0 (w-w0) + (1-alpha)(w-w1)^T H1 (w-w1)]
+ * with diagonal H (the empirical-FIM diagonal), w0 the cold-start model, w1 = w_{t-1}.
+ * Anchors w0, H0, w1, H1 are dense fp32 [total_rows][dim] like W (a NULL pair drops its term).
+ *
+ * cold-weight init ("initialized as alpha w0 + (1-alpha) w_{t-1}"), element-wise:
+ *   w = fl(fl(alpha * w0) + fl(fl(1 - alpha) * w1)). */
+void ora_cold_weight_init(const float* w0, const float* w1, int64_t n, float alpha, float* w);
+
+/* penalty value in fp64 (for pins): lambda/2 [alpha sum H0 (w-w0)^2 + (1-alpha) sum H1 (w-w1)^2]. */
+double ora_fim_penalty(const float* W, int64_t n, const float* w0, const float* H0,
+                       const float* w1, const float* H1, float lambda, float alpha);
+
+/* Its gradient added to the deduplicated row gradient of the TOUCHED rows only (reading 30:
+ * lazy, as sparse optimizers regularize the rows a step updates), before the global norm
+ * (it is part of the loss gradient), with W the pre-update weights:
+ *   pen = fl(lambda * fl(fl(alpha * fl(H0 * fl(w - w0))) + fl(fl(1 - alpha) * fl(H1 * fl(w - w1)))))
+ *   G[u][d] = fl(G[u][d] + pen)                       (a dropped term contributes 0) */
+void ora_fim_penalty_grad(const float* W, const int64_t* keys, int64_t U, int32_t dim,
+                          const float* w0, const float* H0, const float* w1, const float* H1,
+                          float lambda, float alpha, float* G);
+
+/* ora_train_step with the penalty gradient (a5, a6, + penalty, a7, a8). */
+int32_t ora_train_step_fim(const ora_cfg* c, float* W, float* A, int32_t adagrad_mode,
+                           const int32_t* ids, const int32_t* offsets, int32_t B,
+                           const float* grad, float lr, float eps, float max_norm,
+                           double extra_sq_norm, const float* w0, const float* H0,
+                           const float* w1, const float* H1, float lambda, float alpha,
+                           double* S_out, float* c_out);
+
 #ifdef __cplusplus
 }
 #endif
