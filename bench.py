@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--no-qr", action="store_true", help="skip the NEXT-1 QR/Murmur section")
     ap.add_argument("--no-model", action="store_true", help="skip the NEXT-2 end-to-end model section")
     ap.add_argument("--dense-features", type=int, default=256, help="NEXT-2 dense feature count")
+    ap.add_argument("--no-fim", action="store_true", help="skip the NEXT-3 incremental-training section")
     ap.add_argument("--q8-mode", default="middle_max", choices=["middle_max", "min_max"],
                     help="q8 store: the paper's middle-max (default) or NEXT-4's min-max")
     ap.add_argument("--cpu-samples", type=int, default=8192)
@@ -389,6 +390,77 @@ def model_section(emb, batches, dev_in, B, dense_dim, stream, flush, steps=10, w
             "loss_last": float(loss), "clip_last": float(model.c), "steps": steps, "warmup": warmup,
             "tf32": False}
 
+
+# ---------------------------------------------------------------------------
+# NEXT-3 section: incremental training (FIM penalty on touched rows, cold-weight init)
+# ---------------------------------------------------------------------------
+
+def fim_section(emb, dev_in, B, stream, flush, hbm_peak, steps=10, warmup=3):
+    """Eq. (2) (alpha = 0: the prior-model anchor w1 = w_{t-1} with its FIM diagonal H1) on
+    the Feed-1 tables -- the anchors of Eq. (3)'s cold-start term would need 2 more copies of
+    the 32 GB table -- and the cold-weight init as a full-table streaming pass."""
+    import torch
+
+    from workload import gpu as G
+    n = emb.local_rows * emb.pitch
+    with torch.cuda.stream(stream):
+        base = emb.weights_buf[: 4 * n].view(torch.float32).view(emb.local_rows, emb.pitch)
+        w1 = base.clone()
+        H1 = torch.rand_like(w1)
+    stream.synchronize()
+
+    def run(k0):
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for k in range(warmup):
+            ids_d, off_d, gd = dev_in[k % len(dev_in)]
+            emb.forward(ids_d, off_d, B)
+            emb.backward_adagrad(gd, LR)
+        stream.synchronize()
+        emb.profile(True)
+        emb.profile_read(reset=True)
+        with torch.cuda.stream(stream):
+            torch.cuda._sleep(1_000_000)
+            t0.record(stream)
+        for k in range(steps):
+            ids_d, off_d, gd = dev_in[k % len(dev_in)]
+            emb.forward(ids_d, off_d, B)
+            emb.backward_adagrad(gd, LR)
+        with torch.cuda.stream(stream):
+            t1.record(stream)
+        stream.synchronize()
+        ph = emb.profile_read()
+        emb.profile(False)
+        assert emb.sync() == 0
+        return t0.elapsed_time(t1) / steps, ph["norm"][0] / max(ph["norm"][1], 1)
+
+    plain_ms, plain_norm = run(0)
+    emb.set_incremental(None, None, w1, H1, 1e-3, 0.0)
+    fim_ms, fim_norm = run(1)
+    emb.set_incremental(None, None, None, None, 0.0, 0.0)
+    _, _, U = emb.last_stats()
+    ts = []
+    for _ in range(3):
+        G.flush_l2(flush, stream=stream)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            emb.cold_weight_init(w1, H1, 0.5)
+            e1.record(stream)
+        stream.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ci_ms = float(np.median(ts))
+    ci_b = 3 * 4 * n
+    pen_b = U * 4 * (3 * emb.pitch) + U * 4 * (2 * emb.pitch)  # G r/w, W, w1, H1 per touched row
+    del w1, H1
+    torch.cuda.empty_cache()
+    return {"what": "Feed-1 fwd + bwd with the Eq. (2) penalty (w1 = prior model, H1 = its FIM diagonal, "
+                    "lambda 1e-3) on the touched rows; cold-weight init over the 125M-row table",
+            "step_ms_plain": plain_ms, "step_ms_fim": fim_ms, "unique_rows": U,
+            "penalty_ms": fim_norm - plain_norm, "penalty_alg_bytes": pen_b,
+            "penalty_gbs": pen_b / max(fim_norm - plain_norm, 1e-9) * 1e3 / 1e9,
+            "cold_init_ms": ci_ms, "cold_init_gbs": ci_b / (ci_ms / 1e3) / 1e9,
+            "cold_init_frac_of_hbm": ci_b / (ci_ms / 1e3) / 1e9 / hbm_peak}
+
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
@@ -635,6 +707,11 @@ def run_ours(args, cfg, rank, world, local_rank):
             line["model"] = model_section(emb, batches, dev_in, B, args.dense_features, stream, flush)
         except Exception as e:  # report, never hide
             line["model"] = {"error": repr(e)}
+    if world == 1 and not args.no_fim:
+        try:
+            line["fim"] = fim_section(emb, dev_in, B, stream, flush, hbm_peak)
+        except Exception as e:  # report, never hide
+            line["fim"] = {"error": repr(e)}
     if world == 1 and not args.no_qr:
         try:
             line["qr"] = qr_section(cfg, batches[0][0], batches[0][1], B, dev, stream, flush, hbm_peak)

@@ -281,6 +281,27 @@ enum {
 EMB_API emb_status emb_profile(emb_t h, int32_t enable);
 EMB_API emb_status emb_profile_read(emb_t h, double* ms, int64_t* count, int32_t reset);
 
+/* ---- NEXT-3: incremental training (Eq. 2-3) -----------------------------
+ * Total loss = loss_D(w) + lambda_f/2 [alpha (w - w0)^T H0 (w - w0)
+ *                                      + (1 - alpha)(w - w1)^T H1 (w - w1)],
+ * H0, H1 the diagonal empirical-FIM approximations of the Hessian, w0 the cold-start
+ * model, w1 = w_{t-1} (the prior model), alpha the "cold weight".
+ *
+ * emb_set_incremental: every later emb_backward_adagrad* adds the penalty gradient
+ *   lambda_f [alpha H0 (w - w0) + (1 - alpha) H1 (w - w1)] (fp32, in this order) to the
+ *   deduplicated gradient of the rows the step TOUCHES (untouched rows are not regularized:
+ *   lazy, like the sparse update itself), before the global norm and the clip.  w0, H0, w1, H1
+ *   are DEVICE fp32 arrays in the weights' layout ([local_rows][row_pitch], 16-B aligned),
+ *   owned by the caller and read during each backward; a (w, H) pair may be NULL (both) to
+ *   drop its term.  lambda_f = 0 or both pairs NULL turns the penalty off.  EMB_EINVAL for
+ *   lambda_f < 0, alpha outside [0, 1], half a pair or host pointers.
+ * emb_cold_weight_init: W = alpha w0 + (1 - alpha) w1 over all local rows ("initialized
+ *   as alpha w0 + (1 - alpha) w_{t-1}"), fp32 fl(fl(alpha w0) + fl((1 - alpha) w1)); enqueued
+ *   on cfg.stream.  The q8 store is not touched (call emb_quantize_mm8). */
+EMB_API emb_status emb_set_incremental(emb_t h, const float* w0, const float* H0, const float* w1,
+                                       const float* H1, float lambda_f, float alpha);
+EMB_API emb_status emb_cold_weight_init(emb_t h, const float* w0, const float* w1, float alpha);
+
 /* Release the handle (and its NCCL communicator).  Does not free caller buffers. */
 EMB_API emb_status emb_destroy(emb_t h);
 

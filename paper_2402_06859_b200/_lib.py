@@ -99,6 +99,8 @@ SIGNATURES = {
     "emb_profile_read": (C.c_int, [P, P, P, C.c_int32]),
     "emb_destroy": (C.c_int, [P]),
     "emb_backward_adagrad_dev": (C.c_int, [P, P, C.c_float, P, P, P]),
+    "emb_set_incremental": (C.c_int, [P, P, P, P, P, C.c_float, C.c_float]),
+    "emb_cold_weight_init": (C.c_int, [P, P, P, C.c_float]),
     "emb_hash_ids": (C.c_int, [P, P, C.c_int64, P, P]),
     "emb_qr_expand": (C.c_int, [P, P, C.c_int64, C.c_int64, C.c_int32, C.c_int64, C.c_int32, P, P, P]),
     "emb_qr_rows": (C.c_int64, [C.c_int32, C.c_int64, C.c_int32]),

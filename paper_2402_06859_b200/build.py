@@ -23,7 +23,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",
          "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr",
          "-I", os.path.join(ROOT, "include")]
-SOURCES = ["forward.cu", "sort.cu", "backward.cu", "exchange.cu", "api.cu", "comm.cu", "qr.cu"]
+SOURCES = ["forward.cu", "sort.cu", "backward.cu", "exchange.cu", "api.cu", "comm.cu", "qr.cu", "incremental.cu"]
 HEADERS = ["common.cuh", "kernels.h", "comm.h", "handle.h", "lookback.cuh"]
 
 

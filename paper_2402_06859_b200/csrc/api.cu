@@ -390,6 +390,12 @@ emb_status backward_local(emb_t h, const float* grad_dev, float lr, double extra
   }
   {
     Phase ph(h->prof, h->stream, EMB_PH_NORM);
+    if (h->fim_on && n > 0) {  // NEXT-3: penalty gradient of the touched rows, norm re-formed
+      const int64_t ng = launch_fim_penalty(a, h->fim, h->stream);
+      if (ng < 0) return EMB_ECUDA;
+      a.chunks = ng;
+      h->launches += 1;
+    }
     CK(launch_norm_partial(a, h->stream));
     h->launches += 1;
     const double* parts = h->S_local;
@@ -921,6 +927,29 @@ emb_status emb_last_dedup(emb_t h, int32_t* unique, int32_t* seg_offsets, int64_
       sorted_bags[i] = (int32_t)(h->p.exch ? r : (r % F) * B + r / F);
     }
   }
+  return EMB_OK;
+}
+
+emb_status emb_set_incremental(emb_t h, const float* w0, const float* H0, const float* w1,
+                               const float* H1, float lambda_f, float alpha) {
+  if (!h) return EMB_EINVAL;
+  if (!(lambda_f >= 0.f) || !(alpha >= 0.f && alpha <= 1.f)) return EMB_EINVAL;
+  if ((w0 == nullptr) != (H0 == nullptr) || (w1 == nullptr) != (H1 == nullptr)) return EMB_EINVAL;
+  for (const float* p : {w0, H0, w1, H1})
+    if (p && (!is_device_ptr(p) || !aligned(p, 16))) return EMB_EINVAL;
+  h->fim = FimArgs{w0, H0, w1, H1, lambda_f, alpha};
+  h->fim_on = lambda_f > 0.f && (w0 != nullptr || w1 != nullptr);
+  return EMB_OK;
+}
+
+emb_status emb_cold_weight_init(emb_t h, const float* w0, const float* w1, float alpha) {
+  if (!h || !w0 || !w1) return EMB_EINVAL;
+  if (!(alpha >= 0.f && alpha <= 1.f)) return EMB_EINVAL;
+  if (!is_device_ptr(w0) || !is_device_ptr(w1) || !aligned(w0, 16) || !aligned(w1, 16))
+    return EMB_EINVAL;
+  const Plan& p = h->p;
+  CK(launch_cold_init(w0, w1, p.local_rows * p.pitch, alpha, h->W, h->stream));
+  h->launches += p.local_rows > 0;
   return EMB_OK;
 }
 

@@ -170,6 +170,9 @@ struct emb_handle {
   lirank::Transport* comm = nullptr;
   std::vector<uint32_t> h_cnt;  // [world][world] counts of the last forward
   int fmap_B = -1;              // batch the table-wise permute map was uploaded for
+  // NEXT-3 incremental-training penalty (emb_set_incremental)
+  lirank::FimArgs fim{};
+  bool fim_on = false;
   // state
   bool have_fwd = false;
   bool have_q8 = false;

@@ -128,6 +128,17 @@ struct BwdArgs {
 };
 cudaError_t launch_segreduce(const BwdArgs& a, int64_t* launches, cudaStream_t s);
 // reduces norm partials -> S_local (deterministic fixed order)
+// ---- NEXT-3: incremental training (incremental.cu) ----------------------------------
+struct FimArgs {
+  const float *w0, *H0, *w1, *H1;  // [local_rows][pitch] anchors (a NULL pair drops its term)
+  float lambda, alpha;
+};
+cudaError_t launch_cold_init(const float* w0, const float* w1, int64_t n, float alpha, float* w,
+                             cudaStream_t s);
+// adds the penalty gradient to G of the touched rows and rewrites the norm partials
+// (norm_main[0..ngroups), norm_fix zeroed); returns ngroups (-1: launch error)
+int64_t launch_fim_penalty(const BwdArgs& a, const FimArgs& f, cudaStream_t s);
+
 cudaError_t launch_norm_partial(const BwdArgs& a, cudaStream_t s);
 // S_global = sum of `nparts` rank partials (rank order) + extra -> clip factor, status
 cudaError_t launch_norm_finalize(const double* parts, int nparts, const BwdArgs& a,

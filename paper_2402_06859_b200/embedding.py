@@ -159,6 +159,25 @@ class ShardedEmbedding:
                                      _ptr(out)), "emb_forward")
         return out
 
+    def set_incremental(self, w0: Optional[torch.Tensor], H0: Optional[torch.Tensor],
+                        w1: Optional[torch.Tensor], H1: Optional[torch.Tensor], lambda_f: float,
+                        alpha: float) -> None:
+        """NEXT-3: diagonal-FIM penalty toward the cold-start (w0, H0) and prior (w1, H1) models
+        on every later backward (tensors in the weights' layout: [local_rows, pitch] fp32, kept
+        alive by this object)."""
+        for t in (w0, H0, w1, H1):
+            assert t is None or (t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()
+                                 and t.numel() == self.local_rows * self.pitch)
+        self._fim_refs = (w0, H0, w1, H1)
+        L.check(self.lib.emb_set_incremental(self.h, _ptr(w0), _ptr(H0), _ptr(w1), _ptr(H1), float(lambda_f),
+                                             float(alpha)), "emb_set_incremental")
+
+    def cold_weight_init(self, w0: torch.Tensor, w1: torch.Tensor, alpha: float) -> None:
+        """NEXT-3: W = alpha w0 + (1 - alpha) w1, tensors in the weights' layout."""
+        for t in (w0, w1):
+            assert t.is_cuda and t.dtype == torch.float32 and t.numel() == self.local_rows * self.pitch
+        L.check(self.lib.emb_cold_weight_init(self.h, _ptr(w0), _ptr(w1), float(alpha)), "emb_cold_weight_init")
+
     def backward_adagrad_dev(self, grad: torch.Tensor, lr: float,
                              extra_sq_norm: Optional[torch.Tensor] = None,
                              clip_out: Optional[torch.Tensor] = None,
