@@ -49,6 +49,9 @@ def parse():
     ap.add_argument("--no-qr", action="store_true", help="skip the NEXT-1 QR/Murmur section")
     ap.add_argument("--no-model", action="store_true", help="skip the NEXT-2 end-to-end model section")
     ap.add_argument("--dense-features", type=int, default=256, help="NEXT-2 dense feature count")
+    ap.add_argument("--exchange", action="store_true",
+                    help="N=1: run the sharded exchange path on a 1-rank NCCL communicator (its overhead)")
+    ap.add_argument("--sharding", default="row", choices=["row", "table"], help="sharding for N>1 / --exchange")
     ap.add_argument("--no-fim", action="store_true", help="skip the NEXT-3 incremental-training section")
     ap.add_argument("--q8-mode", default="middle_max", choices=["middle_max", "min_max"],
                     help="q8 store: the paper's middle-max (default) or NEXT-4's min-max")
@@ -485,15 +488,16 @@ def run_ours(args, cfg, rank, world, local_rank):
         batches.append((ids, off))
     max_nnz = max(len(i) for i, _ in batches)
     shard_kw = {}
-    if world > 1:
-        # row-wise sharding over NCCL; rank 0 makes the unique id, a broadcast distributes it
+    if world > 1 or args.exchange:
+        # sharded over NCCL (or the exchange path on 1 rank); rank 0 makes the unique id, a broadcast distributes it
         from paper_2402_06859_b200 import nccl_unique_id
         uid = torch.zeros(128, dtype=torch.uint8, device=dev)
         if rank == 0:
             uid.copy_(torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8))
-        dist.broadcast(uid, 0)
-        shard_kw = dict(rank=rank, world_size=world, sharding="row", nccl_unique_id=uid.cpu().numpy().tobytes(),
-                        max_recv_nnz=3 * max_nnz)
+        if world > 1:
+            dist.broadcast(uid, 0)
+        shard_kw = dict(rank=rank, world_size=world, sharding=args.sharding, nccl_unique_id=uid.cpu().numpy().tobytes(),
+                        max_recv_nnz=3 * max_nnz, force_exchange=args.exchange)
     emb = ShardedEmbedding(cfg.table_rows, D, cfg.feature_table, max_nnz=max_nnz, max_batch=B,
                            adagrad=args.adagrad, q8=True, requant=True, device=dev, stream=stream,
                            q8_mode=args.q8_mode, **shard_kw)
@@ -686,7 +690,9 @@ def run_ours(args, cfg, rank, world, local_rank):
         "config": {"workload": cfg.name, "tables": cfg.table_rows, "dim": D, "features": F,
                    "global_batch": world * B, "batch_per_gpu": B, "nnz_per_step": nnz_avg, "alpha": cfg.alpha,
                    "unique_rows": U, "adagrad": args.adagrad, "q8": args.q8_mode,
-                   "parallelism": "single" if world == 1 else f"row-sharded x{world} (NCCL all-to-all ids, reduce-scatter pooled, all-gather grads)",
+                   "parallelism": ("single" if not args.exchange else f"{args.sharding}-sharded exchange path on a 1-rank NCCL communicator")
+                   if world == 1 else (f"row-sharded x{world} (NCCL all-to-all ids, reduce-scatter pooled, all-gather grads)"
+                                       if args.sharding == "row" else f"table-sharded x{world} (NCCL all-to-all ids and pooled blocks)"),
                    "step": "a2 fwd -> a10 q8 fwd (overlapping a5 dedup on a side stream) -> a6-a8 bwd (a9 requant of touched rows fused)",
                    "l2": "flushed between timed steps (256 MiB write, untimed)",
                    "batches_rotated": len(batches)},

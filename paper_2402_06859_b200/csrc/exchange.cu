@@ -60,8 +60,8 @@ k_scan_excl(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, int64_t
       s_warp[w] = t;
       t += c;
     }
-    lb_publish(status, tile, kRadixBinsMax, 0, epoch, t);
-    s_excl = lb_wait(status, tile, kRadixBinsMax, 0, epoch, t);
+    lb_publish(status, tile, 1, 0, epoch, t);
+    s_excl = lb_wait(status, tile, 1, 0, epoch, t);
   }
   __syncthreads();
   uint32_t run = s_excl + s_warp[warp] + x - sum;
@@ -160,8 +160,10 @@ emb_status scan(emb_t h, const uint32_t* in, uint32_t* out, int64_t n, int which
   CK(cudaMemsetAsync(h->x.scan_counter + which, 0, sizeof(uint32_t), h->stream));
   if (n == 0) return cudaMemsetAsync(out, 0, sizeof(uint32_t), h->stream) == cudaSuccess ? EMB_OK : EMB_ECUDA;
   const int64_t tiles = (n + kScanTile - 1) / kScanTile;
+  // its own look-back words: the a5 dedup of the previous forward may still be running on
+  // the side stream with the radix sort's status array
   k_scan_excl<<<(unsigned)tiles, kScanThreads, 0, h->stream>>>(in, out, n, h->x.scan_counter + which,
-                                                               h->sort.status, h->epoch);
+                                                               h->x.scan_status, h->epoch);
   h->epoch += 1;
   h->launches += 1;
   return cudaGetLastError() == cudaSuccess ? EMB_OK : EMB_ECUDA;
@@ -190,6 +192,8 @@ void carve_exchange(const Plan& p, Carver& cv, ExchangeWs* x) {
   x->d_owner0 = cv.take<int32_t>(F);
   x->d_blk = cv.take<int32_t>(F);
   x->scan_counter = cv.take<uint32_t>(4);
+  const int64_t scan_n = std::max<int64_t>(Ltot + 1, W * Fr * B + 1);
+  x->scan_status = cv.take<unsigned long long>((scan_n + kScanTile - 1) / kScanTile + 1);
 }
 
 emb_status exchange_init(emb_t h) {

@@ -124,6 +124,7 @@ struct ExchangeWs {
   int32_t* d_owner0 = nullptr;         // [F]
   int32_t* d_blk = nullptr;            // [F]
   uint32_t* scan_counter = nullptr;    // [4] tile counters of the exchange scans
+  unsigned long long* scan_status = nullptr;  // look-back words of the exchange scans
 };
 
 }  // namespace lirank

@@ -199,3 +199,36 @@ def test_nccl_transport_single_rank(gpu, sharding):
     assert torch.equal(ex.weights, ref.weights) and torch.equal(ex.accum_buf[:4 * sum(rows)], ref.accum_buf[:4 * sum(rows)])
     assert ex.last_stats()[0] == ref.last_stats()[0]
     ex.close()
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("sharding", ["table", "row"])
+def test_exchange_q8_forward_while_dedup_runs(gpu, sharding):
+    """Regression: forward -> forward_q8 -> backward on the exchange path at a size where the
+    a5 dedup (side stream) is still running when forward_q8's exchange scans start.  The
+    scans have their own look-back words (they used to share the radix sort's and could
+    wait forever on a word the sort overwrote)."""
+    from paper_2402_06859_b200 import ShardedEmbedding, nccl_unique_id
+    rows = [400_000, 20_000]
+    ft = [0, 1, 0]
+    cfg = configs.Config("ex_mid", rows, 64, [(t, ("range", 1, 60)) for t in ft], 8192, seed=21)
+    B, F, D = cfg.batch, cfg.num_features, cfg.dim
+    ids, off = gen.make_batch(rows, cfg.features, B, cfg.seed, 0)
+    grad = torch.from_numpy(gen.grad_values(cfg.seed, 0, B, F, D, gen.grad_shift_for(len(ids), D))).cuda()
+    ex = ShardedEmbedding(rows, D, ft, max_nnz=len(ids), max_batch=B, device=torch.device("cuda:0"), rank=0,
+                          world_size=1, sharding=sharding, nccl_unique_id=nccl_unique_id(), force_exchange=True,
+                          q8=True, max_recv_nnz=len(ids))
+    ref = ShardedEmbedding(rows, D, ft, max_nnz=len(ids), max_batch=B, device=torch.device("cuda:0"), q8=True)
+    ids_d, off_d = torch.from_numpy(ids).cuda(), torch.from_numpy(off).cuda()
+    res = []
+    for e in (ex, ref):
+        init_tables_host(e, cfg)
+        e.quantize()
+        for _ in range(3):
+            o = e.forward(ids_d, off_d, B)
+            q = e.forward_q8(ids_d, off_d, B)
+            e.backward_adagrad(grad, 0.05)
+        assert e.sync() == 0
+        res.append((o.cpu().numpy(), q.cpu().numpy()))
+    assert (res[0][0] == res[1][0]).all() and (res[0][1] == res[1][1]).all()
+    assert torch.equal(ex.weights, ref.weights)
