@@ -16,7 +16,6 @@
 //   in shared memory in sorted order; the tile is then written out in digit runs
 //   (coalesced).  Each pass moves 16 B per pair.  Tiles are claimed in launch order
 //   through an atomic counter, so a look-back only waits on tiles already resident.
-#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -266,23 +265,14 @@ cudaError_t radix_sort_pairs(uint2* kv0, uint2* kv1, int64_t n, int bits, const 
     else k_radix_hist<8><<<grid, 128, sm, s>>>(kv0, n, passes, ws.hist);
     ++*launches;
   }
-  static const int variant = [] {
-    const char* v = getenv("LIRANK_SORT_VARIANT");  // tuning experiments only
-    return v ? atoi(v) : 0;
-  }();
   uint2 *a = kv0, *b = kv1;
   for (int p = 0; p < passes; ++p) {
     const int shift = p * dbits;
     const uint32_t* hp = ws.hist + p * bins;
     uint32_t* ctr = ws.counters + p;
-#define OS(BITS) \
-    switch (variant) { \
-      case 1: e = onesweep_pass<BITS, 8, false>(a, b, n, shift, hp, ctr, ws.status, epoch + p, s); break; \
-      case 2: e = onesweep_pass<BITS, 16, true>(a, b, n, shift, hp, ctr, ws.status, epoch + p, s); break; \
-      case 3: e = onesweep_pass<BITS, 12, false>(a, b, n, shift, hp, ctr, ws.status, epoch + p, s); break; \
-      case 4: e = onesweep_pass<BITS, 8, true>(a, b, n, shift, hp, ctr, ws.status, epoch + p, s); break; \
-      default: e = onesweep_pass<BITS, 16, false>(a, b, n, shift, hp, ctr, ws.status, epoch + p, s); \
-    }
+    // 16 items per thread with the ballot multisplit measured best on Feed-1 (8 and 12
+    // items, and match.any ranking, were within noise or slower)
+#define OS(BITS) e = onesweep_pass<BITS, 16, false>(a, b, n, shift, hp, ctr, ws.status, epoch + p, s);
     if (dbits == 9) { OS(9) } else { OS(8) }
 #undef OS
     if (e != cudaSuccess) return e;
