@@ -165,7 +165,7 @@ __device__ __forceinline__ uint4 ld_nc_u4(const void* p) {
 // warp-uniform trip count, so a lane spends its instructions on the dequant, not on
 // per-slot key arithmetic.
 template <int LPB, int VPL, bool MEAN>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 4)
 k_pool_fwd_q8(const uint8_t* __restrict__ codes, int qpitch, int meta_off,
               const int* __restrict__ ids, const int* __restrict__ offsets, int B, int F, int Fb,
               int D, const FeatMeta* __restrict__ meta, float* __restrict__ out,

@@ -107,8 +107,8 @@ k_radix_hist(const uint2* __restrict__ kv, int64_t n, int passes, uint32_t* hist
 // One digit pass.  ITEMS pairs per thread (tile = 256 * ITEMS); MATCH selects the warp
 // ranking primitive (match.any vs a BITS-ballot multisplit).
 // ---------------------------------------------------------------------------
-template <int BITS, int ITEMS, bool MATCH>
-__global__ void __launch_bounds__(kSortThreads)
+template <int BITS, int ITEMS, bool MATCH, int MINB = 4>
+__global__ void __launch_bounds__(kSortThreads, MINB)
 k_onesweep(const uint2* __restrict__ in, uint2* __restrict__ out, int64_t n, int shift,
            const uint32_t* __restrict__ hist, uint32_t* tile_counter,
            unsigned long long* status, uint32_t epoch) {
@@ -226,7 +226,7 @@ k_onesweep(const uint2* __restrict__ in, uint2* __restrict__ out, int64_t n, int
   }
 }
 
-template <int BITS, int ITEMS, bool MATCH>
+template <int BITS, int ITEMS, bool MATCH, int MINB>
 static cudaError_t onesweep_pass(const uint2* a, uint2* b, int64_t n, int shift, const uint32_t* hist,
                                  uint32_t* counter, unsigned long long* status, uint32_t epoch,
                                  cudaStream_t s) {
@@ -234,12 +234,12 @@ static cudaError_t onesweep_pass(const uint2* a, uint2* b, int64_t n, int shift,
   const size_t sm = sizeof(uint2) * TILE + sizeof(uint32_t) * (NW * (1 << BITS) + (1 << BITS) + NW + 2);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_onesweep<BITS, ITEMS, MATCH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(k_onesweep<BITS, ITEMS, MATCH, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     attr = true;
   }
   const int64_t tiles = (n + TILE - 1) / TILE;
-  k_onesweep<BITS, ITEMS, MATCH><<<(unsigned)tiles, kSortThreads, sm, s>>>(a, b, n, shift, hist, counter,
-                                                                          status, epoch);
+  k_onesweep<BITS, ITEMS, MATCH, MINB><<<(unsigned)tiles, kSortThreads, sm, s>>>(a, b, n, shift, hist,
+                                                                                counter, status, epoch);
   return cudaGetLastError();
 }
 
@@ -270,9 +270,11 @@ cudaError_t radix_sort_pairs(uint2* kv0, uint2* kv1, int64_t n, int bits, const 
     const int shift = p * dbits;
     const uint32_t* hp = ws.hist + p * bins;
     uint32_t* ctr = ws.counters + p;
-    // 16 items per thread with the ballot multisplit measured best on Feed-1 (8 and 12
-    // items, and match.any ranking, were within noise or slower)
-#define OS(BITS) e = onesweep_pass<BITS, 16, false>(a, b, n, shift, hp, ctr, ws.status, epoch + p, s);
+    // 16 items per thread, ballot multisplit, 4 CTAs/SM (64 registers: the few spilled
+    // values stay in L1) measured best on Feed-1: the tile's global loads are latency-bound
+    // and more resident CTAs overlap them (2 CTAs at 120 registers: +10% sort time; 8 or
+    // 12 items at 5-8 CTAs and match.any ranking were slower)
+#define OS(BITS) e = onesweep_pass<BITS, 16, false, 4>(a, b, n, shift, hp, ctr, ws.status, epoch + p, s);
     if (dbits == 9) { OS(9) } else { OS(8) }
 #undef OS
     if (e != cudaSuccess) return e;
