@@ -53,6 +53,8 @@ def parse():
                     help="N=1: run the sharded exchange path on a 1-rank NCCL communicator (its overhead)")
     ap.add_argument("--sharding", default="row", choices=["row", "table"], help="sharding for N>1 / --exchange")
     ap.add_argument("--no-fim", action="store_true", help="skip the NEXT-3 incremental-training section")
+    ap.add_argument("--serve", action="store_true",
+                    help="serving bench: q8-only handle, a10 lookups only (default for --config feedq8)")
     ap.add_argument("--q8-mode", default="middle_max", choices=["middle_max", "min_max"],
                     help="q8 store: the paper's middle-max (default) or NEXT-4's min-max")
     ap.add_argument("--cpu-samples", type=int, default=8192)
@@ -464,6 +466,179 @@ def fim_section(emb, dev_in, B, stream, flush, hbm_peak, steps=10, warmup=3):
             "cold_init_ms": ci_ms, "cold_init_gbs": ci_b / (ci_ms / 1e3) / 1e9,
             "cold_init_frac_of_hbm": ci_b / (ci_ms / 1e3) / 1e9 / hbm_peak}
 
+
+# ---------------------------------------------------------------------------
+# serving arm: the Feed-shaped inference config (q8 store only, a10 lookups)
+# ---------------------------------------------------------------------------
+
+def serving_cpu_baseline(cfg, ids, off, B, samples, q8_mode, budget_s=10.0):
+    """The oracle's a10 (as it stands) on the first `samples` samples of batch 0 over the
+    compact q8 table of the rows they touch (quantized by the oracle, untimed)."""
+    import time as _t
+    smp = OracleSample(cfg, ids, off, B, samples, "rowwise")
+    O = smp.O
+    if q8_mode == "min_max":
+        codes, base_, sc, _ = O.quantize_minmax(smp.W0)
+        fn = O.forward_q8_minmax
+    else:
+        codes, base_, sc, _ = O.quantize(smp.W0)
+        fn = O.forward_q8
+    t0 = _t.perf_counter()
+    fn(smp.pb, codes, base_, sc, smp.cids, smp.soff, smp.Bs)
+    t1 = _t.perf_counter() - t0
+    reps = max(1, int(budget_s / max(t1, 1e-3)))
+    t0 = _t.perf_counter()
+    for _ in range(reps):
+        fn(smp.pb, codes, base_, sc, smp.cids, smp.soff, smp.Bs)
+    t = (_t.perf_counter() - t0) / reps
+    return {"value": smp.Bs / t, "unit": "samples/s", "cores": 1, "kind": "oracle",
+            "sample": f"{smp.Bs} of {B} samples of batch 0 ({smp.nnz} ids), a10 over the {len(smp.W0)} "
+                      f"touched rows quantized by the oracle (untimed), single-threaded C oracle, {reps + 1} reps"}
+
+
+def run_serving(args, cfg, rank, world, local_rank):
+    """BASELINE.json's Feed-shaped inference config: the 1B-row Feed tables middle-max 8-bit
+    quantized (96 GB: one q8-only replica per GPU), q8 pooled lookups of B = 262144
+    samples per step.  N GPUs = N independent replicas, each with its own batch ("replicas
+    only": the serving path has no exchange)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2402_06859_b200 import ShardedEmbedding
+    from workload import gpu as G
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.Stream(dev)
+    B, D, F = cfg.batch, cfg.dim, cfg.num_features
+    batches = [gen.make_batch(cfg.table_rows, cfg.features, B, cfg.seed + 7919 * rank, k, alpha=cfg.alpha)
+               for k in range(args.batches)]
+    max_nnz = max(len(i) for i, _ in batches)
+    emb = ShardedEmbedding(cfg.table_rows, D, cfg.feature_table, max_nnz=max_nnz, max_batch=B, q8_only=True,
+                           q8_mode=args.q8_mode, device=dev, stream=stream)
+    chunk = 1 << 25  # 32M rows (8 GB fp32) per generated block
+    with torch.cuda.stream(stream):
+        scratch = torch.empty(min(chunk, max(cfg.table_rows)) * D, device=dev)
+        for t, rows in enumerate(cfg.table_rows):
+            r = 0
+            while r < rows:
+                n = min(chunk, rows - r)
+                blk = scratch[: n * D].view(n, D)
+                G.fill_table(blk, n, D, D, cfg.seed, t, row0=r, stream=stream)
+                emb.quantize_block(t, r, blk)
+                r += n
+        del scratch
+        dev_in = [(torch.from_numpy(i).to(dev), torch.from_numpy(o).to(dev)) for i, o in batches]
+        out = torch.empty((B, F, D), device=dev)
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream.synchronize()
+    torch.cuda.empty_cache()
+    assert emb.sync() == 0
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for k in range(args.warmup):
+        ids_d, off_d = dev_in[k % len(dev_in)]
+        emb.forward_q8(ids_d, off_d, B, out=out)
+    stream.synchronize()
+    K = args.steps
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    clocks = ClockSampler(local_rank).begin()
+    barrier()
+    torch.cuda.synchronize(dev)
+    launches0 = emb.launches
+    emb.profile(True)
+    emb.profile_read(reset=True)
+    for k in range(K):
+        G.flush_l2(flush, stream=stream)
+        ids_d, off_d = dev_in[(args.warmup + k) % len(dev_in)]
+        with torch.cuda.stream(stream):
+            evs[k][0].record(stream)
+        emb.forward_q8(ids_d, off_d, B, out=out)
+        with torch.cuda.stream(stream):
+            evs[k][1].record(stream)
+    torch.cuda.synchronize(dev)
+    barrier()
+    clk = clocks.result()
+    launches = emb.launches - launches0
+    ph = emb.profile_read()
+    emb.profile(False)
+    assert emb.sync() == 0
+    ms = float(np.mean([a.elapsed_time(b) for a, b in evs]))
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    nnz_avg = float(np.mean([len(i) for i, _ in batches]))
+    # e2e: ids/offsets H2D (pinned) and the pooled result D2H, every step, through the API
+    e2e = None
+    if not args.no_e2e:
+        host_in = [(torch.from_numpy(i).pin_memory(), torch.from_numpy(o).pin_memory()) for i, o in batches]
+        out_h = torch.empty((B, F, D), dtype=torch.float32).pin_memory()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        torch.cuda.synchronize(dev)
+        with torch.cuda.stream(stream):
+            t0.record(stream)
+        for k in range(K):
+            ids_h, off_h = host_in[k % len(host_in)]
+            emb.forward_q8(ids_h, off_h, B, out=out_h)
+        with torch.cuda.stream(stream):
+            t1.record(stream)
+        torch.cuda.synchronize(dev)
+        barrier()
+        assert emb.sync() == 0
+        e_ms = t0.elapsed_time(t1) / K
+        if world > 1:
+            t = torch.tensor([e_ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        e2e = {"value": world * B / (e_ms / 1e3), "unit": "samples/s", "ms_per_step": e_ms,
+               "h2d_bytes_per_step": int(nnz_avg * 4 + (F * B + 1) * 4), "d2h_bytes_per_step": B * F * D * 4,
+               "path": "emb_forward_q8 with pinned host ids/offsets/out (staging copies inside the call)"}
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    q_ms = ph["fwd_q8"][0] / max(ph["fwd_q8"][1], 1)
+    ab = alg_bytes("fwd_q8", cfg, nnz_avg, 0, B, emb.pitch)
+    traffic = None
+    try:
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get("serve_fwd_q8", {}).get(
+            "dram_bytes_per_launch")
+    except Exception:
+        pass
+    line = {
+        "metric": METRIC, "value": world * B / (ms / 1e3), "unit": "samples/s", "n_gpus": world, "steps": K,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u8 codes, f32 accumulate", "data": "synthetic (seeded Zipf ids, Irwin-Hall tables)",
+        "config": {"workload": cfg.name, "tables": cfg.table_rows, "dim": D, "features": F, "global_batch": world * B,
+                   "batch_per_gpu": B, "nnz_per_step": nnz_avg, "alpha": cfg.alpha, "q8": args.q8_mode,
+                   "q8_store_bytes": int(emb.local_rows * emb.q8_pitch),
+                   "parallelism": "single" if world == 1 else f"replicas x{world} (one q8 replica per GPU)",
+                   "step": "a10 q8 pooled lookup (serving handle, EMB_F_Q8_ONLY)",
+                   "l2": "flushed between timed steps (256 MiB write, untimed)", "batches_rotated": len(batches)},
+        "q8_lookups_per_s": world * nnz_avg / (ms / 1e3),
+        "roofline": {"bound": "hbm", "kernel": "fwd_q8", "achieved": ab / (q_ms / 1e3) / 1e9, "peak": hbm_peak,
+                     "unit": "GB/s", "frac": ab / (q_ms / 1e3) / 1e9 / hbm_peak, "traffic": traffic,
+                     "alg_bytes_per_launch": ab,
+                     "timing": "CUDA events on the library stream around the kernel phase, mean over timed steps"},
+        "clocks": clk, "gpu_launches": launches, "e2e": e2e,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            line["cpu_baseline"] = serving_cpu_baseline(cfg, batches[0][0], batches[0][1], B, args.cpu_samples,
+                                                        args.q8_mode)
+            line["cpu_baseline"]["cores_available"] = os.cpu_count()
+        except Exception as e:  # report, never hide
+            line["cpu_baseline"] = {"error": repr(e)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
@@ -742,7 +917,8 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1 and args.impl == "ours":
+    serve = args.serve or cfg.name.startswith("feedq8")
+    if world > 1 and args.impl == "ours" and not serve:
         # weak scaling: every GPU keeps the 1-GPU shard size and batch; the tables are the
         # W-fold Feed tables (W=8: the 1B-row Feed config of BASELINE.json), row-wise sharded
         cfg = cfg.with_(name=f"{cfg.name}-x{world}", table_rows=[r * world for r in cfg.table_rows])
@@ -755,7 +931,10 @@ def main():
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
-        run_ours(args, cfg, rank, world, local_rank)
+        if serve:
+            run_serving(args, cfg, rank, world, local_rank)
+        else:
+            run_ours(args, cfg, rank, world, local_rank)
     finally:
         if world > 1:
             import torch.distributed as dist

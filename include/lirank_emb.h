@@ -89,6 +89,13 @@ enum { EMB_SHARD_NONE = 0, EMB_SHARD_TABLE = 1, EMB_SHARD_ROW = 2 };
                              uint8 codes = clamp(round((x - min) / scale), 0, 255), meta {min,
                              scale} in place of {middle, scale}; a10 dequantizes
                              fmaf(code, scale, min).  Same row layout and kernels.             */
+#define EMB_F_Q8_ONLY 32u  /* (needs EMB_F_Q8) SERVING handle (P:549-557 in-memory serving of the
+                             quantized tables): no fp32 weights or accumulators exist
+                             (weights_bytes = accum_bytes = 0; buf.weights / buf.accum may be
+                             NULL) and no training workspace is planned.  Rows enter the q8
+                             store through emb_quantize_block; emb_forward_q8 serves lookups.
+                             Training / fp32 calls return EMB_ESTATE.  This is what lets the
+                             1B-row Feed tables (96 GB as q8) be served from one GPU.          */
 #define EMB_F_EXCHANGE 8u /* run the sharded exchange path even at world_size 1 (a 1-rank
                              communicator; exercises the transport on a single GPU)          */
 #define EMB_F_LOOPBACK 4u /* (world_size > 1) TEST TRANSPORT: the ranks are threads of one
@@ -280,6 +287,15 @@ enum {
 };
 EMB_API emb_status emb_profile(emb_t h, int32_t enable);
 EMB_API emb_status emb_profile_read(emb_t h, double* ms, int64_t* count, int32_t reset);
+
+/* Quantize (a9, the store's mode) a block of table rows given in fp32 into the q8 store:
+ * rows[i * ld .. + D) holds row row0 + i of `table` (GLOBAL row index; every row of the block
+ * must be stored on this rank), i < n.  rows is a DEVICE pointer, 16-B aligned, ld % 4 == 0,
+ * ld >= D.  Enqueued on cfg.stream.  Marks the q8 store as filled (the caller is responsible
+ * for covering every row it will look up).  Needs EMB_F_Q8; works with or without fp32
+ * tables (with them, the block is NOT written to the fp32 table). */
+EMB_API emb_status emb_quantize_block(emb_t h, int32_t table, int64_t row0, int64_t n,
+                                      const float* rows, int64_t ld);
 
 /* ---- NEXT-3: incremental training (Eq. 2-3) -----------------------------
  * Total loss = loss_D(w) + lambda_f/2 [alpha (w - w0)^T H0 (w - w0)

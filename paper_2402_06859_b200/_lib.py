@@ -15,7 +15,7 @@ EMB_ABI_VERSION = 1
 EMB_POOL_SUM, EMB_POOL_MEAN = 0, 1
 EMB_ADAGRAD_ROWWISE, EMB_ADAGRAD_ELEMENTWISE = 0, 1
 EMB_SHARD_NONE, EMB_SHARD_TABLE, EMB_SHARD_ROW = 0, 1, 2
-EMB_F_Q8, EMB_F_REQUANT, EMB_F_LOOPBACK, EMB_F_EXCHANGE, EMB_F_Q8_MINMAX = 1, 2, 4, 8, 16
+EMB_F_Q8, EMB_F_REQUANT, EMB_F_LOOPBACK, EMB_F_EXCHANGE, EMB_F_Q8_MINMAX, EMB_F_Q8_ONLY = 1, 2, 4, 8, 16, 32
 PHASES = ["fwd", "sort", "rle", "segreduce", "norm", "update", "fwd_q8", "quantize", "copy", "exchange"]
 
 STATUS = {0: "EMB_OK", 1: "EMB_EINVAL", 2: "EMB_ENOMEM", 3: "EMB_ECUDA", 4: "EMB_ENCCL",
@@ -100,6 +100,7 @@ SIGNATURES = {
     "emb_destroy": (C.c_int, [P]),
     "emb_backward_adagrad_dev": (C.c_int, [P, P, C.c_float, P, P, P]),
     "emb_set_incremental": (C.c_int, [P, P, P, P, P, C.c_float, C.c_float]),
+    "emb_quantize_block": (C.c_int, [P, C.c_int32, C.c_int64, C.c_int64, P, C.c_int64]),
     "emb_cold_weight_init": (C.c_int, [P, P, P, C.c_float]),
     "emb_hash_ids": (C.c_int, [P, P, C.c_int64, P, P]),
     "emb_qr_expand": (C.c_int, [P, P, C.c_int64, C.c_int64, C.c_int32, C.c_int64, C.c_int32, P, P, P]),

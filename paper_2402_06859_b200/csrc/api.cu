@@ -69,6 +69,8 @@ emb_status make_plan(const emb_config* c, Plan* p) {
   if (!(c->eps >= 0.f) || !(c->max_norm > 0.f) || !(c->init_accumulator >= 0.f)) return EMB_EINVAL;
   if ((c->flags & EMB_F_REQUANT) && !(c->flags & EMB_F_Q8)) return EMB_EINVAL;
   if ((c->flags & EMB_F_Q8_MINMAX) && !(c->flags & EMB_F_Q8)) return EMB_EINVAL;
+  if ((c->flags & EMB_F_Q8_ONLY) && (!(c->flags & EMB_F_Q8) || (c->flags & EMB_F_REQUANT)))
+    return EMB_EINVAL;
   if (c->world_size < 1 || c->world_size > kMaxWorld || c->rank < 0 || c->rank >= c->world_size)
     return EMB_EINVAL;
   if (c->sharding != EMB_SHARD_NONE && c->sharding != EMB_SHARD_TABLE && c->sharding != EMB_SHARD_ROW)
@@ -185,7 +187,9 @@ namespace {
 
 void carve(const Plan& p, Carver& cv, emb_handle* h) {
   const int64_t F = p.F, Bmax = p.max_batch, pitch = p.pitch;
-  const int64_t nnz_cap = p.recv_nnz_cap;  // occurrences pooled here per step
+  // a serving (q8-only) handle plans no training workspace (dedup, G, partials, staging)
+  const bool train = !(p.flags & EMB_F_Q8_ONLY);
+  const int64_t nnz_cap = train ? p.recv_nnz_cap : 1;  // occurrences pooled here per step
   const int64_t bags_cap = p.owner_bags_cap;
   const int64_t dense_cap = std::max<int64_t>(Bmax * F * p.D, 1);
   const int64_t tiles = (std::max<int64_t>(nnz_cap, bags_cap + Bmax * p.dest_base[p.world]) + kSortTileMin - 1) /
@@ -195,7 +199,7 @@ void carve(const Plan& p, Carver& cv, emb_handle* h) {
   auto* meta = cv.take<FeatMeta>(F);
   auto* stage_ids = cv.take<int>(p.max_nnz);
   auto* stage_off = cv.take<int>(F * Bmax + 1);
-  auto* stage_dense = cv.take<float>(dense_cap);
+  auto* stage_dense = cv.take<float>(dense_cap);  // also the device out of a host `out`
   auto* off_copy = cv.take<int>(F * Bmax + 1);
   auto* kvA = cv.take<uint2>(nnz_cap);
   auto* kvB = cv.take<uint2>(nnz_cap);
@@ -512,8 +516,9 @@ emb_status emb_plan(const emb_config* cfg, emb_sizes* out) {
   if (s != EMB_OK) return s;
   Carver cv(nullptr);
   carve(p, cv, nullptr);
-  out->weights_bytes = std::max<int64_t>(p.local_rows * p.pitch * 4, 4);
-  out->accum_bytes = std::max<int64_t>(
+  const bool serving = (p.flags & EMB_F_Q8_ONLY) != 0;
+  out->weights_bytes = serving ? 0 : std::max<int64_t>(p.local_rows * p.pitch * 4, 4);
+  out->accum_bytes = serving ? 0 : std::max<int64_t>(
       p.mode == EMB_ADAGRAD_ROWWISE ? p.local_rows * 4 : p.local_rows * p.pitch * 4, 4);
   out->q8_codes_bytes = (p.flags & EMB_F_Q8) ? std::max<int64_t>(p.local_rows * p.qpitch, 16) : 0;
   out->q8_meta_bytes = 0;  // {middle, scale} live inside the q8 rows
@@ -562,15 +567,16 @@ emb_status emb_create(const emb_config* cfg, const emb_buffers* buf, emb_t* out)
   emb_status s = make_plan(cfg, &h->p);
   if (s != EMB_OK) { delete h; return s; }
   const Plan& p = h->p;
-  if (!buf->weights || !buf->accum || !buf->workspace) { delete h; return EMB_EINVAL; }
+  const bool serving = (p.flags & EMB_F_Q8_ONLY) != 0;
+  if ((!serving && (!buf->weights || !buf->accum)) || !buf->workspace) { delete h; return EMB_EINVAL; }
   if ((p.flags & EMB_F_Q8) && !buf->q8_codes) { delete h; return EMB_EINVAL; }
   const void* ptrs[5] = {buf->weights, buf->accum, buf->workspace, buf->q8_codes, buf->q8_meta};
   for (const void* q : ptrs)
     if (q && !aligned(q, kAlign)) { delete h; return EMB_EINVAL; }
   if (p.exch && !cfg->nccl_unique_id) { delete h; return EMB_EINVAL; }
   h->stream = (cudaStream_t)cfg->stream;
-  h->W = (float*)buf->weights;
-  h->A = (float*)buf->accum;
+  h->W = serving ? nullptr : (float*)buf->weights;
+  h->A = serving ? nullptr : (float*)buf->accum;
   h->codes = (uint8_t*)buf->q8_codes;
   h->q8_meta_off = (int)round_up(p.D, 8);
   Carver cv(buf->workspace);
@@ -580,8 +586,8 @@ emb_status emb_create(const emb_config* cfg, const emb_buffers* buf, emb_t* out)
   cudaError_t e = cudaMemcpyAsync(h->d_meta, m.data(), sizeof(FeatMeta) * m.size(),
                                   cudaMemcpyHostToDevice, h->stream);
   if (e == cudaSuccess) {
-    const int64_t na = p.mode == EMB_ADAGRAD_ROWWISE ? p.local_rows : p.local_rows * p.pitch;
-    e = launch_fill(h->A, na, p.A0, h->stream);
+    const int64_t na = serving ? 0 : (p.mode == EMB_ADAGRAD_ROWWISE ? p.local_rows : p.local_rows * p.pitch);
+    if (na > 0) e = launch_fill(h->A, na, p.A0, h->stream);
     h->launches += na > 0;
   }
   if (e == cudaSuccess) e = cudaMemsetAsync(h->d_status, 0, sizeof(uint32_t), h->stream);
@@ -670,6 +676,7 @@ emb_status emb_forward(emb_t h, const int32_t* ids, const int32_t* offsets, int3
   emb_status s = check_batch_args(h, ids, offsets, batch, nnz, out);
   if (s != EMB_OK) return s;
   const Plan& p = h->p;
+  if (!h->W) return EMB_ESTATE;  // serving (q8-only) handle
   if ((s = join_dedup(h)) != EMB_OK) return s;  // the previous dedup may still read kvA/kvB
   Staged st;
   {
@@ -827,7 +834,7 @@ emb_status emb_backward_adagrad_dev(emb_t h, const float* grad_out, float lr,
 emb_status emb_quantize_mm8(emb_t h) {
   if (!h) return EMB_EINVAL;
   const Plan& p = h->p;
-  if (!(p.flags & EMB_F_Q8)) return EMB_ESTATE;
+  if (!(p.flags & EMB_F_Q8) || !h->W) return EMB_ESTATE;
   {
     Phase ph(h->prof, h->stream, EMB_PH_QUANTIZE);
     CK(launch_quantize(h->W, p.pitch, p.local_rows, p.D, h->codes, p.qpitch, h->q8_meta_off,
@@ -835,6 +842,27 @@ emb_status emb_quantize_mm8(emb_t h) {
                        h->d_status, h->stream));
   }
   h->launches += p.local_rows > 0;
+  h->have_q8 = true;
+  return EMB_OK;
+}
+
+emb_status emb_quantize_block(emb_t h, int32_t table, int64_t row0, int64_t n, const float* rows,
+                              int64_t ld) {
+  if (!h) return EMB_EINVAL;
+  const Plan& p = h->p;
+  if (!(p.flags & EMB_F_Q8)) return EMB_ESTATE;
+  if (table < 0 || table >= p.T || n < 0 || row0 < 0 || ld < p.D || (ld & 3)) return EMB_EINVAL;
+  if (n == 0) return EMB_OK;
+  if (!rows || !is_device_ptr(rows) || !aligned(rows, 16)) return EMB_EINVAL;
+  if (p.local_base[table] < 0 || row0 < p.row_lo[table] || row0 + n > p.row_hi[table])
+    return EMB_EINVAL;  // not stored (entirely) on this rank
+  const int64_t local = p.local_base[table] + (row0 - p.row_lo[table]);
+  {
+    Phase ph(h->prof, h->stream, EMB_PH_QUANTIZE);
+    CK(launch_quantize(rows, (int)ld, n, p.D, h->codes + local * p.qpitch, p.qpitch, h->q8_meta_off,
+                       (p.flags & EMB_F_Q8_MINMAX) != 0, h->d_status, h->stream));
+  }
+  h->launches += 1;
   h->have_q8 = true;
   return EMB_OK;
 }
@@ -847,6 +875,7 @@ emb_status emb_quantize_mm8(emb_t h) {
 emb_status emb_read_rows(emb_t h, int32_t table, const int64_t* rows, int64_t n, float* w,
                          float* acc) {
   if (!h || (n > 0 && !w)) return EMB_EINVAL;
+  if (!h->W) return EMB_ESTATE;
   std::vector<int64_t> r;
   emb_status s = stored_rows(h, table, rows, n, &r);
   if (s != EMB_OK) return s;
@@ -861,6 +890,7 @@ emb_status emb_read_rows(emb_t h, int32_t table, const int64_t* rows, int64_t n,
 emb_status emb_write_rows(emb_t h, int32_t table, const int64_t* rows, int64_t n, const float* w,
                           const float* acc) {
   if (!h) return EMB_EINVAL;
+  if (!h->W) return EMB_ESTATE;
   std::vector<int64_t> r;
   emb_status s = stored_rows(h, table, rows, n, &r);
   if (s != EMB_OK) return s;
@@ -933,6 +963,7 @@ emb_status emb_last_dedup(emb_t h, int32_t* unique, int32_t* seg_offsets, int64_
 emb_status emb_set_incremental(emb_t h, const float* w0, const float* H0, const float* w1,
                                const float* H1, float lambda_f, float alpha) {
   if (!h) return EMB_EINVAL;
+  if (!h->W) return EMB_ESTATE;
   if (!(lambda_f >= 0.f) || !(alpha >= 0.f && alpha <= 1.f)) return EMB_EINVAL;
   if ((w0 == nullptr) != (H0 == nullptr) || (w1 == nullptr) != (H1 == nullptr)) return EMB_EINVAL;
   for (const float* p : {w0, H0, w1, H1})
@@ -944,6 +975,7 @@ emb_status emb_set_incremental(emb_t h, const float* w0, const float* H0, const 
 
 emb_status emb_cold_weight_init(emb_t h, const float* w0, const float* w1, float alpha) {
   if (!h || !w0 || !w1) return EMB_EINVAL;
+  if (!h->W) return EMB_ESTATE;
   if (!(alpha >= 0.f && alpha <= 1.f)) return EMB_EINVAL;
   if (!is_device_ptr(w0) || !is_device_ptr(w1) || !aligned(w0, 16) || !aligned(w1, 16))
     return EMB_EINVAL;

@@ -68,7 +68,7 @@ class ShardedEmbedding:
                  rank: int = 0, world_size: int = 1, sharding: str = "none",
                  table_owner: Optional[Sequence[int]] = None, nccl_unique_id: Optional[bytes] = None,
                  loopback_hub: Optional["LoopbackHub"] = None, force_exchange: bool = False,
-                 max_recv_nnz: int = 0, q8_mode: str = "middle_max"):
+                 max_recv_nnz: int = 0, q8_mode: str = "middle_max", q8_only: bool = False):
         self.lib = L.load()
         assert q8_mode in ("middle_max", "min_max")
         self.q8_mode = q8_mode
@@ -101,7 +101,8 @@ class ShardedEmbedding:
             table_owner=owner_p, rank=rank, world_size=world_size,
             nccl_unique_id=uid_ptr,
             stream=C.c_void_p(self.stream.cuda_stream),
-            flags=(L.EMB_F_Q8 if (q8 or requant) else 0) | (L.EMB_F_REQUANT if requant else 0)
+            flags=(L.EMB_F_Q8 if (q8 or requant or q8_only) else 0) | (L.EMB_F_REQUANT if requant else 0)
+            | (L.EMB_F_Q8_ONLY if q8_only else 0)
             | (L.EMB_F_LOOPBACK if loopback_hub is not None else 0)
             | (L.EMB_F_EXCHANGE if force_exchange else 0)
             | (L.EMB_F_Q8_MINMAX if q8_mode == "min_max" else 0),
@@ -122,8 +123,9 @@ class ShardedEmbedding:
             n = max(int(nbytes), 16)
             return torch.empty(n, dtype=torch.uint8, device=dev)
 
-        self.weights_buf = alloc(s.weights_bytes)
-        self.accum_buf = alloc(s.accum_bytes)
+        self.q8_only = bool(q8_only)  # serving handle: no fp32 tables (EMB_F_Q8_ONLY)
+        self.weights_buf = alloc(s.weights_bytes) if s.weights_bytes else None
+        self.accum_buf = alloc(s.accum_bytes) if s.accum_bytes else None
         self.workspace = alloc(s.workspace_bytes)
         self.codes_buf = alloc(s.q8_codes_bytes) if s.q8_codes_bytes else None
         self.meta_buf = alloc(s.q8_meta_bytes) if s.q8_meta_bytes else None
@@ -141,6 +143,13 @@ class ShardedEmbedding:
         """fp32 [local_rows, row_pitch] view of the stored tables (device)."""
         n = self.local_rows * self.pitch
         return self.weights_buf[: 4 * n].view(torch.float32).view(self.local_rows, self.pitch)
+
+    def quantize_block(self, table: int, row0: int, rows: torch.Tensor) -> None:
+        """Quantize fp32 rows [row0, row0 + n) of `table` (device tensor [n, ld], ld % 4 == 0,
+        ld >= dim) into the q8 store -- how a serving (q8_only) handle is filled."""
+        assert rows.is_cuda and rows.dtype == torch.float32 and rows.dim() == 2 and rows.stride(1) == 1
+        L.check(self.lib.emb_quantize_block(self.h, int(table), int(row0), int(rows.shape[0]), _ptr(rows),
+                                            int(rows.stride(0))), "emb_quantize_block")
 
     def table_view(self, t: int) -> torch.Tensor:
         b = int(self.local_base[t])

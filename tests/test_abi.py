@@ -142,3 +142,28 @@ def test_qr_rows_host_only():
     assert lib.emb_qr_rows(1000, 4294968, 1) == 2 * (4294968 + 1000)
     assert lib.emb_qr_rows(7, 11, 0) == 18
     assert lib.emb_qr_rows(0, 11, 0) < 0 and lib.emb_qr_rows(7, 0, 1) < 0
+
+
+def test_plan_serving_handle_has_no_fp32_tables():
+    """EMB_F_Q8_ONLY (serving): no fp32 weights / accumulators and no training workspace."""
+    from paper_2402_06859_b200 import _lib as L
+    lib = L.load()
+    rows = np.array([1_000_000, 5000], dtype=np.int64)
+    ft = np.array([0, 1, 0], dtype=np.int32)
+
+    def plan(flags):
+        cfg = L.EmbConfig(abi_version=1, num_tables=2, table_rows=rows.ctypes.data_as(C.POINTER(C.c_int64)), dim=64,
+                          num_features=3, feature_table=ft.ctypes.data_as(C.POINTER(C.c_int32)), pooling=0,
+                          adagrad_mode=0, init_accumulator=0.1, eps=1e-7, max_norm=1.0, max_nnz=200_000,
+                          max_batch=4096, sharding=0, table_owner=None, rank=0, world_size=1,
+                          nccl_unique_id=None, stream=None, flags=flags, max_recv_nnz=0)
+        s = L.EmbSizes()
+        return lib.emb_plan(C.byref(cfg), C.byref(s)), s
+    st, train = plan(L.EMB_F_Q8)
+    st2, serve = plan(L.EMB_F_Q8 | L.EMB_F_Q8_ONLY)
+    assert st == 0 and st2 == 0
+    assert serve.weights_bytes == 0 and serve.accum_bytes == 0
+    assert serve.q8_codes_bytes == train.q8_codes_bytes == 1_005_000 * 96
+    assert serve.workspace_bytes < train.workspace_bytes / 4
+    assert plan(L.EMB_F_Q8_ONLY)[0] == L.EMB_EINVAL  # needs EMB_F_Q8
+    assert plan(L.EMB_F_Q8 | L.EMB_F_Q8_ONLY | L.EMB_F_REQUANT)[0] == L.EMB_EINVAL
