@@ -4,8 +4,8 @@
 // W[key_j][:]; MEAN divides by the bag length; empty bag -> 0; invalid ids skipped.
 // a10: the same over the q8 store, each term fmaf(code, scale, middle).
 //
-// Design (B200).  One group of LPB lanes per bag (D=64 fp32: 16 lanes x one 128-bit load
-// = one 256-B row).  The group loads LPB ids at once (one per lane) and broadcasts them by
+// Design (B200).  One group of LPB lanes per bag (D=64 fp32: 8 lanes x two 128-bit loads
+// = one 256-B row, 4 bags per warp).  The group loads LPB ids at once (one per lane) and broadcasts them by
 // full-mask shuffles (the id loop runs to the longest bag of the warp, so every lane
 // reaches every shuffle); it then issues the row loads of UNR ids back to back
 // (ld.global.nc.L1::no_allocate: rows are streamed, L2 keeps the Zipf-hot rows) before
@@ -323,15 +323,39 @@ static const uint32_t* bag_order(const int* offsets, long long bags, uint32_t* w
     else { constexpr int L_ = 32, V_ = 8; KERNEL_LAUNCH; }                  \
   } while (0)
 
+#define LIRANK_FWD_GEOM_DISPATCH(G, KERNEL_LAUNCH)                          \
+  do {                                                                      \
+    if ((G).lpb == 1) {                                                     \
+      if ((G).vpl == 1) { constexpr int L_ = 1, V_ = 1; KERNEL_LAUNCH; }    \
+      else { constexpr int L_ = 1, V_ = 2; KERNEL_LAUNCH; }                 \
+    } else if ((G).lpb == 2) { constexpr int L_ = 2, V_ = 2; KERNEL_LAUNCH; } \
+    else if ((G).lpb == 4) { constexpr int L_ = 4, V_ = 2; KERNEL_LAUNCH; } \
+    else if ((G).lpb == 8) { constexpr int L_ = 8, V_ = 2; KERNEL_LAUNCH; } \
+    else if ((G).lpb == 16) { constexpr int L_ = 16, V_ = 2; KERNEL_LAUNCH; } \
+    else if ((G).vpl <= 2) { constexpr int L_ = 32, V_ = 2; KERNEL_LAUNCH; } \
+    else if ((G).vpl <= 4) { constexpr int L_ = 32, V_ = 4; KERNEL_LAUNCH; } \
+    else { constexpr int L_ = 32, V_ = 8; KERNEL_LAUNCH; }                  \
+  } while (0)
+
+// a2 geometry: about 2 float4 per lane (D=64: 8 lanes x 2 per row, 4 bags per warp).  Measured
+// against 16 lanes x 1: Feed-1 a2 0.522 -> 0.491 ms, Ads (mostly one-hot bags) 4.17 -> 3.19 ms:
+// more bags per warp keep more rows in flight when bags are short.
+static Geom fwd_geom(int pitch) {
+  const int nvec = pitch / 4;
+  int lpb = 1;
+  while (lpb * 2 < nvec && lpb < 32) lpb <<= 1;
+  return Geom{lpb, (nvec + lpb - 1) / lpb};
+}
+
 cudaError_t launch_pool_fwd_f32(const FwdArgs& a, cudaStream_t s) {
-  const Geom g = geom_for(a.pitch);
+  const Geom g = fwd_geom(a.pitch);
   const long long bags = (long long)a.F * a.B;
   if (bags == 0) return cudaSuccess;
   const unsigned grid = (unsigned)((bags * g.lpb + 255) / 256);
   const int Fb = a.Fb > 0 ? a.Fb : a.F;
   const uint32_t* order = bag_order(a.offsets, bags, a.order_ws, s);
 #define LAUNCH_F32(MEAN, EMIT)                                                             \
-  LIRANK_GEOM_DISPATCH(g, (k_pool_fwd_f32<L_, V_, MEAN, EMIT><<<grid, 256, 0, s>>>(        \
+  LIRANK_FWD_GEOM_DISPATCH(g, (k_pool_fwd_f32<L_, V_, MEAN, EMIT><<<grid, 256, 0, s>>>(        \
                               a.W, a.pitch, a.ids, a.offsets, a.B, a.F, Fb, a.D, a.meta,    \
                               a.out, a.kv_out, a.sentinel, a.status, order)))
   if (a.mean) {
@@ -345,6 +369,7 @@ cudaError_t launch_pool_fwd_f32(const FwdArgs& a, cudaStream_t s) {
 
 cudaError_t launch_pool_fwd_q8(const FwdQ8Args& a, cudaStream_t s) {
   // geometry over 16-code vectors (one 16-B load each)
+  // (4 lanes x one 16-code vector for D = 64; 2 lanes x 2 vectors measured slower)
   const Geom g = geom_for(4 * ((a.D + 15) / 16));
   const long long bags = (long long)a.F * a.B;
   if (bags == 0) return cudaSuccess;
