@@ -123,7 +123,9 @@ k_segreduce(const uint32_t* __restrict__ seg, const uint32_t* __restrict__ Up,
             double* __restrict__ part_last, double* __restrict__ norm_main,
             double* __restrict__ norm_fix, uint32_t* __restrict__ owner_list,
             uint32_t* owner_count) {
-  constexpr int UNR = (VPL == 1) ? 8 : (VPL == 2 ? 4 : 2);
+  // rows in flight per group: D=64 (VPL 2) measured best at 2 (64 registers, 4 CTAs/SM:
+  // 0.78 -> 0.72 ms on Feed-1; 1 -> 0.74, 4 -> 0.78 at 80 registers, 8 -> 1.5)
+  constexpr int UNR = (VPL == 1) ? 8 : (VPL == 2 ? 2 : 2);
   const int lane = threadIdx.x & (LPB - 1);
   const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LPB;
   const uint32_t U = *Up;
