@@ -854,6 +854,12 @@ def run_ours(args, cfg, rank, world, local_rank):
             "frac": per_phase[dom]["gbs"] / hbm_peak, "traffic": traffic,
             "alg_bytes_per_launch": per_phase[dom]["alg_bytes"], "peak_source": peak_src,
             "timing": "CUDA events on the library stream around the kernel phase, mean over timed steps"}
+    if traffic:
+        # physical DRAM throughput of the same phase (ncu bytes / live time): below the
+        # algorithmic figure when L2 serves repeated rows (Zipf-hot rows, a bag's gradient
+        # row gathered once per id in the bag)
+        roof["dram_achieved"] = traffic / (per_phase[dom]["ms"] / 1e3) / 1e9
+        roof["dram_frac"] = roof["dram_achieved"] / hbm_peak
 
     value = world * B / (ms / 1e3)
     fwd_ms = per_phase["fwd"]["ms"]
