@@ -302,7 +302,13 @@ class ShardedEmbedding:
 
     def close(self):
         if getattr(self, "h", None) and self.h.value:
-            self.lib.emb_destroy(self.h)
+            # the library's kernels may still use the buffers this object owns (torch tensors
+            # whose memory the caching allocator would hand out again): drain the stream first
+            try:
+                self.stream.synchronize()
+            except Exception:
+                pass
+            self.lib.emb_destroy(self.h)  # also drains the library's side stream
             self.h = C.c_void_p()
 
     def __del__(self):
