@@ -380,9 +380,14 @@ def test_requant_tracks_updates(gpu):
 # full-size configs (the bench's launch configuration)
 # ---------------------------------------------------------------------------
 
-@pytest.mark.parametrize("name", ["jobs", "feed1"])
+@pytest.mark.parametrize("name", ["jobs", "feed1", "feed1@alpha0"])
 def test_full_config_train_step(gpu, name):
-    cfg = configs.get(name)
+    """The bench's launch configuration at full size (Feed-1 also with uniform ids, the
+    alpha = 0 variant of SURVEY §8(d)'s gate: ~5x more unique rows, shorter segments)."""
+    base, _, variant = name.partition("@")
+    cfg = configs.get(base)
+    if variant == "alpha0":
+        cfg = cfg.with_(alpha=0.0)
     B = cfg.batch
     ids, off = gen.make_batch(cfg.table_rows, cfg.features, B, cfg.seed, 0, alpha=cfg.alpha)
     nnz = len(ids)
