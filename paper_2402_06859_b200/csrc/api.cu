@@ -709,7 +709,7 @@ emb_status emb_forward(emb_t h, const int32_t* ids, const int32_t* offsets, int3
       Phase ph(h->prof, h->stream, EMB_PH_FWD);
       CK(launch_pool_fwd_f32(a, h->stream));
     }
-    h->launches += fwd_launches((int64_t)p.F * batch, true);
+    h->launches += fwd_launches((int64_t)p.F * batch, true, true);
     if (a.mean) {
       Phase ph(h->prof, h->stream, EMB_PH_COPY);
       CK(cudaMemcpyAsync(h->off_copy, st.offsets, sizeof(int) * ((int64_t)p.F * batch + 1),
@@ -764,7 +764,7 @@ emb_status emb_forward_q8(emb_t h, const int32_t* ids, const int32_t* offsets, i
       Phase ph(h->prof, h->stream, EMB_PH_FWD_Q8);
       CK(launch_pool_fwd_q8(a, h->stream));
     }
-    h->launches += fwd_launches((int64_t)p.F * batch, true);
+    h->launches += fwd_launches((int64_t)p.F * batch, true, false);
   }
   if (st.host_out) {
     Phase ph(h->prof, h->stream, EMB_PH_COPY);

@@ -336,7 +336,7 @@ emb_status exchange_forward(emb_t h, const Staged& st, int32_t batch, int64_t nn
     Phase ph(h->prof, h->stream, EMB_PH_FWD_Q8);
     CK(launch_pool_fwd_q8(a, h->stream));
   }
-  h->launches += fwd_launches((int64_t)W * Fr * B, true);
+  h->launches += fwd_launches((int64_t)W * Fr * B, true, !q8);
   // ---- a3: pooled exchange back ----------------------------------------------------------
   {
     Phase ph(h->prof, h->stream, EMB_PH_EXCHANGE);

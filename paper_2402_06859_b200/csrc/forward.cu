@@ -67,19 +67,21 @@ k_pool_fwd_f32(const float* __restrict__ W, int pitch, const int* __restrict__ i
                const int* __restrict__ offsets, int B, int F, int Fb, int D,
                const FeatMeta* __restrict__ meta, float* __restrict__ out,
                uint2* __restrict__ kv_out, uint32_t sentinel, uint32_t* status,
-              const uint32_t* __restrict__ order) {
+              const uint32_t* __restrict__ order, bool skip_short) {
   constexpr int UNR = (VPL == 1) ? 4 : (VPL == 2 ? 2 : 1);
   constexpr unsigned kFull = 0xffffffffu;
   const int lane = threadIdx.x & (LPB - 1);
   const long long gid = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / LPB;
-  const bool live = gid < (long long)F * B;  // predicate, never return: shuffles below
-  const long long bag = (order != nullptr && live) ? (long long)__ldg(order + gid) : gid;
+  const bool in_range = gid < (long long)F * B;  // predicate, never return: shuffles below
+  const long long bag = (order != nullptr && in_range) ? (long long)__ldg(order + gid) : gid;
+  const int lo = in_range ? __ldg(offsets + bag) : 0;
+  const int hi = in_range ? __ldg(offsets + bag + 1) : 0;
+  // bags of <= 1 id are k_pool_short_f32's when skip_short (it batches LPB of them per group)
+  const bool live = in_range && !(skip_short && hi - lo <= 1);
+  const int len = live ? hi - lo : 0;
   const int f = live ? (int)(bag / B) : 0;
   const int b = live ? (int)(bag - (long long)f * B) : 0;
   const FeatMeta m = meta[f];
-  const int lo = live ? __ldg(offsets + bag) : 0;
-  const int hi = live ? __ldg(offsets + bag + 1) : 0;
-  const int len = hi - lo;
   const int nvec = pitch >> 2;
   const uint32_t grow = (uint32_t)out_row(f, b, B, Fb);
   float4 acc[VPL];
@@ -132,6 +134,75 @@ k_pool_fwd_f32(const float* __restrict__ W, int pitch, const int* __restrict__ i
   for (int v = 0; v < VPL; ++v) store4(o, 4 * (lane + v * LPB), D, acc[v]);
 }
 
+// Bags of at most one id (one-hot features, empty bags).  The main kernel gives each bag a
+// lane group and keeps UNR of its ids' rows in flight; a one-id bag leaves one row in flight
+// per group.  Here a group serves LPB consecutive (ordered) positions -- lane l resolves the
+// bag at position LPB*g + l and loads its id -- and gathers their rows UNR at a time, so
+// one-hot-heavy batches keep as many rows in flight as multi-hot ones.  Positions whose bag
+// has more ids are left to the main kernel.  A one-id bag's pooled value is its row (SUM and
+// MEAN alike); an empty bag's is 0.
+template <int LPB, int VPL, bool EMIT>
+__global__ void __launch_bounds__(256)
+k_pool_short_f32(const float* __restrict__ W, int pitch, const int* __restrict__ ids,
+                 const int* __restrict__ offsets, int B, int F, int Fb, int D,
+                 const FeatMeta* __restrict__ meta, float* __restrict__ out,
+                 uint2* __restrict__ kv_out, uint32_t sentinel, uint32_t* status,
+                 const uint32_t* __restrict__ order) {
+  constexpr int UNR = VPL >= 4 ? 2 : 4;
+  constexpr unsigned kFull = 0xffffffffu;
+  const int lane = threadIdx.x & (LPB - 1);
+  const long long g = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / LPB;
+  const long long nb = (long long)F * B;
+  const long long pos = g * LPB + lane;
+  bool mine = pos < nb;
+  const long long bag = mine ? (order != nullptr ? (long long)__ldg(order + pos) : pos) : 0;
+  const int lo = mine ? __ldg(offsets + bag) : 0;
+  const int len = mine ? __ldg(offsets + bag + 1) - lo : 2;
+  mine = mine && len <= 1;
+  uint32_t key = sentinel, grow = 0;
+  bool bad = false;
+  if (mine) {
+    const int f = (int)(bag / B), b = (int)(bag - (long long)f * B);
+    grow = (uint32_t)out_row(f, b, B, Fb);
+    if (len == 1) {
+      key = row_key(__ldg(ids + lo), meta[f], sentinel, bad);
+      if (EMIT) kv_out[lo] = make_uint2(key, grow);
+    }
+  }
+  const int nvec = pitch >> 2;
+#pragma unroll
+  for (int j = 0; j < LPB; j += UNR) {
+    uint32_t k[UNR], gr[UNR];
+    bool mm[UNR];
+    float4 r[UNR][VPL];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int src = (j + u) & (LPB - 1);
+      k[u] = __shfl_sync(kFull, key, src, LPB);
+      gr[u] = __shfl_sync(kFull, grow, src, LPB);
+      mm[u] = __shfl_sync(kFull, (int)mine, src, LPB) != 0 && j + u < LPB;
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) {
+        const int vi = lane + v * LPB;
+        r[u][v] = (mm[u] && k[u] != sentinel && vi < nvec) ? ld_nc_f4(W + (size_t)k[u] * pitch + 4 * vi)
+                                                          : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u)
+      if (mm[u]) {
+        float* o = out + (size_t)gr[u] * D;
+        const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);  // 0 + row, as the main kernel (-0 -> +0)
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) store4(o, 4 * (lane + v * LPB), D, f4_add_rn(z, r[u][v]));
+      }
+  }
+  if (bad) set_status(status, kStIdRange);
+}
+
 // X^dequant = X^middle + X^int * X^scale: one fmaf per element (reading 7).
 // The int8 code becomes an exact float without a conversion instruction: with
 // u = byte ^ 0x80 = code + 128, the float with bits 0x4B0000uu is 2^23 + u, so
@@ -170,20 +241,21 @@ k_pool_fwd_q8(const uint8_t* __restrict__ codes, int qpitch, int meta_off,
               const int* __restrict__ ids, const int* __restrict__ offsets, int B, int F, int Fb,
               int D, const FeatMeta* __restrict__ meta, float* __restrict__ out,
               uint32_t* status,
-              const uint32_t* __restrict__ order, uint32_t xmask, float magic) {
+              const uint32_t* __restrict__ order, uint32_t xmask, float magic, bool skip_short) {
   constexpr int UNR = (VPL == 1) ? 4 : 2;
   constexpr uint32_t kNone = 0xffffffffu;
   constexpr unsigned kFull = 0xffffffffu;
   const int lane = threadIdx.x & (LPB - 1);
   const long long gid = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / LPB;
-  const bool live = gid < (long long)F * B;  // predicate, never return: shuffles below
-  const long long bag = (order != nullptr && live) ? (long long)__ldg(order + gid) : gid;
+  const bool in_range = gid < (long long)F * B;  // predicate, never return: shuffles below
+  const long long bag = (order != nullptr && in_range) ? (long long)__ldg(order + gid) : gid;
+  const int lo = in_range ? __ldg(offsets + bag) : 0;
+  const int hi = in_range ? __ldg(offsets + bag + 1) : 0;
+  const bool live = in_range && !(skip_short && hi - lo <= 1);  // (skip_short: unused for a10)
+  const int len = live ? hi - lo : 0;
   const int f = live ? (int)(bag / B) : 0;
   const int b = live ? (int)(bag - (long long)f * B) : 0;
   const FeatMeta m = meta[f];
-  const int lo = live ? __ldg(offsets + bag) : 0;
-  const int hi = live ? __ldg(offsets + bag + 1) : 0;
-  const int len = hi - lo;
   const int nv16 = (D + 15) >> 4;  // 16-code vectors carrying dims < D
   float4 acc[4 * VPL];
 #pragma unroll
@@ -354,16 +426,26 @@ cudaError_t launch_pool_fwd_f32(const FwdArgs& a, cudaStream_t s) {
   const unsigned grid = (unsigned)((bags * g.lpb + 255) / 256);
   const int Fb = a.Fb > 0 ? a.Fb : a.F;
   const uint32_t* order = bag_order(a.offsets, bags, a.order_ws, s);
+  const bool split = order != nullptr;  // short bags sit at the end of the ordered positions
 #define LAUNCH_F32(MEAN, EMIT)                                                             \
   LIRANK_FWD_GEOM_DISPATCH(g, (k_pool_fwd_f32<L_, V_, MEAN, EMIT><<<grid, 256, 0, s>>>(        \
                               a.W, a.pitch, a.ids, a.offsets, a.B, a.F, Fb, a.D, a.meta,    \
-                              a.out, a.kv_out, a.sentinel, a.status, order)))
+                              a.out, a.kv_out, a.sentinel, a.status, order, split)))
   if (a.mean) {
     if (a.kv_out) LAUNCH_F32(true, true); else LAUNCH_F32(true, false);
   } else {
     if (a.kv_out) LAUNCH_F32(false, true); else LAUNCH_F32(false, false);
   }
 #undef LAUNCH_F32
+  if (split) {
+    const unsigned sgrid = (unsigned)(((bags + g.lpb - 1) / g.lpb * g.lpb + 255) / 256);
+#define LAUNCH_SHORT(EMIT)                                                                   \
+  LIRANK_FWD_GEOM_DISPATCH(g, (k_pool_short_f32<L_, V_, EMIT><<<sgrid, 256, 0, s>>>(          \
+                              a.W, a.pitch, a.ids, a.offsets, a.B, a.F, Fb, a.D, a.meta,    \
+                              a.out, a.kv_out, a.sentinel, a.status, order)))
+    if (a.kv_out) LAUNCH_SHORT(true); else LAUNCH_SHORT(false);
+#undef LAUNCH_SHORT
+  }
   return cudaGetLastError();
 }
 
@@ -376,11 +458,14 @@ cudaError_t launch_pool_fwd_q8(const FwdQ8Args& a, cudaStream_t s) {
   const unsigned grid = (unsigned)((bags * g.lpb + 255) / 256);
   const int Fb = a.Fb > 0 ? a.Fb : a.F;
   const uint32_t* order = bag_order(a.offsets, bags, a.order_ws, s);
+  const uint32_t xmask = a.minmax ? 0u : 0x80808080u;
+  const float magic = a.minmax ? 8388608.0f : 8388736.0f;
+  // (no short-bag split here: a k_pool_short_f32-style q8 kernel measured slower -- Ads a10
+  // 3.24 -> 3.79 ms -- the q8 groups already hold 8 bags per warp)
 #define LAUNCH_Q8(MEAN)                                                                    \
   LIRANK_GEOM_DISPATCH(g, (k_pool_fwd_q8<L_, V_, MEAN><<<grid, 256, 0, s>>>(               \
                               a.codes, a.qpitch, a.meta_off, a.ids, a.offsets, a.B, a.F, Fb, \
-                              a.D, a.meta, a.out, a.status, order,                       \
-                              a.minmax ? 0u : 0x80808080u, a.minmax ? 8388608.0f : 8388736.0f)))
+                              a.D, a.meta, a.out, a.status, order, xmask, magic, false)))
   if (a.mean) LAUNCH_Q8(true); else LAUNCH_Q8(false);
 #undef LAUNCH_Q8
   return cudaGetLastError();

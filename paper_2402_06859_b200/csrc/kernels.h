@@ -30,9 +30,10 @@ cudaError_t launch_pool_fwd_f32(const FwdArgs& a, cudaStream_t s);
 // longest bag).  Scratch: the permutation + 2 x 256 bin counters.
 constexpr int kLenBins = 256;
 inline int64_t kOrderWsWords(int64_t bags) { return bags + 2 * kLenBins; }
-// kernels one forward launch issues (the pooling kernel, plus the 2 ordering kernels)
-inline int fwd_launches(int64_t bags, bool ordered) {
-  return bags <= 0 ? 0 : (ordered && bags >= 2 ? 3 : 1);
+// kernels one forward launch issues: the pooling kernel, plus the 2 ordering kernels and,
+// for a2 (fp32), the short-bag kernel
+inline int fwd_launches(int64_t bags, bool ordered, bool fp32) {
+  return bags <= 0 ? 0 : (ordered && bags >= 2 ? (fp32 ? 4 : 3) : 1);
 }
 
 struct FwdQ8Args {
