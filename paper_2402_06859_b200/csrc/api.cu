@@ -705,6 +705,8 @@ emb_status emb_forward(emb_t h, const int32_t* ids, const int32_t* offsets, int3
     a.status = h->d_status;
     a.mean = p.pooling == EMB_POOL_MEAN;
     a.order_ws = h->order_ws;
+    h->order_offsets = st.offsets;
+    h->order_bags = (int64_t)p.F * batch;
     {
       Phase ph(h->prof, h->stream, EMB_PH_FWD);
       CK(launch_pool_fwd_f32(a, h->stream));
@@ -760,11 +762,13 @@ emb_status emb_forward_q8(emb_t h, const int32_t* ids, const int32_t* offsets, i
     a.status = h->d_status;
     a.mean = p.pooling == EMB_POOL_MEAN;
     a.order_ws = h->order_ws;
+    a.order_ready = h->order_offsets == st.offsets && h->order_bags == (int64_t)p.F * batch &&
+                    h->order_bags >= 2;
     {
       Phase ph(h->prof, h->stream, EMB_PH_FWD_Q8);
       CK(launch_pool_fwd_q8(a, h->stream));
     }
-    h->launches += fwd_launches((int64_t)p.F * batch, true, false);
+    h->launches += a.order_ready ? 1 : fwd_launches((int64_t)p.F * batch, true, false);
   }
   if (st.host_out) {
     Phase ph(h->prof, h->stream, EMB_PH_COPY);

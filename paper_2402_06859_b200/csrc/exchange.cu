@@ -297,6 +297,7 @@ emb_status exchange_forward(emb_t h, const Staged& st, int32_t batch, int64_t nn
     if ((s = scan(h, x.recv_lens, x.recv_off, (int64_t)W * Fr * B, 1)) != EMB_OK) return s;
   }
   // ---- owner: pool every source's bags into [src][B][Fr][D] -------------------------------
+  h->order_bags = -1;  // order_ws now holds the owner's order, not a local forward's
   if (!q8) {
     FwdArgs a;
     memset(&a, 0, sizeof(a));

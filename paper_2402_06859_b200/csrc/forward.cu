@@ -457,7 +457,9 @@ cudaError_t launch_pool_fwd_q8(const FwdQ8Args& a, cudaStream_t s) {
   if (bags == 0) return cudaSuccess;
   const unsigned grid = (unsigned)((bags * g.lpb + 255) / 256);
   const int Fb = a.Fb > 0 ? a.Fb : a.F;
-  const uint32_t* order = bag_order(a.offsets, bags, a.order_ws, s);
+  // any permutation of the bags is a correct order (the kernels read the current lengths);
+  // reusing the last a2 forward's order on the same offsets only saves its two kernels
+  const uint32_t* order = a.order_ready ? a.order_ws : bag_order(a.offsets, bags, a.order_ws, s);
   const uint32_t xmask = a.minmax ? 0u : 0x80808080u;
   const float magic = a.minmax ? 8388608.0f : 8388736.0f;
   // (no short-bag split here: a k_pool_short_f32-style q8 kernel measured slower -- Ads a10

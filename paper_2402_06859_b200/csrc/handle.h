@@ -145,6 +145,8 @@ struct emb_handle {
   int q8_meta_off = 0;  // byte offset of {middle, scale} inside a q8 row
   // workspace
   uint32_t* order_ws = nullptr;  // bag order of the pooling kernels (kOrderWsWords)
+  const int* order_offsets = nullptr;  // offsets (device) + bag count the order was built for by
+  int64_t order_bags = -1;             // the last unsharded a2 forward (a10 reuses it)
   lirank::FeatMeta* d_meta = nullptr;
   int* stage_ids = nullptr;
   int* stage_off = nullptr;

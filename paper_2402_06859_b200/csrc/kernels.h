@@ -49,6 +49,7 @@ struct FwdQ8Args {
   uint32_t* status;
   bool mean;
   uint32_t* order_ws;  // as FwdArgs::order_ws
+  bool order_ready;    // order_ws already holds an order of these F*B bags: reuse it
   bool minmax;         // min-max store (uint8 codes, meta {min, scale})
 };
 cudaError_t launch_pool_fwd_q8(const FwdQ8Args& a, cudaStream_t s);
