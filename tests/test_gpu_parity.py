@@ -435,3 +435,29 @@ def test_full_config_train_step(gpu, name):
     w = emb.read_rows(0, rows, with_acc=False)
     codes, mid, sc, _ = O.quantize(w)
     assert (c == codes).all() and (mm == mid).all() and (ss == sc).all()
+
+
+def test_q8_reuses_bag_order_of_a_different_batch(gpu):
+    """emb_forward_q8 reuses the bag order the last emb_forward built when the offsets pointer
+    and bag count match.  Any permutation of the bags is a correct visiting order (the kernels
+    read the current lengths), so a q8 forward on DIFFERENT offsets written into the same
+    buffer must still match the oracle exactly."""
+    cfg = small_cfg(dim=64, rows=(4000, 900), F=[0, 1, 0])
+    B = 300
+    ids1, off1 = gen.make_batch(cfg.table_rows, cfg.features, B, 21, 0)
+    ids2, off2 = gen.make_batch(cfg.table_rows, cfg.features, B, 22, 0)
+    nmax = max(len(ids1), len(ids2))
+    emb = make_emb(cfg, max_nnz=nmax, max_batch=B, q8=True)
+    init_tables_host(emb, cfg)
+    emb.quantize()
+    off_buf = dev(off1)
+    ids_buf = torch.zeros(nmax, dtype=torch.int32, device=gpu)
+    ids_buf[:len(ids1)] = dev(ids1)
+    emb.forward(ids_buf[:len(ids1)], off_buf, B)
+    off_buf.copy_(dev(off2))           # same pointer, new content
+    ids_buf[:len(ids2)] = dev(ids2)
+    out = emb.forward_q8(ids_buf[:len(ids2)], off_buf, B).cpu().numpy()
+    assert emb.sync() == 0
+    codes, mid, sc, _ = O.quantize(dense_tables(cfg))
+    ref, _ = O.forward_q8(problem(cfg), codes, mid, sc, ids2, off2, B)
+    assert (out == ref).all()
