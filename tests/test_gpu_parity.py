@@ -359,12 +359,16 @@ def test_forward_q8(gpu, dim):
     assert (out == ref).all()
 
 
-def test_requant_tracks_updates(gpu):
-    cfg = small_cfg(dim=64, rows=(3000,), F=[0, 0])
+@pytest.mark.parametrize("mode,pooling,dim", [("rowwise", "sum", 64), ("elementwise", "sum", 64),
+                                              ("rowwise", "mean", 30), ("elementwise", "mean", 128)])
+def test_requant_tracks_updates(gpu, mode, pooling, dim):
+    """The fused a8 + a9 re-quantization of the touched rows (both AdaGrad modes, both
+    poolings, several geometries) equals the oracle's a9 of the updated table."""
+    cfg = small_cfg(dim=dim, rows=(3000,), F=[0, 0])
     B = 256
     ids, off = gen.make_batch(cfg.table_rows, cfg.features, B, 4, 0)
-    grad = gen.grad_values(4, 0, B, 2, 64, gen.grad_shift_for(len(ids), 64))
-    emb = make_emb(cfg, max_nnz=len(ids), max_batch=B, q8=True, requant=True)
+    grad = gen.grad_values(4, 0, B, 2, dim, gen.grad_shift_for(len(ids), dim))
+    emb = make_emb(cfg, max_nnz=len(ids), max_batch=B, q8=True, requant=True, adagrad=mode, pooling=pooling)
     init_tables_host(emb, cfg)
     emb.quantize()
     emb.forward(dev(ids), dev(off), B)
