@@ -222,11 +222,26 @@ def cpu_baseline(cfg, ids, off, B, samples, mode, budget_s=15.0):
 # reference arm: the oracle, as it stands, on the host cores
 # ---------------------------------------------------------------------------
 
-def run_reference(args, cfg, rank, world):
+def run_reference(args, cfg, rank, world, serve=False):
     if rank != 0:
         return
     B = cfg.batch
     ids, off = gen.make_batch(cfg.table_rows, cfg.features, B, cfg.seed, 0, alpha=cfg.alpha)
+    if serve:  # the serving arm's metric: the oracle's a10 on a bounded sample
+        r = serving_cpu_baseline(cfg, ids, off, B, args.cpu_samples, args.q8_mode,
+                                 budget_s=max(1.0, 0.5 * args.steps))
+        value = r["value"]
+        line = {
+            "impl": "reference", "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * min(args.cpu_samples, B) / value,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8 codes, f32 accumulate",
+            "data": "synthetic",
+            "config": {"workload": cfg.name, "global_batch": B, "alpha": cfg.alpha, "parallelism": "cpu-oracle"},
+            "cpu_baseline": r,
+            "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }
+        print(json.dumps(line), flush=True)
+        return
     smp = OracleSample(cfg, ids, off, B, args.cpu_samples, args.adagrad)
     t = smp.time(args.steps, args.warmup)
     value = smp.Bs / t
@@ -929,7 +944,7 @@ def main():
         # W-fold Feed tables (W=8: the 1B-row Feed config of BASELINE.json), row-wise sharded
         cfg = cfg.with_(name=f"{cfg.name}-x{world}", table_rows=[r * world for r in cfg.table_rows])
     if args.impl == "reference":
-        run_reference(args, cfg, rank, world)
+        run_reference(args, cfg, rank, world, serve=serve)
         return
     if world > 1:
         import torch
