@@ -218,6 +218,8 @@ void carve(const Plan& p, Carver& cv, emb_handle* h) {
   auto* oc = cv.take<uint32_t>(2);
   auto* sp = cv.take<double>(std::max(p.world, 1));
   auto* sl = cv.take<double>(1);
+  auto* nparts = cv.take<double>(64);     // k_norm_partial CTA partials (kNormParts)
+  auto* ndone = cv.take<uint32_t>(1);     // its arrival counter (zeroed at create)
   auto* sg = cv.take<double>(1);
   auto* cl = cv.take<float>(1);
   auto* st = cv.take<uint32_t>(1);
@@ -244,6 +246,7 @@ void carve(const Plan& p, Carver& cv, emb_handle* h) {
     h->owner_list = ol; h->owner_count = oc;
     h->chunks_cap = chunks;
     h->S_parts = sp; h->S_local = sl; h->S_global = sg; h->d_clip = cl; h->d_status = st;
+    h->norm_parts = nparts; h->norm_done = ndone;
     h->x = x;
   }
 }
@@ -371,6 +374,8 @@ emb_status backward_local(emb_t h, const float* grad_dev, float lr, double extra
   a.owner_count = h->owner_count;
   a.chunks = (n + kChunk - 1) / kChunk;
   a.S_local = h->S_local;
+  a.norm_parts = h->norm_parts;
+  a.norm_done = h->norm_done;
   a.S_global = h->S_global;
   a.clip = h->d_clip;
   a.status = h->d_status;
@@ -591,6 +596,7 @@ emb_status emb_create(const emb_config* cfg, const emb_buffers* buf, emb_t* out)
     h->launches += na > 0;
   }
   if (e == cudaSuccess) e = cudaMemsetAsync(h->d_status, 0, sizeof(uint32_t), h->stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(h->norm_done, 0, sizeof(uint32_t), h->stream);
   if (e == cudaSuccess)
     e = cudaMemsetAsync(h->sort.status, 0, sizeof(unsigned long long) * h->sort.max_tiles * kRadixBinsMax, h->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);  // `m` goes out of scope

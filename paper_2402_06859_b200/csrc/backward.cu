@@ -338,23 +338,41 @@ k_fixup_long(const uint32_t* __restrict__ seg, int pitch, const double* __restri
   }
 }
 
-// S_local = sum over chunks (index order) of norm_main + norm_fix.  One CTA, fixed tree.
-__global__ void __launch_bounds__(1024)
+// S_local = sum over chunks of norm_main + norm_fix in a fixed order: each of up to
+// kNormParts CTAs sums a contiguous range of chunks (fixed tree), the last CTA to finish
+// adds the CTA partials in index order.  Deterministic for a given chunk count.
+constexpr int kNormParts = 64;
+__global__ void __launch_bounds__(256)
 k_norm_partial(const double* __restrict__ norm_main, const double* __restrict__ norm_fix,
-               int64_t chunks, double* S_local) {
-  __shared__ double sm[1024];
+               int64_t chunks, double* __restrict__ parts, uint32_t* done, double* S_local) {
+  __shared__ double sm[256];
+  __shared__ bool last;
+  const int64_t per = (chunks + gridDim.x - 1) / gridDim.x;
+  const int64_t a = (int64_t)blockIdx.x * per, b = min(chunks, a + per);
   double s = 0.0;
-  for (int64_t i = threadIdx.x; i < chunks; i += blockDim.x) {
+  for (int64_t i = a + threadIdx.x; i < b; i += blockDim.x) {
     s += norm_main[i];
     s += norm_fix[i];
   }
   sm[threadIdx.x] = s;
   __syncthreads();
-  for (int o = 512; o > 0; o >>= 1) {
+  for (int o = 128; o > 0; o >>= 1) {
     if (threadIdx.x < o) sm[threadIdx.x] += sm[threadIdx.x + o];
     __syncthreads();
   }
-  if (threadIdx.x == 0) *S_local = sm[0];
+  if (threadIdx.x == 0) {
+    parts[blockIdx.x] = sm[0];
+    __threadfence();
+    last = atomicAdd(done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    double t = 0.0;
+    for (unsigned p = 0; p < gridDim.x; ++p) t += ld_volatile_f64(parts + p);
+    *S_local = t;
+    *done = 0u;  // re-armed for the next launch
+  }
 }
 
 // S = sum of rank partials in rank order + extra; c = (n > max_norm) ? max_norm/n : 1.
@@ -751,7 +769,10 @@ cudaError_t launch_segreduce(const BwdArgs& a, int64_t* launches, cudaStream_t s
 }
 
 cudaError_t launch_norm_partial(const BwdArgs& a, cudaStream_t s) {
-  k_norm_partial<<<1, 1024, 0, s>>>(a.norm_main, a.norm_fix, a.chunks, a.S_local);
+  const int64_t want = (a.chunks + 1023) / 1024;
+  const unsigned grid = (unsigned)(want < 1 ? 1 : (want < kNormParts ? want : kNormParts));
+  k_norm_partial<<<grid, 256, 0, s>>>(a.norm_main, a.norm_fix, a.chunks, a.norm_parts,
+                                      a.norm_done, a.S_local);
   return cudaGetLastError();
 }
 

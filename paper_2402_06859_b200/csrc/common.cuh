@@ -68,6 +68,9 @@ __device__ __forceinline__ int ld_nc_i32(const int* p) {
   return r;
 }
 
+__device__ __forceinline__ double ld_volatile_f64(const double* p) {
+  return *reinterpret_cast<const volatile double*>(p);
+}
 __device__ __forceinline__ float4 f4_add_rn(float4 a, float4 b) {
   return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z),
                      __fadd_rn(a.w, b.w));

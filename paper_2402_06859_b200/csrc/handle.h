@@ -165,6 +165,8 @@ struct emb_handle {
   int64_t chunks_cap = 0;
   double* S_parts = nullptr;  // [world]
   double* S_local = nullptr;
+  double* norm_parts = nullptr;
+  uint32_t* norm_done = nullptr;
   double* S_global = nullptr;
   float* d_clip = nullptr;
   uint32_t* d_status = nullptr;

@@ -110,7 +110,9 @@ struct BwdArgs {
   uint32_t* owner_count;    // device scalar (zeroed by launch_segreduce)
   int64_t chunks;
   // norm / clip
-  double* S_local;          // device scalar: this rank's sum of squares
+  double* S_local;
+  double* norm_parts;   // [kNormParts] CTA partials of the norm (k_norm_partial)
+  uint32_t* norm_done;  // CTA arrival counter (0 between launches)          // device scalar: this rank's sum of squares
   double* S_global;         // device scalar
   float* clip;              // device scalar
   uint32_t* status;
