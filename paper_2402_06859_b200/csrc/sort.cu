@@ -33,8 +33,9 @@ __device__ __forceinline__ unsigned peers_of(uint32_t d, unsigned valid) {
   unsigned m = valid;
 #pragma unroll
   for (int b = 0; b < BITS; ++b) {
-    const unsigned bb = __ballot_sync(0xffffffffu, (d >> b) & 1u);
-    m &= ((d >> b) & 1u) ? bb : ~bb;
+    const uint32_t bit = (d >> b) & 1u;
+    const unsigned bb = __ballot_sync(0xffffffffu, bit);
+    m &= bb ^ (bit - 1u);  // bit 1: bb; bit 0: ~bb (one LOP3)
   }
   return m;
 }
@@ -107,6 +108,38 @@ k_radix_hist(const uint2* __restrict__ kv, int64_t n, int passes, uint32_t* hist
 // One digit pass.  ITEMS pairs per thread (tile = 256 * ITEMS); MATCH selects the warp
 // ranking primitive (match.any vs a BITS-ballot multisplit).
 // ---------------------------------------------------------------------------
+// Load the warp's ITEMS x 32 pairs and rank each within the warp (stable: by item, then
+// lane) against the warp's running digit counters wh[].  FULL: every index is < n.
+template <int BITS, int ITEMS, bool MATCH, bool FULL>
+__device__ __forceinline__ void load_rank(const uint2* __restrict__ in, uint2 (&kv)[ITEMS],
+                                          uint32_t (&r)[ITEMS], int64_t base, int64_t n, int shift,
+                                          uint32_t* wh, int lane, unsigned lt) {
+  constexpr int BINS = 1 << BITS;
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int64_t idx = base + i * 32 + lane;
+    kv[i] = (FULL || idx < n) ? in[idx] : make_uint2(0u, 0u);
+  }
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int64_t idx = base + i * 32 + lane;
+    const bool ok = FULL || idx < n;
+    const uint32_t d = ok ? (kv[i].x >> shift) & (BINS - 1) : (uint32_t)BINS;
+    unsigned peers;
+    if (MATCH) {
+      peers = __match_any_sync(0xffffffffu, d);
+    } else {
+      peers = FULL ? peers_of<BITS>(d, 0xffffffffu)
+                   : peers_of<BITS + 1>(d, 0xffffffffu);  // bit BITS separates out-of-range lanes
+    }
+    const uint32_t cur = ok ? wh[d] : 0u;
+    r[i] = cur + __popc(peers & lt);
+    __syncwarp();
+    if (ok && lane == __ffs(peers) - 1) wh[d] = cur + __popc(peers);
+    __syncwarp();
+  }
+}
+
 template <int BITS, int ITEMS, bool MATCH, int MINB = 4>
 __global__ void __launch_bounds__(kSortThreads, MINB)
 k_onesweep(const uint2* __restrict__ in, uint2* __restrict__ out, int64_t n, int shift,
@@ -131,30 +164,12 @@ k_onesweep(const uint2* __restrict__ in, uint2* __restrict__ out, int64_t n, int
 
   uint2 kv[ITEMS];
   uint32_t r[ITEMS];
-#pragma unroll
-  for (int i = 0; i < ITEMS; ++i) {
-    const int64_t idx = base + i * 32 + lane;
-    kv[i] = idx < n ? in[idx] : make_uint2(0u, 0u);
-  }
   const unsigned lt = lanemask_lt();
   uint32_t* wh = warp_hist + warp * BINS;
-#pragma unroll
-  for (int i = 0; i < ITEMS; ++i) {
-    const int64_t idx = base + i * 32 + lane;
-    const bool ok = idx < n;
-    const uint32_t d = ok ? (kv[i].x >> shift) & (BINS - 1) : (uint32_t)BINS;
-    unsigned peers;
-    if (MATCH) {
-      peers = __match_any_sync(0xffffffffu, d);
-    } else {
-      peers = peers_of<BITS + 1>(d, 0xffffffffu);  // bit BITS separates the out-of-range lanes
-    }
-    const uint32_t cur = ok ? wh[d] : 0u;
-    r[i] = cur + __popc(peers & lt);
-    __syncwarp();
-    if (ok && lane == __ffs(peers) - 1) wh[d] = cur + __popc(peers);
-    __syncwarp();
-  }
+  // every tile but the last is full: its ranking needs no bounds checks and BITS ballots
+  // (the last one separates out-of-range lanes with one more bit)
+  if (tile0 + TILE <= n) load_rank<BITS, ITEMS, MATCH, true>(in, kv, r, base, n, shift, wh, lane, lt);
+  else load_rank<BITS, ITEMS, MATCH, false>(in, kv, r, base, n, shift, wh, lane, lt);
   __syncthreads();
 
   // per digit: exclusive prefix over warps (in place), tile total, and the tile's
