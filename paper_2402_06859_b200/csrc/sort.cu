@@ -104,6 +104,30 @@ k_radix_hist(const uint2* __restrict__ kv, int64_t n, int passes, uint32_t* hist
   }
 }
 
+// Digit histograms -> exclusive prefix sums in place (one CTA per pass), so the onesweep
+// tiles read each digit's global start instead of scanning the histogram themselves.
+__global__ void __launch_bounds__(512)
+k_hist_excl(uint32_t* hist, int bins) {
+  __shared__ uint32_t s_warp[16];
+  uint32_t* h = hist + (size_t)blockIdx.x * bins;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const uint32_t v = t < bins ? h[t] : 0u;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_warp[warp] = x;
+  __syncthreads();
+  if (t == 0) {
+    uint32_t c = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { const uint32_t q = s_warp[w]; s_warp[w] = c; c += q; }
+  }
+  __syncthreads();
+  if (t < bins) h[t] = s_warp[warp] + x - v;
+}
+
 // ---------------------------------------------------------------------------
 // One digit pass.  ITEMS pairs per thread (tile = 256 * ITEMS); MATCH selects the warp
 // ranking primitive (match.any vs a BITS-ballot multisplit).
@@ -197,34 +221,28 @@ k_onesweep(const uint2* __restrict__ in, uint2* __restrict__ out, int64_t n, int
       carry += blk_total;
     }
   }
-  // stage the tile in sorted order (overlaps the look-back of earlier tiles)
+  // stage the tile in sorted order (overlaps the look-back of earlier tiles); item i of
+  // this lane is valid iff i < nv
+  const int nv = tile0 + TILE <= n ? ITEMS
+                                   : (int)max((int64_t)0, min((int64_t)ITEMS, (n - base - lane + 31) / 32));
 #pragma unroll
-  for (int i = 0; i < ITEMS; ++i) {
-    const int64_t idx = base + i * 32 + lane;
-    if (idx < n) r[i] += warp_hist[warp * BINS + ((kv[i].x >> shift) & (BINS - 1))];
-  }
+  for (int i = 0; i < ITEMS; ++i)
+    if (i < nv) r[i] += warp_hist[warp * BINS + ((kv[i].x >> shift) & (BINS - 1))];
 #pragma unroll
   for (int q = 0; q < DPT; ++q) digit_off[tid + q * kSortThreads] = tile_excl[q];
   __syncthreads();
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
-    const int64_t idx = base + i * 32 + lane;
-    if (idx < n) {
+    if (i < nv) {
       const uint32_t d = (kv[i].x >> shift) & (BINS - 1);
       stage[digit_off[d] + r[i]] = kv[i];
     }
   }
   // global position of sorted-tile slot j with digit d: hist_excl[d] + prev[d] + (j - tile_excl[d])
+  // (`hist` holds the exclusive prefix of the pass's digit counts, k_hist_excl)
   uint32_t hist_excl[DPT];
-  {
-    uint32_t carry = 0;
 #pragma unroll
-    for (int q = 0; q < DPT; ++q) {
-      uint32_t blk_total;
-      hist_excl[q] = carry + block_excl_scan(hist[tid + q * kSortThreads], s_misc, &blk_total);
-      carry += blk_total;
-    }
-  }
+  for (int q = 0; q < DPT; ++q) hist_excl[q] = __ldg(hist + tid + q * kSortThreads);
   uint32_t prev[DPT];
 #pragma unroll
   for (int q = 0; q < DPT; ++q) prev[q] = lb_wait(status, tile, BINS, tid + q * kSortThreads, epoch, total[q]);
@@ -278,7 +296,8 @@ cudaError_t radix_sort_pairs(uint2* kv0, uint2* kv1, int64_t n, int bits, const 
     const size_t sm = sizeof(uint32_t) * 4 * passes * bins;
     if (dbits == 9) k_radix_hist<9><<<grid, 128, sm, s>>>(kv0, n, passes, ws.hist);
     else k_radix_hist<8><<<grid, 128, sm, s>>>(kv0, n, passes, ws.hist);
-    ++*launches;
+    k_hist_excl<<<passes, 512, 0, s>>>(ws.hist, bins);
+    *launches += 2;
   }
   uint2 *a = kv0, *b = kv1;
   for (int p = 0; p < passes; ++p) {
