@@ -115,7 +115,7 @@ __device__ __forceinline__ void write_partial(double* P, int pitch, int64_t c, i
 
 // One lane group per chunk of kChunk sorted occurrences.  kv[k] = {row key, grad row}.
 template <int LPB, int VPL, bool MEAN>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 4)
 k_segreduce(const uint32_t* __restrict__ seg, const uint32_t* __restrict__ Up,
             const uint2* __restrict__ kv, const uint32_t* __restrict__ chunk_u0,
             const float* __restrict__ grad, const int* __restrict__ offsets, int B, int F, int D,
@@ -123,8 +123,9 @@ k_segreduce(const uint32_t* __restrict__ seg, const uint32_t* __restrict__ Up,
             double* __restrict__ part_last, double* __restrict__ norm_main,
             double* __restrict__ norm_fix, uint32_t* __restrict__ owner_list,
             uint32_t* owner_count) {
-  // rows in flight per group: D=64 (VPL 2) measured best at 2 (64 registers, 4 CTAs/SM:
-  // 0.78 -> 0.72 ms on Feed-1; 1 -> 0.74, 4 -> 0.78 at 80 registers, 8 -> 1.5)
+  // rows in flight per group: D=64 (VPL 2) measured best at 2 with 4 CTAs/SM (64 registers:
+  // 0.78 -> 0.72 ms on Feed-1; 1 -> 0.74, 4 -> 0.78 at 80 registers, 8 -> 1.5); key-derived
+  // segment heads then took it to 0.69 ms)
   constexpr int UNR = (VPL == 1) ? 8 : (VPL == 2 ? 2 : 2);
   const int lane = threadIdx.x & (LPB - 1);
   const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LPB;
@@ -134,26 +135,38 @@ k_segreduce(const uint32_t* __restrict__ seg, const uint32_t* __restrict__ Up,
   const bool live = c < chunks && k0 < n_valid;
   const int64_t k1 = live ? min(k0 + (int64_t)kChunk, n_valid) : k0;
   uint32_t u = live ? __ldg(chunk_u0 + c) : 0u;  // segment containing occurrence k0 (RLE)
-  int64_t s_start = live ? (int64_t)__ldg(seg + u) : 0, s_end = live ? (int64_t)__ldg(seg + u + 1) : 0;
+  // the open segment started before this chunk (its sum is a part_first partial)
+  bool first_open = live && (int64_t)__ldg(seg + u) < k0;
+  const unsigned gshift = (threadIdx.x & 31) & ~(LPB - 1);  // this group's lanes in the warp
 
   double acc[VPL][4];
   zero(acc);
   double nrm = 0.0;
   // Warp-uniform loop (kChunk/LPB batches for every group): each batch loads LPB {key,
   // grad row} pairs (one per lane) and broadcasts them with full-mask shuffles; slots
-  // past k1 (last chunk, dead groups) are predicated.
+  // past k1 (last chunk, dead groups) are predicated.  Segment boundaries come from the
+  // keys themselves (an occurrence whose key differs from its predecessor's starts a
+  // segment), so no dependent load of the next boundary sits on the segment chain.
+  uint32_t carry_key = 0;  // key of the occurrence before the batch (lane LPB-1's, last batch)
   for (int it = 0; it < kChunk / LPB; ++it) {
     const int64_t kb = k0 + (int64_t)it * LPB;
-    uint32_t grow_l = 0;
+    uint2 kvl = make_uint2(0u, 0u);
     double inv_l = 1.0;
-    if (kb + lane < k1) {
-      grow_l = __ldg(&kv[kb + lane].y);
+    const bool in_l = kb + lane < k1;
+    if (in_l) {
+      kvl = __ldg(kv + kb + lane);
       if (MEAN) {
-        const uint32_t bb = grow_l / (uint32_t)F, ff = grow_l - bb * (uint32_t)F;
+        const uint32_t bb = kvl.y / (uint32_t)F, ff = kvl.y - bb * (uint32_t)F;
         const uint32_t bag = ff * (uint32_t)B + bb;
         inv_l = 1.0 / (double)(__ldg(offsets + bag + 1) - __ldg(offsets + bag));
       }
     }
+    uint32_t prev = __shfl_up_sync(kFull, kvl.x, 1, LPB);
+    if (lane == 0) prev = carry_key;
+    const bool head_l = in_l && kb + lane > k0 && kvl.x != prev;  // k0's segment is the open one
+    const unsigned heads = (__ballot_sync(kFull, head_l) >> gshift) & ((LPB < 32) ? ((1u << LPB) - 1u) : kFull);
+    carry_key = __shfl_sync(kFull, kvl.x, LPB - 1, LPB);
+    const uint32_t grow_l = kvl.y;
 #pragma unroll 1
     for (int jj = 0; jj < LPB; jj += UNR) {  // not unrolled: UNR rows in flight, not LPB
       float4 r[UNR][VPL];
@@ -169,14 +182,12 @@ k_segreduce(const uint32_t* __restrict__ seg, const uint32_t* __restrict__ Up,
 #pragma unroll
       for (int q = 0; q < UNR; ++q) {
         if (ok[q]) {
-          const int64_t occ = kb + jj + q;
-          if (occ == s_end) {  // segment u finished inside this chunk
-            if (s_start < k0) write_partial<VPL>(part_first, pitch, c, lane, LPB, acc);
+          if ((heads >> (jj + q)) & 1u) {  // segment u finished inside this chunk
+            if (first_open) write_partial<VPL>(part_first, pitch, c, lane, LPB, acc);
             else nrm += write_G<VPL>(G, pitch, u, lane, LPB, acc);
             zero(acc);
             ++u;
-            s_start = s_end;
-            s_end = __ldg(seg + u + 1);
+            first_open = false;
           }
 #pragma unroll
           for (int v = 0; v < VPL; ++v) {
@@ -196,12 +207,13 @@ k_segreduce(const uint32_t* __restrict__ seg, const uint32_t* __restrict__ Up,
       }
     }
   }
-  // the segment containing occurrence k1-1
+  // the segment containing occurrence k1-1: it ends here iff k1 is the end of the valid
+  // occurrences or starts another key
   bool owner = false;
   if (live) {
-    if (s_start < k0) {
+    if (first_open) {
       write_partial<VPL>(part_first, pitch, c, lane, LPB, acc);  // continues or ends here
-    } else if (s_end <= k1) {
+    } else if (k1 == n_valid || __ldg(&kv[k1].x) != __ldg(&kv[k1 - 1].x)) {
       nrm += write_G<VPL>(G, pitch, u, lane, LPB, acc);
     } else {
       write_partial<VPL>(part_last, pitch, c, lane, LPB, acc);  // starts here, spills over
