@@ -238,7 +238,7 @@ k_segreduce(const uint32_t* __restrict__ seg, const uint32_t* __restrict__ Up,
 template <int LPB, int VPL>
 __global__ void __launch_bounds__(256)
 k_fixup_short(const uint32_t* __restrict__ seg, const uint32_t* __restrict__ Up,
-              int pitch, const double* __restrict__ part_first,
+              const uint32_t* __restrict__ chunk_u0, int pitch, const double* __restrict__ part_first,
               const double* __restrict__ part_last, const uint32_t* __restrict__ owner_list,
               const uint32_t* __restrict__ owner_count, float* __restrict__ G,
               double* __restrict__ norm_fix, uint32_t* long_list, uint32_t* long_count) {
@@ -257,13 +257,9 @@ k_fixup_short(const uint32_t* __restrict__ seg, const uint32_t* __restrict__ Up,
     int64_t ce = 0;
     if (live) {
       cs = owner_list[e];
-      const int64_t kl = (int64_t)cs * kChunk + kChunk - 1;  // last occurrence of chunk cs
-      uint32_t lo = 0, hi = U - 1;
-      while (lo < hi) {
-        const uint32_t mid = (lo + hi + 1) >> 1;
-        if ((int64_t)__ldg(seg + mid) <= kl) lo = mid; else hi = mid - 1;
-      }
-      u = lo;
+      // the segment spills into chunk cs+1, so it is the one containing that chunk's first
+      // occurrence: chunk_u0[cs+1] (no binary search over seg[])
+      u = __ldg(chunk_u0 + cs + 1);
       ce = ((int64_t)__ldg(seg + u + 1) - 1) / kChunk;
       if (ce - cs > kFixLong) {
         if (lane == 0) {
@@ -769,8 +765,8 @@ cudaError_t launch_segreduce(const BwdArgs& a, int64_t* launches, cudaStream_t s
   uint32_t* long_count = a.owner_count + 1;
   uint32_t* long_list = a.owner_list + a.chunks;  // [2 * chunks] after the owner list
   LIRANK_GEOM2_DISPATCH(g, (k_fixup_short<L_, V_><<<persistent_grid((const void*)k_fixup_short<L_, V_>, a.chunks, L_), 256, 0, s>>>(
-                              a.seg, a.U, a.pitch, a.part_first, a.part_last, a.owner_list,
-                              a.owner_count, a.G, a.norm_fix, long_list, long_count)));
+                              a.seg, a.U, a.chunk_u0, a.pitch, a.part_first, a.part_last,
+                              a.owner_list, a.owner_count, a.G, a.norm_fix, long_list, long_count)));
   ++*launches;
   const int nsplit = a.pitch < kFixThreads ? kFixThreads / a.pitch : 1;
   const size_t smem = sizeof(double) * (size_t)(nsplit * a.pitch > kFixThreads ? nsplit * a.pitch : kFixThreads);
