@@ -91,12 +91,20 @@ k_pool_fwd_f32(const float* __restrict__ W, int pitch, const int* __restrict__ i
   // Warp-uniform trip count (the longest bag among the warp's groups): every lane reaches
   // every shuffle, so shuffles use the full mask; shorter bags are predicated.
   const int maxlen = __reduce_max_sync(kFull, len);
+  // ids are loaded one batch ahead (one per lane, LPB per group), so the next batch's id
+  // loads overlap this batch's row gathers instead of following them
+  uint32_t key_next = sentinel;
+  if (lane < len) {
+    key_next = row_key(__ldg(ids + lo + lane), m, sentinel, bad);
+    if (EMIT) kv_out[lo + lane] = make_uint2(key_next, grow);
+  }
   for (int j0 = 0; j0 < maxlen; j0 += LPB) {
-    const int j = j0 + lane;
-    uint32_t key = sentinel;
-    if (j < len) {  // one id per lane, LPB ids per group at once
-      key = row_key(__ldg(ids + lo + j), m, sentinel, bad);
-      if (EMIT) kv_out[lo + j] = make_uint2(key, grow);
+    const uint32_t key = key_next;
+    const int jn = j0 + LPB + lane;
+    key_next = sentinel;
+    if (jn < len) {
+      key_next = row_key(__ldg(ids + lo + jn), m, sentinel, bad);
+      if (EMIT) kv_out[lo + jn] = make_uint2(key_next, grow);
     }
 #pragma unroll
     for (int jj = 0; jj < LPB; jj += UNR) {
@@ -262,9 +270,11 @@ k_pool_fwd_q8(const uint8_t* __restrict__ codes, int qpitch, int meta_off,
   for (int v = 0; v < 4 * VPL; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
   bool bad = false;
   const int maxlen = __reduce_max_sync(kFull, len);
-  for (int j0 = 0; j0 < maxlen; j0 += LPB) {
-    const int j = j0 + lane;
-    const uint32_t key = j < len ? row_key(__ldg(ids + lo + j), m, kNone, bad) : kNone;
+  uint32_t key_next = lane < len ? row_key(__ldg(ids + lo + lane), m, kNone, bad) : kNone;
+  for (int j0 = 0; j0 < maxlen; j0 += LPB) {  // ids one batch ahead, as in the fp32 kernel
+    const uint32_t key = key_next;
+    const int jn = j0 + LPB + lane;
+    key_next = jn < len ? row_key(__ldg(ids + lo + jn), m, kNone, bad) : kNone;
 #pragma unroll 1
     for (int jj = 0; jj < LPB; jj += UNR) {
       uint32_t k[UNR];
