@@ -148,13 +148,15 @@ k_segreduce(const uint32_t* __restrict__ seg, const uint32_t* __restrict__ Up,
   // keys themselves (an occurrence whose key differs from its predecessor's starts a
   // segment), so no dependent load of the next boundary sits on the segment chain.
   uint32_t carry_key = 0;  // key of the occurrence before the batch (lane LPB-1's, last batch)
+  // the {key, grad row} pairs are loaded one batch ahead of the gradient-row gathers
+  uint2 kv_next = k0 + lane < k1 ? __ldg(kv + k0 + lane) : make_uint2(0u, 0u);
   for (int it = 0; it < kChunk / LPB; ++it) {
     const int64_t kb = k0 + (int64_t)it * LPB;
-    uint2 kvl = make_uint2(0u, 0u);
+    uint2 kvl = kv_next;
+    kv_next = kb + LPB + lane < k1 ? __ldg(kv + kb + LPB + lane) : make_uint2(0u, 0u);
     double inv_l = 1.0;
     const bool in_l = kb + lane < k1;
     if (in_l) {
-      kvl = __ldg(kv + kb + lane);
       if (MEAN) {
         const uint32_t bb = kvl.y / (uint32_t)F, ff = kvl.y - bb * (uint32_t)F;
         const uint32_t bag = ff * (uint32_t)B + bb;
