@@ -53,6 +53,7 @@ __device__ __forceinline__ uint32_t lb_wait(unsigned long long* status, int64_t 
       if (w[i] & kFlagPrefix) { done = true; break; }
     }
     if (done) break;
+    if (i == 0) __nanosleep(64);  // nothing new: yield the issue slots to working warps
     p -= i;
   }
   st_volatile(status + tile * stride + slot, lb_pack(epoch, kFlagPrefix, excl + aggregate));

@@ -33,9 +33,11 @@ __device__ __forceinline__ unsigned peers_of(uint32_t d, unsigned valid) {
   unsigned m = valid;
 #pragma unroll
   for (int b = 0; b < BITS; ++b) {
-    const uint32_t bit = (d >> b) & 1u;
-    const unsigned bb = __ballot_sync(0xffffffffu, bit);
-    m &= bb ^ (bit - 1u);  // bit 1: bb; bit 0: ~bb (one LOP3)
+    const int x = (int)(d << (31 - b));          // bit b of d in the sign bit
+    const unsigned bb = __ballot_sync(0xffffffffu, x < 0);
+    const unsigned t = (unsigned)(x >> 31);      // all ones iff the bit is set
+    // m &= ~(bb ^ t): bit set -> bb, clear -> ~bb, as ONE lop3 (LUT 0x90 = a & ~(b ^ c))
+    asm("lop3.b32 %0, %0, %1, %2, 0x90;" : "+r"(m) : "r"(bb), "r"(t));
   }
   return m;
 }
