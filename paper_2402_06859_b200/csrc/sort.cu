@@ -161,8 +161,7 @@ __device__ __forceinline__ void load_rank(const uint2* __restrict__ in, uint2 (&
     const uint32_t cur = ok ? wh[d] : 0u;
     r[i] = cur + __popc(peers & lt);
     __syncwarp();
-    // the highest peer (its rank is the group's count - 1) advances the counter
-    if (ok && (peers >> lane) == 1u) wh[d] = r[i] + 1u;
+    if (ok && lane == __ffs(peers) - 1) wh[d] = cur + __popc(peers);
     __syncwarp();
   }
 }
