@@ -52,6 +52,9 @@ def parse():
     ap.add_argument("--exchange", action="store_true",
                     help="N=1: run the sharded exchange path on a 1-rank NCCL communicator (its overhead)")
     ap.add_argument("--sharding", default="row", choices=["row", "table"], help="sharding for N>1 / --exchange")
+    ap.add_argument("--exchange-mode", default="p2p", choices=["p2p", "nccl"],
+                    help="sharded: p2p = fused exchange over NVLink peer memory (EMB_F_P2P; falls back to "
+                         "nccl on every rank if any rank cannot map its peers), nccl = collectives")
     ap.add_argument("--no-fim", action="store_true", help="skip the NEXT-3 incremental-training section")
     ap.add_argument("--serve", action="store_true",
                     help="serving bench: q8-only handle, a10 lookups only (default for --config feedq8)")
@@ -681,21 +684,35 @@ def run_ours(args, cfg, rank, world, local_rank):
     if world > 1 or args.exchange:
         # sharded over NCCL (or the exchange path on 1 rank); rank 0 makes the unique id, a broadcast distributes it
         from paper_2402_06859_b200 import nccl_unique_id
-        uid = torch.zeros(128, dtype=torch.uint8, device=dev)
-        if rank == 0:
-            uid.copy_(torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8))
-        if world > 1:
-            dist.broadcast(uid, 0)
-        shard_kw = dict(rank=rank, world_size=world, sharding=args.sharding, nccl_unique_id=uid.cpu().numpy().tobytes(),
+
+        def new_uid():  # one NCCL unique id per communicator
+            uid = torch.zeros(128, dtype=torch.uint8, device=dev)
+            if rank == 0:
+                uid.copy_(torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8))
+            if world > 1:
+                dist.broadcast(uid, 0)
+            return uid.cpu().numpy().tobytes()
+
+        shard_kw = dict(rank=rank, world_size=world, sharding=args.sharding, nccl_unique_id=new_uid(),
                         max_recv_nnz=3 * max_nnz, force_exchange=args.exchange)
-    emb = ShardedEmbedding(cfg.table_rows, D, cfg.feature_table, max_nnz=max_nnz, max_batch=B,
-                           adagrad=args.adagrad, q8=True, requant=True, device=dev, stream=stream,
-                           q8_mode=args.q8_mode, **shard_kw)
+    xmode = None
+    if shard_kw:
+        xmode = args.exchange_mode
+        shard_kw["p2p"] = xmode == "p2p"
+
+    def make_emb():
+        e = ShardedEmbedding(cfg.table_rows, D, cfg.feature_table, max_nnz=max_nnz, max_batch=B,
+                             adagrad=args.adagrad, q8=True, requant=True, device=dev, stream=stream,
+                             q8_mode=args.q8_mode, **shard_kw)
+        with torch.cuda.stream(stream):
+            for t in range(cfg.num_tables):
+                v = e.table_view(t)
+                G.fill_table(v, v.shape[0], D, e.pitch, cfg.seed, t, row0=int(e.row_lo[t]), stream=stream)
+            e.quantize()
+        return e
+
+    emb = make_emb()
     with torch.cuda.stream(stream):
-        for t in range(cfg.num_tables):
-            v = emb.table_view(t)
-            G.fill_table(v, v.shape[0], D, emb.pitch, cfg.seed, t, row0=int(emb.row_lo[t]), stream=stream)
-        emb.quantize()
         gshift = gen.grad_shift_for(max_nnz, D)
         dev_in = []
         for k, (ids, off) in enumerate(batches):
@@ -718,6 +735,18 @@ def run_ours(args, cfg, rank, world, local_rank):
         if world > 1:
             dist.barrier()
 
+    if xmode == "p2p":
+        # the first sharded forward maps the peers (collective: every rank gets the same verdict)
+        try:
+            step(0)
+        except RuntimeError as e:
+            if "EMB_ENCCL" not in str(e) and "ENCCL" not in str(e):
+                raise
+            xmode = f"nccl (p2p unavailable: {e})"
+            emb.close()
+            shard_kw["p2p"] = False
+            shard_kw["nccl_unique_id"] = new_uid()
+            emb = make_emb()
     for k in range(args.warmup):
         step(k)
     stream.synchronize()
@@ -887,8 +916,14 @@ def run_ours(args, cfg, rank, world, local_rank):
                    "global_batch": world * B, "batch_per_gpu": B, "nnz_per_step": nnz_avg, "alpha": cfg.alpha,
                    "unique_rows": U, "adagrad": args.adagrad, "q8": args.q8_mode,
                    "parallelism": ("single" if not args.exchange else f"{args.sharding}-sharded exchange path on a 1-rank NCCL communicator")
-                   if world == 1 else (f"row-sharded x{world} (NCCL all-to-all ids, reduce-scatter pooled, all-gather grads)"
-                                       if args.sharding == "row" else f"table-sharded x{world} (NCCL all-to-all ids and pooled blocks)"),
+                   if world == 1 else f"{args.sharding}-sharded x{world}",
+                   "exchange": None if xmode is None else (
+                       "p2p: ids all-to-all (NCCL); pooled rows stored by the owners' pooling kernels into the "
+                       "destination's buffer over NVLink peer memory (row-wise: per-owner slots summed in rank "
+                       "order); grad rows pushed to the owners by one kernel; NCCL 4-byte all-gather barriers"
+                       if xmode == "p2p" else
+                       f"{xmode}: ids all-to-all; " + ("reduce-scatter pooled, all-gather grads" if args.sharding == "row"
+                                                       else "all-to-all pooled / grad blocks + permute")),
                    "step": "a2 fwd -> a10 q8 fwd (overlapping a5 dedup on a side stream) -> a6-a8 bwd (a9 requant of touched rows fused)",
                    "l2": "flushed between timed steps (256 MiB write, untimed)",
                    "batches_rotated": len(batches)},

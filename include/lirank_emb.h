@@ -98,6 +98,19 @@ enum { EMB_SHARD_NONE = 0, EMB_SHARD_TABLE = 1, EMB_SHARD_ROW = 2 };
                              1B-row Feed tables (96 GB as q8) be served from one GPU.          */
 #define EMB_F_EXCHANGE 8u /* run the sharded exchange path even at world_size 1 (a 1-rank
                              communicator; exercises the transport on a single GPU)          */
+#define EMB_F_P2P 64u     /* (sharded) FUSED EXCHANGE over peer memory (NVLink / NVSwitch): the
+                             owner's pooling kernel stores every pooled row straight into the
+                             source rank's buffer -- table-wise in its final [B][F][D] place,
+                             row-wise into a per-owner slot summed in rank order -- and the
+                             backward's grad rows are pushed into the owners' buffers by one
+                             kernel; a stream-ordered barrier (a 4-byte all-gather) replaces
+                             the pooled / grad all-to-all, reduce-scatter and all-gather.  The
+                             ids exchange (a1) stays on the transport.  Peer mappings: CUDA IPC
+                             of the workspace allocation (NCCL transport) or the other
+                             handle's buffers (loopback), made by the first sharded
+                             forward (collective); it returns EMB_ENCCL on EVERY rank if any
+                             rank cannot map its peers (create again without the flag).  Workspace grows by world * B * F * D floats
+                             (row-wise).                                                     */
 #define EMB_F_LOOPBACK 4u /* (world_size > 1) TEST TRANSPORT: the ranks are threads of one
                              process sharing one device; cfg.nccl_unique_id is the hub from
                              emb_loopback_hub_create().  Every collective becomes a host

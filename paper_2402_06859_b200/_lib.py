@@ -15,7 +15,8 @@ EMB_ABI_VERSION = 1
 EMB_POOL_SUM, EMB_POOL_MEAN = 0, 1
 EMB_ADAGRAD_ROWWISE, EMB_ADAGRAD_ELEMENTWISE = 0, 1
 EMB_SHARD_NONE, EMB_SHARD_TABLE, EMB_SHARD_ROW = 0, 1, 2
-EMB_F_Q8, EMB_F_REQUANT, EMB_F_LOOPBACK, EMB_F_EXCHANGE, EMB_F_Q8_MINMAX, EMB_F_Q8_ONLY = 1, 2, 4, 8, 16, 32
+EMB_F_Q8, EMB_F_REQUANT, EMB_F_LOOPBACK, EMB_F_EXCHANGE, EMB_F_Q8_MINMAX, EMB_F_Q8_ONLY, EMB_F_P2P = \
+    1, 2, 4, 8, 16, 32, 64
 PHASES = ["fwd", "sort", "rle", "segreduce", "norm", "update", "fwd_q8", "quantize", "copy", "exchange"]
 
 STATUS = {0: "EMB_OK", 1: "EMB_EINVAL", 2: "EMB_ENOMEM", 3: "EMB_ECUDA", 4: "EMB_ENCCL",

@@ -89,6 +89,7 @@ emb_status make_plan(const emb_config* c, Plan* p) {
   p->exch = c->world_size > 1 || (c->flags & EMB_F_EXCHANGE);
   if (p->exch && c->sharding == EMB_SHARD_NONE) return EMB_EINVAL;
   if (p->exch && c->pooling == EMB_POOL_MEAN) return EMB_EINVAL;
+  if ((c->flags & EMB_F_P2P) && !p->exch) return EMB_EINVAL;
   p->sharding = p->exch ? c->sharding : EMB_SHARD_NONE;
   p->rank = c->rank;
   p->world = c->world_size;

@@ -55,11 +55,90 @@ static Api& api() {
 }
 }  // namespace nccl
 
+// cuMemGetAddressRange (driver API, dlopen'ed): the base of the allocation a pointer lies
+// in -- CUDA IPC handles name whole allocations (torch sub-allocates its segments).
+static bool alloc_base(const void* p, void** base) {
+  typedef int (*Fn)(unsigned long long*, size_t*, unsigned long long);
+  static Fn fn = [] {
+    void* lib = dlopen("libcuda.so.1", RTLD_NOW | RTLD_GLOBAL);
+    return lib ? (Fn)dlsym(lib, "cuMemGetAddressRange_v2") : (Fn) nullptr;
+  }();
+  unsigned long long b = 0;
+  size_t sz = 0;
+  if (!fn || fn(&b, &sz, (unsigned long long)(uintptr_t)p) != 0) return false;
+  *base = (void*)(uintptr_t)b;
+  return true;
+}
+
 struct NcclTransport : Transport {
   nccl::Comm comm = nullptr;
-  int world = 1;
+  int world = 1, rank = 0;
+  std::vector<void*> opened;  // IPC mappings of peer allocations (closed at destroy)
   ~NcclTransport() override {
+    for (void* q : opened) cudaIpcCloseMemHandle(q);
     if (comm) nccl::api().CommDestroy(comm);
+  }
+  bool barrier(void* scratch, cudaStream_t s) override {
+    // an all-gather of one word completes on a rank only after every rank has enqueued it,
+    // i.e. after every rank's stream finished the work before it (the exchange enqueues a
+    // system-scope fence after its peer-storing kernels)
+    uint8_t* q = (uint8_t*)scratch;
+    return nccl::api().AllGather(q, q + 256, 4, nccl::kUint8, comm, s) == 0;
+  }
+  // all ranks agree on `ok` (logical AND over ranks)
+  bool agree(bool ok, void* scratch, cudaStream_t s) {
+    uint8_t* q = (uint8_t*)scratch;
+    int32_t mine = ok ? 1 : 0;
+    std::vector<int32_t> all(world, 0);
+    if (cudaMemcpyAsync(q, &mine, 4, cudaMemcpyHostToDevice, s) != cudaSuccess) return false;
+    if (nccl::api().AllGather(q, q + 256, 4, nccl::kUint8, comm, s) != 0) return false;
+    if (cudaMemcpyAsync(all.data(), q + 256, 4ull * world, cudaMemcpyDeviceToHost, s) != cudaSuccess) return false;
+    if (cudaStreamSynchronize(s) != cudaSuccess) return false;
+    for (int32_t v : all) ok &= v == 1;
+    return ok;
+  }
+  bool map_peers(void* const* local, int n, void** peers, void* scratch, cudaStream_t s) override {
+    struct Rec { cudaIpcMemHandle_t h; int64_t off; int32_t ok, pad; };
+    const size_t per = sizeof(Rec) * (size_t)n, rbase = 1024;
+    if (rbase + per * world > kPeerScratchBytes) return false;  // same on every rank
+    std::vector<Rec> mine(n), all((size_t)n * world);
+    for (int i = 0; i < n; ++i) {
+      memset(&mine[i], 0, sizeof(Rec));
+      void* base = nullptr;
+      mine[i].ok = alloc_base(local[i], &base) && cudaIpcGetMemHandle(&mine[i].h, base) == cudaSuccess;
+      mine[i].off = (int64_t)((uint8_t*)local[i] - (uint8_t*)base);
+    }
+    uint8_t* q = (uint8_t*)scratch;
+    bool ok = cudaMemcpyAsync(q, mine.data(), per, cudaMemcpyHostToDevice, s) == cudaSuccess &&
+              nccl::api().AllGather(q, q + rbase, per, nccl::kUint8, comm, s) == 0 &&
+              cudaMemcpyAsync(all.data(), q + rbase, per * world, cudaMemcpyDeviceToHost, s) == cudaSuccess &&
+              cudaStreamSynchronize(s) == cudaSuccess;
+    for (size_t k = 0; ok && k < all.size(); ++k) ok &= all[k].ok == 1;
+    std::vector<std::pair<cudaIpcMemHandle_t, void*>> cache;  // one mapping per peer allocation
+    std::vector<void*> mapped;
+    for (int r = 0; ok && r < world; ++r)
+      for (int i = 0; ok && i < n; ++i) {
+        if (r == rank) { peers[(size_t)i * world + r] = local[i]; continue; }
+        const Rec& x = all[(size_t)r * n + i];
+        void* b = nullptr;
+        for (auto& c : cache)
+          if (memcmp(&c.first, &x.h, sizeof(x.h)) == 0) b = c.second;
+        if (!b) {
+          ok = cudaIpcOpenMemHandle(&b, x.h, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess;
+          if (!ok) break;
+          cache.push_back({x.h, b});
+          mapped.push_back(b);
+        }
+        peers[(size_t)i * world + r] = (uint8_t*)b + x.off;
+      }
+    ok = agree(ok, scratch, s);
+    if (!ok) {
+      for (void* b : mapped) cudaIpcCloseMemHandle(b);
+      cudaGetLastError();
+      return false;
+    }
+    opened.insert(opened.end(), mapped.begin(), mapped.end());
+    return true;
   }
   bool allgather(const void* send, void* recv, size_t bytes, cudaStream_t s) override {
     return nccl::api().AllGather(send, recv, bytes, nccl::kUint8, comm, s) == 0;
@@ -97,6 +176,7 @@ Transport* make_nccl_transport(const void* unique_id, int rank, int world) {
   memcpy(&id, unique_id, sizeof(id));
   auto* t = new NcclTransport();
   t->world = world;
+  t->rank = rank;
   if (a.CommInitRank(&t->comm, world, id, rank) != 0) {
     t->comm = nullptr;
     delete t;
@@ -114,6 +194,7 @@ struct Slot {
   const void* send = nullptr;
   const size_t* soff = nullptr;
   const size_t* sbytes = nullptr;
+  void* const* ptrs = nullptr;  // map_peers
   cudaEvent_t ready = nullptr;
   cudaEvent_t done = nullptr;
 };
@@ -216,6 +297,19 @@ struct LoopbackTransport : Transport {
     }
     finish(s);
     return ok;
+  }
+  bool map_peers(void* const* local, int n, void** peers, void*, cudaStream_t) override {
+    hub->slots[rank].ptrs = local;
+    hub->barrier();
+    for (int r = 0; r < hub->world; ++r)
+      for (int i = 0; i < n; ++i) peers[(size_t)i * hub->world + r] = hub->slots[r].ptrs[i];
+    hub->barrier();  // the slots' pointer arrays may go out of scope after this
+    return true;
+  }
+  bool barrier(void*, cudaStream_t s) override {
+    publish(nullptr, nullptr, nullptr, s);
+    finish(s);
+    return true;
   }
 };
 

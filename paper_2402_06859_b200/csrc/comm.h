@@ -25,7 +25,20 @@ struct Transport {
   // bytes into recv + roff[r] (sizes must match pairwise; host arrays of length world).
   virtual bool alltoallv(const void* send, const size_t* soff, const size_t* sbytes, void* recv,
                          const size_t* roff, const size_t* rbytes, cudaStream_t s) = 0;
+  // ---- fused exchange (EMB_F_P2P): peer memory ------------------------------------------
+  // Collective, host-blocking.  Every rank passes n pointers into its own device buffers;
+  // on success peers[i * world + r] is rank r's i-th pointer, addressable by this device's
+  // kernels (own rank: the local pointer; NCCL: CUDA IPC mappings over NVLink; loopback:
+  // the other handle's buffer on the same device).  Every rank returns the same verdict.
+  // `scratch` is a device buffer of >= kPeerScratchBytes the transport may use meanwhile.
+  virtual bool map_peers(void* const* local, int n, void** peers, void* scratch, cudaStream_t s) = 0;
+  // Collective, stream-ordered: work enqueued on s after the barrier starts only once every
+  // rank's stream has reached it, i.e. after every rank's earlier kernels (and their peer
+  // stores) have completed.  `scratch`: device, >= kPeerScratchBytes.
+  virtual bool barrier(void* scratch, cudaStream_t s) = 0;
 };
+
+constexpr size_t kPeerScratchBytes = 16384;
 
 // NCCL: returns nullptr (and a reason) if libnccl.so.2 cannot be loaded or init fails.
 Transport* make_nccl_transport(const void* unique_id, int rank, int world);

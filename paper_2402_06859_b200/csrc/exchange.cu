@@ -156,6 +156,71 @@ __global__ void k_permute(float* __restrict__ dense, float* __restrict__ blocks,
   }
 }
 
+// ---- fused exchange (EMB_F_P2P) ------------------------------------------------------------
+struct PushDst {
+  float* dst[kMaxWorld];  // each owner's pooled buffer (peer mapping)
+  int32_t Fo[kMaxWorld];  // features each owner pools (its pooled row block width)
+};
+
+// a4 fused: this rank's grad row (b, f) goes to every owner o that pooled feature f
+// (jmap[o][f] = j >= 0; table-wise one owner, row-wise all of them), at the row the owner's
+// recorded occurrences point to: dst[o] + ((rank * B + b) * Fo[o] + j) * D.  Replaces the
+// permute + all-to-all (table-wise) and the all-gather (row-wise): the grads cross NVLink
+// once, written by this kernel's stores (k_fence_sys + the barrier publish them).
+__global__ void __launch_bounds__(256)
+k_push_grad(const float* __restrict__ grad, int B, int F, int D, int W, int rank,
+            const int32_t* __restrict__ jmap, const PushDst pd) {
+  const bool vec = (D & 3) == 0;
+  const int nv = vec ? D / 4 : D;
+  const int64_t total = (int64_t)B * F * nv;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / nv;
+    const int v = (int)(i - row * nv);
+    const int b = (int)(row / F), f = (int)(row - (int64_t)b * F);
+    if (vec) {
+      const float4 g = ld_f4(grad + row * D + 4 * v);
+      for (int o = 0; o < W; ++o) {
+        const int j = __ldg(jmap + o * F + f);
+        if (j >= 0) st_f4(pd.dst[o] + (((int64_t)rank * B + b) * pd.Fo[o] + j) * D + 4 * v, g);
+      }
+    } else {
+      const float g = grad[row * D + v];
+      for (int o = 0; o < W; ++o) {
+        const int j = __ldg(jmap + o * F + f);
+        if (j >= 0) pd.dst[o][(((int64_t)rank * B + b) * pd.Fo[o] + j) * D + v] = g;
+      }
+    }
+  }
+}
+
+// Before a fused-exchange barrier: one system-scope fence after the storing kernels (stream
+// order makes their peer stores happen-before it; the fence is cumulative), so the stores are
+// visible to the destination GPU before this rank's arrival at the barrier is.
+__global__ void k_fence_sys() { __threadfence_system(); }
+
+// a3 fused, row-wise: out = slot_0 + slot_1 + ... in rank order (the owners' partial pools
+// their kernels stored here), fp32 adds -- the same sum the reduce-scatter forms.
+__global__ void __launch_bounds__(256)
+k_sum_slots(float* __restrict__ out, const float* __restrict__ slots, int W, int64_t n) {
+  if ((n & 3) == 0) {
+    const int64_t n4 = n / 4;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+         i += (int64_t)gridDim.x * blockDim.x) {
+      float4 a = ld_nc_f4(slots + 4 * i);
+      for (int r = 1; r < W; ++r) a = f4_add_rn(a, ld_nc_f4(slots + (int64_t)r * n + 4 * i));
+      st_f4(out + 4 * i, a);
+    }
+  } else {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+      float a = slots[i];
+      for (int r = 1; r < W; ++r) a = __fadd_rn(a, slots[(int64_t)r * n + i]);
+      out[i] = a;
+    }
+  }
+}
+
 emb_status scan(emb_t h, const uint32_t* in, uint32_t* out, int64_t n, int which) {
   CK(cudaMemsetAsync(h->x.scan_counter + which, 0, sizeof(uint32_t), h->stream));
   if (n == 0) return cudaMemsetAsync(out, 0, sizeof(uint32_t), h->stream) == cudaSuccess ? EMB_OK : EMB_ECUDA;
@@ -194,6 +259,11 @@ void carve_exchange(const Plan& p, Carver& cv, ExchangeWs* x) {
   x->scan_counter = cv.take<uint32_t>(4);
   const int64_t scan_n = std::max<int64_t>(Ltot + 1, W * Fr * B + 1);
   x->scan_status = cv.take<unsigned long long>((scan_n + kScanTile - 1) / kScanTile + 1);
+  if (p.flags & EMB_F_P2P) {
+    if (p.sharding == EMB_SHARD_ROW) x->pslots = cv.take<float>(W * B * F * D);
+    x->d_fcol = cv.take<int32_t>(Fr);
+    x->p2p_scratch = cv.take<uint8_t>((int64_t)kPeerScratchBytes);
+  }
 }
 
 emb_status exchange_init(emb_t h) {
@@ -217,8 +287,43 @@ emb_status exchange_init(emb_t h) {
   CK(cudaMemcpyAsync(x.d_owner0, p.owner0.data(), 4 * p.owner0.size(), cudaMemcpyHostToDevice, h->stream));
   CK(cudaMemcpyAsync(x.d_blk, p.blk.data(), 4 * p.blk.size(), cudaMemcpyHostToDevice, h->stream));
   CK(cudaMemcpyAsync(x.d_fmap, fmap.data(), 4 * fmap.size(), cudaMemcpyHostToDevice, h->stream));
+  std::vector<int32_t> fcol(p.feats_of[p.rank].begin(), p.feats_of[p.rank].end());
+  if (p.flags & EMB_F_P2P && !fcol.empty())
+    CK(cudaMemcpyAsync(x.d_fcol, fcol.data(), 4 * fcol.size(), cudaMemcpyHostToDevice, h->stream));
   CK(cudaStreamSynchronize(h->stream));  // host vectors go out of scope
   return EMB_OK;
+}
+
+// Collective (the first sharded forward; every rank reaches it in the same call): map every
+// rank's fused-exchange destinations into this device.  Lazy rather than at emb_create, so
+// handles of in-process (loopback) ranks can be created one after another.
+static emb_status map_p2p(emb_t h) {
+  ExchangeWs& x = h->x;
+  if (x.peer_pooled[0] != nullptr) return EMB_OK;
+  const int W = h->p.world;
+  void* local[3] = {x.xdense, h->p.sharding == EMB_SHARD_ROW ? (void*)x.pslots : (void*)x.xdense, x.pooled};
+  void* peers[3 * kMaxWorld] = {};
+  if (!h->comm->map_peers(local, 3, peers, x.p2p_scratch, h->stream)) return EMB_ENCCL;
+  for (int r = 0; r < W; ++r) {
+    x.peer_xdense[r] = (float*)peers[0 * W + r];
+    x.peer_pslots[r] = (float*)peers[1 * W + r];
+    x.peer_pooled[r] = (float*)peers[2 * W + r];
+  }
+  return EMB_OK;
+}
+
+// The fused-exchange destination of this rank's owner pooling.
+static PeerOut peer_out(emb_t h) {
+  const Plan& p = h->p;
+  PeerOut pm;
+  memset(&pm, 0, sizeof(pm));
+  if (!(p.flags & EMB_F_P2P)) return pm;
+  const bool row = p.sharding == EMB_SHARD_ROW;
+  for (int r = 0; r < p.world; ++r) pm.base[r] = row ? h->x.peer_pslots[r] : h->x.peer_xdense[r];
+  pm.fcol = h->x.d_fcol;
+  pm.F_out = p.F;
+  pm.slot = row ? p.rank : 0;
+  return pm;
 }
 
 // fmap[3f] must hold dest_base(owner(f)) * B for the current B (B may change per call).
@@ -247,6 +352,7 @@ emb_status exchange_forward(emb_t h, const Staged& st, int32_t batch, int64_t nn
   const unsigned bag_grid = (unsigned)(((int64_t)F * B + 255) / 256);
   emb_status s;
   int64_t n_recv = 0;
+  if ((p.flags & EMB_F_P2P) && (s = map_p2p(h)) != EMB_OK) return s;
   {
     Phase ph(h->prof, h->stream, EMB_PH_EXCHANGE);
     // ---- a1: bucketize -----------------------------------------------------------------
@@ -315,6 +421,7 @@ emb_status exchange_forward(emb_t h, const Staged& st, int32_t batch, int64_t nn
     a.sentinel = (uint32_t)p.local_rows;
     a.status = h->d_status;
     a.order_ws = h->order_ws;
+    a.peer = peer_out(h);
     Phase ph(h->prof, h->stream, EMB_PH_FWD);
     CK(launch_pool_fwd_f32(a, h->stream));
   } else {
@@ -334,6 +441,7 @@ emb_status exchange_forward(emb_t h, const Staged& st, int32_t batch, int64_t nn
     a.out = x.pooled;
     a.status = h->d_status;
     a.order_ws = h->order_ws;
+    a.peer = peer_out(h);
     Phase ph(h->prof, h->stream, EMB_PH_FWD_Q8);
     CK(launch_pool_fwd_q8(a, h->stream));
   }
@@ -341,7 +449,21 @@ emb_status exchange_forward(emb_t h, const Staged& st, int32_t batch, int64_t nn
   // ---- a3: pooled exchange back ----------------------------------------------------------
   {
     Phase ph(h->prof, h->stream, EMB_PH_EXCHANGE);
-    if (p.sharding == EMB_SHARD_ROW) {
+    if (p.flags & EMB_F_P2P) {
+      // the owners' kernels stored straight into this rank's buffers; once every rank has
+      // passed the barrier, they are complete
+      k_fence_sys<<<1, 1, 0, h->stream>>>();
+      h->launches += 1;
+      if (!h->comm->barrier(x.p2p_scratch, h->stream)) return EMB_ENCCL;
+      const int64_t n = (int64_t)B * F * D;
+      if (n > 0 && p.sharding == EMB_SHARD_ROW) {
+        k_sum_slots<<<148 * 4, 256, 0, h->stream>>>(st.out, x.pslots, W, n);
+        h->launches += 1;
+        CK(cudaGetLastError());
+      } else if (n > 0) {
+        CK(cudaMemcpyAsync(st.out, x.xdense, 4ull * n, cudaMemcpyDeviceToDevice, h->stream));
+      }
+    } else if (p.sharding == EMB_SHARD_ROW) {
       if (!h->comm->reduce_scatter_f32(x.pooled, st.out, (size_t)B * F * D, h->stream)) return EMB_ENCCL;
     } else {
       std::vector<size_t> soff(W), sb(W), roff(W), rb(W);
@@ -375,7 +497,20 @@ emb_status exchange_backward(emb_t h, const float* grad_dev) {
   const int W = p.world, F = p.F, Fr = p.Fr, D = p.D, B = h->fwd_B;
   {
     Phase ph(h->prof, h->stream, EMB_PH_EXCHANGE);
-    if (p.sharding == EMB_SHARD_ROW) {
+    if (p.flags & EMB_F_P2P) {
+      if (x.peer_pooled[0] == nullptr) return EMB_ESTATE;  // (a forward maps the peers)
+      if ((int64_t)B * F * D > 0) {
+        PushDst pd;
+        memset(&pd, 0, sizeof(pd));
+        for (int o = 0; o < W; ++o) { pd.dst[o] = x.peer_pooled[o]; pd.Fo[o] = p.Fo[o]; }
+        k_push_grad<<<148 * 8, 256, 0, h->stream>>>(grad_dev, B, F, D, W, p.rank, x.d_jmap, pd);
+        h->launches += 1;
+        CK(cudaGetLastError());
+      }
+      k_fence_sys<<<1, 1, 0, h->stream>>>();
+      h->launches += 1;
+      if (!h->comm->barrier(x.p2p_scratch, h->stream)) return EMB_ENCCL;
+    } else if (p.sharding == EMB_SHARD_ROW) {
       if (!h->comm->allgather(grad_dev, x.pooled, 4ull * B * F * D, h->stream)) return EMB_ENCCL;
     } else {
       if ((int64_t)B * F * D > 0) {

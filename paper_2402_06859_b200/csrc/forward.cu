@@ -59,15 +59,27 @@ __device__ __forceinline__ size_t out_row(int f, int b, int B, int Fb) {
   return ((size_t)blk * B + b) * Fb + (f - blk * Fb);
 }
 
+// Destination of the pooled row with block-order index grow (= out_row): `out` in block
+// order, or (fused exchange) the source rank's buffer through its peer mapping.
+template <bool PEER>
+__device__ __forceinline__ float* dst_row(float* out, uint32_t grow, int B, int Fb, int D,
+                                          const PeerOut& pm) {
+  if (!PEER) return out + (size_t)grow * D;
+  const uint32_t per = (uint32_t)B * (uint32_t)Fb;
+  const uint32_t blk = grow / per, rem = grow - blk * per;
+  const uint32_t b = rem / (uint32_t)Fb, j = rem - b * (uint32_t)Fb;
+  return pm.base[blk] + ((size_t)((size_t)pm.slot * B + b) * pm.F_out + __ldg(pm.fcol + j)) * D;
+}
+
 }  // namespace
 
-template <int LPB, int VPL, bool MEAN, bool EMIT>
+template <int LPB, int VPL, bool MEAN, bool EMIT, bool PEER>
 __global__ void __launch_bounds__(256)
 k_pool_fwd_f32(const float* __restrict__ W, int pitch, const int* __restrict__ ids,
                const int* __restrict__ offsets, int B, int F, int Fb, int D,
                const FeatMeta* __restrict__ meta, float* __restrict__ out,
                uint2* __restrict__ kv_out, uint32_t sentinel, uint32_t* status,
-              const uint32_t* __restrict__ order, bool skip_short) {
+              const uint32_t* __restrict__ order, bool skip_short, const PeerOut pm) {
   constexpr int UNR = (VPL == 1) ? 4 : (VPL == 2 ? 2 : 1);
   constexpr unsigned kFull = 0xffffffffu;
   const int lane = threadIdx.x & (LPB - 1);
@@ -137,7 +149,7 @@ k_pool_fwd_f32(const float* __restrict__ W, int pitch, const int* __restrict__ i
   if (!live) return;
   if (bad) set_status(status, kStIdRange);  // any lane: each lane validated its own ids
   if (MEAN) mean_div(acc, len);
-  float* o = out + (size_t)grow * D;
+  float* o = dst_row<PEER>(out, grow, B, Fb, D, pm);
 #pragma unroll
   for (int v = 0; v < VPL; ++v) store4(o, 4 * (lane + v * LPB), D, acc[v]);
 }
@@ -149,13 +161,13 @@ k_pool_fwd_f32(const float* __restrict__ W, int pitch, const int* __restrict__ i
 // one-hot-heavy batches keep as many rows in flight as multi-hot ones.  Positions whose bag
 // has more ids are left to the main kernel.  A one-id bag's pooled value is its row (SUM and
 // MEAN alike); an empty bag's is 0.
-template <int LPB, int VPL, bool EMIT>
+template <int LPB, int VPL, bool EMIT, bool PEER>
 __global__ void __launch_bounds__(256)
 k_pool_short_f32(const float* __restrict__ W, int pitch, const int* __restrict__ ids,
                  const int* __restrict__ offsets, int B, int F, int Fb, int D,
                  const FeatMeta* __restrict__ meta, float* __restrict__ out,
                  uint2* __restrict__ kv_out, uint32_t sentinel, uint32_t* status,
-                 const uint32_t* __restrict__ order) {
+                 const uint32_t* __restrict__ order, const PeerOut pm) {
   constexpr int UNR = VPL >= 4 ? 2 : 4;
   constexpr unsigned kFull = 0xffffffffu;
   const int lane = threadIdx.x & (LPB - 1);
@@ -202,7 +214,7 @@ k_pool_short_f32(const float* __restrict__ W, int pitch, const int* __restrict__
 #pragma unroll
     for (int u = 0; u < UNR; ++u)
       if (mm[u]) {
-        float* o = out + (size_t)gr[u] * D;
+        float* o = dst_row<PEER>(out, gr[u], B, Fb, D, pm);
         const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);  // 0 + row, as the main kernel (-0 -> +0)
 #pragma unroll
         for (int v = 0; v < VPL; ++v) store4(o, 4 * (lane + v * LPB), D, f4_add_rn(z, r[u][v]));
@@ -243,13 +255,14 @@ __device__ __forceinline__ uint4 ld_nc_u4(const void* p) {
 // kernel, ids are loaded LPB at a time and broadcast by full-mask shuffles over a
 // warp-uniform trip count, so a lane spends its instructions on the dequant, not on
 // per-slot key arithmetic.
-template <int LPB, int VPL, bool MEAN>
+template <int LPB, int VPL, bool MEAN, bool PEER>
 __global__ void __launch_bounds__(256, 4)
 k_pool_fwd_q8(const uint8_t* __restrict__ codes, int qpitch, int meta_off,
               const int* __restrict__ ids, const int* __restrict__ offsets, int B, int F, int Fb,
               int D, const FeatMeta* __restrict__ meta, float* __restrict__ out,
               uint32_t* status,
-              const uint32_t* __restrict__ order, uint32_t xmask, float magic, bool skip_short) {
+              const uint32_t* __restrict__ order, uint32_t xmask, float magic, bool skip_short,
+              const PeerOut pm) {
   constexpr int UNR = (VPL == 1) ? 4 : 2;
   constexpr uint32_t kNone = 0xffffffffu;
   constexpr unsigned kFull = 0xffffffffu;
@@ -314,7 +327,8 @@ k_pool_fwd_q8(const uint8_t* __restrict__ codes, int qpitch, int meta_off,
   if (bad) set_status(status, kStIdRange);  // any lane: each lane validated its own ids
   if (MEAN) mean_div(acc, len);
   // lane l holds dims 16*(l + v*LPB) .. +16
-  float* o = out + out_row(f, b, B, Fb) * D;
+  float* o = PEER ? dst_row<true>(out, (uint32_t)out_row(f, b, B, Fb), B, Fb, D, pm)
+                  : out + out_row(f, b, B, Fb) * D;
 #pragma unroll
   for (int v = 0; v < VPL; ++v) {
     const int d = 16 * (lane + v * LPB);
@@ -437,23 +451,29 @@ cudaError_t launch_pool_fwd_f32(const FwdArgs& a, cudaStream_t s) {
   const int Fb = a.Fb > 0 ? a.Fb : a.F;
   const uint32_t* order = bag_order(a.offsets, bags, a.order_ws, s);
   const bool split = order != nullptr;  // short bags sit at the end of the ordered positions
-#define LAUNCH_F32(MEAN, EMIT)                                                             \
-  LIRANK_FWD_GEOM_DISPATCH(g, (k_pool_fwd_f32<L_, V_, MEAN, EMIT><<<grid, 256, 0, s>>>(        \
+  const bool peer = a.peer.base[0] != nullptr;  // fused exchange (sharded: SUM, recording)
+#define LAUNCH_F32(MEAN, EMIT, PEER)                                                       \
+  LIRANK_FWD_GEOM_DISPATCH(g, (k_pool_fwd_f32<L_, V_, MEAN, EMIT, PEER><<<grid, 256, 0, s>>>( \
                               a.W, a.pitch, a.ids, a.offsets, a.B, a.F, Fb, a.D, a.meta,    \
-                              a.out, a.kv_out, a.sentinel, a.status, order, split)))
-  if (a.mean) {
-    if (a.kv_out) LAUNCH_F32(true, true); else LAUNCH_F32(true, false);
+                              a.out, a.kv_out, a.sentinel, a.status, order, split, a.peer)))
+  if (peer) {
+    if (a.mean || !a.kv_out) return cudaErrorInvalidValue;
+    LAUNCH_F32(false, true, true);
+  } else if (a.mean) {
+    if (a.kv_out) LAUNCH_F32(true, true, false); else LAUNCH_F32(true, false, false);
   } else {
-    if (a.kv_out) LAUNCH_F32(false, true); else LAUNCH_F32(false, false);
+    if (a.kv_out) LAUNCH_F32(false, true, false); else LAUNCH_F32(false, false, false);
   }
 #undef LAUNCH_F32
   if (split) {
     const unsigned sgrid = (unsigned)(((bags + g.lpb - 1) / g.lpb * g.lpb + 255) / 256);
-#define LAUNCH_SHORT(EMIT)                                                                   \
-  LIRANK_FWD_GEOM_DISPATCH(g, (k_pool_short_f32<L_, V_, EMIT><<<sgrid, 256, 0, s>>>(          \
+#define LAUNCH_SHORT(EMIT, PEER)                                                             \
+  LIRANK_FWD_GEOM_DISPATCH(g, (k_pool_short_f32<L_, V_, EMIT, PEER><<<sgrid, 256, 0, s>>>(    \
                               a.W, a.pitch, a.ids, a.offsets, a.B, a.F, Fb, a.D, a.meta,    \
-                              a.out, a.kv_out, a.sentinel, a.status, order)))
-    if (a.kv_out) LAUNCH_SHORT(true); else LAUNCH_SHORT(false);
+                              a.out, a.kv_out, a.sentinel, a.status, order, a.peer)))
+    if (peer) LAUNCH_SHORT(true, true);
+    else if (a.kv_out) LAUNCH_SHORT(true, false);
+    else LAUNCH_SHORT(false, false);
 #undef LAUNCH_SHORT
   }
   return cudaGetLastError();
@@ -474,11 +494,18 @@ cudaError_t launch_pool_fwd_q8(const FwdQ8Args& a, cudaStream_t s) {
   const float magic = a.minmax ? 8388608.0f : 8388736.0f;
   // (no short-bag split here: a k_pool_short_f32-style q8 kernel measured slower -- Ads a10
   // 3.24 -> 3.79 ms -- the q8 groups already hold 8 bags per warp)
-#define LAUNCH_Q8(MEAN)                                                                    \
-  LIRANK_GEOM_DISPATCH(g, (k_pool_fwd_q8<L_, V_, MEAN><<<grid, 256, 0, s>>>(               \
+#define LAUNCH_Q8(MEAN, PEER)                                                              \
+  LIRANK_GEOM_DISPATCH(g, (k_pool_fwd_q8<L_, V_, MEAN, PEER><<<grid, 256, 0, s>>>(         \
                               a.codes, a.qpitch, a.meta_off, a.ids, a.offsets, a.B, a.F, Fb, \
-                              a.D, a.meta, a.out, a.status, order, xmask, magic, false)))
-  if (a.mean) LAUNCH_Q8(true); else LAUNCH_Q8(false);
+                              a.D, a.meta, a.out, a.status, order, xmask, magic, false, a.peer)))
+  if (a.peer.base[0] != nullptr) {
+    if (a.mean) return cudaErrorInvalidValue;
+    LAUNCH_Q8(false, true);
+  } else if (a.mean) {
+    LAUNCH_Q8(true, false);
+  } else {
+    LAUNCH_Q8(false, false);
+  }
 #undef LAUNCH_Q8
   return cudaGetLastError();
 }

@@ -125,6 +125,13 @@ struct ExchangeWs {
   int32_t* d_blk = nullptr;            // [F]
   uint32_t* scan_counter = nullptr;    // [4] tile counters of the exchange scans
   unsigned long long* scan_status = nullptr;  // look-back words of the exchange scans
+  // fused exchange (EMB_F_P2P)
+  float* pslots = nullptr;        // row-wise: [world][B][F][D] owner partials, summed in rank order
+  int32_t* d_fcol = nullptr;      // [Fr]: global feature of owner-local feature j
+  uint8_t* p2p_scratch = nullptr; // [kPeerScratchBytes] transport scratch (barrier, mapping)
+  float* peer_xdense[kMaxWorld] = {};  // table-wise: each rank's xdense (fwd destination)
+  float* peer_pslots[kMaxWorld] = {};  // row-wise: each rank's pslots (fwd destination)
+  float* peer_pooled[kMaxWorld] = {};  // each rank's pooled (bwd grad destination)
 };
 
 }  // namespace lirank

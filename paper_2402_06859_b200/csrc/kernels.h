@@ -8,6 +8,21 @@
 
 namespace lirank {
 
+// Fused exchange (EMB_F_P2P): a pooling kernel stores the pooled row of the bag with
+// block-order index (s * B + b) * Fb + j (source block s, owner-local feature j, sample b)
+// straight into rank s's receive buffer over NVLink peer memory:
+//   base[s] + ((slot * B + b) * F_out + fcol[j]) * D.
+// Table-wise: F_out = F, slot 0, fcol[j] = the global feature (the row lands in its final
+// [B][F][D] place).  Row-wise: one [B][F][D] slot per owner (slot = this rank) that the
+// destination sums in rank order.  base[0] == NULL: off (rows go to `out` in block order).
+constexpr int kPeerMax = 16;
+struct PeerOut {
+  float* base[kPeerMax];
+  const int32_t* fcol;  // device [Fb]
+  int32_t F_out;
+  int32_t slot;
+};
+
 struct FwdArgs {
   const float* W;
   int pitch;
@@ -22,6 +37,7 @@ struct FwdArgs {
   uint32_t* status;
   bool mean;
   uint32_t* order_ws;  // NULL: bags in index order; else [kOrderWsWords(F*B)] scratch
+  PeerOut peer;        // fused exchange destination (base[0] NULL: off)
 };
 cudaError_t launch_pool_fwd_f32(const FwdArgs& a, cudaStream_t s);
 
@@ -51,6 +67,7 @@ struct FwdQ8Args {
   uint32_t* order_ws;  // as FwdArgs::order_ws
   bool order_ready;    // order_ws already holds an order of these F*B bags: reuse it
   bool minmax;         // min-max store (uint8 codes, meta {min, scale})
+  PeerOut peer;        // as FwdArgs::peer
 };
 cudaError_t launch_pool_fwd_q8(const FwdQ8Args& a, cudaStream_t s);
 

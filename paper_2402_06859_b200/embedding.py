@@ -68,7 +68,8 @@ class ShardedEmbedding:
                  rank: int = 0, world_size: int = 1, sharding: str = "none",
                  table_owner: Optional[Sequence[int]] = None, nccl_unique_id: Optional[bytes] = None,
                  loopback_hub: Optional["LoopbackHub"] = None, force_exchange: bool = False,
-                 max_recv_nnz: int = 0, q8_mode: str = "middle_max", q8_only: bool = False):
+                 max_recv_nnz: int = 0, q8_mode: str = "middle_max", q8_only: bool = False,
+                 p2p: bool = False):
         self.lib = L.load()
         assert q8_mode in ("middle_max", "min_max")
         self.q8_mode = q8_mode
@@ -105,6 +106,7 @@ class ShardedEmbedding:
             | (L.EMB_F_Q8_ONLY if q8_only else 0)
             | (L.EMB_F_LOOPBACK if loopback_hub is not None else 0)
             | (L.EMB_F_EXCHANGE if force_exchange else 0)
+            | (L.EMB_F_P2P if p2p else 0)
             | (L.EMB_F_Q8_MINMAX if q8_mode == "min_max" else 0),
             max_recv_nnz=int(max_recv_nnz))
         self.sizes = L.EmbSizes()

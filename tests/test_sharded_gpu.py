@@ -49,9 +49,10 @@ def global_batch(per_rank, F, B):
     return np.concatenate(ids_g).astype(np.int32), off_g.astype(np.int32)
 
 
+@pytest.mark.parametrize("p2p", [False, True])
 @pytest.mark.parametrize("W", [2, 4, 3])
 @pytest.mark.parametrize("sharding", ["table", "row"])
-def test_sharded_train_step_matches_unsharded_oracle(gpu, W, sharding):
+def test_sharded_train_step_matches_unsharded_oracle(gpu, W, sharding, p2p):
     from paper_2402_06859_b200 import LoopbackHub, ShardedEmbedding
     rows = [3000, 1200, 500, 77, 2000]
     ft = [0, 1, 2, 3, 4, 0, 1]  # features 5, 6 share tables 0, 1
@@ -68,7 +69,7 @@ def test_sharded_train_step_matches_unsharded_oracle(gpu, W, sharding):
         e = ShardedEmbedding(rows, D, ft, max_nnz=max(len(i) for i, _ in per_rank), max_batch=B,
                              max_recv_nnz=W * max(len(i) for i, _ in per_rank),
                              device=torch.device("cuda:0"), stream=s, rank=r, world_size=W,
-                             sharding=sharding, loopback_hub=hub)
+                             sharding=sharding, loopback_hub=hub, p2p=p2p)
         init_tables_host(e, cfg)
         embs.append(e)
     torch.cuda.synchronize()
@@ -123,8 +124,9 @@ def test_sharded_train_step_matches_unsharded_oracle(gpu, W, sharding):
     hub.close()
 
 
+@pytest.mark.parametrize("p2p", [False, True])
 @pytest.mark.parametrize("sharding", ["table", "row"])
-def test_sharded_q8_forward(gpu, sharding):
+def test_sharded_q8_forward(gpu, sharding, p2p):
     from paper_2402_06859_b200 import LoopbackHub, ShardedEmbedding
     W = 2
     rows = [2000, 900, 300]
@@ -138,7 +140,7 @@ def test_sharded_q8_forward(gpu, sharding):
         e = ShardedEmbedding(rows, D, ft, max_nnz=max(len(i) for i, _ in per_rank), max_batch=B,
                              max_recv_nnz=W * max(len(i) for i, _ in per_rank),
                              device=torch.device("cuda:0"), stream=torch.cuda.Stream(), rank=r,
-                             world_size=W, sharding=sharding, q8=True, loopback_hub=hub)
+                             world_size=W, sharding=sharding, q8=True, loopback_hub=hub, p2p=p2p)
         init_tables_host(e, cfg)
         e.quantize()
         embs.append(e)
@@ -166,8 +168,9 @@ def test_sharded_q8_forward(gpu, sharding):
     hub.close()
 
 
+@pytest.mark.parametrize("p2p", [False, True])
 @pytest.mark.parametrize("sharding", ["table", "row"])
-def test_nccl_transport_single_rank(gpu, sharding):
+def test_nccl_transport_single_rank(gpu, sharding, p2p):
     """The NCCL transport (torch's libnccl, dlopen'ed) on a 1-rank communicator: the whole
     exchange path runs (send/recv to self, all-gather, reduce-scatter) and must reproduce
     the unsharded handle bit for bit (with one rank the owner sees occurrences in the
@@ -183,7 +186,7 @@ def test_nccl_transport_single_rank(gpu, sharding):
     assert len(uid) == 128
     ex = ShardedEmbedding(rows, D, ft, max_nnz=len(ids), max_batch=B, device=torch.device("cuda:0"),
                           rank=0, world_size=1, sharding=sharding, nccl_unique_id=uid, force_exchange=True,
-                          q8=True)
+                          q8=True, p2p=p2p)
     ref = ShardedEmbedding(rows, D, ft, max_nnz=len(ids), max_batch=B, device=torch.device("cuda:0"), q8=True)
     for e in (ex, ref):
         init_tables_host(e, cfg)
@@ -232,3 +235,62 @@ def test_exchange_q8_forward_while_dedup_runs(gpu, sharding):
         res.append((o.cpu().numpy(), q.cpu().numpy()))
     assert (res[0][0] == res[1][0]).all() and (res[0][1] == res[1][1]).all()
     assert torch.equal(ex.weights, ref.weights)
+
+
+@pytest.mark.parametrize("W", [2, 3])
+@pytest.mark.parametrize("sharding", ["table", "row"])
+def test_p2p_exchange_matches_collective_exchange(gpu, W, sharding):
+    """EMB_F_P2P (pooled rows stored straight into the destination rank's buffer, grad rows
+    pushed into the owners' buffers, stream-ordered barriers) against the collective exchange
+    on the same ranks: three back-to-back steps of forward -> forward_q8 -> backward (buffer
+    reuse across steps) must agree bit for bit -- the row-wise slots are summed in rank order,
+    as the reduce-scatter does."""
+    from paper_2402_06859_b200 import LoopbackHub, ShardedEmbedding
+    rows = [5000, 1500, 600, 64]
+    ft = [0, 1, 2, 3, 0, 2]
+    cfg = configs.Config("p2p", rows, 64, [(t, ("range", 0, 14)) for t in ft], 96, seed=31)
+    B, F, D = cfg.batch, cfg.num_features, cfg.dim
+    nsteps = 3
+    batches = [[gen.make_batch(rows, cfg.features, B, cfg.seed + 100 * k + r, 0) for r in range(W)]
+               for k in range(nsteps)]
+    nnz_max = max(len(i) for bk in batches for i, _ in bk)
+    grads = [gen.grad_values(cfg.seed, k, W * B, F, D, gen.grad_shift_for(nnz_max * W, D)) for k in range(nsteps)]
+    results = {}
+    for p2p in (False, True):
+        hub = LoopbackHub(W)
+        embs = []
+        for r in range(W):
+            e = ShardedEmbedding(rows, D, ft, max_nnz=nnz_max, max_batch=B, max_recv_nnz=W * nnz_max,
+                                 device=torch.device("cuda:0"), stream=torch.cuda.Stream(), rank=r,
+                                 world_size=W, sharding=sharding, q8=True, requant=True, loopback_hub=hub,
+                                 p2p=p2p)
+            init_tables_host(e, cfg)
+            e.quantize()
+            embs.append(e)
+        torch.cuda.synchronize()
+
+        def run(r):
+            e = embs[r]
+            outs = []
+            with torch.cuda.stream(e.stream):
+                for k in range(nsteps):
+                    ids, off = batches[k][r]
+                    ids_d, off_d = torch.from_numpy(ids).cuda(), torch.from_numpy(off).cuda()
+                    o = e.forward(ids_d, off_d, B)
+                    q = e.forward_q8(ids_d, off_d, B)
+                    e.backward_adagrad(torch.from_numpy(grads[k][r * B:(r + 1) * B].copy()).cuda(), 0.05)
+                    outs.append((o.clone(), q.clone()))
+            assert e.sync() == 0
+            return [(o.cpu().numpy(), q.cpu().numpy()) for o, q in outs], e.weights.cpu().numpy().copy(), \
+                e.last_stats()[0]
+
+        results[p2p] = run_ranks(W, run)
+        for e in embs:
+            e.close()
+        hub.close()
+    for r in range(W):
+        (o_c, w_c, s_c), (o_p, w_p, s_p) = results[False][r], results[True][r]
+        for (a1, b1), (a2, b2) in zip(o_c, o_p):
+            assert np.array_equal(a1, a2) and np.array_equal(b1, b2)
+        assert np.array_equal(w_c, w_p)
+        assert s_c == s_p
