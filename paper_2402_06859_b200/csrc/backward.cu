@@ -592,6 +592,14 @@ k_adagrad(const uint32_t* __restrict__ unique, const uint32_t* __restrict__ Up,
   const int64_t gbase = g0 - (threadIdx.x & 31) / LPB;
   const int nvec = pitch >> 2;
   const double dimD = (double)D;
+  // the unique-row keys are loaded one iteration ahead: the key -> row-load dependence of
+  // the next iteration overlaps this iteration's row loads and updates
+  uint32_t key_next[R];
+#pragma unroll
+  for (int q = 0; q < R; ++q) {
+    const int64_t u = g0 + q * gstride;
+    key_next[q] = u < U ? __ldg(unique + u) : 0u;
+  }
   for (int64_t ub = gbase; ub < U; ub += R * gstride) {  // uniform per warp
     const int64_t u0 = g0 + (ub - gbase);
     uint32_t key[R];
@@ -602,7 +610,9 @@ k_adagrad(const uint32_t* __restrict__ unique, const uint32_t* __restrict__ Up,
     for (int q = 0; q < R; ++q) {
       const int64_t u = u0 + q * gstride;
       has[q] = u < U;
-      key[q] = has[q] ? __ldg(unique + u) : 0u;
+      key[q] = key_next[q];
+      const int64_t un = u + R * gstride;
+      key_next[q] = un < U ? __ldg(unique + un) : 0u;
     }
 #pragma unroll
     for (int q = 0; q < R; ++q) {
