@@ -8,6 +8,10 @@
    all-to-all-v and the CPU oracle as the owner's local compute, against the unsharded
    oracle on each rank's batch.  (a4 and the rank-ordered norm are covered on the GPU by
    tests/test_sharded_gpu.py through the loopback transport.)
+3. The fused-exchange (EMB_F_P2P) addressing: the owner's peer stores of pooled rows
+   (final [B][F] column table-wise; per-owner slots summed in rank order row-wise) and the
+   grad-row pushes to the owners, simulated as (row index, row) messages: every destination
+   row is written exactly once and the result equals the unsharded oracle.
 """
 import ctypes as C
 import os
@@ -96,7 +100,7 @@ def test_plan_consistent_across_gloo_ranks(sharding):
 # protocol simulation
 # ---------------------------------------------------------------------------------------
 
-def _protocol_worker(rank, world, port, sharding, q):
+def _protocol_worker(rank, world, port, sharding, q, mode="collective"):
     try:
         _init(rank, world, port)
         import oracle as O
@@ -157,18 +161,76 @@ def _protocol_worker(rank, world, port, sharding, q):
                 ob, _ = O.forward(pb1, Wfull, sub_ids, sub_off, B)
                 out_s[:, j] = ob[:, 0]
             pooled.append(out_s)
-        # a3: return: each source sums (row-wise) / places (table-wise) owner blocks in rank order
-        back = a2a([p.ravel() for p in pooled], np.float32)
-        out = np.zeros((B, F, D), dtype=np.float32)
-        for o in range(world):
-            blk = back[o].reshape(B, len(feats_of[o]), D)
-            for j, f in enumerate(feats_of[o]):
-                out[:, f] = out[:, f] + blk[:, j]
+        ok = True
+        if mode == "collective":
+            # a3: return: each source sums (row-wise) / places (table-wise) owner blocks in rank order
+            back = a2a([p.ravel() for p in pooled], np.float32)
+            out = np.zeros((B, F, D), dtype=np.float32)
+            for o in range(world):
+                blk = back[o].reshape(B, len(feats_of[o]), D)
+                for j, f in enumerate(feats_of[o]):
+                    out[:, f] = out[:, f] + blk[:, j]
+        else:
+            # a3 fused (EMB_F_P2P, exchange.cu peer_out / forward.cu dst_row): the owner stores
+            # the pooled row of (source s, owner-local feature j, sample b) at row
+            # (slot * B + b) * F + fcol[j] of rank s's buffer -- table-wise slot 0 and fcol[j]
+            # = the global feature (final [B][F] place), row-wise slot = owner rank into a
+            # [W][B][F] slot array summed in rank order.  Peer stores are simulated by
+            # shipping (row index, row) pairs.
+            row_wise = sharding == "row"
+            slot = rank if row_wise else 0
+            fcol = feats_of[rank]
+            idx_to, rows_to = [], []
+            for s_ in range(world):
+                ix = np.array([(slot * B + b) * F + fcol[j] for b in range(B) for j in range(Fr)], dtype=np.int64)
+                idx_to.append(ix)
+                rows_to.append(pooled[s_].reshape(B * Fr, D))
+            r_idx = a2a(idx_to, np.int64)
+            r_rows = a2a(rows_to, np.float32)
+            nslots = world if row_wise else 1
+            buf = np.full((nslots * B * F, D), np.nan, dtype=np.float32)
+            hits = np.zeros(nslots * B * F, dtype=np.int64)
+            for o in range(world):
+                buf[r_idx[o]] = r_rows[o].reshape(-1, D)
+                np.add.at(hits, r_idx[o], 1)
+            ok &= bool((hits == 1).all())  # every destination row written exactly once
+            if row_wise:
+                sl = buf.reshape(world, B, F, D)
+                out = sl[0].copy()
+                for o in range(1, world):
+                    out = out + sl[o]
+            else:
+                out = buf.reshape(B, F, D)
+            # a4 fused (k_push_grad): grad row (b, f) of this rank goes to every owner o with
+            # jmap[o][f] = j >= 0, at row (rank * B + b) * Fo[o] + j of o's pooled buffer
+            grad = gen.grad_values(cfg.seed, 0, world * B, F, D, 0)[rank * B:(rank + 1) * B]
+            jmap = [{f: j for j, f in enumerate(feats_of[o])} for o in range(world)]
+            idx_to, rows_to = [], []
+            for o in range(world):
+                pairs = [((rank * B + b) * len(feats_of[o]) + jmap[o][f], grad[b, f]) for b in range(B)
+                         for f in range(F) if f in jmap[o]]
+                idx_to.append(np.array([i for i, _ in pairs], dtype=np.int64))
+                rows_to.append(np.array([g for _, g in pairs], dtype=np.float32).reshape(-1))
+            r_idx = a2a(idx_to, np.int64)
+            r_rows = a2a(rows_to, np.float32)
+            gbuf = np.full((world * B * Fr, D), np.nan, dtype=np.float32)
+            ghits = np.zeros(world * B * Fr, dtype=np.int64)
+            for s_ in range(world):
+                gbuf[r_idx[s_]] = r_rows[s_].reshape(-1, D)
+                np.add.at(ghits, r_idx[s_], 1)
+            ok &= bool((ghits == 1).all())
+            # the owner's recorded occurrences point at grad row (src * B + b) * Fr + j: it must
+            # hold source src's gradient of (b, feats_of[rank][j])
+            gsrc = [gen.grad_values(cfg.seed, 0, world * B, F, D, 0)[s_ * B:(s_ + 1) * B] for s_ in range(world)]
+            g3 = gbuf.reshape(world, B, Fr, D)
+            for s_ in range(world):
+                for j, f in enumerate(feats_of[rank]):
+                    ok &= bool((g3[s_, :, j] == gsrc[s_][:, f]).all())
         # reference: unsharded oracle on this rank's batch
         pb = O.Problem(rows, D, ft)
         ref, _ = O.forward(pb, Wfull, ids, off, B)
         mag, _ = O.forward(pb, np.abs(Wfull), ids, off, B)
-        ok = bool((np.abs(out - ref) <= 1e-5 * mag + 1e-30).all())
+        ok &= bool((np.abs(out - ref) <= 1e-5 * mag + 1e-30).all())
         if sharding == "table":
             ok &= bool((out == ref).all())
         oks = [torch.zeros(1) for _ in range(world)]
@@ -181,12 +243,13 @@ def _protocol_worker(rank, world, port, sharding, q):
         q.put(traceback.format_exc())
 
 
+@pytest.mark.parametrize("mode", ["collective", "p2p"])
 @pytest.mark.parametrize("sharding", ["table", "row"])
-def test_exchange_protocol_gloo_matches_unsharded_oracle(sharding):
+def test_exchange_protocol_gloo_matches_unsharded_oracle(sharding, mode):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = free_port()
-    ps = [ctx.Process(target=_protocol_worker, args=(r, 2, port, sharding, q)) for r in range(2)]
+    ps = [ctx.Process(target=_protocol_worker, args=(r, 2, port, sharding, q, mode)) for r in range(2)]
     for p in ps:
         p.start()
     res = q.get(timeout=300)
