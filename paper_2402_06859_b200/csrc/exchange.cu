@@ -199,24 +199,42 @@ k_push_grad(const float* __restrict__ grad, int B, int F, int D, int W, int rank
 // visible to the destination GPU before this rank's arrival at the barrier is.
 __global__ void k_fence_sys() { __threadfence_system(); }
 
-// a3 fused, row-wise: out = slot_0 + slot_1 + ... in rank order (the owners' partial pools
-// their kernels stored here), fp32 adds -- the same sum the reduce-scatter forms.
+// a3 fused, row-wise: out[b][f] = sum over owners o, in rank order, of slot_o[b][f] (the
+// owners' partial pools their kernels stored here) -- the sum the reduce-scatter forms.
+// Owner o stored only bags with ids on it (lens[(o * F + f) * B + b] > 0, this rank's a1
+// lengths): the others are +0 and skipped (a partial sum is never -0, so x + 0 == x), which
+// keeps one-hot and short bags off NVLink for all but the owners holding their ids.
 __global__ void __launch_bounds__(256)
-k_sum_slots(float* __restrict__ out, const float* __restrict__ slots, int W, int64_t n) {
-  if ((n & 3) == 0) {
-    const int64_t n4 = n / 4;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
-         i += (int64_t)gridDim.x * blockDim.x) {
-      float4 a = ld_nc_f4(slots + 4 * i);
-      for (int r = 1; r < W; ++r) a = f4_add_rn(a, ld_nc_f4(slots + (int64_t)r * n + 4 * i));
-      st_f4(out + 4 * i, a);
-    }
-  } else {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-      float a = slots[i];
-      for (int r = 1; r < W; ++r) a = __fadd_rn(a, slots[(int64_t)r * n + i]);
-      out[i] = a;
+k_sum_slots(float* __restrict__ out, const float* __restrict__ slots, const uint32_t* __restrict__ lens,
+            int W, int B, int F, int D) {
+  const bool vec = (D & 3) == 0;
+  const int nv = vec ? D / 4 : D;
+  const int64_t n = (int64_t)B * F * D, total = (int64_t)B * F * nv;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / nv;
+    const int v = (int)(i - row * nv);
+    const int b = (int)(row / F), f = (int)(row - (int64_t)b * F);
+    if (vec) {
+      float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+      bool any = false;
+      for (int o = 0; o < W; ++o) {
+        if (__ldg(lens + ((int64_t)o * F + f) * B + b) == 0) continue;
+        const float4 x = ld_nc_f4(slots + (int64_t)o * n + row * D + 4 * v);
+        a = any ? f4_add_rn(a, x) : x;
+        any = true;
+      }
+      st_f4(out + row * D + 4 * v, a);
+    } else {
+      float a = 0.f;
+      bool any = false;
+      for (int o = 0; o < W; ++o) {
+        if (__ldg(lens + ((int64_t)o * F + f) * B + b) == 0) continue;
+        const float x = slots[(int64_t)o * n + row * D + v];
+        a = any ? __fadd_rn(a, x) : x;
+        any = true;
+      }
+      out[row * D + v] = a;
     }
   }
 }
@@ -323,6 +341,7 @@ static PeerOut peer_out(emb_t h) {
   pm.fcol = h->x.d_fcol;
   pm.F_out = p.F;
   pm.slot = row ? p.rank : 0;
+  pm.skip_empty = row ? 1 : 0;
   return pm;
 }
 
@@ -457,7 +476,7 @@ emb_status exchange_forward(emb_t h, const Staged& st, int32_t batch, int64_t nn
       if (!h->comm->barrier(x.p2p_scratch, h->stream)) return EMB_ENCCL;
       const int64_t n = (int64_t)B * F * D;
       if (n > 0 && p.sharding == EMB_SHARD_ROW) {
-        k_sum_slots<<<148 * 4, 256, 0, h->stream>>>(st.out, x.pslots, W, n);
+        k_sum_slots<<<148 * 4, 256, 0, h->stream>>>(st.out, x.pslots, x.lens, W, B, F, D);
         h->launches += 1;
         CK(cudaGetLastError());
       } else if (n > 0) {

@@ -148,6 +148,7 @@ k_pool_fwd_f32(const float* __restrict__ W, int pitch, const int* __restrict__ i
   }
   if (!live) return;
   if (bad) set_status(status, kStIdRange);  // any lane: each lane validated its own ids
+  if (PEER && pm.skip_empty && len == 0) return;
   if (MEAN) mean_div(acc, len);
   float* o = dst_row<PEER>(out, grow, B, Fb, D, pm);
 #pragma unroll
@@ -178,7 +179,7 @@ k_pool_short_f32(const float* __restrict__ W, int pitch, const int* __restrict__
   const long long bag = mine ? (order != nullptr ? (long long)__ldg(order + pos) : pos) : 0;
   const int lo = mine ? __ldg(offsets + bag) : 0;
   const int len = mine ? __ldg(offsets + bag + 1) - lo : 2;
-  mine = mine && len <= 1;
+  mine = mine && len <= 1 && !(PEER && pm.skip_empty && len == 0);
   uint32_t key = sentinel, grow = 0;
   bool bad = false;
   if (mine) {
@@ -325,6 +326,7 @@ k_pool_fwd_q8(const uint8_t* __restrict__ codes, int qpitch, int meta_off,
   }
   if (!live) return;
   if (bad) set_status(status, kStIdRange);  // any lane: each lane validated its own ids
+  if (PEER && pm.skip_empty && len == 0) return;
   if (MEAN) mean_div(acc, len);
   // lane l holds dims 16*(l + v*LPB) .. +16
   float* o = PEER ? dst_row<true>(out, (uint32_t)out_row(f, b, B, Fb), B, Fb, D, pm)

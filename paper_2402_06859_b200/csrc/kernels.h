@@ -21,6 +21,8 @@ struct PeerOut {
   const int32_t* fcol;  // device [Fb]
   int32_t F_out;
   int32_t slot;
+  int32_t skip_empty;   // row-wise: bags with no id on this owner are not stored (the
+                        // destination's slot sum skips them by its a1 lengths)
 };
 
 struct FwdArgs {

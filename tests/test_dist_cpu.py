@@ -182,9 +182,11 @@ def _protocol_worker(rank, world, port, sharding, q, mode="collective"):
             fcol = feats_of[rank]
             idx_to, rows_to = [], []
             for s_ in range(world):
-                ix = np.array([(slot * B + b) * F + fcol[j] for b in range(B) for j in range(Fr)], dtype=np.int64)
-                idx_to.append(ix)
-                rows_to.append(pooled[s_].reshape(B * Fr, D))
+                # row-wise: a bag with no id on this owner is not stored (skip_empty)
+                L_ = r_lens[s_].reshape(Fr, B)
+                keep = [(b, j) for b in range(B) for j in range(Fr) if not row_wise or L_[j, b] > 0]
+                idx_to.append(np.array([(slot * B + b) * F + fcol[j] for b, j in keep], dtype=np.int64))
+                rows_to.append(np.array([pooled[s_][b, j] for b, j in keep], dtype=np.float32).reshape(-1))
             r_idx = a2a(idx_to, np.int64)
             r_rows = a2a(rows_to, np.float32)
             nslots = world if row_wise else 1
@@ -193,13 +195,23 @@ def _protocol_worker(rank, world, port, sharding, q, mode="collective"):
             for o in range(world):
                 buf[r_idx[o]] = r_rows[o].reshape(-1, D)
                 np.add.at(hits, r_idx[o], 1)
-            ok &= bool((hits == 1).all())  # every destination row written exactly once
             if row_wise:
+                # slot o row (b, f) is written iff this rank sent ids of bag (f, b) to owner o
+                # (its a1 lengths), exactly once; the sum skips the others (k_sum_slots)
+                sent = np.stack([lens[o].T for o in range(world)])  # [W][B][F]
+                ok &= bool((hits == (sent > 0).ravel()).all())
                 sl = buf.reshape(world, B, F, D)
-                out = sl[0].copy()
-                for o in range(1, world):
-                    out = out + sl[o]
+                out = np.zeros((B, F, D), dtype=np.float32)
+                for b_ in range(B):
+                    for f in range(F):
+                        first = True
+                        for o in range(world):
+                            if sent[o, b_, f] == 0:
+                                continue
+                            out[b_, f] = sl[o, b_, f] if first else out[b_, f] + sl[o, b_, f]
+                            first = False
             else:
+                ok &= bool((hits == 1).all())  # every destination row written exactly once
                 out = buf.reshape(B, F, D)
             # a4 fused (k_push_grad): grad row (b, f) of this rank goes to every owner o with
             # jmap[o][f] = j >= 0, at row (rank * B + b) * Fo[o] + j of o's pooled buffer
