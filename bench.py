@@ -851,6 +851,9 @@ def run_ours(args, cfg, rank, world, local_rank):
         h2d_b = int(nnz_avg * 4 + (F * B + 1) * 4 + B * F * D * 4)
         e2e = {"value": world * B / (e_ms / 1e3), "unit": "samples/s", "ms_per_step": e_ms,
                "h2d_bytes_per_step": h2d_b, "d2h_bytes_per_step": 8,
+               # the device step (ms_per_step of the line) hides behind the next step's input
+               # copy: the e2e step is bound by host->device bandwidth (PCIe) at this rate
+               "h2d_gbs_per_gpu": h2d_b / (e_ms / 1e3) / 1e9,
                "path": "pinned host ids/offsets/grads -> H2D one step ahead on a copy stream -> "
                        "emb_forward, emb_forward_q8, emb_backward_adagrad(-> S, D2H), every step"}
 

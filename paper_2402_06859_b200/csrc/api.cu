@@ -224,6 +224,7 @@ void carve(const Plan& p, Carver& cv, emb_handle* h) {
   auto* sg = cv.take<double>(1);
   auto* cl = cv.take<float>(1);
   auto* st = cv.take<uint32_t>(1);
+  auto* ep = cv.take<uint32_t>(2);
   auto* order = cv.take<uint32_t>(kOrderWsWords(std::max<int64_t>(F * Bmax, bags_cap)));
   ExchangeWs x{};
   if (p.exch) carve_exchange(p, cv, &x);
@@ -247,6 +248,7 @@ void carve(const Plan& p, Carver& cv, emb_handle* h) {
     h->owner_list = ol; h->owner_count = oc;
     h->chunks_cap = chunks;
     h->S_parts = sp; h->S_local = sl; h->S_global = sg; h->d_clip = cl; h->d_status = st;
+    h->d_epoch = ep;
     h->norm_parts = nparts; h->norm_done = ndone;
     h->x = x;
   }
@@ -316,16 +318,15 @@ emb_status launch_dedup(emb_t h) {
     bool in1 = false;
     {
       Phase ph(h->prof, h->side, EMB_PH_SORT);
-      CK(radix_sort_pairs(h->kvA, h->kvB, n, p.key_bits, h->sort, h->epoch, &passes, &in1,
+      CK(radix_sort_pairs(h->kvA, h->kvB, n, p.key_bits, h->sort, h->d_epoch, &passes, &in1,
                           &h->launches, h->side));
     }
-    h->epoch += (uint32_t)passes;
     if (in1) kres = h->kvB;
     Phase ph(h->prof, h->side, EMB_PH_RLE);
     CK(launch_rle(kres, n, (uint32_t)p.local_rows, h->unique, h->seg, h->d_U, h->chunk_u0,
-                  h->sort.counters + kMaxPasses, h->sort.status, h->epoch, h->side));
-    h->epoch += 1;
-    h->launches += 1;
+                  h->sort.counters + kMaxPasses, h->sort.status, h->d_epoch, (uint32_t)passes, h->side));
+    CK(launch_epoch_advance(h->d_epoch, (uint32_t)passes + 1, h->side));
+    h->launches += 2;
   } else {
     CK(cudaMemsetAsync(h->d_U, 0, sizeof(uint32_t), h->side));
     CK(cudaMemsetAsync(h->seg, 0, sizeof(uint32_t), h->side));
@@ -597,6 +598,9 @@ emb_status emb_create(const emb_config* cfg, const emb_buffers* buf, emb_t* out)
     h->launches += na > 0;
   }
   if (e == cudaSuccess) e = cudaMemsetAsync(h->d_status, 0, sizeof(uint32_t), h->stream);
+  const uint32_t epoch0[2] = {1u, 1u};  // status words are zeroed: epoch 0 is never current
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(h->d_epoch, epoch0, sizeof(epoch0), cudaMemcpyHostToDevice, h->stream);
   if (e == cudaSuccess) e = cudaMemsetAsync(h->norm_done, 0, sizeof(uint32_t), h->stream);
   if (e == cudaSuccess)
     e = cudaMemsetAsync(h->sort.status, 0, sizeof(unsigned long long) * h->sort.max_tiles * kRadixBinsMax, h->stream);

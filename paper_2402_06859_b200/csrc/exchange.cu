@@ -32,8 +32,9 @@ constexpr int kScanTile = kScanThreads * kScanItems;
 // Exclusive scan of n uint32 (one pass, decoupled look-back); out[n] = total.
 __global__ void __launch_bounds__(kScanThreads)
 k_scan_excl(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, int64_t n,
-            uint32_t* tile_counter, unsigned long long* status, uint32_t epoch) {
+            uint32_t* tile_counter, unsigned long long* status, const uint32_t* epoch_p) {
   __shared__ uint32_t s_tile, s_warp[kScanThreads / 32], s_excl;
+  const uint32_t epoch = *epoch_p;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
   __syncthreads();
@@ -246,9 +247,10 @@ emb_status scan(emb_t h, const uint32_t* in, uint32_t* out, int64_t n, int which
   // its own look-back words: the a5 dedup of the previous forward may still be running on
   // the side stream with the radix sort's status array
   k_scan_excl<<<(unsigned)tiles, kScanThreads, 0, h->stream>>>(in, out, n, h->x.scan_counter + which,
-                                                               h->x.scan_status, h->epoch);
-  h->epoch += 1;
-  h->launches += 1;
+                                                               h->x.scan_status, h->d_epoch + 1);
+  CK(cudaGetLastError());
+  CK(launch_epoch_advance(h->d_epoch + 1, 1, h->stream));
+  h->launches += 2;
   return cudaGetLastError() == cudaSuccess ? EMB_OK : EMB_ECUDA;
 }
 

@@ -191,7 +191,9 @@ struct emb_handle {
   int64_t fwd_nnz = 0;  // occurrences recorded (pooled on this rank) by the last forward
   int fwd_B = 0;        // local batch of the last forward
   const uint2* sorted_kv = nullptr;
-  uint32_t epoch = 1;
+  // look-back epochs in device memory: [0] the dedup (side stream), [1] the exchange scans
+  // (main stream); read by the kernels, advanced by k_epoch_advance (graph-replayable)
+  uint32_t* d_epoch = nullptr;
   int64_t launches = 0;
 };
 

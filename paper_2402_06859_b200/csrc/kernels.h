@@ -91,9 +91,10 @@ struct SortWs {
 };
 
 // Sorts n pairs by the low `bits` bits of .x, stably.  Ping-pongs between kv0 and kv1;
-// *result_in_1 tells whether the result is in kv1.  Uses epochs [epoch, epoch+passes).
+// *result_in_1 tells whether the result is in kv1.  Uses epochs [*epoch, *epoch+passes): the
+// epoch is read from device memory by the kernels (graph-replayable), advanced by the caller.
 cudaError_t radix_sort_pairs(uint2* kv0, uint2* kv1, int64_t n, int bits, const SortWs& ws,
-                             uint32_t epoch, int* passes_out, bool* result_in_1, int64_t* launches,
+                             const uint32_t* epoch, int* passes_out, bool* result_in_1, int64_t* launches,
                              cudaStream_t s);
 
 // Run-length encode sorted pairs (sentinel = invalid, sorts last): unique[U], seg[U+1],
@@ -101,7 +102,10 @@ cudaError_t radix_sort_pairs(uint2* kv0, uint2* kv1, int64_t n, int bits, const 
 // writes U = 0, seg[0] = 0.
 cudaError_t launch_rle(const uint2* kv, int64_t n, uint32_t sentinel, uint32_t* unique,
                        uint32_t* seg, uint32_t* U_out, uint32_t* chunk_u0, uint32_t* counter,
-                       unsigned long long* status, uint32_t epoch, cudaStream_t s);
+                       unsigned long long* status, const uint32_t* epoch, uint32_t epoch_off,
+                       cudaStream_t s);
+// *epoch += n, in stream order after the kernels that used epochs [*epoch, *epoch + n)
+cudaError_t launch_epoch_advance(uint32_t* epoch, uint32_t n, cudaStream_t s);
 
 // ---- a6-a8 ----------------------------------------------------------------------------
 constexpr int kChunk = 256;  // occurrences per group in the segment-reduce

@@ -170,8 +170,9 @@ template <int BITS, int ITEMS, bool MATCH, int MINB = 4>
 __global__ void __launch_bounds__(kSortThreads, MINB)
 k_onesweep(const uint2* __restrict__ in, uint2* __restrict__ out, int64_t n, int shift,
            const uint32_t* __restrict__ hist, uint32_t* tile_counter,
-           unsigned long long* status, uint32_t epoch) {
+           unsigned long long* status, const uint32_t* epoch_p, uint32_t epoch_off) {
   constexpr int BINS = 1 << BITS;
+  const uint32_t epoch = *epoch_p + epoch_off;  // device-resident: graph replays advance it
   constexpr int DPT = BINS / kSortThreads;  // digits per thread (1 or 2)
   constexpr int TILE = kSortThreads * ITEMS;
   extern __shared__ uint8_t smem_raw[];
@@ -263,8 +264,8 @@ k_onesweep(const uint2* __restrict__ in, uint2* __restrict__ out, int64_t n, int
 
 template <int BITS, int ITEMS, bool MATCH, int MINB>
 static cudaError_t onesweep_pass(const uint2* a, uint2* b, int64_t n, int shift, const uint32_t* hist,
-                                 uint32_t* counter, unsigned long long* status, uint32_t epoch,
-                                 cudaStream_t s) {
+                                 uint32_t* counter, unsigned long long* status, const uint32_t* epoch,
+                                 uint32_t epoch_off, cudaStream_t s) {
   constexpr int TILE = kSortThreads * ITEMS;
   const size_t sm = sizeof(uint2) * TILE + sizeof(uint32_t) * (NW * (1 << BITS) + (1 << BITS) + NW + 2);
   static bool attr = false;
@@ -274,12 +275,13 @@ static cudaError_t onesweep_pass(const uint2* a, uint2* b, int64_t n, int shift,
   }
   const int64_t tiles = (n + TILE - 1) / TILE;
   k_onesweep<BITS, ITEMS, MATCH, MINB><<<(unsigned)tiles, kSortThreads, sm, s>>>(a, b, n, shift, hist,
-                                                                                counter, status, epoch);
+                                                                                counter, status, epoch,
+                                                                                epoch_off);
   return cudaGetLastError();
 }
 
 cudaError_t radix_sort_pairs(uint2* kv0, uint2* kv1, int64_t n, int bits, const SortWs& ws,
-                             uint32_t epoch, int* passes_out, bool* result_in_1, int64_t* launches,
+                             const uint32_t* epoch, int* passes_out, bool* result_in_1, int64_t* launches,
                              cudaStream_t s) {
   // digit width: 9 bits when it saves a pass (e.g. 27-bit Feed-1 keys: 3 passes, not 4)
   const int dbits = (bits > 24 && bits <= 27) || (bits > 16 && bits <= 18) ? 9 : 8;
@@ -310,7 +312,7 @@ cudaError_t radix_sort_pairs(uint2* kv0, uint2* kv1, int64_t n, int bits, const 
     // values stay in L1) measured best on Feed-1: the tile's global loads are latency-bound
     // and more resident CTAs overlap them (2 CTAs at 120 registers: +10% sort time; 8 or
     // 12 items at 5-8 CTAs and match.any ranking were slower)
-#define OS(BITS) e = onesweep_pass<BITS, 16, false, 4>(a, b, n, shift, hp, ctr, ws.status, epoch + p, s);
+#define OS(BITS) e = onesweep_pass<BITS, 16, false, 4>(a, b, n, shift, hp, ctr, ws.status, epoch, (uint32_t)p, s);
     if (dbits == 9) { OS(9) } else { OS(8) }
 #undef OS
     if (e != cudaSuccess) return e;
@@ -331,7 +333,8 @@ cudaError_t radix_sort_pairs(uint2* kv0, uint2* kv1, int64_t n, int bits, const 
 __global__ void __launch_bounds__(kSortThreads)
 k_rle(const uint2* __restrict__ kv, int64_t n, uint32_t sentinel, uint32_t* unique,
       uint32_t* seg, uint32_t* U_out, uint32_t* chunk_u0, uint32_t* tile_counter,
-      unsigned long long* status, uint32_t epoch) {
+      unsigned long long* status, const uint32_t* epoch_p, uint32_t epoch_off) {
+  const uint32_t epoch = *epoch_p + epoch_off;
   __shared__ uint32_t s_tile;
   __shared__ uint32_t s_warp[NW];
   __shared__ uint32_t s_excl;
@@ -394,11 +397,22 @@ k_rle(const uint2* __restrict__ kv, int64_t n, uint32_t sentinel, uint32_t* uniq
 
 cudaError_t launch_rle(const uint2* kv, int64_t n, uint32_t sentinel, uint32_t* unique,
                        uint32_t* seg, uint32_t* U_out, uint32_t* chunk_u0, uint32_t* counter,
-                       unsigned long long* status, uint32_t epoch, cudaStream_t s) {
+                       unsigned long long* status, const uint32_t* epoch, uint32_t epoch_off,
+                       cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   const int64_t tiles = (n + kSortTile - 1) / kSortTile;
   k_rle<<<(unsigned)tiles, kSortThreads, 0, s>>>(kv, n, sentinel, unique, seg, U_out, chunk_u0,
-                                                 counter, status, epoch);
+                                                 counter, status, epoch, epoch_off);
+  return cudaGetLastError();
+}
+
+// The look-back epochs live in device memory and are advanced by a kernel in stream order
+// (not baked into launch parameters), so a captured CUDA graph of a step can be replayed:
+// every replay tags its status words with fresh epochs.
+__global__ void k_epoch_advance(uint32_t* epoch, uint32_t n) { *epoch += n; }
+
+cudaError_t launch_epoch_advance(uint32_t* epoch, uint32_t n, cudaStream_t s) {
+  k_epoch_advance<<<1, 1, 0, s>>>(epoch, n);
   return cudaGetLastError();
 }
 
