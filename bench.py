@@ -56,6 +56,7 @@ def parse():
                     help="sharded: p2p = fused exchange over NVLink peer memory (EMB_F_P2P; falls back to "
                          "nccl on every rank if any rank cannot map its peers), nccl = collectives")
     ap.add_argument("--no-fim", action="store_true", help="skip the NEXT-3 incremental-training section")
+    ap.add_argument("--no-graph", action="store_true", help="skip the CUDA-graph replay section")
     ap.add_argument("--serve", action="store_true",
                     help="serving bench: q8-only handle, a10 lookups only (default for --config feedq8)")
     ap.add_argument("--q8-mode", default="middle_max", choices=["middle_max", "min_max"],
@@ -375,6 +376,60 @@ def qr_section(cfg, ids, off, B, dev, stream, flush, hbm_peak, reps=5):
 # ---------------------------------------------------------------------------
 # NEXT-2 section: the end-to-end Feed train step (embedding + MLP tower, one global clip)
 # ---------------------------------------------------------------------------
+
+def graph_section(emb, cfg, dev_in, B, out, out_q8, stream, flush, steps=10, small_batch=4096):
+    """The W = 1 step captured once per resident batch as a CUDA graph and replayed (the step has
+    no host synchronisation and its look-back epochs live in device memory), at the full batch
+    (L2 flushed between replays, as the main line) and at a small batch where host launch cost
+    matters (no flush: latency)."""
+    import torch
+    from workload import gpu as G
+
+    def step(ids_d, off_d, g, b, o, oq):
+        emb.forward(ids_d, off_d, b, out=o)
+        emb.forward_q8(ids_d, off_d, b, out=oq)
+        emb.backward_adagrad(g, LR)
+
+    def timed(fn, n, flush_between):
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
+        torch.cuda.synchronize()
+        for k in range(n):
+            if flush_between:
+                G.flush_l2(flush, stream=stream)
+            with torch.cuda.stream(stream):
+                evs[k][0].record(stream)
+                fn(k)
+                evs[k][1].record(stream)
+        torch.cuda.synchronize()
+        return float(np.mean([a.elapsed_time(b_) for a, b_ in evs]))
+
+    res = {"what": "whole W=1 step (a2, a10, a5-a8 + requant) as one CUDA graph per batch, replayed"}
+    graphs = []
+    for (ids_d, off_d, g) in dev_in:
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr, stream=stream):
+            step(ids_d, off_d, g, B, out, out_q8)
+        graphs.append(gr)
+    res["full_ms_per_step_graph"] = timed(lambda k: graphs[k % len(graphs)].replay(), steps, True)
+    # small batch: latency, host launch cost visible
+    ids, off = gen.make_batch(cfg.table_rows, cfg.features, small_batch, cfg.seed + 1, 0, alpha=cfg.alpha)
+    F, D = cfg.num_features, cfg.dim
+    ids_d, off_d = torch.from_numpy(ids).cuda(), torch.from_numpy(off).cuda()
+    gs = torch.empty((small_batch, F, D), device=out.device)
+    G.fill_grad(gs, small_batch, F, D, cfg.seed, 1, gen.grad_shift_for(len(ids), D), stream=stream)
+    o_s, oq_s = torch.empty_like(gs), torch.empty_like(gs)
+    for _ in range(3):
+        with torch.cuda.stream(stream):
+            step(ids_d, off_d, gs, small_batch, o_s, oq_s)
+    res["small_batch"] = small_batch
+    res["small_ms_per_step_eager"] = timed(lambda k: step(ids_d, off_d, gs, small_batch, o_s, oq_s), 3 * steps, False)
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gr, stream=stream):
+        step(ids_d, off_d, gs, small_batch, o_s, oq_s)
+    res["small_ms_per_step_graph"] = timed(lambda k: gr.replay(), 3 * steps, False)
+    assert emb.sync() == 0
+    return res
+
 
 def model_section(emb, batches, dev_in, B, dense_dim, stream, flush, steps=10, warmup=3):
     """FeedModel (paper_2402_06859_b200/feed_model.py) on the bench's Feed-1 tables: pooled
@@ -942,6 +997,11 @@ def run_ours(args, cfg, rank, world, local_rank):
         "e2e": e2e,
         "clip": {"sq_norm": S, "c": float(c)},
     }
+    if world == 1 and not args.no_graph:
+        try:
+            line["graph"] = graph_section(emb, cfg, dev_in, B, out, out_q8, stream, flush)
+        except Exception as e:  # report, never hide
+            line["graph"] = {"error": repr(e)}
     if world == 1 and not args.no_model:
         try:
             line["model"] = model_section(emb, batches, dev_in, B, args.dense_features, stream, flush)
