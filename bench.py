@@ -57,6 +57,7 @@ def parse():
                          "nccl on every rank if any rank cannot map its peers), nccl = collectives")
     ap.add_argument("--no-fim", action="store_true", help="skip the NEXT-3 incremental-training section")
     ap.add_argument("--no-graph", action="store_true", help="skip the CUDA-graph replay section")
+    ap.add_argument("--no-lib", action="store_true", help="skip the library (torch embedding_bag) baseline")
     ap.add_argument("--serve", action="store_true",
                     help="serving bench: q8-only handle, a10 lookups only (default for --config feedq8)")
     ap.add_argument("--q8-mode", default="middle_max", choices=["middle_max", "min_max"],
@@ -429,6 +430,37 @@ def graph_section(emb, cfg, dev_in, B, out, out_q8, stream, flush, steps=10, sma
     res["small_ms_per_step_graph"] = timed(lambda k: gr.replay(), 3 * steps, False)
     assert emb.sync() == 0
     return res
+
+
+def library_section(emb, cfg, dev_in, B, stream, flush, steps=10):
+    """Library baseline beside a2 on the same tables and batches: torch.nn.functional.embedding_bag
+    (PyTorch's CUDA kernel, mode='sum') over the stored tables with the same global row keys and
+    offsets (feature-major bags; its output is [F*B, D] instead of [B, F, D])."""
+    import torch
+    import torch.nn.functional as Fn
+    from workload import gpu as G
+    D, F = cfg.dim, cfg.num_features
+    W = emb.weights[:, :D] if emb.pitch != D else emb.weights
+    inputs = []
+    for (ids_d, off_d, _) in dev_in:
+        base = torch.tensor([int(emb.local_base[cfg.feature_table[f]]) for f in range(F)], dtype=torch.int64,
+                            device=ids_d.device)
+        counts = (off_d[1:] - off_d[:-1]).view(F, B).sum(1)
+        keys = (ids_d.to(torch.int64) + torch.repeat_interleave(base, counts.to(torch.int64))).contiguous()
+        inputs.append((keys, off_d[:-1].to(torch.int64).contiguous()))
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    torch.cuda.synchronize()
+    with torch.cuda.stream(stream):
+        for k in range(steps):
+            keys, offs = inputs[k % len(inputs)]
+            G.flush_l2(flush, stream=stream)
+            evs[k][0].record(stream)
+            out = Fn.embedding_bag(keys, W, offs, mode="sum")
+            evs[k][1].record(stream)
+    torch.cuda.synchronize()
+    ms = float(np.mean([a.elapsed_time(b_) for a, b_ in evs]))
+    return {"what": "torch.nn.functional.embedding_bag(mode='sum') on the same tables / bags (a2's work)",
+            "torch_embedding_bag_ms": ms, "rows_out": int(out.shape[0])}
 
 
 def model_section(emb, batches, dev_in, B, dense_dim, stream, flush, steps=10, warmup=3):
@@ -997,6 +1029,12 @@ def run_ours(args, cfg, rank, world, local_rank):
         "e2e": e2e,
         "clip": {"sq_norm": S, "c": float(c)},
     }
+    if world == 1 and not args.no_lib:
+        try:
+            line["library"] = library_section(emb, cfg, dev_in, B, stream, flush)
+            line["library"]["ours_a2_ms"] = per_phase["fwd"]["ms"]
+        except Exception as e:  # report, never hide
+            line["library"] = {"error": repr(e)}
     if world == 1 and not args.no_graph:
         try:
             line["graph"] = graph_section(emb, cfg, dev_in, B, out, out_q8, stream, flush)
