@@ -489,17 +489,24 @@ __device__ __forceinline__ void quantize_group_row(const float4 (&x)[VPL], int D
   if (!zero_codes) {
     float err = fast ? 0.0f : 1.0f;
     uint32_t wv[VPL];
+    // (paired FADD2 / FMUL2 arithmetic: each element exactly the scalar operation)
+    const float2 nmid = make_float2(-middle, -middle), rc = make_float2(rcp, rcp);
+    const float2 kbig = make_float2(12582912.0f, 12582912.0f), nkbig = make_float2(-12582912.0f, -12582912.0f);
 #pragma unroll
     for (int v = 0; v < VPL; ++v) {
       const int d = 4 * (lane + v * LPB);
-      const float e[4] = {x[v].x, x[v].y, x[v].z, x[v].w};
+      float2 q[2] = {f2_mul_rn(f2_add_rn(make_float2(x[v].x, x[v].y), nmid), rc),
+                     f2_mul_rn(f2_add_rn(make_float2(x[v].z, x[v].w), nmid), rc)};
       uint32_t bits[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const float qa = fminf(fmaxf(__fmul_rn(__fsub_rn(e[i], middle), rcp), qlo), qhi);
-        const float big = __fadd_rn(qa, 12582912.0f);
-        err = fmaxf(err, fabsf(__fsub_rn(qa, __fsub_rn(big, 12582912.0f))));
-        bits[i] = __float_as_uint(big);
+      for (int h = 0; h < 2; ++h) {
+        q[h] = make_float2(fminf(fmaxf(q[h].x, qlo), qhi), fminf(fmaxf(q[h].y, qlo), qhi));
+        const float2 big = f2_add_rn(q[h], kbig);
+        const float2 rq = f2_add_rn(big, nkbig);
+        const float2 dq = f2_add_rn(q[h], make_float2(-rq.x, -rq.y));
+        err = fmaxf(err, fmaxf(fabsf(dq.x), fabsf(dq.y)));
+        bits[2 * h] = __float_as_uint(big.x);
+        bits[2 * h + 1] = __float_as_uint(big.y);
       }
       uint32_t w = __byte_perm(__byte_perm(bits[0], bits[1], 0x0040),
                                __byte_perm(bits[2], bits[3], 0x0040), 0x5410);

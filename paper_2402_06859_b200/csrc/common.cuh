@@ -71,9 +71,37 @@ __device__ __forceinline__ int ld_nc_i32(const int* p) {
 __device__ __forceinline__ double ld_volatile_f64(const double* p) {
   return *reinterpret_cast<const volatile double*>(p);
 }
+// Paired fp32 arithmetic (sm_100a FADD2 / FFMA2 / FMUL2: two IEEE round-to-nearest fp32
+// operations per instruction, each element exactly the scalar __fadd_rn / __fmaf_rn /
+// __fmul_rn): half the issue slots of the scalar form on the same FP32 pipe.
+__device__ __forceinline__ float2 f2_add_rn(float2 a, float2 b) {
+  float2 r;
+  asm("{.reg .b64 a, b, r;\n\t"
+      "mov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\t"
+      "add.rn.f32x2 r, a, b;\n\tmov.b64 {%0, %1}, r;}"
+      : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+__device__ __forceinline__ float2 f2_mul_rn(float2 a, float2 b) {
+  float2 r;
+  asm("{.reg .b64 a, b, r;\n\t"
+      "mov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\t"
+      "mul.rn.f32x2 r, a, b;\n\tmov.b64 {%0, %1}, r;}"
+      : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+__device__ __forceinline__ float2 f2_fma_rn(float2 a, float2 b, float2 c) {
+  float2 r;
+  asm("{.reg .b64 a, b, c, r;\n\t"
+      "mov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\tmov.b64 c, {%6, %7};\n\t"
+      "fma.rn.f32x2 r, a, b, c;\n\tmov.b64 {%0, %1}, r;}"
+      : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return r;
+}
 __device__ __forceinline__ float4 f4_add_rn(float4 a, float4 b) {
-  return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z),
-                     __fadd_rn(a.w, b.w));
+  const float2 lo = f2_add_rn(make_float2(a.x, a.y), make_float2(b.x, b.y));
+  const float2 hi = f2_add_rn(make_float2(a.z, a.w), make_float2(b.z, b.w));
+  return make_float4(lo.x, lo.y, hi.x, hi.y);
 }
 
 __device__ __forceinline__ void set_status(uint32_t* st, uint32_t bit) {

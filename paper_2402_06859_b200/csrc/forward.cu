@@ -229,18 +229,22 @@ k_pool_short_f32(const float* __restrict__ W, int pitch, const int* __restrict__
 // u = byte ^ 0x80 = code + 128, the float with bits 0x4B0000uu is 2^23 + u, so
 // (2^23 + u) - (2^23 + 128) = code exactly.
 // Min-max stores (NEXT-4) hold unsigned codes u directly: xmask = 0 and magic = 2^23.
-__device__ __forceinline__ float code_f(uint32_t x, uint32_t sel, float magic) {
-  return __fsub_rn(__int_as_float((int)__byte_perm(x, 0x4B000000u, sel)), magic);
+// 4 codes (one 32-bit word) -> acc += base + code * scale, element by element (each element
+// exactly fl(acc + fmaf(code, scale, base)); the magic subtraction, fma and add run paired,
+// FADD2 / FFMA2, two elements per instruction).
+__device__ __forceinline__ float code_bits(uint32_t x, uint32_t sel) {  // 2^23 + u
+  return __int_as_float((int)__byte_perm(x, 0x4B000000u, sel));
 }
-// 4 codes (one 32-bit word) -> acc += base + code * scale, element by element.
 __device__ __forceinline__ float4 deq4_add(float4 acc, uint32_t w, float scale, float middle,
                                            uint32_t xmask, float magic) {
   const uint32_t x = w ^ xmask;
-  acc.x = __fadd_rn(acc.x, __fmaf_rn(code_f(x, 0x7540, magic), scale, middle));
-  acc.y = __fadd_rn(acc.y, __fmaf_rn(code_f(x, 0x7541, magic), scale, middle));
-  acc.z = __fadd_rn(acc.z, __fmaf_rn(code_f(x, 0x7542, magic), scale, middle));
-  acc.w = __fadd_rn(acc.w, __fmaf_rn(code_f(x, 0x7543, magic), scale, middle));
-  return acc;
+  const float2 nm = make_float2(-magic, -magic), sc = make_float2(scale, scale),
+               md = make_float2(middle, middle);
+  const float2 c01 = f2_add_rn(make_float2(code_bits(x, 0x7540), code_bits(x, 0x7541)), nm);
+  const float2 c23 = f2_add_rn(make_float2(code_bits(x, 0x7542), code_bits(x, 0x7543)), nm);
+  const float2 a01 = f2_add_rn(make_float2(acc.x, acc.y), f2_fma_rn(c01, sc, md));
+  const float2 a23 = f2_add_rn(make_float2(acc.z, acc.w), f2_fma_rn(c23, sc, md));
+  return make_float4(a01.x, a01.y, a23.x, a23.y);
 }
 __device__ __forceinline__ uint4 ld_nc_u4(const void* p) {
   uint4 r;
