@@ -1035,7 +1035,7 @@ def run_ours(args, cfg, rank, world, local_rank):
             line["library"]["ours_a2_ms"] = per_phase["fwd"]["ms"]
         except Exception as e:  # report, never hide
             line["library"] = {"error": repr(e)}
-    if world == 1 and not args.no_graph:
+    if world == 1 and not args.no_graph and not args.exchange:  # (the exchange path syncs the host)
         try:
             line["graph"] = graph_section(emb, cfg, dev_in, B, out, out_q8, stream, flush)
         except Exception as e:  # report, never hide
