@@ -69,7 +69,7 @@ class ShardedEmbedding:
                  table_owner: Optional[Sequence[int]] = None, nccl_unique_id: Optional[bytes] = None,
                  loopback_hub: Optional["LoopbackHub"] = None, force_exchange: bool = False,
                  max_recv_nnz: int = 0, q8_mode: str = "middle_max", q8_only: bool = False,
-                 p2p: bool = False):
+                 p2p: bool = False, guard_bytes: int = 0):
         self.lib = L.load()
         assert q8_mode in ("middle_max", "min_max")
         self.q8_mode = q8_mode
@@ -121,9 +121,17 @@ class ShardedEmbedding:
                                           self.row_hi.ctypes.data_as(C.c_void_p)), "emb_local_layout")
         dev = self.device
 
+        # guard_bytes > 0 (tests): every buffer gets a 0xA5-filled tail the library must never
+        # touch (a write past a planned size shows up in guards_intact())
+        self._guards = []
+
         def alloc(nbytes, dtype=torch.uint8):
             n = max(int(nbytes), 16)
-            return torch.empty(n, dtype=torch.uint8, device=dev)
+            t = torch.empty(n + int(guard_bytes), dtype=torch.uint8, device=dev)
+            if guard_bytes:
+                t[n:].fill_(0xA5)
+                self._guards.append((t, n))
+            return t
 
         self.q8_only = bool(q8_only)  # serving handle: no fp32 tables (EMB_F_Q8_ONLY)
         self.weights_buf = alloc(s.weights_bytes) if s.weights_bytes else None
@@ -138,6 +146,10 @@ class ShardedEmbedding:
                             _ptr(self.meta_buf), _ptr(self.workspace))
         self.h = C.c_void_p()
         L.check(self.lib.emb_create(C.byref(self.cfg), C.byref(bufs), C.byref(self.h)), "emb_create")
+
+    def guards_intact(self) -> bool:
+        torch.cuda.synchronize(self.device)
+        return all(bool((t[n:] == 0xA5).all()) for t, n in self._guards)
 
     # ---- views -------------------------------------------------------------------------
     @property
