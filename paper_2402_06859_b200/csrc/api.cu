@@ -393,6 +393,7 @@ emb_status backward_local(emb_t h, const float* grad_dev, float lr, double extra
   a.q8_codes = (p.flags & EMB_F_REQUANT) ? h->codes : nullptr;
   a.q8_meta_off = h->q8_meta_off;
   a.q8_minmax = (p.flags & EMB_F_Q8_MINMAX) != 0;
+  a.tma = LIRANK_TMA_UPDATE;
   a.qpitch = p.qpitch;
 
   {

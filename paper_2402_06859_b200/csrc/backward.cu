@@ -433,15 +433,21 @@ __device__ __forceinline__ uint32_t code_exact(float e, float base, float scale,
   return (uint32_t)((int)r) & 0xffu;
 }
 
+// rot (full rows only, D == 4 * LPB * VPL): this lane holds float4 (lane + v * LPB + rot) mod
+// (LPB * VPL) of the row in x[v] (the TMA update's bank-conflict-free smem layout).
+template <int LPB, int VPL>
+__device__ __forceinline__ int rot_idx(int lane, int v, int rot) {
+  return rot ? (lane + v * LPB + rot) % (LPB * VPL) : lane + v * LPB;
+}
 template <int LPB, int VPL>
 __device__ __forceinline__ void quantize_group_row(const float4 (&x)[VPL], int D, int lane, bool live,
                                                    uint8_t* __restrict__ code_row,
                                                    int meta_off, int qpitch, bool minmax,
-                                                   uint32_t* status) {
+                                                   uint32_t* status, int rot = 0) {
   float mn = FLT_MAX, mx = -FLT_MAX;
 #pragma unroll
   for (int v = 0; v < VPL; ++v) {
-    const int d = 4 * (lane + v * LPB);
+    const int d = 4 * (rot_idx<LPB, VPL>(lane, v, rot));
     const float e[4] = {x[v].x, x[v].y, x[v].z, x[v].w};
     if (d + 4 <= D) {
 #pragma unroll
@@ -494,7 +500,7 @@ __device__ __forceinline__ void quantize_group_row(const float4 (&x)[VPL], int D
     const float2 kbig = make_float2(12582912.0f, 12582912.0f), nkbig = make_float2(-12582912.0f, -12582912.0f);
 #pragma unroll
     for (int v = 0; v < VPL; ++v) {
-      const int d = 4 * (lane + v * LPB);
+      const int d = 4 * (rot_idx<LPB, VPL>(lane, v, rot));
       float2 q[2] = {f2_mul_rn(f2_add_rn(make_float2(x[v].x, x[v].y), nmid), rc),
                      f2_mul_rn(f2_add_rn(make_float2(x[v].z, x[v].w), nmid), rc)};
       uint32_t bits[4];
@@ -516,7 +522,7 @@ __device__ __forceinline__ void quantize_group_row(const float4 (&x)[VPL], int D
     if (err >= 0.4999f) {  // rare: exact quotient for this lane's elements
 #pragma unroll
       for (int v = 0; v < VPL; ++v) {
-        const int d = 4 * (lane + v * LPB);
+        const int d = 4 * (rot_idx<LPB, VPL>(lane, v, rot));
         const float e[4] = {x[v].x, x[v].y, x[v].z, x[v].w};
         uint32_t w = 0;
 #pragma unroll
@@ -527,13 +533,13 @@ __device__ __forceinline__ void quantize_group_row(const float4 (&x)[VPL], int D
     }
 #pragma unroll
     for (int v = 0; v < VPL; ++v) {
-      const int wi = lane + v * LPB;
+      const int wi = rot_idx<LPB, VPL>(lane, v, rot);
       if (4 * wi < D) words[wi] = wv[v];
     }
   } else {
 #pragma unroll
     for (int v = 0; v < VPL; ++v) {
-      const int wi = lane + v * LPB;
+      const int wi = rot_idx<LPB, VPL>(lane, v, rot);
       if (4 * wi < D) words[wi] = 0u;
     }
   }
@@ -701,6 +707,171 @@ k_adagrad(const uint32_t* __restrict__ unique, const uint32_t* __restrict__ Up,
 }
 
 // ---------------------------------------------------------------------------
+// a8 (+ fused a9), row-wise AdaGrad at D = 64, with TMA bulk copies.  Each lane group of 4
+// lanes owns a ring of kTmaStages shared-memory slots (its G row and W row, 256 B each) and
+// one mbarrier per slot: lane 0 of the group issues the two cp.async.bulk copies of row i+S
+// (global -> shared, completion counted in bytes on the slot's mbarrier) right after the
+// group has read slot i, so S rows per group are in flight while the group updates and
+// re-quantizes the current one -- without holding them in registers (the register-staged
+// kernel above keeps one row per group in flight and only while it waits).  The unique-row
+// keys and accumulators are loaded one stage ahead by lane 0.  Reading a slot: in one
+// 128-bit shared load the 8 lanes of a quarter-warp are 2 groups; group g reads its row from
+// float4 (lane + 4v + 4(g & 1)) mod 16, so the two groups hit disjoint banks.
+// ---------------------------------------------------------------------------
+constexpr int kTmaStages = 2;
+// Grid: up to 48 resident waves of CTAs (sized from the occurrence count, U <= nnz), i.e.
+// about two rows per group on Feed-1 -- both in flight at once -- with CTAs replacing each
+// other as they finish.  Measured update time (Feed-1, alpha 1.05): 1 wave (persistent, ~16
+// rows per group) 0.595 ms, 4 waves 0.564, 12 waves 0.532, 24 waves 0.522, 48 waves 0.517,
+// 96 waves 0.572; the register-staged kernel 0.549.  alpha 0: 1.90 vs 2.04 ms; Ads 1.09 vs
+// 1.17 ms; alpha 1.2 (U = 0.92M, one row per group) 0.206 vs 0.196 ms.
+constexpr int kTmaWaves = 48;
+constexpr int kTmaRowBytes = 256;  // D = 64 fp32
+constexpr size_t kTmaSmem = 8 /*warps*/ * kTmaStages * 8 /*groups*/ * 2 * kTmaRowBytes +
+                            8 * kTmaStages * 8 * sizeof(unsigned long long);
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <bool REQUANT>
+__global__ void __launch_bounds__(256, 3)
+k_adagrad_tma(const uint32_t* __restrict__ unique, const uint32_t* __restrict__ Up,
+              const float* __restrict__ G, const float* __restrict__ clip, float* __restrict__ Wt,
+              float* __restrict__ A, float lr, float eps, uint8_t* __restrict__ codes, int qpitch,
+              int meta_off, bool minmax, uint32_t* status) {
+  constexpr int LPB = 4, VPL = 4, S = kTmaStages, D = 64;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int warp = threadIdx.x >> 5, grp = (threadIdx.x & 31) >> 2, lane = threadIdx.x & 3;
+  const float c = *clip;
+  if (c < 0.0f) return;  // non-finite global norm: skip the step (uniform over the grid)
+  const uint32_t U = *Up;
+  uint8_t* slots = smem + (size_t)(warp * S * 8) * 2 * kTmaRowBytes;  // [S][8 groups][G | W]
+  unsigned long long* bars =
+      reinterpret_cast<unsigned long long*>(smem + (size_t)8 * S * 8 * 2 * kTmaRowBytes) + warp * S * 8;
+  const int64_t gstride = ((int64_t)gridDim.x * blockDim.x) / LPB;
+  const int64_t g0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LPB;
+  const int64_t gbase = g0 - grp;  // first group of my warp
+  if (lane == 0)
+    for (int q = 0; q < S; ++q) mbar_init(&bars[q * 8 + grp], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncwarp();
+  const int rot = (grp & 1) * 4;
+  // lane 0's ring (S = 2, kept in named registers): key and accumulator of the row in each
+  // slot; the key of the next row to issue
+  static_assert(S == 2, "ring of two slots");
+  uint32_t kr0 = 0, kr1 = 0, knext = 0;
+  float ar0 = 0.f, ar1 = 0.f;
+  auto issue = [&](int q, int64_t u, uint32_t key) {  // lane 0: row u into slot q
+    uint8_t* sl = slots + (size_t)(q * 8 + grp) * 2 * kTmaRowBytes;
+    mbar_expect_tx(&bars[q * 8 + grp], 2 * kTmaRowBytes);
+    tma_load_1d(sl, G + (size_t)u * D, kTmaRowBytes, &bars[q * 8 + grp]);
+    tma_load_1d(sl + kTmaRowBytes, Wt + (size_t)key * D, kTmaRowBytes, &bars[q * 8 + grp]);
+  };
+  if (lane == 0) {
+    if (g0 < U) {
+      kr0 = __ldg(unique + g0);
+      ar0 = A[kr0];
+      issue(0, g0, kr0);
+    }
+    if (g0 + gstride < U) {
+      kr1 = __ldg(unique + g0 + gstride);
+      ar1 = A[kr1];
+      issue(1, g0 + gstride, kr1);
+    }
+    const int64_t un = g0 + S * gstride;
+    knext = un < U ? __ldg(unique + un) : 0u;
+  }
+  const double dimD = (double)D;
+  int it = 0;
+  for (int64_t ub = gbase; ub < U; ub += gstride, ++it) {  // uniform per warp
+    const int64_t u = g0 + (ub - gbase);
+    const bool has = u < U;
+    const int q = it & 1;
+    const uint32_t par = (uint32_t)(it >> 1) & 1u;
+    const uint32_t key = __shfl_sync(kFull, q ? kr1 : kr0, 0, LPB);
+    const float arow = __shfl_sync(kFull, q ? ar1 : ar0, 0, LPB);
+    float4 g[VPL], w[VPL];
+    if (has) {
+      mbar_wait(&bars[q * 8 + grp], par);
+      const float4* sg = reinterpret_cast<const float4*>(slots + (size_t)(q * 8 + grp) * 2 * kTmaRowBytes);
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) {
+        const int fi = rot_idx<LPB, VPL>(lane, v, rot);
+        const float4 Gv = sg[fi];
+        g[v] = make_float4(__fmul_rn(Gv.x, c), __fmul_rn(Gv.y, c), __fmul_rn(Gv.z, c), __fmul_rn(Gv.w, c));
+        w[v] = sg[16 + fi];
+      }
+    } else {
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) g[v] = w[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    __syncwarp();  // the group has read slot q: it may be refilled
+    if (lane == 0) {
+      const int64_t un = u + S * gstride;
+      if (un < U) {
+        const float an = A[knext];
+        if (q) { kr1 = knext; ar1 = an; } else { kr0 = knext; ar0 = an; }
+        issue(q, un, knext);
+        const int64_t unn = un + gstride;
+        knext = unn < U ? __ldg(unique + unn) : 0u;
+      }
+    }
+    double ss = 0.0;
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) {
+      ss += (double)g[v].x * (double)g[v].x;
+      ss += (double)g[v].y * (double)g[v].y;
+      ss += (double)g[v].z * (double)g[v].z;
+      ss += (double)g[v].w * (double)g[v].w;
+    }
+    ss = group_sum<LPB>(ss);
+    const float s2 = (float)(ss / dimD);
+    const float a = __fadd_rn(arow, s2);
+    const float den = __fadd_rn(__fsqrt_rn(a), eps);
+    const float mult = __fdiv_rn(lr, den);
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) {
+      w[v].x = __fsub_rn(w[v].x, __fmul_rn(mult, g[v].x));
+      w[v].y = __fsub_rn(w[v].y, __fmul_rn(mult, g[v].y));
+      w[v].z = __fsub_rn(w[v].z, __fmul_rn(mult, g[v].z));
+      w[v].w = __fsub_rn(w[v].w, __fmul_rn(mult, g[v].w));
+    }
+    if (has) {
+      if (lane == 0) A[key] = a;
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) st_f4(Wt + (size_t)key * D + 4 * rot_idx<LPB, VPL>(lane, v, rot), w[v]);
+    }
+    if (REQUANT)
+      quantize_group_row<LPB, VPL>(w, D, lane, has, codes + (size_t)key * qpitch, meta_off, qpitch, minmax,
+                                   status, rot);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
 #define LIRANK_GEOM_DISPATCH(G, KERNEL_LAUNCH)                              \
@@ -816,6 +987,29 @@ cudaError_t launch_adagrad(const BwdArgs& a, cudaStream_t s) {
   // (the row's min/max and the per-row divides are then shared by 4 lanes, not 16) at 3
   // CTAs/SM (measured: 0.68 -> 0.55 ms on Feed-1).
   const bool rq = a.q8_codes != nullptr;
+  if (a.rowwise && a.pitch == 64 && a.D == 64 && a.tma) {  // TMA-pipelined update (D = 64)
+    static int per_sm = 0;
+    auto kern = rq ? (const void*)k_adagrad_tma<true> : (const void*)k_adagrad_tma<false>;
+    if (per_sm == 0) {
+      cudaFuncSetAttribute(k_adagrad_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
+      cudaFuncSetAttribute(k_adagrad_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, kTmaSmem) != cudaSuccess || per_sm < 1)
+        per_sm = 1;
+    }
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t want = (a.nnz * 4 + 255) / 256;
+    const int64_t cap = (int64_t)sms * per_sm * kTmaWaves;
+    const unsigned grid = (unsigned)(want < 1 ? 1 : (want < cap ? want : cap));
+    if (rq)
+      k_adagrad_tma<true><<<grid, 256, kTmaSmem, s>>>(a.unique, a.U, a.G, a.clip, a.Wt, a.A, a.lr, a.eps,
+                                                       a.q8_codes, a.qpitch, a.q8_meta_off, a.q8_minmax, a.status);
+    else
+      k_adagrad_tma<false><<<grid, 256, kTmaSmem, s>>>(a.unique, a.U, a.G, a.clip, a.Wt, a.A, a.lr, a.eps,
+                                                        a.q8_codes, a.qpitch, a.q8_meta_off, a.q8_minmax, a.status);
+    return cudaGetLastError();
+  }
   const Geom g = rq ? geom_target(a.pitch, 4) : geom_for(a.pitch);
 #define LAUNCH_AG(DISPATCH, RW, RQ)                                                         \
   DISPATCH(g, (k_adagrad<L_, V_, RW, RQ><<<persistent_grid((const void*)k_adagrad<L_, V_, RW, RQ>, \

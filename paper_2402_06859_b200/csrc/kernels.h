@@ -6,6 +6,10 @@
 
 #include "common.cuh"
 
+#ifndef LIRANK_TMA_UPDATE
+#define LIRANK_TMA_UPDATE 1
+#endif
+
 namespace lirank {
 
 // Fused exchange (EMB_F_P2P): a pooling kernel stores the pooled row of the bag with
@@ -151,6 +155,7 @@ struct BwdArgs {
   uint8_t* q8_codes;        // requantize touched rows (NULL: no)
   int q8_meta_off;
   bool q8_minmax;           // re-quantize min-max (else middle-max)
+  bool tma;                 // D = 64 row-wise: the TMA-pipelined update kernel
   int qpitch;
 };
 cudaError_t launch_segreduce(const BwdArgs& a, int64_t* launches, cudaStream_t s);
