@@ -43,15 +43,39 @@ __global__ void __launch_bounds__(256) k_ldg(const uint8_t* __restrict__ tab, co
   if (acc == 12345.f) out[0] = acc;
 }
 
+// 256-B rows (a2's fp32 D = 64 row): 8 lanes x 2 x 16 B, UNR rows in flight per group
+template <int UNR>
+__global__ void __launch_bounds__(256) k_ldg256(const uint8_t* __restrict__ tab, const uint32_t* __restrict__ ids,
+                                                int64_t n, float* out) {
+  const int lane = threadIdx.x & 7;
+  const int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 8;
+  const int64_t G = (gridDim.x * (int64_t)blockDim.x) / 8;
+  float acc = 0.f;
+  for (int64_t i = g * UNR; i < n; i += G * UNR) {
+    float4 r[UNR][2];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const float4* row = reinterpret_cast<const float4*>(tab + (size_t)__ldg(ids + min(i + u, n - 1)) * 256);
+#pragma unroll
+      for (int v = 0; v < 2; ++v)
+        asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                     : "=f"(r[u][v].x), "=f"(r[u][v].y), "=f"(r[u][v].z), "=f"(r[u][v].w) : "l"(row + lane + 8 * v));
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) acc += r[u][0].x + r[u][1].y + r[u][0].z + r[u][1].w;
+  }
+  if (acc == 12345.f) out[0] = acc;
+}
+
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
-template <int S>
+template <int S, int RB = 96>
 __global__ void __launch_bounds__(256) k_tma(const uint8_t* __restrict__ tab, const uint32_t* __restrict__ ids,
                                              int64_t n, float* out) {
   extern __shared__ __align__(128) uint8_t sm[];
   const int grp = threadIdx.x >> 2, lane = threadIdx.x & 3;  // 64 groups per CTA
-  uint8_t* slots = sm + (size_t)grp * S * 96;
-  unsigned long long* bars = reinterpret_cast<unsigned long long*>(sm + 64 * S * 96) + grp * S;
+  uint8_t* slots = sm + (size_t)grp * S * RB;
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(sm + 64 * S * RB) + grp * S;
   const int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 4;
   const int64_t G = (gridDim.x * (int64_t)blockDim.x) / 4;
   if (lane == 0)
@@ -59,10 +83,10 @@ __global__ void __launch_bounds__(256) k_tma(const uint8_t* __restrict__ tab, co
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncwarp();
   auto issue = [&](int q, int64_t i) {
-    const uint8_t* src = tab + (size_t)__ldg(ids + i) * 96;
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], 96;" ::"r"(su32(&bars[q])) : "memory");
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 96, [%2];" ::"r"(
-                     su32(slots + q * 96)), "l"(src), "r"(su32(&bars[q])) : "memory");
+    const uint8_t* src = tab + (size_t)__ldg(ids + i) * RB;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&bars[q])), "n"(RB) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     su32(slots + q * RB)), "l"(src), "n"(RB), "r"(su32(&bars[q])) : "memory");
   };
   if (lane == 0)
     for (int q = 0; q < S; ++q)
@@ -74,8 +98,8 @@ __global__ void __launch_bounds__(256) k_tma(const uint8_t* __restrict__ tab, co
     const uint32_t par = (it / S) & 1;
     asm volatile("{\n\t.reg .pred p;\nW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra W_%=;\n}" ::"r"(
                      su32(&bars[q])), "r"(par) : "memory");
-    const uint4 r = reinterpret_cast<const uint4*>(slots + q * 96)[lane];
-    const float2 m = *reinterpret_cast<const float2*>(slots + q * 96 + 64);
+    const uint4 r = reinterpret_cast<const uint4*>(slots + q * RB)[lane];
+    const float2 m = *reinterpret_cast<const float2*>(slots + q * RB + 64);
     __syncwarp(0xfu << (threadIdx.x & 28));
     if (lane == 0 && i + S * G < n) issue(q, i + S * G);
     acc += (float)(r.x ^ r.y ^ r.z ^ r.w) * m.x + m.y;
@@ -110,5 +134,24 @@ int main() {
     timeit(nm, [&] { k_tma<S><<<148 * per * CTAS, 256, smem>>>(tab, ids, n, out); });                \
   }
   T(2, 1) T(4, 1) T(8, 1) T(4, 8) T(8, 8) T(16, 1)
+  // 256-B rows from a 32 GB table (a2's fp32 rows)
+  uint8_t* tab2 = nullptr;
+  const uint64_t rows2 = 125000000;
+  cudaFree(tab);
+  if (cudaMalloc(&tab2, rows2 * 256) == cudaSuccess) {
+    cudaMemset(tab2, 1, rows2 * 256);
+    k_ids<<<1184, 256>>>(ids, n, rows2, 9);
+    timeit("256B ldg UNR=2 (a2 scheme)", [&] { k_ldg256<2><<<148 * 5 * 4, 256>>>(tab2, ids, n, out); });
+    timeit("256B ldg UNR=4", [&] { k_ldg256<4><<<148 * 4 * 4, 256>>>(tab2, ids, n, out); });
+#define T2(S)                                                                                        \
+  {                                                                                                  \
+    const int smem = 64 * S * 256 + 64 * S * 8;                                                      \
+    cudaFuncSetAttribute(k_tma<S, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);          \
+    int per = 0; cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_tma<S, 256>, 256, smem);      \
+    char nm[64]; snprintf(nm, 64, "256B tma S=%d (%d CTA/SM)", S, per);                              \
+    timeit(nm, [&] { k_tma<S, 256><<<148 * per, 256, smem>>>(tab2, ids, n, out); });                 \
+  }
+    T2(2) T2(4) T2(6)
+  }
   printf("err %s\n", cudaGetErrorString(cudaGetLastError()));
 }
