@@ -48,15 +48,16 @@ __device__ __forceinline__ double group_sum(double x) {
   return x;
 }
 
+// (the pooled-gradient rows are re-read once per id of their bag: kept in L2 with evict_last)
 template <int VPL>
 __device__ __forceinline__ void load_grad_row(const float* __restrict__ grad, size_t row_off,
                                               int D, int lane, int LPB, float4 (&r)[VPL]) {
+  const uint64_t pol = l2_policy_last();
 #pragma unroll
   for (int v = 0; v < VPL; ++v) {
     const int d = 4 * (lane + v * LPB);
     if ((D & 3) == 0) {
-      r[v] = d < D ? __ldg(reinterpret_cast<const float4*>(grad + row_off + d))
-                   : make_float4(0.f, 0.f, 0.f, 0.f);
+      r[v] = d < D ? ld_nc_f4_hint(grad + row_off + d, pol) : make_float4(0.f, 0.f, 0.f, 0.f);
     } else {
       r[v].x = d + 0 < D ? __ldg(grad + row_off + d + 0) : 0.f;
       r[v].y = d + 1 < D ? __ldg(grad + row_off + d + 1) : 0.f;
@@ -86,7 +87,7 @@ __device__ __forceinline__ double write_G(float* G, int pitch, uint32_t u, int l
     if (vi < nvec) {
       float4 g = make_float4((float)acc[v][0], (float)acc[v][1], (float)acc[v][2],
                              (float)acc[v][3]);
-      st_f4(G + (size_t)u * pitch + 4 * vi, g);
+      st_f4_hint(G + (size_t)u * pitch + 4 * vi, g, l2_policy_first());  // G: streamed to a8
       nrm += (double)g.x * (double)g.x;
       nrm += (double)g.y * (double)g.y;
       nrm += (double)g.z * (double)g.z;

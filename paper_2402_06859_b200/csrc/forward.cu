@@ -96,6 +96,7 @@ k_pool_fwd_f32(const float* __restrict__ W, int pitch, const int* __restrict__ i
   const FeatMeta m = meta[f];
   const int nvec = pitch >> 2;
   const uint32_t grow = (uint32_t)out_row(f, b, B, Fb);
+  const uint64_t pol_last = l2_policy_last();
   float4 acc[VPL];
 #pragma unroll
   for (int v = 0; v < VPL; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -134,7 +135,7 @@ k_pool_fwd_f32(const float* __restrict__ W, int pitch, const int* __restrict__ i
 #pragma unroll
           for (int v = 0; v < VPL; ++v) {
             const int vi = lane + v * LPB;
-            r[u][v] = vi < nvec ? ld_nc_f4(row + 4 * vi) : make_float4(0.f, 0.f, 0.f, 0.f);
+            r[u][v] = vi < nvec ? ld_nc_f4_hint(row + 4 * vi, pol_last) : make_float4(0.f, 0.f, 0.f, 0.f);
           }
         }
       }
@@ -151,8 +152,15 @@ k_pool_fwd_f32(const float* __restrict__ W, int pitch, const int* __restrict__ i
   if (PEER && pm.skip_empty && len == 0) return;
   if (MEAN) mean_div(acc, len);
   float* o = dst_row<PEER>(out, grow, B, Fb, D, pm);
+  if ((D & 3) == 0) {
+    const uint64_t pol_first = l2_policy_first();
 #pragma unroll
-  for (int v = 0; v < VPL; ++v) store4(o, 4 * (lane + v * LPB), D, acc[v]);
+    for (int v = 0; v < VPL; ++v)
+      if (4 * (lane + v * LPB) < D) st_f4_hint(o + 4 * (lane + v * LPB), acc[v], pol_first);
+  } else {
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) store4(o, 4 * (lane + v * LPB), D, acc[v]);
+  }
 }
 
 // Bags of at most one id (one-hot features, empty bags).  The main kernel gives each bag a
@@ -246,6 +254,12 @@ __device__ __forceinline__ float4 deq4_add(float4 acc, uint32_t w, float scale, 
   const float2 a23 = f2_add_rn(make_float2(acc.z, acc.w), f2_fma_rn(c23, sc, md));
   return make_float4(a01.x, a01.y, a23.x, a23.y);
 }
+__device__ __forceinline__ uint4 ld_nc_u4_hint(const void* p, uint64_t pol) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p), "l"(pol));
+  return r;
+}
 __device__ __forceinline__ uint4 ld_nc_u4(const void* p) {
   uint4 r;
   asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -283,6 +297,7 @@ k_pool_fwd_q8(const uint8_t* __restrict__ codes, int qpitch, int meta_off,
   const int b = live ? (int)(bag - (long long)f * B) : 0;
   const FeatMeta m = meta[f];
   const int nv16 = (D + 15) >> 4;  // 16-code vectors carrying dims < D
+  const uint64_t pol_last = l2_policy_last();  // q8 rows: Zipf-hot, keep in L2
   float4 acc[4 * VPL];
 #pragma unroll
   for (int v = 0; v < 4 * VPL; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -311,7 +326,7 @@ k_pool_fwd_q8(const uint8_t* __restrict__ codes, int qpitch, int meta_off,
 #pragma unroll
           for (int v = 0; v < VPL; ++v) {
             const int vi = lane + v * LPB;
-            w[u][v] = vi < nv16 ? ld_nc_u4(row + 16 * vi) : make_uint4(0u, 0u, 0u, 0u);
+            w[u][v] = vi < nv16 ? ld_nc_u4_hint(row + 16 * vi, pol_last) : make_uint4(0u, 0u, 0u, 0u);
           }
         }
       }
@@ -339,7 +354,15 @@ k_pool_fwd_q8(const uint8_t* __restrict__ codes, int qpitch, int meta_off,
   for (int v = 0; v < VPL; ++v) {
     const int d = 16 * (lane + v * LPB);
 #pragma unroll
-    for (int h = 0; h < 4; ++h) store4(o, d + 4 * h, D, acc[4 * v + h]);
+    if ((D & 3) == 0) {
+      const uint64_t pol_first = l2_policy_first();  // outputs: written once
+#pragma unroll
+      for (int h = 0; h < 4; ++h)
+        if (d + 4 * h < D) st_f4_hint(o + d + 4 * h, acc[4 * v + h], pol_first);
+    } else {
+#pragma unroll
+      for (int h = 0; h < 4; ++h) store4(o, d + 4 * h, D, acc[4 * v + h]);
+    }
   }
 }
 
