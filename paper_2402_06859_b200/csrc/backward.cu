@@ -770,6 +770,9 @@ k_adagrad_tma(const uint32_t* __restrict__ unique, const uint32_t* __restrict__ 
   const float c = *clip;
   if (c < 0.0f) return;  // non-finite global norm: skip the step (uniform over the grid)
   const uint32_t U = *Up;
+  // the grid is sized from the occurrence count (U is only known on the device): CTAs past
+  // the unique rows leave before setting anything up
+  if ((int64_t)blockIdx.x * (blockDim.x / 4) >= (int64_t)U) return;
   uint8_t* slots = smem + (size_t)(warp * S * 8) * 2 * kTmaRowBytes;  // [S][8 groups][G | W]
   unsigned long long* bars =
       reinterpret_cast<unsigned long long*>(smem + (size_t)8 * S * 8 * 2 * kTmaRowBytes) + warp * S * 8;
