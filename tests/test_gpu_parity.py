@@ -384,7 +384,7 @@ def test_requant_tracks_updates(gpu, mode, pooling, dim):
 # full-size configs (the bench's launch configuration)
 # ---------------------------------------------------------------------------
 
-@pytest.mark.parametrize("name", ["jobs", "feed1", "feed1@alpha0"])
+@pytest.mark.parametrize("name", ["jobs", "feed1", "feed1@alpha0", "ads"])
 def test_full_config_train_step(gpu, name):
     """The bench's launch configuration at full size (Feed-1 also with uniform ids, the
     alpha = 0 variant of SURVEY §8(d)'s gate: ~5x more unique rows, shorter segments)."""
@@ -434,11 +434,26 @@ def test_full_config_train_step(gpu, name):
         assert w_close(w, W[m], comp.W[m], np.abs(W[m] - comp.W[m])).all()
     # q8 of the updated table on a sample of rows
     emb.quantize()
-    rows = rng.choice(cfg.table_rows[0], 5000, replace=False)
-    c, mm, ss = emb.read_q8(0, rows)
-    w = emb.read_rows(0, rows, with_acc=False)
+    tq = int(np.argmax(cfg.table_rows))
+    rows = rng.choice(cfg.table_rows[tq], min(5000, cfg.table_rows[tq]), replace=False)
+    c, mm, ss = emb.read_q8(tq, rows)
+    w = emb.read_rows(tq, rows, with_acc=False)
     codes, mid, sc, _ = O.quantize(w)
     assert (c == codes).all() and (mm == mid).all() and (ss == sc).all()
+    # a10 at full size: the q8 lookup of the same batch on the sampled samples, against the
+    # oracle's lookup over the oracle's quantization of the (GPU-updated) compact rows
+    q8 = emb.forward_q8(dev(ids), dev(off), B).cpu().numpy()[samples]
+    assert emb.sync() == 0
+    skeys = np.unique(sids[sids >= 0]) if len(sids) else np.zeros(0, np.int64)
+    Wq = np.zeros_like(comp.W)
+    for t in np.unique(comp.table_of_key[skeys]):
+        m = skeys[comp.table_of_key[skeys] == t]
+        Wq[m] = emb.read_rows(int(t), comp.row_of_key[m], with_acc=False)
+    qc, qm, qs, _ = O.quantize(Wq)
+    ref_q8, _ = O.forward_q8(comp.pb, qc, qm, qs, sids, soff, len(samples))
+    deq = np.abs(qm.astype(np.float64))[:, None] + np.abs(qc.astype(np.float64) * qs[:, None])
+    mag, _ = O.forward(comp.pb, deq.astype(np.float32), sids, soff, len(samples))
+    assert cond_close(q8, ref_q8, mag).all()
 
 
 def test_q8_reuses_bag_order_of_a_different_batch(gpu):
