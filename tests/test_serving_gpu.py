@@ -65,3 +65,45 @@ def test_quantize_block_equals_full_quantize(gpu):
     ca, ma, sa = a.read_q8(0, np.arange(3000))
     cb, mb, sb = b.read_q8(0, np.arange(3000))
     assert (ca == cb).all() and (ma == mb).all() and (sa == sb).all()
+
+
+@pytest.mark.timeout(900)
+def test_serving_full_size_feedq8(gpu):
+    """BASELINE config 5 at full size, in the bench's launch configuration: the 1B-row Feed
+    tables as one middle-max q8 replica (96 GB) filled block by block from the GPU generator,
+    one a10 lookup of the whole B = 262,144 batch; sampled samples (all features) must equal
+    the oracle's lookup over the oracle's quantization of the same rows, bit for bit."""
+    from helpers import Compact, sample_bags
+    from workload import configs
+    from workload import gpu as G
+    cfg = configs.get("feedq8")
+    B, D = cfg.batch, cfg.dim
+    ids, off = gen.make_batch(cfg.table_rows, cfg.features, B, cfg.seed, 0, alpha=cfg.alpha)
+    emb = make_emb(cfg, max_nnz=len(ids), max_batch=B, q8_only=True)
+    chunk = 1 << 25
+    blk = torch.empty(chunk * D, device=gpu)
+    for t, rows in enumerate(cfg.table_rows):
+        r = 0
+        while r < rows:
+            n = min(chunk, rows - r)
+            v = blk[: n * D].view(n, D)
+            G.fill_table(v, n, D, D, cfg.seed, t, row0=r)
+            emb.quantize_block(t, r, v)
+            r += n
+    del blk
+    out = emb.forward_q8(dev(ids), dev(off), B).cpu().numpy()
+    assert emb.sync() == 0
+    rng = np.random.default_rng(3)
+    samples = np.sort(rng.choice(B, 64, replace=False))
+    sids, soff = sample_bags(cfg, ids, off, B, samples)
+    comp = Compact(cfg, sids, soff, len(samples))
+    codes, mid, sc, _ = O.quantize(comp.W)
+    ref, _ = O.forward_q8(comp.pb, codes, mid, sc, comp.cids, soff, len(samples))
+    assert (out[samples] == ref).all()
+    # and the stored q8 rows of a sample of touched keys equal the oracle's quantization
+    pick = rng.choice(len(comp.keys), min(500, len(comp.keys)), replace=False)
+    for t in np.unique(comp.table_of_key[pick]):
+        m = pick[comp.table_of_key[pick] == t]
+        c, mm, ss = emb.read_q8(int(t), comp.row_of_key[m])
+        assert (c == codes[m]).all() and (mm == mid[m]).all() and (ss == sc[m]).all()
+    emb.close()
