@@ -791,6 +791,9 @@ k_adagrad_tma(const uint32_t* __restrict__ unique, const uint32_t* __restrict__ 
   float ar0 = 0.f, ar1 = 0.f;
   auto issue = [&](int q, int64_t u, uint32_t key) {  // lane 0: row u into slot q
     uint8_t* sl = slots + (size_t)(q * 8 + grp) * 2 * kTmaRowBytes;
+    // the group's generic-proxy reads of this slot (ordered before by __syncwarp) before the
+    // async-proxy (TMA) writes that refill it
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     mbar_expect_tx(&bars[q * 8 + grp], 2 * kTmaRowBytes);
     tma_load_1d(sl, G + (size_t)u * D, kTmaRowBytes, &bars[q * 8 + grp]);
     tma_load_1d(sl + kTmaRowBytes, Wt + (size_t)key * D, kTmaRowBytes, &bars[q * 8 + grp]);
