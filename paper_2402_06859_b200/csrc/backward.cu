@@ -245,6 +245,7 @@ k_fixup_short(const uint32_t* __restrict__ seg, const uint32_t* __restrict__ Up,
               const double* __restrict__ part_last, const uint32_t* __restrict__ owner_list,
               const uint32_t* __restrict__ owner_count, float* __restrict__ G,
               double* __restrict__ norm_fix, uint32_t* long_list, uint32_t* long_count) {
+  pdl_wait();
   constexpr int GPW = 32 / LPB;  // groups per warp
   const int lane = threadIdx.x & (LPB - 1);
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;  // global warp
@@ -303,6 +304,7 @@ k_fixup_long(const uint32_t* __restrict__ seg, int pitch, const double* __restri
              const double* __restrict__ part_last, const uint32_t* __restrict__ long_list,
              const uint32_t* __restrict__ long_count, float* __restrict__ G,
              double* __restrict__ norm_fix) {
+  pdl_wait();
   extern __shared__ double sm[];  // [max(nsplit * pitch, kFixThreads)]
   const uint32_t n_entries = *long_count;
   const int nsplit = max(1, kFixThreads / pitch);
@@ -356,6 +358,7 @@ constexpr int kNormParts = 64;
 __global__ void __launch_bounds__(256)
 k_norm_partial(const double* __restrict__ norm_main, const double* __restrict__ norm_fix,
                int64_t chunks, double* __restrict__ parts, uint32_t* done, double* S_local) {
+  pdl_wait();
   __shared__ double sm[256];
   __shared__ bool last;
   const int64_t per = (chunks + gridDim.x - 1) / gridDim.x;
@@ -391,6 +394,7 @@ k_norm_partial(const double* __restrict__ norm_main, const double* __restrict__ 
 __global__ void k_norm_finalize(const double* parts, int nparts, double extra,
                                 const double* extra_dev, float max_norm, double* S_global,
                                 float* clip, float* clip_out, uint32_t* status) {
+  pdl_wait();
   double S = 0.0;
   for (int r = 0; r < nparts; ++r) S += parts[r];
   S += extra;
@@ -766,6 +770,7 @@ k_adagrad_tma(const uint32_t* __restrict__ unique, const uint32_t* __restrict__ 
               int meta_off, bool minmax, uint32_t* status) {
   constexpr int LPB = 4, VPL = 4, S = kTmaStages, D = 64;
   extern __shared__ __align__(128) uint8_t smem[];
+  pdl_wait();
   const int warp = threadIdx.x >> 5, grp = (threadIdx.x & 31) >> 2, lane = threadIdx.x & 3;
   const float c = *clip;
   if (c < 0.0f) return;  // non-finite global norm: skip the step (uniform over the grid)
@@ -961,14 +966,14 @@ cudaError_t launch_segreduce(const BwdArgs& a, int64_t* launches, cudaStream_t s
   ++*launches;
   uint32_t* long_count = a.owner_count + 1;
   uint32_t* long_list = a.owner_list + a.chunks;  // [2 * chunks] after the owner list
-  LIRANK_GEOM2_DISPATCH(g, (k_fixup_short<L_, V_><<<persistent_grid((const void*)k_fixup_short<L_, V_>, a.chunks, L_), 256, 0, s>>>(
+  LIRANK_GEOM2_DISPATCH(g, (launch_pdl(k_fixup_short<L_, V_>, persistent_grid((const void*)k_fixup_short<L_, V_>, a.chunks, L_), 256, 0, s,
                               a.seg, a.U, a.chunk_u0, a.pitch, a.part_first, a.part_last,
                               a.owner_list, a.owner_count, a.G, a.norm_fix, long_list, long_count)));
   ++*launches;
   const int nsplit = a.pitch < kFixThreads ? kFixThreads / a.pitch : 1;
   const size_t smem = sizeof(double) * (size_t)(nsplit * a.pitch > kFixThreads ? nsplit * a.pitch : kFixThreads);
-  k_fixup_long<<<148, kFixThreads, smem, s>>>(a.seg, a.pitch, a.part_first, a.part_last,
-                                              long_list, long_count, a.G, a.norm_fix);
+  launch_pdl(k_fixup_long, 148, kFixThreads, smem, s, a.seg, a.pitch, a.part_first, a.part_last,
+             long_list, long_count, a.G, a.norm_fix);
   ++*launches;
   return cudaGetLastError();
 }
@@ -976,15 +981,15 @@ cudaError_t launch_segreduce(const BwdArgs& a, int64_t* launches, cudaStream_t s
 cudaError_t launch_norm_partial(const BwdArgs& a, cudaStream_t s) {
   const int64_t want = (a.chunks + 1023) / 1024;
   const unsigned grid = (unsigned)(want < 1 ? 1 : (want < kNormParts ? want : kNormParts));
-  k_norm_partial<<<grid, 256, 0, s>>>(a.norm_main, a.norm_fix, a.chunks, a.norm_parts,
-                                      a.norm_done, a.S_local);
+  launch_pdl(k_norm_partial, grid, 256, 0, s, a.norm_main, a.norm_fix, a.chunks, a.norm_parts,
+             a.norm_done, a.S_local);
   return cudaGetLastError();
 }
 
 cudaError_t launch_norm_finalize(const double* parts, int nparts, const BwdArgs& a,
                                  cudaStream_t s) {
-  k_norm_finalize<<<1, 1, 0, s>>>(parts, nparts, a.extra_sq_norm, a.extra_dev, a.max_norm,
-                                  a.S_global, a.clip, a.clip_out, a.status);
+  launch_pdl(k_norm_finalize, 1, 1, 0, s, parts, nparts, a.extra_sq_norm, a.extra_dev, a.max_norm,
+             a.S_global, a.clip, a.clip_out, a.status);
   return cudaGetLastError();
 }
 
@@ -1010,11 +1015,11 @@ cudaError_t launch_adagrad(const BwdArgs& a, cudaStream_t s) {
     const int64_t cap = (int64_t)sms * per_sm * kTmaWaves;
     const unsigned grid = (unsigned)(want < 1 ? 1 : (want < cap ? want : cap));
     if (rq)
-      k_adagrad_tma<true><<<grid, 256, kTmaSmem, s>>>(a.unique, a.U, a.G, a.clip, a.Wt, a.A, a.lr, a.eps,
-                                                       a.q8_codes, a.qpitch, a.q8_meta_off, a.q8_minmax, a.status);
+      launch_pdl(k_adagrad_tma<true>, grid, 256, kTmaSmem, s, a.unique, a.U, a.G, a.clip, a.Wt, a.A, a.lr,
+                 a.eps, a.q8_codes, a.qpitch, a.q8_meta_off, a.q8_minmax, a.status);
     else
-      k_adagrad_tma<false><<<grid, 256, kTmaSmem, s>>>(a.unique, a.U, a.G, a.clip, a.Wt, a.A, a.lr, a.eps,
-                                                        a.q8_codes, a.qpitch, a.q8_meta_off, a.q8_minmax, a.status);
+      launch_pdl(k_adagrad_tma<false>, grid, 256, kTmaSmem, s, a.unique, a.U, a.G, a.clip, a.Wt, a.A, a.lr,
+                 a.eps, a.q8_codes, a.qpitch, a.q8_meta_off, a.q8_minmax, a.status);
     return cudaGetLastError();
   }
   const Geom g = rq ? geom_target(a.pitch, 4) : geom_for(a.pitch);

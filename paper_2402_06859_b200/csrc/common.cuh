@@ -136,6 +136,29 @@ __device__ __forceinline__ float4 f4_add_rn(float4 a, float4 b) {
   return make_float4(lo.x, lo.y, hi.x, hi.y);
 }
 
+// Programmatic dependent launch: a kernel launched with launch_pdl may be scheduled while its
+// stream predecessor drains (its CTAs take SM slots as the predecessor's retire, instead of a
+// full drain + launch gap); pdl_wait() -- its first statement -- blocks until the predecessor
+// has completed and its memory is visible, so nothing before it may read predecessor output.
+// In a kernel launched normally pdl_wait() returns at once.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+static inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                                     cudaStream_t s, Args... args) {
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
 __device__ __forceinline__ void set_status(uint32_t* st, uint32_t bit) {
   // Rare path; one atomic per offending warp is plenty.
   atomicOr(st, bit);

@@ -83,6 +83,7 @@ k_pool_fwd_f32(const float* __restrict__ W, int pitch, const int* __restrict__ i
                const FeatMeta* __restrict__ meta, float* __restrict__ out,
                uint2* __restrict__ kv_out, uint32_t sentinel, uint32_t* status,
               const uint32_t* __restrict__ order, bool skip_short, const PeerOut pm) {
+  pdl_wait();
   constexpr int UNR = (VPL == 1) ? 4 : (VPL == 2 ? 2 : 1);
   constexpr unsigned kFull = 0xffffffffu;
   const int lane = threadIdx.x & (LPB - 1);
@@ -180,6 +181,7 @@ k_pool_short_f32(const float* __restrict__ W, int pitch, const int* __restrict__
                  const FeatMeta* __restrict__ meta, float* __restrict__ out,
                  uint2* __restrict__ kv_out, uint32_t sentinel, uint32_t* status,
                  const uint32_t* __restrict__ order, const PeerOut pm) {
+  pdl_wait();
   constexpr int UNR = VPL >= 4 ? 2 : 4;
   constexpr unsigned kFull = 0xffffffffu;
   const int lane = threadIdx.x & (LPB - 1);
@@ -286,6 +288,7 @@ k_pool_fwd_q8(const uint8_t* __restrict__ codes, int qpitch, int meta_off,
               uint32_t* status,
               const uint32_t* __restrict__ order, uint32_t xmask, float magic, bool skip_short,
               const PeerOut pm) {
+  pdl_wait();
   constexpr int UNR = (VPL == 1) ? 4 : 2;
   constexpr uint32_t kNone = 0xffffffffu;
   constexpr unsigned kFull = 0xffffffffu;
@@ -399,6 +402,7 @@ k_len_hist(const int* __restrict__ offsets, long long nbags, uint32_t* __restric
 __global__ void __launch_bounds__(256)
 k_len_scatter(const int* __restrict__ offsets, long long nbags, const uint32_t* __restrict__ hist,
               uint32_t* __restrict__ cursor, uint32_t* __restrict__ order) {
+  pdl_wait();
   __shared__ uint32_t h[kLenBins], base[kLenBins], start[kLenBins];
   const long long per = (nbags + gridDim.x - 1) / gridDim.x;
   const long long b0 = (long long)blockIdx.x * per;
@@ -431,7 +435,7 @@ static const uint32_t* bag_order(const int* offsets, long long bags, uint32_t* w
   const long long want = (bags + 255) / 256;
   const unsigned grid = (unsigned)(want < 148 * 4 ? want : 148 * 4);
   k_len_hist<<<grid, 256, 0, s>>>(offsets, bags, hist);
-  k_len_scatter<<<grid, 256, 0, s>>>(offsets, bags, hist, cursor, ws);
+  launch_pdl(k_len_scatter, grid, 256, 0, s, offsets, bags, (const uint32_t*)hist, cursor, ws);
   return ws;
 }
 
@@ -486,7 +490,7 @@ cudaError_t launch_pool_fwd_f32(const FwdArgs& a, cudaStream_t s) {
   const bool split = order != nullptr;  // short bags sit at the end of the ordered positions
   const bool peer = a.peer.base[0] != nullptr;  // fused exchange (sharded: SUM, recording)
 #define LAUNCH_F32(MEAN, EMIT, PEER)                                                       \
-  LIRANK_FWD_GEOM_DISPATCH(g, (k_pool_fwd_f32<L_, V_, MEAN, EMIT, PEER><<<grid, 256, 0, s>>>( \
+  LIRANK_FWD_GEOM_DISPATCH(g, (launch_pdl(k_pool_fwd_f32<L_, V_, MEAN, EMIT, PEER>, grid, 256, 0, s, \
                               a.W, a.pitch, a.ids, a.offsets, a.B, a.F, Fb, a.D, a.meta,    \
                               a.out, a.kv_out, a.sentinel, a.status, order, split, a.peer)))
   if (peer) {
@@ -501,7 +505,7 @@ cudaError_t launch_pool_fwd_f32(const FwdArgs& a, cudaStream_t s) {
   if (split) {
     const unsigned sgrid = (unsigned)(((bags + g.lpb - 1) / g.lpb * g.lpb + 255) / 256);
 #define LAUNCH_SHORT(EMIT, PEER)                                                             \
-  LIRANK_FWD_GEOM_DISPATCH(g, (k_pool_short_f32<L_, V_, EMIT, PEER><<<sgrid, 256, 0, s>>>(    \
+  LIRANK_FWD_GEOM_DISPATCH(g, (launch_pdl(k_pool_short_f32<L_, V_, EMIT, PEER>, sgrid, 256, 0, s, \
                               a.W, a.pitch, a.ids, a.offsets, a.B, a.F, Fb, a.D, a.meta,    \
                               a.out, a.kv_out, a.sentinel, a.status, order, a.peer)))
     if (peer) LAUNCH_SHORT(true, true);
@@ -528,7 +532,7 @@ cudaError_t launch_pool_fwd_q8(const FwdQ8Args& a, cudaStream_t s) {
   // (no short-bag split here: a k_pool_short_f32-style q8 kernel measured slower -- Ads a10
   // 3.24 -> 3.79 ms -- the q8 groups already hold 8 bags per warp)
 #define LAUNCH_Q8(MEAN, PEER)                                                              \
-  LIRANK_GEOM_DISPATCH(g, (k_pool_fwd_q8<L_, V_, MEAN, PEER><<<grid, 256, 0, s>>>(         \
+  LIRANK_GEOM_DISPATCH(g, (launch_pdl(k_pool_fwd_q8<L_, V_, MEAN, PEER>, grid, 256, 0, s,   \
                               a.codes, a.qpitch, a.meta_off, a.ids, a.offsets, a.B, a.F, Fb, \
                               a.D, a.meta, a.out, a.status, order, xmask, magic, false, a.peer)))
   if (a.peer.base[0] != nullptr) {
