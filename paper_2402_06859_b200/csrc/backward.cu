@@ -124,6 +124,7 @@ k_segreduce(const uint32_t* __restrict__ seg, const uint32_t* __restrict__ Up,
             double* __restrict__ part_last, double* __restrict__ norm_main,
             double* __restrict__ norm_fix, uint32_t* __restrict__ owner_list,
             uint32_t* owner_count) {
+  pdl_wait();
   // rows in flight per group: D=64 (VPL 2) measured best at 2 with 4 CTAs/SM (64 registers:
   // 0.78 -> 0.72 ms on Feed-1; 1 -> 0.74, 4 -> 0.78 at 80 registers, 8 -> 1.5); key-derived
   // segment heads then took it to 0.69 ms)
@@ -561,6 +562,7 @@ template <int LPB, int VPL>
 __global__ void __launch_bounds__(256, 4)
 k_quantize(const float* __restrict__ W, int pitch, int64_t rows, int D,
            uint8_t* __restrict__ codes, int qpitch, int meta_off, bool minmax, uint32_t* status) {
+  pdl_wait();
   // rows in flight per group; at 4 CTAs/SM (64 registers) one row per group streams best
   // (D=64: 7.99 ms for 125M rows vs 8.15 at 2 rows / 3 CTAs and 9.6 at 2 rows / 116 regs)
   constexpr int R = VPL >= 4 ? 1 : 2;
@@ -600,6 +602,7 @@ k_adagrad(const uint32_t* __restrict__ unique, const uint32_t* __restrict__ Up,
           const float* __restrict__ G, const float* __restrict__ clip, float* __restrict__ Wt,
           float* __restrict__ A, int pitch, int D, float lr, float eps,
           uint8_t* __restrict__ codes, int qpitch, int meta_off, bool minmax, uint32_t* status) {
+  pdl_wait();
   constexpr int R = VPL >= 4 ? 1 : 2;
   const float c = *clip;
   if (c < 0.0f) return;  // non-finite global norm: skip the step (uniform over the grid)
@@ -957,7 +960,7 @@ cudaError_t launch_segreduce(const BwdArgs& a, int64_t* launches, cudaStream_t s
   if (e != cudaSuccess) return e;
   const unsigned grid = (unsigned)((a.chunks * g.lpb + 255) / 256);
 #define LAUNCH_SR(MEAN)                                                                     \
-  LIRANK_GEOM2_DISPATCH(g, (k_segreduce<L_, V_, MEAN><<<grid, 256, 0, s>>>(                \
+  LIRANK_GEOM2_DISPATCH(g, (launch_pdl(k_segreduce<L_, V_, MEAN>, grid, 256, 0, s,          \
                               a.seg, a.U, a.kv, a.chunk_u0, a.grad, a.offsets, a.B, a.F, a.D, \
                               a.pitch, a.chunks, a.G, a.part_first, a.part_last, a.norm_main, \
                               a.norm_fix, a.owner_list, a.owner_count)))
@@ -1024,8 +1027,8 @@ cudaError_t launch_adagrad(const BwdArgs& a, cudaStream_t s) {
   }
   const Geom g = rq ? geom_target(a.pitch, 4) : geom_for(a.pitch);
 #define LAUNCH_AG(DISPATCH, RW, RQ)                                                         \
-  DISPATCH(g, (k_adagrad<L_, V_, RW, RQ><<<persistent_grid((const void*)k_adagrad<L_, V_, RW, RQ>, \
-                                                            a.nnz, L_, 2), 256, 0, s>>>(    \
+  DISPATCH(g, (launch_pdl(k_adagrad<L_, V_, RW, RQ>, persistent_grid((const void*)k_adagrad<L_, V_, RW, RQ>, \
+                                                            a.nnz, L_, 2), 256, 0, s,       \
                   a.unique, a.U, a.G, a.clip, a.Wt, a.A, a.pitch, a.D, a.lr, a.eps,         \
                   a.q8_codes, a.qpitch, a.q8_meta_off, a.q8_minmax, a.status)))
   if (a.rowwise) {
@@ -1054,7 +1057,7 @@ cudaError_t launch_quantize(const float* W, int pitch, int64_t rows, int D, uint
   if (rows == 0) return cudaSuccess;
   const Geom g = quant_geom(pitch);
 #define LAUNCH_Q(L, V)                                                                 \
-  k_quantize<L, V><<<persistent_grid((const void*)k_quantize<L, V>, rows, L), 256, 0, s>>>( \
+  launch_pdl(k_quantize<L, V>, persistent_grid((const void*)k_quantize<L, V>, rows, L), 256, 0, s, \
       W, pitch, rows, D, codes, qpitch, meta_off, minmax, status)
   if (g.lpb == 1) {
     if (g.vpl == 1) LAUNCH_Q(1, 1); else if (g.vpl == 2) LAUNCH_Q(1, 2); else if (g.vpl == 3) LAUNCH_Q(1, 3); else LAUNCH_Q(1, 4);

@@ -386,6 +386,7 @@ __device__ __forceinline__ int len_bin(const int* __restrict__ offsets, long lon
 
 __global__ void __launch_bounds__(256)
 k_len_hist(const int* __restrict__ offsets, long long nbags, uint32_t* __restrict__ hist) {
+  pdl_wait();
   __shared__ uint32_t h[kLenBins];
   for (int i = threadIdx.x; i < kLenBins; i += blockDim.x) h[i] = 0;
   __syncthreads();
@@ -434,7 +435,7 @@ static const uint32_t* bag_order(const int* offsets, long long bags, uint32_t* w
   if (cudaMemsetAsync(hist, 0, 2 * kLenBins * sizeof(uint32_t), s) != cudaSuccess) return nullptr;
   const long long want = (bags + 255) / 256;
   const unsigned grid = (unsigned)(want < 148 * 4 ? want : 148 * 4);
-  k_len_hist<<<grid, 256, 0, s>>>(offsets, bags, hist);
+  launch_pdl(k_len_hist, grid, 256, 0, s, offsets, bags, hist);
   launch_pdl(k_len_scatter, grid, 256, 0, s, offsets, bags, (const uint32_t*)hist, cursor, ws);
   return ws;
 }

@@ -76,6 +76,7 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp
 template <int BITS>
 __global__ void __launch_bounds__(128)
 k_radix_hist(const uint2* __restrict__ kv, int64_t n, int passes, uint32_t* hist) {
+  pdl_wait();
   constexpr int BINS = 1 << BITS;
   extern __shared__ uint32_t sh[];  // [4 warps][passes][BINS]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -110,6 +111,7 @@ k_radix_hist(const uint2* __restrict__ kv, int64_t n, int passes, uint32_t* hist
 // tiles read each digit's global start instead of scanning the histogram themselves.
 __global__ void __launch_bounds__(512)
 k_hist_excl(uint32_t* hist, int bins) {
+  pdl_wait();
   __shared__ uint32_t s_warp[16];
   uint32_t* h = hist + (size_t)blockIdx.x * bins;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -171,6 +173,7 @@ __global__ void __launch_bounds__(kSortThreads, MINB)
 k_onesweep(const uint2* __restrict__ in, uint2* __restrict__ out, int64_t n, int shift,
            const uint32_t* __restrict__ hist, uint32_t* tile_counter,
            unsigned long long* status, const uint32_t* epoch_p, uint32_t epoch_off) {
+  pdl_wait();
   constexpr int BINS = 1 << BITS;
   const uint32_t epoch = *epoch_p + epoch_off;  // device-resident: graph replays advance it
   constexpr int DPT = BINS / kSortThreads;  // digits per thread (1 or 2)
@@ -274,7 +277,7 @@ static cudaError_t onesweep_pass(const uint2* a, uint2* b, int64_t n, int shift,
     attr = true;
   }
   const int64_t tiles = (n + TILE - 1) / TILE;
-  k_onesweep<BITS, ITEMS, MATCH, MINB><<<(unsigned)tiles, kSortThreads, sm, s>>>(a, b, n, shift, hist,
+  launch_pdl(k_onesweep<BITS, ITEMS, MATCH, MINB>, (unsigned)tiles, kSortThreads, sm, s, a, b, n, shift, hist,
                                                                                 counter, status, epoch,
                                                                                 epoch_off);
   return cudaGetLastError();
@@ -298,9 +301,9 @@ cudaError_t radix_sort_pairs(uint2* kv0, uint2* kv1, int64_t n, int bits, const 
     const int64_t want = (n + 128 * 8 - 1) / (128 * 8);
     const unsigned grid = (unsigned)(want < 148 * 8 ? want : 148 * 8);
     const size_t sm = sizeof(uint32_t) * 4 * passes * bins;
-    if (dbits == 9) k_radix_hist<9><<<grid, 128, sm, s>>>(kv0, n, passes, ws.hist);
-    else k_radix_hist<8><<<grid, 128, sm, s>>>(kv0, n, passes, ws.hist);
-    k_hist_excl<<<passes, 512, 0, s>>>(ws.hist, bins);
+    if (dbits == 9) launch_pdl(k_radix_hist<9>, grid, 128, sm, s, (const uint2*)kv0, n, passes, ws.hist);
+    else launch_pdl(k_radix_hist<8>, grid, 128, sm, s, (const uint2*)kv0, n, passes, ws.hist);
+    launch_pdl(k_hist_excl, passes, 512, 0, s, ws.hist, bins);
     *launches += 2;
   }
   uint2 *a = kv0, *b = kv1;
@@ -334,6 +337,7 @@ __global__ void __launch_bounds__(kSortThreads)
 k_rle(const uint2* __restrict__ kv, int64_t n, uint32_t sentinel, uint32_t* unique,
       uint32_t* seg, uint32_t* U_out, uint32_t* chunk_u0, uint32_t* tile_counter,
       unsigned long long* status, const uint32_t* epoch_p, uint32_t epoch_off) {
+  pdl_wait();
   const uint32_t epoch = *epoch_p + epoch_off;
   __shared__ uint32_t s_tile;
   __shared__ uint32_t s_warp[NW];
@@ -401,7 +405,7 @@ cudaError_t launch_rle(const uint2* kv, int64_t n, uint32_t sentinel, uint32_t* 
                        cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   const int64_t tiles = (n + kSortTile - 1) / kSortTile;
-  k_rle<<<(unsigned)tiles, kSortThreads, 0, s>>>(kv, n, sentinel, unique, seg, U_out, chunk_u0,
+  launch_pdl(k_rle, (unsigned)tiles, kSortThreads, 0, s, kv, n, sentinel, unique, seg, U_out, chunk_u0,
                                                  counter, status, epoch, epoch_off);
   return cudaGetLastError();
 }
@@ -409,10 +413,13 @@ cudaError_t launch_rle(const uint2* kv, int64_t n, uint32_t sentinel, uint32_t* 
 // The look-back epochs live in device memory and are advanced by a kernel in stream order
 // (not baked into launch parameters), so a captured CUDA graph of a step can be replayed:
 // every replay tags its status words with fresh epochs.
-__global__ void k_epoch_advance(uint32_t* epoch, uint32_t n) { *epoch += n; }
+__global__ void k_epoch_advance(uint32_t* epoch, uint32_t n) {
+  pdl_wait();
+  *epoch += n;
+}
 
 cudaError_t launch_epoch_advance(uint32_t* epoch, uint32_t n, cudaStream_t s) {
-  k_epoch_advance<<<1, 1, 0, s>>>(epoch, n);
+  launch_pdl(k_epoch_advance, 1, 1, 0, s, epoch, n);
   return cudaGetLastError();
 }
 
