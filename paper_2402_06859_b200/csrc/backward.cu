@@ -300,7 +300,7 @@ k_fixup_short(const uint32_t* __restrict__ seg, const uint32_t* __restrict__ Up,
 
 // Long spans: one CTA per entry.  Thread t owns element (t % pitch) of the row for chunk
 // sub-range (t / pitch); sub-ranges are contiguous and combined in order.
-__global__ void __launch_bounds__(kFixThreads)
+__global__ void __launch_bounds__(kFixThreads, 1)  // 1: 64 registers, all 16 loads in flight
 k_fixup_long(const uint32_t* __restrict__ seg, int pitch, const double* __restrict__ part_first,
              const double* __restrict__ part_last, const uint32_t* __restrict__ long_list,
              const uint32_t* __restrict__ long_count, float* __restrict__ G,
@@ -320,12 +320,12 @@ k_fixup_long(const uint32_t* __restrict__ seg, int pitch, const double* __restri
       const int64_t b = cs + 1 + (nch * (sp + 1)) / nsplit;
       double s = 0.0;
       int64_t cc = a;
-      for (; cc + 8 <= b; cc += 8) {  // 8 loads in flight, adds in chunk order
-        double x[8];
+      for (; cc + 16 <= b; cc += 16) {  // 16 loads in flight, adds in chunk order
+        double x[16];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) x[q] = __ldg(part_first + (size_t)(cc + q) * pitch + el);
+        for (int q = 0; q < 16; ++q) x[q] = __ldg(part_first + (size_t)(cc + q) * pitch + el);
 #pragma unroll
-        for (int q = 0; q < 8; ++q) s += x[q];
+        for (int q = 0; q < 16; ++q) s += x[q];
       }
       for (; cc < b; ++cc) s += part_first[(size_t)cc * pitch + el];
       sm[sp * pitch + el] = s;
@@ -339,15 +339,18 @@ k_fixup_long(const uint32_t* __restrict__ seg, int pitch, const double* __restri
       G[(size_t)u * pitch + el] = g;
       nrm_part += (double)g * (double)g;
     }
-    // deterministic block reduction of nrm_part (threads < pitch hold values)
+    // deterministic block reduction of nrm_part (threads < pitch hold values): a fixed
+    // shuffle tree per warp, then the warp partials in warp order (3 barriers, not 12)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) nrm_part += __shfl_xor_sync(0xffffffffu, nrm_part, o);
+    __syncthreads();  // this entry's reads of sm are done
+    if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = nrm_part;
     __syncthreads();
-    sm[threadIdx.x] = nrm_part;
-    __syncthreads();
-    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-      if (threadIdx.x < o) sm[threadIdx.x] += sm[threadIdx.x + o];
-      __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sm[w];
+      norm_fix[cs] = t;
     }
-    if (threadIdx.x == 0) norm_fix[cs] = sm[0];
     __syncthreads();
   }
 }
