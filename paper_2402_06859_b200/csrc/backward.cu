@@ -283,9 +283,18 @@ k_fixup_short(const uint32_t* __restrict__ seg, const uint32_t* __restrict__ Up,
         if (vi < nvec) {
           const double* p = part_last + (size_t)cs * pitch + 4 * vi;
           double a0 = p[0], a1 = p[1], a2 = p[2], a3 = p[3];
-          for (int64_t cc = cs + 1; cc <= ce; ++cc) {
-            const double* q = part_first + (size_t)cc * pitch + 4 * vi;
-            a0 += q[0]; a1 += q[1]; a2 += q[2]; a3 += q[3];
+          for (int64_t cc = cs + 1; cc <= ce; cc += 4) {  // 4 partial rows in flight, added in order
+            double2 x[4][2];
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              if (cc + j <= ce) {
+                const double2* q = reinterpret_cast<const double2*>(part_first + (size_t)(cc + j) * pitch + 4 * vi);
+                x[j][0] = q[0];
+                x[j][1] = q[1];
+              }
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              if (cc + j <= ce) { a0 += x[j][0].x; a1 += x[j][0].y; a2 += x[j][1].x; a3 += x[j][1].y; }
           }
           const float4 g = make_float4((float)a0, (float)a1, (float)a2, (float)a3);
           st_f4(G + (size_t)u * pitch + 4 * vi, g);
