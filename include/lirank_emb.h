@@ -35,9 +35,11 @@
  * - Pointers "host or device": ids, offsets, grad and out arguments may be device
  *   pointers or host pointers (detected with cudaPointerGetAttributes).  Host inputs are
  *   copied into library workspace on the stream before the kernels; a host `out` is
- *   filled by a device-to-host copy enqueued after the kernels.  Host buffers must stay
- *   valid (and host outputs are only complete) after emb_sync() returns.  Pinned host
- *   memory gives asynchronous copies; pageable memory works but copies synchronously.
+ *   filled by a device-to-host copy after the kernels and the call then WAITS for the
+ *   stream, so a host `out` is complete when the call returns.  Host inputs must stay
+ *   valid until the call's work is done (a host-`out` call, emb_sync(), or a stream
+ *   synchronisation).  Pinned host memory gives asynchronous copies; pageable memory works
+ *   but copies synchronously.
  * - Errors: argument errors are returned synchronously and nothing is enqueued.  Data-
  *   dependent errors (out-of-range ids, non-finite gradient norm, non-finite table row
  *   at quantize) are recorded in a sticky device status word and reported (and cleared)
@@ -55,7 +57,7 @@
 extern "C" {
 #endif
 
-#define EMB_ABI_VERSION 1
+#define EMB_ABI_VERSION 2  /* 2: emb_config.table_cost, EMB_F_HOSTCOMM, emb_allreduce_f32 */
 
 #if defined(__GNUC__)
 #define EMB_API __attribute__((visibility("default")))
@@ -66,7 +68,9 @@ extern "C" {
 typedef enum {
   EMB_OK = 0,
   EMB_EINVAL = 1,      /* bad argument (null pointer, size out of range, misalignment)   */
-  EMB_ENOMEM = 2,      /* a supplied buffer is smaller than emb_plan() asked for         */
+  EMB_ENOMEM = 2,      /* a supplied buffer is smaller than emb_plan() asked for; sticky
+                          (sharded): a call's ids exceeded a planned receive capacity
+                          (max_recv_nnz) -- the call was discarded on every rank        */
   EMB_ECUDA = 3,       /* a CUDA runtime call failed                                     */
   EMB_ENCCL = 4,       /* an NCCL call failed                                            */
   EMB_EIDRANGE = 5,    /* sticky: an id was < 0 or >= rows of its table (it was skipped) */
@@ -99,23 +103,43 @@ enum { EMB_SHARD_NONE = 0, EMB_SHARD_TABLE = 1, EMB_SHARD_ROW = 2 };
 #define EMB_F_EXCHANGE 8u /* run the sharded exchange path even at world_size 1 (a 1-rank
                              communicator; exercises the transport on a single GPU)          */
 #define EMB_F_P2P 64u     /* (sharded) FUSED EXCHANGE over peer memory (NVLink / NVSwitch): the
-                             owner's pooling kernel stores every pooled row straight into the
-                             source rank's buffer -- table-wise in its final [B][F][D] place,
-                             row-wise into a per-owner slot summed in rank order -- and the
-                             backward's grad rows are pushed into the owners' buffers by one
-                             kernel; a stream-ordered barrier (a 4-byte all-gather) replaces
-                             the pooled / grad all-to-all, reduce-scatter and all-gather.  The
-                             ids exchange (a1) stays on the transport.  Peer mappings: CUDA IPC
-                             of the workspace allocation (NCCL transport) or the other
-                             handle's buffers (loopback), made by the first sharded
-                             forward (collective); it returns EMB_ENCCL on EVERY rank if any
-                             rank cannot map its peers (create again without the flag).  Workspace grows by world * B * F * D floats
-                             (row-wise).                                                     */
+                             a1 ids are stored by one kernel at their final (compacted, source-
+                             ordered) place in each owner's receive buffer; the owner's pooling
+                             kernel stores every pooled row straight into the source rank's
+                             buffer -- table-wise in its final [B][F][D] place, row-wise into a
+                             per-owner slot summed in rank order -- and the backward's grad
+                             rows are pushed into the owners' buffers by one kernel; stream-
+                             ordered barriers (a 4-byte all-gather) replace the all-to-alls,
+                             the reduce-scatter and the all-gather.  Peer mappings: CUDA IPC
+                             of the workspace allocation (NCCL / host transports) or the other
+                             handle's buffers (loopback), made by the first sharded forward
+                             (collective); it returns EMB_ENCCL on EVERY rank if any rank
+                             cannot map its peers (create again without the flag).  Workspace
+                             grows by world * B * F * D floats (row-wise).
+                             Without the flag the ids travel as an all-to-all of capacity-
+                             padded slots (min(max_nnz, max_recv_nnz) ids per rank pair).
+                             Either way no call of a sharded step reads a count on the host:
+                             a sharded step can be captured as a CUDA graph.              */
 #define EMB_F_LOOPBACK 4u /* (world_size > 1) TEST TRANSPORT: the ranks are threads of one
                              process sharing one device; cfg.nccl_unique_id is the hub from
                              emb_loopback_hub_create().  Every collective becomes a host
                              rendezvous + stream-ordered device copies (no kernel waits on
                              another rank).  Same exchange code path as NCCL otherwise.       */
+
+#define EMB_F_HOSTCOMM 128u /* (world_size > 1) TEST TRANSPORT: one rank per PROCESS (e.g. several
+                             processes sharing one GPU); cfg.nccl_unique_id points to an
+                             emb_host_comm.  Every collective drains the stream and moves its
+                             bytes through host memory with the caller's host all-gather; peer
+                             memory (EMB_F_P2P) is mapped with CUDA IPC.  No kernel waits on
+                             another rank.  Same exchange code path as NCCL otherwise.        */
+
+/* The caller's host all-gather for EMB_F_HOSTCOMM: recv[r * bytes .. (r+1) * bytes) = the
+ * `bytes` at send of rank r, for every rank r (a blocking collective over host memory, e.g.
+ * torch.distributed.all_gather over gloo).  Returns 0 on success. */
+typedef struct {
+  void* ctx;
+  int32_t (*allgather)(void* ctx, const void* send, void* recv, int64_t bytes);
+} emb_host_comm;
 
 typedef struct {
   uint32_t abi_version;          /* must be EMB_ABI_VERSION                                    */
@@ -142,7 +166,13 @@ typedef struct {
   uint32_t flags;                /* EMB_F_*                                                   */
   int64_t max_recv_nnz;          /* sharded: capacity of occurrences this rank pools per call
                                     (its rows' share of every rank's ids); 0 = min(2, W) *
-                                    max_nnz.  A call that exceeds it returns EMB_ENOMEM.      */
+                                    max_nnz.  A call that exceeds it on any rank is discarded
+                                    on every rank (zero outputs, no occurrences) with sticky
+                                    EMB_ENOMEM (emb_sync).                                    */
+  const double* table_cost;      /* host [T] or NULL: table-wise planning weight of each table,
+                                    e.g. its expected bytes per step (B * mean bag length * 4 +
+                                    row bytes) + B * row bytes, SURVEY.md §8(e).  The
+                                    automatic plan balances these; NULL balances rows.      */
 } emb_config;
 
 typedef struct {
@@ -175,7 +205,8 @@ EMB_API const char* emb_status_string(emb_status s);
 
 /* Validate cfg and report buffer sizes (host-only; no CUDA calls).  For sharded
  * configurations it also fixes the plan: table-wise = cfg.table_owner if given, else a
- * greedy longest-processing-time assignment of tables by rows (ties to the lower rank);
+ * greedy longest-processing-time assignment of tables by cfg.table_cost (by rows when
+ * NULL): largest first, each to the least-loaded rank (ties to the lower rank);
  * row-wise = rank r owns rows [r*ceil(R/W), (r+1)*ceil(R/W)) of every table. */
 EMB_API emb_status emb_plan(const emb_config* cfg, emb_sizes* out);
 
@@ -216,14 +247,25 @@ EMB_API emb_status emb_forward(emb_t h, const int32_t* ids, const int32_t* offse
 /* a5-a8 (+ a4 when sharded) for the batch of the most recent emb_forward (EMB_ESTATE if
  * none).  grad_out: fp32 [B][F][D] = dL/d(out) of that forward.  Dedups the occurrences by
  * (table, row), reduces G_u in fp64, forms the global squared norm
- * S = sum_u ||G_u||^2 + extra_sq_norm (summed over ranks in rank order), the clip factor
+ * S = sum over ranks (rank order) of sum_u ||G_u||^2, + extra_sq_norm, the clip factor
  * c = min(1, max_norm / sqrt(S)), and applies AdaGrad (cfg.adagrad_mode) with step lr to
  * the touched rows only.  extra_sq_norm lets the caller fold the dense-tower gradient into
- * the global norm (pass 0 otherwise).  Non-finite S: no row is updated, sticky
+ * the global norm (pass 0 otherwise); it is added ONCE, not summed over ranks, so with
+ * world_size > 1 every rank must pass the SAME value (the norm of the all-reduced dense
+ * gradient, emb_allreduce_f32), or ranks would clip with different factors.  Non-finite S: no row is updated, sticky
  * EMB_ENONFINITE.  If sq_norm_out (host) is non-NULL the call waits for the step and
  * returns S there. */
 EMB_API emb_status emb_backward_adagrad(emb_t h, const float* grad_out, float lr, double extra_sq_norm,
                                 double* sq_norm_out);
+
+/* Data-parallel dense side (NEXT-2, "Other layers ... processed in a data
+ * parallel way"): data[0..count) (DEVICE fp32) = its sum over all ranks, in place, on the
+ * library stream and transport (NCCL all-reduce; loopback / host transports sum in rank
+ * order).  Every rank ends with identical values -- which is what makes the dense squared
+ * norm a caller then passes as extra_sq_norm(_dev) identical on every rank, as the global
+ * clip requires.  count <= max_batch * num_features * dim (the staging scratch), else
+ * EMB_EINVAL.  world_size 1: no-op. */
+EMB_API emb_status emb_allreduce_f32(emb_t h, float* data, int64_t count);
 
 /* As emb_backward_adagrad, with no host synchronisation for a dense side on the device
  * (NEXT-2, "global gradient clipped to unit norm" over sparse + dense; P:538 tower):

@@ -11,12 +11,12 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "liblirank_emb.so")
 
-EMB_ABI_VERSION = 1
+EMB_ABI_VERSION = 2
 EMB_POOL_SUM, EMB_POOL_MEAN = 0, 1
 EMB_ADAGRAD_ROWWISE, EMB_ADAGRAD_ELEMENTWISE = 0, 1
 EMB_SHARD_NONE, EMB_SHARD_TABLE, EMB_SHARD_ROW = 0, 1, 2
-EMB_F_Q8, EMB_F_REQUANT, EMB_F_LOOPBACK, EMB_F_EXCHANGE, EMB_F_Q8_MINMAX, EMB_F_Q8_ONLY, EMB_F_P2P = \
-    1, 2, 4, 8, 16, 32, 64
+EMB_F_Q8, EMB_F_REQUANT, EMB_F_LOOPBACK, EMB_F_EXCHANGE, EMB_F_Q8_MINMAX, EMB_F_Q8_ONLY, EMB_F_P2P, \
+    EMB_F_HOSTCOMM = 1, 2, 4, 8, 16, 32, 64, 128
 PHASES = ["fwd", "sort", "rle", "segreduce", "norm", "update", "fwd_q8", "quantize", "copy", "exchange"]
 
 STATUS = {0: "EMB_OK", 1: "EMB_EINVAL", 2: "EMB_ENOMEM", 3: "EMB_ECUDA", 4: "EMB_ENCCL",
@@ -53,7 +53,16 @@ class EmbConfig(C.Structure):
         ("stream", C.c_void_p),
         ("flags", C.c_uint32),
         ("max_recv_nnz", C.c_int64),
+        ("table_cost", C.POINTER(C.c_double)),
     ]
+
+
+# int32 (*allgather)(void* ctx, const void* send, void* recv, int64 bytes)
+HOST_ALLGATHER = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64)
+
+
+class EmbHostComm(C.Structure):
+    _fields_ = [("ctx", C.c_void_p), ("allgather", HOST_ALLGATHER)]
 
 
 class EmbSizes(C.Structure):
@@ -100,6 +109,7 @@ SIGNATURES = {
     "emb_profile_read": (C.c_int, [P, P, P, C.c_int32]),
     "emb_destroy": (C.c_int, [P]),
     "emb_backward_adagrad_dev": (C.c_int, [P, P, C.c_float, P, P, P]),
+    "emb_allreduce_f32": (C.c_int, [P, P, C.c_int64]),
     "emb_set_incremental": (C.c_int, [P, P, P, P, P, C.c_float, C.c_float]),
     "emb_quantize_block": (C.c_int, [P, C.c_int32, C.c_int64, C.c_int64, P, C.c_int64]),
     "emb_cold_weight_init": (C.c_int, [P, P, P, C.c_float]),

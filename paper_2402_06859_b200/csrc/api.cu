@@ -90,6 +90,7 @@ emb_status make_plan(const emb_config* c, Plan* p) {
   if (p->exch && c->sharding == EMB_SHARD_NONE) return EMB_EINVAL;
   if (p->exch && c->pooling == EMB_POOL_MEAN) return EMB_EINVAL;
   if ((c->flags & EMB_F_P2P) && !p->exch) return EMB_EINVAL;
+  if ((c->flags & EMB_F_LOOPBACK) && (c->flags & EMB_F_HOSTCOMM)) return EMB_EINVAL;
   p->sharding = p->exch ? c->sharding : EMB_SHARD_NONE;
   p->rank = c->rank;
   p->world = c->world_size;
@@ -115,18 +116,23 @@ emb_status make_plan(const emb_config* c, Plan* p) {
         p->owner[t] = c->table_owner[t];
       }
     } else {
-      // greedy LPT by rows (largest first, ties by table index), to the least-loaded rank
+      // greedy LPT by cost (cfg.table_cost, else rows; largest first, ties by table
+      // index), each table to the least-loaded rank (ties to the lower rank)
+      std::vector<double> cost(p->T);
+      for (int t = 0; t < p->T; ++t) {
+        cost[t] = c->table_cost ? c->table_cost[t] : (double)p->table_rows[t];
+        if (!(cost[t] >= 0.0)) return EMB_EINVAL;
+      }
       std::vector<int> order(p->T);
       for (int t = 0; t < p->T; ++t) order[t] = t;
-      std::stable_sort(order.begin(), order.end(),
-                       [&](int a, int b) { return p->table_rows[a] > p->table_rows[b]; });
-      std::vector<int64_t> load(W, 0);
+      std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost[a] > cost[b]; });
+      std::vector<double> load(W, 0.0);
       for (int t : order) {
         int best = 0;
         for (int r = 1; r < W; ++r)
           if (load[r] < load[best]) best = r;
         p->owner[t] = best;
-        load[best] += p->table_rows[t];
+        load[best] += cost[t];
       }
     }
   }
@@ -181,6 +187,10 @@ emb_status make_plan(const emb_config* c, Plan* p) {
                   : c->max_recv_nnz > 0 ? c->max_recv_nnz
                                         : std::min<int64_t>(p->max_nnz * std::min(W, 2), (int64_t(1) << 30) - 1);
   p->owner_bags_cap = (int64_t)p->max_batch * (p->exch ? (int64_t)p->Fr * W : F);
+  // collective a1: one key slot per (source, owner) pair, capacity-padded so the all-to-all
+  // sizes are fixed by the plan (no host read of the counts); a source sends at most its
+  // max_nnz ids, an owner receives at most recv_nnz_cap
+  p->pair_cap = std::min<int64_t>(p->max_nnz, p->recv_nnz_cap);
   return EMB_OK;
 }
 
@@ -195,7 +205,7 @@ void carve(const Plan& p, Carver& cv, emb_handle* h) {
   const int64_t dense_cap = std::max<int64_t>(Bmax * F * p.D, 1);
   const int64_t tiles = (std::max<int64_t>(nnz_cap, bags_cap + Bmax * p.dest_base[p.world]) + kSortTileMin - 1) /
                             kSortTileMin + 1;
-  const int64_t chunks = (nnz_cap + kChunk - 1) / kChunk + 1;
+  const int64_t chunks = chunks_cap_for(nnz_cap);
   const int64_t max_unique = std::min<int64_t>(nnz_cap, p.local_rows) + 1;
   auto* meta = cv.take<FeatMeta>(F);
   auto* stage_ids = cv.take<int>(p.max_nnz);
@@ -225,6 +235,7 @@ void carve(const Plan& p, Carver& cv, emb_handle* h) {
   auto* cl = cv.take<float>(1);
   auto* st = cv.take<uint32_t>(1);
   auto* ep = cv.take<uint32_t>(2);
+  auto* fwdn = cv.take<uint32_t>(1);
   auto* order = cv.take<uint32_t>(kOrderWsWords(std::max<int64_t>(F * Bmax, bags_cap)));
   ExchangeWs x{};
   if (p.exch) carve_exchange(p, cv, &x);
@@ -249,6 +260,7 @@ void carve(const Plan& p, Carver& cv, emb_handle* h) {
     h->chunks_cap = chunks;
     h->S_parts = sp; h->S_local = sl; h->S_global = sg; h->d_clip = cl; h->d_status = st;
     h->d_epoch = ep;
+    h->d_fwd_n = fwdn;
     h->norm_parts = nparts; h->norm_done = ndone;
     h->x = x;
   }
@@ -309,8 +321,13 @@ emb_status stage_inputs(emb_t h, const int32_t* ids, const int32_t* offsets, int
 // the rank partials of the global squared norm are all-gathered and summed in rank order.
 emb_status launch_dedup(emb_t h) {
   const Plan& p = h->p;
-  const int64_t n = h->fwd_nnz;
+  const int64_t n = h->fwd_nnz;  // exact (unsharded) or the capacity (sharded: count on device)
   const uint2* kres = h->kvA;
+  // segment-reduce chunk: sized for the call's ids (small batches still fill every SM), and
+  // large enough that a capacity's worth of chunks fits the planned partials
+  int cl = chunk_log2_for(h->fwd_nnz_hint);
+  while (cl < kChunkLog2Max && ((n + (int64_t(1) << cl) - 1) >> cl) + 1 > h->chunks_cap) ++cl;
+  h->chunk_log2 = cl;
   CK(cudaEventRecord(h->ev_kv, h->stream));
   CK(cudaStreamWaitEvent(h->side, h->ev_kv, 0));
   if (n > 0) {
@@ -318,12 +335,12 @@ emb_status launch_dedup(emb_t h) {
     bool in1 = false;
     {
       Phase ph(h->prof, h->side, EMB_PH_SORT);
-      CK(radix_sort_pairs(h->kvA, h->kvB, n, p.key_bits, h->sort, h->d_epoch, &passes, &in1,
+      CK(radix_sort_pairs(h->kvA, h->kvB, n, h->fwd_n_dev, p.key_bits, h->sort, h->d_epoch, &passes, &in1,
                           &h->launches, h->side));
     }
     if (in1) kres = h->kvB;
     Phase ph(h->prof, h->side, EMB_PH_RLE);
-    CK(launch_rle(kres, n, (uint32_t)p.local_rows, h->unique, h->seg, h->d_U, h->chunk_u0,
+    CK(launch_rle(kres, n, h->fwd_n_dev, (uint32_t)p.local_rows, h->unique, h->seg, h->d_U, h->chunk_u0, cl,
                   h->sort.counters + kMaxPasses, h->sort.status, h->d_epoch, (uint32_t)passes, h->side));
     CK(launch_epoch_advance(h->d_epoch, (uint32_t)passes + 1, h->side));
     h->launches += 2;
@@ -374,7 +391,8 @@ emb_status backward_local(emb_t h, const float* grad_dev, float lr, double extra
   a.norm_fix = h->norm_fix;
   a.owner_list = h->owner_list;
   a.owner_count = h->owner_count;
-  a.chunks = (n + kChunk - 1) / kChunk;
+  a.chunk_log2 = h->chunk_log2;
+  a.chunks = (n + (int64_t(1) << a.chunk_log2) - 1) >> a.chunk_log2;
   a.S_local = h->S_local;
   a.norm_parts = h->norm_parts;
   a.norm_done = h->norm_done;
@@ -611,8 +629,9 @@ emb_status emb_create(const emb_config* cfg, const emb_buffers* buf, emb_t* out)
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_dedup, cudaEventDisableTiming);
   if (e != cudaSuccess) { delete h; return EMB_ECUDA; }
   if (p.exch) {
-    h->comm = (p.flags & EMB_F_LOOPBACK) ? make_loopback_transport((void*)cfg->nccl_unique_id, p.rank)
-                                         : make_nccl_transport(cfg->nccl_unique_id, p.rank, p.world);
+    h->comm = (p.flags & EMB_F_LOOPBACK)   ? make_loopback_transport((void*)cfg->nccl_unique_id, p.rank)
+              : (p.flags & EMB_F_HOSTCOMM) ? make_host_transport(cfg->nccl_unique_id, p.rank, p.world)
+                                           : make_nccl_transport(cfg->nccl_unique_id, p.rank, p.world);
     if (!h->comm) { delete h; return EMB_ENCCL; }
     if ((s = exchange_init(h)) != EMB_OK) { delete h->comm; delete h; return s; }
   }
@@ -674,6 +693,7 @@ emb_status emb_sync(emb_t h) {
   CK(cudaMemcpy(&st, h->d_status, sizeof(st), cudaMemcpyDeviceToHost));
   CK(cudaMemsetAsync(h->d_status, 0, sizeof(uint32_t), h->stream));
   CK(cudaStreamSynchronize(h->stream));
+  if (st & kStOverflow) return EMB_ENOMEM;
   if (st & kStNonFinite) return EMB_ENONFINITE;
   if (st & kStIdRange) return EMB_EIDRANGE;
   return EMB_OK;
@@ -731,6 +751,8 @@ emb_status emb_forward(emb_t h, const int32_t* ids, const int32_t* offsets, int3
     }
     h->have_fwd = true;
     h->fwd_nnz = nnz;
+    h->fwd_n_dev = nullptr;
+    h->fwd_nnz_hint = nnz;
     h->fwd_B = batch;
     if ((s = launch_dedup(h)) != EMB_OK) return s;  // a5 starts now, on the side stream
   }
@@ -738,6 +760,7 @@ emb_status emb_forward(emb_t h, const int32_t* ids, const int32_t* offsets, int3
     Phase ph(h->prof, h->stream, EMB_PH_COPY);
     CK(cudaMemcpyAsync(out, st.out, sizeof(float) * (int64_t)batch * p.F * p.D,
                        cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));  // a host `out` is complete when the call returns
   }
   return EMB_OK;
 }
@@ -786,6 +809,7 @@ emb_status emb_forward_q8(emb_t h, const int32_t* ids, const int32_t* offsets, i
     Phase ph(h->prof, h->stream, EMB_PH_COPY);
     CK(cudaMemcpyAsync(out, st.out, sizeof(float) * (int64_t)batch * p.F * p.D,
                        cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));  // a host `out` is complete when the call returns
   }
   return EMB_OK;
 }
@@ -828,6 +852,16 @@ emb_status emb_backward_adagrad(emb_t h, const float* grad_out, float lr, double
     CK(cudaStreamSynchronize(h->stream));
   }
   return EMB_OK;
+}
+
+emb_status emb_allreduce_f32(emb_t h, float* data, int64_t count) {
+  if (!h || count < 0 || (count > 0 && !data)) return EMB_EINVAL;
+  const Plan& p = h->p;
+  if (count > std::max<int64_t>((int64_t)p.max_batch * p.F * p.D, 1)) return EMB_EINVAL;
+  if (count == 0 || !p.exch) return EMB_OK;
+  if (!is_device_ptr(data)) return EMB_EINVAL;
+  Phase ph(h->prof, h->stream, EMB_PH_EXCHANGE);
+  return h->comm->allreduce_sum_f32(data, (size_t)count, h->stage_dense, h->stream) ? EMB_OK : EMB_ENCCL;
 }
 
 emb_status emb_backward_adagrad_dev(emb_t h, const float* grad_out, float lr,

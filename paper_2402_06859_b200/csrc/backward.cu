@@ -13,7 +13,8 @@
 //
 // Design (B200):
 // * segment-reduce is load-balanced by OCCURRENCES, not by segments: the sorted
-//   occurrence list is cut into fixed chunks of kChunk, one lane group (LPB lanes, one
+//   occurrence list is cut into chunks of 2^chunk_log2 (32..256, chosen per call so a small
+//   batch still spreads over every SM: chunk_log2_for), one lane group (LPB lanes, one
 //   float4 of the 256-B grad row per lane at D=64) per chunk, fp64 accumulators in
 //   registers, UNR grad-row gathers in flight.  Segments wholly inside a chunk are
 //   finished in place; a segment cut by chunk boundaries leaves fp64 partials that a
@@ -114,13 +115,13 @@ __device__ __forceinline__ void write_partial(double* P, int pitch, int64_t c, i
 
 }  // namespace
 
-// One lane group per chunk of kChunk sorted occurrences.  kv[k] = {row key, grad row}.
+// One lane group per chunk of 2^chunk_log2 sorted occurrences.  kv[k] = {row key, grad row}.
 template <int LPB, int VPL, bool MEAN>
 __global__ void __launch_bounds__(256, 4)
 k_segreduce(const uint32_t* __restrict__ seg, const uint32_t* __restrict__ Up,
             const uint2* __restrict__ kv, const uint32_t* __restrict__ chunk_u0,
             const float* __restrict__ grad, const int* __restrict__ offsets, int B, int F, int D,
-            int pitch, int64_t chunks, float* __restrict__ G, double* __restrict__ part_first,
+            int pitch, int64_t chunks, int chunk_log2, float* __restrict__ G, double* __restrict__ part_first,
             double* __restrict__ part_last, double* __restrict__ norm_main,
             double* __restrict__ norm_fix, uint32_t* __restrict__ owner_list,
             uint32_t* owner_count) {
@@ -133,9 +134,10 @@ k_segreduce(const uint32_t* __restrict__ seg, const uint32_t* __restrict__ Up,
   const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LPB;
   const uint32_t U = *Up;
   const int64_t n_valid = seg[U];
-  const int64_t k0 = c * kChunk;
+  const int chunk = 1 << chunk_log2;
+  const int64_t k0 = c << chunk_log2;
   const bool live = c < chunks && k0 < n_valid;
-  const int64_t k1 = live ? min(k0 + (int64_t)kChunk, n_valid) : k0;
+  const int64_t k1 = live ? min(k0 + (int64_t)chunk, n_valid) : k0;
   uint32_t u = live ? __ldg(chunk_u0 + c) : 0u;  // segment containing occurrence k0 (RLE)
   // the open segment started before this chunk (its sum is a part_first partial)
   bool first_open = live && (int64_t)__ldg(seg + u) < k0;
@@ -144,7 +146,7 @@ k_segreduce(const uint32_t* __restrict__ seg, const uint32_t* __restrict__ Up,
   double acc[VPL][4];
   zero(acc);
   double nrm = 0.0;
-  // Warp-uniform loop (kChunk/LPB batches for every group): each batch loads LPB {key,
+  // Warp-uniform loop (chunk/LPB batches for every group): each batch loads LPB {key,
   // grad row} pairs (one per lane) and broadcasts them with full-mask shuffles; slots
   // past k1 (last chunk, dead groups) are predicated.  Segment boundaries come from the
   // keys themselves (an occurrence whose key differs from its predecessor's starts a
@@ -152,7 +154,7 @@ k_segreduce(const uint32_t* __restrict__ seg, const uint32_t* __restrict__ Up,
   uint32_t carry_key = 0;  // key of the occurrence before the batch (lane LPB-1's, last batch)
   // the {key, grad row} pairs are loaded one batch ahead of the gradient-row gathers
   uint2 kv_next = k0 + lane < k1 ? __ldg(kv + k0 + lane) : make_uint2(0u, 0u);
-  for (int it = 0; it < kChunk / LPB; ++it) {
+  for (int it = 0; it < chunk / LPB; ++it) {
     const int64_t kb = k0 + (int64_t)it * LPB;
     uint2 kvl = kv_next;
     kv_next = kb + LPB + lane < k1 ? __ldg(kv + kb + LPB + lane) : make_uint2(0u, 0u);
@@ -245,7 +247,7 @@ k_fixup_short(const uint32_t* __restrict__ seg, const uint32_t* __restrict__ Up,
               const uint32_t* __restrict__ chunk_u0, int pitch, const double* __restrict__ part_first,
               const double* __restrict__ part_last, const uint32_t* __restrict__ owner_list,
               const uint32_t* __restrict__ owner_count, float* __restrict__ G,
-              double* __restrict__ norm_fix, uint32_t* long_list, uint32_t* long_count) {
+              double* __restrict__ norm_fix, uint32_t* long_list, uint32_t* long_count, int chunk_log2) {
   pdl_wait();
   constexpr int GPW = 32 / LPB;  // groups per warp
   const int lane = threadIdx.x & (LPB - 1);
@@ -265,7 +267,7 @@ k_fixup_short(const uint32_t* __restrict__ seg, const uint32_t* __restrict__ Up,
       // the segment spills into chunk cs+1, so it is the one containing that chunk's first
       // occurrence: chunk_u0[cs+1] (no binary search over seg[])
       u = __ldg(chunk_u0 + cs + 1);
-      ce = ((int64_t)__ldg(seg + u + 1) - 1) / kChunk;
+      ce = ((int64_t)__ldg(seg + u + 1) - 1) >> chunk_log2;
       if (ce - cs > kFixLong) {
         if (lane == 0) {
           const uint32_t slot = atomicAdd(long_count, 1u);
@@ -313,7 +315,7 @@ __global__ void __launch_bounds__(kFixThreads, 1)  // 1: 64 registers, all 16 lo
 k_fixup_long(const uint32_t* __restrict__ seg, int pitch, const double* __restrict__ part_first,
              const double* __restrict__ part_last, const uint32_t* __restrict__ long_list,
              const uint32_t* __restrict__ long_count, float* __restrict__ G,
-             double* __restrict__ norm_fix) {
+             double* __restrict__ norm_fix, int chunk_log2) {
   pdl_wait();
   extern __shared__ double sm[];  // [max(nsplit * pitch, kFixThreads)]
   const uint32_t n_entries = *long_count;
@@ -321,7 +323,7 @@ k_fixup_long(const uint32_t* __restrict__ seg, int pitch, const double* __restri
   for (uint32_t e = blockIdx.x; e < n_entries; e += gridDim.x) {
     const uint32_t cs = long_list[2 * e], u = long_list[2 * e + 1];
     const int64_t s_end = __ldg(seg + u + 1);
-    const int64_t ce = (s_end - 1) / kChunk;
+    const int64_t ce = (s_end - 1) >> chunk_log2;
     const int64_t nch = ce - cs;  // chunks cs+1 .. ce
     for (int t = threadIdx.x; t < nsplit * pitch; t += blockDim.x) {
       const int el = t % pitch, sp = t / pitch;
@@ -949,13 +951,10 @@ static Geom geom_target(int pitch, int target);
 // `waves` > 1 oversubscribes: for the random-access update, later CTAs fill SMs whose
 // first CTAs finished early (measured 0.58 -> 0.55 ms at 8 CTAs/SM requested vs 3 resident).
 static unsigned persistent_grid(const void* kernel, int64_t groups, int lpb, int waves = 1) {
-  static int sms = 0;
-  if (sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms < 1) sms = 148;
-  }
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (sms < 1) sms = 148;
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, 0) != cudaSuccess ||
       per_sm < 1)
@@ -974,8 +973,8 @@ cudaError_t launch_segreduce(const BwdArgs& a, int64_t* launches, cudaStream_t s
 #define LAUNCH_SR(MEAN)                                                                     \
   LIRANK_GEOM2_DISPATCH(g, (launch_pdl(k_segreduce<L_, V_, MEAN>, grid, 256, 0, s,          \
                               a.seg, a.U, a.kv, a.chunk_u0, a.grad, a.offsets, a.B, a.F, a.D, \
-                              a.pitch, a.chunks, a.G, a.part_first, a.part_last, a.norm_main, \
-                              a.norm_fix, a.owner_list, a.owner_count)))
+                              a.pitch, a.chunks, a.chunk_log2, a.G, a.part_first, a.part_last, \
+                              a.norm_main, a.norm_fix, a.owner_list, a.owner_count)))
   if (a.mean) LAUNCH_SR(true); else LAUNCH_SR(false);
 #undef LAUNCH_SR
   ++*launches;
@@ -983,12 +982,13 @@ cudaError_t launch_segreduce(const BwdArgs& a, int64_t* launches, cudaStream_t s
   uint32_t* long_list = a.owner_list + a.chunks;  // [2 * chunks] after the owner list
   LIRANK_GEOM2_DISPATCH(g, (launch_pdl(k_fixup_short<L_, V_>, persistent_grid((const void*)k_fixup_short<L_, V_>, a.chunks, L_), 256, 0, s,
                               a.seg, a.U, a.chunk_u0, a.pitch, a.part_first, a.part_last,
-                              a.owner_list, a.owner_count, a.G, a.norm_fix, long_list, long_count)));
+                              a.owner_list, a.owner_count, a.G, a.norm_fix, long_list, long_count,
+                              a.chunk_log2)));
   ++*launches;
   const int nsplit = a.pitch < kFixThreads ? kFixThreads / a.pitch : 1;
   const size_t smem = sizeof(double) * (size_t)(nsplit * a.pitch > kFixThreads ? nsplit * a.pitch : kFixThreads);
   launch_pdl(k_fixup_long, 148, kFixThreads, smem, s, a.seg, a.pitch, a.part_first, a.part_last,
-             long_list, long_count, a.G, a.norm_fix);
+             long_list, long_count, a.G, a.norm_fix, a.chunk_log2);
   ++*launches;
   return cudaGetLastError();
 }
@@ -1015,16 +1015,20 @@ cudaError_t launch_adagrad(const BwdArgs& a, cudaStream_t s) {
   // CTAs/SM (measured: 0.68 -> 0.55 ms on Feed-1).
   const bool rq = a.q8_codes != nullptr;
   if (a.rowwise && a.pitch == 64 && a.D == 64 && a.tma) {  // TMA-pipelined update (D = 64)
-    static int per_sm = 0;
+    // function attributes and occupancy are per device and per kernel variant: cached so
+    // (per device, variant) they are set before any graph capture of a step
+    static int per_sm_cache[kMaxDevices][2] = {};
     auto kern = rq ? (const void*)k_adagrad_tma<true> : (const void*)k_adagrad_tma<false>;
-    if (per_sm == 0) {
-      cudaFuncSetAttribute(k_adagrad_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
-      cudaFuncSetAttribute(k_adagrad_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
-      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, kTmaSmem) != cudaSuccess || per_sm < 1)
-        per_sm = 1;
-    }
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
+    const int dv = dev >= 0 && dev < kMaxDevices ? dev : 0;
+    int& per_sm = per_sm_cache[dv][rq ? 1 : 0];
+    if (per_sm == 0 || dev != dv) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
+      int ps = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, kern, 256, kTmaSmem) != cudaSuccess || ps < 1) ps = 1;
+      per_sm = ps;
+    }
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t want = (a.nnz * 4 + 255) / 256;
     const int64_t cap = (int64_t)sms * per_sm * kTmaWaves;

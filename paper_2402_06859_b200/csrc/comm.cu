@@ -1,6 +1,8 @@
 // comm.cu -- NCCL and loopback transports for the sharded exchange (see comm.h).
 #include "comm.h"
 
+#include "../../include/lirank_emb.h"
+
 #include <dlfcn.h>
 #include <string.h>
 
@@ -30,6 +32,7 @@ struct Api {
   Result (*Recv)(void*, size_t, int, int, Comm, cudaStream_t) = nullptr;
   Result (*AllGather)(const void*, void*, size_t, int, Comm, cudaStream_t) = nullptr;
   Result (*ReduceScatter)(const void*, void*, size_t, int, int, Comm, cudaStream_t) = nullptr;
+  Result (*AllReduce)(const void*, void*, size_t, int, int, Comm, cudaStream_t) = nullptr;
   bool ok = false;
 };
 static Api& api() {
@@ -47,8 +50,10 @@ static Api& api() {
     x.AllGather = (Result(*)(const void*, void*, size_t, int, Comm, cudaStream_t))dlsym(lib, "ncclAllGather");
     x.ReduceScatter =
         (Result(*)(const void*, void*, size_t, int, int, Comm, cudaStream_t))dlsym(lib, "ncclReduceScatter");
+    x.AllReduce =
+        (Result(*)(const void*, void*, size_t, int, int, Comm, cudaStream_t))dlsym(lib, "ncclAllReduce");
     x.ok = x.GetUniqueId && x.CommInitRank && x.CommDestroy && x.GroupStart && x.GroupEnd &&
-           x.Send && x.Recv && x.AllGather && x.ReduceScatter;
+           x.Send && x.Recv && x.AllGather && x.ReduceScatter && x.AllReduce;
     return x;
   }();
   return a;
@@ -145,6 +150,9 @@ struct NcclTransport : Transport {
   }
   bool reduce_scatter_f32(const float* send, float* recv, size_t count, cudaStream_t s) override {
     return nccl::api().ReduceScatter(send, recv, count, nccl::kFloat32, nccl::kSum, comm, s) == 0;
+  }
+  bool allreduce_sum_f32(float* data, size_t count, float*, cudaStream_t s) override {
+    return nccl::api().AllReduce(data, data, count, nccl::kFloat32, nccl::kSum, comm, s) == 0;
   }
   bool alltoallv(const void* send, const size_t* soff, const size_t* sbytes, void* recv,
                  const size_t* roff, const size_t* rbytes, cudaStream_t s) override {
@@ -282,6 +290,23 @@ struct LoopbackTransport : Transport {
     finish(s);
     return ok;
   }
+  bool allreduce_sum_f32(float* data, size_t count, float* scratch, cudaStream_t s) override {
+    publish(data, nullptr, nullptr, s);
+    bool ok = true;
+    for (int r = 0; r < hub->world; ++r) {  // rank order: every rank forms the same sum
+      ok &= cudaStreamWaitEvent(s, hub->slots[r].ready, 0) == cudaSuccess;
+      const float* src = (const float*)hub->slots[r].send;
+      if (r == 0) {
+        ok &= cudaMemcpyAsync(scratch, src, count * sizeof(float), cudaMemcpyDeviceToDevice, s) == cudaSuccess;
+      } else if (count) {
+        k_add_f32<<<148 * 4, 256, 0, s>>>(scratch, src, count);
+        ok &= cudaGetLastError() == cudaSuccess;
+      }
+    }
+    finish(s);  // every rank has read every `data` before any overwrites its own
+    ok &= cudaMemcpyAsync(data, scratch, count * sizeof(float), cudaMemcpyDeviceToDevice, s) == cudaSuccess;
+    return ok;
+  }
   bool alltoallv(const void* send, const size_t* soff, const size_t* sbytes, void* recv,
                  const size_t* roff, const size_t* rbytes, cudaStream_t s) override {
     publish(send, soff, sbytes, s);
@@ -320,6 +345,173 @@ void loopback_hub_destroy(void* hub) { delete (Hub*)hub; }
 Transport* make_loopback_transport(void* hub, int rank) {
   if (!hub) return nullptr;
   return new LoopbackTransport((Hub*)hub, rank);
+}
+
+// ---------------------------------------------------------------------------
+// Host transport: one rank per process (any device, e.g. several processes sharing one
+// GPU in a test); the bytes of every collective go device -> host -> caller's host
+// all-gather -> host -> device, after the stream has drained.  Synchronous by design (a
+// test transport: the point is to run the sharded protocol, the CUDA IPC peer mappings and
+// the fused-exchange fences across real process boundaries without any kernel waiting on
+// another rank's kernel -- which two processes time-sliced on one GPU cannot guarantee).
+// ---------------------------------------------------------------------------
+namespace {
+
+struct HostTransport : Transport {
+  emb_host_comm hc;
+  int world = 1, rank = 0;
+  std::vector<void*> opened;
+  float* tmp = nullptr;  // device staging for the reductions ([world][count] floats)
+  size_t tmp_floats = 0;
+  ~HostTransport() override {
+    for (void* q : opened) cudaIpcCloseMemHandle(q);
+    if (tmp) cudaFree(tmp);
+  }
+  bool gather(const void* mine, void* all, size_t bytes) {
+    return hc.allgather(hc.ctx, mine, all, (int64_t)bytes) == 0;
+  }
+  bool dev_tmp(size_t floats) {
+    if (floats <= tmp_floats) return true;
+    if (tmp) cudaFree(tmp);
+    tmp = nullptr;
+    tmp_floats = 0;
+    if (cudaMalloc(&tmp, floats * sizeof(float)) != cudaSuccess) return false;
+    tmp_floats = floats;
+    return true;
+  }
+  bool allgather(const void* send, void* recv, size_t bytes, cudaStream_t s) override {
+    std::vector<uint8_t> h(bytes), all(bytes * world);
+    if (cudaStreamSynchronize(s) != cudaSuccess) return false;
+    if (bytes && cudaMemcpy(h.data(), send, bytes, cudaMemcpyDeviceToHost) != cudaSuccess) return false;
+    if (!gather(h.data(), all.data(), bytes)) return false;
+    return !bytes || cudaMemcpyAsync(recv, all.data(), bytes * world, cudaMemcpyHostToDevice, s) == cudaSuccess &&
+                         cudaStreamSynchronize(s) == cudaSuccess;
+  }
+  // reduce W device vectors (host-gathered, [world][count] in tmp) in rank order into dst
+  bool sum_ranks(float* dst, size_t count, cudaStream_t s) {
+    if (cudaMemcpyAsync(dst, tmp, count * sizeof(float), cudaMemcpyDeviceToDevice, s) != cudaSuccess) return false;
+    for (int r = 1; r < world && count; ++r) {
+      k_add_f32<<<148 * 4, 256, 0, s>>>(dst, tmp + (size_t)r * count, count);
+      if (cudaGetLastError() != cudaSuccess) return false;
+    }
+    return cudaStreamSynchronize(s) == cudaSuccess;
+  }
+  bool reduce_scatter_f32(const float* send, float* recv, size_t count, cudaStream_t s) override {
+    const size_t n = count * world;
+    std::vector<float> h(n), all(n * world), mine(n);
+    if (cudaStreamSynchronize(s) != cudaSuccess) return false;
+    if (n && cudaMemcpy(h.data(), send, n * 4, cudaMemcpyDeviceToHost) != cudaSuccess) return false;
+    if (!gather(h.data(), all.data(), n * 4)) return false;
+    for (int r = 0; r < world; ++r)  // rank r's slice for this rank
+      memcpy(mine.data() + (size_t)r * count, all.data() + (size_t)r * n + (size_t)rank * count, count * 4);
+    if (!dev_tmp(n)) return false;
+    if (n && cudaMemcpy(tmp, mine.data(), n * 4, cudaMemcpyHostToDevice) != cudaSuccess) return false;
+    return sum_ranks(recv, count, s);
+  }
+  bool allreduce_sum_f32(float* data, size_t count, float*, cudaStream_t s) override {
+    std::vector<float> h(count), all(count * world);
+    if (cudaStreamSynchronize(s) != cudaSuccess) return false;
+    if (count && cudaMemcpy(h.data(), data, count * 4, cudaMemcpyDeviceToHost) != cudaSuccess) return false;
+    if (!gather(h.data(), all.data(), count * 4)) return false;
+    if (!dev_tmp(count * world)) return false;
+    if (count && cudaMemcpy(tmp, all.data(), count * world * 4, cudaMemcpyHostToDevice) != cudaSuccess) return false;
+    return sum_ranks(data, count, s);
+  }
+  bool alltoallv(const void* send, const size_t* soff, const size_t* sbytes, void* recv,
+                 const size_t* roff, const size_t* rbytes, cudaStream_t s) override {
+    // every rank publishes [world sizes][its payloads for ranks 0..W-1], padded to the
+    // largest rank's size (one all-gather of the sizes first)
+    if (cudaStreamSynchronize(s) != cudaSuccess) return false;
+    int64_t tot = 0;
+    for (int r = 0; r < world; ++r) tot += (int64_t)sbytes[r];
+    std::vector<int64_t> tots(world);
+    if (!gather(&tot, tots.data(), sizeof(int64_t))) return false;
+    int64_t mx = 0;
+    for (int64_t t : tots) mx = t > mx ? t : mx;
+    const size_t hdr = sizeof(int64_t) * world, per = hdr + (size_t)mx;
+    std::vector<uint8_t> mine(per, 0), all(per * world);
+    int64_t at = 0;
+    for (int r = 0; r < world; ++r) {
+      const int64_t b = (int64_t)sbytes[r];
+      memcpy(mine.data() + sizeof(int64_t) * r, &b, sizeof(b));
+      if (b && cudaMemcpy(mine.data() + hdr + at, (const uint8_t*)send + soff[r], b, cudaMemcpyDeviceToHost) != cudaSuccess)
+        return false;
+      at += b;
+    }
+    if (!gather(mine.data(), all.data(), per)) return false;
+    for (int src = 0; src < world; ++src) {
+      const uint8_t* blk = all.data() + per * src;
+      int64_t off = 0, b = 0;
+      for (int r = 0; r <= rank; ++r) {
+        memcpy(&b, blk + sizeof(int64_t) * r, sizeof(b));
+        if (r < rank) off += b;
+      }
+      if ((size_t)b != rbytes[src]) return false;
+      if (b && cudaMemcpy((uint8_t*)recv + roff[src], blk + hdr + off, b, cudaMemcpyHostToDevice) != cudaSuccess)
+        return false;
+    }
+    return true;
+  }
+  bool barrier(void*, cudaStream_t s) override {
+    if (cudaStreamSynchronize(s) != cudaSuccess) return false;
+    uint8_t one = 1;
+    std::vector<uint8_t> all(world);
+    return gather(&one, all.data(), 1);
+  }
+  bool map_peers(void* const* local, int n, void** peers, void*, cudaStream_t s) override {
+    struct Rec { cudaIpcMemHandle_t h; int64_t off; int32_t ok, pad; };
+    if (cudaStreamSynchronize(s) != cudaSuccess) return false;
+    std::vector<Rec> mine(n), all((size_t)n * world);
+    for (int i = 0; i < n; ++i) {
+      memset(&mine[i], 0, sizeof(Rec));
+      void* base = nullptr;
+      mine[i].ok = alloc_base(local[i], &base) && cudaIpcGetMemHandle(&mine[i].h, base) == cudaSuccess;
+      mine[i].off = (int64_t)((uint8_t*)local[i] - (uint8_t*)base);
+    }
+    bool ok = gather(mine.data(), all.data(), sizeof(Rec) * n);
+    for (size_t k = 0; ok && k < all.size(); ++k) ok &= all[k].ok == 1;
+    std::vector<std::pair<cudaIpcMemHandle_t, void*>> cache;
+    std::vector<void*> mapped;
+    for (int r = 0; ok && r < world; ++r)
+      for (int i = 0; ok && i < n; ++i) {
+        if (r == rank) { peers[(size_t)i * world + r] = local[i]; continue; }
+        const Rec& x = all[(size_t)r * n + i];
+        void* b = nullptr;
+        for (auto& c : cache)
+          if (memcmp(&c.first, &x.h, sizeof(x.h)) == 0) b = c.second;
+        if (!b) {
+          ok = cudaIpcOpenMemHandle(&b, x.h, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess;
+          if (!ok) break;
+          cache.push_back({x.h, b});
+          mapped.push_back(b);
+        }
+        peers[(size_t)i * world + r] = (uint8_t*)b + x.off;
+      }
+    int32_t me = ok ? 1 : 0;  // agree on the verdict
+    std::vector<int32_t> v(world, 0);
+    if (!gather(&me, v.data(), sizeof(me))) ok = false;
+    for (int32_t q : v) ok &= q == 1;
+    if (!ok) {
+      for (void* b : mapped) cudaIpcCloseMemHandle(b);
+      cudaGetLastError();
+      return false;
+    }
+    opened.insert(opened.end(), mapped.begin(), mapped.end());
+    return true;
+  }
+};
+
+}  // namespace
+
+Transport* make_host_transport(const void* host_comm, int rank, int world) {
+  if (!host_comm) return nullptr;
+  const emb_host_comm* hc = (const emb_host_comm*)host_comm;
+  if (!hc->allgather) return nullptr;
+  auto* t = new HostTransport();
+  t->hc = *hc;
+  t->rank = rank;
+  t->world = world;
+  return t;
 }
 
 }  // namespace lirank

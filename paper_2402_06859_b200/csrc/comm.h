@@ -1,11 +1,15 @@
 // comm.h -- transports of the sharded exchange (a1/a3/a4 and the norm exchange).
 //
-// Two implementations behind one interface:
+// Three implementations behind one interface:
 // * NcclTransport: NCCL (torch's libnccl.so.2, dlopen'ed) over NVLink/NVSwitch, one rank
 //   per GPU, communicator created from a 128-B ncclUniqueId the caller distributes.
 // * LoopbackTransport: W ranks as W host threads of ONE process (test transport): every
 //   collective is a host rendezvous plus cudaMemcpyAsync between the ranks' buffers,
 //   ordered with CUDA events (no kernel ever waits on another rank's kernel).
+// * HostTransport: one rank per PROCESS, any devices (test transport for several processes
+//   on one GPU): every collective waits for the stream, moves the bytes through host memory
+//   with a caller-supplied host all-gather (e.g. torch.distributed over gloo), and copies
+//   them back; peer memory is mapped with CUDA IPC.  Kernels never wait on another rank.
 // All calls enqueue on the caller's stream and are collective (same order on all ranks).
 #pragma once
 
@@ -25,6 +29,9 @@ struct Transport {
   // bytes into recv + roff[r] (sizes must match pairwise; host arrays of length world).
   virtual bool alltoallv(const void* send, const size_t* soff, const size_t* sbytes, void* recv,
                          const size_t* roff, const size_t* rbytes, cudaStream_t s) = 0;
+  // data[0..count) = sum over ranks of data_r (fp32; every rank gets the same values).
+  // `scratch`: device, >= count floats, the transport may use it meanwhile.
+  virtual bool allreduce_sum_f32(float* data, size_t count, float* scratch, cudaStream_t s) = 0;
   // ---- fused exchange (EMB_F_P2P): peer memory ------------------------------------------
   // Collective, host-blocking.  Every rank passes n pointers into its own device buffers;
   // on success peers[i * world + r] is rank r's i-th pointer, addressable by this device's
@@ -48,5 +55,8 @@ bool nccl_get_unique_id(void* out128);
 void* loopback_hub_create(int world);
 void loopback_hub_destroy(void* hub);
 Transport* make_loopback_transport(void* hub, int rank);
+
+// Host transport over a caller-supplied host all-gather (emb_host_comm in the header).
+Transport* make_host_transport(const void* host_comm, int rank, int world);
 
 }  // namespace lirank

@@ -16,6 +16,8 @@ constexpr int kWarp = 32;
 // Sticky status bits (device word; emb_sync maps them to emb_status).
 constexpr uint32_t kStIdRange = 1u;
 constexpr uint32_t kStNonFinite = 2u;
+constexpr uint32_t kStOverflow = 4u;
+constexpr int kMaxDevices = 64;  // per-device caches of launch set-up (function attributes)  // sharded: received ids exceed a planned capacity
 
 // ---------------------------------------------------------------------------
 // Row-group geometry.  One "group" of LPB lanes (a power of two <= 32) owns one

@@ -9,8 +9,13 @@
 //       row-wise: id / ceil(rows/W)), already translated to the owner's stored-row key.
 //       Per destination the message is [features of that owner][B] bag lengths + the keys
 //       in (feature, sample, bag) order -- built by count -> exclusive scan -> stable
-//       scatter, then one count exchange (the only host sync of the step) and two
-//       all-to-alls (keys: variable sizes; lengths: sizes fixed by the plan).
+//       scatter, then a device-side count all-gather and the keys + lengths moved WITHOUT
+//       the host reading any count: fused (EMB_F_P2P) by one kernel storing each rank's
+//       keys at their compacted place in the owner's receive buffer; collective by an
+//       all-to-all of capacity-padded key slots ([W][pair_cap], sizes fixed by the plan)
+//       and an owner-side compaction.  The received count stays on the device (the a5-a8
+//       kernels read it), so a sharded step has no host synchronisation and can be
+//       captured as a CUDA graph.  Overflow of a planned capacity is a sticky error.
 //   owner: pools every source's bags with the a2 kernel into [src][B][Fr][D] and records
 //       the {key, grad row} pairs for its backward.
 //   a3: table-wise: all-to-all of the pooled blocks back + a column permute into
@@ -110,17 +115,21 @@ __global__ void k_bucket_scatter(const int* __restrict__ ids, const int* __restr
                                  const int32_t* __restrict__ owner0, const int32_t* __restrict__ blk,
                                  const int32_t* __restrict__ jmap, const int32_t* __restrict__ dest_base,
                                  const int64_t* __restrict__ key_base, const uint32_t* __restrict__ pos,
-                                 uint32_t* __restrict__ send_keys) {
+                                 uint32_t* __restrict__ send_keys, uint32_t pair_cap, uint32_t* status) {
   const int64_t bag = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (bag >= (int64_t)F * B) return;
   const int f = (int)(bag / B), b = (int)(bag - (int64_t)f * B);
   const int rows = meta[f].rows, o0 = owner0[f], bk = blk[f];
+  // p[o] = where the next key for owner o goes: contiguous by owner (pair_cap == 0), or
+  // slot o of a capacity-padded [W][pair_cap] buffer (the collective path's fixed sizes)
   uint32_t p[kMaxWorld];
 #pragma unroll
   for (int o = 0; o < kMaxWorld; ++o) {
     const int jj = o < W ? jmap[o * F + f] : -1;
     p[o] = jj >= 0 ? pos[((int64_t)dest_base[o] + jj) * B + b] : 0u;
+    if (pair_cap && jj >= 0) p[o] = p[o] - __ldg(pos + (int64_t)dest_base[o] * B) + (uint32_t)o * pair_cap;
   }
+  bool over = false;
   for (int j = __ldg(offsets + bag), e = __ldg(offsets + bag + 1); j < e; ++j) {
     const int id = __ldg(ids + j);
     if (id < 0 || id >= rows) continue;
@@ -130,8 +139,85 @@ __global__ void k_bucket_scatter(const int* __restrict__ ids, const int* __restr
 #pragma unroll
     for (int q = 0; q < kMaxWorld; ++q)
       if (q == o) { at = p[q]; p[q] = at + 1; }
+    if (pair_cap && at >= (uint32_t)(o + 1) * pair_cap) { over = true; continue; }
     send_keys[at] = key;
   }
+  if (over) atomicOr(status, kStOverflow);
+}
+
+// Counts of the whole exchange: cnt_all[s * W + o] = keys rank s sends owner o (all-gathered,
+// so every rank sees the same matrix).  The call overflows if some owner receives more than
+// its capacity or, collective path, some source's keys exceed their pair slot: then EVERY
+// rank discards it (decided identically everywhere from cnt_all): no keys are moved, the
+// owners' a1 lengths are zeroed (every bag pools to 0 and records no occurrence), the
+// row-wise slot sum outputs 0, and each rank raises the sticky overflow status.
+__device__ __forceinline__ bool exchange_overflow(const uint32_t* __restrict__ cnt_all, int W,
+                                                  uint32_t recv_cap, uint32_t pair_cap) {
+  bool over = false;
+  for (int o = 0; o < W; ++o) {
+    uint64_t tot = 0;
+    for (int s = 0; s < W; ++s) {
+      const uint32_t c = __ldg(cnt_all + s * W + o);
+      tot += c;
+      over |= pair_cap && c > pair_cap;
+    }
+    over |= tot > recv_cap;
+  }
+  return over;
+}
+
+__global__ void k_recv_guard(const uint32_t* __restrict__ cnt_all, int W, uint32_t recv_cap,
+                             uint32_t pair_cap, uint32_t* __restrict__ recv_lens, int64_t n_lens,
+                             uint32_t* status) {
+  if (!exchange_overflow(cnt_all, W, recv_cap, pair_cap)) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(status, kStOverflow);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_lens; i += (int64_t)gridDim.x * blockDim.x)
+    recv_lens[i] = 0u;
+}
+
+// Fused a1 (EMB_F_P2P): this rank's keys for owner o (blockIdx.y) go straight to their
+// compacted place in o's receive buffer -- after the keys of ranks 0..rank-1 (the
+// all-gathered counts), so every owner sees the sources in rank order -- and this rank's
+// [Fo][B] bag lengths to o's [rank][Fo][B] block.
+struct PushIds {
+  uint32_t* keys[kMaxWorld];  // each owner's recv_keys (peer mapping)
+  uint32_t* lens[kMaxWorld];  // each owner's recv_lens
+};
+__global__ void __launch_bounds__(256)
+k_push_ids(const uint32_t* __restrict__ send_keys, const uint32_t* __restrict__ pos,
+           const uint32_t* __restrict__ lens, const uint32_t* __restrict__ cnt_all,
+           const int32_t* __restrict__ dest_base, int W, int rank, int B, uint32_t recv_cap,
+           const PushIds pd) {
+  if (exchange_overflow(cnt_all, W, recv_cap, 0u)) return;  // discarded everywhere
+  const int o = blockIdx.y;
+  const uint32_t n = __ldg(cnt_all + rank * W + o);
+  uint32_t base = 0;
+  for (int s = 0; s < rank; ++s) base += __ldg(cnt_all + s * W + o);
+  const uint32_t* src = send_keys + __ldg(pos + (int64_t)__ldg(dest_base + o) * B);
+  uint32_t* dst = pd.keys[o] + base;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    dst[i] = __ldg(src + i);
+  const int Fo = __ldg(dest_base + o + 1) - __ldg(dest_base + o);
+  const int64_t nl = (int64_t)Fo * B;
+  const uint32_t* ls = lens + (int64_t)__ldg(dest_base + o) * B;
+  uint32_t* ld = pd.lens[o] + (int64_t)rank * nl;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nl; i += (int64_t)gridDim.x * blockDim.x)
+    ld[i] = __ldg(ls + i);
+}
+
+// Collective a1: the padded slots [W][pair_cap] of the received keys -> compacted in
+// source order (source s's keys after those of sources 0..s-1).
+__global__ void __launch_bounds__(256)
+k_compact_ids(const uint32_t* __restrict__ pad, const uint32_t* __restrict__ cnt_all, int W, int rank,
+              uint32_t pair_cap, uint32_t recv_cap, uint32_t* __restrict__ keys) {
+  if (exchange_overflow(cnt_all, W, recv_cap, pair_cap)) return;  // discarded everywhere
+  const int s = blockIdx.y;
+  uint32_t base = 0;
+  for (int q = 0; q < s; ++q) base += __ldg(cnt_all + q * W + rank);
+  const uint32_t n = __ldg(cnt_all + s * W + rank);
+  const uint32_t* src = pad + (size_t)s * pair_cap;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    keys[base + i] = __ldg(src + i);
 }
 
 // per-destination send counts from the scanned lengths
@@ -141,7 +227,8 @@ __global__ void k_send_counts(const uint32_t* __restrict__ pos, const int32_t* _
   if (o < W) cnt[o] = pos[(int64_t)dest_base[o + 1] * B] - pos[(int64_t)dest_base[o] * B];
 }
 
-// table-wise a3: out[b][f] = recv block of owner(f) at [b][j(f)]  (and the a4 transpose)
+// table-wise a3: out[b][f] = recv block of owner(f) at [b][j(f)]  (and the a4 transpose);
+// fmap[f] = {dest_base(owner), Fo(owner), j}: the block starts at dest_base * B
 template <bool TO_OUT>
 __global__ void k_permute(float* __restrict__ dense, float* __restrict__ blocks, int B, int F, int D,
                           const int32_t* __restrict__ fmap) {
@@ -151,7 +238,7 @@ __global__ void k_permute(float* __restrict__ dense, float* __restrict__ blocks,
     const int64_t row = i / D;
     const int d = (int)(i - row * D);
     const int b = (int)(row / F), f = (int)(row - (int64_t)b * F);
-    const int64_t src = ((int64_t)fmap[3 * f] + (int64_t)b * fmap[3 * f + 1] + fmap[3 * f + 2]) * D + d;
+    const int64_t src = ((int64_t)fmap[3 * f] * B + (int64_t)b * fmap[3 * f + 1] + fmap[3 * f + 2]) * D + d;
     if (TO_OUT) dense[i] = blocks[src];
     else blocks[src] = dense[i];
   }
@@ -207,7 +294,8 @@ __global__ void k_fence_sys() { __threadfence_system(); }
 // keeps one-hot and short bags off NVLink for all but the owners holding their ids.
 __global__ void __launch_bounds__(256)
 k_sum_slots(float* __restrict__ out, const float* __restrict__ slots, const uint32_t* __restrict__ lens,
-            int W, int B, int F, int D) {
+            int W, int B, int F, int D, const uint32_t* __restrict__ cnt_all, uint32_t recv_cap) {
+  const bool discard = exchange_overflow(cnt_all, W, recv_cap, 0u);  // the owners stored nothing
   const bool vec = (D & 3) == 0;
   const int nv = vec ? D / 4 : D;
   const int64_t n = (int64_t)B * F * D, total = (int64_t)B * F * nv;
@@ -220,7 +308,7 @@ k_sum_slots(float* __restrict__ out, const float* __restrict__ slots, const uint
       float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
       bool any = false;
       for (int o = 0; o < W; ++o) {
-        if (__ldg(lens + ((int64_t)o * F + f) * B + b) == 0) continue;
+        if (discard || __ldg(lens + ((int64_t)o * F + f) * B + b) == 0) continue;
         const float4 x = ld_nc_f4(slots + (int64_t)o * n + row * D + 4 * v);
         a = any ? f4_add_rn(a, x) : x;
         any = true;
@@ -230,7 +318,7 @@ k_sum_slots(float* __restrict__ out, const float* __restrict__ slots, const uint
       float a = 0.f;
       bool any = false;
       for (int o = 0; o < W; ++o) {
-        if (__ldg(lens + ((int64_t)o * F + f) * B + b) == 0) continue;
+        if (discard || __ldg(lens + ((int64_t)o * F + f) * B + b) == 0) continue;
         const float x = slots[(int64_t)o * n + row * D + v];
         a = any ? __fadd_rn(a, x) : x;
         any = true;
@@ -259,13 +347,16 @@ emb_status scan(emb_t h, const uint32_t* in, uint32_t* out, int64_t n, int which
 void carve_exchange(const Plan& p, Carver& cv, ExchangeWs* x) {
   const int64_t W = p.world, B = p.max_batch, F = p.F, Fr = p.Fr, D = p.D;
   const int64_t Ltot = B * p.dest_base[W];
+  const bool p2p = (p.flags & EMB_F_P2P) != 0;
   x->lens = cv.take<uint32_t>(Ltot);
   x->pos = cv.take<uint32_t>(Ltot + 1);
-  x->send_keys = cv.take<uint32_t>(p.max_nnz);
+  // fused: keys contiguous by owner (pushed from there); collective: [W][pair_cap] slots
+  x->send_keys = cv.take<uint32_t>(p2p ? p.max_nnz : W * p.pair_cap);
   x->cnt = cv.take<uint32_t>(W + W * W);
   x->recv_lens = cv.take<uint32_t>(W * Fr * B);
   x->recv_off = cv.take<uint32_t>(W * Fr * B + 1);
   x->recv_keys = cv.take<uint32_t>(p.recv_nnz_cap);
+  if (!p2p) x->recv_pad = cv.take<uint32_t>(W * p.pair_cap);
   x->pooled = cv.take<float>(W * B * Fr * D);
   x->xdense = cv.take<float>(B * F * D);
   x->ident = cv.take<FeatMeta>(W * Fr);
@@ -279,7 +370,7 @@ void carve_exchange(const Plan& p, Carver& cv, ExchangeWs* x) {
   x->scan_counter = cv.take<uint32_t>(4);
   const int64_t scan_n = std::max<int64_t>(Ltot + 1, W * Fr * B + 1);
   x->scan_status = cv.take<unsigned long long>((scan_n + kScanTile - 1) / kScanTile + 1);
-  if (p.flags & EMB_F_P2P) {
+  if (p2p) {
     if (p.sharding == EMB_SHARD_ROW) x->pslots = cv.take<float>(W * B * F * D);
     x->d_fcol = cv.take<int32_t>(Fr);
     x->p2p_scratch = cv.take<uint8_t>((int64_t)kPeerScratchBytes);
@@ -295,7 +386,7 @@ emb_status exchange_init(emb_t h) {
   if (p.sharding == EMB_SHARD_TABLE)
     for (int f = 0; f < F; ++f) {
       const int o = p.owner[p.feature_table[f]];
-      fmap[3 * f] = 0;  // filled with B at use (dest_base * B), see exchange_forward
+      fmap[3 * f] = p.dest_base[o];  // x B on the device (k_permute): no per-B upload
       fmap[3 * f + 1] = p.Fo[o];
       fmap[3 * f + 2] = p.jmap[(size_t)o * F + f];
     }
@@ -321,13 +412,16 @@ static emb_status map_p2p(emb_t h) {
   ExchangeWs& x = h->x;
   if (x.peer_pooled[0] != nullptr) return EMB_OK;
   const int W = h->p.world;
-  void* local[3] = {x.xdense, h->p.sharding == EMB_SHARD_ROW ? (void*)x.pslots : (void*)x.xdense, x.pooled};
-  void* peers[3 * kMaxWorld] = {};
-  if (!h->comm->map_peers(local, 3, peers, x.p2p_scratch, h->stream)) return EMB_ENCCL;
+  void* local[5] = {x.xdense, h->p.sharding == EMB_SHARD_ROW ? (void*)x.pslots : (void*)x.xdense, x.pooled,
+                    x.recv_keys, x.recv_lens};
+  void* peers[5 * kMaxWorld] = {};
+  if (!h->comm->map_peers(local, 5, peers, x.p2p_scratch, h->stream)) return EMB_ENCCL;
   for (int r = 0; r < W; ++r) {
     x.peer_xdense[r] = (float*)peers[0 * W + r];
     x.peer_pslots[r] = (float*)peers[1 * W + r];
     x.peer_pooled[r] = (float*)peers[2 * W + r];
+    x.peer_recv_keys[r] = (uint32_t*)peers[3 * W + r];
+    x.peer_recv_lens[r] = (uint32_t*)peers[4 * W + r];
   }
   return EMB_OK;
 }
@@ -347,33 +441,19 @@ static PeerOut peer_out(emb_t h) {
   return pm;
 }
 
-// fmap[3f] must hold dest_base(owner(f)) * B for the current B (B may change per call).
-static emb_status upload_fmap(emb_t h, int B) {
-  if (h->fmap_B == B) return EMB_OK;
-  h->fmap_B = B;
-  const Plan& p = h->p;
-  const int F = p.F;
-  std::vector<int32_t> fmap(3 * F);
-  for (int f = 0; f < F; ++f) {
-    const int o = p.owner[p.feature_table[f]];
-    fmap[3 * f] = p.dest_base[o] * B;
-    fmap[3 * f + 1] = p.Fo[o];
-    fmap[3 * f + 2] = p.jmap[(size_t)o * F + f];
-  }
-  CK(cudaMemcpyAsync(h->x.d_fmap, fmap.data(), 4 * fmap.size(), cudaMemcpyHostToDevice, h->stream));
-  CK(cudaStreamSynchronize(h->stream));
-  return EMB_OK;
-}
-
 emb_status exchange_forward(emb_t h, const Staged& st, int32_t batch, int64_t nnz, bool q8) {
   const Plan& p = h->p;
   const ExchangeWs& x = h->x;
   const int W = p.world, F = p.F, Fr = p.Fr, D = p.D, B = batch, r = p.rank;
   const int64_t Ltot = (int64_t)B * p.dest_base[W];
+  const int64_t n_lens = (int64_t)W * Fr * B;
   const unsigned bag_grid = (unsigned)(((int64_t)F * B + 255) / 256);
+  const bool p2p = (p.flags & EMB_F_P2P) != 0;
+  const uint32_t pair_cap = p2p ? 0u : (uint32_t)p.pair_cap;
+  const uint32_t recv_cap = (uint32_t)p.recv_nnz_cap;
+  uint32_t* cnt_all = x.cnt + W;  // [W][W], all-gathered
   emb_status s;
-  int64_t n_recv = 0;
-  if ((p.flags & EMB_F_P2P) && (s = map_p2p(h)) != EMB_OK) return s;
+  if (p2p && (s = map_p2p(h)) != EMB_OK) return s;
   {
     Phase ph(h->prof, h->stream, EMB_PH_EXCHANGE);
     // ---- a1: bucketize -----------------------------------------------------------------
@@ -387,41 +467,51 @@ emb_status exchange_forward(emb_t h, const Staged& st, int32_t batch, int64_t nn
     if (F * (int64_t)B > 0) {
       k_bucket_scatter<<<bag_grid, 256, 0, h->stream>>>(st.ids, st.offsets, B, F, W, h->d_meta, x.d_owner0,
                                                         x.d_blk, x.d_jmap, x.d_dest_base, x.d_key_base,
-                                                        x.pos, x.send_keys);
+                                                        x.pos, x.send_keys, pair_cap, h->d_status);
       h->launches += 1;
     }
     k_send_counts<<<1, 32, 0, h->stream>>>(x.pos, x.d_dest_base, W, B, x.cnt);
     h->launches += 1;
     CK(cudaGetLastError());
-    // one count exchange + host read: the only host sync of the step
-    if (!h->comm->allgather(x.cnt, x.cnt + W, sizeof(uint32_t) * W, h->stream)) return EMB_ENCCL;
-    h->h_cnt.resize((size_t)W * W);
-    CK(cudaMemcpyAsync(h->h_cnt.data(), x.cnt + W, 4ull * W * W, cudaMemcpyDeviceToHost, h->stream));
-    CK(cudaStreamSynchronize(h->stream));
-    std::vector<size_t> soff(W), sb(W), roff(W), rb(W);
-    size_t so = 0, ro = 0;
-    for (int o = 0; o < W; ++o) {
-      sb[o] = 4ull * h->h_cnt[(size_t)r * W + o];
-      soff[o] = so;
-      so += sb[o];
-      rb[o] = 4ull * h->h_cnt[(size_t)o * W + r];
-      roff[o] = ro;
-      ro += rb[o];
+    // the count matrix, on the device only.  (It also orders buffer reuse: no rank passes it
+    // before every rank has finished the previous call's reads of its receive buffers.)
+    if (!h->comm->allgather(x.cnt, cnt_all, sizeof(uint32_t) * W, h->stream)) return EMB_ENCCL;
+    if (p2p) {
+      PushIds pd;
+      memset(&pd, 0, sizeof(pd));
+      for (int o = 0; o < W; ++o) { pd.keys[o] = x.peer_recv_keys[o]; pd.lens[o] = x.peer_recv_lens[o]; }
+      k_push_ids<<<dim3(148 * 2, W), 256, 0, h->stream>>>(x.send_keys, x.pos, x.lens, cnt_all, x.d_dest_base,
+                                                           W, r, B, recv_cap, pd);
+      k_fence_sys<<<1, 1, 0, h->stream>>>();
+      h->launches += 2;
+      CK(cudaGetLastError());
+      if (!h->comm->barrier(x.p2p_scratch, h->stream)) return EMB_ENCCL;
+    } else {
+      std::vector<size_t> soff(W), sb(W), roff(W), rb(W);
+      for (int o = 0; o < W; ++o) {  // capacity-padded slots: sizes fixed by the plan
+        soff[o] = roff[o] = 4ull * o * p.pair_cap;
+        sb[o] = rb[o] = 4ull * p.pair_cap;
+      }
+      if (!h->comm->alltoallv(x.send_keys, soff.data(), sb.data(), x.recv_pad, roff.data(), rb.data(), h->stream))
+        return EMB_ENCCL;
+      // bag lengths: [Fo x B] to each owner; [Fr x B] from each source
+      for (int o = 0; o < W; ++o) {
+        soff[o] = 4ull * p.dest_base[o] * B;
+        sb[o] = 4ull * p.Fo[o] * B;
+        roff[o] = 4ull * o * Fr * B;
+        rb[o] = 4ull * Fr * B;
+      }
+      if (!h->comm->alltoallv(x.lens, soff.data(), sb.data(), x.recv_lens, roff.data(), rb.data(), h->stream))
+        return EMB_ENCCL;
+      k_compact_ids<<<dim3(148, W), 256, 0, h->stream>>>(x.recv_pad, cnt_all, W, r, pair_cap, recv_cap,
+                                                         x.recv_keys);
+      h->launches += 1;
+      CK(cudaGetLastError());
     }
-    n_recv = (int64_t)(ro / 4);
-    if (n_recv > p.recv_nnz_cap) return EMB_ENOMEM;
-    if (!h->comm->alltoallv(x.send_keys, soff.data(), sb.data(), x.recv_keys, roff.data(), rb.data(), h->stream))
-      return EMB_ENCCL;
-    // bag lengths: [Fo x B] to each owner; [Fr x B] from each source
-    for (int o = 0; o < W; ++o) {
-      soff[o] = 4ull * p.dest_base[o] * B;
-      sb[o] = 4ull * p.Fo[o] * B;
-      roff[o] = 4ull * o * Fr * B;
-      rb[o] = 4ull * Fr * B;
-    }
-    if (!h->comm->alltoallv(x.lens, soff.data(), sb.data(), x.recv_lens, roff.data(), rb.data(), h->stream))
-      return EMB_ENCCL;
-    if ((s = scan(h, x.recv_lens, x.recv_off, (int64_t)W * Fr * B, 1)) != EMB_OK) return s;
+    k_recv_guard<<<148, 256, 0, h->stream>>>(cnt_all, W, recv_cap, pair_cap, x.recv_lens, n_lens, h->d_status);
+    h->launches += 1;
+    CK(cudaGetLastError());
+    if ((s = scan(h, x.recv_lens, x.recv_off, n_lens, 1)) != EMB_OK) return s;
   }
   // ---- owner: pool every source's bags into [src][B][Fr][D] -------------------------------
   h->order_bags = -1;  // order_ws now holds the owner's order, not a local forward's
@@ -470,7 +560,7 @@ emb_status exchange_forward(emb_t h, const Staged& st, int32_t batch, int64_t nn
   // ---- a3: pooled exchange back ----------------------------------------------------------
   {
     Phase ph(h->prof, h->stream, EMB_PH_EXCHANGE);
-    if (p.flags & EMB_F_P2P) {
+    if (p2p) {
       // the owners' kernels stored straight into this rank's buffers; once every rank has
       // passed the barrier, they are complete
       k_fence_sys<<<1, 1, 0, h->stream>>>();
@@ -478,7 +568,7 @@ emb_status exchange_forward(emb_t h, const Staged& st, int32_t batch, int64_t nn
       if (!h->comm->barrier(x.p2p_scratch, h->stream)) return EMB_ENCCL;
       const int64_t n = (int64_t)B * F * D;
       if (n > 0 && p.sharding == EMB_SHARD_ROW) {
-        k_sum_slots<<<148 * 4, 256, 0, h->stream>>>(st.out, x.pslots, x.lens, W, B, F, D);
+        k_sum_slots<<<148 * 4, 256, 0, h->stream>>>(st.out, x.pslots, x.lens, W, B, F, D, cnt_all, recv_cap);
         h->launches += 1;
         CK(cudaGetLastError());
       } else if (n > 0) {
@@ -496,7 +586,6 @@ emb_status exchange_forward(emb_t h, const Staged& st, int32_t batch, int64_t nn
       }
       if (!h->comm->alltoallv(x.pooled, soff.data(), sb.data(), x.xdense, roff.data(), rb.data(), h->stream))
         return EMB_ENCCL;
-      if ((s = upload_fmap(h, B)) != EMB_OK) return s;
       if ((int64_t)B * F * D > 0) {
         k_permute<true><<<148 * 8, 256, 0, h->stream>>>(st.out, x.xdense, B, F, D, x.d_fmap);
         h->launches += 1;
@@ -505,8 +594,13 @@ emb_status exchange_forward(emb_t h, const Staged& st, int32_t batch, int64_t nn
     }
   }
   if (!q8) {
+    // the received count, for the backward's a5-a8 (device only; a later q8 forward reuses
+    // recv_off, so it is copied out here, in stream order before the dedup reads it)
+    CK(cudaMemcpyAsync(h->d_fwd_n, x.recv_off + n_lens, sizeof(uint32_t), cudaMemcpyDeviceToDevice, h->stream));
     h->have_fwd = true;
-    h->fwd_nnz = n_recv;
+    h->fwd_nnz = p.recv_nnz_cap;  // capacity: the kernels read the count from d_fwd_n
+    h->fwd_n_dev = h->d_fwd_n;
+    h->fwd_nnz_hint = nnz;
     h->fwd_B = B;
   }
   return EMB_OK;

@@ -61,6 +61,7 @@ struct Plan {
   int Fr = 0;                               // = Fo[rank]
   bool exch = false;                        // run the exchange path (world > 1, or forced)
   int64_t recv_nnz_cap = 0;                 // occurrences this rank may pool per step
+  int64_t pair_cap = 0;                     // collective a1: key slot per (source, owner)
   int64_t owner_bags_cap = 0;               // bags this rank may pool per step
 };
 
@@ -112,12 +113,13 @@ struct ExchangeWs {
   uint32_t* cnt = nullptr;        // [world] send counts, then [world][world] all counts
   uint32_t* recv_lens = nullptr;  // [world * Fr * B]
   uint32_t* recv_off = nullptr;   // [world * Fr * B + 1]
-  uint32_t* recv_keys = nullptr;  // [recv_nnz_cap]
+  uint32_t* recv_keys = nullptr;  // [recv_nnz_cap] received keys, compacted in source order
+  uint32_t* recv_pad = nullptr;   // collective: [world][pair_cap] received key slots
   float* pooled = nullptr;        // [world][B][Fr][D]: owner partials / owner grads
   float* xdense = nullptr;        // [B][F][D]: table-wise return / grad send blocks
   FeatMeta* ident = nullptr;      // [world * Fr] identity metas for the owner's pooling
   int32_t* d_jmap = nullptr;      // [world][F]
-  int32_t* d_fmap = nullptr;      // [F][3]: {dest_base(owner) * B, Fo(owner), j} (table-wise)
+  int32_t* d_fmap = nullptr;      // [F][3]: {dest_base(owner), Fo(owner), j} (table-wise)
   int32_t* d_feats_by_dest = nullptr;  // [F]: feats_of concatenated by dest (table-wise)
   int32_t* d_dest_base = nullptr;      // [world+1]
   int64_t* d_key_base = nullptr;       // [world][F]
@@ -132,6 +134,8 @@ struct ExchangeWs {
   float* peer_xdense[kMaxWorld] = {};  // table-wise: each rank's xdense (fwd destination)
   float* peer_pslots[kMaxWorld] = {};  // row-wise: each rank's pslots (fwd destination)
   float* peer_pooled[kMaxWorld] = {};  // each rank's pooled (bwd grad destination)
+  uint32_t* peer_recv_keys[kMaxWorld] = {};  // each rank's recv_keys (a1 key destination)
+  uint32_t* peer_recv_lens[kMaxWorld] = {};  // each rank's recv_lens
 };
 
 }  // namespace lirank
@@ -180,15 +184,18 @@ struct emb_handle {
   // sharded exchange
   lirank::ExchangeWs x{};
   lirank::Transport* comm = nullptr;
-  std::vector<uint32_t> h_cnt;  // [world][world] counts of the last forward
-  int fmap_B = -1;              // batch the table-wise permute map was uploaded for
+  uint32_t* d_fwd_n = nullptr;  // sharded: occurrences the last fp32 forward pooled here
   // NEXT-3 incremental-training penalty (emb_set_incremental)
   lirank::FimArgs fim{};
   bool fim_on = false;
   // state
   bool have_fwd = false;
   bool have_q8 = false;
-  int64_t fwd_nnz = 0;  // occurrences recorded (pooled on this rank) by the last forward
+  int64_t fwd_nnz = 0;  // occurrences recorded (pooled on this rank) by the last forward;
+                        // sharded: the capacity, the count itself is on the device:
+  const uint32_t* fwd_n_dev = nullptr;  // (sharded) device count, read by the a5-a6 kernels
+  int64_t fwd_nnz_hint = 0;  // the ids of the forward call (picks the segment-reduce chunk)
+  int chunk_log2 = lirank::kChunkLog2Max;  // segment-reduce chunk of the last dedup
   int fwd_B = 0;        // local batch of the last forward
   const uint2* sorted_kv = nullptr;
   // look-back epochs in device memory: [0] the dedup (side stream), [1] the exchange scans

@@ -94,25 +94,50 @@ struct SortWs {
   int64_t max_tiles;
 };
 
-// Sorts n pairs by the low `bits` bits of .x, stably.  Ping-pongs between kv0 and kv1;
+// Sorts n pairs by the low `bits` bits of .x, stably.  n is the launch capacity; with n_dev
+// (device scalar, optional) the kernels sort min(n, *n_dev) pairs -- the sharded path's
+// received count, never read by the host.  Ping-pongs between kv0 and kv1;
 // *result_in_1 tells whether the result is in kv1.  Uses epochs [*epoch, *epoch+passes): the
 // epoch is read from device memory by the kernels (graph-replayable), advanced by the caller.
-cudaError_t radix_sort_pairs(uint2* kv0, uint2* kv1, int64_t n, int bits, const SortWs& ws,
+cudaError_t radix_sort_pairs(uint2* kv0, uint2* kv1, int64_t n, const uint32_t* n_dev, int bits, const SortWs& ws,
                              const uint32_t* epoch, int* passes_out, bool* result_in_1, int64_t* launches,
                              cudaStream_t s);
 
 // Run-length encode sorted pairs (sentinel = invalid, sorts last): unique[U], seg[U+1],
-// *U_out, and chunk_u0[c] = segment containing occurrence c*kChunk.  For n == 0 the caller
-// writes U = 0, seg[0] = 0.
-cudaError_t launch_rle(const uint2* kv, int64_t n, uint32_t sentinel, uint32_t* unique,
-                       uint32_t* seg, uint32_t* U_out, uint32_t* chunk_u0, uint32_t* counter,
+// *U_out, and chunk_u0[c] = segment containing occurrence c << chunk_log2.  For n == 0 the
+// caller writes U = 0, seg[0] = 0; a device count *n_dev == 0 makes the kernel write them.
+cudaError_t launch_rle(const uint2* kv, int64_t n, const uint32_t* n_dev, uint32_t sentinel, uint32_t* unique,
+                       uint32_t* seg, uint32_t* U_out, uint32_t* chunk_u0, int chunk_log2, uint32_t* counter,
                        unsigned long long* status, const uint32_t* epoch, uint32_t epoch_off,
                        cudaStream_t s);
 // *epoch += n, in stream order after the kernels that used epochs [*epoch, *epoch + n)
 cudaError_t launch_epoch_advance(uint32_t* epoch, uint32_t n, cudaStream_t s);
 
 // ---- a6-a8 ----------------------------------------------------------------------------
-constexpr int kChunk = 256;  // occurrences per group in the segment-reduce
+// Occurrences per lane group in the segment-reduce: 2^chunk_log2, 32..256.  256 once the
+// batch fills every SM (Feed-1: 13.2M ids -> 51.7k chunks); smaller for small batches so
+// that ~kSegGroups groups still run (a 5k-id batch: 163 chunks of 32, not 21 of 256).
+constexpr int kChunkLog2Min = 5, kChunkLog2Max = 8;
+constexpr int64_t kSegGroups = 148 * 4 * 32;  // resident lane groups (148 SMs x 4 CTAs x 32)
+inline int chunk_log2_for(int64_t n) {
+  int l = kChunkLog2Min;
+  while (l < kChunkLog2Max && (n >> (l + 1)) >= kSegGroups) ++l;
+  return l;
+}
+// chunks a workspace must hold for any call of up to n occurrences (chunk_log2_for(m) for
+// every m <= n)
+inline int64_t chunks_cap_for(int64_t n) {
+  int64_t m = 0;
+  for (int l = kChunkLog2Min; l <= kChunkLog2Max; ++l) {
+    const int64_t lo = l == kChunkLog2Min ? 0 : (kSegGroups << l);  // smallest n using l
+    if (lo > n) break;
+    int64_t hi = n;
+    if (l < kChunkLog2Max && hi > (kSegGroups << (l + 1)) - 1) hi = (kSegGroups << (l + 1)) - 1;
+    const int64_t c = (hi + (int64_t(1) << l) - 1) >> l;
+    m = c > m ? c : m;
+  }
+  return m + 1;
+}
 
 struct BwdArgs {
   // dedup results
@@ -122,6 +147,7 @@ struct BwdArgs {
   const uint2* kv;          // sorted {key, bag} per occurrence
   const uint32_t* chunk_u0; // [chunks] segment containing the chunk's first occurrence
   int64_t nnz;              // upper bound of valid occurrences
+  int chunk_log2;           // segment-reduce chunk = 2^chunk_log2 occurrences (as the RLE's)
   // gradient input
   const float* grad;        // [B][F][D]
   const int* offsets;       // [F*B+1] (MEAN only)

@@ -75,8 +75,9 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp
 // ---------------------------------------------------------------------------
 template <int BITS>
 __global__ void __launch_bounds__(128)
-k_radix_hist(const uint2* __restrict__ kv, int64_t n, int passes, uint32_t* hist) {
+k_radix_hist(const uint2* __restrict__ kv, int64_t n, const uint32_t* n_dev, int passes, uint32_t* hist) {
   pdl_wait();
+  if (n_dev) n = min(n, (int64_t)*n_dev);  // device-resident count (sharded: no host sync)
   constexpr int BINS = 1 << BITS;
   extern __shared__ uint32_t sh[];  // [4 warps][passes][BINS]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -170,10 +171,11 @@ __device__ __forceinline__ void load_rank(const uint2* __restrict__ in, uint2 (&
 
 template <int BITS, int ITEMS, bool MATCH, int MINB = 4>
 __global__ void __launch_bounds__(kSortThreads, MINB)
-k_onesweep(const uint2* __restrict__ in, uint2* __restrict__ out, int64_t n, int shift,
-           const uint32_t* __restrict__ hist, uint32_t* tile_counter,
+k_onesweep(const uint2* __restrict__ in, uint2* __restrict__ out, int64_t n, const uint32_t* n_dev,
+           int shift, const uint32_t* __restrict__ hist, uint32_t* tile_counter,
            unsigned long long* status, const uint32_t* epoch_p, uint32_t epoch_off) {
   pdl_wait();
+  if (n_dev) n = min(n, (int64_t)*n_dev);
   constexpr int BINS = 1 << BITS;
   const uint32_t epoch = *epoch_p + epoch_off;  // device-resident: graph replays advance it
   constexpr int DPT = BINS / kSortThreads;  // digits per thread (1 or 2)
@@ -190,6 +192,9 @@ k_onesweep(const uint2* __restrict__ in, uint2* __restrict__ out, int64_t n, int
   __syncthreads();
   const int64_t tile = s_misc[NW];
   const int64_t tile0 = tile * TILE;
+  // grid sized for a capacity: tiles past the device count have nothing to do (no later
+  // tile looks back at them -- every later tile is past it too)
+  if (tile0 >= n) return;
   const int64_t base = tile0 + (int64_t)warp * (ITEMS * 32);
 
   uint2 kv[ITEMS];
@@ -266,24 +271,28 @@ k_onesweep(const uint2* __restrict__ in, uint2* __restrict__ out, int64_t n, int
 }
 
 template <int BITS, int ITEMS, bool MATCH, int MINB>
-static cudaError_t onesweep_pass(const uint2* a, uint2* b, int64_t n, int shift, const uint32_t* hist,
+static cudaError_t onesweep_pass(const uint2* a, uint2* b, int64_t n, const uint32_t* n_dev, int shift,
+                                 const uint32_t* hist,
                                  uint32_t* counter, unsigned long long* status, const uint32_t* epoch,
                                  uint32_t epoch_off, cudaStream_t s) {
   constexpr int TILE = kSortThreads * ITEMS;
   const size_t sm = sizeof(uint2) * TILE + sizeof(uint32_t) * (NW * (1 << BITS) + (1 << BITS) + NW + 2);
-  static bool attr = false;
-  if (!attr) {
+  // the attribute is per device: set once per device (before any graph capture of a step)
+  static bool attr[kMaxDevices] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= kMaxDevices || !attr[dev]) {
     cudaFuncSetAttribute(k_onesweep<BITS, ITEMS, MATCH, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    attr = true;
+    if (dev >= 0 && dev < kMaxDevices) attr[dev] = true;
   }
   const int64_t tiles = (n + TILE - 1) / TILE;
-  launch_pdl(k_onesweep<BITS, ITEMS, MATCH, MINB>, (unsigned)tiles, kSortThreads, sm, s, a, b, n, shift, hist,
+  launch_pdl(k_onesweep<BITS, ITEMS, MATCH, MINB>, (unsigned)tiles, kSortThreads, sm, s, a, b, n, n_dev, shift, hist,
                                                                                 counter, status, epoch,
                                                                                 epoch_off);
   return cudaGetLastError();
 }
 
-cudaError_t radix_sort_pairs(uint2* kv0, uint2* kv1, int64_t n, int bits, const SortWs& ws,
+cudaError_t radix_sort_pairs(uint2* kv0, uint2* kv1, int64_t n, const uint32_t* n_dev, int bits, const SortWs& ws,
                              const uint32_t* epoch, int* passes_out, bool* result_in_1, int64_t* launches,
                              cudaStream_t s) {
   // digit width: 9 bits when it saves a pass (e.g. 27-bit Feed-1 keys: 3 passes, not 4)
@@ -301,8 +310,8 @@ cudaError_t radix_sort_pairs(uint2* kv0, uint2* kv1, int64_t n, int bits, const 
     const int64_t want = (n + 128 * 8 - 1) / (128 * 8);
     const unsigned grid = (unsigned)(want < 148 * 8 ? want : 148 * 8);
     const size_t sm = sizeof(uint32_t) * 4 * passes * bins;
-    if (dbits == 9) launch_pdl(k_radix_hist<9>, grid, 128, sm, s, (const uint2*)kv0, n, passes, ws.hist);
-    else launch_pdl(k_radix_hist<8>, grid, 128, sm, s, (const uint2*)kv0, n, passes, ws.hist);
+    if (dbits == 9) launch_pdl(k_radix_hist<9>, grid, 128, sm, s, (const uint2*)kv0, n, n_dev, passes, ws.hist);
+    else launch_pdl(k_radix_hist<8>, grid, 128, sm, s, (const uint2*)kv0, n, n_dev, passes, ws.hist);
     launch_pdl(k_hist_excl, passes, 512, 0, s, ws.hist, bins);
     *launches += 2;
   }
@@ -315,7 +324,7 @@ cudaError_t radix_sort_pairs(uint2* kv0, uint2* kv1, int64_t n, int bits, const 
     // values stay in L1) measured best on Feed-1: the tile's global loads are latency-bound
     // and more resident CTAs overlap them (2 CTAs at 120 registers: +10% sort time; 8 or
     // 12 items at 5-8 CTAs and match.any ranking were slower)
-#define OS(BITS) e = onesweep_pass<BITS, 16, false, 4>(a, b, n, shift, hp, ctr, ws.status, epoch, (uint32_t)p, s);
+#define OS(BITS) e = onesweep_pass<BITS, 16, false, 4>(a, b, n, n_dev, shift, hp, ctr, ws.status, epoch, (uint32_t)p, s);
     if (dbits == 9) { OS(9) } else { OS(8) }
 #undef OS
     if (e != cudaSuccess) return e;
@@ -331,13 +340,15 @@ cudaError_t radix_sort_pairs(uint2* kv0, uint2* kv1, int64_t n, int bits, const 
 // A "head" is the first occurrence of a key; the first sentinel (invalid) key is also a
 // head, so its position is U and seg[U] = n_valid.  Without sentinels the tile holding
 // item n-1 writes seg[U] = n.  Also records, for every segment-reduce chunk c, the
-// segment that contains occurrence c*kChunk (chunk_u0[c]).
+// segment that contains occurrence c << chunk_log2 (chunk_u0[c]).  n: capacity (grid
+// size); n_dev (optional): the device-resident count, read by the kernel.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kSortThreads)
-k_rle(const uint2* __restrict__ kv, int64_t n, uint32_t sentinel, uint32_t* unique,
-      uint32_t* seg, uint32_t* U_out, uint32_t* chunk_u0, uint32_t* tile_counter,
+k_rle(const uint2* __restrict__ kv, int64_t n, const uint32_t* n_dev, uint32_t sentinel, uint32_t* unique,
+      uint32_t* seg, uint32_t* U_out, uint32_t* chunk_u0, int chunk_log2, uint32_t* tile_counter,
       unsigned long long* status, const uint32_t* epoch_p, uint32_t epoch_off) {
   pdl_wait();
+  if (n_dev) n = min(n, (int64_t)*n_dev);
   const uint32_t epoch = *epoch_p + epoch_off;
   __shared__ uint32_t s_tile;
   __shared__ uint32_t s_warp[NW];
@@ -346,6 +357,11 @@ k_rle(const uint2* __restrict__ kv, int64_t n, uint32_t sentinel, uint32_t* uniq
   if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
   __syncthreads();
   const int64_t tile = s_tile;
+  if (n == 0) {  // (device count 0) no occurrence: U = 0
+    if (tile == 0 && tid == 0) { *U_out = 0u; seg[0] = 0u; }
+    return;
+  }
+  if (tile * kSortTile >= n) return;  // past the device count
   const int64_t base = tile * kSortTile + (int64_t)warp * (kSortItems * 32);
   unsigned ball[kSortItems];
   uint32_t kk[kSortItems];
@@ -387,7 +403,7 @@ k_rle(const uint2* __restrict__ kv, int64_t n, uint32_t sentinel, uint32_t* uniq
       if (kk[i] != sentinel) unique[p] = kk[i];
       seg[p] = (uint32_t)idx;
     }
-    if (idx < n && (idx % kChunk) == 0) chunk_u0[idx / kChunk] = p + (head ? 1u : 0u) - 1u;
+    if (idx < n && (idx & ((1 << chunk_log2) - 1)) == 0) chunk_u0[idx >> chunk_log2] = p + (head ? 1u : 0u) - 1u;
     pos += __popc(ball[i]);
     if (idx == n - 1) {
       // pos now = number of heads in [0, n) (incl. the sentinel head if any)
@@ -399,14 +415,14 @@ k_rle(const uint2* __restrict__ kv, int64_t n, uint32_t sentinel, uint32_t* uniq
   }
 }
 
-cudaError_t launch_rle(const uint2* kv, int64_t n, uint32_t sentinel, uint32_t* unique,
-                       uint32_t* seg, uint32_t* U_out, uint32_t* chunk_u0, uint32_t* counter,
+cudaError_t launch_rle(const uint2* kv, int64_t n, const uint32_t* n_dev, uint32_t sentinel, uint32_t* unique,
+                       uint32_t* seg, uint32_t* U_out, uint32_t* chunk_u0, int chunk_log2, uint32_t* counter,
                        unsigned long long* status, const uint32_t* epoch, uint32_t epoch_off,
                        cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   const int64_t tiles = (n + kSortTile - 1) / kSortTile;
-  launch_pdl(k_rle, (unsigned)tiles, kSortThreads, 0, s, kv, n, sentinel, unique, seg, U_out, chunk_u0,
-                                                 counter, status, epoch, epoch_off);
+  launch_pdl(k_rle, (unsigned)tiles, kSortThreads, 0, s, kv, n, n_dev, sentinel, unique, seg, U_out, chunk_u0,
+                                                 chunk_log2, counter, status, epoch, epoch_off);
   return cudaGetLastError();
 }
 

@@ -26,6 +26,36 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
+class HostComm:
+    """Test transport (EMB_F_HOSTCOMM): one rank per process -- e.g. several processes on one
+    GPU -- with the library's collectives moved through host memory by a torch.distributed
+    all-gather over `group` (gloo).  Keep this object alive as long as the handle."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+
+        def _allgather(ctx, send, recv, nbytes):
+            try:
+                n = int(nbytes)
+                src = torch.zeros(n, dtype=torch.uint8)
+                if n:
+                    C.memmove(src.data_ptr(), send, n)
+                outs = [torch.empty(n, dtype=torch.uint8) for _ in range(self.world)]
+                dist.all_gather(outs, src, group=self.group)
+                if n:
+                    for r, o in enumerate(outs):
+                        C.memmove(recv + r * n, o.data_ptr(), n)
+                return 0
+            except Exception:  # pragma: no cover - reported to the library as a failure
+                return 1
+
+        self._cb = L.HOST_ALLGATHER(_allgather)
+        self.struct = L.EmbHostComm(None, self._cb)
+        self.ptr = C.cast(C.pointer(self.struct), C.c_void_p)
+
+
 class LoopbackHub:
     """Test transport: W ranks as W threads of one process on one device (EMB_F_LOOPBACK)."""
 
@@ -69,7 +99,8 @@ class ShardedEmbedding:
                  table_owner: Optional[Sequence[int]] = None, nccl_unique_id: Optional[bytes] = None,
                  loopback_hub: Optional["LoopbackHub"] = None, force_exchange: bool = False,
                  max_recv_nnz: int = 0, q8_mode: str = "middle_max", q8_only: bool = False,
-                 p2p: bool = False, guard_bytes: int = 0):
+                 p2p: bool = False, guard_bytes: int = 0, table_cost: Optional[Sequence[float]] = None,
+                 host_comm: Optional["HostComm"] = None):
         self.lib = L.load()
         assert q8_mode in ("middle_max", "min_max")
         self.q8_mode = q8_mode
@@ -91,6 +122,12 @@ class ShardedEmbedding:
         self._hub = loopback_hub
         if loopback_hub is not None:
             uid_ptr = loopback_hub.ptr
+        self._host_comm = host_comm
+        if host_comm is not None:
+            uid_ptr = host_comm.ptr
+        cost_p = None
+        if table_cost is not None:
+            self._cost, cost_p = _arr(np.asarray(table_cost, dtype=np.float64), C.c_double)
         self.cfg = L.EmbConfig(
             abi_version=L.EMB_ABI_VERSION, num_tables=len(self.table_rows), table_rows=rows_p,
             dim=self.dim, num_features=self.num_features, feature_table=ft_p,
@@ -107,8 +144,9 @@ class ShardedEmbedding:
             | (L.EMB_F_LOOPBACK if loopback_hub is not None else 0)
             | (L.EMB_F_EXCHANGE if force_exchange else 0)
             | (L.EMB_F_P2P if p2p else 0)
-            | (L.EMB_F_Q8_MINMAX if q8_mode == "min_max" else 0),
-            max_recv_nnz=int(max_recv_nnz))
+            | (L.EMB_F_Q8_MINMAX if q8_mode == "min_max" else 0)
+            | (L.EMB_F_HOSTCOMM if host_comm is not None else 0),
+            max_recv_nnz=int(max_recv_nnz), table_cost=cost_p)
         self.sizes = L.EmbSizes()
         L.check(self.lib.emb_plan(C.byref(self.cfg), C.byref(self.sizes)), "emb_plan")
         s = self.sizes
@@ -200,6 +238,13 @@ class ShardedEmbedding:
         for t in (w0, w1):
             assert t.is_cuda and t.dtype == torch.float32 and t.numel() == self.local_rows * self.pitch
         L.check(self.lib.emb_cold_weight_init(self.h, _ptr(w0), _ptr(w1), float(alpha)), "emb_cold_weight_init")
+
+    def allreduce_(self, t: torch.Tensor) -> torch.Tensor:
+        """In-place sum over the ranks of a device fp32 tensor, on the library's stream and
+        transport (the data-parallel dense side of NEXT-2)."""
+        assert t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()
+        L.check(self.lib.emb_allreduce_f32(self.h, _ptr(t), int(t.numel())), "emb_allreduce_f32")
+        return t
 
     def backward_adagrad_dev(self, grad: torch.Tensor, lr: float,
                              extra_sq_norm: Optional[torch.Tensor] = None,

@@ -9,6 +9,13 @@ step has no host synchronisation: the dense squared norm is handed to the librar
 device (``emb_backward_adagrad_dev``), the library returns the clip factor on the device,
 and the dense AdaGrad update reads it there.  The a5 dedup the forward launched on the
 library's side stream overlaps the tower's forward and backward.
+
+Data parallel (world_size > 1, "Other layers ... processed in a data parallel
+way"): every rank holds the same tower and its local batch; the loss each rank
+differentiates is its local mean / W, so the sum over ranks is the global-batch mean loss.
+The dense gradients are summed over ranks (emb_allreduce_f32, on the library stream and
+transport) BEFORE their squared norm is formed, so every rank folds the same dense term into
+the one global norm and applies the same dense update.
 """
 from typing import List, Optional
 
@@ -57,6 +64,7 @@ class FeedModel:
         self.c = torch.zeros(1, dtype=torch.float32, device=dev)
         self.S = torch.zeros(1, dtype=torch.float64, device=dev)
         self.dense_sq = torch.zeros(1, dtype=torch.float64, device=dev)
+        self.world = int(emb.cfg.world_size)
         self._pooled: Optional[torch.Tensor] = None
 
     def train_step(self, ids: torch.Tensor, offsets: torch.Tensor, batch: int, dense_x: torch.Tensor,
@@ -71,15 +79,24 @@ class FeedModel:
             x = torch.cat([p.view(batch, self.F * self.D), dense_x], dim=1)
             logits = self.tower(x)
             loss = torch.nn.functional.binary_cross_entropy_with_logits(logits, labels)
-            grads = torch.autograd.grad(loss, [p] + self.params)
-            g_pooled, g_dense = grads[0].contiguous(), grads[1:]
-            flat = torch.cat([g.reshape(-1) for g in g_dense]).double()
-            torch.sum(flat * flat, dim=0, keepdim=True, out=self.dense_sq)
+            # local mean / W: summed over the ranks this is the global-batch mean loss
+            grads = torch.autograd.grad(loss / self.world if self.world > 1 else loss, [p] + self.params)
+            g_pooled, g_dense = grads[0].contiguous(), list(grads[1:])
+            flat = torch.cat([g.reshape(-1) for g in g_dense])
+            if self.world > 1:  # data-parallel dense side: one all-reduce of all tower grads
+                emb.allreduce_(flat)
+                g_dense = [f.view_as(g) for f, g in zip(torch.split(flat, [g.numel() for g in g_dense]), g_dense)]
+            fd = flat.double()
+            torch.sum(fd * fd, dim=0, keepdim=True, out=self.dense_sq)
             emb.backward_adagrad_dev(g_pooled, self.lr, extra_sq_norm=self.dense_sq, clip_out=self.c,
                                      sq_norm_out=self.S)                       # a6-a8, global clip
-            c = torch.clamp(self.c, min=0.0)  # c = -1: non-finite norm -> no dense update either
+            # c = -1: the global norm was not finite (possibly because a dense gradient is
+            # inf/NaN) -- the sparse update was skipped, so skip the dense one too: the
+            # scaled gradient is masked to 0 (not multiplied by 0, which keeps a NaN)
+            ok = self.c >= 0
+            c = self.c.reshape(())
             with torch.no_grad():  # multi-tensor (foreach) AdaGrad: a few launches for all layers
-                gc = torch._foreach_mul(list(g_dense), c.reshape(()))
+                gc = [torch.where(ok, g * c, torch.zeros((), device=g.device)) for g in g_dense]
                 torch._foreach_addcmul_(self.acc, gc, gc)
                 den = torch._foreach_sqrt(self.acc)
                 torch._foreach_add_(den, self.eps)

@@ -152,7 +152,7 @@ def test_plan_serving_handle_has_no_fp32_tables():
     ft = np.array([0, 1, 0], dtype=np.int32)
 
     def plan(flags):
-        cfg = L.EmbConfig(abi_version=1, num_tables=2, table_rows=rows.ctypes.data_as(C.POINTER(C.c_int64)), dim=64,
+        cfg = L.EmbConfig(abi_version=L.EMB_ABI_VERSION, num_tables=2, table_rows=rows.ctypes.data_as(C.POINTER(C.c_int64)), dim=64,
                           num_features=3, feature_table=ft.ctypes.data_as(C.POINTER(C.c_int32)), pooling=0,
                           adagrad_mode=0, init_accumulator=0.1, eps=1e-7, max_norm=1.0, max_nnz=200_000,
                           max_batch=4096, sharding=0, table_owner=None, rank=0, world_size=1,

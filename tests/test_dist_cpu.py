@@ -47,7 +47,7 @@ def layout_of(rows, ft, D, rank, world, sharding):
     lib = L.load()
     ra = np.asarray(rows, dtype=np.int64)
     fa = np.asarray(ft, dtype=np.int32)
-    cfg = L.EmbConfig(abi_version=1, num_tables=len(rows), table_rows=ra.ctypes.data_as(C.POINTER(C.c_int64)),
+    cfg = L.EmbConfig(abi_version=L.EMB_ABI_VERSION, num_tables=len(rows), table_rows=ra.ctypes.data_as(C.POINTER(C.c_int64)),
                       dim=D, num_features=len(ft), feature_table=fa.ctypes.data_as(C.POINTER(C.c_int32)),
                       pooling=0, adagrad_mode=0, init_accumulator=0.1, eps=1e-7, max_norm=1.0, max_nnz=10000,
                       max_batch=256, sharding={"table": 1, "row": 2}[sharding], table_owner=None, rank=rank,

@@ -90,3 +90,115 @@ def test_feed_train_step_has_no_host_sync_and_overlaps_dedup(gpu):
     assert not ev.query()  # the host got here while the device is still busy
     torch.cuda.synchronize()
     assert emb.sync() == 0 and np.isfinite(float(loss))
+
+
+def test_feed_model_skips_dense_update_on_nonfinite_norm(gpu):
+    """a non-finite global norm (here from an inf dense feature, so the dense
+    gradients themselves are inf/NaN) skips BOTH updates: the library leaves the sparse rows
+    alone (c = -1) and the tower parameters and accumulators stay bit-identical (the scaled
+    gradient is masked to 0, not multiplied by 0)."""
+    from paper_2402_06859_b200 import _lib as L
+    from paper_2402_06859_b200.feed_model import FeedModel
+    cfg = small_cfg(dim=32, rows=(3000, 500, 80), F=[0, 1, 0, 2], B=64)
+    B, Dd = 64, 16
+    ids, off = gen.make_batch(cfg.table_rows, cfg.features, B, 3, 0)
+    emb = make_emb(cfg, max_nnz=len(ids), max_batch=B)
+    init_tables_host(emb, cfg)
+    model = FeedModel(emb, Dd, lr=0.05, seed=7)
+    dense = np.ones((B, Dd), dtype=np.float32)
+    dense[3, 5] = np.inf
+    labels = np.zeros(B, dtype=np.float32)
+    p0 = [p.detach().clone() for p in model.params]
+    a0 = [a.clone() for a in model.acc]
+    w0 = emb.weights.clone()
+    model.train_step(dev(ids), dev(off), B, dev(dense), dev(labels))
+    torch.cuda.synchronize()
+    assert emb.sync() == L.EMB_ENONFINITE
+    assert float(model.c) == -1.0
+    for p, q in zip(model.params, p0):
+        assert torch.equal(p.detach(), q)
+    for a, q in zip(model.acc, a0):
+        assert torch.equal(a, q)
+    assert torch.equal(emb.weights, w0)
+
+
+@pytest.mark.parametrize("sharding", ["row", "table"])
+def test_feed_model_data_parallel_w2_matches_global_batch_oracle(gpu, sharding):
+    """NEXT-2 at W = 2 (PAPER.md:576 data-parallel dense side, PAPER.md:17 one global clip):
+    two loopback ranks, each with its local batch and its own tower replica; the tower
+    gradients are summed over ranks (emb_allreduce_f32) before their norm, so both ranks
+    clip with the same c and end with identical towers -- equal to the oracle's single step on
+    the GLOBAL batch (2B samples)."""
+    import threading
+    from paper_2402_06859_b200 import LoopbackHub, ShardedEmbedding
+    from paper_2402_06859_b200.feed_model import FeedModel
+    from test_sharded_gpu import global_batch, run_ranks
+    torch.backends.cuda.matmul.allow_tf32 = False
+    W = 2
+    cfg = small_cfg(dim=32, rows=(3000, 500, 80), F=[0, 1, 0, 2], B=64)
+    B, Dd, F, D = 64, 16, cfg.num_features, cfg.dim
+    per_rank = [gen.make_batch(cfg.table_rows, cfg.features, B, 3 + r, 0) for r in range(W)]
+    nnz_max = max(len(i) for i, _ in per_rank)
+    rng = np.random.default_rng(5)
+    dense = rng.standard_normal((W * B, Dd)).astype(np.float32)
+    labels = rng.integers(0, 2, size=W * B).astype(np.float32)
+    hub = LoopbackHub(W)
+    models = []
+    for r in range(W):
+        e = ShardedEmbedding(cfg.table_rows, D, cfg.feature_table, max_nnz=nnz_max, max_batch=B,
+                             max_recv_nnz=W * nnz_max, device=gpu, stream=torch.cuda.Stream(), rank=r,
+                             world_size=W, sharding=sharding, loopback_hub=hub, p2p=True)
+        init_tables_host(e, cfg)
+        m = FeedModel(e, Dd, lr=0.05, seed=7)
+        with torch.no_grad():
+            for p in m.params:
+                p.mul_(40.0)  # clip active
+        models.append(m)
+    torch.cuda.synchronize()
+    params0 = [p.detach().cpu().double().numpy().copy() for p in models[0].params]
+
+    def step(r):
+        m = models[r]
+        ids, off = per_rank[r]
+        sl = slice(r * B, (r + 1) * B)
+        loss = m.train_step(dev(ids), dev(off), B, dev(dense[sl].copy()), dev(labels[sl].copy()))
+        torch.cuda.synchronize()
+        return float(loss), m.emb.sync()
+
+    res = run_ranks(W, step)
+    assert all(st == 0 for _, st in res)
+    ids_g, off_g = global_batch(per_rank, F, B)
+    Wt = dense_tables(cfg)
+    W0 = Wt.copy()
+    A = np.full(cfg.total_rows, 0.1, dtype=np.float32)
+    params = [p.copy() for p in params0]
+    accs = [np.full_like(p, 0.1) for p in params]
+    r_or = FM.feed_train_step(problem(cfg), Wt, A, ids_g, off_g, W * B, dense.astype(np.float64),
+                              labels.astype(np.float64), params, accs, 0.05, 1e-7, 1.0)
+    assert abs(np.mean([l for l, _ in res]) - r_or["loss"]) <= 1e-5 * abs(r_or["loss"])
+    assert r_or["c"] < 1.0
+    for m in models:
+        assert abs(float(m.S) - r_or["S"]) <= 1e-5 * r_or["S"]
+        assert abs(float(m.c) - float(r_or["c"])) <= 1e-5 * float(r_or["c"])
+    # identical tower replicas, each equal to the oracle's update
+    for a, b in zip(models[0].params, models[1].params):
+        assert torch.equal(a, b)
+    for got, ref, old in zip(models[0].params, params, params0):
+        g = got.detach().cpu().double().numpy()
+        stp = np.abs(ref - old)
+        assert (np.abs(g - ref) <= 1e-3 * stp + 4 * np.spacing(np.abs(ref).astype(np.float32))).all()
+    # sparse rows, from their owners
+    base = np.concatenate([[0], np.cumsum(cfg.table_rows)])
+    for t, R in enumerate(cfg.table_rows):
+        for m in models:
+            e = m.emb
+            lo, hi = int(e.row_lo[t]), int(e.row_hi[t])
+            if e.local_base[t] < 0 or hi <= lo:
+                continue
+            w = e.read_rows(t, np.arange(lo, hi), with_acc=False)
+            sl = slice(base[t] + lo, base[t] + hi)
+            stp = np.abs(Wt[sl] - W0[sl])
+            assert (np.abs(w - Wt[sl]) <= 1e-3 * stp + 4 * np.spacing(np.abs(Wt[sl]))).all()
+    for m in models:
+        m.emb.close()
+    hub.close()

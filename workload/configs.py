@@ -124,6 +124,27 @@ def feedq8() -> Config:
                   note="BASELINE.json configs[4]")
 
 
+def bag_mean(kind) -> float:
+    if kind[0] == "onehot":
+        return 1.0
+    if kind[0] == "multi":
+        return float(kind[1])
+    return (kind[1] + kind[2]) / 2.0
+
+
+def table_cost(cfg: Config, batch: int = None) -> List[float]:
+    """Table-wise planning weight: per table, the algorithmic bytes one step
+    moves for it, sum over the features reading it of B * L_f * (4 + 4 D) (ids + row gathers)
+    + B * 4 D (the pooled row).  Passed as emb_config.table_cost so the LPT placement balances
+    lookup traffic, not rows."""
+    B = cfg.batch if batch is None else batch
+    row = 4 * cfg.dim
+    cost = [0.0] * cfg.num_tables
+    for (t, kind) in cfg.features:
+        cost[t] += B * bag_mean(kind) * (4 + row) + B * row
+    return cost
+
+
 CONFIGS = {c.__name__: c for c in (tiny, jobs, jobs_shared, ads, feed1, feed8, feedq8)}
 
 
