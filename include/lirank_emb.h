@@ -263,8 +263,8 @@ EMB_API emb_status emb_backward_adagrad(emb_t h, const float* grad_out, float lr
  * library stream and transport (NCCL all-reduce; loopback / host transports sum in rank
  * order).  Every rank ends with identical values -- which is what makes the dense squared
  * norm a caller then passes as extra_sq_norm(_dev) identical on every rank, as the global
- * clip requires.  count <= max_batch * num_features * dim (the staging scratch), else
- * EMB_EINVAL.  world_size 1: no-op. */
+ * clip requires.  world_size 1: no-op.  (The loopback transport stages through a device
+ * buffer it allocates on first use, so do not call it first inside a graph capture.) */
 EMB_API emb_status emb_allreduce_f32(emb_t h, float* data, int64_t count);
 
 /* As emb_backward_adagrad, with no host synchronisation for a dense side on the device

@@ -14,14 +14,16 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "liboracle.so")
+LIB_OMP_PATH = os.path.join(_HERE, "liboracle_omp.so")  # same source, -fopenmp
 CFLAGS = ["-O2", "-std=c99", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared"]
 
 
 def build(force: bool = False) -> str:
     src = os.path.join(_HERE, "oracle.c")
-    if force or not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < max(
-            os.path.getmtime(src), os.path.getmtime(os.path.join(_HERE, "oracle.h"))):
-        subprocess.check_call(["gcc", *CFLAGS, src, "-o", LIB_PATH, "-lm"])
+    newest = max(os.path.getmtime(src), os.path.getmtime(os.path.join(_HERE, "oracle.h")))
+    for path, extra in ((LIB_PATH, []), (LIB_OMP_PATH, ["-fopenmp"])):
+        if force or not os.path.exists(path) or os.path.getmtime(path) < newest:
+            subprocess.check_call(["gcc", *CFLAGS, *extra, src, "-o", path, "-lm"])
     return LIB_PATH
 
 
@@ -31,14 +33,26 @@ class _Cfg(C.Structure):
                 ("feature_table", C.POINTER(C.c_int32)), ("pooling", C.c_int32)]
 
 
-_lib = None
+_libs = {}
+_parallel = False
+
+
+def set_parallel(on: bool, threads: int = 0) -> int:
+    """Route every oracle call to the OpenMP build (on) or the sequential one (off).  Both
+    give bit-identical results; returns the thread count now in use."""
+    global _parallel
+    _parallel = bool(on)
+    L = lib()
+    if on and threads > 0:
+        L.ora_set_threads(int(threads))
+    return int(L.ora_threads())
 
 
 def lib():
-    global _lib
-    if _lib is None:
+    path = LIB_OMP_PATH if _parallel else LIB_PATH
+    if path not in _libs:
         build()
-        L = C.CDLL(LIB_PATH)
+        L = C.CDLL(path)
         P = C.c_void_p
         i32, i64, f32, f64 = C.c_int32, C.c_int64, C.c_float, C.c_double
         sig = {
@@ -64,13 +78,15 @@ def lib():
             "ora_fim_penalty": (f64, [P, i64, P, P, P, P, f32, f32]),
             "ora_fim_penalty_grad": (None, [P, P, i64, i32, P, P, P, P, f32, f32, P]),
             "ora_train_step_fim": (i32, [P, P, P, i32, P, P, i32, P, f32, f32, f32, f64, P, P, P, P, f32, f32, P, P]),
+            "ora_threads": (i32, []),
+            "ora_set_threads": (None, [i32]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args
-        _lib = L
-    return _lib
+        _libs[path] = L
+    return _libs[path]
 
 
 def _p(a):

@@ -4,12 +4,40 @@
  * step by step; the paper passages are cited at each definition in oracle.h.
  *
  * Build: gcc -O2 -std=c99 -ffp-contract=off -fno-fast-math -fPIC -shared oracle.c -lm
+ * (liboracle.so, sequential), and the same source with -fopenmp (liboracle_omp.so): the
+ * OpenMP pragmas only split loops whose iterations are independent -- bags (a2, a10),
+ * segments (a6), unique rows (a8), table rows (a9), and the a5 sort into key ranges (the
+ * concatenation of range-sorted buckets is the same total (key, occurrence) order) -- so
+ * every arithmetic operation, and its order within an output, is the sequential one and
+ * both builds give bit-identical results (tests/test_oracle_omp.py).  The global norm
+ * (one running fp64 sum in (u, d) order) stays sequential.
  */
 #include "oracle.h"
 
 #include <math.h>
 #include <stdlib.h>
 #include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+static int ora_nthreads(void) {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}
+
+int32_t ora_threads(void) { return (int32_t)ora_nthreads(); }
+
+void ora_set_threads(int32_t n) {
+#ifdef _OPENMP
+  if (n > 0) omp_set_num_threads(n);
+#else
+  (void)n;
+#endif
+}
 
 /* ------------------------------------------------------------------------- */
 /* Row addressing                                    */
@@ -37,12 +65,15 @@ static int64_t row_key(const ora_cfg* c, const int64_t* base, int32_t f, int32_t
 int64_t ora_forward(const ora_cfg* c, const float* W, const int32_t* ids,
                     const int32_t* offsets, int32_t B, float* out) {
   const int32_t D = c->dim, F = c->num_features;
+  const int64_t nbags = (int64_t)F * B;
   int64_t invalid = 0;
   int64_t* base = table_bases(c);
-  float* acc = (float*)malloc(sizeof(float) * (size_t)D);
-  for (int32_t f = 0; f < F; ++f) {
-    for (int32_t b = 0; b < B; ++b) {
-      int64_t bag = (int64_t)f * B + b;
+#pragma omp parallel reduction(+ : invalid)
+  {
+    float* acc = (float*)malloc(sizeof(float) * (size_t)D);
+#pragma omp for schedule(dynamic, 512)
+    for (int64_t bag = 0; bag < nbags; ++bag) {
+      int32_t f = (int32_t)(bag / B), b = (int32_t)(bag % B);
       int32_t lo = offsets[bag], hi = offsets[bag + 1];
       for (int32_t d = 0; d < D; ++d) acc[d] = 0.0f;
       for (int32_t j = lo; j < hi; ++j) {
@@ -58,8 +89,8 @@ int64_t ora_forward(const ora_cfg* c, const float* W, const int32_t* ids,
       float* o = out + ((int64_t)b * F + f) * D;
       for (int32_t d = 0; d < D; ++d) o[d] = acc[d];
     }
+    free(acc);
   }
-  free(acc);
   free(base);
   return invalid;
 }
@@ -76,6 +107,35 @@ static int cmp_occ(const void* a, const void* b) {
   if (x->key != y->key) return x->key < y->key ? -1 : 1;
   if (x->occ != y->occ) return x->occ < y->occ ? -1 : 1; /* stability, explicitly */
   return 0;
+}
+
+/* Sort by (key, occurrence).  With several threads: P buckets of equal key ranges,
+ * scattered in occurrence order and sorted each on its own thread; buckets hold disjoint,
+ * increasing key ranges, so their concatenation is the one (key, occurrence) order. */
+static void sort_occ(occ_t* v, int64_t n) {
+  const int P = ora_nthreads();
+  if (P <= 1 || n < 65536) {
+    qsort(v, (size_t)n, sizeof(occ_t), cmp_occ);
+    return;
+  }
+  int64_t kmax = 0;
+  for (int64_t k = 0; k < n; ++k)
+    if (v[k].key > kmax) kmax = v[k].key;
+  const int64_t span = kmax / P + 1;
+  int64_t* start = (int64_t*)calloc((size_t)P + 1, sizeof(int64_t));
+  for (int64_t k = 0; k < n; ++k) ++start[v[k].key / span + 1];
+  for (int p = 0; p < P; ++p) start[p + 1] += start[p];
+  int64_t* at = (int64_t*)malloc(sizeof(int64_t) * (size_t)P);
+  memcpy(at, start, sizeof(int64_t) * (size_t)P);
+  occ_t* tmp = (occ_t*)malloc(sizeof(occ_t) * (size_t)n);
+  for (int64_t k = 0; k < n; ++k) tmp[at[v[k].key / span]++] = v[k];
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int p = 0; p < P; ++p)
+    qsort(tmp + start[p], (size_t)(start[p + 1] - start[p]), sizeof(occ_t), cmp_occ);
+  memcpy(v, tmp, sizeof(occ_t) * (size_t)n);
+  free(tmp);
+  free(at);
+  free(start);
 }
 
 int64_t ora_dedup(const ora_cfg* c, const int32_t* ids, const int32_t* offsets, int32_t B,
@@ -95,7 +155,7 @@ int64_t ora_dedup(const ora_cfg* c, const int32_t* ids, const int32_t* offsets, 
         v[n].key = key; v[n].occ = j; v[n].bag = bag; ++n;
       }
     }
-  qsort(v, (size_t)n, sizeof(occ_t), cmp_occ);
+  sort_occ(v, n);
   int64_t U = 0;
   for (int64_t k = 0; k < n; ++k) {
     if (k == 0 || v[k].key != v[k - 1].key) {
@@ -120,24 +180,28 @@ void ora_segment_reduce(const ora_cfg* c, const int32_t* offsets, int32_t B, int
                         const int64_t* seg_offsets, const int64_t* sorted_bags,
                         const float* grad, float* G) {
   const int32_t D = c->dim, F = c->num_features;
-  double* acc = (double*)malloc(sizeof(double) * (size_t)D);
-  for (int64_t u = 0; u < U; ++u) {
-    for (int32_t d = 0; d < D; ++d) acc[d] = 0.0;
-    for (int64_t k = seg_offsets[u]; k < seg_offsets[u + 1]; ++k) {
-      int64_t bag = sorted_bags[k];
-      int64_t f = bag / B, b = bag % B;
-      const float* g = grad + (b * F + f) * D;
-      if (c->pooling == 1) {
-        int32_t L = offsets[bag + 1] - offsets[bag];
-        double inv = 1.0 / (double)L;
-        for (int32_t d = 0; d < D; ++d) acc[d] = acc[d] + (double)g[d] * inv;
-      } else {
-        for (int32_t d = 0; d < D; ++d) acc[d] = acc[d] + (double)g[d];
+#pragma omp parallel
+  {
+    double* acc = (double*)malloc(sizeof(double) * (size_t)D);
+#pragma omp for schedule(dynamic, 256)
+    for (int64_t u = 0; u < U; ++u) {
+      for (int32_t d = 0; d < D; ++d) acc[d] = 0.0;
+      for (int64_t k = seg_offsets[u]; k < seg_offsets[u + 1]; ++k) {
+        int64_t bag = sorted_bags[k];
+        int64_t f = bag / B, b = bag % B;
+        const float* g = grad + (b * F + f) * D;
+        if (c->pooling == 1) {
+          int32_t L = offsets[bag + 1] - offsets[bag];
+          double inv = 1.0 / (double)L;
+          for (int32_t d = 0; d < D; ++d) acc[d] = acc[d] + (double)g[d] * inv;
+        } else {
+          for (int32_t d = 0; d < D; ++d) acc[d] = acc[d] + (double)g[d];
+        }
       }
+      for (int32_t d = 0; d < D; ++d) G[u * D + d] = (float)acc[d];
     }
-    for (int32_t d = 0; d < D; ++d) G[u * D + d] = (float)acc[d];
+    free(acc);
   }
-  free(acc);
 }
 
 /* ------------------------------------------------------------------------- */
@@ -162,6 +226,7 @@ float ora_clip_factor(double S, float max_norm, int* nonfinite) {
 }
 
 void ora_clip(const float* G, int64_t n, float c, float* g) {
+#pragma omp parallel for schedule(static)
   for (int64_t i = 0; i < n; ++i) g[i] = G[i] * c;
 }
 
@@ -171,6 +236,7 @@ void ora_clip(const float* G, int64_t n, float c, float* g) {
 
 void ora_adagrad_rowwise(float* W, float* A, const int64_t* keys, int64_t U,
                          const float* g, int32_t dim, float lr, float eps) {
+#pragma omp parallel for schedule(static)
   for (int64_t u = 0; u < U; ++u) {
     int64_t r = keys[u];
     const float* gu = g + u * dim;
@@ -188,6 +254,7 @@ void ora_adagrad_rowwise(float* W, float* A, const int64_t* keys, int64_t U,
 
 void ora_adagrad_elementwise(float* W, float* A, const int64_t* keys, int64_t U,
                              const float* g, int32_t dim, float lr, float eps) {
+#pragma omp parallel for schedule(static)
   for (int64_t u = 0; u < U; ++u) {
     int64_t r = keys[u];
     const float* gu = g + u * dim;
@@ -247,6 +314,7 @@ int32_t ora_quantize_row(const float* x, int32_t dim, int8_t* codes, float* midd
 int64_t ora_quantize_mm8(const float* X, int64_t rows, int32_t dim, int8_t* codes,
                          float* middle, float* scale) {
   int64_t bad = 0;
+#pragma omp parallel for schedule(static) reduction(+ : bad)
   for (int64_t r = 0; r < rows; ++r)
     bad += ora_quantize_row(X + r * dim, dim, codes + r * dim, middle + r, scale + r);
   return bad;
@@ -260,12 +328,15 @@ int64_t ora_forward_q8(const ora_cfg* c, const int8_t* codes, const float* middl
                        const float* scale, const int32_t* ids, const int32_t* offsets,
                        int32_t B, float* out) {
   const int32_t D = c->dim, F = c->num_features;
+  const int64_t nbags = (int64_t)F * B;
   int64_t invalid = 0;
   int64_t* base = table_bases(c);
-  float* acc = (float*)malloc(sizeof(float) * (size_t)D);
-  for (int32_t f = 0; f < F; ++f)
-    for (int32_t b = 0; b < B; ++b) {
-      int64_t bag = (int64_t)f * B + b;
+#pragma omp parallel reduction(+ : invalid)
+  {
+    float* acc = (float*)malloc(sizeof(float) * (size_t)D);
+#pragma omp for schedule(dynamic, 512)
+    for (int64_t bag = 0; bag < nbags; ++bag) {
+      int32_t f = (int32_t)(bag / B), b = (int32_t)(bag % B);
       int32_t lo = offsets[bag], hi = offsets[bag + 1];
       for (int32_t d = 0; d < D; ++d) acc[d] = 0.0f;
       for (int32_t j = lo; j < hi; ++j) {
@@ -284,7 +355,8 @@ int64_t ora_forward_q8(const ora_cfg* c, const int8_t* codes, const float* middl
       float* o = out + ((int64_t)b * F + f) * D;
       for (int32_t d = 0; d < D; ++d) o[d] = acc[d];
     }
-  free(acc);
+    free(acc);
+  }
   free(base);
   return invalid;
 }

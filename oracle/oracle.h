@@ -6,7 +6,11 @@
  * (paper_2402_06859_b200/) never includes, links or calls anything in this directory,
  * and this directory never includes anything from the product.
  *
- * Plain, sequential, obviously-correct C99.  Built with -O2 -ffp-contract=off and no
+ * Plain, obviously-correct C99; sequential as liboracle.so.  The same source built with
+ * -fopenmp (liboracle_omp.so, for timing the oracle on all host cores) runs independent
+ * iterations (bags, segments, rows, key-range sort buckets) on several threads without
+ * changing any operation or its order within an output: both builds are bit-identical.
+ * Built with -O2 -ffp-contract=off and no
  * fast-math, so every float operation below is one IEEE-754 binary32 round-to-nearest
  * operation in the written order ("fl(.)" in SURVEY.md §8(c)).  Sums that the contract
  * accumulates in fp64 are plain sequential double sums.
@@ -25,6 +29,10 @@
 #ifdef __cplusplus
 extern "C" {
 #endif
+
+/* threads the OpenMP build uses (1 for liboracle.so); set them (no-op sequentially) */
+int32_t ora_threads(void);
+void ora_set_threads(int32_t n);
 
 typedef struct {
   int32_t num_tables;

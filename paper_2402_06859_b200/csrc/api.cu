@@ -857,11 +857,10 @@ emb_status emb_backward_adagrad(emb_t h, const float* grad_out, float lr, double
 emb_status emb_allreduce_f32(emb_t h, float* data, int64_t count) {
   if (!h || count < 0 || (count > 0 && !data)) return EMB_EINVAL;
   const Plan& p = h->p;
-  if (count > std::max<int64_t>((int64_t)p.max_batch * p.F * p.D, 1)) return EMB_EINVAL;
   if (count == 0 || !p.exch) return EMB_OK;
   if (!is_device_ptr(data)) return EMB_EINVAL;
   Phase ph(h->prof, h->stream, EMB_PH_EXCHANGE);
-  return h->comm->allreduce_sum_f32(data, (size_t)count, h->stage_dense, h->stream) ? EMB_OK : EMB_ENCCL;
+  return h->comm->allreduce_sum_f32(data, (size_t)count, h->stream) ? EMB_OK : EMB_ENCCL;
 }
 
 emb_status emb_backward_adagrad_dev(emb_t h, const float* grad_out, float lr,

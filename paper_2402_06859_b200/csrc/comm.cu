@@ -151,7 +151,7 @@ struct NcclTransport : Transport {
   bool reduce_scatter_f32(const float* send, float* recv, size_t count, cudaStream_t s) override {
     return nccl::api().ReduceScatter(send, recv, count, nccl::kFloat32, nccl::kSum, comm, s) == 0;
   }
-  bool allreduce_sum_f32(float* data, size_t count, float*, cudaStream_t s) override {
+  bool allreduce_sum_f32(float* data, size_t count, cudaStream_t s) override {
     return nccl::api().AllReduce(data, data, count, nccl::kFloat32, nccl::kSum, comm, s) == 0;
   }
   bool alltoallv(const void* send, const size_t* soff, const size_t* sbytes, void* recv,
@@ -244,6 +244,7 @@ struct LoopbackTransport : Transport {
   ~LoopbackTransport() override {
     cudaEventDestroy(ready);
     cudaEventDestroy(done);
+    if (scratch) cudaFree(scratch);
   }
   // phase 1: publish + barrier; caller issues its reads; phase 2: done + barriers.
   void publish(const void* send, const size_t* soff, const size_t* sbytes, cudaStream_t s) {
@@ -290,7 +291,17 @@ struct LoopbackTransport : Transport {
     finish(s);
     return ok;
   }
-  bool allreduce_sum_f32(float* data, size_t count, float* scratch, cudaStream_t s) override {
+  float* scratch = nullptr;  // allreduce staging (grown on demand: a test transport)
+  size_t scratch_floats = 0;
+  bool allreduce_sum_f32(float* data, size_t count, cudaStream_t s) override {
+    if (count > scratch_floats) {
+      if (cudaStreamSynchronize(s) != cudaSuccess) return false;
+      if (scratch) cudaFree(scratch);
+      scratch = nullptr;
+      scratch_floats = 0;
+      if (cudaMalloc(&scratch, count * sizeof(float)) != cudaSuccess) return false;
+      scratch_floats = count;
+    }
     publish(data, nullptr, nullptr, s);
     bool ok = true;
     for (int r = 0; r < hub->world; ++r) {  // rank order: every rank forms the same sum
@@ -408,7 +419,7 @@ struct HostTransport : Transport {
     if (n && cudaMemcpy(tmp, mine.data(), n * 4, cudaMemcpyHostToDevice) != cudaSuccess) return false;
     return sum_ranks(recv, count, s);
   }
-  bool allreduce_sum_f32(float* data, size_t count, float*, cudaStream_t s) override {
+  bool allreduce_sum_f32(float* data, size_t count, cudaStream_t s) override {
     std::vector<float> h(count), all(count * world);
     if (cudaStreamSynchronize(s) != cudaSuccess) return false;
     if (count && cudaMemcpy(h.data(), data, count * 4, cudaMemcpyDeviceToHost) != cudaSuccess) return false;

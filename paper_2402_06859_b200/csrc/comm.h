@@ -30,8 +30,7 @@ struct Transport {
   virtual bool alltoallv(const void* send, const size_t* soff, const size_t* sbytes, void* recv,
                          const size_t* roff, const size_t* rbytes, cudaStream_t s) = 0;
   // data[0..count) = sum over ranks of data_r (fp32; every rank gets the same values).
-  // `scratch`: device, >= count floats, the transport may use it meanwhile.
-  virtual bool allreduce_sum_f32(float* data, size_t count, float* scratch, cudaStream_t s) = 0;
+  virtual bool allreduce_sum_f32(float* data, size_t count, cudaStream_t s) = 0;
   // ---- fused exchange (EMB_F_P2P): peer memory ------------------------------------------
   // Collective, host-blocking.  Every rank passes n pointers into its own device buffers;
   // on success peers[i * world + r] is rank r's i-th pointer, addressable by this device's

@@ -108,3 +108,16 @@ def cond_close(gpu, ora, mag, rel=1e-5):
 def w_close(gpu, ora, w_old, step, rel=1e-6):
     tol = rel * np.maximum(np.maximum(np.abs(ora), np.abs(w_old)), np.abs(step)) + 1e-12
     return np.abs(gpu.astype(np.float64) - ora.astype(np.float64)) <= tol
+
+
+# Global squared norm S (a7) against the oracle.  G is each segment's fp64 sum rounded to
+# fp32; a segment split across segment-reduce chunks is summed in another fp64 order, so a G
+# element may round to the neighbouring fp32 value (SURVEY.md §8(c) comparison classes:
+# "an occasional 1-ulp difference"; reading 13).  A 1-ulp change of every element
+# moves S = sum G^2 by at most 2 * 2^-24 relative: the bound below.  Unsplit segments (and
+# fp64 sums that stay exact) agree bit for bit.
+S_REL = 2.0 ** -22
+
+
+def S_close(gpu, ora):
+    return abs(gpu - ora) <= S_REL * abs(ora)

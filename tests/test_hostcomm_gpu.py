@@ -39,7 +39,7 @@ def _worker(rank, world, port, sharding, p2p, q):
         os.environ["MASTER_PORT"] = str(port)
         dist.init_process_group("gloo", rank=rank, world_size=world)
         import oracle as O
-        from helpers import cond_close, dense_tables, init_tables_host, w_close
+        from helpers import S_close, cond_close, dense_tables, init_tables_host, w_close
         from paper_2402_06859_b200 import HostComm, ShardedEmbedding
         from workload import configs, gen
         from test_sharded_gpu import global_batch
@@ -100,7 +100,7 @@ def _worker(rank, world, port, sharding, p2p, q):
         Ss = [torch.zeros(1, dtype=torch.float64) for _ in range(world)]
         dist.all_gather(Ss, torch.tensor([S_mine], dtype=torch.float64))
         ok["norm_same_on_ranks"] = all(float(x) == S_mine for x in Ss)
-        ok["norm"] = abs(S_mine - r_or["S"]) <= 1e-12 * r_or["S"]
+        ok["norm"] = S_close(S_mine, r_or["S"])
         base = np.concatenate([[0], np.cumsum(rows)])
         rows_ok = True
         for t, R in enumerate(rows):

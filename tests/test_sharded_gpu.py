@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 
 import oracle as O
-from helpers import cond_close, dense_tables, init_tables_host, w_close
+from helpers import S_close, cond_close, dense_tables, init_tables_host, w_close
 from workload import configs, gen
 
 pytestmark = pytest.mark.gpu
@@ -101,7 +101,7 @@ def test_sharded_train_step_matches_unsharded_oracle(gpu, W, sharding, p2p):
     # global norm identical on every rank (rank partials summed in rank order)
     Ss = [e.last_stats()[0] for e in embs]
     assert all(S == Ss[0] for S in Ss)
-    assert abs(Ss[0] - r_or["S"]) <= 1e-12 * r_or["S"]
+    assert S_close(Ss[0], r_or["S"])
     assert sum(e.last_stats()[2] for e in embs) == r_or["U"]
     # every row from its owner
     base = np.concatenate([[0], np.cumsum(rows)])
