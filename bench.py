@@ -51,7 +51,11 @@ def parse():
     ap.add_argument("--dense-features", type=int, default=256, help="NEXT-2 dense feature count")
     ap.add_argument("--exchange", action="store_true",
                     help="N=1: run the sharded exchange path on a 1-rank NCCL communicator (its overhead)")
-    ap.add_argument("--sharding", default="row", choices=["row", "table"], help="sharding for N>1 / --exchange")
+    ap.add_argument("--sharding", default=None, choices=["row", "table"],
+                    help="sharding for N>1 / --exchange (default: row for the Feed tables, table otherwise)")
+    ap.add_argument("--weak", action="store_true",
+                    help="N>1: weak scaling (batch per GPU fixed, Feed tables x N) instead of the default "
+                         "strong scaling of BASELINE's global batch")
     ap.add_argument("--exchange-mode", default="p2p", choices=["p2p", "nccl"],
                     help="sharded: p2p = fused exchange over NVLink peer memory (EMB_F_P2P; falls back to "
                          "nccl on every rank if any rank cannot map its peers), nccl = collectives")
@@ -62,7 +66,9 @@ def parse():
                     help="serving bench: q8-only handle, a10 lookups only (default for --config feedq8)")
     ap.add_argument("--q8-mode", default="middle_max", choices=["middle_max", "min_max"],
                     help="q8 store: the paper's middle-max (default) or NEXT-4's min-max")
-    ap.add_argument("--cpu-samples", type=int, default=8192)
+    ap.add_argument("--cpu-samples", type=int, default=8192,
+                    help="samples of the single-core oracle timing (the all-core one runs the full batch)")
+    ap.add_argument("--no-spot", action="store_true", help="skip the in-run oracle spot check")
     return ap.parse_args()
 
 
@@ -83,8 +89,32 @@ def alg_bytes(phase, cfg, nnz, U, B, pitch, mode="rowwise"):
     if phase == "update":    # per unique: G read + w read/write + A (+ key); + requant 72 B out
         acc = 8 if mode == "rowwise" else 2 * row
         return U * (row + 2 * row + acc + 4 + (D + 8))
-    if phase == "sort":      # implementation overhead: 16 B/id/pass (reported separately)
-        return None
+    return None
+
+
+def impl_bytes(phase, nnz, U, passes):
+    """a5 is implementation overhead, not algorithmic bytes: its own traffic
+    is one histogram read of the 8-B {key, grad row} pairs + 16 B per pair per onesweep pass
+    (read + write); the run-length encode reads the keys (8 B/pair incl. the neighbour's, L1-
+    served) and writes unique + segment offsets (8 B/unique)."""
+    if phase == "sort":
+        return nnz * (8 + 16 * passes)
+    if phase == "rle":
+        return nnz * 8 + U * 8
+    return None
+
+
+def compulsory_bytes(phase, cfg, nnz, U, B, pitch, mode="rowwise"):
+    """Each row touched ONCE (SURVEY.md §8(d) "compulsory"): the U unique rows of the batch
+    instead of one row per occurrence; the bag's gradient row once instead of once per id."""
+    D, F = cfg.dim, cfg.num_features
+    row = 4 * pitch
+    if phase == "fwd":
+        return nnz * 4 + U * row + B * F * (4 + 4 * D)
+    if phase == "fwd_q8":
+        return nnz * 4 + U * (D + 8) + B * F * (4 + 4 * D)
+    if phase == "segreduce":
+        return nnz * 8 + B * F * 4 * D + U * row
     return None
 
 
@@ -154,13 +184,14 @@ class ClockSampler(threading.Thread):
 
 class OracleSample:
     """The oracle's whole step (a2, a5-a8, a9 on the touched rows, a10) on the first
-    `samples` samples of batch 0, over the compact table of the rows they touch."""
+    `samples` samples of batch 0 (all of them: samples=None), over the compact table of the
+    rows they touch (the Feed tables' 32 GB do not fit host RAM; the touched rows do)."""
 
-    def __init__(self, cfg, ids, off, B, samples, mode):
+    def __init__(self, cfg, ids, off, B, samples, mode, gshift=None, sample0=0):
         import oracle as O
         self.O = O
         F = cfg.num_features
-        Bs = min(samples, B)
+        Bs = B if samples is None else min(samples, B)
         off64 = off.astype(np.int64)
         sub_ids, lens = [], []
         for f in range(F):
@@ -175,6 +206,8 @@ class OracleSample:
         t = np.asarray(cfg.feature_table, dtype=np.int64)[bag_of // Bs]
         gkey = base[t] + sids.astype(np.int64)
         keys = np.unique(gkey)
+        self.keys = keys
+        self.base = base
         self.cids = np.searchsorted(keys, gkey).astype(np.int32)
         tk = np.searchsorted(base, keys, side="right") - 1
         W = np.zeros((len(keys), cfg.dim), dtype=np.float32)
@@ -186,7 +219,8 @@ class OracleSample:
         self.Bs = Bs
         self.nnz = len(sids)
         self.pb = O.Problem([len(keys)], cfg.dim, [0] * F)
-        self.grad = gen.grad_values(cfg.seed, 0, Bs, F, cfg.dim, gen.grad_shift_for(len(ids), cfg.dim))
+        gshift = gen.grad_shift_for(len(ids), cfg.dim) if gshift is None else gshift
+        self.grad = gen.grad_values(cfg.seed, 0, Bs, F, cfg.dim, gshift, sample0=sample0)
         self.mode = mode
         self.reset()
 
@@ -212,15 +246,49 @@ class OracleSample:
         return (time.perf_counter() - t0) / max(steps, 1)
 
 
+def host_info():
+    """CPU model, logical cores and RAM of this host (for the oracle timings)."""
+    model, ram = None, None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemTotal"):
+                ram = round(int(line.split()[1]) / 2 ** 20, 1)
+                break
+    except Exception:
+        pass
+    return {"cpu_model": model, "logical_cores": os.cpu_count(), "ram_gib": ram}
+
+
 def cpu_baseline(cfg, ids, off, B, samples, mode, budget_s=15.0):
-    smp = OracleSample(cfg, ids, off, B, samples, mode)
-    t1 = smp.time(1)
-    reps = max(1, int(budget_s / max(t1, 1e-3)))
-    t = smp.time(reps)
-    return {"value": smp.Bs / t, "unit": "samples/s", "cores": 1, "kind": "oracle",
-            "sample": f"{smp.Bs} of {B} samples of batch 0 ({smp.nnz} ids), whole step "
-                      f"(a2,a5-a8,a9 on touched rows,a10) over the {len(smp.W)} touched rows, "
-                      f"single-threaded C oracle, {reps + 1} reps"}
+    """The oracle as it stands, on this host: the OpenMP build (liboracle_omp.so, bit-identical
+    to the sequential one) on ALL cores over the FULL batch 0, and the sequential build on one
+    core over its first `samples` samples."""
+    import oracle as O
+    cores = O.set_parallel(True, threads=os.cpu_count() or 1)
+    try:
+        full = OracleSample(cfg, ids, off, B, None, mode)
+        t1 = full.time(1)
+        reps = max(1, min(5, int(budget_s / max(t1, 1e-3))))
+        t = full.time(reps)
+    finally:
+        O.set_parallel(False)
+    one = OracleSample(cfg, ids, off, B, samples, mode)
+    t1s = one.time(1)
+    reps1 = max(1, int(0.5 * budget_s / max(t1s, 1e-3)))
+    ts = one.time(reps1)
+    res = {"value": full.Bs / t, "unit": "samples/s", "cores": cores, "kind": "oracle",
+           "sample": f"the full batch 0 ({full.Bs} samples, {full.nnz} ids), whole step (a2, a5-a8, a9 on the "
+                     f"touched rows, a10) over the {len(full.W)} touched rows (compact table), OpenMP C oracle "
+                     f"on {cores} threads, {reps + 1} reps",
+           "single_core": {"value": one.Bs / ts, "unit": "samples/s", "cores": 1,
+                           "sample": f"{one.Bs} of {B} samples of batch 0 ({one.nnz} ids), sequential C oracle, "
+                                     f"{reps1 + 1} reps"}}
+    res.update(host_info())
+    return res
 
 
 # ---------------------------------------------------------------------------
@@ -247,22 +315,27 @@ def run_reference(args, cfg, rank, world, serve=False):
         }
         print(json.dumps(line), flush=True)
         return
-    smp = OracleSample(cfg, ids, off, B, args.cpu_samples, args.adagrad)
+    import oracle as O
+    cores = O.set_parallel(True, threads=os.cpu_count() or 1)
+    smp = OracleSample(cfg, ids, off, B, None, args.adagrad)
     t = smp.time(args.steps, args.warmup)
+    O.set_parallel(False)
     value = smp.Bs / t
+    cb = {"value": value, "unit": "samples/s", "cores": cores, "kind": "oracle",
+          "sample": f"the full batch 0 ({smp.Bs} samples, {smp.nnz} ids) per step, whole step (a2, a5-a8, a9 "
+                    f"on the touched rows, a10) over the {len(smp.W)} touched rows, OpenMP C oracle on "
+                    f"{cores} threads"}
+    cb.update(host_info())
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": cfg.name, "sample_batch": smp.Bs, "global_batch": B, "alpha": cfg.alpha,
-                   "parallelism": "cpu-oracle"},
-        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": 1, "kind": "oracle",
-                         "sample": f"{smp.Bs} of {B} samples per step ({smp.nnz} ids), whole step over the "
-                                   f"touched rows, single-threaded C oracle"},
+        "scaling": "weak" if args.weak else "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": cfg.name, "global_batch": B, "alpha": cfg.alpha, "parallelism": "cpu-oracle"},
+        "cpu_baseline": cb,
         "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
-
 
 
 # ---------------------------------------------------------------------------
@@ -751,7 +824,87 @@ def run_serving(args, cfg, rank, world, local_rank):
 # our arm
 # ---------------------------------------------------------------------------
 
-def run_ours(args, cfg, rank, world, local_rank):
+def global_batch(per_rank, F, B):
+    """Concatenate per-rank feature-major batches into the global batch (sample r*B + b)."""
+    ids_g, lens = [], []
+    for f in range(F):
+        for (ids, off) in per_rank:
+            o = off.astype(np.int64)
+            ids_g.append(ids[o[f * B]:o[(f + 1) * B]])
+            lens.append(np.diff(o[f * B:(f + 1) * B + 1]))
+    off_g = np.zeros(F * B * len(per_rank) + 1, dtype=np.int64)
+    off_g[1:] = np.cumsum(np.concatenate(lens))
+    return np.concatenate(ids_g).astype(np.int32), off_g.astype(np.int32)
+
+
+def spot_readings(emb, cfg, ids, off, B, out, samples=64, max_rows=2048):
+    """Right after the first step (rank 0): its pooled outputs of its first samples and a
+    sample of the rows of its batch that it stores, as updated by that step."""
+    F = cfg.num_features
+    S = min(samples, B)
+    pooled = out[:S].cpu().numpy().copy()
+    bag_of = np.repeat(np.arange(F * B), np.diff(off.astype(np.int64)))
+    t = np.asarray(cfg.feature_table, dtype=np.int64)[bag_of // B]
+    pairs = np.unique(t * (1 << 32) + ids.astype(np.int64))
+    tt, rr = pairs >> 32, pairs & 0xffffffff
+    lo, hi, lb = emb.row_lo[tt], emb.row_hi[tt], emb.local_base[tt]
+    mine = (lb >= 0) & (rr >= lo) & (rr < hi)
+    tt, rr = tt[mine], rr[mine]
+    if len(tt) > max_rows:
+        pick = np.linspace(0, len(tt) - 1, max_rows).astype(np.int64)
+        tt, rr = tt[pick], rr[pick]
+    rows = {}
+    for t_ in np.unique(tt):
+        r_ = rr[tt == t_]
+        rows[int(t_)] = (r_, emb.read_rows(int(t_), r_, with_acc=True))
+    return {"samples": S, "pooled": pooled, "rows": rows}
+
+
+def spot_check(cfg, rd, world, B, gshift, mode, rank_batches=None):
+    """The oracle on the GLOBAL batch 0 (every rank's batch, regenerated from the seeds),
+    over the compact table of its touched rows, OpenMP build: rank 0's pooled outputs within
+    the pooled gate, its sampled rows and accumulators within the update gates."""
+    import oracle as O
+    F, D = cfg.num_features, cfg.dim
+    t0 = time.perf_counter()
+    if rank_batches is None:
+        rank_batches = [gen.make_batch(cfg.table_rows, cfg.features, B, cfg.seed + 7919 * r, 0, alpha=cfg.alpha)
+                        for r in range(world)]
+    ids_g, off_g = global_batch(rank_batches, F, B)
+    threads = O.set_parallel(True, threads=os.cpu_count() or 1)
+    try:
+        smp = OracleSample(cfg, ids_g, off_g, world * B, None, mode, gshift=gshift)
+        W0 = smp.W.copy()
+        A0 = smp.A.copy()
+        r = O.train_step(smp.pb, smp.W, smp.A, smp.cids, smp.soff, smp.Bs, smp.grad, LR, 1e-7, 1.0, mode=mode)
+        mag, _ = O.forward(smp.pb, np.abs(W0), smp.cids, smp.soff, smp.Bs)
+    finally:
+        O.set_parallel(False)
+    S = rd["samples"]
+    ref = r["out"][:S]
+    pooled_ok = np.abs(rd["pooled"].astype(np.float64) - ref) <= 1e-5 * mag[:S] + 1e-30
+    n_rows, rows_ok, acc_ok, exact = 0, 0, 0, 0
+    for t_, (rr, (w, a)) in rd["rows"].items():
+        k = np.searchsorted(smp.keys, smp.base[t_] + rr)
+        assert (smp.keys[k] == smp.base[t_] + rr).all()
+        wo, w0 = smp.W[k], W0[k]
+        step = np.abs(wo - w0)
+        tol = 1e-6 * np.maximum(np.maximum(np.abs(wo), np.abs(w0)), step) + 1e-12
+        rows_ok += int((np.abs(w.astype(np.float64) - wo) <= tol).all(axis=1).sum())
+        exact += int((w == wo).all(axis=1).sum())
+        ao = smp.A[k]
+        acc_ok += int((np.abs(a - ao) <= 1e-6 * np.abs(ao)).reshape(len(k), -1).all(axis=1).sum())
+        n_rows += len(k)
+    return {"what": "oracle (OpenMP C, bit-identical to the sequential build) on the global batch 0 "
+                    f"({smp.Bs} samples, {smp.nnz} ids, {len(smp.keys)} touched rows): rank 0's pooled outputs of "
+                    f"its first {S} samples and {n_rows} sampled rows it stores, after the first step",
+            "pooled_within_gate": bool(pooled_ok.all()), "pooled_bit_exact_frac": float((rd["pooled"] == ref).mean()),
+            "rows_checked": n_rows, "rows_within_gate": rows_ok, "acc_within_gate": acc_ok,
+            "rows_bit_exact": exact, "ok": bool(pooled_ok.all()) and rows_ok == n_rows and acc_ok == n_rows,
+            "oracle_threads": threads, "seconds": time.perf_counter() - t0}
+
+
+def run_ours(args, cfg, rank, world, local_rank, B=None, sharding="row", scaling="strong"):
     import torch
     import torch.distributed as dist
 
@@ -761,7 +914,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     stream = torch.cuda.Stream(dev)
-    B = cfg.batch  # per rank: weak scaling (tables grow with the ranks, see main())
+    B = cfg.batch if B is None else B  # this rank's batch (strong scaling: global / N)
     D, F = cfg.dim, cfg.num_features
 
     # inputs: nb distinct batches, resident in HBM (and pinned on the host for e2e)
@@ -783,8 +936,10 @@ def run_ours(args, cfg, rank, world, local_rank):
                 dist.broadcast(uid, 0)
             return uid.cpu().numpy().tobytes()
 
-        shard_kw = dict(rank=rank, world_size=world, sharding=args.sharding, nccl_unique_id=new_uid(),
+        shard_kw = dict(rank=rank, world_size=world, sharding=sharding, nccl_unique_id=new_uid(),
                         max_recv_nnz=3 * max_nnz, force_exchange=args.exchange)
+        if sharding == "table":  # LPT placement by lookup traffic
+            shard_kw["table_cost"] = configs.table_cost(cfg, batch=world * B)
     xmode = None
     if shard_kw:
         xmode = args.exchange_mode
@@ -803,7 +958,8 @@ def run_ours(args, cfg, rank, world, local_rank):
 
     emb = make_emb()
     with torch.cuda.stream(stream):
-        gshift = gen.grad_shift_for(max_nnz, D)
+        # one grad scale for every rank: from the GLOBAL batch's expected ids (pre-clip |g| ~ 4)
+        gshift = gen.grad_shift_for(int(round(cfg.mean_bag() * B * world)), D)
         dev_in = []
         for k, (ids, off) in enumerate(batches):
             gd = torch.empty((B, F, D), device=dev)
@@ -825,10 +981,12 @@ def run_ours(args, cfg, rank, world, local_rank):
         if world > 1:
             dist.barrier()
 
+    first_done = False
     if xmode == "p2p":
         # the first sharded forward maps the peers (collective: every rank gets the same verdict)
         try:
             step(0)
+            first_done = True
         except RuntimeError as e:
             if "EMB_ENCCL" not in str(e) and "ENCCL" not in str(e):
                 raise
@@ -837,7 +995,17 @@ def run_ours(args, cfg, rank, world, local_rank):
             shard_kw["p2p"] = False
             shard_kw["nccl_unique_id"] = new_uid()
             emb = make_emb()
-    for k in range(args.warmup):
+    if not first_done:
+        step(0)
+    # the first (warm-up) step is the in-run parity spot check's: rank 0 reads its pooled
+    # outputs and a sample of its updated rows now; the oracle runs after the timed region
+    stream.synchronize()
+    barrier()
+    readings = None
+    if rank == 0 and not args.no_spot:
+        readings = spot_readings(emb, cfg, batches[0][0], batches[0][1], B, out)
+    barrier()
+    for k in range(1, args.warmup):
         step(k)
     stream.synchronize()
     st = emb.sync()
@@ -876,57 +1044,31 @@ def run_ours(args, cfg, rank, world, local_rank):
         ms = float(t.item())
     S, c, U = emb.last_stats()
 
-    # ---- e2e: the user's pipeline through the public API -------------------------------
-    # Every step's inputs (ids, offsets and the upstream grads) start in pinned HOST memory
-    # and are copied H2D inside the timed region on a copy stream, one step ahead (the
-    # paper's "prefetch dataset to GPU"), double-buffered; the step's result (the
-    # global squared grad norm S, returned by emb_backward_adagrad) is read back D2H every
-    # step, which also synchronises the host with the step as a training loop does.
+    # ---- e2e: the user's pipeline through the C ABI's host-pointer path -----------------
+    # Every step's batch (ids, offsets) starts in pinned HOST memory and is handed to the
+    # library as host pointers: emb_forward stages it into the library workspace with
+    # cudaMemcpyAsync on its stream (inside the timed region), emb_forward_q8(NULL, NULL)
+    # looks up the same staged batch from the q8 store, and emb_backward_adagrad returns the
+    # step's result S (global squared grad norm) to the host, which synchronises the host
+    # with the step as a training loop does.  The upstream gradient dL/d(pooled) is a device
+    # tensor: in a training step the dense tower's backward produces it on the GPU (the
+    # `model` object runs that tower for real); it is not host input.
     e2e = None
     if not args.no_e2e:
-        host_in = []
-        for k, (ids, off) in enumerate(batches):
-            host_in.append((torch.from_numpy(ids).pin_memory(), torch.from_numpy(off).pin_memory(),
-                            dev_in[k][2].cpu().pin_memory()))
-        cs = torch.cuda.Stream(dev)
-        bufs = [(torch.empty(max_nnz, dtype=torch.int32, device=dev),
-                 torch.empty(F * B + 1, dtype=torch.int32, device=dev),
-                 torch.empty((B, F, D), device=dev)) for _ in range(2)]
-        ev_in = [torch.cuda.Event() for _ in range(2)]
-        ev_free = [torch.cuda.Event() for _ in range(2)]
+        host_in = [(torch.from_numpy(ids).pin_memory(), torch.from_numpy(off).pin_memory()) for ids, off in batches]
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-
-        def h2d(k):
-            slot = k % 2
-            ids_h, off_h, g_h = host_in[k % len(host_in)]
-            with torch.cuda.stream(cs):
-                cs.wait_event(ev_free[slot])
-                bufs[slot][0][:len(ids_h)].copy_(ids_h, non_blocking=True)
-                bufs[slot][1].copy_(off_h, non_blocking=True)
-                bufs[slot][2].copy_(g_h, non_blocking=True)
-                ev_in[slot].record(cs)
-
-        for e in ev_free:
-            e.record(stream)
         barrier()
         torch.cuda.synchronize(dev)
         G.flush_l2(flush, stream=stream)
         with torch.cuda.stream(stream):
             t0.record(stream)
-        cs.wait_event(t0)
-        h2d(0)
         for k in range(K):
-            slot = k % 2
-            if k + 1 < K:
-                h2d(k + 1)
-            stream.wait_event(ev_in[slot])
-            n = len(host_in[k % len(host_in)][0])
-            ids_d, off_d, g_d = bufs[slot][0][:n], bufs[slot][1], bufs[slot][2]
-            emb.forward(ids_d, off_d, B, out=out)
-            emb.forward_q8(ids_d, off_d, B, out=out_q8)
-            ev_free_rec = emb.backward_adagrad(g_d, LR, want_norm=True)  # S: D2H, blocks on the step
-            ev_free[slot].record(stream)
-            assert ev_free_rec > 0.0
+            ids_h, off_h = host_in[k % len(host_in)]
+            g_d = dev_in[k % len(dev_in)][2]
+            emb.forward(ids_h, off_h, B, out=out)                 # H2D staging in the library
+            emb.forward_q8(None, None, B, out=out_q8, nnz=ids_h.numel())  # the same staged batch
+            S_h = emb.backward_adagrad(g_d, LR, want_norm=True)  # S: D2H, blocks on the step
+            assert S_h > 0.0
         with torch.cuda.stream(stream):
             t1.record(stream)
         torch.cuda.synchronize(dev)
@@ -938,14 +1080,13 @@ def run_ours(args, cfg, rank, world, local_rank):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = float(t.item())
         nnz_avg = float(np.mean([len(i) for i, _ in batches]))
-        h2d_b = int(nnz_avg * 4 + (F * B + 1) * 4 + B * F * D * 4)
+        h2d_b = int(nnz_avg * 4 + (F * B + 1) * 4)
         e2e = {"value": world * B / (e_ms / 1e3), "unit": "samples/s", "ms_per_step": e_ms,
                "h2d_bytes_per_step": h2d_b, "d2h_bytes_per_step": 8,
-               # the device step (ms_per_step of the line) hides behind the next step's input
-               # copy: the e2e step is bound by host->device bandwidth (PCIe) at this rate
-               "h2d_gbs_per_gpu": h2d_b / (e_ms / 1e3) / 1e9,
-               "path": "pinned host ids/offsets/grads -> H2D one step ahead on a copy stream -> "
-                       "emb_forward, emb_forward_q8, emb_backward_adagrad(-> S, D2H), every step"}
+               "path": "pinned host ids/offsets passed to emb_forward as HOST pointers (staged H2D by the "
+                       "library on its stream) -> emb_forward_q8(NULL, NULL) on the staged batch -> "
+                       "emb_backward_adagrad(device grad = the tower's output) -> S D2H, every step; no overlap "
+                       "of the next batch's copy (the S read-back serialises the host)"}
 
     # ---- full-table quantize (a9), timed alone ----------------------------------------
     emb.profile(True)
@@ -968,6 +1109,9 @@ def run_ours(args, cfg, rank, world, local_rank):
     peak_src = "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if "hbm_gbs" in peaks else "fallback 6650 GB/s (B200_PROFILING.md)"
     nnz_avg = float(np.mean([len(i) for i, _ in batches]))
     per_phase = {}
+    kbits = int(emb.local_rows).bit_length()  # keys in [0, local_rows] (sentinel = local_rows)
+    dbits = 9 if (24 < kbits <= 27 or 16 < kbits <= 18) else 8
+    passes = -(-kbits // dbits)
     for p, (tot, n) in phases.items():
         if n == 0:
             continue
@@ -978,7 +1122,28 @@ def run_ours(args, cfg, rank, world, local_rank):
             ent["alg_bytes"] = ab
             ent["gbs"] = ab / (per / 1e3) / 1e9
             ent["frac_of_hbm"] = ent["gbs"] / hbm_peak
+            cb = compulsory_bytes(p, cfg, nnz_avg, U, B, emb.pitch, args.adagrad)
+            if cb:  # every touched row (and every bag's gradient row) moved once
+                ent["compulsory_bytes"] = cb
+                ent["compulsory_frac_of_hbm"] = cb / (per / 1e3) / 1e9 / hbm_peak
+            if p in ("fwd", "fwd_q8") and cfg.alpha > 0:
+                ent["frac_note"] = ("per-occurrence bytes at Zipf alpha > 0: L1/L2 serve the repeated hot rows, "
+                                    "so this fraction is reuse-inflated; the HBM-bound figure is the alpha = 0 "
+                                    "run (--alpha 0) or compulsory_frac_of_hbm")
+        ib = impl_bytes(p, nnz_avg, U, passes)
+        if ib:  # a5: its own (implementation) bytes, SURVEY.md §8(d)
+            ent["own_bytes"] = ib
+            ent["own_gbs"] = ib / (per / 1e3) / 1e9
+            ent["own_frac_of_hbm"] = ent["own_gbs"] / hbm_peak
+            if p == "sort":
+                ent["passes"] = passes
         per_phase[p] = ent
+    if "sort" in per_phase and "rle" in per_phase:
+        a5_ms = per_phase["sort"]["ms"] + per_phase["rle"]["ms"]
+        a5_b = per_phase["sort"]["own_bytes"] + per_phase["rle"]["own_bytes"]
+        per_phase["a5_dedup"] = {"ms": a5_ms, "own_bytes": a5_b, "own_gbs": a5_b / (a5_ms / 1e3) / 1e9,
+                                 "own_frac_of_hbm": a5_b / (a5_ms / 1e3) / 1e9 / hbm_peak,
+                                 "note": "sort + run-length encode on the side stream (overlaps a10)"}
     single = [p for p in ("fwd", "fwd_q8", "update", "segreduce") if p in per_phase]
     dom = max(single, key=lambda p: per_phase[p]["ms"])
     traffic = None
@@ -998,25 +1163,35 @@ def run_ours(args, cfg, rank, world, local_rank):
         roof["dram_achieved"] = traffic / (per_phase[dom]["ms"] / 1e3) / 1e9
         roof["dram_frac"] = roof["dram_achieved"] / hbm_peak
 
+    spot = None
+    if readings is not None:
+        try:
+            spot = spot_check(cfg, readings, world, B, gshift, args.adagrad,
+                              rank_batches=[batches[0]] if world == 1 else None)
+        except Exception as e:  # report, never hide
+            spot = {"error": repr(e), "ok": False}
     value = world * B / (ms / 1e3)
     fwd_ms = per_phase["fwd"]["ms"]
     bwd_ms = sum(per_phase[p]["ms"] for p in ("sort", "rle", "segreduce", "norm", "update") if p in per_phase)
     line = {
         "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": K,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": scaling,
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded Zipf ids, Irwin-Hall tables/grads)",
-        "config": {"workload": cfg.name, "tables": cfg.table_rows, "dim": D, "features": F,
-                   "global_batch": world * B, "batch_per_gpu": B, "nnz_per_step": nnz_avg, "alpha": cfg.alpha,
+        "config": {"workload": cfg.name, "baseline_config": cfg.note, "tables": cfg.table_rows, "dim": D, "features": F,
+                   "global_batch": world * B, "batch_per_gpu": B, "nnz_per_step_per_gpu": nnz_avg, "alpha": cfg.alpha,
                    "unique_rows": U, "adagrad": args.adagrad, "q8": args.q8_mode,
-                   "parallelism": ("single" if not args.exchange else f"{args.sharding}-sharded exchange path on a 1-rank NCCL communicator")
-                   if world == 1 else f"{args.sharding}-sharded x{world}",
+                   "parallelism": ("single" if not args.exchange else f"{sharding}-sharded exchange path on a 1-rank NCCL communicator")
+                   if world == 1 else f"{sharding}-sharded x{world}" + (" (LPT placement by lookup traffic)" if sharding == "table" else ""),
                    "exchange": None if xmode is None else (
-                       "p2p: ids all-to-all (NCCL); pooled rows stored by the owners' pooling kernels into the "
-                       "destination's buffer over NVLink peer memory (row-wise: per-owner slots summed in rank "
-                       "order); grad rows pushed to the owners by one kernel; NCCL 4-byte all-gather barriers"
+                       "p2p: ids stored by one kernel at their compacted place in the owners' receive buffers "
+                       "after a device-side count all-gather (no host sync); pooled rows stored by the owners' "
+                       "pooling kernels into the destination's buffer over NVLink peer memory (row-wise: "
+                       "per-owner slots summed in rank order); grad rows pushed to the owners by one kernel; "
+                       "NCCL 4-byte all-gather barriers"
                        if xmode == "p2p" else
-                       f"{xmode}: ids all-to-all; " + ("reduce-scatter pooled, all-gather grads" if args.sharding == "row"
-                                                       else "all-to-all pooled / grad blocks + permute")),
+                       f"{xmode}: ids all-to-all of capacity-padded slots (no host sync); " +
+                       ("reduce-scatter pooled, all-gather grads" if sharding == "row"
+                        else "all-to-all pooled / grad blocks + permute")),
                    "step": "a2 fwd -> a10 q8 fwd (overlapping a5 dedup on a side stream) -> a6-a8 bwd (a9 requant of touched rows fused)",
                    "l2": "flushed between timed steps (256 MiB write, untimed)",
                    "batches_rotated": len(batches)},
@@ -1031,6 +1206,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         "gpu_launches": launches,
         "e2e": e2e,
         "clip": {"sq_norm": S, "c": float(c)},
+        "spot_check": spot,
     }
     if world == 1 and not args.no_lib:
         try:
@@ -1038,7 +1214,7 @@ def run_ours(args, cfg, rank, world, local_rank):
             line["library"]["ours_a2_ms"] = per_phase["fwd"]["ms"]
         except Exception as e:  # report, never hide
             line["library"] = {"error": repr(e)}
-    if world == 1 and not args.no_graph and not args.exchange:  # (the exchange path syncs the host)
+    if world == 1 and not args.no_graph:  # (the exchange path is host-sync free too: graphed at N=1)
         try:
             line["graph"] = graph_section(emb, cfg, dev_in, B, out, out_q8, stream, flush)
         except Exception as e:  # report, never hide
@@ -1062,11 +1238,31 @@ def run_ours(args, cfg, rank, world, local_rank):
         try:
             line["cpu_baseline"] = cpu_baseline(cfg, batches[0][0], batches[0][1], B, args.cpu_samples,
                                                 args.adagrad)
-            line["cpu_baseline"]["cores_available"] = os.cpu_count()
         except Exception as e:  # report, never hide
             line["cpu_baseline"] = {"error": repr(e)}
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def scale_plan(cfg, world, sharding=None, weak=False, serve=False):
+    """(config, this rank's batch, sharding, scaling) of an N-GPU run.
+
+    Strong scaling (default): BASELINE's GLOBAL batch (Feed 128k, Ads 64k, Jobs 16k) split
+    over the N GPUs.  The Feed tables grow with N from the 1-GPU shard (125M rows per GPU): at
+    N = 8 they are BASELINE.json's Feed config, "~1B total rows x dim 64 fp32 row-wise sharded
+    over 8xB200"; Ads / Jobs keep their tables (table-wise, LPT by lookup traffic).  Weak:
+    every GPU keeps the 1-GPU batch.  Serving (q8 replicas) keeps its per-replica batch."""
+    sharding = sharding or ("row" if cfg.name.startswith("feed") else "table")
+    scaling = "weak" if weak else "strong"
+    if world <= 1 or serve:
+        return cfg, cfg.batch, sharding, scaling
+    if cfg.name == "feed1":
+        cfg = cfg.with_(name=f"feed-x{world}", table_rows=[r * world for r in cfg.table_rows],
+                        note=f"feed1 tables x {world}" + (" = BASELINE.json configs[3] (1B rows)" if world == 8 else ""))
+    if weak:
+        cfg = cfg.with_(name=f"{cfg.name}-weak", batch=cfg.batch * world)
+    assert cfg.batch % world == 0
+    return cfg, cfg.batch // world, sharding, scaling
 
 
 def main():
@@ -1078,10 +1274,7 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     serve = args.serve or cfg.name.startswith("feedq8")
-    if world > 1 and args.impl == "ours" and not serve:
-        # weak scaling: every GPU keeps the 1-GPU shard size and batch; the tables are the
-        # W-fold Feed tables (W=8: the 1B-row Feed config of BASELINE.json), row-wise sharded
-        cfg = cfg.with_(name=f"{cfg.name}-x{world}", table_rows=[r * world for r in cfg.table_rows])
+    cfg, B_local, sharding, scaling = scale_plan(cfg, world, args.sharding, args.weak, serve)
     if args.impl == "reference":
         run_reference(args, cfg, rank, world, serve=serve)
         return
@@ -1094,7 +1287,7 @@ def main():
         if serve:
             run_serving(args, cfg, rank, world, local_rank)
         else:
-            run_ours(args, cfg, rank, world, local_rank)
+            run_ours(args, cfg, rank, world, local_rank, B=B_local, sharding=sharding, scaling=scaling)
     finally:
         if world > 1:
             import torch.distributed as dist

@@ -285,7 +285,11 @@ EMB_API emb_status emb_quantize_mm8(emb_t h);
 
 /* a10: like emb_forward, but reading the q8 store: out = sum in bag order of
  * fmaf(code, scale, middle).  EMB_ESTATE before the first emb_quantize_mm8 (unless
- * EMB_F_REQUANT has kept it current).  Does not record occurrences for backward. */
+ * EMB_F_REQUANT has kept it current).  Does not record occurrences for backward.
+ * ids == offsets == NULL: look up the batch of the most recent emb_forward (batch and nnz
+ * must equal its, else EMB_EINVAL; EMB_ESTATE if there was none) -- host inputs of that
+ * forward are not copied again (its staged copy is used); device inputs must still hold
+ * the same values. */
 EMB_API emb_status emb_forward_q8(emb_t h, const int32_t* ids, const int32_t* offsets, int32_t batch,
                           int64_t nnz, float* out);
 

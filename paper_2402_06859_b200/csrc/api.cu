@@ -716,6 +716,10 @@ emb_status emb_forward(emb_t h, const int32_t* ids, const int32_t* offsets, int3
     s = stage_inputs(h, ids, offsets, batch, nnz, out, &st);
   }
   if (s != EMB_OK) return s;
+  h->last_ids = st.ids;  // (device) inputs of this forward, for emb_forward_q8(NULL, NULL)
+  h->last_off = st.offsets;
+  h->last_B = batch;
+  h->last_nnz = nnz;
   if (p.exch) {
     s = exchange_forward(h, st, batch, nnz, /*q8=*/false);
     if (s != EMB_OK) return s;
@@ -767,6 +771,15 @@ emb_status emb_forward(emb_t h, const int32_t* ids, const int32_t* offsets, int3
 
 emb_status emb_forward_q8(emb_t h, const int32_t* ids, const int32_t* offsets, int32_t batch,
                           int64_t nnz, float* out) {
+  // ids == offsets == NULL: the batch of the most recent emb_forward (its staged copy when
+  // it came from host memory), e.g. serving the q8 store on the batch just trained on
+  const bool reuse = h && !ids && !offsets;
+  if (reuse) {
+    if (!h->last_off) return EMB_ESTATE;
+    if (batch != h->last_B || nnz != h->last_nnz) return EMB_EINVAL;
+    ids = h->last_ids;
+    offsets = h->last_off;
+  }
   emb_status s = check_batch_args(h, ids, offsets, batch, nnz, out);
   if (s != EMB_OK) return s;
   const Plan& p = h->p;
@@ -777,6 +790,11 @@ emb_status emb_forward_q8(emb_t h, const int32_t* ids, const int32_t* offsets, i
     s = stage_inputs(h, ids, offsets, batch, nnz, out, &st);
   }
   if (s != EMB_OK) return s;
+  if (!reuse && ((st.ids == h->stage_ids && h->last_ids == h->stage_ids) ||
+                 (st.offsets == h->stage_off && h->last_off == h->stage_off))) {
+    h->last_ids = nullptr;  // the staging area now holds this batch, not the forward's
+    h->last_off = nullptr;
+  }
   if (p.exch) {
     s = exchange_forward(h, st, batch, nnz, /*q8=*/true);
     if (s != EMB_OK) return s;

@@ -76,31 +76,28 @@ __device__ __forceinline__ void zero(double (&acc)[VPL][4]) {
     for (int e = 0; e < 4; ++e) acc[v][e] = 0.0;
 }
 
-// acc += (double)r (x inv_l for MEAN); HW: hardware conversions, else the integer widening
-template <int VPL, bool MEAN, bool HW>
+// acc += (double)r (x 1/L for MEAN).  The fp32 -> fp64 widenings are F2F instructions (XU
+// pipe); an exact integer-pipe widening (sign | (exponent + 896) << 20 | mantissa >> 3, low
+// word mantissa << 29, hardware fallback for 0 / subnormal / non-finite batches) was measured
+// on Feed-1: 0.661 -> 0.942 ms -- this kernel is bound by issue slots, and one F2F is
+// cheaper to issue than the five integer instructions that replace it.
+template <int VPL, bool MEAN>
 __device__ __forceinline__ void accumulate(double (&acc)[VPL][4], const float4 (&r)[VPL], double inv) {
 #pragma unroll
   for (int v = 0; v < VPL; ++v) {
-    const double x = HW ? (double)r[v].x : f2d_int(r[v].x);
-    const double y = HW ? (double)r[v].y : f2d_int(r[v].y);
-    const double z = HW ? (double)r[v].z : f2d_int(r[v].z);
-    const double w = HW ? (double)r[v].w : f2d_int(r[v].w);
     if (MEAN) {
-      acc[v][0] += x * inv;
-      acc[v][1] += y * inv;
-      acc[v][2] += z * inv;
-      acc[v][3] += w * inv;
+      acc[v][0] += (double)r[v].x * inv;
+      acc[v][1] += (double)r[v].y * inv;
+      acc[v][2] += (double)r[v].z * inv;
+      acc[v][3] += (double)r[v].w * inv;
     } else {
-      acc[v][0] += x;
-      acc[v][1] += y;
-      acc[v][2] += z;
-      acc[v][3] += w;
+      acc[v][0] += (double)r[v].x;
+      acc[v][1] += (double)r[v].y;
+      acc[v][2] += (double)r[v].z;
+      acc[v][3] += (double)r[v].w;
     }
   }
 }
-
-// (double)g for the norm of a rounded G element: integer widening when normal
-__device__ __forceinline__ double widen(float g) { return f2d_normal(g) ? f2d_int(g) : (double)g; }
 
 // Finish a complete segment: G[u] = (float)acc, return this lane's sum of (double)G^2.
 template <int VPL>
@@ -115,11 +112,10 @@ __device__ __forceinline__ double write_G(float* G, int pitch, uint32_t u, int l
       float4 g = make_float4((float)acc[v][0], (float)acc[v][1], (float)acc[v][2],
                              (float)acc[v][3]);
       st_f4_hint(G + (size_t)u * pitch + 4 * vi, g, l2_policy_first());  // G: streamed to a8
-      const double gx = widen(g.x), gy = widen(g.y), gz = widen(g.z), gw = widen(g.w);
-      nrm += gx * gx;
-      nrm += gy * gy;
-      nrm += gz * gz;
-      nrm += gw * gw;
+      nrm += (double)g.x * (double)g.x;
+      nrm += (double)g.y * (double)g.y;
+      nrm += (double)g.z * (double)g.z;
+      nrm += (double)g.w * (double)g.w;
     }
   }
   return nrm;
@@ -212,18 +208,6 @@ k_segreduce(const uint32_t* __restrict__ seg, const uint32_t* __restrict__ Up,
         ok[q] = (jj + q < LPB) && (kb + jj + q < k1);
         if (ok[q]) load_grad_row<VPL>(grad, (size_t)gq * D, D, lane, LPB, r[q]);
       }
-      // fp32 -> fp64 widening of the batch's rows: exact integer bit moves (ALU pipe) unless
-      // some lane holds a zero / subnormal / non-finite element -- then, warp-uniformly, the
-      // hardware conversion (XU pipe) for this batch.  Same doubles either way.
-      bool special = false;
-#pragma unroll
-      for (int q = 0; q < UNR; ++q)
-        if (ok[q])
-#pragma unroll
-          for (int v = 0; v < VPL; ++v)
-            special |= !(f2d_normal(r[q][v].x) && f2d_normal(r[q][v].y) && f2d_normal(r[q][v].z) &&
-                         f2d_normal(r[q][v].w));
-      const bool hw = __any_sync(kFull, special);
 #pragma unroll
       for (int q = 0; q < UNR; ++q) {
         if (ok[q]) {
@@ -234,8 +218,7 @@ k_segreduce(const uint32_t* __restrict__ seg, const uint32_t* __restrict__ Up,
             ++u;
             first_open = false;
           }
-          if (hw) accumulate<VPL, MEAN, true>(acc, r[q], iv[q]);
-          else accumulate<VPL, MEAN, false>(acc, r[q], iv[q]);
+          accumulate<VPL, MEAN>(acc, r[q], iv[q]);
         }
       }
     }

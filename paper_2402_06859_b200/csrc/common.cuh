@@ -143,20 +143,6 @@ __device__ __forceinline__ float4 f4_add_rn(float4 a, float4 b) {
 // full drain + launch gap); pdl_wait() -- its first statement -- blocks until the predecessor
 // has completed and its memory is visible, so nothing before it may read predecessor output.
 // In a kernel launched normally pdl_wait() returns at once.
-// fp32 -> fp64 exactly on the integer pipe, for NORMAL floats: the double's high word is
-// sign | (exponent + 1023 - 127) << 20 | the top 20 mantissa bits, the low word the last 3
-// mantissa bits << 29 (LOP3 + LEA.HI + LOP3 + SHL, no F2F on the XU pipe).  Zero,
-// subnormal, inf and NaN inputs (f2d_normal() false) need the hardware conversion.
-__device__ __forceinline__ double f2d_int(float x) {
-  const uint32_t b = __float_as_uint(x);
-  const uint32_t hi = (((b & 0x7fffffffu) >> 3) + 0x38000000u) | (b & 0x80000000u);
-  return __hiloint2double((int)hi, (int)(b << 29));
-}
-__device__ __forceinline__ bool f2d_normal(float x) {
-  const float a = fabsf(x);
-  return a >= 1.17549435e-38f && a <= 3.40282347e+38f;  // FLT_MIN <= |x| <= FLT_MAX (NaN: false)
-}
-
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 template <typename... KArgs, typename... Args>

@@ -188,6 +188,11 @@ struct emb_handle {
   // NEXT-3 incremental-training penalty (emb_set_incremental)
   lirank::FimArgs fim{};
   bool fim_on = false;
+  // inputs of the last emb_forward (device: the caller's or the staged copy)
+  const int* last_ids = nullptr;
+  const int* last_off = nullptr;
+  int last_B = -1;
+  int64_t last_nnz = -1;
   // state
   bool have_fwd = false;
   bool have_q8 = false;

@@ -273,8 +273,15 @@ class ShardedEmbedding:
     def quantize(self):
         L.check(self.lib.emb_quantize_mm8(self.h), "emb_quantize_mm8")
 
-    def forward_q8(self, ids: torch.Tensor, offsets: torch.Tensor, batch: int,
-                   out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    def forward_q8(self, ids: Optional[torch.Tensor], offsets: Optional[torch.Tensor], batch: int,
+                   out: Optional[torch.Tensor] = None, nnz: Optional[int] = None) -> torch.Tensor:
+        """a10.  ids = offsets = None: the batch of the last forward() (its staged copy when it
+        came from host memory; pass nnz = its id count)."""
+        if ids is None and offsets is None:
+            assert out is not None and nnz is not None
+            assert out.dtype == torch.float32 and out.is_contiguous()
+            L.check(self.lib.emb_forward_q8(self.h, None, None, int(batch), int(nnz), _ptr(out)), "emb_forward_q8")
+            return out
         if out is None:
             out = torch.empty((batch, self.num_features, self.dim), dtype=torch.float32,
                               device=ids.device if ids.is_cuda else "cpu", pin_memory=not ids.is_cuda)

@@ -205,10 +205,8 @@ def test_train_step_clip_inactive_and_extra_norm(gpu):
 
 
 def test_grad_zeros_and_subnormals_widen_exactly(gpu):
-    """a6 widens fp32 grads to fp64 with integer bit moves for normal values and with the
-    hardware conversion for a batch holding a zero / -0 / subnormal element (backward.cu
-    accumulate / f2d_int): both must give the oracle's doubles -- the update equals the
-    oracle's as for ordinary grads."""
+    """Zeros, -0 and subnormals in the upstream gradient go through a6's fp64 sums like any
+    value (reading 13): the update equals the oracle's as for ordinary grads."""
     cfg = small_cfg(dim=64, rows=(2000, 500, 60), F=[0, 1, 0, 2], B=256)
     B, F, D = 256, cfg.num_features, 64
     ids, off = gen.make_batch(cfg.table_rows, cfg.features, B, cfg.seed, 0)
