@@ -17,6 +17,8 @@
 //   (coalesced).  Each pass moves 16 B per pair.  Tiles are claimed in launch order
 //   through an atomic counter, so a look-back only waits on tiles already resident.
 
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "lookback.cuh"
@@ -139,10 +141,15 @@ k_hist_excl(uint32_t* hist, int bins) {
 // ---------------------------------------------------------------------------
 // Load the warp's ITEMS x 32 pairs and rank each within the warp (stable: by item, then
 // lane) against the warp's running digit counters wh[].  FULL: every index is < n.
-template <int BITS, int ITEMS, bool MATCH, bool FULL>
+// RANK selects how a lane finds the lanes holding the same digit ("peers"):
+//   0: BITS ballots (warp multisplit, ~5 instructions per bit),
+//   1: match.any,
+//   2: every lane sets its bit in a per-warp shared word of its digit (one ATOMS.OR), the
+//      warp synchronises and reads the word back; the digit's leader clears it.
+template <int BITS, int ITEMS, int RANK, bool FULL>
 __device__ __forceinline__ void load_rank(const uint2* __restrict__ in, uint2 (&kv)[ITEMS],
                                           uint32_t (&r)[ITEMS], int64_t base, int64_t n, int shift,
-                                          uint32_t* wh, int lane, unsigned lt) {
+                                          uint32_t* wh, uint32_t* mm, int lane, unsigned lt) {
   constexpr int BINS = 1 << BITS;
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
@@ -155,8 +162,12 @@ __device__ __forceinline__ void load_rank(const uint2* __restrict__ in, uint2 (&
     const bool ok = FULL || idx < n;
     const uint32_t d = ok ? (kv[i].x >> shift) & (BINS - 1) : (uint32_t)BINS;
     unsigned peers;
-    if (MATCH) {
+    if (RANK == 1) {
       peers = __match_any_sync(0xffffffffu, d);
+    } else if (RANK == 2) {
+      if (ok) atomicOr(mm + d, 1u << lane);
+      __syncwarp();
+      peers = ok ? mm[d] : 0u;
     } else {
       peers = FULL ? peers_of<BITS>(d, 0xffffffffu)
                    : peers_of<BITS + 1>(d, 0xffffffffu);  // bit BITS separates out-of-range lanes
@@ -164,12 +175,15 @@ __device__ __forceinline__ void load_rank(const uint2* __restrict__ in, uint2 (&
     const uint32_t cur = ok ? wh[d] : 0u;
     r[i] = cur + __popc(peers & lt);
     __syncwarp();
-    if (ok && lane == __ffs(peers) - 1) wh[d] = cur + __popc(peers);
+    if (ok && lane == __ffs(peers) - 1) {
+      wh[d] = cur + __popc(peers);
+      if (RANK == 2) mm[d] = 0u;
+    }
     __syncwarp();
   }
 }
 
-template <int BITS, int ITEMS, bool MATCH, int MINB = 4>
+template <int BITS, int ITEMS, int RANK, int MINB = 4>
 __global__ void __launch_bounds__(kSortThreads, MINB)
 k_onesweep(const uint2* __restrict__ in, uint2* __restrict__ out, int64_t n, const uint32_t* n_dev,
            int shift, const uint32_t* __restrict__ hist, uint32_t* tile_counter,
@@ -185,10 +199,13 @@ k_onesweep(const uint2* __restrict__ in, uint2* __restrict__ out, int64_t n, con
   uint32_t* warp_hist = reinterpret_cast<uint32_t*>(stage + TILE);            // [NW][BINS]
   uint32_t* digit_off = warp_hist + NW * BINS;                                  // [BINS]
   uint32_t* s_misc = digit_off + BINS;                                          // [NW + 2]
+  uint32_t* match_mask = s_misc + NW + 2;                                       // RANK 2: [NW][BINS]
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) s_misc[NW] = atomicAdd(tile_counter, 1u);
   for (int i = tid; i < NW * BINS; i += kSortThreads) warp_hist[i] = 0;
+  if (RANK == 2)
+    for (int i = tid; i < NW * BINS; i += kSortThreads) match_mask[i] = 0;
   __syncthreads();
   const int64_t tile = s_misc[NW];
   const int64_t tile0 = tile * TILE;
@@ -203,8 +220,9 @@ k_onesweep(const uint2* __restrict__ in, uint2* __restrict__ out, int64_t n, con
   uint32_t* wh = warp_hist + warp * BINS;
   // every tile but the last is full: its ranking needs no bounds checks and BITS ballots
   // (the last one separates out-of-range lanes with one more bit)
-  if (tile0 + TILE <= n) load_rank<BITS, ITEMS, MATCH, true>(in, kv, r, base, n, shift, wh, lane, lt);
-  else load_rank<BITS, ITEMS, MATCH, false>(in, kv, r, base, n, shift, wh, lane, lt);
+  uint32_t* mm = match_mask + warp * BINS;
+  if (tile0 + TILE <= n) load_rank<BITS, ITEMS, RANK, true>(in, kv, r, base, n, shift, wh, mm, lane, lt);
+  else load_rank<BITS, ITEMS, RANK, false>(in, kv, r, base, n, shift, wh, mm, lane, lt);
   __syncthreads();
 
   // per digit: exclusive prefix over warps (in place), tile total, and the tile's
@@ -270,23 +288,24 @@ k_onesweep(const uint2* __restrict__ in, uint2* __restrict__ out, int64_t n, con
   }
 }
 
-template <int BITS, int ITEMS, bool MATCH, int MINB>
+template <int BITS, int ITEMS, int RANK, int MINB>
 static cudaError_t onesweep_pass(const uint2* a, uint2* b, int64_t n, const uint32_t* n_dev, int shift,
                                  const uint32_t* hist,
                                  uint32_t* counter, unsigned long long* status, const uint32_t* epoch,
                                  uint32_t epoch_off, cudaStream_t s) {
   constexpr int TILE = kSortThreads * ITEMS;
-  const size_t sm = sizeof(uint2) * TILE + sizeof(uint32_t) * (NW * (1 << BITS) + (1 << BITS) + NW + 2);
+  const size_t sm = sizeof(uint2) * TILE + sizeof(uint32_t) * (NW * (1 << BITS) + (1 << BITS) + NW + 2) +
+                    (RANK == 2 ? sizeof(uint32_t) * NW * (1 << BITS) : 0);
   // the attribute is per device: set once per device (before any graph capture of a step)
   static bool attr[kMaxDevices] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= kMaxDevices || !attr[dev]) {
-    cudaFuncSetAttribute(k_onesweep<BITS, ITEMS, MATCH, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(k_onesweep<BITS, ITEMS, RANK, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (dev >= 0 && dev < kMaxDevices) attr[dev] = true;
   }
   const int64_t tiles = (n + TILE - 1) / TILE;
-  launch_pdl(k_onesweep<BITS, ITEMS, MATCH, MINB>, (unsigned)tiles, kSortThreads, sm, s, a, b, n, n_dev, shift, hist,
+  launch_pdl(k_onesweep<BITS, ITEMS, RANK, MINB>, (unsigned)tiles, kSortThreads, sm, s, a, b, n, n_dev, shift, hist,
                                                                                 counter, status, epoch,
                                                                                 epoch_off);
   return cudaGetLastError();
@@ -324,8 +343,15 @@ cudaError_t radix_sort_pairs(uint2* kv0, uint2* kv1, int64_t n, const uint32_t* 
     // values stay in L1) measured best on Feed-1: the tile's global loads are latency-bound
     // and more resident CTAs overlap them (2 CTAs at 120 registers: +10% sort time; 8 or
     // 12 items at 5-8 CTAs and match.any ranking were slower)
-#define OS(BITS) e = onesweep_pass<BITS, 16, false, 4>(a, b, n, n_dev, shift, hp, ctr, ws.status, epoch, (uint32_t)p, s);
-    if (dbits == 9) { OS(9) } else { OS(8) }
+    static const int variant = [] {  // (measurement knob while the ranking variants are compared)
+      const char* v = getenv("LIRANK_SORT_VARIANT");
+      return v ? atoi(v) : 0;
+    }();
+#define OS(BITS, IT, RK, MB) e = onesweep_pass<BITS, IT, RK, MB>(a, b, n, n_dev, shift, hp, ctr, ws.status, epoch, (uint32_t)p, s);
+    if (variant == 1) { if (dbits == 9) { OS(9, 16, 2, 3) } else { OS(8, 16, 2, 3) } }
+    else if (variant == 2) { if (dbits == 9) { OS(9, 10, 2, 4) } else { OS(8, 10, 2, 4) } }
+    else if (variant == 3) { if (dbits == 9) { OS(9, 12, 2, 3) } else { OS(8, 12, 2, 3) } }
+    else { if (dbits == 9) { OS(9, 16, 0, 4) } else { OS(8, 16, 0, 4) } }
 #undef OS
     if (e != cudaSuccess) return e;
     ++*launches;

@@ -419,18 +419,23 @@ def test_requant_tracks_updates(gpu, mode, pooling, dim):
 # full-size configs (the bench's launch configuration)
 # ---------------------------------------------------------------------------
 
-@pytest.mark.parametrize("name", ["jobs", "feed1", "feed1@alpha0", "ads"])
+@pytest.mark.parametrize("name", ["jobs", "feed1", "feed1@alpha0", "ads", "feed1@elementwise", "feed1@minmax"])
 def test_full_config_train_step(gpu, name):
     """The bench's launch configuration at full size (Feed-1 also with uniform ids, the
-    alpha = 0 variant of SURVEY §8(d)'s gate: ~5x more unique rows, shorter segments)."""
+    alpha = 0 variant of SURVEY §8(d)'s gate: ~5x more unique rows, shorter segments; and
+    Feed-1 with element-wise AdaGrad and with the NEXT-4 min-max q8 store)."""
     base, _, variant = name.partition("@")
     cfg = configs.get(base)
     if variant == "alpha0":
         cfg = cfg.with_(alpha=0.0)
+    mode = "elementwise" if variant == "elementwise" else "rowwise"
+    minmax = variant == "minmax"
+    quant = O.quantize_minmax if minmax else O.quantize
     B = cfg.batch
     ids, off = gen.make_batch(cfg.table_rows, cfg.features, B, cfg.seed, 0, alpha=cfg.alpha)
     nnz = len(ids)
-    emb = make_emb(cfg, max_nnz=nnz, max_batch=B, q8=True)
+    emb = make_emb(cfg, max_nnz=nnz, max_batch=B, q8=True, adagrad=mode,
+                   q8_mode="min_max" if minmax else "middle_max")
     init_tables_gpu(emb, cfg)
     gshift = gen.grad_shift_for(nnz, cfg.dim)
     grad = torch.empty((B, cfg.num_features, cfg.dim), device=gpu)
@@ -449,10 +454,10 @@ def test_full_config_train_step(gpu, name):
     assert (got == ref).all()
     # whole backward on the compact problem
     W = comp.W.copy()
-    A = np.full(len(comp.keys), 0.1, dtype=np.float32)
+    A = np.full(len(comp.keys) if mode == "rowwise" else (len(comp.keys), cfg.dim), 0.1, dtype=np.float32)
     g_host = grad.cpu().numpy()
     assert (g_host[:3] == gen.grad_values(cfg.seed, 0, 3, cfg.num_features, cfg.dim, gshift)).all()
-    r = O.train_step(comp.pb, W, A, comp.cids, off, B, g_host, 0.05, 1e-7, 1.0, want_out=False)
+    r = O.train_step(comp.pb, W, A, comp.cids, off, B, g_host, 0.05, 1e-7, 1.0, want_out=False, mode=mode)
     u, s, bg = emb.last_dedup()
     keys, segs, bags = O.dedup(comp.pb, comp.cids, off, B)
     assert len(u) == len(comp.keys) == r["U"]
@@ -473,8 +478,8 @@ def test_full_config_train_step(gpu, name):
     rows = rng.choice(cfg.table_rows[tq], min(5000, cfg.table_rows[tq]), replace=False)
     c, mm, ss = emb.read_q8(tq, rows)
     w = emb.read_rows(tq, rows, with_acc=False)
-    codes, mid, sc, _ = O.quantize(w)
-    assert (c == codes).all() and (mm == mid).all() and (ss == sc).all()
+    codes, mid, sc, _ = quant(w)
+    assert (c.view(np.uint8) == codes.view(np.uint8)).all() and (mm == mid).all() and (ss == sc).all()
     # a10 at full size: the q8 lookup of the same batch on the sampled samples, against the
     # oracle's lookup over the oracle's quantization of the (GPU-updated) compact rows
     q8 = emb.forward_q8(dev(ids), dev(off), B).cpu().numpy()[samples]
@@ -484,8 +489,8 @@ def test_full_config_train_step(gpu, name):
     for t in np.unique(comp.table_of_key[skeys]):
         m = skeys[comp.table_of_key[skeys] == t]
         Wq[m] = emb.read_rows(int(t), comp.row_of_key[m], with_acc=False)
-    qc, qm, qs, _ = O.quantize(Wq)
-    ref_q8, _ = O.forward_q8(comp.pb, qc, qm, qs, sids, soff, len(samples))
+    qc, qm, qs, _ = quant(Wq)
+    ref_q8, _ = (O.forward_q8_minmax if minmax else O.forward_q8)(comp.pb, qc, qm, qs, sids, soff, len(samples))
     deq = np.abs(qm.astype(np.float64))[:, None] + np.abs(qc.astype(np.float64) * qs[:, None])
     mag, _ = O.forward(comp.pb, deq.astype(np.float32), sids, soff, len(samples))
     assert cond_close(q8, ref_q8, mag).all()
