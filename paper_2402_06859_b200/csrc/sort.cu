@@ -17,8 +17,6 @@
 //   (coalesced).  Each pass moves 16 B per pair.  Tiles are claimed in launch order
 //   through an atomic counter, so a look-back only waits on tiles already resident.
 
-#include <stdlib.h>
-
 #include "common.cuh"
 #include "kernels.h"
 #include "lookback.cuh"
@@ -136,20 +134,19 @@ k_hist_excl(uint32_t* hist, int bins) {
 }
 
 // ---------------------------------------------------------------------------
-// One digit pass.  ITEMS pairs per thread (tile = 256 * ITEMS); MATCH selects the warp
+// One digit pass.  ITEMS pairs per thread (tile = 256 * ITEMS); RANK selects the warp
 // ranking primitive (match.any vs a BITS-ballot multisplit).
 // ---------------------------------------------------------------------------
 // Load the warp's ITEMS x 32 pairs and rank each within the warp (stable: by item, then
 // lane) against the warp's running digit counters wh[].  FULL: every index is < n.
-// RANK selects how a lane finds the lanes holding the same digit ("peers"):
-//   0: BITS ballots (warp multisplit, ~5 instructions per bit),
-//   1: match.any,
-//   2: every lane sets its bit in a per-warp shared word of its digit (one ATOMS.OR), the
-//      warp synchronises and reads the word back; the digit's leader clears it.
+// RANK selects how a lane finds the lanes holding the same digit ("peers"): 0: BITS ballots
+// (warp multisplit), 1: match.any.  (Measured on Feed-1, 3 passes alone: ballots 0.347 ms;
+// match.any slower; a shared-memory atomic-OR match -- each lane ORs its bit into a per-warp
+// word of its digit and reads it back -- 0.41-0.44 ms at 3-4 CTAs/SM.)
 template <int BITS, int ITEMS, int RANK, bool FULL>
 __device__ __forceinline__ void load_rank(const uint2* __restrict__ in, uint2 (&kv)[ITEMS],
                                           uint32_t (&r)[ITEMS], int64_t base, int64_t n, int shift,
-                                          uint32_t* wh, uint32_t* mm, int lane, unsigned lt) {
+                                          uint32_t* wh, int lane, unsigned lt) {
   constexpr int BINS = 1 << BITS;
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
@@ -164,10 +161,6 @@ __device__ __forceinline__ void load_rank(const uint2* __restrict__ in, uint2 (&
     unsigned peers;
     if (RANK == 1) {
       peers = __match_any_sync(0xffffffffu, d);
-    } else if (RANK == 2) {
-      if (ok) atomicOr(mm + d, 1u << lane);
-      __syncwarp();
-      peers = ok ? mm[d] : 0u;
     } else {
       peers = FULL ? peers_of<BITS>(d, 0xffffffffu)
                    : peers_of<BITS + 1>(d, 0xffffffffu);  // bit BITS separates out-of-range lanes
@@ -175,10 +168,7 @@ __device__ __forceinline__ void load_rank(const uint2* __restrict__ in, uint2 (&
     const uint32_t cur = ok ? wh[d] : 0u;
     r[i] = cur + __popc(peers & lt);
     __syncwarp();
-    if (ok && lane == __ffs(peers) - 1) {
-      wh[d] = cur + __popc(peers);
-      if (RANK == 2) mm[d] = 0u;
-    }
+    if (ok && lane == __ffs(peers) - 1) wh[d] = cur + __popc(peers);
     __syncwarp();
   }
 }
@@ -199,13 +189,10 @@ k_onesweep(const uint2* __restrict__ in, uint2* __restrict__ out, int64_t n, con
   uint32_t* warp_hist = reinterpret_cast<uint32_t*>(stage + TILE);            // [NW][BINS]
   uint32_t* digit_off = warp_hist + NW * BINS;                                  // [BINS]
   uint32_t* s_misc = digit_off + BINS;                                          // [NW + 2]
-  uint32_t* match_mask = s_misc + NW + 2;                                       // RANK 2: [NW][BINS]
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) s_misc[NW] = atomicAdd(tile_counter, 1u);
   for (int i = tid; i < NW * BINS; i += kSortThreads) warp_hist[i] = 0;
-  if (RANK == 2)
-    for (int i = tid; i < NW * BINS; i += kSortThreads) match_mask[i] = 0;
   __syncthreads();
   const int64_t tile = s_misc[NW];
   const int64_t tile0 = tile * TILE;
@@ -220,9 +207,8 @@ k_onesweep(const uint2* __restrict__ in, uint2* __restrict__ out, int64_t n, con
   uint32_t* wh = warp_hist + warp * BINS;
   // every tile but the last is full: its ranking needs no bounds checks and BITS ballots
   // (the last one separates out-of-range lanes with one more bit)
-  uint32_t* mm = match_mask + warp * BINS;
-  if (tile0 + TILE <= n) load_rank<BITS, ITEMS, RANK, true>(in, kv, r, base, n, shift, wh, mm, lane, lt);
-  else load_rank<BITS, ITEMS, RANK, false>(in, kv, r, base, n, shift, wh, mm, lane, lt);
+  if (tile0 + TILE <= n) load_rank<BITS, ITEMS, RANK, true>(in, kv, r, base, n, shift, wh, lane, lt);
+  else load_rank<BITS, ITEMS, RANK, false>(in, kv, r, base, n, shift, wh, lane, lt);
   __syncthreads();
 
   // per digit: exclusive prefix over warps (in place), tile total, and the tile's
@@ -294,8 +280,7 @@ static cudaError_t onesweep_pass(const uint2* a, uint2* b, int64_t n, const uint
                                  uint32_t* counter, unsigned long long* status, const uint32_t* epoch,
                                  uint32_t epoch_off, cudaStream_t s) {
   constexpr int TILE = kSortThreads * ITEMS;
-  const size_t sm = sizeof(uint2) * TILE + sizeof(uint32_t) * (NW * (1 << BITS) + (1 << BITS) + NW + 2) +
-                    (RANK == 2 ? sizeof(uint32_t) * NW * (1 << BITS) : 0);
+  const size_t sm = sizeof(uint2) * TILE + sizeof(uint32_t) * (NW * (1 << BITS) + (1 << BITS) + NW + 2);
   // the attribute is per device: set once per device (before any graph capture of a step)
   static bool attr[kMaxDevices] = {};
   int dev = 0;
@@ -343,15 +328,8 @@ cudaError_t radix_sort_pairs(uint2* kv0, uint2* kv1, int64_t n, const uint32_t* 
     // values stay in L1) measured best on Feed-1: the tile's global loads are latency-bound
     // and more resident CTAs overlap them (2 CTAs at 120 registers: +10% sort time; 8 or
     // 12 items at 5-8 CTAs and match.any ranking were slower)
-    static const int variant = [] {  // (measurement knob while the ranking variants are compared)
-      const char* v = getenv("LIRANK_SORT_VARIANT");
-      return v ? atoi(v) : 0;
-    }();
-#define OS(BITS, IT, RK, MB) e = onesweep_pass<BITS, IT, RK, MB>(a, b, n, n_dev, shift, hp, ctr, ws.status, epoch, (uint32_t)p, s);
-    if (variant == 1) { if (dbits == 9) { OS(9, 16, 2, 3) } else { OS(8, 16, 2, 3) } }
-    else if (variant == 2) { if (dbits == 9) { OS(9, 10, 2, 4) } else { OS(8, 10, 2, 4) } }
-    else if (variant == 3) { if (dbits == 9) { OS(9, 12, 2, 3) } else { OS(8, 12, 2, 3) } }
-    else { if (dbits == 9) { OS(9, 16, 0, 4) } else { OS(8, 16, 0, 4) } }
+#define OS(BITS) e = onesweep_pass<BITS, 16, 0, 4>(a, b, n, n_dev, shift, hp, ctr, ws.status, epoch, (uint32_t)p, s);
+    if (dbits == 9) { OS(9) } else { OS(8) }
 #undef OS
     if (e != cudaSuccess) return e;
     ++*launches;
