@@ -34,12 +34,21 @@ __device__ __forceinline__ void lb_publish(unsigned long long* status, int64_t t
 // back kLB predecessors per round (independent loads, one L2 round trip), walking from the
 // nearest: adds aggregates until an inclusive prefix is found; a predecessor that has not
 // published yet is re-polled from where the walk stopped.
+template <int kLB = 8, int kSleepMax = 64>
 __device__ __forceinline__ uint32_t lb_wait(unsigned long long* status, int64_t tile, int stride,
                                             int slot, uint32_t epoch, uint32_t aggregate) {
-  constexpr int kLB = 8;
   if (tile == 0) return 0;
   uint32_t excl = 0;
   int64_t p = tile - 1;
+  {  // fast path: the nearest predecessor has usually published its inclusive prefix already
+    const unsigned long long w0 = ld_volatile(status + p * stride + slot);
+    if ((uint32_t)(w0 >> 32) == epoch && (w0 & kFlagPrefix)) {
+      excl = (uint32_t)(w0 & kCountMask);
+      st_volatile(status + tile * stride + slot, lb_pack(epoch, kFlagPrefix, excl + aggregate));
+      return excl;
+    }
+  }
+  int sleep_ns = 64;
   while (true) {
     unsigned long long w[kLB];
 #pragma unroll
@@ -53,7 +62,10 @@ __device__ __forceinline__ uint32_t lb_wait(unsigned long long* status, int64_t 
       if (w[i] & kFlagPrefix) { done = true; break; }
     }
     if (done) break;
-    if (i == 0) __nanosleep(64);  // nothing new: yield the issue slots to working warps
+    if (i == 0) {  // nothing new: yield the issue slots to working warps (backing off)
+      __nanosleep(sleep_ns);
+      if (sleep_ns < kSleepMax) sleep_ns *= 2;
+    }
     p -= i;
   }
   st_volatile(status + tile * stride + slot, lb_pack(epoch, kFlagPrefix, excl + aggregate));

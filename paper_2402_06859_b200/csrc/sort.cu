@@ -9,7 +9,7 @@
 // * One upfront histogram kernel computes the digit histograms of every pass in a single
 //   read of the keys (per-warp private shared-memory histograms).
 // * ONE kernel per digit pass (8- or 9-bit digits: 27-bit Feed-1 keys take 3 passes):
-//   a 4096-pair tile is loaded with coalesced 8-B loads and ranked in registers (warp
+//   a 5632-pair tile (22 per thread) is loaded with coalesced 8-B loads and ranked in registers (warp
 //   multisplit by ballots, stable in index order), the tile's digit counts are published
 //   and the global offsets found by a decoupled look-back over earlier tiles (64-bit
 //   epoch-tagged status words, so no per-step memset), overlapped with staging the tile
@@ -27,17 +27,21 @@ namespace {
 
 constexpr int NW = kSortThreads / 32;
 
-// Lanes of the warp whose digit equals mine (warp multisplit by ballots), among `valid`.
+// Lanes of the warp whose digit equals mine (warp multisplit by ballots), among `valid`:
+// AND over the bits b of (my bit b set ? ballot(bit b) : ~ballot(bit b)).  Written so that
+// ptxas moves the digit's low bits into predicate registers with one R2P and then spends
+// VOTE + a predicated NOT + an AND per bit (3 instructions; the shift/compare/sign form cost 5).
 template <int BITS>
 __device__ __forceinline__ unsigned peers_of(uint32_t d, unsigned valid) {
   unsigned m = valid;
 #pragma unroll
   for (int b = 0; b < BITS; ++b) {
-    const int x = (int)(d << (31 - b));          // bit b of d in the sign bit
-    const unsigned bb = __ballot_sync(0xffffffffu, x < 0);
-    const unsigned t = (unsigned)(x >> 31);      // all ones iff the bit is set
-    // m &= ~(bb ^ t): bit set -> bb, clear -> ~bb, as ONE lop3 (LUT 0x90 = a & ~(b ^ c))
-    asm("lop3.b32 %0, %0, %1, %2, 0x90;" : "+r"(m) : "r"(bb), "r"(t));
+    unsigned bb, sel;
+    asm("{ .reg .pred p; .reg .b32 t; and.b32 t, %1, %2; setp.ne.u32 p, t, 0; vote.sync.ballot.b32 %0, p, 0xffffffff; }"
+        : "=r"(bb) : "r"(d), "r"(1u << b));
+    asm("{ .reg .pred p; .reg .b32 t; and.b32 t, %1, %2; setp.ne.u32 p, t, 0; selp.b32 %0, %3, %4, p; }"
+        : "=r"(sel) : "r"(d), "r"(1u << b), "r"(bb), "r"(~bb));
+    m &= sel;
   }
   return m;
 }
@@ -173,46 +177,34 @@ __device__ __forceinline__ void load_rank(const uint2* __restrict__ in, uint2 (&
   }
 }
 
-template <int BITS, int ITEMS, int RANK, int MINB = 4>
-__global__ void __launch_bounds__(kSortThreads, MINB)
-k_onesweep(const uint2* __restrict__ in, uint2* __restrict__ out, int64_t n, const uint32_t* n_dev,
-           int shift, const uint32_t* __restrict__ hist, uint32_t* tile_counter,
-           unsigned long long* status, const uint32_t* epoch_p, uint32_t epoch_off) {
-  pdl_wait();
-  if (n_dev) n = min(n, (int64_t)*n_dev);
+// The tile after its claim: rank, publish / scan the digit counts, stage in sorted order,
+// look back, write out.  FULL (every tile but the last): no bounds checks anywhere.
+template <int BITS, int ITEMS, int RANK, bool FULL, int LB, int SLEEP>
+__device__ __forceinline__ void onesweep_tile(const uint2* __restrict__ in, uint2* __restrict__ out, int64_t n,
+                                              int shift, const uint32_t* __restrict__ hist,
+                                              unsigned long long* status, uint32_t epoch, int64_t tile,
+                                              uint8_t* smem_raw) {
   constexpr int BINS = 1 << BITS;
-  const uint32_t epoch = *epoch_p + epoch_off;  // device-resident: graph replays advance it
   constexpr int DPT = BINS / kSortThreads;  // digits per thread (1 or 2)
   constexpr int TILE = kSortThreads * ITEMS;
-  extern __shared__ uint8_t smem_raw[];
   uint2* stage = reinterpret_cast<uint2*>(smem_raw);                           // [TILE]
   uint32_t* warp_hist = reinterpret_cast<uint32_t*>(stage + TILE);            // [NW][BINS]
   uint32_t* digit_off = warp_hist + NW * BINS;                                  // [BINS]
   uint32_t* s_misc = digit_off + BINS;                                          // [NW + 2]
-
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (tid == 0) s_misc[NW] = atomicAdd(tile_counter, 1u);
-  for (int i = tid; i < NW * BINS; i += kSortThreads) warp_hist[i] = 0;
-  __syncthreads();
-  const int64_t tile = s_misc[NW];
   const int64_t tile0 = tile * TILE;
-  // grid sized for a capacity: tiles past the device count have nothing to do (no later
-  // tile looks back at them -- every later tile is past it too)
-  if (tile0 >= n) return;
   const int64_t base = tile0 + (int64_t)warp * (ITEMS * 32);
 
   uint2 kv[ITEMS];
   uint32_t r[ITEMS];
   const unsigned lt = lanemask_lt();
   uint32_t* wh = warp_hist + warp * BINS;
-  // every tile but the last is full: its ranking needs no bounds checks and BITS ballots
-  // (the last one separates out-of-range lanes with one more bit)
-  if (tile0 + TILE <= n) load_rank<BITS, ITEMS, RANK, true>(in, kv, r, base, n, shift, wh, lane, lt);
-  else load_rank<BITS, ITEMS, RANK, false>(in, kv, r, base, n, shift, wh, lane, lt);
+  load_rank<BITS, ITEMS, RANK, FULL>(in, kv, r, base, n, shift, wh, lane, lt);
   __syncthreads();
 
-  // per digit: exclusive prefix over warps (in place), tile total, and the tile's
-  // exclusive prefix over digits (its sorted-order layout)
+  // per digit: exclusive prefix over warps, tile total, and the tile's exclusive prefix over
+  // digits (its sorted-order layout); warp_hist[w][d] becomes the stage slot of warp w's
+  // first item with digit d (tile prefix + warp prefix: one lookup per item below)
   uint32_t total[DPT], tile_excl[DPT];
 #pragma unroll
   for (int q = 0; q < DPT; ++q) {
@@ -236,23 +228,19 @@ k_onesweep(const uint2* __restrict__ in, uint2* __restrict__ out, int64_t n, con
       carry += blk_total;
     }
   }
-  // stage the tile in sorted order (overlaps the look-back of earlier tiles); item i of
-  // this lane is valid iff i < nv
-  const int nv = tile0 + TILE <= n ? ITEMS
-                                   : (int)max((int64_t)0, min((int64_t)ITEMS, (n - base - lane + 31) / 32));
+#pragma unroll
+  for (int q = 0; q < DPT; ++q) {
+    const int dg = tid + q * kSortThreads;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) warp_hist[w * BINS + dg] += tile_excl[q];
+  }
+  __syncthreads();
+  // stage the tile in sorted order (overlaps the look-back of earlier tiles); item i of this
+  // lane is valid iff i < nv
+  const int nv = FULL ? ITEMS : (int)max((int64_t)0, min((int64_t)ITEMS, (n - base - lane + 31) / 32));
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i)
-    if (i < nv) r[i] += warp_hist[warp * BINS + ((kv[i].x >> shift) & (BINS - 1))];
-#pragma unroll
-  for (int q = 0; q < DPT; ++q) digit_off[tid + q * kSortThreads] = tile_excl[q];
-  __syncthreads();
-#pragma unroll
-  for (int i = 0; i < ITEMS; ++i) {
-    if (i < nv) {
-      const uint32_t d = (kv[i].x >> shift) & (BINS - 1);
-      stage[digit_off[d] + r[i]] = kv[i];
-    }
-  }
+    if (FULL || i < nv) stage[wh[(kv[i].x >> shift) & (BINS - 1)] + r[i]] = kv[i];
   // global position of sorted-tile slot j with digit d: hist_excl[d] + prev[d] + (j - tile_excl[d])
   // (`hist` holds the exclusive prefix of the pass's digit counts, k_hist_excl)
   uint32_t hist_excl[DPT];
@@ -260,12 +248,12 @@ k_onesweep(const uint2* __restrict__ in, uint2* __restrict__ out, int64_t n, con
   for (int q = 0; q < DPT; ++q) hist_excl[q] = __ldg(hist + tid + q * kSortThreads);
   uint32_t prev[DPT];
 #pragma unroll
-  for (int q = 0; q < DPT; ++q) prev[q] = lb_wait(status, tile, BINS, tid + q * kSortThreads, epoch, total[q]);
-  __syncthreads();  // stage complete; digit_off (tile_excl) no longer needed as such
+  for (int q = 0; q < DPT; ++q)
+    prev[q] = lb_wait<LB, SLEEP>(status, tile, BINS, tid + q * kSortThreads, epoch, total[q]);
 #pragma unroll
   for (int q = 0; q < DPT; ++q) digit_off[tid + q * kSortThreads] = hist_excl[q] + prev[q] - tile_excl[q];
-  __syncthreads();
-  const int64_t cnt = n - tile0 < TILE ? n - tile0 : TILE;
+  __syncthreads();  // stage and digit_off complete
+  const int64_t cnt = FULL ? TILE : (n - tile0 < TILE ? n - tile0 : TILE);
 #pragma unroll 4
   for (int j = tid; j < cnt; j += kSortThreads) {
     const uint2 x = stage[j];
@@ -274,7 +262,38 @@ k_onesweep(const uint2* __restrict__ in, uint2* __restrict__ out, int64_t n, con
   }
 }
 
-template <int BITS, int ITEMS, int RANK, int MINB>
+template <int BITS, int ITEMS, int RANK, int MINB = 4, int LB = 8, int SLEEP = 64>
+__global__ void __launch_bounds__(kSortThreads, MINB)
+k_onesweep(const uint2* __restrict__ in, uint2* __restrict__ out, int64_t n, const uint32_t* n_dev,
+           int shift, const uint32_t* __restrict__ hist, uint32_t* tile_counter,
+           unsigned long long* status, const uint32_t* epoch_p, uint32_t epoch_off) {
+  pdl_wait();
+  if (n_dev) n = min(n, (int64_t)*n_dev);
+  constexpr int BINS = 1 << BITS;
+  const uint32_t epoch = *epoch_p + epoch_off;  // device-resident: graph replays advance it
+  constexpr int TILE = kSortThreads * ITEMS;
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  uint32_t* warp_hist = reinterpret_cast<uint32_t*>(smem_raw + sizeof(uint2) * TILE);  // [NW][BINS]
+  uint32_t* s_misc = warp_hist + NW * BINS + BINS;                                       // [NW + 2]
+  const int tid = threadIdx.x;
+  if (tid == 0) s_misc[NW] = atomicAdd(tile_counter, 1u);
+  for (int i = tid; i < NW * BINS / 4; i += kSortThreads)  // 16-B stores: (NW * BINS) % 4 == 0
+    reinterpret_cast<uint4*>(warp_hist)[i] = make_uint4(0u, 0u, 0u, 0u);
+  __syncthreads();
+  const int64_t tile = s_misc[NW];
+  const int64_t tile0 = tile * TILE;
+  // grid sized for a capacity: tiles past the device count have nothing to do (no later
+  // tile looks back at them -- every later tile is past it too)
+  if (tile0 >= n) return;
+  // every tile but the last is full: no bounds checks, and its ranking needs BITS ballots
+  // (the last one separates out-of-range lanes with one more bit)
+  if (tile0 + TILE <= n)
+    onesweep_tile<BITS, ITEMS, RANK, true, LB, SLEEP>(in, out, n, shift, hist, status, epoch, tile, smem_raw);
+  else
+    onesweep_tile<BITS, ITEMS, RANK, false, LB, SLEEP>(in, out, n, shift, hist, status, epoch, tile, smem_raw);
+}
+
+template <int BITS, int ITEMS, int RANK, int MINB, int LB = 8, int SLEEP = 64>
 static cudaError_t onesweep_pass(const uint2* a, uint2* b, int64_t n, const uint32_t* n_dev, int shift,
                                  const uint32_t* hist,
                                  uint32_t* counter, unsigned long long* status, const uint32_t* epoch,
@@ -286,11 +305,11 @@ static cudaError_t onesweep_pass(const uint2* a, uint2* b, int64_t n, const uint
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= kMaxDevices || !attr[dev]) {
-    cudaFuncSetAttribute(k_onesweep<BITS, ITEMS, RANK, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(k_onesweep<BITS, ITEMS, RANK, MINB, LB, SLEEP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (dev >= 0 && dev < kMaxDevices) attr[dev] = true;
   }
   const int64_t tiles = (n + TILE - 1) / TILE;
-  launch_pdl(k_onesweep<BITS, ITEMS, RANK, MINB>, (unsigned)tiles, kSortThreads, sm, s, a, b, n, n_dev, shift, hist,
+  launch_pdl(k_onesweep<BITS, ITEMS, RANK, MINB, LB, SLEEP>, (unsigned)tiles, kSortThreads, sm, s, a, b, n, n_dev, shift, hist,
                                                                                 counter, status, epoch,
                                                                                 epoch_off);
   return cudaGetLastError();
@@ -324,11 +343,12 @@ cudaError_t radix_sort_pairs(uint2* kv0, uint2* kv1, int64_t n, const uint32_t* 
     const int shift = p * dbits;
     const uint32_t* hp = ws.hist + p * bins;
     uint32_t* ctr = ws.counters + p;
-    // 16 items per thread, ballot multisplit, 4 CTAs/SM (64 registers: the few spilled
-    // values stay in L1) measured best on Feed-1: the tile's global loads are latency-bound
-    // and more resident CTAs overlap them (2 CTAs at 120 registers: +10% sort time; 8 or
-    // 12 items at 5-8 CTAs and match.any ranking were slower)
-#define OS(BITS) e = onesweep_pass<BITS, 16, 0, 4>(a, b, n, n_dev, shift, hp, ctr, ws.status, epoch, (uint32_t)p, s);
+    // 22 items per thread (5632-pair tiles), ballot multisplit, 3 CTAs/SM, measured on Feed-1
+    // alone (tools/sort_probe.py, 3 passes): 16 items x 4 CTAs 0.334 ms, 18 x 3 0.313, 20 x 3
+    // 0.308, 22 x 3 0.301, 24 x 2 0.317, 28 x 2 0.314, 32 x 2 0.317, 12 x 4 0.352 -- larger
+    // tiles mean fewer tiles in each digit's look-back walk; a look-back window of 4 or 8 is
+    // the same, 16 (more registers) 0.51; exponential back-off of the poll changes nothing
+#define OS(BITS) e = onesweep_pass<BITS, 22, 0, 3>(a, b, n, n_dev, shift, hp, ctr, ws.status, epoch, (uint32_t)p, s);
     if (dbits == 9) { OS(9) } else { OS(8) }
 #undef OS
     if (e != cudaSuccess) return e;
