@@ -391,6 +391,8 @@ k_rle(const uint2* __restrict__ kv, int64_t n, const uint32_t* n_dev, uint32_t s
   uint32_t kk[kSortItems];
   uint32_t wcount = 0;
   const unsigned lt = lanemask_lt();
+  // (each item also loads its predecessor's key -- an L1 hit; taking it from the previous
+  // lane by a shuffle instead measured slower: 0.059 -> 0.061 ms on Feed-1)
 #pragma unroll
   for (int i = 0; i < kSortItems; ++i) {
     const int64_t idx = base + i * 32 + lane;

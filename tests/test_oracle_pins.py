@@ -410,6 +410,23 @@ def test_adagrad_second_hand_example():
             assert abs(float(A[0]) - Aexp) < 1e-7
 
 
+@pytest.mark.parametrize("mode", ["elementwise", "rowwise"])
+def test_adagrad_epsilon_outside_the_root(mode):
+    """Reading 9 (eps OUTSIDE the square root, Duchi et al. as the paper cites at P:12; TF,
+    torch) pinned where the placement is decisive: A0 = 0 and g = 1e-7 give A' = g^2 = 1e-14,
+    sqrt(A') = 1e-7 = eps, so w' = w - lr * g / (|g| + eps) = 0.5 - 0.1 / 2 = 0.45 exactly in
+    the closed form -- eps inside the root would give w' = 0.5 - 0.1 * 1e-7 / sqrt(1e-14 +
+    1e-7) ~ 0.49999997.  (The hand examples above have A' ~ 0.1-0.5, where the two forms differ
+    by ~4e-8 relative, inside their 2e-7 tolerance.)"""
+    W = np.array([[0.5, 0.5]], dtype=f32)
+    A = np.zeros((1, 2) if mode == "elementwise" else (1,), dtype=f32)
+    g = np.array([[1e-7, 1e-7]], dtype=f32)
+    O.adagrad(W, A, [0], g, 0.1, 1e-7, mode)
+    assert np.allclose(W[0], [0.45, 0.45], rtol=1e-6, atol=0)
+    inside = 0.5 - 0.1 * 1e-7 / np.sqrt(1e-14 + 1e-7)
+    assert abs(float(W[0, 0]) - inside) > 0.04
+
+
 def test_adagrad_elementwise_matches_torch_optim():
     # torch.optim.Adagrad (dense, CPU): A += g^2; w -= lr * g / (sqrt(A) + eps).
     rng = np.random.default_rng(0)
