@@ -1046,34 +1046,46 @@ def run_ours(args, cfg, rank, world, local_rank, B=None, sharding="row", scaling
 
     # ---- e2e: the user's pipeline through the C ABI's host-pointer path -----------------
     # Every step's batch (ids, offsets) starts in pinned HOST memory and is handed to the
-    # library as host pointers: emb_forward stages it into the library workspace with
-    # cudaMemcpyAsync on its stream (inside the timed region), emb_forward_q8(NULL, NULL)
-    # looks up the same staged batch from the q8 store, and emb_backward_adagrad returns the
-    # step's result S (global squared grad norm) to the host, which synchronises the host
-    # with the step as a training loop does.  The upstream gradient dL/d(pooled) is a device
-    # tensor: in a training step the dense tower's backward produces it on the GPU (the
-    # `model` object runs that tower for real); it is not host input.
+    # library as host pointers: emb_forward stages it into one of its two staging slots on
+    # its copy stream (inside the timed region; the transfer overlaps the previous step's
+    # kernels), emb_forward_q8(NULL, NULL) looks up the same staged batch from the q8 store,
+    # and emb_backward_adagrad_dev writes the step's result S (global squared grad norm) to
+    # the device, copied to pinned host memory at the end of the step; the host reads step
+    # k-1's S before it issues step k+1 (a training loop one step deep).  The upstream
+    # gradient dL/d(pooled) is a device tensor: in a training step the dense tower's backward
+    # produces it on the GPU (the `model` object runs that tower for real), not host input.
     e2e = None
     if not args.no_e2e:
         host_in = [(torch.from_numpy(ids).pin_memory(), torch.from_numpy(off).pin_memory()) for ids, off in batches]
+        S_dev = [torch.zeros(1, dtype=torch.float64, device=dev) for _ in range(2)]
+        S_host = [torch.zeros(1, dtype=torch.float64).pin_memory() for _ in range(2)]
+        evS = [torch.cuda.Event() for _ in range(2)]
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        S_seen = []
         barrier()
         torch.cuda.synchronize(dev)
         G.flush_l2(flush, stream=stream)
         with torch.cuda.stream(stream):
             t0.record(stream)
         for k in range(K):
+            slot = k % 2
             ids_h, off_h = host_in[k % len(host_in)]
             g_d = dev_in[k % len(dev_in)][2]
-            emb.forward(ids_h, off_h, B, out=out)                 # H2D staging in the library
-            emb.forward_q8(None, None, B, out=out_q8, nnz=ids_h.numel())  # the same staged batch
-            S_h = emb.backward_adagrad(g_d, LR, want_norm=True)  # S: D2H, blocks on the step
-            assert S_h > 0.0
+            emb.forward(ids_h, off_h, B, out=out)                             # H2D staged by the library
+            emb.forward_q8(None, None, B, out=out_q8, nnz=ids_h.numel())     # the same staged batch
+            emb.backward_adagrad_dev(g_d, LR, sq_norm_out=S_dev[slot])       # S on the device
+            with torch.cuda.stream(stream):
+                S_host[slot].copy_(S_dev[slot], non_blocking=True)           # D2H of the step's result
+                evS[slot].record(stream)
+            if k >= 1:
+                evS[1 - slot].synchronize()
+                S_seen.append(float(S_host[1 - slot]))
         with torch.cuda.stream(stream):
             t1.record(stream)
         torch.cuda.synchronize(dev)
+        S_seen.append(float(S_host[(K - 1) % 2]))
         barrier()
-        assert emb.sync() == 0
+        assert emb.sync() == 0 and len(S_seen) == K and min(S_seen) > 0.0
         e_ms = t0.elapsed_time(t1) / K
         if world > 1:
             t = torch.tensor([e_ms], device=dev)
@@ -1084,9 +1096,9 @@ def run_ours(args, cfg, rank, world, local_rank, B=None, sharding="row", scaling
         e2e = {"value": world * B / (e_ms / 1e3), "unit": "samples/s", "ms_per_step": e_ms,
                "h2d_bytes_per_step": h2d_b, "d2h_bytes_per_step": 8,
                "path": "pinned host ids/offsets passed to emb_forward as HOST pointers (staged H2D by the "
-                       "library on its stream) -> emb_forward_q8(NULL, NULL) on the staged batch -> "
-                       "emb_backward_adagrad(device grad = the tower's output) -> S D2H, every step; no overlap "
-                       "of the next batch's copy (the S read-back serialises the host)"}
+                       "library on its copy stream, double-buffered) -> emb_forward_q8(NULL, NULL) on the "
+                       "staged batch -> emb_backward_adagrad_dev (device grad = the tower's output) -> S D2H "
+                       "every step; the host reads step k-1's S before issuing step k+1"}
 
     # ---- a5 alone: forward -> backward with nothing beside the dedup -------------------
     # (in the step above the dedup shares the GPU with the a10 lookup on the main stream, so

@@ -33,8 +33,11 @@
  * - Streams: every call is enqueued on cfg.stream (a cudaStream_t; NULL = legacy default
  *   stream) and returns without waiting, unless it is documented to return host values.
  * - Pointers "host or device": ids, offsets, grad and out arguments may be device
- *   pointers or host pointers (detected with cudaPointerGetAttributes).  Host inputs are
- *   copied into library workspace on the stream before the kernels; a host `out` is
+ *   pointers or host pointers (detected with cudaPointerGetAttributes).  Host ids / offsets
+ *   are copied into one of two library staging slots on an internal copy stream (the call's
+ *   kernels wait for the copy; the copy waits only for the slot's previous readers, so the
+ *   next call's transfer overlaps this call's kernels); a host grad is copied on the stream
+ *   before the kernels; a host `out` is
  *   filled by a device-to-host copy after the kernels and the call then WAITS for the
  *   stream, so a host `out` is complete when the call returns.  Host inputs must stay
  *   valid until the call's work is done (a host-`out` call, emb_sync(), or a stream
@@ -287,9 +290,9 @@ EMB_API emb_status emb_quantize_mm8(emb_t h);
  * fmaf(code, scale, middle).  EMB_ESTATE before the first emb_quantize_mm8 (unless
  * EMB_F_REQUANT has kept it current).  Does not record occurrences for backward.
  * ids == offsets == NULL: look up the batch of the most recent emb_forward (batch and nnz
- * must equal its, else EMB_EINVAL; EMB_ESTATE if there was none) -- host inputs of that
- * forward are not copied again (its staged copy is used); device inputs must still hold
- * the same values. */
+ * must equal its, else EMB_EINVAL; EMB_ESTATE if there was none, or if its staging slot
+ * has since been refilled by two later host-input calls) -- host inputs of that forward are
+ * not copied again (its staged copy is used); device inputs must still hold the same values. */
 EMB_API emb_status emb_forward_q8(emb_t h, const int32_t* ids, const int32_t* offsets, int32_t batch,
                           int64_t nnz, float* out);
 

@@ -208,8 +208,12 @@ void carve(const Plan& p, Carver& cv, emb_handle* h) {
   const int64_t chunks = chunks_cap_for(nnz_cap);
   const int64_t max_unique = std::min<int64_t>(nnz_cap, p.local_rows) + 1;
   auto* meta = cv.take<FeatMeta>(F);
-  auto* stage_ids = cv.take<int>(p.max_nnz);
-  auto* stage_off = cv.take<int>(F * Bmax + 1);
+  int* stage_ids[2];
+  int* stage_off[2];
+  for (int k = 0; k < 2; ++k) {
+    stage_ids[k] = cv.take<int>(p.max_nnz);
+    stage_off[k] = cv.take<int>(F * Bmax + 1);
+  }
   auto* stage_dense = cv.take<float>(dense_cap);  // also the device out of a host `out`
   auto* off_copy = cv.take<int>(F * Bmax + 1);
   auto* kvA = cv.take<uint2>(nnz_cap);
@@ -242,8 +246,10 @@ void carve(const Plan& p, Carver& cv, emb_handle* h) {
   if (h) {
     h->order_ws = order;
     h->d_meta = meta;
-    h->stage_ids = stage_ids;
-    h->stage_off = stage_off;
+    for (int k = 0; k < 2; ++k) {
+      h->stage_ids[k] = stage_ids[k];
+      h->stage_off[k] = stage_off[k];
+    }
     h->stage_dense = stage_dense;
     h->off_copy = off_copy;
     h->kvA = kvA; h->kvB = kvB; h->chunk_u0 = cu0;
@@ -298,14 +304,29 @@ emb_status stage_inputs(emb_t h, const int32_t* ids, const int32_t* offsets, int
   s->offsets = offsets;
   s->out = out;
   s->host_out = false;
-  if (nnz > 0 && !is_device_ptr(ids)) {
-    CK(cudaMemcpyAsync(h->stage_ids, ids, sizeof(int) * nnz, cudaMemcpyHostToDevice, h->stream));
-    s->ids = h->stage_ids;
-  }
-  if (!is_device_ptr(offsets)) {
-    CK(cudaMemcpyAsync(h->stage_off, offsets, sizeof(int) * (nbags + 1), cudaMemcpyHostToDevice,
-                       h->stream));
-    s->offsets = h->stage_off;
+  s->slot = -1;
+  const bool host_ids = nnz > 0 && !is_device_ptr(ids), host_off = !is_device_ptr(offsets);
+  if (host_ids || host_off) {
+    // copy stream, double-buffered slot: waits only for the slot's previous readers
+    const int k = h->stage_next;
+    h->stage_next ^= 1;
+    if (k == h->last_slot) {  // the last forward's staged batch is overwritten
+      h->last_ids = nullptr;
+      h->last_off = nullptr;
+      h->last_slot = -1;
+    }
+    CK(cudaStreamWaitEvent(h->copy, h->ev_free[k], 0));
+    if (host_ids) {
+      CK(cudaMemcpyAsync(h->stage_ids[k], ids, sizeof(int) * nnz, cudaMemcpyHostToDevice, h->copy));
+      s->ids = h->stage_ids[k];
+    }
+    if (host_off) {
+      CK(cudaMemcpyAsync(h->stage_off[k], offsets, sizeof(int) * (nbags + 1), cudaMemcpyHostToDevice, h->copy));
+      s->offsets = h->stage_off[k];
+    }
+    CK(cudaEventRecord(h->ev_ready[k], h->copy));
+    CK(cudaStreamWaitEvent(h->stream, h->ev_ready[k], 0));
+    s->slot = k;
   }
   if (!is_device_ptr(out)) {
     s->out = h->stage_dense;
@@ -313,6 +334,11 @@ emb_status stage_inputs(emb_t h, const int32_t* ids, const int32_t* offsets, int
   } else if ((h->p.D & 3) == 0 && !aligned(out, 16)) {
     return EMB_EINVAL;
   }
+  return EMB_OK;
+}
+
+emb_status release_stage(emb_t h, const Staged& s) {
+  if (s.slot >= 0) CK(cudaEventRecord(h->ev_free[s.slot], h->stream));
   return EMB_OK;
 }
 
@@ -627,6 +653,12 @@ emb_status emb_create(const emb_config* cfg, const emb_buffers* buf, emb_t* out)
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_kv, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_dedup, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->copy, cudaStreamNonBlocking);
+  for (int k = 0; k < 2 && e == cudaSuccess; ++k) {
+    e = cudaEventCreateWithFlags(&h->ev_ready[k], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_free[k], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventRecord(h->ev_free[k], h->stream);  // slots start free
+  }
   if (e != cudaSuccess) { delete h; return EMB_ECUDA; }
   if (p.exch) {
     h->comm = (p.flags & EMB_F_LOOPBACK)   ? make_loopback_transport((void*)cfg->nccl_unique_id, p.rank)
@@ -647,6 +679,14 @@ emb_status emb_destroy(emb_t h) {
   }
   if (h->ev_kv) cudaEventDestroy(h->ev_kv);
   if (h->ev_dedup) cudaEventDestroy(h->ev_dedup);
+  if (h->copy) {
+    cudaStreamSynchronize(h->copy);
+    cudaStreamDestroy(h->copy);
+  }
+  for (int k = 0; k < 2; ++k) {
+    if (h->ev_ready[k]) cudaEventDestroy(h->ev_ready[k]);
+    if (h->ev_free[k]) cudaEventDestroy(h->ev_free[k]);
+  }
   delete h->comm;
   delete h;
   return EMB_OK;
@@ -720,6 +760,7 @@ emb_status emb_forward(emb_t h, const int32_t* ids, const int32_t* offsets, int3
   h->last_off = st.offsets;
   h->last_B = batch;
   h->last_nnz = nnz;
+  h->last_slot = st.slot;
   if (p.exch) {
     s = exchange_forward(h, st, batch, nnz, /*q8=*/false);
     if (s != EMB_OK) return s;
@@ -760,6 +801,7 @@ emb_status emb_forward(emb_t h, const int32_t* ids, const int32_t* offsets, int3
     h->fwd_B = batch;
     if ((s = launch_dedup(h)) != EMB_OK) return s;  // a5 starts now, on the side stream
   }
+  if ((s = release_stage(h, st)) != EMB_OK) return s;
   if (st.host_out) {
     Phase ph(h->prof, h->stream, EMB_PH_COPY);
     CK(cudaMemcpyAsync(out, st.out, sizeof(float) * (int64_t)batch * p.F * p.D,
@@ -790,11 +832,7 @@ emb_status emb_forward_q8(emb_t h, const int32_t* ids, const int32_t* offsets, i
     s = stage_inputs(h, ids, offsets, batch, nnz, out, &st);
   }
   if (s != EMB_OK) return s;
-  if (!reuse && ((st.ids == h->stage_ids && h->last_ids == h->stage_ids) ||
-                 (st.offsets == h->stage_off && h->last_off == h->stage_off))) {
-    h->last_ids = nullptr;  // the staging area now holds this batch, not the forward's
-    h->last_off = nullptr;
-  }
+  if (reuse) st.slot = h->last_slot;  // the forward's staged batch: its slot is read again
   if (p.exch) {
     s = exchange_forward(h, st, batch, nnz, /*q8=*/true);
     if (s != EMB_OK) return s;
@@ -823,6 +861,7 @@ emb_status emb_forward_q8(emb_t h, const int32_t* ids, const int32_t* offsets, i
     }
     h->launches += a.order_ready ? 1 : fwd_launches((int64_t)p.F * batch, true, false);
   }
+  if ((s = release_stage(h, st)) != EMB_OK) return s;
   if (st.host_out) {
     Phase ph(h->prof, h->stream, EMB_PH_COPY);
     CK(cudaMemcpyAsync(out, st.out, sizeof(float) * (int64_t)batch * p.F * p.D,

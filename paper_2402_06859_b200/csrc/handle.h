@@ -159,8 +159,15 @@ struct emb_handle {
   const int* order_offsets = nullptr;  // offsets (device) + bag count the order was built for by
   int64_t order_bags = -1;             // the last unsharded a2 forward (a10 reuses it)
   lirank::FeatMeta* d_meta = nullptr;
-  int* stage_ids = nullptr;
-  int* stage_off = nullptr;
+  // host inputs are staged into one of two slots on the copy stream (double-buffered: the
+  // next call's host-to-device copy overlaps this call's kernels on the main stream)
+  int* stage_ids[2] = {nullptr, nullptr};
+  int* stage_off[2] = {nullptr, nullptr};
+  cudaStream_t copy = nullptr;
+  cudaEvent_t ev_ready[2] = {nullptr, nullptr};  // slot filled (copy stream)
+  cudaEvent_t ev_free[2] = {nullptr, nullptr};   // slot's last reader done (main stream)
+  int stage_next = 0;                            // slot the next host input goes to
+  int last_slot = -1;                            // slot holding the last forward's inputs
   float* stage_dense = nullptr;
   int* off_copy = nullptr;
   uint2 *kvA = nullptr, *kvB = nullptr;  // {row key, grad row} per occurrence (sort ping-pong)
@@ -225,7 +232,10 @@ struct Staged {
   const int* offsets;
   float* out;
   bool host_out;
+  int slot;  // staging slot the inputs were copied to (-1: device inputs, nothing staged)
 };
+// after the kernels of a call that read staged inputs: the slot may be refilled
+emb_status release_stage(emb_t h, const Staged& s);
 emb_status stage_inputs(emb_t h, const int32_t* ids, const int32_t* offsets, int32_t batch,
                         int64_t nnz, float* out, Staged* s);
 

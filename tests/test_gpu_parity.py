@@ -121,6 +121,65 @@ def test_forward_host_pointers_equal_device(gpu):
     assert (out_h.numpy() == a).all()
 
 
+def test_host_out_is_complete_when_the_call_returns(gpu):
+    """a host `out` is filled and the call waits for it -- reading it right after
+    the call (no emb_sync) sees the result, even with ~0.1 s of device work queued ahead."""
+    cfg = configs.tiny()
+    ids, off = gen.make_batch(cfg.table_rows, cfg.features, cfg.batch, cfg.seed, 2)
+    emb = make_emb(cfg, max_nnz=len(ids), max_batch=cfg.batch, q8=True)
+    init_tables_host(emb, cfg)
+    emb.quantize()
+    ref = emb.forward(dev(ids), dev(off), cfg.batch).cpu().numpy()
+    ref_q8 = emb.forward_q8(dev(ids), dev(off), cfg.batch).cpu().numpy()
+    for q8 in (False, True):
+        out_h = torch.full((cfg.batch, cfg.num_features, cfg.dim), 7.0).pin_memory()
+        with torch.cuda.stream(emb.stream):
+            torch.cuda._sleep(200_000_000)
+        (emb.forward_q8 if q8 else emb.forward)(dev(ids), dev(off), cfg.batch, out=out_h)
+        assert (out_h.numpy() == (ref_q8 if q8 else ref)).all()
+    assert emb.sync() == 0
+
+
+def test_forward_q8_null_inputs_reuse_the_last_forward_batch(gpu):
+    """emb_forward_q8(NULL, NULL): the batch of the last emb_forward -- host inputs are not
+    staged again (its staged copy is used); batch / nnz must match; once its staging slot has
+    been refilled by later host inputs, reuse is refused."""
+    from paper_2402_06859_b200._lib import EmbError, EMB_EINVAL, EMB_ESTATE
+    cfg = small_cfg(dim=64, rows=(4000, 900), F=[0, 1, 0])
+    B = 200
+    ids, off = gen.make_batch(cfg.table_rows, cfg.features, B, 11, 0)
+    ids2, off2 = gen.make_batch(cfg.table_rows, cfg.features, B, 12, 0)
+    emb = make_emb(cfg, max_nnz=max(len(ids), len(ids2)), max_batch=B, q8=True)
+    init_tables_host(emb, cfg)
+    emb.quantize()
+    out = torch.empty((B, cfg.num_features, 64), device=gpu)
+    with pytest.raises(EmbError) as e:  # no forward yet
+        emb.forward_q8(None, None, B, out=out, nnz=len(ids))
+    assert e.value.code == EMB_ESTATE
+    ref = emb.forward_q8(dev(ids), dev(off), B).cpu().numpy()
+    emb.forward(torch.from_numpy(ids).pin_memory(), torch.from_numpy(off).pin_memory(), B, out=out)
+    q = torch.empty_like(out)
+    emb.forward_q8(None, None, B, out=q, nnz=len(ids))
+    assert emb.sync() == 0
+    assert (q.cpu().numpy() == ref).all()
+    with pytest.raises(EmbError) as e:
+        emb.forward_q8(None, None, B, out=q, nnz=len(ids) + 1)
+    assert e.value.code == EMB_EINVAL
+    # host inputs are staged into two alternating slots: one q8 call with other host inputs
+    # keeps the forward's staged batch; the second one overwrites it and reuse is refused
+    h2 = (torch.from_numpy(ids2).pin_memory(), torch.from_numpy(off2).pin_memory())
+    emb.forward_q8(*h2, B, out=q)
+    q2 = torch.empty_like(out)
+    emb.forward_q8(None, None, B, out=q2, nnz=len(ids))
+    assert emb.sync() == 0
+    assert (q2.cpu().numpy() == ref).all()
+    emb.forward_q8(*h2, B, out=q)
+    with pytest.raises(EmbError) as e:
+        emb.forward_q8(None, None, B, out=q, nnz=len(ids))
+    assert e.value.code == EMB_ESTATE
+    assert emb.sync() == 0
+
+
 # ---------------------------------------------------------------------------
 # a5-a8 backward
 # ---------------------------------------------------------------------------
