@@ -50,14 +50,16 @@ __device__ __forceinline__ double group_sum(double x) {
 }
 
 // (the pooled-gradient rows are re-read once per id of their bag: kept in L2 with evict_last)
-template <int VPL>
+// FR (full rows: D == pitch == 4 * LPB * VPL): no bounds logic at all.
+template <int VPL, bool FR>
 __device__ __forceinline__ void load_grad_row(const float* __restrict__ grad, size_t row_off,
-                                              int D, int lane, int LPB, float4 (&r)[VPL]) {
-  const uint64_t pol = l2_policy_last();
+                                              int D, int lane, int LPB, float4 (&r)[VPL], uint64_t pol) {
 #pragma unroll
   for (int v = 0; v < VPL; ++v) {
     const int d = 4 * (lane + v * LPB);
-    if ((D & 3) == 0) {
+    if (FR) {
+      r[v] = ld_nc_f4_hint(grad + row_off + d, pol);
+    } else if ((D & 3) == 0) {
       r[v] = d < D ? ld_nc_f4_hint(grad + row_off + d, pol) : make_float4(0.f, 0.f, 0.f, 0.f);
     } else {
       r[v].x = d + 0 < D ? __ldg(grad + row_off + d + 0) : 0.f;
@@ -100,7 +102,7 @@ __device__ __forceinline__ void accumulate(double (&acc)[VPL][4], const float4 (
 }
 
 // Finish a complete segment: G[u] = (float)acc, return this lane's sum of (double)G^2.
-template <int VPL>
+template <int VPL, bool FR>
 __device__ __forceinline__ double write_G(float* G, int pitch, uint32_t u, int lane, int LPB,
                                           const double (&acc)[VPL][4]) {
   double nrm = 0.0;
@@ -108,7 +110,7 @@ __device__ __forceinline__ double write_G(float* G, int pitch, uint32_t u, int l
 #pragma unroll
   for (int v = 0; v < VPL; ++v) {
     const int vi = lane + v * LPB;
-    if (vi < nvec) {
+    if (FR || vi < nvec) {
       float4 g = make_float4((float)acc[v][0], (float)acc[v][1], (float)acc[v][2],
                              (float)acc[v][3]);
       st_f4_hint(G + (size_t)u * pitch + 4 * vi, g, l2_policy_first());  // G: streamed to a8
@@ -121,14 +123,14 @@ __device__ __forceinline__ double write_G(float* G, int pitch, uint32_t u, int l
   return nrm;
 }
 
-template <int VPL>
+template <int VPL, bool FR>
 __device__ __forceinline__ void write_partial(double* P, int pitch, int64_t c, int lane, int LPB,
                                               const double (&acc)[VPL][4]) {
   const int nvec = pitch >> 2;
 #pragma unroll
   for (int v = 0; v < VPL; ++v) {
     const int vi = lane + v * LPB;
-    if (vi < nvec) {
+    if (FR || vi < nvec) {
       double* p = P + (size_t)c * pitch + 4 * vi;
       reinterpret_cast<double2*>(p)[0] = make_double2(acc[v][0], acc[v][1]);
       reinterpret_cast<double2*>(p)[1] = make_double2(acc[v][2], acc[v][3]);
@@ -139,7 +141,7 @@ __device__ __forceinline__ void write_partial(double* P, int pitch, int64_t c, i
 }  // namespace
 
 // One lane group per chunk of 2^chunk_log2 sorted occurrences.  kv[k] = {row key, grad row}.
-template <int LPB, int VPL, bool MEAN>
+template <int LPB, int VPL, bool MEAN, bool FR>
 __global__ void __launch_bounds__(256, 4)
 k_segreduce(const uint32_t* __restrict__ seg, const uint32_t* __restrict__ Up,
             const uint2* __restrict__ kv, const uint32_t* __restrict__ chunk_u0,
@@ -153,6 +155,8 @@ k_segreduce(const uint32_t* __restrict__ seg, const uint32_t* __restrict__ Up,
   // 0.78 -> 0.72 ms on Feed-1; 1 -> 0.74, 4 -> 0.78 at 80 registers, 8 -> 1.5); key-derived
   // segment heads then took it to 0.69 ms)
   constexpr int UNR = (VPL == 1) ? 8 : (VPL == 2 ? 2 : 2);
+  if (FR) { D = 4 * LPB * VPL; pitch = D; }  // compile-time row geometry (the launcher checked)
+  const uint64_t pol = l2_policy_last();
   const int lane = threadIdx.x & (LPB - 1);
   const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LPB;
   const uint32_t U = *Up;
@@ -206,14 +210,14 @@ k_segreduce(const uint32_t* __restrict__ seg, const uint32_t* __restrict__ Up,
         const uint32_t gq = __shfl_sync(kFull, grow_l, (jj + q) & (LPB - 1), LPB);
         iv[q] = MEAN ? __shfl_sync(kFull, inv_l, (jj + q) & (LPB - 1), LPB) : 1.0;
         ok[q] = (jj + q < LPB) && (kb + jj + q < k1);
-        if (ok[q]) load_grad_row<VPL>(grad, (size_t)gq * D, D, lane, LPB, r[q]);
+        if (ok[q]) load_grad_row<VPL, FR>(grad, (size_t)gq * D, D, lane, LPB, r[q], pol);
       }
 #pragma unroll
       for (int q = 0; q < UNR; ++q) {
         if (ok[q]) {
           if ((heads >> (jj + q)) & 1u) {  // segment u finished inside this chunk
-            if (first_open) write_partial<VPL>(part_first, pitch, c, lane, LPB, acc);
-            else nrm += write_G<VPL>(G, pitch, u, lane, LPB, acc);
+            if (first_open) write_partial<VPL, FR>(part_first, pitch, c, lane, LPB, acc);
+            else nrm += write_G<VPL, FR>(G, pitch, u, lane, LPB, acc);
             zero(acc);
             ++u;
             first_open = false;
@@ -228,11 +232,11 @@ k_segreduce(const uint32_t* __restrict__ seg, const uint32_t* __restrict__ Up,
   bool owner = false;
   if (live) {
     if (first_open) {
-      write_partial<VPL>(part_first, pitch, c, lane, LPB, acc);  // continues or ends here
+      write_partial<VPL, FR>(part_first, pitch, c, lane, LPB, acc);  // continues or ends here
     } else if (k1 == n_valid || __ldg(&kv[k1].x) != __ldg(&kv[k1 - 1].x)) {
-      nrm += write_G<VPL>(G, pitch, u, lane, LPB, acc);
+      nrm += write_G<VPL, FR>(G, pitch, u, lane, LPB, acc);
     } else {
-      write_partial<VPL>(part_last, pitch, c, lane, LPB, acc);  // starts here, spills over
+      write_partial<VPL, FR>(part_last, pitch, c, lane, LPB, acc);  // starts here, spills over
       owner = true;
     }
   }
@@ -980,8 +984,9 @@ cudaError_t launch_segreduce(const BwdArgs& a, int64_t* launches, cudaStream_t s
   cudaError_t e = cudaMemsetAsync(a.owner_count, 0, 2 * sizeof(uint32_t), s);
   if (e != cudaSuccess) return e;
   const unsigned grid = (unsigned)((a.chunks * g.lpb + 255) / 256);
+  const bool full_row = (a.D & 3) == 0 && a.pitch == a.D && a.D == 4 * g.lpb * g.vpl;
 #define LAUNCH_SR(MEAN)                                                                     \
-  LIRANK_GEOM2_DISPATCH(g, (launch_pdl(k_segreduce<L_, V_, MEAN>, grid, 256, 0, s,          \
+  LIRANK_GEOM2_DISPATCH(g, (launch_pdl(full_row ? k_segreduce<L_, V_, MEAN, true> : k_segreduce<L_, V_, MEAN, false>, grid, 256, 0, s, \
                               a.seg, a.U, a.kv, a.chunk_u0, a.grad, a.offsets, a.B, a.F, a.D, \
                               a.pitch, a.chunks, a.chunk_log2, a.G, a.part_first, a.part_last, \
                               a.norm_main, a.norm_fix, a.owner_list, a.owner_count)))

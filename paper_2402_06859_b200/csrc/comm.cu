@@ -369,6 +369,12 @@ Transport* make_loopback_transport(void* hub, int rank) {
 namespace {
 
 struct HostTransport : Transport {
+  // every copy is enqueued on the caller's stream and waited for: a plain cudaMemcpy runs on
+  // the legacy stream (which non-blocking streams do not order against) and, host to device
+  // from pageable memory, may return before its DMA has landed
+  static bool copy(void* dst, const void* src, size_t bytes, cudaMemcpyKind k, cudaStream_t s) {
+    return !bytes || (cudaMemcpyAsync(dst, src, bytes, k, s) == cudaSuccess && cudaStreamSynchronize(s) == cudaSuccess);
+  }
   emb_host_comm hc;
   int world = 1, rank = 0;
   std::vector<void*> opened;
@@ -393,7 +399,7 @@ struct HostTransport : Transport {
   bool allgather(const void* send, void* recv, size_t bytes, cudaStream_t s) override {
     std::vector<uint8_t> h(bytes), all(bytes * world);
     if (cudaStreamSynchronize(s) != cudaSuccess) return false;
-    if (bytes && cudaMemcpy(h.data(), send, bytes, cudaMemcpyDeviceToHost) != cudaSuccess) return false;
+    if (!copy(h.data(), send, bytes, cudaMemcpyDeviceToHost, s)) return false;
     if (!gather(h.data(), all.data(), bytes)) return false;
     return !bytes || cudaMemcpyAsync(recv, all.data(), bytes * world, cudaMemcpyHostToDevice, s) == cudaSuccess &&
                          cudaStreamSynchronize(s) == cudaSuccess;
@@ -411,21 +417,21 @@ struct HostTransport : Transport {
     const size_t n = count * world;
     std::vector<float> h(n), all(n * world), mine(n);
     if (cudaStreamSynchronize(s) != cudaSuccess) return false;
-    if (n && cudaMemcpy(h.data(), send, n * 4, cudaMemcpyDeviceToHost) != cudaSuccess) return false;
+    if (!copy(h.data(), send, n * 4, cudaMemcpyDeviceToHost, s)) return false;
     if (!gather(h.data(), all.data(), n * 4)) return false;
     for (int r = 0; r < world; ++r)  // rank r's slice for this rank
       memcpy(mine.data() + (size_t)r * count, all.data() + (size_t)r * n + (size_t)rank * count, count * 4);
     if (!dev_tmp(n)) return false;
-    if (n && cudaMemcpy(tmp, mine.data(), n * 4, cudaMemcpyHostToDevice) != cudaSuccess) return false;
+    if (!copy(tmp, mine.data(), n * 4, cudaMemcpyHostToDevice, s)) return false;
     return sum_ranks(recv, count, s);
   }
   bool allreduce_sum_f32(float* data, size_t count, cudaStream_t s) override {
     std::vector<float> h(count), all(count * world);
     if (cudaStreamSynchronize(s) != cudaSuccess) return false;
-    if (count && cudaMemcpy(h.data(), data, count * 4, cudaMemcpyDeviceToHost) != cudaSuccess) return false;
+    if (!copy(h.data(), data, count * 4, cudaMemcpyDeviceToHost, s)) return false;
     if (!gather(h.data(), all.data(), count * 4)) return false;
     if (!dev_tmp(count * world)) return false;
-    if (count && cudaMemcpy(tmp, all.data(), count * world * 4, cudaMemcpyHostToDevice) != cudaSuccess) return false;
+    if (!copy(tmp, all.data(), count * world * 4, cudaMemcpyHostToDevice, s)) return false;
     return sum_ranks(data, count, s);
   }
   bool alltoallv(const void* send, const size_t* soff, const size_t* sbytes, void* recv,
@@ -445,8 +451,7 @@ struct HostTransport : Transport {
     for (int r = 0; r < world; ++r) {
       const int64_t b = (int64_t)sbytes[r];
       memcpy(mine.data() + sizeof(int64_t) * r, &b, sizeof(b));
-      if (b && cudaMemcpy(mine.data() + hdr + at, (const uint8_t*)send + soff[r], b, cudaMemcpyDeviceToHost) != cudaSuccess)
-        return false;
+      if (!copy(mine.data() + hdr + at, (const uint8_t*)send + soff[r], b, cudaMemcpyDeviceToHost, s)) return false;
       at += b;
     }
     if (!gather(mine.data(), all.data(), per)) return false;
@@ -458,8 +463,7 @@ struct HostTransport : Transport {
         if (r < rank) off += b;
       }
       if ((size_t)b != rbytes[src]) return false;
-      if (b && cudaMemcpy((uint8_t*)recv + roff[src], blk + hdr + off, b, cudaMemcpyHostToDevice) != cudaSuccess)
-        return false;
+      if ((size_t)b && !copy((uint8_t*)recv + roff[src], blk + hdr + off, b, cudaMemcpyHostToDevice, s)) return false;
     }
     return true;
   }
