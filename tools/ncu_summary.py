@@ -75,7 +75,26 @@ def main():
     if "--out" in sys.argv:
         open(sys.argv[sys.argv.index("--out") + 1], "w").write(f"# ncu summary of {rep}\n" + text + "\n")
     if "--json" in sys.argv:
-        j = {k: {"dram_bytes_per_launch": sum(v) / len(v), "launches": len(v)} for k, v in traffic.items()}
+        # per library phase (emb_profile's phases; what bench.py's roofline.traffic reads): the
+        # DRAM bytes of one instance of the phase = sum over its kernels of (bytes per launch x
+        # launches per step); the capture is one step of tools/profile_step.py
+        phases = {"fwd": ["k_pool_fwd_f32", "k_pool_short_f32", "k_len_hist", "k_len_scatter"],
+                  "fwd_q8": ["k_pool_fwd_q8"], "sort": ["k_radix_hist", "k_hist_excl", "k_onesweep"],
+                  "rle": ["k_rle"], "segreduce": ["k_segreduce", "k_fixup_short", "k_fixup_long"],
+                  "norm": ["k_norm_partial", "k_norm_finalize"], "update": ["k_adagrad_tma", "k_adagrad"],
+                  "quantize": ["k_quantize"]}
+        per_step = {"k_onesweep": 3}  # digit passes per step (27-bit Feed-1 keys)
+        j = {"_source": f"ncu --set full --clock-control none, one step of tools/profile_step.py ({rep}); "
+                        "dram__bytes_read.sum + dram__bytes_write.sum per phase instance"}
+        for ph, ks in phases.items():
+            tot, have = 0.0, []
+            for k in ks:
+                if k in traffic:
+                    v = traffic[k]
+                    tot += sum(v) / len(v) * per_step.get(k, 1)
+                    have.append(k)
+            if have:
+                j[ph] = {"dram_bytes_per_launch": tot, "kernels": have}
         json.dump(j, open(sys.argv[sys.argv.index("--json") + 1], "w"), indent=1)
 
 
