@@ -511,12 +511,15 @@ int64_t ora_forward_q8_minmax(const ora_cfg* c, const uint8_t* codes, const floa
                               const float* scale, const int32_t* ids, const int32_t* offsets,
                               int32_t B, float* out) {
   const int32_t D = c->dim, F = c->num_features;
+  const int64_t nbags = (int64_t)F * B;
   int64_t invalid = 0;
   int64_t* base = table_bases(c);
-  float* acc = (float*)malloc(sizeof(float) * (size_t)D);
-  for (int32_t f = 0; f < F; ++f)
-    for (int32_t b = 0; b < B; ++b) {
-      int64_t bag = (int64_t)f * B + b;
+#pragma omp parallel reduction(+ : invalid)
+  {
+    float* acc = (float*)malloc(sizeof(float) * (size_t)D);
+#pragma omp for schedule(dynamic, 512)
+    for (int64_t bag = 0; bag < nbags; ++bag) {
+      int32_t f = (int32_t)(bag / B), b = (int32_t)(bag % B);
       int32_t lo = offsets[bag], hi = offsets[bag + 1];
       for (int32_t d = 0; d < D; ++d) acc[d] = 0.0f;
       for (int32_t j = lo; j < hi; ++j) {
@@ -532,7 +535,8 @@ int64_t ora_forward_q8_minmax(const ora_cfg* c, const uint8_t* codes, const floa
       float* o = out + ((int64_t)b * F + f) * D;
       for (int32_t d = 0; d < D; ++d) o[d] = acc[d];
     }
-  free(acc);
+    free(acc);
+  }
   free(base);
   return invalid;
 }

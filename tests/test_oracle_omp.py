@@ -30,7 +30,9 @@ def test_omp_oracle_bit_identical_to_sequential(mode):
         keys, segs, bags = O.dedup(pb, ids, off, B)
         codes, mid, sc, _ = O.quantize(W)
         q, _ = O.forward_q8(pb, codes, mid, sc, ids, off, B)
-        res[par] = (r["out"], W, A, r["S"], keys, segs, bags, codes, mid, sc, q)
+        cm, mn, scm, _ = O.quantize_minmax(W)
+        qm, _ = O.forward_q8_minmax(pb, cm, mn, scm, ids, off, B)
+        res[par] = (r["out"], W, A, r["S"], keys, segs, bags, codes, mid, sc, q, cm, mn, scm, qm)
     O.set_parallel(False)
     for a, b in zip(res[False], res[True]):
         if isinstance(a, float):
