@@ -1044,10 +1044,17 @@ def run_ours(args, cfg, rank, world, local_rank, B=None, sharding="row", scaling
     assert st == 0, f"status {st} in timed region"
     step_ms = [a.elapsed_time(b) for a, b in evs]
     ms = float(np.mean(step_ms))
+    per_rank = None
     if world > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        # every rank's mean step and phase times (row-wise: the owner of the Zipf-hottest rows
+        # does more a5-a8 work); the line's time is the max over ranks
+        ph_ms = [phases[p][0] / max(phases[p][1], 1) for p in ("fwd", "sort", "segreduce", "update", "exchange")
+                 if p in phases]
+        mine = torch.tensor([ms] + ph_ms, device=dev, dtype=torch.float64)
+        allr = [torch.zeros_like(mine) for _ in range(world)]
+        dist.all_gather(allr, mine)
+        per_rank = [[round(float(x), 4) for x in r.tolist()] for r in allr]
+        ms = max(r[0] for r in per_rank)
     S, c, U = emb.last_stats()
 
     # ---- e2e: the user's pipeline through the C ABI's host-pointer path -----------------
@@ -1248,6 +1255,9 @@ def run_ours(args, cfg, rank, world, local_rank, B=None, sharding="row", scaling
         "e2e": e2e,
         "clip": {"sq_norm": S, "c": float(c)},
         "spot_check": spot,
+        "per_rank_ms": None if per_rank is None else {
+            "columns": ["step"] + [p for p in ("fwd", "sort", "segreduce", "update", "exchange") if p in phases],
+            "ranks": per_rank},
     }
     if world == 1 and not args.no_lib:
         try:
