@@ -76,7 +76,10 @@ __device__ __forceinline__ float* dst_row(float* out, uint32_t grow, int B, int 
 
 }  // namespace
 
-template <int LPB, int VPL, bool MEAN, bool EMIT, bool PEER>
+// FR (full rows: D == pitch == 4 * LPB * VPL, the D = 64 geometry): compile-time row size,
+// no bounds logic on the row loads and stores (the bounds / address arithmetic was ~40% of
+// the kernel's instructions on the ncu source page).
+template <int LPB, int VPL, bool MEAN, bool EMIT, bool PEER, bool FR>
 __global__ void __launch_bounds__(256)
 k_pool_fwd_f32(const float* __restrict__ W, int pitch, const int* __restrict__ ids,
                const int* __restrict__ offsets, int B, int F, int Fb, int D,
@@ -86,6 +89,7 @@ k_pool_fwd_f32(const float* __restrict__ W, int pitch, const int* __restrict__ i
   pdl_wait();
   constexpr int UNR = (VPL == 1) ? 4 : (VPL == 2 ? 2 : 1);
   constexpr unsigned kFull = 0xffffffffu;
+  if (FR) { D = 4 * LPB * VPL; pitch = D; }
   const int lane = threadIdx.x & (LPB - 1);
   const long long gid = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / LPB;
   const bool in_range = gid < (long long)F * B;  // predicate, never return: shuffles below
@@ -139,7 +143,7 @@ k_pool_fwd_f32(const float* __restrict__ W, int pitch, const int* __restrict__ i
 #pragma unroll
           for (int v = 0; v < VPL; ++v) {
             const int vi = lane + v * LPB;
-            r[u][v] = vi < nvec ? ld_l1_f4_hint(row + 4 * vi, pol_last) : make_float4(0.f, 0.f, 0.f, 0.f);
+            r[u][v] = (FR || vi < nvec) ? ld_l1_f4_hint(row + 4 * vi, pol_last) : make_float4(0.f, 0.f, 0.f, 0.f);
           }
         }
       }
@@ -160,7 +164,7 @@ k_pool_fwd_f32(const float* __restrict__ W, int pitch, const int* __restrict__ i
     const uint64_t pol_first = l2_policy_first();
 #pragma unroll
     for (int v = 0; v < VPL; ++v)
-      if (4 * (lane + v * LPB) < D) st_f4_hint(o + 4 * (lane + v * LPB), acc[v], pol_first);
+      if (FR || 4 * (lane + v * LPB) < D) st_f4_hint(o + 4 * (lane + v * LPB), acc[v], pol_first);
   } else {
 #pragma unroll
     for (int v = 0; v < VPL; ++v) store4(o, 4 * (lane + v * LPB), D, acc[v]);
@@ -174,7 +178,7 @@ k_pool_fwd_f32(const float* __restrict__ W, int pitch, const int* __restrict__ i
 // one-hot-heavy batches keep as many rows in flight as multi-hot ones.  Positions whose bag
 // has more ids are left to the main kernel.  A one-id bag's pooled value is its row (SUM and
 // MEAN alike); an empty bag's is 0.
-template <int LPB, int VPL, bool EMIT, bool PEER>
+template <int LPB, int VPL, bool EMIT, bool PEER, bool FR>
 __global__ void __launch_bounds__(256)
 k_pool_short_f32(const float* __restrict__ W, int pitch, const int* __restrict__ ids,
                  const int* __restrict__ offsets, int B, int F, int Fb, int D,
@@ -184,6 +188,7 @@ k_pool_short_f32(const float* __restrict__ W, int pitch, const int* __restrict__
   pdl_wait();
   constexpr int UNR = VPL >= 4 ? 2 : 4;
   constexpr unsigned kFull = 0xffffffffu;
+  if (FR) { D = 4 * LPB * VPL; pitch = D; }
   const int lane = threadIdx.x & (LPB - 1);
   const long long g = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / LPB;
   const long long nb = (long long)F * B;
@@ -222,7 +227,7 @@ k_pool_short_f32(const float* __restrict__ W, int pitch, const int* __restrict__
 #pragma unroll
       for (int v = 0; v < VPL; ++v) {
         const int vi = lane + v * LPB;
-        r[u][v] = (mm[u] && k[u] != sentinel && vi < nvec) ? ld_l1_f4_hint(W + (size_t)k[u] * pitch + 4 * vi, pol_last)
+        r[u][v] = (mm[u] && k[u] != sentinel && (FR || vi < nvec)) ? ld_l1_f4_hint(W + (size_t)k[u] * pitch + 4 * vi, pol_last)
                                                           : make_float4(0.f, 0.f, 0.f, 0.f);
       }
     }
@@ -232,7 +237,10 @@ k_pool_short_f32(const float* __restrict__ W, int pitch, const int* __restrict__
         float* o = dst_row<PEER>(out, gr[u], B, Fb, D, pm);
         const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);  // 0 + row, as the main kernel (-0 -> +0)
 #pragma unroll
-        for (int v = 0; v < VPL; ++v) store4(o, 4 * (lane + v * LPB), D, f4_add_rn(z, r[u][v]));
+        for (int v = 0; v < VPL; ++v) {
+          if (FR) st_f4(o + 4 * (lane + v * LPB), f4_add_rn(z, r[u][v]));
+          else store4(o, 4 * (lane + v * LPB), D, f4_add_rn(z, r[u][v]));
+        }
       }
   }
   if (bad) set_status(status, kStIdRange);
@@ -490,8 +498,10 @@ cudaError_t launch_pool_fwd_f32(const FwdArgs& a, cudaStream_t s) {
   const uint32_t* order = bag_order(a.offsets, bags, a.order_ws, s);
   const bool split = order != nullptr;  // short bags sit at the end of the ordered positions
   const bool peer = a.peer.base[0] != nullptr;  // fused exchange (sharded: SUM, recording)
+  const bool fr = (a.D & 3) == 0 && a.pitch == a.D && a.D == 4 * g.lpb * g.vpl;
 #define LAUNCH_F32(MEAN, EMIT, PEER)                                                       \
-  LIRANK_FWD_GEOM_DISPATCH(g, (launch_pdl(k_pool_fwd_f32<L_, V_, MEAN, EMIT, PEER>, grid, 256, 0, s, \
+  LIRANK_FWD_GEOM_DISPATCH(g, (launch_pdl(fr ? k_pool_fwd_f32<L_, V_, MEAN, EMIT, PEER, true>          \
+                                             : k_pool_fwd_f32<L_, V_, MEAN, EMIT, PEER, false>, grid, 256, 0, s, \
                               a.W, a.pitch, a.ids, a.offsets, a.B, a.F, Fb, a.D, a.meta,    \
                               a.out, a.kv_out, a.sentinel, a.status, order, split, a.peer)))
   if (peer) {
@@ -506,7 +516,8 @@ cudaError_t launch_pool_fwd_f32(const FwdArgs& a, cudaStream_t s) {
   if (split) {
     const unsigned sgrid = (unsigned)(((bags + g.lpb - 1) / g.lpb * g.lpb + 255) / 256);
 #define LAUNCH_SHORT(EMIT, PEER)                                                             \
-  LIRANK_FWD_GEOM_DISPATCH(g, (launch_pdl(k_pool_short_f32<L_, V_, EMIT, PEER>, sgrid, 256, 0, s, \
+  LIRANK_FWD_GEOM_DISPATCH(g, (launch_pdl(fr ? k_pool_short_f32<L_, V_, EMIT, PEER, true>            \
+                                             : k_pool_short_f32<L_, V_, EMIT, PEER, false>, sgrid, 256, 0, s, \
                               a.W, a.pitch, a.ids, a.offsets, a.B, a.F, Fb, a.D, a.meta,    \
                               a.out, a.kv_out, a.sentinel, a.status, order, a.peer)))
     if (peer) LAUNCH_SHORT(true, true);
