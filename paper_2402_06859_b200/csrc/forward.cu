@@ -288,9 +288,7 @@ __device__ __forceinline__ uint4 ld_nc_u4(const void* p) {
 // kernel, ids are loaded LPB at a time and broadcast by full-mask shuffles over a
 // warp-uniform trip count, so a lane spends its instructions on the dequant, not on
 // per-slot key arithmetic.
-// FR (full rows: D == 16 * LPB * VPL with the library's q8 row layout): compile-time row
-// geometry, no bounds logic (as the fp32 kernel's FR).
-template <int LPB, int VPL, bool MEAN, bool PEER, bool FR>
+template <int LPB, int VPL, bool MEAN, bool PEER>
 __global__ void __launch_bounds__(256, 4)
 k_pool_fwd_q8(const uint8_t* __restrict__ codes, int qpitch, int meta_off,
               const int* __restrict__ ids, const int* __restrict__ offsets, int B, int F, int Fb,
@@ -302,12 +300,6 @@ k_pool_fwd_q8(const uint8_t* __restrict__ codes, int qpitch, int meta_off,
   constexpr int UNR = (VPL == 1) ? 4 : 2;
   constexpr uint32_t kNone = 0xffffffffu;
   constexpr unsigned kFull = 0xffffffffu;
-  if (FR) {
-    constexpr int kD = 16 * LPB * VPL;
-    D = kD;
-    meta_off = kD;                              // round_up(D, 8)
-    qpitch = ((kD + 8 + 31) / 32) * 32;         // [codes][meta][pad to 32]
-  }
   const int lane = threadIdx.x & (LPB - 1);
   const long long gid = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / LPB;
   const bool in_range = gid < (long long)F * B;  // predicate, never return: shuffles below
@@ -349,7 +341,7 @@ k_pool_fwd_q8(const uint8_t* __restrict__ codes, int qpitch, int meta_off,
 #pragma unroll
           for (int v = 0; v < VPL; ++v) {
             const int vi = lane + v * LPB;
-            w[u][v] = (FR || vi < nv16) ? ld_l1_u4_hint(row + 16 * vi, pol_last) : make_uint4(0u, 0u, 0u, 0u);
+            w[u][v] = vi < nv16 ? ld_l1_u4_hint(row + 16 * vi, pol_last) : make_uint4(0u, 0u, 0u, 0u);
           }
         }
       }
@@ -381,7 +373,7 @@ k_pool_fwd_q8(const uint8_t* __restrict__ codes, int qpitch, int meta_off,
       const uint64_t pol_first = l2_policy_first();  // outputs: written once
 #pragma unroll
       for (int h = 0; h < 4; ++h)
-        if (FR || d + 4 * h < D) st_f4_hint(o + d + 4 * h, acc[4 * v + h], pol_first);
+        if (d + 4 * h < D) st_f4_hint(o + d + 4 * h, acc[4 * v + h], pol_first);
     } else {
 #pragma unroll
       for (int h = 0; h < 4; ++h) store4(o, d + 4 * h, D, acc[4 * v + h]);
@@ -551,11 +543,8 @@ cudaError_t launch_pool_fwd_q8(const FwdQ8Args& a, cudaStream_t s) {
   const float magic = a.minmax ? 8388608.0f : 8388736.0f;
   // (no short-bag split here: a k_pool_short_f32-style q8 kernel measured slower -- Ads a10
   // 3.24 -> 3.79 ms -- the q8 groups already hold 8 bags per warp)
-  const bool fr = (a.D % 16) == 0 && a.D == 16 * g.lpb * g.vpl && a.meta_off == a.D &&
-                  a.qpitch == (a.D + 8 + 31) / 32 * 32;
 #define LAUNCH_Q8(MEAN, PEER)                                                              \
-  LIRANK_GEOM_DISPATCH(g, (launch_pdl(fr ? k_pool_fwd_q8<L_, V_, MEAN, PEER, true>              \
-                                         : k_pool_fwd_q8<L_, V_, MEAN, PEER, false>, grid, 256, 0, s, \
+  LIRANK_GEOM_DISPATCH(g, (launch_pdl(k_pool_fwd_q8<L_, V_, MEAN, PEER>, grid, 256, 0, s,   \
                               a.codes, a.qpitch, a.meta_off, a.ids, a.offsets, a.B, a.F, Fb, \
                               a.D, a.meta, a.out, a.status, order, xmask, magic, false, a.peer)))
   if (a.peer.base[0] != nullptr) {
