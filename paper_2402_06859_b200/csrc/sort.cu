@@ -17,6 +17,8 @@
 //   (coalesced).  Each pass moves 16 B per pair.  Tiles are claimed in launch order
 //   through an atomic counter, so a look-back only waits on tiles already resident.
 
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "lookback.cuh"
@@ -367,6 +369,7 @@ cudaError_t radix_sort_pairs(uint2* kv0, uint2* kv1, int64_t n, const uint32_t* 
 // segment that contains occurrence c << chunk_log2 (chunk_u0[c]).  n: capacity (grid
 // size); n_dev (optional): the device-resident count, read by the kernel.
 // ---------------------------------------------------------------------------
+template <int ITEMS>
 __global__ void __launch_bounds__(kSortThreads)
 k_rle(const uint2* __restrict__ kv, int64_t n, const uint32_t* n_dev, uint32_t sentinel, uint32_t* unique,
       uint32_t* seg, uint32_t* U_out, uint32_t* chunk_u0, int chunk_log2, uint32_t* tile_counter,
@@ -385,16 +388,17 @@ k_rle(const uint2* __restrict__ kv, int64_t n, const uint32_t* n_dev, uint32_t s
     if (tile == 0 && tid == 0) { *U_out = 0u; seg[0] = 0u; }
     return;
   }
-  if (tile * kSortTile >= n) return;  // past the device count
-  const int64_t base = tile * kSortTile + (int64_t)warp * (kSortItems * 32);
-  unsigned ball[kSortItems];
-  uint32_t kk[kSortItems];
+  constexpr int TILE = kSortThreads * ITEMS;
+  if (tile * TILE >= n) return;  // past the device count
+  const int64_t base = tile * TILE + (int64_t)warp * (ITEMS * 32);
+  unsigned ball[ITEMS];
+  uint32_t kk[ITEMS];
   uint32_t wcount = 0;
   const unsigned lt = lanemask_lt();
   // (each item also loads its predecessor's key -- an L1 hit; taking it from the previous
   // lane by a shuffle instead measured slower: 0.059 -> 0.061 ms on Feed-1)
 #pragma unroll
-  for (int i = 0; i < kSortItems; ++i) {
+  for (int i = 0; i < ITEMS; ++i) {
     const int64_t idx = base + i * 32 + lane;
     bool head = false;
     uint32_t k = 0;
@@ -421,7 +425,7 @@ k_rle(const uint2* __restrict__ kv, int64_t n, const uint32_t* n_dev, uint32_t s
   __syncthreads();
   uint32_t pos = s_excl + s_warp[warp];
 #pragma unroll
-  for (int i = 0; i < kSortItems; ++i) {
+  for (int i = 0; i < ITEMS; ++i) {
     const int64_t idx = base + i * 32 + lane;
     const bool head = (ball[i] >> lane) & 1u;
     const uint32_t p = pos + __popc(ball[i] & lt);  // heads before idx
@@ -446,9 +450,18 @@ cudaError_t launch_rle(const uint2* kv, int64_t n, const uint32_t* n_dev, uint32
                        unsigned long long* status, const uint32_t* epoch, uint32_t epoch_off,
                        cudaStream_t s) {
   if (n == 0) return cudaSuccess;
-  const int64_t tiles = (n + kSortTile - 1) / kSortTile;
-  launch_pdl(k_rle, (unsigned)tiles, kSortThreads, 0, s, kv, n, n_dev, sentinel, unique, seg, U_out, chunk_u0,
-                                                 chunk_log2, counter, status, epoch, epoch_off);
+  static const int variant = [] {  // TEMPORARY measurement knob (RLE tile)
+    const char* v = getenv("LIRANK_RLE_ITEMS");
+    return v ? atoi(v) : 16;
+  }();
+#define RL(IT)                                                                                          \
+  {                                                                                                     \
+    const int64_t tiles = (n + kSortThreads * IT - 1) / (kSortThreads * IT);                           \
+    launch_pdl(k_rle<IT>, (unsigned)tiles, kSortThreads, 0, s, kv, n, n_dev, sentinel, unique, seg, U_out, \
+               chunk_u0, chunk_log2, counter, status, epoch, epoch_off);                                \
+  }
+  if (variant == 8) RL(8) else if (variant == 24) RL(24) else if (variant == 32) RL(32) else RL(16)
+#undef RL
   return cudaGetLastError();
 }
 
