@@ -81,8 +81,6 @@ cudaError_t launch_pool_fwd_q8(const FwdQ8Args& a, cudaStream_t s);
 // Occurrences are packed {key = stored row (sentinel if invalid), bag index} pairs.
 constexpr int kRadixBinsMax = 512;      // 8- or 9-bit digits
 constexpr int kSortThreads = 256;
-constexpr int kSortItems = 16;          // per thread
-constexpr int kSortTile = kSortThreads * kSortItems;
 constexpr int kSortTileMin = kSortThreads * 8;  // smallest onesweep tile (capacity sizing)
 constexpr int kMaxPasses = 4;           // keys < 2^32
 constexpr int kHistWords = kMaxPasses * kRadixBinsMax;
