@@ -87,6 +87,8 @@ k_pool_fwd_f32(const float* __restrict__ W, int pitch, const int* __restrict__ i
                uint2* __restrict__ kv_out, uint32_t sentinel, uint32_t* status,
               const uint32_t* __restrict__ order, bool skip_short, const PeerOut pm) {
   pdl_wait();
+  // rows in flight per group (D = 64 full rows, measured: 2 -> 0.343 ms at 48 registers, 3 ->
+  // 0.361 at 56, 4 -> 0.359 at 64; at alpha 0 all within 1%)
   constexpr int UNR = (VPL == 1) ? 4 : (VPL == 2 ? 2 : 1);
   constexpr unsigned kFull = 0xffffffffu;
   if (FR) { D = 4 * LPB * VPL; pitch = D; }
