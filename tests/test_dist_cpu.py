@@ -268,3 +268,87 @@ def test_exchange_protocol_gloo_matches_unsharded_oracle(sharding, mode):
     for p in ps:
         p.join(timeout=60)
     assert res is True, res
+
+
+# ---------------------------------------------------------------------------------------
+# sync-free a1 (exchange.cu k_push_ids / k_compact_ids / k_recv_guard): the count matrix is
+# all-gathered (device-side in the library); keys land compacted in SOURCE order -- fused: each
+# source stores at base = sum of lower ranks' counts for that owner; collective: capacity-padded
+# [W][pair_cap] slots then compaction -- and an overflow is decided identically on every rank.
+# ---------------------------------------------------------------------------------------
+
+def _a1_worker(rank, world, port, q):
+    try:
+        _init(rank, world, port)
+        rng = np.random.default_rng(100 + rank)
+        # this rank's keys per owner (variable counts, one owner much hotter)
+        counts = [int(rng.integers(0, 50)) + (120 if o == 1 else 0) for o in range(world)]
+        keys = [rng.integers(0, 1 << 20, counts[o]).astype(np.int64) + (o << 24) for o in range(world)]
+        cnt = torch.tensor(counts, dtype=torch.int64)
+        allc = [torch.zeros(world, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(allc, cnt)
+        M = torch.stack(allc).numpy()  # M[s][o] = keys rank s sends owner o
+        # reference: the variable-size all-to-all, sources concatenated in rank order
+        sz = torch.tensor(counts, dtype=torch.int64)
+        rsz = torch.zeros(world, dtype=torch.int64)
+        dist.all_to_all_single(rsz, sz)
+        flat = torch.from_numpy(np.concatenate(keys))
+        recv = torch.zeros(int(rsz.sum()), dtype=torch.int64)
+        dist.all_to_all_single(recv, flat, rsz.tolist(), sz.tolist())
+        ref = recv.numpy()
+        ok = bool((rsz.numpy() == M[:, rank]).all())
+        # fused: source s writes its keys for owner o at base_o = sum_{s' < s} M[s'][o]
+        tot_me = int(M[:, rank].sum())
+        buf = np.full(tot_me, -1, dtype=np.int64)
+        msgs = []
+        for o in range(world):
+            base = int(M[:rank, o].sum())
+            msgs.append(np.concatenate([[base], keys[o]]).astype(np.int64))
+        lens_ = torch.tensor([len(m) for m in msgs], dtype=torch.int64)
+        rl = torch.zeros(world, dtype=torch.int64)
+        dist.all_to_all_single(rl, lens_)
+        rbuf = torch.zeros(int(rl.sum()), dtype=torch.int64)
+        dist.all_to_all_single(rbuf, torch.from_numpy(np.concatenate(msgs)), rl.tolist(), lens_.tolist())
+        for m in torch.split(rbuf, rl.tolist()):
+            m = m.numpy()
+            buf[m[0]:m[0] + len(m) - 1] = m[1:]
+        ok &= bool((buf == ref).all())
+        # collective: [W][pair_cap] padded slots, then compaction in source order
+        pair_cap = 200
+        send = np.full((world, pair_cap), -7, dtype=np.int64)
+        for o in range(world):
+            send[o, :counts[o]] = keys[o]
+        pad = torch.zeros(world * pair_cap, dtype=torch.int64)
+        dist.all_to_all_single(pad, torch.from_numpy(send.ravel()))
+        pad = pad.numpy().reshape(world, pair_cap)
+        comp = np.concatenate([pad[s, :M[s, rank]] for s in range(world)])
+        ok &= bool((comp == ref).all())
+        # overflow: owner 1 is over a capacity below its total -> every rank discards
+        for cap, pcap in ((int(M[:, 1].sum()) - 1, 0), (10 ** 9, int(M.max()) - 1), (10 ** 9, 0)):
+            over = bool((M.sum(0) > cap).any() or (pcap and (M > pcap).any()))
+            flags = [torch.zeros(1) for _ in range(world)]
+            dist.all_gather(flags, torch.tensor([1.0 if over else 0.0]))
+            ok &= len({f.item() for f in flags}) == 1  # the same verdict everywhere
+            ok &= over == (cap < 10 ** 9 or pcap > 0)
+        oks = [torch.zeros(1) for _ in range(world)]
+        dist.all_gather(oks, torch.tensor([1.0 if ok else 0.0]))
+        if rank == 0:
+            q.put(all(x.item() == 1.0 for x in oks))
+        dist.destroy_process_group()
+    except Exception:  # pragma: no cover
+        import traceback
+        q.put(traceback.format_exc())
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_syncfree_a1_compaction_and_overflow_gloo(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    ps = [ctx.Process(target=_a1_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = q.get(timeout=300)
+    for p in ps:
+        p.join(timeout=60)
+    assert res is True, res
