@@ -1,4 +1,4 @@
-"""World-size-2 gloo tests of the sharded path's host logic on CPU (-m "not gpu").
+"""Multi-process (gloo, world size 2-3) tests of the sharded path's host logic on CPU (-m "not gpu").
 
 1. The C planner (emb_plan / emb_local_layout, host-only) gives every rank a consistent
    plan: the union of the ranks' stored rows covers every row exactly once.
@@ -12,6 +12,10 @@
    (final [B][F] column table-wise; per-owner slots summed in rank order row-wise) and the
    grad-row pushes to the owners, simulated as (row index, row) messages: every destination
    row is written exactly once and the result equals the unsharded oracle.
+4. The sync-free a1 (device-side count all-gather, then fused key push at the lower ranks'
+   prefix, or capacity-padded slots + compaction): both land the keys exactly where the
+   variable-size all-to-all puts them (sources in rank order), and a capacity overflow is
+   decided identically on every rank from the gathered count matrix (world sizes 2 and 3).
 """
 import ctypes as C
 import os
