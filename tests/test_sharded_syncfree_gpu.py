@@ -228,3 +228,100 @@ def test_table_wise_backward_uses_forward_batch_after_q8_of_other_batch(gpu):
     for e in embs:
         e.close()
     hub.close()
+
+
+@pytest.mark.parametrize("p2p", [True, False])
+@pytest.mark.parametrize("sharding", ["row", "table"])
+def test_sharded_empty_and_all_invalid_batches(gpu, sharding, p2p):
+    """Degenerate sharded calls: a batch with no ids at all, and one whose ids are all out of
+    range, on every rank -- zero outputs, no update, the id-range error only for the latter;
+    then a normal step still matches the oracle (the device-resident count went to 0 and back)."""
+    from paper_2402_06859_b200 import LoopbackHub, ShardedEmbedding
+    from paper_2402_06859_b200._lib import EMB_EIDRANGE
+    W = 2
+    rows = [900, 300]
+    ft = [0, 1, 0]
+    cfg = configs.Config("deg", rows, 32, [(t, ("range", 0, 6)) for t in ft], 16, seed=71)
+    B, F, D = cfg.batch, cfg.num_features, cfg.dim
+    per_rank = [gen.make_batch(rows, cfg.features, B, cfg.seed + r, 0) for r in range(W)]
+    nnz_max = max(max(len(i) for i, _ in per_rank), 8)
+    hub = LoopbackHub(W)
+    embs = [ShardedEmbedding(rows, D, ft, max_nnz=nnz_max, max_batch=B, max_recv_nnz=W * nnz_max, device=gpu,
+                             stream=torch.cuda.Stream(), rank=r, world_size=W, sharding=sharding,
+                             loopback_hub=hub, p2p=p2p) for r in range(W)]
+    for e in embs:
+        init_tables_host(e, cfg)
+    torch.cuda.synchronize()
+    w0 = [e.weights.cpu().clone() for e in embs]
+    empty_off = torch.zeros(F * B + 1, dtype=torch.int32, device=gpu)
+    bad_ids = torch.full((8,), 10 ** 6, dtype=torch.int32, device=gpu)
+    bad_off = torch.tensor([0] * (F * B) + [8], dtype=torch.int32, device=gpu)
+    g = torch.ones((B, F, D), device=gpu)
+
+    def step(r, ids, off):
+        e = embs[r]
+        with torch.cuda.stream(e.stream):
+            out = torch.full((B, F, D), 3.0, device=gpu)
+            e.forward(ids, off, B, out=out)
+            e.backward_adagrad(g, 0.05)
+        return out.cpu().numpy(), e.sync()
+
+    res = run_ranks(W, lambda r: step(r, torch.zeros(0, dtype=torch.int32, device=gpu), empty_off))
+    assert all(st == 0 and (o == 0).all() for o, st in res)
+    res = run_ranks(W, lambda r: step(r, bad_ids, bad_off))
+    assert all(st == EMB_EIDRANGE and (o == 0).all() for o, st in res)
+    for e, w in zip(embs, w0):
+        assert torch.equal(e.weights.cpu(), w)
+    # a normal step afterwards
+    ids_g, off_g = global_batch(per_rank, F, B)
+    grad_g = gen.grad_values(cfg.seed, 0, W * B, F, D, gen.grad_shift_for(len(ids_g), D))
+    res = run_ranks(W, lambda r: _normal(embs[r], per_rank[r], grad_g[r * B:(r + 1) * B], B))
+    pb = O.Problem(rows, D, ft)
+    Wo = dense_tables(cfg)
+    A = np.full(cfg.total_rows, 0.1, dtype=np.float32)
+    r_or = O.train_step(pb, Wo, A, ids_g, off_g, W * B, grad_g, 0.05, 1e-7, 1.0)
+    mag, _ = O.forward(pb, np.abs(dense_tables(cfg)), ids_g, off_g, W * B)
+    for r in range(W):
+        out, st = res[r]
+        assert st == 0
+        assert cond_close(out, r_or["out"][r * B:(r + 1) * B], mag[r * B:(r + 1) * B]).all()
+    for e in embs:
+        e.close()
+    hub.close()
+
+
+def _normal(e, batch, grad, B):
+    ids, off = batch
+    with torch.cuda.stream(e.stream):
+        out = e.forward(torch.from_numpy(ids).cuda(), torch.from_numpy(off).cuda(), B)
+        e.backward_adagrad(torch.from_numpy(grad.copy()).cuda(), 0.05)
+    return out.cpu().numpy(), e.sync()
+
+
+def test_allreduce_f32_is_the_rank_ordered_sum(gpu):
+    """emb_allreduce_f32 (NEXT-2's data-parallel dense side) over the loopback transport: every
+    rank ends with the same fp32 vector, the sum over ranks in rank order."""
+    from paper_2402_06859_b200 import LoopbackHub, ShardedEmbedding
+    W = 3
+    hub = LoopbackHub(W)
+    embs = [ShardedEmbedding([100, 50], 8, [0, 1], max_nnz=16, max_batch=4, device=gpu, stream=torch.cuda.Stream(),
+                             rank=r, world_size=W, sharding="row", loopback_hub=hub) for r in range(W)]
+    rng = np.random.default_rng(9)
+    vals = [rng.standard_normal(100_003).astype(np.float32) for _ in range(W)]
+
+    def body(r):
+        t = torch.from_numpy(vals[r]).to(gpu)
+        with torch.cuda.stream(embs[r].stream):
+            embs[r].allreduce_(t)
+        embs[r].stream.synchronize()
+        return t.cpu().numpy()
+
+    res = run_ranks(W, body)
+    ref = vals[0].copy()
+    for r in range(1, W):
+        ref = (ref + vals[r]).astype(np.float32)
+    for r in range(W):
+        assert np.array_equal(res[r], ref)
+    for e in embs:
+        e.close()
+    hub.close()
