@@ -154,6 +154,7 @@ k_segreduce(const uint32_t* __restrict__ seg, const uint32_t* __restrict__ Up,
   // rows in flight per group: D=64 (VPL 2) measured best at 2 with 4 CTAs/SM (64 registers:
   // 0.78 -> 0.72 ms on Feed-1; 1 -> 0.74, 4 -> 0.78 at 80 registers, 8 -> 1.5); key-derived
   // segment heads then took it to 0.69 ms)
+  // (full-row kernel, round 2: 1 -> 0.643 ms, 2 -> 0.610, 4 -> 0.706 with spills)
   constexpr int UNR = (VPL == 1) ? 8 : (VPL == 2 ? 2 : 2);
   if (FR) { D = 4 * LPB * VPL; pitch = D; }  // compile-time row geometry (the launcher checked)
   const uint64_t pol = l2_policy_last();
@@ -985,6 +986,7 @@ cudaError_t launch_segreduce(const BwdArgs& a, int64_t* launches, cudaStream_t s
   if (e != cudaSuccess) return e;
   const unsigned grid = (unsigned)((a.chunks * g.lpb + 255) / 256);
   const bool full_row = (a.D & 3) == 0 && a.pitch == a.D && a.D == 4 * g.lpb * g.vpl;
+
 #define LAUNCH_SR(MEAN)                                                                     \
   LIRANK_GEOM2_DISPATCH(g, (launch_pdl(full_row ? k_segreduce<L_, V_, MEAN, true> : k_segreduce<L_, V_, MEAN, false>, grid, 256, 0, s, \
                               a.seg, a.U, a.kv, a.chunk_u0, a.grad, a.offsets, a.B, a.F, a.D, \
