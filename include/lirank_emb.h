@@ -173,9 +173,10 @@ typedef struct {
                                     on every rank (zero outputs, no occurrences) with sticky
                                     EMB_ENOMEM (emb_sync).                                    */
   const double* table_cost;      /* host [T] or NULL: table-wise planning weight of each table,
-                                    e.g. its expected bytes per step (B * mean bag length * 4 +
-                                    row bytes) + B * row bytes, SURVEY.md §8(e).  The
-                                    automatic plan balances these; NULL balances rows.      */
+                                    e.g. its expected bytes per step, B * L_t * (4 + row
+                                    bytes) + B * row bytes with L_t the mean ids per sample
+                                    on the table.  The automatic plan
+                                    balances these; NULL balances rows.                     */
 } emb_config;
 
 typedef struct {
