@@ -942,8 +942,11 @@ def run_ours(args, cfg, rank, world, local_rank, B=None, sharding="row", scaling
                 dist.broadcast(uid, 0)
             return uid.cpu().numpy().tobytes()
 
+        # receive capacity: a 1-rank exchange receives exactly its own ids; with N ranks an owner
+        # receives about the average share (table-wise placement by traffic; row-wise the owner of
+        # the Zipf-hottest rows ~1/3 more): 2x (the sharded a5/a6 grids are sized for it)
         shard_kw = dict(rank=rank, world_size=world, sharding=sharding, nccl_unique_id=new_uid(),
-                        max_recv_nnz=3 * max_nnz, force_exchange=args.exchange)
+                        max_recv_nnz=(2 if world > 1 else 1) * max_nnz, force_exchange=args.exchange)
         if sharding == "table":  # LPT placement by lookup traffic
             shard_kw["table_cost"] = configs.table_cost(cfg, batch=world * B)
     xmode = None
