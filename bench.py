@@ -69,6 +69,10 @@ def parse():
     ap.add_argument("--cpu-samples", type=int, default=8192,
                     help="samples of the single-core oracle timing (the all-core one runs the full batch)")
     ap.add_argument("--no-spot", action="store_true", help="skip the in-run oracle spot check")
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "host"],
+                    help="N>1: NCCL (one GPU per rank), or the library's host transport over a gloo group "
+                         "(EMB_F_HOSTCOMM: a functional check of the N-rank bench with every rank on the "
+                         "same GPU; times are not NVLink numbers)")
     return ap.parse_args()
 
 
@@ -733,7 +737,7 @@ def run_serving(args, cfg, rank, world, local_rank):
     stream.synchronize()
     K = args.steps
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
-    clocks = ClockSampler(local_rank).begin()
+    clocks = ClockSampler(dev.index).begin()
     barrier()
     torch.cuda.synchronize(dev)
     launches0 = emb.launches
@@ -780,7 +784,7 @@ def run_serving(args, cfg, rank, world, local_rank):
         assert emb.sync() == 0
         e_ms = t0.elapsed_time(t1) / K
         if world > 1:
-            t = torch.tensor([e_ms], device=dev)
+            t = torch.tensor([e_ms], device=cdev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = float(t.item())
         e2e = {"value": world * B / (e_ms / 1e3), "unit": "samples/s", "ms_per_step": e_ms,
@@ -917,10 +921,11 @@ def run_ours(args, cfg, rank, world, local_rank, B=None, sharding="row", scaling
     from paper_2402_06859_b200 import ShardedEmbedding
     from workload import gpu as G
 
-    dev = torch.device("cuda", local_rank)
+    dev = torch.device("cuda", local_rank % torch.cuda.device_count())  # (host transport: ranks may share a GPU)
     torch.cuda.set_device(dev)
     stream = torch.cuda.Stream(dev)
     B = cfg.batch if B is None else B  # this rank's batch (strong scaling: global / N)
+    cdev = torch.device("cpu") if args.transport == "host" else dev  # tensors of torch.distributed calls
     D, F = cfg.dim, cfg.num_features
 
     # inputs: nb distinct batches, resident in HBM (and pinned on the host for e2e)
@@ -935,7 +940,7 @@ def run_ours(args, cfg, rank, world, local_rank, B=None, sharding="row", scaling
         from paper_2402_06859_b200 import nccl_unique_id
 
         def new_uid():  # one NCCL unique id per communicator
-            uid = torch.zeros(128, dtype=torch.uint8, device=dev)
+            uid = torch.zeros(128, dtype=torch.uint8, device=cdev)
             if rank == 0:
                 uid.copy_(torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8))
             if world > 1:
@@ -945,8 +950,13 @@ def run_ours(args, cfg, rank, world, local_rank, B=None, sharding="row", scaling
         # receive capacity: a 1-rank exchange receives exactly its own ids; with N ranks an owner
         # receives about the average share (table-wise placement by traffic; row-wise the owner of
         # the Zipf-hottest rows ~1/3 more): 2x (the sharded a5/a6 grids are sized for it)
-        shard_kw = dict(rank=rank, world_size=world, sharding=sharding, nccl_unique_id=new_uid(),
+        shard_kw = dict(rank=rank, world_size=world, sharding=sharding,
                         max_recv_nnz=(2 if world > 1 else 1) * max_nnz, force_exchange=args.exchange)
+        if args.transport == "host" and world > 1:
+            from paper_2402_06859_b200 import HostComm
+            shard_kw["host_comm"] = HostComm()
+        else:
+            shard_kw["nccl_unique_id"] = new_uid()
         if sharding == "table":  # LPT placement by lookup traffic
             shard_kw["table_cost"] = configs.table_cost(cfg, batch=world * B)
     xmode = None
@@ -1002,7 +1012,8 @@ def run_ours(args, cfg, rank, world, local_rank, B=None, sharding="row", scaling
             xmode = f"nccl (p2p unavailable: {e})"
             emb.close()
             shard_kw["p2p"] = False
-            shard_kw["nccl_unique_id"] = new_uid()
+            if "nccl_unique_id" in shard_kw:
+                shard_kw["nccl_unique_id"] = new_uid()
             emb = make_emb()
     if not first_done:
         step(0)
@@ -1023,7 +1034,7 @@ def run_ours(args, cfg, rank, world, local_rank, B=None, sharding="row", scaling
     # ---- timed region: device-resident inputs --------------------------------------
     K = args.steps
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
-    clocks = ClockSampler(local_rank).begin()
+    clocks = ClockSampler(dev.index).begin()
     barrier()
     torch.cuda.synchronize(dev)
     launches0 = emb.launches
@@ -1053,7 +1064,7 @@ def run_ours(args, cfg, rank, world, local_rank, B=None, sharding="row", scaling
         # does more a5-a8 work); the line's time is the max over ranks
         ph_ms = [phases[p][0] / max(phases[p][1], 1) for p in ("fwd", "sort", "segreduce", "update", "exchange")
                  if p in phases]
-        mine = torch.tensor([ms] + ph_ms, device=dev, dtype=torch.float64)
+        mine = torch.tensor([ms] + ph_ms, device=cdev, dtype=torch.float64)
         allr = [torch.zeros_like(mine) for _ in range(world)]
         dist.all_gather(allr, mine)
         per_rank = [[round(float(x), 4) for x in r.tolist()] for r in allr]
@@ -1104,7 +1115,7 @@ def run_ours(args, cfg, rank, world, local_rank, B=None, sharding="row", scaling
         assert emb.sync() == 0 and len(S_seen) == K and min(S_seen) > 0.0
         e_ms = t0.elapsed_time(t1) / K
         if world > 1:
-            t = torch.tensor([e_ms], device=dev)
+            t = torch.tensor([e_ms], device=cdev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = float(t.item())
         nnz_avg = float(np.mean([len(i) for i, _ in batches]))
@@ -1335,8 +1346,11 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if args.transport == "host":
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
         if serve:
             run_serving(args, cfg, rank, world, local_rank)
