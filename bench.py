@@ -1249,11 +1249,13 @@ def run_ours(args, cfg, rank, world, local_rank, B=None, sharding="row", scaling
                        "after a device-side count all-gather (no host sync); pooled rows stored by the owners' "
                        "pooling kernels into the destination's buffer over NVLink peer memory (row-wise: "
                        "per-owner slots summed in rank order); grad rows pushed to the owners by one kernel; "
-                       "NCCL 4-byte all-gather barriers"
+                       + ("NCCL 4-byte all-gather barriers" if args.transport == "nccl" else
+                          "host-transport barriers (stream drain + gloo all-gather; ranks share one GPU)")
                        if xmode == "p2p" else
                        f"{xmode}: ids all-to-all of capacity-padded slots (no host sync); " +
                        ("reduce-scatter pooled, all-gather grads" if sharding == "row"
                         else "all-to-all pooled / grad blocks + permute")),
+                   "transport": None if world == 1 and not args.exchange else args.transport,
                    "step": "a2 fwd -> a10 q8 fwd (overlapping a5 dedup on a side stream) -> a6-a8 bwd (a9 requant of touched rows fused)",
                    "l2": "flushed between timed steps (256 MiB write, untimed)",
                    "batches_rotated": len(batches)},
