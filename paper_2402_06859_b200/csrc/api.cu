@@ -305,6 +305,9 @@ emb_status stage_inputs(emb_t h, const int32_t* ids, const int32_t* offsets, int
   s->out = out;
   s->host_out = false;
   s->slot = -1;
+  // argument errors first: nothing is enqueued for a call that fails
+  const bool dev_out = is_device_ptr(out);
+  if (dev_out && (h->p.D & 3) == 0 && !aligned(out, 16)) return EMB_EINVAL;
   const bool host_ids = nnz > 0 && !is_device_ptr(ids), host_off = !is_device_ptr(offsets);
   if (host_ids || host_off) {
     // copy stream, double-buffered slot: waits only for the slot's previous readers
@@ -328,11 +331,9 @@ emb_status stage_inputs(emb_t h, const int32_t* ids, const int32_t* offsets, int
     CK(cudaStreamWaitEvent(h->stream, h->ev_ready[k], 0));
     s->slot = k;
   }
-  if (!is_device_ptr(out)) {
+  if (!dev_out) {
     s->out = h->stage_dense;
     s->host_out = true;
-  } else if ((h->p.D & 3) == 0 && !aligned(out, 16)) {
-    return EMB_EINVAL;
   }
   return EMB_OK;
 }
