@@ -9,7 +9,7 @@
 // * One upfront histogram kernel computes the digit histograms of every pass in a single
 //   read of the keys (per-warp private shared-memory histograms).
 // * ONE kernel per digit pass (8- or 9-bit digits: 27-bit Feed-1 keys take 3 passes):
-//   a 5632-pair tile (22 per thread) is loaded with coalesced 8-B loads and ranked in registers (warp
+//   an 8192-pair tile (512 threads x 16) is loaded with coalesced 8-B loads and ranked in registers (warp
 //   multisplit by ballots, stable in index order), the tile's digit counts are published
 //   and the global offsets found by a decoupled look-back over earlier tiles (64-bit
 //   epoch-tagged status words, so no per-step memset), overlapped with staging the tile
@@ -46,8 +46,9 @@ __device__ __forceinline__ unsigned peers_of(uint32_t d, unsigned valid) {
   return m;
 }
 
-// Exclusive block scan of one value per thread (256 threads); returns the exclusive
+// Exclusive block scan of one value per thread (NWARPS warps); returns the exclusive
 // prefix, *total gets the block sum.
+template <int NWARPS = NW>
 __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp, uint32_t* total) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t x = v;
@@ -60,7 +61,7 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp
   __syncthreads();
   uint32_t wpre = 0, tot = 0;
 #pragma unroll
-  for (int w = 0; w < NW; ++w) {
+  for (int w = 0; w < NWARPS; ++w) {
     const uint32_t s = s_warp[w];
     if (w < warp) wpre += s;
     tot += s;
@@ -179,18 +180,19 @@ __device__ __forceinline__ void load_rank(const uint2* __restrict__ in, uint2 (&
 
 // The tile after its claim: rank, publish / scan the digit counts, stage in sorted order,
 // look back, write out.  FULL (every tile but the last): no bounds checks anywhere.
-template <int BITS, int ITEMS, int RANK, bool FULL, int LB, int SLEEP>
+template <int BITS, int ITEMS, int RANK, bool FULL, int LB, int SLEEP, int THREADS>
 __device__ __forceinline__ void onesweep_tile(const uint2* __restrict__ in, uint2* __restrict__ out, int64_t n,
                                               int shift, const uint32_t* __restrict__ hist,
                                               unsigned long long* status, uint32_t epoch, int64_t tile,
                                               uint8_t* smem_raw) {
   constexpr int BINS = 1 << BITS;
-  constexpr int DPT = BINS / kSortThreads;  // digits per thread (1 or 2)
-  constexpr int TILE = kSortThreads * ITEMS;
+  constexpr int NWT = THREADS / 32;
+  constexpr int DPT = (BINS + THREADS - 1) / THREADS;  // digits per thread (digit tid + q * THREADS)
+  constexpr int TILE = THREADS * ITEMS;
   uint2* stage = reinterpret_cast<uint2*>(smem_raw);                           // [TILE]
-  uint32_t* warp_hist = reinterpret_cast<uint32_t*>(stage + TILE);            // [NW][BINS]
-  uint32_t* digit_off = warp_hist + NW * BINS;                                  // [BINS]
-  uint32_t* s_misc = digit_off + BINS;                                          // [NW + 2]
+  uint32_t* warp_hist = reinterpret_cast<uint32_t*>(stage + TILE);            // [NWT][BINS]
+  uint32_t* digit_off = warp_hist + NWT * BINS;                                  // [BINS]
+  uint32_t* s_misc = digit_off + BINS;                                          // [NWT + 2]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t tile0 = tile * TILE;
   const int64_t base = tile0 + (int64_t)warp * (ITEMS * 32);
@@ -208,31 +210,34 @@ __device__ __forceinline__ void onesweep_tile(const uint2* __restrict__ in, uint
   uint32_t total[DPT], tile_excl[DPT];
 #pragma unroll
   for (int q = 0; q < DPT; ++q) {
-    const int dg = tid + q * kSortThreads;
+    const int dg = tid + q * THREADS;
     uint32_t t = 0;
+    if (dg < BINS) {
 #pragma unroll
-    for (int w = 0; w < NW; ++w) {
-      const uint32_t c = warp_hist[w * BINS + dg];
-      warp_hist[w * BINS + dg] = t;
-      t += c;
+      for (int w = 0; w < NWT; ++w) {
+        const uint32_t c = warp_hist[w * BINS + dg];
+        warp_hist[w * BINS + dg] = t;
+        t += c;
+      }
+      lb_publish(status, tile, BINS, dg, epoch, t);
     }
     total[q] = t;
-    lb_publish(status, tile, BINS, dg, epoch, t);
   }
   {
     uint32_t carry = 0;
 #pragma unroll
     for (int q = 0; q < DPT; ++q) {
       uint32_t blk_total;
-      tile_excl[q] = carry + block_excl_scan(total[q], s_misc, &blk_total);
+      tile_excl[q] = carry + block_excl_scan<NWT>(total[q], s_misc, &blk_total);
       carry += blk_total;
     }
   }
 #pragma unroll
   for (int q = 0; q < DPT; ++q) {
-    const int dg = tid + q * kSortThreads;
+    const int dg = tid + q * THREADS;
+    if (dg < BINS)
 #pragma unroll
-    for (int w = 0; w < NW; ++w) warp_hist[w * BINS + dg] += tile_excl[q];
+      for (int w = 0; w < NWT; ++w) warp_hist[w * BINS + dg] += tile_excl[q];
   }
   __syncthreads();
   // stage the tile in sorted order (overlaps the look-back of earlier tiles); item i of this
@@ -245,25 +250,26 @@ __device__ __forceinline__ void onesweep_tile(const uint2* __restrict__ in, uint
   // (`hist` holds the exclusive prefix of the pass's digit counts, k_hist_excl)
   uint32_t hist_excl[DPT];
 #pragma unroll
-  for (int q = 0; q < DPT; ++q) hist_excl[q] = __ldg(hist + tid + q * kSortThreads);
+  for (int q = 0; q < DPT; ++q) hist_excl[q] = tid + q * THREADS < BINS ? __ldg(hist + tid + q * THREADS) : 0u;
   uint32_t prev[DPT];
 #pragma unroll
   for (int q = 0; q < DPT; ++q)
-    prev[q] = lb_wait<LB, SLEEP>(status, tile, BINS, tid + q * kSortThreads, epoch, total[q]);
+    prev[q] = tid + q * THREADS < BINS ? lb_wait<LB, SLEEP>(status, tile, BINS, tid + q * THREADS, epoch, total[q]) : 0u;
 #pragma unroll
-  for (int q = 0; q < DPT; ++q) digit_off[tid + q * kSortThreads] = hist_excl[q] + prev[q] - tile_excl[q];
+  for (int q = 0; q < DPT; ++q)
+    if (tid + q * THREADS < BINS) digit_off[tid + q * THREADS] = hist_excl[q] + prev[q] - tile_excl[q];
   __syncthreads();  // stage and digit_off complete
   const int64_t cnt = FULL ? TILE : (n - tile0 < TILE ? n - tile0 : TILE);
 #pragma unroll 4
-  for (int j = tid; j < cnt; j += kSortThreads) {
+  for (int j = tid; j < cnt; j += THREADS) {
     const uint2 x = stage[j];
     const uint32_t d = (x.x >> shift) & (BINS - 1);
     out[digit_off[d] + j] = x;
   }
 }
 
-template <int BITS, int ITEMS, int RANK, int MINB = 4, int LB = 8, int SLEEP = 64>
-__global__ void __launch_bounds__(kSortThreads, MINB)
+template <int BITS, int ITEMS, int RANK, int MINB = 4, int LB = 8, int SLEEP = 64, int THREADS = kSortThreads>
+__global__ void __launch_bounds__(THREADS, MINB)
 k_onesweep(const uint2* __restrict__ in, uint2* __restrict__ out, int64_t n, const uint32_t* n_dev,
            int shift, const uint32_t* __restrict__ hist, uint32_t* tile_counter,
            unsigned long long* status, const uint32_t* epoch_p, uint32_t epoch_off) {
@@ -271,16 +277,17 @@ k_onesweep(const uint2* __restrict__ in, uint2* __restrict__ out, int64_t n, con
   if (n_dev) n = min(n, (int64_t)*n_dev);
   constexpr int BINS = 1 << BITS;
   const uint32_t epoch = *epoch_p + epoch_off;  // device-resident: graph replays advance it
-  constexpr int TILE = kSortThreads * ITEMS;
+  constexpr int TILE = THREADS * ITEMS;
+  constexpr int NWT = THREADS / 32;
   extern __shared__ __align__(16) uint8_t smem_raw[];
-  uint32_t* warp_hist = reinterpret_cast<uint32_t*>(smem_raw + sizeof(uint2) * TILE);  // [NW][BINS]
-  uint32_t* s_misc = warp_hist + NW * BINS + BINS;                                       // [NW + 2]
+  uint32_t* warp_hist = reinterpret_cast<uint32_t*>(smem_raw + sizeof(uint2) * TILE);  // [NWT][BINS]
+  uint32_t* s_misc = warp_hist + NWT * BINS + BINS;                                       // [NWT + 2]
   const int tid = threadIdx.x;
-  if (tid == 0) s_misc[NW] = atomicAdd(tile_counter, 1u);
-  for (int i = tid; i < NW * BINS / 4; i += kSortThreads)  // 16-B stores: (NW * BINS) % 4 == 0
+  if (tid == 0) s_misc[NWT] = atomicAdd(tile_counter, 1u);
+  for (int i = tid; i < NWT * BINS / 4; i += THREADS)  // 16-B stores: (NWT * BINS) % 4 == 0
     reinterpret_cast<uint4*>(warp_hist)[i] = make_uint4(0u, 0u, 0u, 0u);
   __syncthreads();
-  const int64_t tile = s_misc[NW];
+  const int64_t tile = s_misc[NWT];
   const int64_t tile0 = tile * TILE;
   // grid sized for a capacity: tiles past the device count have nothing to do (no later
   // tile looks back at them -- every later tile is past it too)
@@ -288,28 +295,29 @@ k_onesweep(const uint2* __restrict__ in, uint2* __restrict__ out, int64_t n, con
   // every tile but the last is full: no bounds checks, and its ranking needs BITS ballots
   // (the last one separates out-of-range lanes with one more bit)
   if (tile0 + TILE <= n)
-    onesweep_tile<BITS, ITEMS, RANK, true, LB, SLEEP>(in, out, n, shift, hist, status, epoch, tile, smem_raw);
+    onesweep_tile<BITS, ITEMS, RANK, true, LB, SLEEP, THREADS>(in, out, n, shift, hist, status, epoch, tile, smem_raw);
   else
-    onesweep_tile<BITS, ITEMS, RANK, false, LB, SLEEP>(in, out, n, shift, hist, status, epoch, tile, smem_raw);
+    onesweep_tile<BITS, ITEMS, RANK, false, LB, SLEEP, THREADS>(in, out, n, shift, hist, status, epoch, tile, smem_raw);
 }
 
-template <int BITS, int ITEMS, int RANK, int MINB, int LB = 8, int SLEEP = 64>
+template <int BITS, int ITEMS, int RANK, int MINB, int LB = 8, int SLEEP = 64, int THREADS = kSortThreads>
 static cudaError_t onesweep_pass(const uint2* a, uint2* b, int64_t n, const uint32_t* n_dev, int shift,
                                  const uint32_t* hist,
                                  uint32_t* counter, unsigned long long* status, const uint32_t* epoch,
                                  uint32_t epoch_off, cudaStream_t s) {
-  constexpr int TILE = kSortThreads * ITEMS;
-  const size_t sm = sizeof(uint2) * TILE + sizeof(uint32_t) * (NW * (1 << BITS) + (1 << BITS) + NW + 2);
+  constexpr int TILE = THREADS * ITEMS;
+  constexpr int NWT = THREADS / 32;
+  const size_t sm = sizeof(uint2) * TILE + sizeof(uint32_t) * (NWT * (1 << BITS) + (1 << BITS) + NWT + 2);
   // the attribute is per device: set once per device (before any graph capture of a step)
   static bool attr[kMaxDevices] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= kMaxDevices || !attr[dev]) {
-    cudaFuncSetAttribute(k_onesweep<BITS, ITEMS, RANK, MINB, LB, SLEEP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(k_onesweep<BITS, ITEMS, RANK, MINB, LB, SLEEP, THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (dev >= 0 && dev < kMaxDevices) attr[dev] = true;
   }
   const int64_t tiles = (n + TILE - 1) / TILE;
-  launch_pdl(k_onesweep<BITS, ITEMS, RANK, MINB, LB, SLEEP>, (unsigned)tiles, kSortThreads, sm, s, a, b, n, n_dev, shift, hist,
+  launch_pdl(k_onesweep<BITS, ITEMS, RANK, MINB, LB, SLEEP, THREADS>, (unsigned)tiles, THREADS, sm, s, a, b, n, n_dev, shift, hist,
                                                                                 counter, status, epoch,
                                                                                 epoch_off);
   return cudaGetLastError();
@@ -348,7 +356,10 @@ cudaError_t radix_sort_pairs(uint2* kv0, uint2* kv1, int64_t n, const uint32_t* 
     // 0.308, 22 x 3 0.301, 24 x 2 0.317, 28 x 2 0.314, 32 x 2 0.317, 12 x 4 0.352 -- larger
     // tiles mean fewer tiles in each digit's look-back walk; a look-back window of 4 or 8 is
     // the same, 16 (more registers) 0.51; exponential back-off of the poll changes nothing
-#define OS(BITS) e = onesweep_pass<BITS, 22, 0, 3>(a, b, n, n_dev, shift, hp, ctr, ws.status, epoch, (uint32_t)p, s);
+    // (CTA width, round 2: 512 threads x 16 items at 2 CTAs/SM 0.297 ms vs 256 x 22 at 3 CTAs
+    // 0.31 in the same run, 384 x 22 x 2 0.315, 384 x 20 x 2 0.310, 512 x 12 x 2 0.303; Ads
+    // 0.964 vs 0.998 ms: the wider tile halves the look-back walks per item at equal occupancy)
+#define OS(BITS) e = onesweep_pass<BITS, 16, 0, 2, 8, 64, 512>(a, b, n, n_dev, shift, hp, ctr, ws.status, epoch, (uint32_t)p, s);
     if (dbits == 9) { OS(9) } else { OS(8) }
 #undef OS
     if (e != cudaSuccess) return e;

@@ -59,7 +59,7 @@ sort_ms = ph["sort"][0] / ph["sort"][1]
 rle_ms = ph["rle"][0] / ph["rle"][1]
 sb, rb = n * (8 + 16 * passes), n * 8 + U * 8
 print(json.dumps({"config": cfg.name, "alpha": cfg.alpha, "nnz": n, "U": U, "passes": passes,
-                  "variant": os.environ.get("LIRANK_SORT_VARIANT", "0"),
+                  "variant": os.environ.get("LIRANK_OS_VARIANT", "0"),
                   "sort_ms": sort_ms, "rle_ms": rle_ms,
                   "sort_own_frac": sb / (sort_ms / 1e3) / 1e9 / peak,
                   "a5_own_frac": (sb + rb) / ((sort_ms + rle_ms) / 1e3) / 1e9 / peak,
