@@ -351,8 +351,8 @@ cudaError_t radix_sort_pairs(uint2* kv0, uint2* kv1, int64_t n, const uint32_t* 
     const int shift = p * dbits;
     const uint32_t* hp = ws.hist + p * bins;
     uint32_t* ctr = ws.counters + p;
-    // 22 items per thread (5632-pair tiles), ballot multisplit, 3 CTAs/SM, measured on Feed-1
-    // alone (tools/sort_probe.py, 3 passes): 16 items x 4 CTAs 0.334 ms, 18 x 3 0.313, 20 x 3
+    // tile geometry, measured on Feed-1 alone (tools/sort_probe.py, 3 passes), 256-thread CTAs
+    // first: 16 items x 4 CTAs 0.334 ms, 18 x 3 0.313, 20 x 3
     // 0.308, 22 x 3 0.301, 24 x 2 0.317, 28 x 2 0.314, 32 x 2 0.317, 12 x 4 0.352 -- larger
     // tiles mean fewer tiles in each digit's look-back walk; a look-back window of 4 or 8 is
     // the same, 16 (more registers) 0.51; exponential back-off of the poll changes nothing
