@@ -15,7 +15,7 @@ __global__ void k_ids(uint32_t* ids, int64_t n, uint64_t rows, uint64_t seed) {
   }
 }
 
-template <int UNR>
+template <int UNR, int RB = 96>
 __global__ void __launch_bounds__(256) k_ldg(const uint8_t* __restrict__ tab, const uint32_t* __restrict__ ids,
                                              int64_t n, float* out) {
   const int lane = threadIdx.x & 3;
@@ -28,7 +28,7 @@ __global__ void __launch_bounds__(256) k_ldg(const uint8_t* __restrict__ tab, co
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
       if (i + u < n) {
-        const uint8_t* row = tab + (size_t)__ldg(ids + i + u) * 96;
+        const uint8_t* row = tab + (size_t)__ldg(ids + i + u) * RB;
         asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
                      : "=r"(r[u].x), "=r"(r[u].y), "=r"(r[u].z), "=r"(r[u].w) : "l"(row + 16 * lane));
         m[u] = *reinterpret_cast<const float2*>(row + 64);
@@ -63,6 +63,32 @@ __global__ void __launch_bounds__(256) k_ldg256(const uint8_t* __restrict__ tab,
     }
 #pragma unroll
     for (int u = 0; u < UNR; ++u) acc += r[u][0].x + r[u][1].y + r[u][0].z + r[u][1].w;
+  }
+  if (acc == 12345.f) out[0] = acc;
+}
+
+// generic: a 4-lane group reads BYTES (<= 64, in 16-B lane pieces) of each random row at pitch RB
+// -- the rows/s rate as a function of row size and pitch alignment
+template <int UNR, int RB, int BYTES>
+__global__ void __launch_bounds__(256) k_ldgn(const uint8_t* __restrict__ tab, const uint32_t* __restrict__ ids,
+                                              int64_t n, float* out) {
+  const int lane = threadIdx.x & 3;
+  const int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 4;
+  const int64_t G = (gridDim.x * (int64_t)blockDim.x) / 4;
+  float acc = 0.f;
+  for (int64_t i = g * UNR; i < n; i += G * UNR) {
+    uint4 r[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      r[u] = make_uint4(0, 0, 0, 0);
+      if (i + u < n && 16 * lane < BYTES) {
+        const uint8_t* row = tab + (size_t)__ldg(ids + i + u) * RB;
+        asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(r[u].x), "=r"(r[u].y), "=r"(r[u].z), "=r"(r[u].w) : "l"(row + 16 * lane));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) acc += (float)(r[u].x ^ r[u].y ^ r[u].z ^ r[u].w);
   }
   if (acc == 12345.f) out[0] = acc;
 }
@@ -107,6 +133,43 @@ __global__ void __launch_bounds__(256) k_tma(const uint8_t* __restrict__ tab, co
   if (acc == 12345.f) out[0] = acc;
 }
 
+// per-lane LDGSTS (cp.async 16 B, L1 bypass) of each 96-B row into a per-group shared-memory ring
+// of S slots, one commit group per row: rows in flight without registers
+template <int S>
+__global__ void __launch_bounds__(256) k_ldgsts(const uint8_t* __restrict__ tab, const uint32_t* __restrict__ ids,
+                                                int64_t n, float* out) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  const int grp = threadIdx.x >> 2, lane = threadIdx.x & 3;
+  uint8_t* slots = sm + (size_t)grp * S * 96;
+  const int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 4;
+  const int64_t G = (gridDim.x * (int64_t)blockDim.x) / 4;
+  auto issue = [&](int q, int64_t i) {
+    if (i < n) {
+      const uint8_t* src = tab + (size_t)__ldg(ids + i) * 96;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(su32(slots + q * 96 + 16 * lane)), "l"(src + 16 * lane)
+                   : "memory");
+      if (lane == 0)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(su32(slots + q * 96 + 64)), "l"(src + 64)
+                     : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  for (int q = 0; q < S; ++q) issue(q, g + q * G);
+  float acc = 0.f;
+  int it = 0;
+  for (int64_t i = g; i < n; i += G, ++it) {
+    const int q = it % S;
+    asm volatile("cp.async.wait_group %0;" ::"n"(S - 1) : "memory");
+    __syncwarp(0xfu << (threadIdx.x & 28));
+    const uint4 r = reinterpret_cast<const uint4*>(slots + q * 96)[lane];
+    const float2 m = *reinterpret_cast<const float2*>(slots + q * 96 + 64);
+    __syncwarp(0xfu << (threadIdx.x & 28));
+    issue(q, i + S * G);
+    acc += (float)(r.x ^ r.y ^ r.z ^ r.w) * m.x + m.y;
+  }
+  if (acc == 12345.f) out[0] = acc;
+}
+
 int main() {
   const int64_t n = 13238272;
   const uint64_t rows = 125000000;  // 12 GB of 96-B rows (Feed-1's q8 store)
@@ -134,6 +197,32 @@ int main() {
     timeit(nm, [&] { k_tma<S><<<148 * per * CTAS, 256, smem>>>(tab, ids, n, out); });                \
   }
   T(2, 1) T(4, 1) T(8, 1) T(4, 8) T(8, 8) T(16, 1)
+#define L(S)                                                                                         \
+  {                                                                                                  \
+    const int smem = 64 * S * 96;                                                                    \
+    cudaFuncSetAttribute(k_ldgsts<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);            \
+    int per = 0; cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_ldgsts<S>, 256, smem);        \
+    char nm[64]; snprintf(nm, 64, "ldgsts S=%d (%d CTA/SM)", S, per);                                \
+    timeit(nm, [&] { k_ldgsts<S><<<148 * per, 256, smem>>>(tab, ids, n, out); });                    \
+  }
+  L(4) L(8) L(12) L(16)
+  // rows/s by row size and pitch (the same 12 GB region, ids < rows): 16, 32, 64 B at pitch 96;
+  // 64 B at pitch 64 (one atom, aligned) and 128 B rows at pitch 128 (1 line) from rows*96/128 rows
+  timeit("16B of 96-B rows", [&] { k_ldgn<4, 96, 16><<<148 * 4 * 4, 256>>>(tab, ids, n, out); });
+  timeit("32B of 96-B rows", [&] { k_ldgn<4, 96, 32><<<148 * 4 * 4, 256>>>(tab, ids, n, out); });
+  timeit("64B of 96-B rows", [&] { k_ldgn<4, 96, 64><<<148 * 4 * 4, 256>>>(tab, ids, n, out); });
+  timeit("64B rows, pitch 64", [&] { k_ldgn<4, 64, 64><<<148 * 4 * 4, 256>>>(tab, ids, n, out); });
+  k_ids<<<1184, 256>>>(ids, n, rows * 96 / 128, 11);
+  timeit("64B of 128-B rows", [&] { k_ldgn<4, 128, 64><<<148 * 4 * 4, 256>>>(tab, ids, n, out); });
+  timeit("64B of 128-B rows UNR8", [&] { k_ldgn<8, 128, 64><<<148 * 4 * 4, 256>>>(tab, ids, n, out); });
+  // the whole a10 row (64 codes + 8-B meta at +64) at a 128-B pitch: one 128-B line per row
+  timeit("a10 row, pitch 128 UNR4", [&] { k_ldg<4, 128><<<148 * 4 * 4, 256>>>(tab, ids, n, out); });
+  timeit("a10 row, pitch 128 UNR8", [&] { k_ldg<8, 128><<<148 * 4 * 4, 256>>>(tab, ids, n, out); });
+  k_ids<<<1184, 256>>>(ids, n, rows, 7);
+  timeit("a10 row, pitch 96 UNR4", [&] { k_ldg<4, 96><<<148 * 4 * 4, 256>>>(tab, ids, n, out); });
+  // even rows only at pitch 96 (rows that never straddle a 128-B line)
+  k_ids<<<1184, 256>>>(ids, n, rows / 2, 7);
+  timeit("a10 row, pitch 192 UNR4", [&] { k_ldg<4, 192><<<148 * 4 * 4, 256>>>(tab, ids, n, out); });
   // 256-B rows from a 32 GB table (a2's fp32 rows)
   uint8_t* tab2 = nullptr;
   const uint64_t rows2 = 125000000;
