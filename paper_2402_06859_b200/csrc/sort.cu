@@ -17,8 +17,6 @@
 //   (coalesced).  Each pass moves 16 B per pair.  Tiles are claimed in launch order
 //   through an atomic counter, so a look-back only waits on tiles already resident.
 
-#include <stdlib.h>
-
 #include "common.cuh"
 #include "kernels.h"
 #include "lookback.cuh"
@@ -380,17 +378,16 @@ cudaError_t radix_sort_pairs(uint2* kv0, uint2* kv1, int64_t n, const uint32_t* 
 // segment that contains occurrence c << chunk_log2 (chunk_u0[c]).  n: capacity (grid
 // size); n_dev (optional): the device-resident count, read by the kernel.
 // ---------------------------------------------------------------------------
-template <int ITEMS, int THREADS = kSortThreads>
-__global__ void __launch_bounds__(THREADS)
+template <int ITEMS>
+__global__ void __launch_bounds__(kSortThreads)
 k_rle(const uint2* __restrict__ kv, int64_t n, const uint32_t* n_dev, uint32_t sentinel, uint32_t* unique,
       uint32_t* seg, uint32_t* U_out, uint32_t* chunk_u0, int chunk_log2, uint32_t* tile_counter,
       unsigned long long* status, const uint32_t* epoch_p, uint32_t epoch_off) {
   pdl_wait();
   if (n_dev) n = min(n, (int64_t)*n_dev);
   const uint32_t epoch = *epoch_p + epoch_off;
-  constexpr int NWT = THREADS / 32;
   __shared__ uint32_t s_tile;
-  __shared__ uint32_t s_warp[NWT];
+  __shared__ uint32_t s_warp[NW];
   __shared__ uint32_t s_excl;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
@@ -400,7 +397,7 @@ k_rle(const uint2* __restrict__ kv, int64_t n, const uint32_t* n_dev, uint32_t s
     if (tile == 0 && tid == 0) { *U_out = 0u; seg[0] = 0u; }
     return;
   }
-  constexpr int TILE = THREADS * ITEMS;
+  constexpr int TILE = kSortThreads * ITEMS;
   if (tile * TILE >= n) return;  // past the device count
   const int64_t base = tile * TILE + (int64_t)warp * (ITEMS * 32);
   unsigned ball[ITEMS];
@@ -426,7 +423,7 @@ k_rle(const uint2* __restrict__ kv, int64_t n, const uint32_t* n_dev, uint32_t s
   __syncthreads();
   if (tid == 0) {
     uint32_t t = 0;
-    for (int w = 0; w < NWT; ++w) {
+    for (int w = 0; w < NW; ++w) {
       const uint32_t c = s_warp[w];
       s_warp[w] = t;
       t += c;
@@ -462,19 +459,14 @@ cudaError_t launch_rle(const uint2* kv, int64_t n, const uint32_t* n_dev, uint32
                        unsigned long long* status, const uint32_t* epoch, uint32_t epoch_off,
                        cudaStream_t s) {
   if (n == 0) return cudaSuccess;
-  // 16 items per thread measured best (Feed-1: 8 -> 0.082 ms, 16 -> 0.059, 24 -> 0.065, 32 -> 0.073)
-  static const int variant = [] {  // TEMPORARY measurement knob (RLE CTA width)
-    const char* v = getenv("LIRANK_RLE_VARIANT");
-    return v ? atoi(v) : 0;
-  }();
-#define RL(IT, TH)                                                                                      \
-  {                                                                                                     \
-    const int64_t tiles = (n + TH * IT - 1) / (TH * IT);                                                \
-    launch_pdl(k_rle<IT, TH>, (unsigned)tiles, TH, 0, s, kv, n, n_dev, sentinel, unique, seg, U_out, chunk_u0, \
-               chunk_log2, counter, status, epoch, epoch_off);                                          \
-  }
-  if (variant == 1) RL(16, 512) else if (variant == 2) RL(8, 512) else if (variant == 3) RL(16, 1024) else RL(16, 256)
-#undef RL
+  // 16 items per thread measured best (Feed-1: 8 -> 0.082 ms, 16 -> 0.059, 24 -> 0.065, 32 -> 0.073);
+  // CTA width, round 2 (16 items): 256 threads 0.059 ms, 512 0.063, 1024 0.066, 128 0.068;
+  // 8 x 512 0.068, 8 x 256 0.083, 32 x 128 0.091 -- fewer look-backs do not pay for the
+  // longer barrier wait behind thread 0's walk
+  constexpr int IT = 16;
+  const int64_t tiles = (n + kSortThreads * IT - 1) / (kSortThreads * IT);
+  launch_pdl(k_rle<IT>, (unsigned)tiles, kSortThreads, 0, s, kv, n, n_dev, sentinel, unique, seg, U_out, chunk_u0,
+             chunk_log2, counter, status, epoch, epoch_off);
   return cudaGetLastError();
 }
 
