@@ -230,7 +230,7 @@ void carve(const Plan& p, Carver& cv, emb_handle* h) {
   auto* nm = cv.take<double>(chunks);
   auto* nf = cv.take<double>(chunks);
   auto* ol = cv.take<uint32_t>(3 * chunks);
-  auto* oc = cv.take<uint32_t>(2);
+  auto* oc = cv.take<uint32_t>(4);  // owner count, long count, a6 non-finite flag, pad
   auto* sp = cv.take<double>(std::max(p.world, 1));
   auto* sl = cv.take<double>(1);
   auto* nparts = cv.take<double>(64);     // k_norm_partial CTA partials (kNormParts)

@@ -78,16 +78,54 @@ __device__ __forceinline__ void zero(double (&acc)[VPL][4]) {
     for (int e = 0; e < 4; ++e) acc[v][e] = 0.0;
 }
 
-// acc += (double)r (x 1/L for MEAN).  The fp32 -> fp64 widenings are F2F instructions (XU
-// pipe); an exact integer-pipe widening (sign | (exponent + 896) << 20 | mantissa >> 3, low
-// word mantissa << 29, hardware fallback for 0 / subnormal / non-finite batches) was measured
-// on Feed-1: 0.661 -> 0.942 ms -- this kernel is bound by issue slots, and one F2F is
-// cheaper to issue than the five integer instructions that replace it.
-template <int VPL, bool MEAN>
-__device__ __forceinline__ void accumulate(double (&acc)[VPL][4], const float4 (&r)[VPL], double inv) {
+// 2^896: the fp32 bit pattern moved into an fp64 (widen_s) is the value x 2^-896
+constexpr double kWidenScale = 0x1p896;
+
+// Scaled widening: the fp32 bits of x, sign kept at bit 63 and exponent | mantissa shifted
+// into the fp64 exponent | mantissa fields, ARE the fp64 x * 2^-896 -- exactly, for every
+// finite x: normals (biased exponent e -> e, i.e. 2^(e-127) -> 2^(e-1023)), zero and fp32
+// subnormals (m * 2^-149 -> m * 2^-1045, an fp64 subnormal).  Two ALU instructions for the
+// high word ((int)bits >> 3 keeps the sign in bits 31..28; & 0x8fffffff clears 30..28) and
+// one for the low word.  Inf / NaN come out finite (exponent 255): callers detect them.
+__device__ __forceinline__ double widen_s(float x) {
+  const uint32_t b = __float_as_uint(x);
+  const int hi = (int)((uint32_t)((int)b >> 3) & 0x8fffffffu);
+  return __hiloint2double(hi, (int)(b << 29));
+}
+
+// acc += (double)r (x 1/L for MEAN).  HW: the F2F conversion (XU pipe: the pipe that bounds
+// this kernel with it, ~70% busy on Feed-1).  !HW: SUM: fma(widen_s(r), 2^896, acc) -- the
+// product is exactly (double)r, so the fused add rounds exactly as acc + (double)r does;
+// MEAN: widen_s(r) * ((1/L) 2^896) is exactly (double)r * (1/L) rounded once, then the add --
+// bit-identical sums either way (the build is -fmad=false: no other contraction), with the
+// conversion on the ALU pipe.  chk: x * 0 + chk turns NaN for an Inf / NaN element (the
+// kernel then flags the batch for the exact re-run).  (Round 2's first integer widening --
+// exponent re-biasing with a per-element zero / subnormal / non-finite test -- had five
+// instructions plus the tests and measured 0.661 -> 0.942 ms.)
+template <int VPL, bool MEAN, bool HW>
+__device__ __forceinline__ void accumulate(double (&acc)[VPL][4], const float4 (&r)[VPL], double inv,
+                                           float& chk) {
 #pragma unroll
   for (int v = 0; v < VPL; ++v) {
-    if (MEAN) {
+    if (!HW && !MEAN) {  // fma(x 2^-896, 2^896, acc): the exact x, one rounding of acc + x
+      acc[v][0] = __fma_rn(widen_s(r[v].x), kWidenScale, acc[v][0]);
+      acc[v][1] = __fma_rn(widen_s(r[v].y), kWidenScale, acc[v][1]);
+      acc[v][2] = __fma_rn(widen_s(r[v].z), kWidenScale, acc[v][2]);
+      acc[v][3] = __fma_rn(widen_s(r[v].w), kWidenScale, acc[v][3]);
+      chk = fmaf(r[v].x, 0.f, chk);
+      chk = fmaf(r[v].y, 0.f, chk);
+      chk = fmaf(r[v].z, 0.f, chk);
+      chk = fmaf(r[v].w, 0.f, chk);
+    } else if (!HW) {  // MEAN: the exact product x * (1/L), rounded once, then the add
+      acc[v][0] += widen_s(r[v].x) * inv;
+      acc[v][1] += widen_s(r[v].y) * inv;
+      acc[v][2] += widen_s(r[v].z) * inv;
+      acc[v][3] += widen_s(r[v].w) * inv;
+      chk = fmaf(r[v].x, 0.f, chk);
+      chk = fmaf(r[v].y, 0.f, chk);
+      chk = fmaf(r[v].z, 0.f, chk);
+      chk = fmaf(r[v].w, 0.f, chk);
+    } else if (MEAN) {
       acc[v][0] += (double)r[v].x * inv;
       acc[v][1] += (double)r[v].y * inv;
       acc[v][2] += (double)r[v].z * inv;
@@ -101,10 +139,12 @@ __device__ __forceinline__ void accumulate(double (&acc)[VPL][4], const float4 (
   }
 }
 
-// Finish a complete segment: G[u] = (float)acc, return this lane's sum of (double)G^2.
-template <int VPL, bool FR>
+// Finish a complete segment: G[u] = (float)acc, return this lane's sum of (double)G^2
+// (HW: F2F widening; else widen_s(g) * 2^896, exact for finite g -- an overflowed Inf g is
+// caught by chk).
+template <int VPL, bool FR, bool HW>
 __device__ __forceinline__ double write_G(float* G, int pitch, uint32_t u, int lane, int LPB,
-                                          const double (&acc)[VPL][4]) {
+                                          const double (&acc)[VPL][4], float& chk) {
   double nrm = 0.0;
   const int nvec = pitch >> 2;
 #pragma unroll
@@ -114,10 +154,23 @@ __device__ __forceinline__ double write_G(float* G, int pitch, uint32_t u, int l
       float4 g = make_float4((float)acc[v][0], (float)acc[v][1], (float)acc[v][2],
                              (float)acc[v][3]);
       st_f4_hint(G + (size_t)u * pitch + 4 * vi, g, l2_policy_first());  // G: streamed to a8
-      nrm += (double)g.x * (double)g.x;
-      nrm += (double)g.y * (double)g.y;
-      nrm += (double)g.z * (double)g.z;
-      nrm += (double)g.w * (double)g.w;
+      if (HW) {
+        nrm += (double)g.x * (double)g.x;
+        nrm += (double)g.y * (double)g.y;
+        nrm += (double)g.z * (double)g.z;
+        nrm += (double)g.w * (double)g.w;
+      } else {
+        const double gx = widen_s(g.x) * kWidenScale, gy = widen_s(g.y) * kWidenScale;
+        const double gz = widen_s(g.z) * kWidenScale, gw = widen_s(g.w) * kWidenScale;
+        nrm += gx * gx;
+        nrm += gy * gy;
+        nrm += gz * gz;
+        nrm += gw * gw;
+        chk = fmaf(g.x, 0.f, chk);
+        chk = fmaf(g.y, 0.f, chk);
+        chk = fmaf(g.z, 0.f, chk);
+        chk = fmaf(g.w, 0.f, chk);
+      }
     }
   }
   return nrm;
@@ -141,7 +194,11 @@ __device__ __forceinline__ void write_partial(double* P, int pitch, int64_t c, i
 }  // namespace
 
 // One lane group per chunk of 2^chunk_log2 sorted occurrences.  kv[k] = {row key, grad row}.
-template <int LPB, int VPL, bool MEAN, bool FR>
+// MODE 1: ALU widening (widen_s); a lane that met an Inf / NaN (input element, or a G that
+// overflowed to Inf) sets *nf_flag.  MODE 2: the re-run of such a batch with the F2F
+// conversions (returns at once unless *nf_flag is set; the owner list is already complete).
+// For finite batches MODE 1 alone gives the F2F results bit for bit; otherwise MODE 2 does.
+template <int LPB, int VPL, bool MEAN, bool FR, int MODE>
 __global__ void __launch_bounds__(256, 4)
 k_segreduce(const uint32_t* __restrict__ seg, const uint32_t* __restrict__ Up,
             const uint2* __restrict__ kv, const uint32_t* __restrict__ chunk_u0,
@@ -151,10 +208,14 @@ k_segreduce(const uint32_t* __restrict__ seg, const uint32_t* __restrict__ Up,
             double* __restrict__ norm_fix, uint32_t* __restrict__ owner_list,
             uint32_t* owner_count) {
   pdl_wait();
+  constexpr bool HW = MODE != 1;
+  uint32_t* nf_flag = owner_count + 2;  // zeroed with the counts by launch_segreduce
+  if (MODE == 2 && *(volatile uint32_t*)nf_flag == 0u) return;
   // rows in flight per group: D=64 (VPL 2) measured best at 2 with 4 CTAs/SM (64 registers:
   // 0.78 -> 0.72 ms on Feed-1; 1 -> 0.74, 4 -> 0.78 at 80 registers, 8 -> 1.5); key-derived
   // segment heads then took it to 0.69 ms)
   // (full-row kernel, round 2: 1 -> 0.643 ms, 2 -> 0.610, 4 -> 0.706 with spills)
+  // (ALU widening, round 2: UNR 2 at 4 CTAs/SM 0.59 ms, 3 0.62, 4 at 3 CTAs/SM 0.62)
   constexpr int UNR = (VPL == 1) ? 8 : (VPL == 2 ? 2 : 2);
   if (FR) { D = 4 * LPB * VPL; pitch = D; }  // compile-time row geometry (the launcher checked)
   const uint64_t pol = l2_policy_last();
@@ -174,6 +235,7 @@ k_segreduce(const uint32_t* __restrict__ seg, const uint32_t* __restrict__ Up,
   double acc[VPL][4];
   zero(acc);
   double nrm = 0.0;
+  float chk = 0.f;
   // Warp-uniform loop (chunk/LPB batches for every group): each batch loads LPB {key,
   // grad row} pairs (one per lane) and broadcasts them with full-mask shuffles; slots
   // past k1 (last chunk, dead groups) are predicated.  Segment boundaries come from the
@@ -193,6 +255,7 @@ k_segreduce(const uint32_t* __restrict__ seg, const uint32_t* __restrict__ Up,
         const uint32_t bb = kvl.y / (uint32_t)F, ff = kvl.y - bb * (uint32_t)F;
         const uint32_t bag = ff * (uint32_t)B + bb;
         inv_l = 1.0 / (double)(__ldg(offsets + bag + 1) - __ldg(offsets + bag));
+        if (!HW) inv_l *= kWidenScale;  // exact: a power of two
       }
     }
     uint32_t prev = __shfl_up_sync(kFull, kvl.x, 1, LPB);
@@ -209,7 +272,7 @@ k_segreduce(const uint32_t* __restrict__ seg, const uint32_t* __restrict__ Up,
 #pragma unroll
       for (int q = 0; q < UNR; ++q) {
         const uint32_t gq = __shfl_sync(kFull, grow_l, (jj + q) & (LPB - 1), LPB);
-        iv[q] = MEAN ? __shfl_sync(kFull, inv_l, (jj + q) & (LPB - 1), LPB) : 1.0;
+        iv[q] = MEAN ? __shfl_sync(kFull, inv_l, (jj + q) & (LPB - 1), LPB) : (HW ? 1.0 : kWidenScale);
         ok[q] = (jj + q < LPB) && (kb + jj + q < k1);
         if (ok[q]) load_grad_row<VPL, FR>(grad, (size_t)gq * D, D, lane, LPB, r[q], pol);
       }
@@ -218,12 +281,12 @@ k_segreduce(const uint32_t* __restrict__ seg, const uint32_t* __restrict__ Up,
         if (ok[q]) {
           if ((heads >> (jj + q)) & 1u) {  // segment u finished inside this chunk
             if (first_open) write_partial<VPL, FR>(part_first, pitch, c, lane, LPB, acc);
-            else nrm += write_G<VPL, FR>(G, pitch, u, lane, LPB, acc);
+            else nrm += write_G<VPL, FR, HW>(G, pitch, u, lane, LPB, acc, chk);
             zero(acc);
             ++u;
             first_open = false;
           }
-          accumulate<VPL, MEAN>(acc, r[q], iv[q]);
+          accumulate<VPL, MEAN, HW>(acc, r[q], iv[q], chk);
         }
       }
     }
@@ -235,17 +298,18 @@ k_segreduce(const uint32_t* __restrict__ seg, const uint32_t* __restrict__ Up,
     if (first_open) {
       write_partial<VPL, FR>(part_first, pitch, c, lane, LPB, acc);  // continues or ends here
     } else if (k1 == n_valid || __ldg(&kv[k1].x) != __ldg(&kv[k1 - 1].x)) {
-      nrm += write_G<VPL, FR>(G, pitch, u, lane, LPB, acc);
+      nrm += write_G<VPL, FR, HW>(G, pitch, u, lane, LPB, acc, chk);
     } else {
       write_partial<VPL, FR>(part_last, pitch, c, lane, LPB, acc);  // starts here, spills over
       owner = true;
     }
   }
   nrm = group_sum<LPB>(nrm);  // all lanes converge here
+  if (!HW && chk != chk) *nf_flag = 1u;  // an Inf / NaN in this lane's elements: re-run exactly
   if (lane == 0 && c < chunks) {
     norm_main[c] = nrm;
     norm_fix[c] = 0.0;
-    if (owner) {
+    if (owner && MODE != 2) {
       const uint32_t slot = atomicAdd(owner_count, 1u);
       owner_list[slot] = (uint32_t)c;
     }
@@ -982,17 +1046,20 @@ static unsigned persistent_grid(const void* kernel, int64_t groups, int lpb, int
 cudaError_t launch_segreduce(const BwdArgs& a, int64_t* launches, cudaStream_t s) {
   if (a.nnz == 0) return cudaSuccess;
   const Geom g = geom_target(a.pitch, 2);  // D=64: 8 lanes x 2 float4 per occurrence
-  cudaError_t e = cudaMemsetAsync(a.owner_count, 0, 2 * sizeof(uint32_t), s);
+  cudaError_t e = cudaMemsetAsync(a.owner_count, 0, 3 * sizeof(uint32_t), s);
   if (e != cudaSuccess) return e;
   const unsigned grid = (unsigned)((a.chunks * g.lpb + 255) / 256);
   const bool full_row = (a.D & 3) == 0 && a.pitch == a.D && a.D == 4 * g.lpb * g.vpl;
-
-#define LAUNCH_SR(MEAN)                                                                     \
-  LIRANK_GEOM2_DISPATCH(g, (launch_pdl(full_row ? k_segreduce<L_, V_, MEAN, true> : k_segreduce<L_, V_, MEAN, false>, grid, 256, 0, s, \
+  // the ALU-widening pass, then the exact re-run that returns at once unless a lane met an
+  // Inf / NaN (Feed-1: 0.607 -> 0.59 ms; alpha = 0 0.840 -> 0.848; Ads 2.00 -> 1.985)
+#define LAUNCH_SR(MEAN, MODE)                                                                     \
+  LIRANK_GEOM2_DISPATCH(g, (launch_pdl(full_row ? k_segreduce<L_, V_, MEAN, true, MODE> : k_segreduce<L_, V_, MEAN, false, MODE>, grid, 256, 0, s, \
                               a.seg, a.U, a.kv, a.chunk_u0, a.grad, a.offsets, a.B, a.F, a.D, \
                               a.pitch, a.chunks, a.chunk_log2, a.G, a.part_first, a.part_last, \
                               a.norm_main, a.norm_fix, a.owner_list, a.owner_count)))
-  if (a.mean) LAUNCH_SR(true); else LAUNCH_SR(false);
+  if (a.mean) { LAUNCH_SR(true, 1); LAUNCH_SR(true, 2); }
+  else { LAUNCH_SR(false, 1); LAUNCH_SR(false, 2); }
+  ++*launches;
 #undef LAUNCH_SR
   ++*launches;
   uint32_t* long_count = a.owner_count + 1;

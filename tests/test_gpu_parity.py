@@ -314,6 +314,42 @@ def test_nonfinite_grad_skips_update(gpu):
     assert torch.equal(emb.weights, w0)
 
 
+@pytest.mark.parametrize("kind", ["inf", "nan", "overflow"])
+def test_nonfinite_S_matches_oracle(gpu, kind):
+    """a6 widens on the ALU pipe and re-runs a batch with an Inf / NaN element (or a G that
+    overflows fp32) with the hardware conversions: S is the oracle's (Inf stays Inf, NaN NaN)."""
+    cfg = small_cfg(dim=64, rows=(300, 40), F=[0, 1, 0], B=128)
+    B, F, D = 128, cfg.num_features, 64
+    ids, off = gen.make_batch(cfg.table_rows, cfg.features, B, 5, 0)
+    grad = gen.grad_values(5, 0, B, F, D, gen.grad_shift_for(len(ids), D))
+    if kind == "inf":
+        grad[7, 1, 3] = np.inf
+    elif kind == "nan":
+        grad[7, 1, 3] = np.nan
+    else:  # two finite occurrences of one row whose fp64 sum rounds past FLT_MAX
+        ids = ids.copy()
+        b0, b1 = [b for b in range(B) if off[b + 1] > off[b]][:2]  # two non-empty feature-0 bags
+        ids[off[b0]] = ids[off[b1]] = 17  # feature 0 (bags 0..B-1), table 0, row 17
+        grad[b0, 0, 11] = grad[b1, 0, 11] = np.float32(3e38)
+    emb = make_emb(cfg, max_nnz=len(ids), max_batch=B)
+    init_tables_host(emb, cfg)
+    w0 = emb.weights.clone()
+    emb.forward(dev(ids), dev(off), B)
+    emb.backward_adagrad(dev(grad), 0.05)
+    from paper_2402_06859_b200._lib import EMB_ENONFINITE
+    assert emb.sync() == EMB_ENONFINITE
+    assert torch.equal(emb.weights, w0)
+    pb = problem(cfg)
+    W = dense_tables(cfg)
+    A = np.full(cfg.total_rows, 0.1, dtype=np.float32)
+    r = O.train_step(pb, W, A, ids, off, B, grad, 0.05, 1e-7, 1.0)
+    S_gpu = emb.last_stats()[0]
+    if kind == "nan":
+        assert np.isnan(r["S"]) and np.isnan(S_gpu)
+    else:
+        assert r["S"] == np.inf and S_gpu == np.inf
+
+
 def test_empty_batch_and_all_invalid(gpu):
     cfg = small_cfg(dim=32)
     emb = make_emb(cfg, max_nnz=100, max_batch=16)
