@@ -72,6 +72,40 @@ __device__ __forceinline__ uint32_t lb_wait(unsigned long long* status, int64_t 
   return excl;
 }
 
+// The same for one counter, walked by a whole warp (all 32 lanes call it): lane i reads the
+// status of tile p - i, so one L2 round trip covers 32 predecessors.  The walk adds the
+// aggregates up to the nearest inclusive prefix; if an unpublished tile comes first it adds
+// the published ones before it and re-polls from there.  Lane 0 publishes the inclusive
+// prefix; every lane returns the exclusive one.
+template <int kSleepMax = 64>
+__device__ __forceinline__ uint32_t lb_wait_warp(unsigned long long* status, int64_t tile, int stride,
+                                                 int slot, uint32_t epoch, uint32_t aggregate, int lane) {
+  if (tile == 0) return 0;
+  uint32_t excl = 0;
+  int64_t p = tile - 1;
+  int sleep_ns = 32;
+  while (true) {
+    const unsigned long long w = p - lane >= 0 ? ld_volatile(status + (p - lane) * stride + slot) : 0ull;
+    const bool valid = (uint32_t)(w >> 32) == epoch && (w & (3ull << 30)) != 0;
+    const unsigned bad = __ballot_sync(0xffffffffu, !valid);
+    const unsigned pref = __ballot_sync(0xffffffffu, valid && (w & kFlagPrefix));
+    const int first_bad = bad ? __ffs(bad) - 1 : 32;
+    const int first_pref = pref ? __ffs(pref) - 1 : 32;
+    if (first_pref < first_bad) {  // lanes 0..first_pref: aggregates, then the prefix
+      excl += __reduce_add_sync(0xffffffffu, lane <= first_pref ? (uint32_t)(w & kCountMask) : 0u);
+      break;
+    }
+    excl += __reduce_add_sync(0xffffffffu, lane < first_bad ? (uint32_t)(w & kCountMask) : 0u);
+    p -= first_bad;
+    if (first_bad == 0) {
+      __nanosleep(sleep_ns);
+      if (sleep_ns < kSleepMax) sleep_ns *= 2;
+    }
+  }
+  if (lane == 0) st_volatile(status + tile * stride + slot, lb_pack(epoch, kFlagPrefix, excl + aggregate));
+  return excl;
+}
+
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));

@@ -421,15 +421,19 @@ k_rle(const uint2* __restrict__ kv, int64_t n, const uint32_t* n_dev, uint32_t s
   }
   if (lane == 0) s_warp[warp] = wcount;
   __syncthreads();
-  if (tid == 0) {
-    uint32_t t = 0;
-    for (int w = 0; w < NW; ++w) {
-      const uint32_t c = s_warp[w];
-      s_warp[w] = t;
-      t += c;
+  if (warp == 0) {  // the warps' prefix and the tile total, then a warp-wide look-back
+    const uint32_t c = lane < NW ? s_warp[lane] : 0u;
+    uint32_t x = c;
+#pragma unroll
+    for (int o = 1; o < NW; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
     }
-    lb_publish(status, tile, kRadixBinsMax, 0, epoch, t);
-    s_excl = lb_wait(status, tile, kRadixBinsMax, 0, epoch, t);
+    const uint32_t t = __shfl_sync(0xffffffffu, x, NW - 1);
+    if (lane < NW) s_warp[lane] = x - c;
+    if (lane == 0) lb_publish(status, tile, kRadixBinsMax, 0, epoch, t);
+    const uint32_t ex = lb_wait_warp(status, tile, kRadixBinsMax, 0, epoch, t, lane);
+    if (lane == 0) s_excl = ex;
   }
   __syncthreads();
   uint32_t pos = s_excl + s_warp[warp];
