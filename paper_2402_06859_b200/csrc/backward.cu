@@ -81,6 +81,16 @@ __device__ __forceinline__ void zero(double (&acc)[VPL][4]) {
 // 2^896: the fp32 bit pattern moved into an fp64 (widen_s) is the value x 2^-896
 constexpr double kWidenScale = 0x1p896;
 
+// chk += {x, y} * 0 on both halves (FFMA2): a NaN half marks an Inf / NaN element
+__device__ __forceinline__ void chk2(unsigned long long& chk, float x, float y) {
+  const unsigned long long v = (unsigned long long)__float_as_uint(x) | ((unsigned long long)__float_as_uint(y) << 32);
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(chk) : "l"(v), "l"(0ull));
+}
+__device__ __forceinline__ bool chk_bad(unsigned long long chk) {
+  const float a = __uint_as_float((uint32_t)chk), b = __uint_as_float((uint32_t)(chk >> 32));
+  return a != a || b != b;
+}
+
 // Scaled widening: the fp32 bits of x, sign kept at bit 63 and exponent | mantissa shifted
 // into the fp64 exponent | mantissa fields, ARE the fp64 x * 2^-896 -- exactly, for every
 // finite x: normals (biased exponent e -> e, i.e. 2^(e-127) -> 2^(e-1023)), zero and fp32
@@ -98,13 +108,13 @@ __device__ __forceinline__ double widen_s(float x) {
 // product is exactly (double)r, so the fused add rounds exactly as acc + (double)r does;
 // MEAN: widen_s(r) * ((1/L) 2^896) is exactly (double)r * (1/L) rounded once, then the add --
 // bit-identical sums either way (the build is -fmad=false: no other contraction), with the
-// conversion on the ALU pipe.  chk: x * 0 + chk turns NaN for an Inf / NaN element (the
-// kernel then flags the batch for the exact re-run).  (Round 2's first integer widening --
+// conversion on the ALU pipe.  chk: x * 0 + chk (FFMA2, two elements per instruction) turns
+// NaN for an Inf / NaN element (the kernel then flags the batch for the exact re-run).  (Round 2's first integer widening --
 // exponent re-biasing with a per-element zero / subnormal / non-finite test -- had five
 // instructions plus the tests and measured 0.661 -> 0.942 ms.)
 template <int VPL, bool MEAN, bool HW>
 __device__ __forceinline__ void accumulate(double (&acc)[VPL][4], const float4 (&r)[VPL], double inv,
-                                           float& chk) {
+                                           unsigned long long& chk) {
 #pragma unroll
   for (int v = 0; v < VPL; ++v) {
     if (!HW && !MEAN) {  // fma(x 2^-896, 2^896, acc): the exact x, one rounding of acc + x
@@ -112,19 +122,15 @@ __device__ __forceinline__ void accumulate(double (&acc)[VPL][4], const float4 (
       acc[v][1] = __fma_rn(widen_s(r[v].y), kWidenScale, acc[v][1]);
       acc[v][2] = __fma_rn(widen_s(r[v].z), kWidenScale, acc[v][2]);
       acc[v][3] = __fma_rn(widen_s(r[v].w), kWidenScale, acc[v][3]);
-      chk = fmaf(r[v].x, 0.f, chk);
-      chk = fmaf(r[v].y, 0.f, chk);
-      chk = fmaf(r[v].z, 0.f, chk);
-      chk = fmaf(r[v].w, 0.f, chk);
+      chk2(chk, r[v].x, r[v].y);
+      chk2(chk, r[v].z, r[v].w);
     } else if (!HW) {  // MEAN: the exact product x * (1/L), rounded once, then the add
       acc[v][0] += widen_s(r[v].x) * inv;
       acc[v][1] += widen_s(r[v].y) * inv;
       acc[v][2] += widen_s(r[v].z) * inv;
       acc[v][3] += widen_s(r[v].w) * inv;
-      chk = fmaf(r[v].x, 0.f, chk);
-      chk = fmaf(r[v].y, 0.f, chk);
-      chk = fmaf(r[v].z, 0.f, chk);
-      chk = fmaf(r[v].w, 0.f, chk);
+      chk2(chk, r[v].x, r[v].y);
+      chk2(chk, r[v].z, r[v].w);
     } else if (MEAN) {
       acc[v][0] += (double)r[v].x * inv;
       acc[v][1] += (double)r[v].y * inv;
@@ -139,12 +145,12 @@ __device__ __forceinline__ void accumulate(double (&acc)[VPL][4], const float4 (
   }
 }
 
-// Finish a complete segment: G[u] = (float)acc, return this lane's sum of (double)G^2
-// (HW: F2F widening; else widen_s(g) * 2^896, exact for finite g -- an overflowed Inf g is
-// caught by chk).
-template <int VPL, bool FR, bool HW>
+// Finish a complete segment: G[u] = (float)acc, return this lane's sum of (double)G^2.  The
+// norm's re-widening stays on F2F (once per unique row: the XU pipe has room now, the issue
+// slots do not -- widen_s + the rescale there measured 0.567 -> 0.591 ms).
+template <int VPL, bool FR>
 __device__ __forceinline__ double write_G(float* G, int pitch, uint32_t u, int lane, int LPB,
-                                          const double (&acc)[VPL][4], float& chk) {
+                                          const double (&acc)[VPL][4]) {
   double nrm = 0.0;
   const int nvec = pitch >> 2;
 #pragma unroll
@@ -154,23 +160,10 @@ __device__ __forceinline__ double write_G(float* G, int pitch, uint32_t u, int l
       float4 g = make_float4((float)acc[v][0], (float)acc[v][1], (float)acc[v][2],
                              (float)acc[v][3]);
       st_f4_hint(G + (size_t)u * pitch + 4 * vi, g, l2_policy_first());  // G: streamed to a8
-      if (HW) {
-        nrm += (double)g.x * (double)g.x;
-        nrm += (double)g.y * (double)g.y;
-        nrm += (double)g.z * (double)g.z;
-        nrm += (double)g.w * (double)g.w;
-      } else {
-        const double gx = widen_s(g.x) * kWidenScale, gy = widen_s(g.y) * kWidenScale;
-        const double gz = widen_s(g.z) * kWidenScale, gw = widen_s(g.w) * kWidenScale;
-        nrm += gx * gx;
-        nrm += gy * gy;
-        nrm += gz * gz;
-        nrm += gw * gw;
-        chk = fmaf(g.x, 0.f, chk);
-        chk = fmaf(g.y, 0.f, chk);
-        chk = fmaf(g.z, 0.f, chk);
-        chk = fmaf(g.w, 0.f, chk);
-      }
+      nrm += (double)g.x * (double)g.x;
+      nrm += (double)g.y * (double)g.y;
+      nrm += (double)g.z * (double)g.z;
+      nrm += (double)g.w * (double)g.w;
     }
   }
   return nrm;
@@ -194,8 +187,8 @@ __device__ __forceinline__ void write_partial(double* P, int pitch, int64_t c, i
 }  // namespace
 
 // One lane group per chunk of 2^chunk_log2 sorted occurrences.  kv[k] = {row key, grad row}.
-// MODE 1: ALU widening (widen_s); a lane that met an Inf / NaN (input element, or a G that
-// overflowed to Inf) sets *nf_flag.  MODE 2: the re-run of such a batch with the F2F
+// MODE 1: ALU widening (widen_s); a lane that met an Inf / NaN input element sets *nf_flag
+// (a G that overflows to Inf needs nothing: its norm term is the F2F one, Inf).  MODE 2: the re-run of such a batch with the F2F
 // conversions (returns at once unless *nf_flag is set; the owner list is already complete).
 // For finite batches MODE 1 alone gives the F2F results bit for bit; otherwise MODE 2 does.
 template <int LPB, int VPL, bool MEAN, bool FR, int MODE>
@@ -235,7 +228,7 @@ k_segreduce(const uint32_t* __restrict__ seg, const uint32_t* __restrict__ Up,
   double acc[VPL][4];
   zero(acc);
   double nrm = 0.0;
-  float chk = 0.f;
+  unsigned long long chk = 0ull;  // two fp32 zeros
   // Warp-uniform loop (chunk/LPB batches for every group): each batch loads LPB {key,
   // grad row} pairs (one per lane) and broadcasts them with full-mask shuffles; slots
   // past k1 (last chunk, dead groups) are predicated.  Segment boundaries come from the
@@ -281,7 +274,7 @@ k_segreduce(const uint32_t* __restrict__ seg, const uint32_t* __restrict__ Up,
         if (ok[q]) {
           if ((heads >> (jj + q)) & 1u) {  // segment u finished inside this chunk
             if (first_open) write_partial<VPL, FR>(part_first, pitch, c, lane, LPB, acc);
-            else nrm += write_G<VPL, FR, HW>(G, pitch, u, lane, LPB, acc, chk);
+            else nrm += write_G<VPL, FR>(G, pitch, u, lane, LPB, acc);
             zero(acc);
             ++u;
             first_open = false;
@@ -298,14 +291,14 @@ k_segreduce(const uint32_t* __restrict__ seg, const uint32_t* __restrict__ Up,
     if (first_open) {
       write_partial<VPL, FR>(part_first, pitch, c, lane, LPB, acc);  // continues or ends here
     } else if (k1 == n_valid || __ldg(&kv[k1].x) != __ldg(&kv[k1 - 1].x)) {
-      nrm += write_G<VPL, FR, HW>(G, pitch, u, lane, LPB, acc, chk);
+      nrm += write_G<VPL, FR>(G, pitch, u, lane, LPB, acc);
     } else {
       write_partial<VPL, FR>(part_last, pitch, c, lane, LPB, acc);  // starts here, spills over
       owner = true;
     }
   }
   nrm = group_sum<LPB>(nrm);  // all lanes converge here
-  if (!HW && chk != chk) *nf_flag = 1u;  // an Inf / NaN in this lane's elements: re-run exactly
+  if (!HW && chk_bad(chk)) *nf_flag = 1u;  // an Inf / NaN in this lane's elements: re-run exactly
   if (lane == 0 && c < chunks) {
     norm_main[c] = nrm;
     norm_fix[c] = 0.0;
@@ -1051,7 +1044,8 @@ cudaError_t launch_segreduce(const BwdArgs& a, int64_t* launches, cudaStream_t s
   const unsigned grid = (unsigned)((a.chunks * g.lpb + 255) / 256);
   const bool full_row = (a.D & 3) == 0 && a.pitch == a.D && a.D == 4 * g.lpb * g.vpl;
   // the ALU-widening pass, then the exact re-run that returns at once unless a lane met an
-  // Inf / NaN (Feed-1: 0.607 -> 0.59 ms; alpha = 0 0.840 -> 0.848; Ads 2.00 -> 1.985)
+  // Inf / NaN (Feed-1: 0.607 -> 0.567 ms; alpha = 0 0.840 -> 0.842; Ads 2.00 -> 1.967; the
+  // re-run folded into the same kernel behind a warp vote measured 0.592 ms)
 #define LAUNCH_SR(MEAN, MODE)                                                                     \
   LIRANK_GEOM2_DISPATCH(g, (launch_pdl(full_row ? k_segreduce<L_, V_, MEAN, true, MODE> : k_segreduce<L_, V_, MEAN, false, MODE>, grid, 256, 0, s, \
                               a.seg, a.U, a.kv, a.chunk_u0, a.grad, a.offsets, a.B, a.F, a.D, \
