@@ -59,15 +59,20 @@ k_scan_excl(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, int64_t
   }
   if (lane == 31) s_warp[warp] = x;
   __syncthreads();
-  if (tid == 0) {
-    uint32_t t = 0;
-    for (int w = 0; w < kScanThreads / 32; ++w) {
-      const uint32_t c = s_warp[w];
-      s_warp[w] = t;
-      t += c;
+  if (warp == 0) {  // the warps' prefix, then a warp-wide look-back (as the RLE's)
+    constexpr int NWS = kScanThreads / 32;
+    const uint32_t c = lane < NWS ? s_warp[lane] : 0u;
+    uint32_t xs = c;
+#pragma unroll
+    for (int o = 1; o < NWS; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, xs, o);
+      if (lane >= o) xs += y;
     }
-    lb_publish(status, tile, 1, 0, epoch, t);
-    s_excl = lb_wait(status, tile, 1, 0, epoch, t);
+    const uint32_t t = __shfl_sync(0xffffffffu, xs, NWS - 1);
+    if (lane < NWS) s_warp[lane] = xs - c;
+    if (lane == 0) lb_publish(status, tile, 1, 0, epoch, t);
+    const uint32_t ex = lb_wait_warp(status, tile, 1, 0, epoch, t, lane);
+    if (lane == 0) s_excl = ex;
   }
   __syncthreads();
   uint32_t run = s_excl + s_warp[warp] + x - sum;
