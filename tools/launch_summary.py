@@ -2,7 +2,8 @@
 """Summarise an ncu launch list (--metrics gpu__time_duration.sum --csv --log-file X.csv):
 per kernel name the launch count and mean time, then each step kernel's share of one step.
 
-Usage: python tools/launch_summary.py launches.csv --steps K [--header "..."] [--out file.txt]
+Usage: python tools/launch_summary.py launches.csv [--steps K] [--header "..."] [--out file.txt]
+(K defaults to the launch count of k_norm_finalize, which runs once per step.)
 The per-step share divides every lirank:: kernel's total by the launches it had per step
 (launches // (warmup + steps) is not known here, so kernels launched exactly once per step
 are the ones the bench's timed + warm-up steps run; setup kernels are listed but excluded)."""
@@ -17,7 +18,7 @@ SETUP = ("k_fill", "k_fill_table", "k_fill_grad", "k_flush", "k_quantize", "k_ga
 
 def main():
     path = sys.argv[1]
-    nsteps = int(sys.argv[sys.argv.index("--steps") + 1]) if "--steps" in sys.argv else 1
+    nsteps = int(sys.argv[sys.argv.index("--steps") + 1]) if "--steps" in sys.argv else 0
     header = sys.argv[sys.argv.index("--header") + 1] if "--header" in sys.argv else ""
     text = open(path).read()
     start = text.find('"ID"')
@@ -41,6 +42,8 @@ def main():
     out.append(f"{'kernel':44s} {'launches':>8s} {'mean_us':>10s}")
     for k, (n, t) in agg.items():
         out.append(f"{k:44s} {n:8d} {t / n:10.1f}")
+    if nsteps <= 0:  # a7's finalize runs exactly once per step
+        nsteps = max([n for k, (n, _) in agg.items() if k.split("<")[0].endswith("k_norm_finalize")] or [1])
     step = OrderedDict()
     for k, (n, t) in agg.items():
         base = k.split("<")[0]
