@@ -69,6 +69,7 @@ def parse():
     ap.add_argument("--cpu-samples", type=int, default=8192,
                     help="samples of the single-core oracle timing (the all-core one runs the full batch)")
     ap.add_argument("--no-spot", action="store_true", help="skip the in-run oracle spot check")
+    ap.add_argument("--no-a5", action="store_true", help="skip the a5-alone timing (launch lists: every step the same)")
     ap.add_argument("--transport", default="nccl", choices=["nccl", "host"],
                     help="N>1: NCCL (one GPU per rank), or the library's host transport over a gloo group "
                          "(EMB_F_HOSTCOMM: a functional check of the N-rank bench with every rank on the "
@@ -1131,7 +1132,7 @@ def run_ours(args, cfg, rank, world, local_rank, B=None, sharding="row", scaling
     # (in the step above the dedup shares the GPU with the a10 lookup on the main stream, so
     # its phase time there is not its own)
     a5_alone = None
-    if world == 1:
+    if world == 1 and not args.no_a5:
         emb.profile(True)
         emb.profile_read(reset=True)
         for k in range(5):

@@ -12,7 +12,7 @@ timeout 600 python bench.py --alpha 0 $Q > gpurun_out/${T}_cfg_alpha0.log 2>&1; 
 timeout 600 python bench.py --config ads $Q > gpurun_out/${T}_cfg_ads.log 2>&1; echo ads=$?
 timeout 600 python bench.py --config jobs $Q > gpurun_out/${T}_cfg_jobs.log 2>&1; echo jobs=$?
 timeout 900 python bench.py --config feedq8 --steps 20 > gpurun_out/${T}_cfg_feedq8.log 2>&1; echo q8=$?
-L="--steps 2 --warmup 3 --no-cpu --no-qr --no-model --no-fim --no-lib --no-graph --no-spot --no-e2e"
+L="--steps 2 --warmup 3 --no-cpu --no-qr --no-model --no-fim --no-lib --no-graph --no-spot --no-e2e --no-a5"
 timeout 600 python bench.py $L > gpurun_out/ncu_l_plain.log 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 1500 --csv --log-file gpurun_out/${T}_launches.csv python bench.py $L > gpurun_out/ncu_l.log 2>&1; echo l=$?
 timeout 600 python tools/profile_step.py --warmup 0 --steps 1 --quantize > gpurun_out/ps.log 2>&1 && \
