@@ -192,18 +192,15 @@ __device__ __forceinline__ void write_partial(double* P, int pitch, int64_t c, i
 // conversions (returns at once unless *nf_flag is set; the owner list is already complete).
 // For finite batches MODE 1 alone gives the F2F results bit for bit; otherwise MODE 2 does.
 template <int LPB, int VPL, bool MEAN, bool FR, int MODE>
-__global__ void __launch_bounds__(256, 4)
-k_segreduce(const uint32_t* __restrict__ seg, const uint32_t* __restrict__ Up,
-            const uint2* __restrict__ kv, const uint32_t* __restrict__ chunk_u0,
-            const float* __restrict__ grad, const int* __restrict__ offsets, int B, int F, int D,
-            int pitch, int64_t chunks, int chunk_log2, float* __restrict__ G, double* __restrict__ part_first,
-            double* __restrict__ part_last, double* __restrict__ norm_main,
-            double* __restrict__ norm_fix, uint32_t* __restrict__ owner_list,
-            uint32_t* owner_count) {
-  pdl_wait();
+__device__ __forceinline__ void segreduce_block(
+    int64_t vb, const uint32_t* __restrict__ seg, const uint32_t* __restrict__ Up,
+    const uint2* __restrict__ kv, const uint32_t* __restrict__ chunk_u0, const float* __restrict__ grad,
+    const int* __restrict__ offsets, int B, int F, int D, int pitch, int64_t chunks, int chunk_log2,
+    float* __restrict__ G, double* __restrict__ part_first, double* __restrict__ part_last,
+    double* __restrict__ norm_main, double* __restrict__ norm_fix, uint32_t* __restrict__ owner_list,
+    uint32_t* owner_count) {
   constexpr bool HW = MODE != 1;
   uint32_t* nf_flag = owner_count + 2;  // zeroed with the counts by launch_segreduce
-  if (MODE == 2 && *(volatile uint32_t*)nf_flag == 0u) return;
   // rows in flight per group: D=64 (VPL 2) measured best at 2 with 4 CTAs/SM (64 registers:
   // 0.78 -> 0.72 ms on Feed-1; 1 -> 0.74, 4 -> 0.78 at 80 registers, 8 -> 1.5); key-derived
   // segment heads then took it to 0.69 ms)
@@ -213,7 +210,7 @@ k_segreduce(const uint32_t* __restrict__ seg, const uint32_t* __restrict__ Up,
   if (FR) { D = 4 * LPB * VPL; pitch = D; }  // compile-time row geometry (the launcher checked)
   const uint64_t pol = l2_policy_last();
   const int lane = threadIdx.x & (LPB - 1);
-  const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LPB;
+  const int64_t c = (vb * blockDim.x + threadIdx.x) / LPB;
   const uint32_t U = *Up;
   const int64_t n_valid = seg[U];
   const int chunk = 1 << chunk_log2;
@@ -307,6 +304,31 @@ k_segreduce(const uint32_t* __restrict__ seg, const uint32_t* __restrict__ Up,
       owner_list[slot] = (uint32_t)c;
     }
   }
+}
+
+template <int LPB, int VPL, bool MEAN, bool FR, int MODE>
+__global__ void __launch_bounds__(256, 4)
+k_segreduce(const uint32_t* __restrict__ seg, const uint32_t* __restrict__ Up,
+            const uint2* __restrict__ kv, const uint32_t* __restrict__ chunk_u0,
+            const float* __restrict__ grad, const int* __restrict__ offsets, int B, int F, int D,
+            int pitch, int64_t chunks, int chunk_log2, float* __restrict__ G, double* __restrict__ part_first,
+            double* __restrict__ part_last, double* __restrict__ norm_main,
+            double* __restrict__ norm_fix, uint32_t* __restrict__ owner_list,
+            uint32_t* owner_count, int64_t nblocks) {
+  pdl_wait();
+  if (MODE != 2) {  // one block of chunks per CTA
+    segreduce_block<LPB, VPL, MEAN, FR, MODE>(blockIdx.x, seg, Up, kv, chunk_u0, grad, offsets, B, F, D, pitch,
+                                              chunks, chunk_log2, G, part_first, part_last, norm_main,
+                                              norm_fix, owner_list, owner_count);
+    return;
+  }
+  // the re-run: a small grid that returns at once unless the first pass flagged an Inf / NaN,
+  // then strides over the same blocks (block-uniform loop: the shuffles stay full-warp)
+  if (*(volatile uint32_t*)(owner_count + 2) == 0u) return;
+  for (int64_t vb = blockIdx.x; vb < nblocks; vb += gridDim.x)
+    segreduce_block<LPB, VPL, MEAN, FR, MODE>(vb, seg, Up, kv, chunk_u0, grad, offsets, B, F, D, pitch,
+                                              chunks, chunk_log2, G, part_first, part_last, norm_main,
+                                              norm_fix, owner_list, owner_count);
 }
 
 // Fix-up of segments spanning chunks.  Entry e = chunk c_s where segment u starts and
@@ -1047,10 +1069,11 @@ cudaError_t launch_segreduce(const BwdArgs& a, int64_t* launches, cudaStream_t s
   // Inf / NaN (Feed-1: 0.607 -> 0.567 ms; alpha = 0 0.840 -> 0.842; Ads 2.00 -> 1.967; the
   // re-run folded into the same kernel behind a warp vote measured 0.592 ms)
 #define LAUNCH_SR(MEAN, MODE)                                                                     \
-  LIRANK_GEOM2_DISPATCH(g, (launch_pdl(full_row ? k_segreduce<L_, V_, MEAN, true, MODE> : k_segreduce<L_, V_, MEAN, false, MODE>, grid, 256, 0, s, \
+  LIRANK_GEOM2_DISPATCH(g, (launch_pdl(full_row ? k_segreduce<L_, V_, MEAN, true, MODE> : k_segreduce<L_, V_, MEAN, false, MODE>, \
+                              MODE == 2 ? (grid < 148u ? grid : 148u) : grid, 256, 0, s, \
                               a.seg, a.U, a.kv, a.chunk_u0, a.grad, a.offsets, a.B, a.F, a.D, \
                               a.pitch, a.chunks, a.chunk_log2, a.G, a.part_first, a.part_last, \
-                              a.norm_main, a.norm_fix, a.owner_list, a.owner_count)))
+                              a.norm_main, a.norm_fix, a.owner_list, a.owner_count, (int64_t)grid)))
   if (a.mean) { LAUNCH_SR(true, 1); LAUNCH_SR(true, 2); }
   else { LAUNCH_SR(false, 1); LAUNCH_SR(false, 2); }
   ++*launches;

@@ -10,4 +10,4 @@ grep '^{' gpurun_out/probe.log | python -c "
 import sys, json
 for l in sys.stdin:
     d=json.loads(l); print(d['config'], d['alpha'], 'sort', round(d['sort_ms'],4), 'rle', round(d['rle_ms'],4), 'a6', round(d['segreduce_ms'],4), 'a8', round(d['update_ms'],4))"
-timeout 1200 python -m pytest -q -x -m gpu tests/test_gpu_parity.py tests/test_feed_model_gpu.py tests/test_sharded_syncfree_gpu.py > gpurun_out/probe_t.log 2>&1; echo t=$?; tail -2 gpurun_out/probe_t.log
+timeout 1500 python -m pytest -q -x -m gpu tests/test_gpu_parity.py tests/test_feed_model_gpu.py tests/test_sharded_syncfree_gpu.py tests/test_sharded_gpu.py tests/test_graph_gpu.py > gpurun_out/probe_t.log 2>&1; echo t=$?; tail -2 gpurun_out/probe_t.log
