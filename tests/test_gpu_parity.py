@@ -314,6 +314,41 @@ def test_nonfinite_grad_skips_update(gpu):
     assert torch.equal(emb.weights, w0)
 
 
+@pytest.mark.parametrize("pooling", ["sum", "mean"])
+def test_a6_widening_exact_over_the_fp32_range(gpu, pooling):
+    """a6 widens fp32 -> fp64 on the ALU pipe (the fp32 bits placed in the fp64 fields, then a
+    fused multiply-add by 2^896; MEAN: by (1/L) 2^896).  It must give the hardware conversion's
+    sums bit for bit on every exponent class: gradient elements with random sign and mantissa and
+    exponents from fp32 subnormals to 2^60, plus zeros and -0.  Element-wise AdaGrad with the
+    clip inactive (c = 1) updates each element from its own G element only, so W and A must equal
+    the oracle's exactly; every row occurs twice, so G is a real two-term sum."""
+    rows, B, F, D = 600, 200, 2, 64
+    cfg = small_cfg(dim=D, rows=(rows,), F=[0, 0], B=B)
+    rng = np.random.default_rng(11)
+    ids = rng.permutation(np.repeat(np.arange(rows), 2)).astype(np.int32)
+    off = np.arange(0, 3 * F * B + 1, 3, dtype=np.int32)  # 400 bags of 3
+    sign = rng.integers(0, 2, (B, F, D), dtype=np.uint32) << np.uint32(31)
+    expo = rng.integers(0, 188, (B, F, D), dtype=np.uint32) << np.uint32(23)  # 2^-149 .. 2^60
+    mant = rng.integers(0, 1 << 23, (B, F, D), dtype=np.uint32)
+    grad = (sign | expo | mant).view(np.float32)
+    m = rng.random(grad.shape)
+    grad[m < 0.03] = 0.0
+    grad[(m >= 0.03) & (m < 0.05)] = -0.0
+    emb = make_emb(cfg, max_nnz=len(ids), max_batch=B, adagrad="elementwise", pooling=pooling, max_norm=1e30)
+    init_tables_host(emb, cfg)
+    emb.forward(dev(ids), dev(off), B)
+    emb.backward_adagrad(dev(grad), 0.05)
+    assert emb.sync() == 0
+    pb = problem(cfg, 1 if pooling == "mean" else 0)
+    W = dense_tables(cfg)
+    A = np.full((rows, D), 0.1, dtype=np.float32)
+    r = O.train_step(pb, W, A, ids, off, B, grad, 0.05, 1e-7, 1e30, mode="elementwise")
+    assert float(r["c"]) == 1.0 and float(emb.last_stats()[1]) == 1.0
+    w, a = emb.read_rows(0, np.arange(rows))
+    assert (a == A).all()
+    assert (w == W).all()
+
+
 @pytest.mark.parametrize("kind", ["inf", "nan", "overflow"])
 def test_nonfinite_S_matches_oracle(gpu, kind):
     """a6 widens on the ALU pipe and re-runs a batch with an Inf / NaN element (or a G that
