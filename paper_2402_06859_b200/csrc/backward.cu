@@ -205,7 +205,9 @@ __device__ __forceinline__ void segreduce_block(
   // 0.78 -> 0.72 ms on Feed-1; 1 -> 0.74, 4 -> 0.78 at 80 registers, 8 -> 1.5); key-derived
   // segment heads then took it to 0.69 ms)
   // (full-row kernel, round 2: 1 -> 0.643 ms, 2 -> 0.610, 4 -> 0.706 with spills)
-  // (ALU widening, round 2: UNR 2 at 4 CTAs/SM 0.59 ms, 3 0.62, 4 at 3 CTAs/SM 0.62)
+  // (ALU widening, round 2: UNR 2 at 4 CTAs/SM 0.59 ms, 3 0.62, 4 at 3 CTAs/SM 0.62; groups of
+  // 16 lanes x one float4 -- half the groups per warp, so less write-out divergence: UNR 4 or
+  // 6 0.584 ms, 8 0.688 (spills) vs 8 x 2 0.565)
   constexpr int UNR = (VPL == 1) ? 8 : (VPL == 2 ? 2 : 2);
   if (FR) { D = 4 * LPB * VPL; pitch = D; }  // compile-time row geometry (the launcher checked)
   const uint64_t pol = l2_policy_last();
