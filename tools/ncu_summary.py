@@ -95,7 +95,16 @@ def main():
                     have.append(k)
             if have:
                 j[ph] = {"dram_bytes_per_launch": tot, "kernels": have}
-        json.dump(j, open(sys.argv[sys.argv.index("--json") + 1], "w"), indent=1)
+        # phases this capture does not cover (e.g. the full-table a9) keep their earlier entries
+        path = sys.argv[sys.argv.index("--json") + 1]
+        try:
+            old = json.load(open(path))
+            for ph, v in old.items():
+                if ph not in j and not ph.startswith("_"):
+                    j[ph] = dict(v, note=v.get("note", "from an earlier capture: " + old.get("_source", "")[-60:]))
+        except (OSError, ValueError):
+            pass
+        json.dump(j, open(path, "w"), indent=1)
 
 
 if __name__ == "__main__":

@@ -16,4 +16,10 @@ L="--steps 2 --warmup 3 --no-cpu --no-qr --no-model --no-fim --no-lib --no-graph
 timeout 600 python bench.py $L > gpurun_out/ncu_l_plain.log 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 1500 --csv --log-file gpurun_out/${T}_launches.csv python bench.py $L > gpurun_out/ncu_l.log 2>&1; echo l=$?
 timeout 600 python tools/profile_step.py --warmup 0 --steps 1 --quantize > gpurun_out/ps.log 2>&1 && \
-timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"^k_(pool|radix|onesweep|rle|segreduce|fixup|norm|adagrad|quantize|len)" -o gpurun_out/${T}_step_full python tools/profile_step.py --warmup 0 --steps 1 --quantize > gpurun_out/ncu_full.log 2>&1; echo full=$?
+timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"^k_(pool|radix|onesweep|rle|segreduce|fixup|norm|adagrad|len)" -o gpurun_out/${T}_step_full python tools/profile_step.py --warmup 0 --steps 1 --quantize > gpurun_out/ncu_full.log 2>&1; echo full=$?
+# summaries on the box (the copy-back is capped at 64 MiB: a report that would break it stays in /tmp)
+python tools/ncu_summary.py gpurun_out/${T}_step_full.ncu-rep > gpurun_out/${T}_ncu_summary.txt 2>&1
+for k in k_segreduce k_onesweep k_adagrad_tma k_pool_fwd_f32 k_pool_fwd_q8 k_rle; do
+  python tools/ncu_opmix.py gpurun_out/${T}_step_full.ncu-rep "$k" --top 14; echo
+done > gpurun_out/${T}_opmix.txt 2>&1
+if [ $(stat -c %s gpurun_out/${T}_step_full.ncu-rep) -gt 50000000 ]; then mv gpurun_out/${T}_step_full.ncu-rep /tmp/; echo "rep kept on the box only (size)"; fi
