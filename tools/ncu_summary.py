@@ -37,9 +37,26 @@ def load(rep):
     return rows[0], rows[1], rows[2:]
 
 
+def from_text(path):
+    """(header, units, rows) rebuilt from a saved summary text (its first three metric columns)."""
+    h, units, rows = ["Kernel Name"], [""], []
+    for n, m, _ in METRICS:
+        h.append(m)
+        units.append("")
+    for line in open(path):
+        parts = line.split()
+        if not parts or parts[0] in ("kernel", "#", "stalls(cycles/issue):") or line.startswith(" "):
+            continue
+        # the name may contain spaces ("k_pool_fwd_f32<8, 2, 0, 1, 0, 1>"): numbers are the tail
+        nums = parts[-len(METRICS):]
+        name = line[:38].strip()
+        rows.append([name] + nums)
+    return h, units, rows
+
+
 def main():
     rep = sys.argv[1]
-    h, units, rows = load(rep)
+    h, units, rows = from_text(rep) if rep.endswith(".txt") else load(rep)
     ki = h.index("Kernel Name")
     lines, traffic = [], {}
     hdr = f"{'kernel':38s} " + " ".join(f"{n:>10s}" for n, _, _ in METRICS)
@@ -67,9 +84,8 @@ def main():
                     pass
         if st:
             lines.append(f"{'':38s}   stalls(cycles/issue): " + " ".join(st))
-        key = name.split("<")[0]
         rd = vals[1] + vals[2]
-        traffic.setdefault(key, []).append(rd * 1e9)
+        traffic.setdefault(name, []).append(rd * 1e9)  # per instantiation (template arguments kept)
     text = "\n".join(lines)
     print(text)
     if "--out" in sys.argv:
@@ -86,13 +102,15 @@ def main():
         per_step = {"k_onesweep": 3}  # digit passes per step (27-bit Feed-1 keys)
         j = {"_source": f"ncu --set full --clock-control none, one step of tools/profile_step.py ({rep}); "
                         "dram__bytes_read.sum + dram__bytes_write.sum per phase instance"}
+        # each distinct instantiation of a phase's kernels runs once per step (the sort's digit
+        # passes: per_step times), e.g. a6's ALU-widening pass and its Inf/NaN re-run are summed
         for ph, ks in phases.items():
             tot, have = 0.0, []
-            for k in ks:
-                if k in traffic:
-                    v = traffic[k]
-                    tot += sum(v) / len(v) * per_step.get(k, 1)
-                    have.append(k)
+            for name, v in traffic.items():
+                base = name.split("<")[0]
+                if base in ks:
+                    tot += sum(v) / len(v) * per_step.get(base, 1)
+                    have.append(name)
             if have:
                 j[ph] = {"dram_bytes_per_launch": tot, "kernels": have}
         # phases this capture does not cover (e.g. the full-table a9) keep their earlier entries
