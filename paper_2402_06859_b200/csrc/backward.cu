@@ -109,9 +109,9 @@ __device__ __forceinline__ double widen_s(float x) {
 // MEAN: widen_s(r) * ((1/L) 2^896) is exactly (double)r * (1/L) rounded once, then the add --
 // bit-identical sums either way (the build is -fmad=false: no other contraction), with the
 // conversion on the ALU pipe.  chk: x * 0 + chk (FFMA2, two elements per instruction) turns
-// NaN for an Inf / NaN element (the kernel then flags the batch for the exact re-run).  (Round 2's first integer widening --
-// exponent re-biasing with a per-element zero / subnormal / non-finite test -- had five
-// instructions plus the tests and measured 0.661 -> 0.942 ms.)
+// NaN for an Inf / NaN element (the kernel then flags the batch for the exact re-run).
+// (Round 2's first integer widening -- exponent re-biasing with a per-element zero /
+// subnormal / non-finite test -- had five instructions plus the tests: 0.661 -> 0.942 ms.)
 template <int VPL, bool MEAN, bool HW>
 __device__ __forceinline__ void accumulate(double (&acc)[VPL][4], const float4 (&r)[VPL], double inv,
                                            unsigned long long& chk) {
