@@ -349,8 +349,9 @@ def test_a6_widening_exact_over_the_fp32_range(gpu, pooling):
     assert (w == W).all()
 
 
-@pytest.mark.parametrize("kind", ["inf", "nan", "overflow"])
-def test_nonfinite_S_matches_oracle(gpu, kind):
+@pytest.mark.parametrize("kind,pooling", [("inf", "sum"), ("nan", "sum"), ("overflow", "sum"),
+                                          ("inf", "mean"), ("nan", "mean")])
+def test_nonfinite_S_matches_oracle(gpu, kind, pooling):
     """a6 widens on the ALU pipe and re-runs a batch with an Inf / NaN element (or a G that
     overflows fp32) with the hardware conversions: S is the oracle's (Inf stays Inf, NaN NaN)."""
     cfg = small_cfg(dim=64, rows=(300, 40), F=[0, 1, 0], B=128)
@@ -366,7 +367,7 @@ def test_nonfinite_S_matches_oracle(gpu, kind):
         b0, b1 = [b for b in range(B) if off[b + 1] > off[b]][:2]  # two non-empty feature-0 bags
         ids[off[b0]] = ids[off[b1]] = 17  # feature 0 (bags 0..B-1), table 0, row 17
         grad[b0, 0, 11] = grad[b1, 0, 11] = np.float32(3e38)
-    emb = make_emb(cfg, max_nnz=len(ids), max_batch=B)
+    emb = make_emb(cfg, max_nnz=len(ids), max_batch=B, pooling=pooling)
     init_tables_host(emb, cfg)
     w0 = emb.weights.clone()
     emb.forward(dev(ids), dev(off), B)
@@ -374,7 +375,7 @@ def test_nonfinite_S_matches_oracle(gpu, kind):
     from paper_2402_06859_b200._lib import EMB_ENONFINITE
     assert emb.sync() == EMB_ENONFINITE
     assert torch.equal(emb.weights, w0)
-    pb = problem(cfg)
+    pb = problem(cfg, 1 if pooling == "mean" else 0)
     W = dense_tables(cfg)
     A = np.full(cfg.total_rows, 0.1, dtype=np.float32)
     r = O.train_step(pb, W, A, ids, off, B, grad, 0.05, 1e-7, 1.0)

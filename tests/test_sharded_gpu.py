@@ -124,6 +124,58 @@ def test_sharded_train_step_matches_unsharded_oracle(gpu, W, sharding, p2p):
     hub.close()
 
 
+@pytest.mark.parametrize("kind", ["inf", "nan"])
+@pytest.mark.parametrize("sharding", ["table", "row"])
+def test_sharded_nonfinite_grad_skips_update_on_every_rank(gpu, sharding, kind):
+    """An Inf / NaN in one rank's upstream gradient: the owner's a6 (ALU widening) flags it and
+    re-runs with the hardware conversions, so its norm partial is the oracle's class; the
+    rank-ordered global S is then Inf (NaN) on EVERY rank, every rank reports EMB_ENONFINITE
+    and no rank updates a row (P:17's clip has no finite factor)."""
+    from paper_2402_06859_b200 import LoopbackHub, ShardedEmbedding
+    from paper_2402_06859_b200._lib import EMB_ENONFINITE
+    W = 2
+    rows = [1500, 600, 90]
+    ft = [0, 1, 2, 0]
+    cfg = configs.Config("shnf", rows, 32, [(t, ("range", 1, 10)) for t in ft], 40, seed=12)
+    B, F, D = cfg.batch, cfg.num_features, cfg.dim
+    per_rank = [gen.make_batch(rows, cfg.features, B, cfg.seed + r, 0) for r in range(W)]
+    ids_g, off_g = global_batch(per_rank, F, B)
+    grad_g = gen.grad_values(cfg.seed, 0, W * B, F, D, gen.grad_shift_for(len(ids_g), D))
+    grad_g[B + 3, 1, 7] = np.inf if kind == "inf" else np.nan  # rank 1's sample 3
+    hub = LoopbackHub(W)
+    embs = []
+    for r in range(W):
+        e = ShardedEmbedding(rows, D, ft, max_nnz=max(len(i) for i, _ in per_rank), max_batch=B,
+                             max_recv_nnz=W * max(len(i) for i, _ in per_rank),
+                             device=torch.device("cuda:0"), stream=torch.cuda.Stream(), rank=r, world_size=W,
+                             sharding=sharding, loopback_hub=hub)
+        init_tables_host(e, cfg)
+        embs.append(e)
+    torch.cuda.synchronize()
+    w0 = [e.weights.clone() for e in embs]
+
+    def step(r):
+        e = embs[r]
+        ids, off = per_rank[r]
+        with torch.cuda.stream(e.stream):
+            e.forward(torch.from_numpy(ids).cuda(), torch.from_numpy(off).cuda(), B)
+            e.backward_adagrad(torch.from_numpy(grad_g[r * B:(r + 1) * B].copy()).cuda(), 0.05)
+        return e.sync()
+
+    assert all(st == EMB_ENONFINITE for st in run_ranks(W, step))
+    for e, w in zip(embs, w0):
+        assert torch.equal(e.weights, w)
+    pb = O.Problem(rows, D, ft)
+    r_or = O.train_step(pb, dense_tables(cfg), np.full(cfg.total_rows, 0.1, dtype=np.float32), ids_g, off_g,
+                        W * B, grad_g, 0.05, 1e-7, 1.0)
+    for e in embs:
+        S = e.last_stats()[0]
+        assert (np.isnan(S) and np.isnan(r_or["S"])) if kind == "nan" else (S == np.inf and r_or["S"] == np.inf)
+    for e in embs:
+        e.close()
+    hub.close()
+
+
 @pytest.mark.parametrize("p2p", [False, True])
 @pytest.mark.parametrize("sharding", ["table", "row"])
 def test_sharded_q8_forward(gpu, sharding, p2p):
