@@ -545,7 +545,8 @@ cudaError_t launch_pool_fwd_q8(const FwdQ8Args& a, cudaStream_t s) {
   const float magic = a.minmax ? 8388608.0f : 8388736.0f;
   // (no short-bag split here: a k_pool_short_f32-style q8 kernel measured slower -- Ads a10
   // 3.24 -> 3.79 ms -- the q8 groups already hold 8 bags per warp; nor a compile-time full-row
-  // variant as a2 has: Feed-1 a10 0.274 -> 0.375 ms, serving 0.74 -> 0.92 ms)
+  // variant as a2 has: Feed-1 a10 0.274 -> 0.375 ms, serving 0.74 -> 0.92 ms; the meta pair
+  // loaded with the rows' L2 evict_last hint too: unchanged, 0.2744 vs 0.2753 ms)
 #define LAUNCH_Q8(MEAN, PEER)                                                              \
   LIRANK_GEOM_DISPATCH(g, (launch_pdl(k_pool_fwd_q8<L_, V_, MEAN, PEER>, grid, 256, 0, s,   \
                               a.codes, a.qpitch, a.meta_off, a.ids, a.offsets, a.B, a.F, Fb, \
