@@ -13,7 +13,7 @@
 //
 // Design (B200):
 // * segment-reduce is load-balanced by OCCURRENCES, not by segments: the sorted
-//   occurrence list is cut into chunks of 2^chunk_log2 (32..256, chosen per call so a small
+//   occurrence list is cut into chunks of 2^chunk_log2 (32..128, chosen per call so a small
 //   batch still spreads over every SM: chunk_log2_for), one lane group (LPB lanes, one
 //   float4 of the 256-B grad row per lane at D=64) per chunk, fp64 accumulators in
 //   registers, UNR grad-row gathers in flight.  Segments wholly inside a chunk are

@@ -112,10 +112,13 @@ cudaError_t launch_rle(const uint2* kv, int64_t n, const uint32_t* n_dev, uint32
 cudaError_t launch_epoch_advance(uint32_t* epoch, uint32_t n, cudaStream_t s);
 
 // ---- a6-a8 ----------------------------------------------------------------------------
-// Occurrences per lane group in the segment-reduce: 2^chunk_log2, 32..256.  256 once the
-// batch fills every SM (Feed-1: 13.2M ids -> 51.7k chunks); smaller for small batches so
-// that ~kSegGroups groups still run (a 5k-id batch: 163 chunks of 32, not 21 of 256).
-constexpr int kChunkLog2Min = 5, kChunkLog2Max = 8;
+// Occurrences per lane group in the segment-reduce: 2^chunk_log2, 32..128.  128 once the
+// batch fills every SM twice over (Feed-1: 13.2M ids -> 103k chunks); smaller for small
+// batches so that ~kSegGroups groups still run (a 5k-id batch: 163 chunks of 32, not 41 of 128).
+// (max 128, round 2: Feed-1 a6 0.563 -> 0.548 ms, Ads 1.955 -> 1.838, alpha = 0 0.838 -> 0.827 vs
+// 256 -- twice the lane-group "waves", so the last one idles less; 64 0.578 / 1.866 / 0.814; a
+// persistent grid claiming blocks dynamically instead: 0.583)
+constexpr int kChunkLog2Min = 5, kChunkLog2Max = 7;
 constexpr int64_t kSegGroups = 148 * 4 * 32;  // resident lane groups (148 SMs x 4 CTAs x 32)
 inline int chunk_log2_for(int64_t n) {
   int l = kChunkLog2Min;
