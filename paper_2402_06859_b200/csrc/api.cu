@@ -229,7 +229,7 @@ void carve(const Plan& p, Carver& cv, emb_handle* h) {
   auto* pl = cv.take<double>(chunks * pitch);
   auto* nm = cv.take<double>(chunks);
   auto* nf = cv.take<double>(chunks);
-  auto* ol = cv.take<uint32_t>(3 * chunks);
+  auto* ol = cv.take<uint32_t>(3 * chunks + 2 * (chunks / 512 + 1));  // owners, long and big spans
   auto* oc = cv.take<uint32_t>(4);  // owner count, long count, a6 non-finite flag, pad
   auto* sp = cv.take<double>(std::max(p.world, 1));
   auto* sl = cv.take<double>(1);

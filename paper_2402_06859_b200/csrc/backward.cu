@@ -39,6 +39,8 @@ namespace lirank {
 namespace {
 
 constexpr int kFixLong = 8;           // spans of more chunks than this use a whole CTA
+constexpr int kFixBig = 512;          // ... and of more than this, kLongPieces CTAs first
+constexpr int kLongPieces = 8;
 constexpr int kFixThreads = 1024;
 constexpr unsigned kFull = 0xffffffffu;
 
@@ -343,7 +345,8 @@ k_fixup_short(const uint32_t* __restrict__ seg, const uint32_t* __restrict__ Up,
               const uint32_t* __restrict__ chunk_u0, int pitch, const double* __restrict__ part_first,
               const double* __restrict__ part_last, const uint32_t* __restrict__ owner_list,
               const uint32_t* __restrict__ owner_count, float* __restrict__ G,
-              double* __restrict__ norm_fix, uint32_t* long_list, uint32_t* long_count, int chunk_log2) {
+              double* __restrict__ norm_fix, uint32_t* long_list, uint32_t* long_count, uint32_t* big_list,
+              uint32_t* big_count, int chunk_log2) {
   pdl_wait();
   constexpr int GPW = 32 / LPB;  // groups per warp
   const int lane = threadIdx.x & (LPB - 1);
@@ -369,6 +372,11 @@ k_fixup_short(const uint32_t* __restrict__ seg, const uint32_t* __restrict__ Up,
           const uint32_t slot = atomicAdd(long_count, 1u);
           long_list[2 * slot] = cs;
           long_list[2 * slot + 1] = u;
+          if (ce - cs > kFixBig) {  // the Zipf head: its partials are summed in pieces first
+            const uint32_t b = atomicAdd(big_count, 1u);
+            big_list[2 * b] = cs;
+            big_list[2 * b + 1] = u;
+          }
         }
         live = false;
       }
@@ -405,8 +413,59 @@ k_fixup_short(const uint32_t* __restrict__ seg, const uint32_t* __restrict__ Up,
   }
 }
 
+// First chunk of piece k of a span of nch chunks after chunk cs (k = kLongPieces: the end).
+__device__ __forceinline__ int64_t piece_lo(int64_t cs, int64_t nch, int k) {
+  return cs + 1 + (nch * k) / kLongPieces;
+}
+
+// The spans of more than kFixBig chunks (the hottest rows: up to ~10^4 chunks; one CTA alone
+// walked the hottest one's partial rows in ~32 dependent rounds, 39 us of the step) are cut
+// into kLongPieces contiguous pieces, one CTA each (a piece: its own sub-ranges combined in
+// order, as below).  A piece's sum is stored over the partial of the piece's first chunk --
+// read only by this piece, and already consumed -- so no other scratch; k_fixup_long then
+// adds part_last + the pieces in piece order.
+__global__ void __launch_bounds__(kFixThreads, 1)
+k_fixup_long_pieces(const uint32_t* __restrict__ seg, int pitch, double* __restrict__ part_first,
+                    const uint32_t* __restrict__ big_list, const uint32_t* __restrict__ big_count,
+                    int chunk_log2) {
+  pdl_wait();
+  extern __shared__ double sm[];  // [nsplit * pitch]
+  const uint32_t n_big = *big_count;
+  const int nsplit = max(1, kFixThreads / pitch);
+  for (int64_t w = blockIdx.x; w < (int64_t)n_big * kLongPieces; w += gridDim.x) {
+    const int64_t e = w / kLongPieces;
+    const int k = (int)(w % kLongPieces);
+    const uint32_t cs = big_list[2 * e], u = big_list[2 * e + 1];
+    const int64_t nch = (((int64_t)__ldg(seg + u + 1) - 1) >> chunk_log2) - cs;
+    const int64_t lo = piece_lo(cs, nch, k), m = piece_lo(cs, nch, k + 1) - lo;  // m > 64
+    for (int t = threadIdx.x; t < nsplit * pitch; t += blockDim.x) {
+      const int el = t % pitch, sp = t / pitch;
+      const int64_t a = lo + (m * sp) / nsplit, b = lo + (m * (sp + 1)) / nsplit;
+      double acc = 0.0;
+      int64_t cc = a;
+      for (; cc + 16 <= b; cc += 16) {  // 16 loads in flight, adds in chunk order
+        double x[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) x[q] = part_first[(size_t)(cc + q) * pitch + el];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) acc += x[q];
+      }
+      for (; cc < b; ++cc) acc += part_first[(size_t)cc * pitch + el];
+      sm[sp * pitch + el] = acc;
+    }
+    __syncthreads();  // every read of the piece's partials is done
+    for (int el = threadIdx.x; el < pitch; el += blockDim.x) {
+      double acc = 0.0;
+      for (int sp = 0; sp < nsplit; ++sp) acc += sm[sp * pitch + el];
+      part_first[(size_t)lo * pitch + el] = acc;
+    }
+    __syncthreads();  // sm is reused by the next piece
+  }
+}
+
 // Long spans: one CTA per entry.  Thread t owns element (t % pitch) of the row for chunk
-// sub-range (t / pitch); sub-ranges are contiguous and combined in order.
+// sub-range (t / pitch); sub-ranges are contiguous and combined in order.  A span of more
+// than kFixBig chunks instead adds its kLongPieces piece sums (k_fixup_long_pieces) in order.
 __global__ void __launch_bounds__(kFixThreads, 1)  // 1: 64 registers, all 16 loads in flight
 k_fixup_long(const uint32_t* __restrict__ seg, int pitch, const double* __restrict__ part_first,
              const double* __restrict__ part_last, const uint32_t* __restrict__ long_list,
@@ -421,7 +480,8 @@ k_fixup_long(const uint32_t* __restrict__ seg, int pitch, const double* __restri
     const int64_t s_end = __ldg(seg + u + 1);
     const int64_t ce = (s_end - 1) >> chunk_log2;
     const int64_t nch = ce - cs;  // chunks cs+1 .. ce
-    for (int t = threadIdx.x; t < nsplit * pitch; t += blockDim.x) {
+    const bool big = nch > kFixBig;  // (uniform over the CTA)
+    for (int t = threadIdx.x; !big && t < nsplit * pitch; t += blockDim.x) {
       const int el = t % pitch, sp = t / pitch;
       const int64_t a = cs + 1 + (nch * sp) / nsplit;
       const int64_t b = cs + 1 + (nch * (sp + 1)) / nsplit;
@@ -441,7 +501,11 @@ k_fixup_long(const uint32_t* __restrict__ seg, int pitch, const double* __restri
     double nrm_part = 0.0;
     for (int el = threadIdx.x; el < pitch; el += blockDim.x) {
       double s = part_last[(size_t)cs * pitch + el];
-      for (int sp = 0; sp < nsplit; ++sp) s += sm[sp * pitch + el];
+      if (big) {
+        for (int k = 0; k < kLongPieces; ++k) s += part_first[(size_t)piece_lo(cs, nch, k) * pitch + el];
+      } else {
+        for (int sp = 0; sp < nsplit; ++sp) s += sm[sp * pitch + el];
+      }
       const float g = (float)s;
       G[(size_t)u * pitch + el] = g;
       nrm_part += (double)g * (double)g;
@@ -1063,7 +1127,7 @@ static unsigned persistent_grid(const void* kernel, int64_t groups, int lpb, int
 cudaError_t launch_segreduce(const BwdArgs& a, int64_t* launches, cudaStream_t s) {
   if (a.nnz == 0) return cudaSuccess;
   const Geom g = geom_target(a.pitch, 2);  // D=64: 8 lanes x 2 float4 per occurrence
-  cudaError_t e = cudaMemsetAsync(a.owner_count, 0, 3 * sizeof(uint32_t), s);
+  cudaError_t e = cudaMemsetAsync(a.owner_count, 0, 4 * sizeof(uint32_t), s);
   if (e != cudaSuccess) return e;
   const unsigned grid = (unsigned)((a.chunks * g.lpb + 255) / 256);
   const bool full_row = (a.D & 3) == 0 && a.pitch == a.D && a.D == 4 * g.lpb * g.vpl;
@@ -1083,16 +1147,20 @@ cudaError_t launch_segreduce(const BwdArgs& a, int64_t* launches, cudaStream_t s
   ++*launches;
   uint32_t* long_count = a.owner_count + 1;
   uint32_t* long_list = a.owner_list + a.chunks;  // [2 * chunks] after the owner list
+  uint32_t* big_count = a.owner_count + 3;
+  uint32_t* big_list = a.owner_list + 3 * a.chunks;  // [2 * chunks / kFixBig] after the long list
   LIRANK_GEOM2_DISPATCH(g, (launch_pdl(k_fixup_short<L_, V_>, persistent_grid((const void*)k_fixup_short<L_, V_>, a.chunks, L_), 256, 0, s,
                               a.seg, a.U, a.chunk_u0, a.pitch, a.part_first, a.part_last,
-                              a.owner_list, a.owner_count, a.G, a.norm_fix, long_list, long_count,
+                              a.owner_list, a.owner_count, a.G, a.norm_fix, long_list, long_count, big_list, big_count,
                               a.chunk_log2)));
   ++*launches;
   const int nsplit = a.pitch < kFixThreads ? kFixThreads / a.pitch : 1;
   const size_t smem = sizeof(double) * (size_t)(nsplit * a.pitch > kFixThreads ? nsplit * a.pitch : kFixThreads);
+  launch_pdl(k_fixup_long_pieces, 148, kFixThreads, smem, s, a.seg, a.pitch, a.part_first, big_list, big_count,
+             a.chunk_log2);
   launch_pdl(k_fixup_long, 148, kFixThreads, smem, s, a.seg, a.pitch, a.part_first, a.part_last,
              long_list, long_count, a.G, a.norm_fix, a.chunk_log2);
-  ++*launches;
+  *launches += 2;
   return cudaGetLastError();
 }
 

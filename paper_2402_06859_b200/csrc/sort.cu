@@ -9,7 +9,7 @@
 // * One upfront histogram kernel computes the digit histograms of every pass in a single
 //   read of the keys (per-warp private shared-memory histograms).
 // * ONE kernel per digit pass (8- or 9-bit digits: 27-bit Feed-1 keys take 3 passes):
-//   an 8192-pair tile (512 threads x 16) is loaded with coalesced 8-B loads and ranked in registers (warp
+//   a 7680-pair tile (512 threads x 15) is loaded with coalesced 8-B loads and ranked in registers (warp
 //   multisplit by ballots, stable in index order), the tile's digit counts are published
 //   and the global offsets found by a decoupled look-back over earlier tiles (64-bit
 //   epoch-tagged status words, so no per-step memset), overlapped with staging the tile
@@ -358,8 +358,11 @@ cudaError_t radix_sort_pairs(uint2* kv0, uint2* kv1, int64_t n, const uint32_t* 
     // the same, 16 (more registers) 0.51; exponential back-off of the poll changes nothing
     // (CTA width, round 2: 512 threads x 16 items at 2 CTAs/SM 0.297 ms vs 256 x 22 at 3 CTAs
     // 0.31 in the same run, 384 x 22 x 2 0.315, 384 x 20 x 2 0.310, 512 x 12 x 2 0.303; Ads
-    // 0.964 vs 0.998 ms: the wider tile halves the look-back walks per item at equal occupancy)
-#define OS(BITS) e = onesweep_pass<BITS, 16, 0, 2, 8, 64, 512>(a, b, n, n_dev, shift, hp, ctr, ws.status, epoch, (uint32_t)p, s);
+    // 0.964 vs 0.998 ms: the wider tile halves the look-back walks per item at equal occupancy;
+    // then 512 x 15: 0.297 -> 0.286 ms, Ads 0.965 -> 0.931, alpha 0 0.306 -> 0.297 (14: 0.287 /
+    // 0.953, 17: 0.295 / 0.963) -- fewer spilled registers at the 64-register cap, and Feed-1's
+    // 1724 tiles fill the 296 resident CTAs in 5.8 rounds instead of 5.5)
+#define OS(BITS) e = onesweep_pass<BITS, 15, 0, 2, 8, 64, 512>(a, b, n, n_dev, shift, hp, ctr, ws.status, epoch, (uint32_t)p, s);
     if (dbits == 9) { OS(9) } else { OS(8) }
 #undef OS
     if (e != cudaSuccess) return e;

@@ -96,7 +96,7 @@ def main():
         # launches per step); the capture is one step of tools/profile_step.py
         phases = {"fwd": ["k_pool_fwd_f32", "k_pool_short_f32", "k_len_hist", "k_len_scatter"],
                   "fwd_q8": ["k_pool_fwd_q8"], "sort": ["k_radix_hist", "k_hist_excl", "k_onesweep"],
-                  "rle": ["k_rle"], "segreduce": ["k_segreduce", "k_fixup_short", "k_fixup_long"],
+                  "rle": ["k_rle"], "segreduce": ["k_segreduce", "k_fixup_short", "k_fixup_long", "k_fixup_long_pieces", "k_fixup_long_combine"],
                   "norm": ["k_norm_partial", "k_norm_finalize"], "update": ["k_adagrad_tma", "k_adagrad"],
                   "quantize": ["k_quantize"]}
         per_step = {"k_onesweep": 3}  # digit passes per step (27-bit Feed-1 keys)
