@@ -423,7 +423,8 @@ __device__ __forceinline__ int64_t piece_lo(int64_t cs, int64_t nch, int k) {
 // into kLongPieces contiguous pieces, one CTA each (a piece: its own sub-ranges combined in
 // order, as below).  A piece's sum is stored over the partial of the piece's first chunk --
 // read only by this piece, and already consumed -- so no other scratch; k_fixup_long then
-// adds part_last + the pieces in piece order.
+// adds part_last + the pieces in piece order.  (Cutting EVERY long span into 8 pieces
+// measured a6 0.549 -> 0.617 ms: a 1024-thread CTA and two barriers per piece of a few chunks.)
 __global__ void __launch_bounds__(kFixThreads, 1)
 k_fixup_long_pieces(const uint32_t* __restrict__ seg, int pitch, double* __restrict__ part_first,
                     const uint32_t* __restrict__ big_list, const uint32_t* __restrict__ big_count,
