@@ -467,10 +467,12 @@ cudaError_t launch_rle(const uint2* kv, int64_t n, const uint32_t* n_dev, uint32
                        cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   // 16 items per thread measured best (Feed-1: 8 -> 0.082 ms, 16 -> 0.059, 24 -> 0.065, 32 -> 0.073);
+  // with the warp-wide look-back, round 2: 12 0.0569, 14 0.0548, 16 0.0548, 18 0.0544, 20 0.066 ms
+  // (Ads: 0.171 / 0.158 / 0.155 / 0.148 / 0.207) -> 18;
   // CTA width, round 2 (16 items): 256 threads 0.059 ms, 512 0.063, 1024 0.066, 128 0.068;
   // 8 x 512 0.068, 8 x 256 0.083, 32 x 128 0.091 -- fewer look-backs do not pay for the
   // longer barrier wait behind thread 0's walk
-  constexpr int IT = 16;
+  constexpr int IT = 18;
   const int64_t tiles = (n + kSortThreads * IT - 1) / (kSortThreads * IT);
   launch_pdl(k_rle<IT>, (unsigned)tiles, kSortThreads, 0, s, kv, n, n_dev, sentinel, unique, seg, U_out, chunk_u0,
              chunk_log2, counter, status, epoch, epoch_off);
