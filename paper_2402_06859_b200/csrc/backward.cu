@@ -907,7 +907,9 @@ constexpr int kTmaStages = 2;
 // other as they finish.  Measured update time (Feed-1, alpha 1.05): 1 wave (persistent, ~16
 // rows per group) 0.595 ms, 4 waves 0.564, 12 waves 0.532, 24 waves 0.522, 48 waves 0.517,
 // 96 waves 0.572; the register-staged kernel 0.549.  alpha 0: 1.90 vs 2.04 ms; Ads 1.09 vs
-// 1.17 ms; alpha 1.2 (U = 0.92M, one row per group) 0.206 vs 0.196 ms.
+// 1.17 ms; alpha 1.2 (U = 0.92M, one row per group) 0.206 vs 0.196 ms.  (Round 2: the top ncu
+// stall, lane 0's accumulator address waiting on its key, moved by loading keys two rows
+// ahead -- a8 unchanged, 0.4046 vs 0.4034 ms without requant: the rows' DRAM time dominates.)
 constexpr int kTmaWaves = 48;
 constexpr int kTmaRowBytes = 256;  // D = 64 fp32
 constexpr size_t kTmaSmem = 8 /*warps*/ * kTmaStages * 8 /*groups*/ * 2 * kTmaRowBytes +
