@@ -88,7 +88,8 @@ k_pool_fwd_f32(const float* __restrict__ W, int pitch, const int* __restrict__ i
               const uint32_t* __restrict__ order, bool skip_short, const PeerOut pm) {
   pdl_wait();
   // rows in flight per group (D = 64 full rows, measured: 2 -> 0.343 ms at 48 registers, 3 ->
-  // 0.361 at 56, 4 -> 0.359 at 64; at alpha 0 all within 1%)
+  // 0.361 at 56, 4 -> 0.359 at 64; at alpha 0 all within 1%).  Occupancy (round 2): 6 CTAs/SM
+  // at 40 registers spills, 0.351 ms; 7 at 32, 0.503 -- the default 5 at 48 stays.
   constexpr int UNR = (VPL == 1) ? 4 : (VPL == 2 ? 2 : 1);
   constexpr unsigned kFull = 0xffffffffu;
   if (FR) { D = 4 * LPB * VPL; pitch = D; }
