@@ -466,7 +466,7 @@ def graph_section(emb, cfg, dev_in, B, out, out_q8, stream, flush, steps=10, sma
 
     def step(ids_d, off_d, g, b, o, oq):
         emb.forward(ids_d, off_d, b, out=o)
-        emb.forward_q8(ids_d, off_d, b, out=oq)
+        emb.forward_q8(None, None, b, out=oq, nnz=ids_d.numel())  # the same batch, as the main step
         emb.backward_adagrad(g, LR)
 
     def timed(fn, n, flush_between):
@@ -994,7 +994,8 @@ def run_ours(args, cfg, rank, world, local_rank, B=None, sharding="row", scaling
     def step(k):
         ids_d, off_d, gd = dev_in[k % len(dev_in)]
         emb.forward(ids_d, off_d, B, out=out)          # a2 (+ a5 dedup starts on the side stream)
-        emb.forward_q8(ids_d, off_d, B, out=out_q8)    # a10 from the q8 store (overlaps a5)
+        # a10 from the q8 store on the same batch (overlaps a5; sharded: its ids exchange is reused)
+        emb.forward_q8(None, None, B, out=out_q8, nnz=ids_d.numel())
         emb.backward_adagrad(gd, LR)                   # a6-a8 (+ a9 requant of touched rows)
 
     def barrier():

@@ -835,7 +835,7 @@ emb_status emb_forward_q8(emb_t h, const int32_t* ids, const int32_t* offsets, i
   if (s != EMB_OK) return s;
   if (reuse) st.slot = h->last_slot;  // the forward's staged batch: its slot is read again
   if (p.exch) {
-    s = exchange_forward(h, st, batch, nnz, /*q8=*/true);
+    s = exchange_forward(h, st, batch, nnz, /*q8=*/true, reuse);
     if (s != EMB_OK) return s;
   } else {
     FwdQ8Args a;

@@ -209,6 +209,7 @@ struct emb_handle {
   int64_t fwd_nnz_hint = 0;  // the ids of the forward call (picks the segment-reduce chunk)
   int chunk_log2 = lirank::kChunkLog2Max;  // segment-reduce chunk of the last dedup
   int fwd_B = 0;        // local batch of the last forward
+  bool x_ids_fwd = false;  // the receive buffers hold the last (fp32) forward's exchanged ids
   const uint2* sorted_kv = nullptr;
   // look-back epochs in device memory: [0] the dedup (side stream), [1] the exchange scans
   // (main stream); read by the kernels, advanced by k_epoch_advance (graph-replayable)
@@ -248,7 +249,9 @@ emb_status launch_dedup(emb_t h);
 emb_status join_dedup(emb_t h);
 
 // sharded forward / backward (exchange.cu)
-emb_status exchange_forward(emb_t h, const Staged& st, int32_t batch, int64_t nnz, bool q8);
+// reuse: a q8 forward of the last forward's batch (emb_forward_q8(NULL, NULL)): the ids
+// exchange of that forward is still in the receive buffers, so a1 is skipped
+emb_status exchange_forward(emb_t h, const Staged& st, int32_t batch, int64_t nnz, bool q8, bool reuse = false);
 emb_status exchange_backward(emb_t h, const float* grad_dev);
 void carve_exchange(const Plan& p, Carver& cv, ExchangeWs* x);
 emb_status exchange_init(emb_t h);  // upload the exchange maps (emb_create)

@@ -207,6 +207,21 @@ def test_sharded_q8_forward(gpu, sharding, p2p):
         return out.cpu().numpy()
 
     outs = run_ranks(W, fwd)
+
+    def fwd_reuse(r):  # forward, then the q8 lookup of ITS batch (ids exchange skipped), twice
+        e = embs[r]
+        ids, off = per_rank[r]
+        with torch.cuda.stream(e.stream):
+            e.forward(torch.from_numpy(ids).cuda(), torch.from_numpy(off).cuda(), B)
+            q1 = torch.empty((B, F, D), device="cuda")
+            q2 = torch.empty((B, F, D), device="cuda")
+            e.forward_q8(None, None, B, out=q1, nnz=len(ids))
+            e.forward_q8(None, None, B, out=q2, nnz=len(ids))
+        assert e.sync() == 0
+        return q1.cpu().numpy(), q2.cpu().numpy()
+
+    for r, (q1, q2) in enumerate(run_ranks(W, fwd_reuse)):
+        assert (q1 == outs[r]).all() and (q2 == outs[r]).all()
     W0 = dense_tables(cfg)
     codes, mid, sc, _ = O.quantize(W0)
     pb = O.Problem(rows, D, ft)
