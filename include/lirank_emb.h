@@ -293,7 +293,10 @@ EMB_API emb_status emb_quantize_mm8(emb_t h);
  * ids == offsets == NULL: look up the batch of the most recent emb_forward (batch and nnz
  * must equal its, else EMB_EINVAL; EMB_ESTATE if there was none, or if its staging slot
  * has since been refilled by two later host-input calls) -- host inputs of that forward are
- * not copied again (its staged copy is used); device inputs must still hold the same values. */
+ * not copied again (its staged copy is used); device inputs must still hold the same values.
+ * Sharded (W > 1 or EMB_F_EXCHANGE): if no other q8 lookup with fresh inputs came in between,
+ * the forward's ids exchange (a1) is reused -- the owners look up the ids they already hold
+ * (collective: every rank must make the same call, as always).                               */
 EMB_API emb_status emb_forward_q8(emb_t h, const int32_t* ids, const int32_t* offsets, int32_t batch,
                           int64_t nnz, float* out);
 
