@@ -85,32 +85,35 @@ k_scan_excl(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, int64_t
 }
 
 // a1 count: ids of bag (f, b) per destination rank -> lens[dest_base[o]*B + j*B + b].
-// (One thread per bag.  A group of 8 lanes per bag -- coalesced id loads, owners counted by
-// shuffles and ranked by match.any / ballots -- measured slower: count 90 -> 113 us, scatter
-// 121 -> 159 us on Feed-1: twice the instructions per id for 4 bags per warp.)
+// One thread per bag, bags visited longest first (order: the a2 length-binned permutation), so
+// a warp's threads walk bags of about the same length.  (A group of 8 lanes per bag --
+// coalesced id loads, owners counted by shuffles and ranked by match.any / ballots -- measured
+// slower: count 90 -> 113 us, scatter 121 -> 159 us on Feed-1: twice the instructions per id.)
+template <int WMAX>  // >= W: the owners' counters in registers
 __global__ void k_bucket_count(const int* __restrict__ ids, const int* __restrict__ offsets, int B,
                                int F, int W, const FeatMeta* __restrict__ meta,
                                const int32_t* __restrict__ owner0, const int32_t* __restrict__ blk,
                                const int32_t* __restrict__ jmap, const int32_t* __restrict__ dest_base,
-                               uint32_t* __restrict__ lens, uint32_t* status) {
-  const int64_t bag = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (bag >= (int64_t)F * B) return;
+                               uint32_t* __restrict__ lens, uint32_t* status, const uint32_t* __restrict__ order) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)F * B) return;
+  const int64_t bag = order ? (int64_t)__ldg(order + t) : t;
   const int f = (int)(bag / B), b = (int)(bag - (int64_t)f * B);
   const int rows = meta[f].rows, o0 = owner0[f], bk = blk[f];
-  uint32_t cnt[kMaxWorld];
+  uint32_t cnt[WMAX];
 #pragma unroll
-  for (int o = 0; o < kMaxWorld; ++o) cnt[o] = 0;
+  for (int o = 0; o < WMAX; ++o) cnt[o] = 0;
   bool bad = false;
   for (int j = __ldg(offsets + bag), e = __ldg(offsets + bag + 1); j < e; ++j) {
     const int id = __ldg(ids + j);
     if (id < 0 || id >= rows) { bad = true; continue; }
     const int o = o0 + id / bk;
 #pragma unroll
-    for (int q = 0; q < kMaxWorld; ++q) cnt[q] += (q == o);
+    for (int q = 0; q < WMAX; ++q) cnt[q] += (q == o);
   }
   if (bad) atomicOr(status, kStIdRange);
 #pragma unroll
-  for (int o = 0; o < kMaxWorld; ++o) {
+  for (int o = 0; o < WMAX; ++o) {
     if (o >= W) break;
     const int jj = jmap[o * F + f];
     if (jj >= 0) lens[((int64_t)dest_base[o] + jj) * B + b] = cnt[o];
@@ -118,21 +121,24 @@ __global__ void k_bucket_count(const int* __restrict__ ids, const int* __restric
 }
 
 // a1 scatter: keys (owner-local stored rows) into the send buffer, stable per bag.
+template <int WMAX>
 __global__ void k_bucket_scatter(const int* __restrict__ ids, const int* __restrict__ offsets, int B,
                                  int F, int W, const FeatMeta* __restrict__ meta,
                                  const int32_t* __restrict__ owner0, const int32_t* __restrict__ blk,
                                  const int32_t* __restrict__ jmap, const int32_t* __restrict__ dest_base,
                                  const int64_t* __restrict__ key_base, const uint32_t* __restrict__ pos,
-                                 uint32_t* __restrict__ send_keys, uint32_t pair_cap, uint32_t* status) {
-  const int64_t bag = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (bag >= (int64_t)F * B) return;
+                                 uint32_t* __restrict__ send_keys, uint32_t pair_cap, uint32_t* status,
+                                 const uint32_t* __restrict__ order) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)F * B) return;
+  const int64_t bag = order ? (int64_t)__ldg(order + t) : t;
   const int f = (int)(bag / B), b = (int)(bag - (int64_t)f * B);
   const int rows = meta[f].rows, o0 = owner0[f], bk = blk[f];
   // p[o] = where the next key for owner o goes: contiguous by owner (pair_cap == 0), or
   // slot o of a capacity-padded [W][pair_cap] buffer (the collective path's fixed sizes)
-  uint32_t p[kMaxWorld];
+  uint32_t p[WMAX];
 #pragma unroll
-  for (int o = 0; o < kMaxWorld; ++o) {
+  for (int o = 0; o < WMAX; ++o) {
     const int jj = o < W ? jmap[o * F + f] : -1;
     p[o] = jj >= 0 ? pos[((int64_t)dest_base[o] + jj) * B + b] : 0u;
     if (pair_cap && jj >= 0) p[o] = p[o] - __ldg(pos + (int64_t)dest_base[o] * B) + (uint32_t)o * pair_cap;
@@ -145,7 +151,7 @@ __global__ void k_bucket_scatter(const int* __restrict__ ids, const int* __restr
     const uint32_t key = (uint32_t)(key_base[(int64_t)o * F + f] + (id - (int64_t)(o - o0) * bk));
     uint32_t at = 0;
 #pragma unroll
-    for (int q = 0; q < kMaxWorld; ++q)
+    for (int q = 0; q < WMAX; ++q)
       if (q == o) { at = p[q]; p[q] = at + 1; }
     if (pair_cap && at >= (uint32_t)(o + 1) * pair_cap) { over = true; continue; }
     send_keys[at] = key;
@@ -554,17 +560,31 @@ emb_status exchange_forward(emb_t h, const Staged& st, int32_t batch, int64_t nn
     Phase ph(h->prof, h->stream, EMB_PH_EXCHANGE);
     h->x_ids_fwd = !q8;  // this call's exchange overwrites the receive buffers
     // ---- a1: bucketize -----------------------------------------------------------------
+    const uint32_t* bag_ord = launch_bag_order(st.offsets, (long long)F * B, h->order_ws, h->stream);
+    if (bag_ord) h->launches += 2;
     if (F * (int64_t)B > 0) {
-      k_bucket_count<<<bag_grid, 256, 0, h->stream>>>(st.ids, st.offsets, B, F, W, h->d_meta, x.d_owner0,
-                                                      x.d_blk, x.d_jmap, x.d_dest_base, x.lens, h->d_status);
+      if (W <= 8)
+        k_bucket_count<8><<<bag_grid, 256, 0, h->stream>>>(st.ids, st.offsets, B, F, W, h->d_meta, x.d_owner0,
+                                                           x.d_blk, x.d_jmap, x.d_dest_base, x.lens, h->d_status,
+                                                           bag_ord);
+      else
+        k_bucket_count<kMaxWorld><<<bag_grid, 256, 0, h->stream>>>(st.ids, st.offsets, B, F, W, h->d_meta,
+                                                                   x.d_owner0, x.d_blk, x.d_jmap, x.d_dest_base,
+                                                                   x.lens, h->d_status, bag_ord);
       h->launches += 1;
       CK(cudaGetLastError());
     }
     if ((s = scan(h, x.lens, x.pos, Ltot, 0)) != EMB_OK) return s;
     if (F * (int64_t)B > 0) {
-      k_bucket_scatter<<<bag_grid, 256, 0, h->stream>>>(st.ids, st.offsets, B, F, W, h->d_meta, x.d_owner0,
-                                                        x.d_blk, x.d_jmap, x.d_dest_base, x.d_key_base,
-                                                        x.pos, x.send_keys, pair_cap, h->d_status);
+      if (W <= 8)
+        k_bucket_scatter<8><<<bag_grid, 256, 0, h->stream>>>(st.ids, st.offsets, B, F, W, h->d_meta, x.d_owner0,
+                                                             x.d_blk, x.d_jmap, x.d_dest_base, x.d_key_base,
+                                                             x.pos, x.send_keys, pair_cap, h->d_status, bag_ord);
+      else
+        k_bucket_scatter<kMaxWorld><<<bag_grid, 256, 0, h->stream>>>(st.ids, st.offsets, B, F, W, h->d_meta,
+                                                                     x.d_owner0, x.d_blk, x.d_jmap, x.d_dest_base,
+                                                                     x.d_key_base, x.pos, x.send_keys, pair_cap,
+                                                                     h->d_status, bag_ord);
       h->launches += 1;
     }
     k_send_counts<<<1, 32, 0, h->stream>>>(x.pos, x.d_dest_base, W, B, x.cnt);

@@ -451,6 +451,10 @@ static const uint32_t* bag_order(const int* offsets, long long bags, uint32_t* w
   return ws;
 }
 
+const uint32_t* launch_bag_order(const int* offsets, long long bags, uint32_t* ws, cudaStream_t s) {
+  return bag_order(offsets, bags, ws, s);
+}
+
 // ---------------------------------------------------------------------------
 // Host launchers
 // ---------------------------------------------------------------------------

@@ -52,6 +52,8 @@ cudaError_t launch_pool_fwd_f32(const FwdArgs& a, cudaStream_t s);
 // longest bag).  Scratch: the permutation + 2 x 256 bin counters.
 constexpr int kLenBins = 256;
 inline int64_t kOrderWsWords(int64_t bags) { return bags + 2 * kLenBins; }
+// the longest-first bag permutation of F*B bags into ws (2 kernels); NULL if bags < 2
+const uint32_t* launch_bag_order(const int* offsets, long long bags, uint32_t* ws, cudaStream_t s);
 // kernels one forward launch issues: the pooling kernel, plus the 2 ordering kernels and,
 // for a2 (fp32), the short-bag kernel
 inline int fwd_launches(int64_t bags, bool ordered, bool fp32) {
