@@ -324,6 +324,22 @@ struct PushDst {
 __global__ void __launch_bounds__(256)
 k_push_grad(const float* __restrict__ grad, int B, int F, int D, int W, int rank,
             const int32_t* __restrict__ jmap, const PushDst pd) {
+  if (walk_ok(D) && (D / 4) % 2 == 0) {  // two float4 columns per thread: 2 loads in flight
+    const int h = D / 8;
+    const int64_t nrows = (int64_t)B * F;
+    for (RowWalk w(F, h); w.row < nrows; w.next(F)) {
+      const float4 g0 = ld_f4(grad + w.row * D + 4 * w.v), g1 = ld_f4(grad + w.row * D + 4 * (w.v + h));
+      for (int o = 0; o < W; ++o) {
+        const int j = __ldg(jmap + o * F + w.f);
+        if (j >= 0) {
+          float* d = pd.dst[o] + (((int64_t)rank * B + w.b) * pd.Fo[o] + j) * D;
+          st_f4(d + 4 * w.v, g0);
+          st_f4(d + 4 * (w.v + h), g1);
+        }
+      }
+    }
+    return;
+  }
   if (walk_ok(D)) {  // float4 columns, no per-element division
     const int nv = D / 4;
     const int64_t nrows = (int64_t)B * F;
@@ -374,6 +390,25 @@ __global__ void __launch_bounds__(256)
 k_sum_slots(float* __restrict__ out, const float* __restrict__ slots, const uint32_t* __restrict__ lens,
             int W, int B, int F, int D, const uint32_t* __restrict__ cnt_all, uint32_t recv_cap) {
   const bool discard = exchange_overflow(cnt_all, W, recv_cap, 0u);  // the owners stored nothing
+  if (walk_ok(D) && (D / 4) % 2 == 0) {  // two float4 columns per thread (v, v + nv/2): 2 loads in flight
+    const int nv = D / 4, h = nv / 2;
+    const int64_t n = (int64_t)B * F * D, nrows = (int64_t)B * F;
+    for (RowWalk w(F, h); w.row < nrows; w.next(F)) {
+      float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0;
+      bool any = false;
+      for (int o = 0; o < W; ++o) {
+        if (discard || __ldg(lens + ((int64_t)o * F + w.f) * B + w.b) == 0) continue;
+        const float* sl = slots + (int64_t)o * n + w.row * D + 4 * w.v;
+        const float4 x0 = ld_nc_f4(sl), x1 = ld_nc_f4(sl + 4 * h);
+        a0 = any ? f4_add_rn(a0, x0) : x0;
+        a1 = any ? f4_add_rn(a1, x1) : x1;
+        any = true;
+      }
+      st_f4(out + w.row * D + 4 * w.v, a0);
+      st_f4(out + w.row * D + 4 * (w.v + h), a1);
+    }
+    return;
+  }
   if (walk_ok(D)) {  // float4 columns, no per-element division
     const int nv = D / 4;
     const int64_t n = (int64_t)B * F * D, nrows = (int64_t)B * F;
