@@ -361,7 +361,8 @@ cudaError_t radix_sort_pairs(uint2* kv0, uint2* kv1, int64_t n, const uint32_t* 
     // 0.964 vs 0.998 ms: the wider tile halves the look-back walks per item at equal occupancy;
     // then 512 x 15: 0.297 -> 0.286 ms, Ads 0.965 -> 0.931, alpha 0 0.306 -> 0.297 (14: 0.287 /
     // 0.953, 17: 0.295 / 0.963) -- fewer spilled registers at the 64-register cap, and Feed-1's
-    // 1724 tiles fill the 296 resident CTAs in 5.8 rounds instead of 5.5)
+    // 1724 tiles fill the 296 resident CTAs in 5.8 rounds instead of 5.5; at 512 x 15 the
+    // look-back window 4 / 8 / 16: 0.286 / 0.286 / 0.469 ms, poll sleep 32 / 64 / 256 ns: same)
 #define OS(BITS) e = onesweep_pass<BITS, 15, 0, 2, 8, 64, 512>(a, b, n, n_dev, shift, hp, ctr, ws.status, epoch, (uint32_t)p, s);
     if (dbits == 9) { OS(9) } else { OS(8) }
 #undef OS
