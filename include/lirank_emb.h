@@ -183,14 +183,16 @@ typedef struct {
   int64_t weights_bytes;    /* fp32 [local_rows][row_pitch]                                    */
   int64_t accum_bytes;      /* fp32 [local_rows] (row-wise) or [local_rows][row_pitch]         */
   int64_t q8_codes_bytes;   /* q8 rows [local_rows][q8_pitch] (0 without EMB_F_Q8), each row =
-                               [D int8 codes][pad to 8][fp32 middle][fp32 scale][pad to 32]: one
-                               contiguous run of whole 32-B sectors (D=64: 96 B); every write
+                               [D int8 codes][pad to 8][fp32 middle][fp32 scale][pad]: one
+                               contiguous run of whole 32-B sectors (D=64: 96 B), or of whole
+                               64-B DRAM atoms with EMB_F_REQUANT (D=64: 128 B); every write
                                of a row rewrites all of it, pads as zero bytes                 */
   int64_t q8_meta_bytes;    /* 0 (metadata lives in the q8 rows; kept for ABI stability)       */
   int64_t workspace_bytes;  /* library scratch (staging, sort, segment partials, scalars)      */
   int64_t local_rows;       /* rows stored on this rank (sum over its local tables)            */
   int32_t row_pitch;        /* floats per stored fp32 row: round_up(D, 4) (16-B aligned rows)  */
-  int32_t q8_pitch;         /* bytes per q8 row: round_up(round_up(D, 8) + 8, 32)              */
+  int32_t q8_pitch;         /* bytes per q8 row: round_up(round_up(D, 8) + 8, 32), or ... 64)
+                               with EMB_F_REQUANT                                              */
 } emb_sizes;
 
 typedef struct {
