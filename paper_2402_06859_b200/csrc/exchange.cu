@@ -487,7 +487,11 @@ void carve_exchange(const Plan& p, Carver& cv, ExchangeWs* x) {
   x->recv_keys = cv.take<uint32_t>(p.recv_nnz_cap);
   if (!p2p) x->recv_pad = cv.take<uint32_t>(W * p.pair_cap);
   x->pooled = cv.take<float>(W * B * Fr * D);
-  x->xdense = cv.take<float>(B * F * D);
+  // fused exchange: two destination sets (the fp32 forward's and the q8 forward's), so a q8
+  // lookup of the forward's batch needs no barrier before its owners store (set 1 was last
+  // read by the previous step's q8 slot sum, ordered before by this step's forward barriers)
+  const bool row = p.sharding == EMB_SHARD_ROW;
+  x->xdense = cv.take<float>((p2p && !row ? 2 : 1) * B * F * D);
   x->ident = cv.take<FeatMeta>(W * Fr);
   x->d_jmap = cv.take<int32_t>(W * F);
   x->d_fmap = cv.take<int32_t>(3 * F);
@@ -500,7 +504,8 @@ void carve_exchange(const Plan& p, Carver& cv, ExchangeWs* x) {
   const int64_t scan_n = std::max<int64_t>(Ltot + 1, W * Fr * B + 1);
   x->scan_status = cv.take<unsigned long long>((scan_n + kScanTile - 1) / kScanTile + 1);
   if (p2p) {
-    if (p.sharding == EMB_SHARD_ROW) x->pslots = cv.take<float>(W * B * F * D);
+    if (row) x->pslots = cv.take<float>(2 * W * B * F * D);
+    x->fdst_stride = row ? (int64_t)W * B * F * D : (int64_t)B * F * D;
     x->d_fcol = cv.take<int32_t>(Fr);
     x->p2p_scratch = cv.take<uint8_t>((int64_t)kPeerScratchBytes);
   }
@@ -556,13 +561,14 @@ static emb_status map_p2p(emb_t h) {
 }
 
 // The fused-exchange destination of this rank's owner pooling.
-static PeerOut peer_out(emb_t h) {
+static PeerOut peer_out(emb_t h, int set) {
   const Plan& p = h->p;
   PeerOut pm;
   memset(&pm, 0, sizeof(pm));
   if (!(p.flags & EMB_F_P2P)) return pm;
   const bool row = p.sharding == EMB_SHARD_ROW;
-  for (int r = 0; r < p.world; ++r) pm.base[r] = row ? h->x.peer_pslots[r] : h->x.peer_xdense[r];
+  for (int r = 0; r < p.world; ++r)
+    pm.base[r] = (row ? h->x.peer_pslots[r] : h->x.peer_xdense[r]) + set * h->x.fdst_stride;
   pm.fcol = h->x.d_fcol;
   pm.F_out = p.F;
   pm.slot = row ? p.rank : 0;
@@ -588,9 +594,8 @@ emb_status exchange_forward(emb_t h, const Staged& st, int32_t batch, int64_t nn
   const bool skip_a1 = q8 && reuse && h->x_ids_fwd && h->fwd_B == B;
   if (skip_a1) {
     Phase ph(h->prof, h->stream, EMB_PH_EXCHANGE);
-    // the owners store pooled rows into the sources' slots next: every rank must be past its
-    // reads of those slots (the last forward's slot sum) -- one barrier instead of the whole a1
-    if (p2p && !h->comm->barrier(x.p2p_scratch, h->stream)) return EMB_ENCCL;
+    // (fused: the owners store into the q8 destination set, last read by the previous step's
+    // q8 slot sum -- ordered before by this step's forward barriers: no barrier here)
   } else {
     Phase ph(h->prof, h->stream, EMB_PH_EXCHANGE);
     h->x_ids_fwd = !q8;  // this call's exchange overwrites the receive buffers
@@ -684,7 +689,7 @@ emb_status exchange_forward(emb_t h, const Staged& st, int32_t batch, int64_t nn
     a.sentinel = (uint32_t)p.local_rows;
     a.status = h->d_status;
     a.order_ws = h->order_ws;
-    a.peer = peer_out(h);
+    a.peer = peer_out(h, q8 ? 1 : 0);
     Phase ph(h->prof, h->stream, EMB_PH_FWD);
     CK(launch_pool_fwd_f32(a, h->stream));
   } else {
@@ -705,7 +710,7 @@ emb_status exchange_forward(emb_t h, const Staged& st, int32_t batch, int64_t nn
     a.status = h->d_status;
     a.order_ws = h->order_ws;
     a.order_ready = skip_a1 && (int64_t)W * Fr * B >= 2;  // the forward ordered these receive bags
-    a.peer = peer_out(h);
+    a.peer = peer_out(h, q8 ? 1 : 0);
     Phase ph(h->prof, h->stream, EMB_PH_FWD_Q8);
     CK(launch_pool_fwd_q8(a, h->stream));
   }
@@ -721,11 +726,13 @@ emb_status exchange_forward(emb_t h, const Staged& st, int32_t batch, int64_t nn
       if (!h->comm->barrier(x.p2p_scratch, h->stream)) return EMB_ENCCL;
       const int64_t n = (int64_t)B * F * D;
       if (n > 0 && p.sharding == EMB_SHARD_ROW) {
-        k_sum_slots<<<148 * 4, 256, 0, h->stream>>>(st.out, x.pslots, x.lens, W, B, F, D, cnt_all, recv_cap);
+        k_sum_slots<<<148 * 4, 256, 0, h->stream>>>(st.out, x.pslots + (q8 ? x.fdst_stride : 0), x.lens, W, B, F, D,
+                                                    cnt_all, recv_cap);
         h->launches += 1;
         CK(cudaGetLastError());
       } else if (n > 0) {
-        CK(cudaMemcpyAsync(st.out, x.xdense, 4ull * n, cudaMemcpyDeviceToDevice, h->stream));
+        CK(cudaMemcpyAsync(st.out, x.xdense + (q8 ? x.fdst_stride : 0), 4ull * n, cudaMemcpyDeviceToDevice,
+                           h->stream));
       }
     } else if (p.sharding == EMB_SHARD_ROW) {
       if (!h->comm->reduce_scatter_f32(x.pooled, st.out, (size_t)B * F * D, h->stream)) return EMB_ENCCL;

@@ -128,7 +128,8 @@ struct ExchangeWs {
   uint32_t* scan_counter = nullptr;    // [4] tile counters of the exchange scans
   unsigned long long* scan_status = nullptr;  // look-back words of the exchange scans
   // fused exchange (EMB_F_P2P)
-  float* pslots = nullptr;        // row-wise: [world][B][F][D] owner partials, summed in rank order
+  float* pslots = nullptr;        // row-wise: [2][world][B][F][D] owner partials, summed in rank order
+  int64_t fdst_stride = 0;        // fused: floats between the two destination sets (fp32 / q8 forward)
   int32_t* d_fcol = nullptr;      // [Fr]: global feature of owner-local feature j
   uint8_t* p2p_scratch = nullptr; // [kPeerScratchBytes] transport scratch (barrier, mapping)
   float* peer_xdense[kMaxWorld] = {};  // table-wise: each rank's xdense (fwd destination)
