@@ -222,6 +222,28 @@ def test_sharded_q8_forward(gpu, sharding, p2p):
 
     for r, (q1, q2) in enumerate(run_ranks(W, fwd_reuse)):
         assert (q1 == outs[r]).all() and (q2 == outs[r]).all()
+
+    # alternate batches: each step's fp32 forward and its q8 reuse use the two destination sets of
+    # the fused exchange in turn; every q8 output must equal the fresh lookup of its batch
+    other = [gen.make_batch(rows, cfg.features, B, cfg.seed + 100 + r, 1) for r in range(W)]
+
+    def alternate(r):
+        e = embs[r]
+        res = []
+        for k in range(4):
+            ids, off = (per_rank if k % 2 == 0 else other)[r]
+            with torch.cuda.stream(e.stream):
+                e.forward(torch.from_numpy(ids).cuda(), torch.from_numpy(off).cuda(), B)
+                q = torch.empty((B, F, D), device="cuda")
+                e.forward_q8(None, None, B, out=q, nnz=len(ids))
+                fresh = e.forward_q8(torch.from_numpy(ids).cuda(), torch.from_numpy(off).cuda(), B)
+            assert e.sync() == 0
+            res.append((q.cpu().numpy(), fresh.cpu().numpy()))
+        return res
+
+    for r, res in enumerate(run_ranks(W, alternate)):
+        for k, (q, fresh) in enumerate(res):
+            assert (q == fresh).all(), (r, k)
     W0 = dense_tables(cfg)
     codes, mid, sc, _ = O.quantize(W0)
     pb = O.Problem(rows, D, ft)
